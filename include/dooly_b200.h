@@ -1,0 +1,206 @@
+/*
+ * libdooly_b200 — C-ABI for the B200-native Dooly latency-database hot path.
+ *
+ * The reference (arxiv/paper_2605_07985, read-only at /root/reference) is pure
+ * Python and ships the hot path only as a specification; every entry point
+ * below replaces one `[OP]` of that specification, cited as SPEC.md:line.  The
+ * Python mirror (paper_2605_07985_b200/{profiler,sim}.py) binds these through
+ * ctypes; INTEGRATION.md shows the binding a maintainer adds to pkg/src/dooly.
+ *
+ * Conventions
+ *  - Every pointer argument except `ctx`, `cfg`/`ops` structs and the string
+ *    tables noted below is DEVICE memory owned by the caller.
+ *  - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy default)
+ *    and never allocate or synchronise; scratch comes from a caller-provided
+ *    workspace sized by the matching *_workspace_size() query.
+ *  - Return value: DOOLY_OK or a DOOLY_ERR_* status; message via
+ *    dooly_last_error().  Per-item conditions (insufficient data, unknown
+ *    signature, extrapolation, clamping) are reported in per-item arrays so
+ *    the host wrapper can raise the reference's exception (errors.py:48-85)
+ *    after it synchronises.
+ *  - A dooly_ctx is bound to one device and is not thread-safe.
+ */
+#ifndef DOOLY_B200_H
+#define DOOLY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DOOLY_ABI_VERSION 1
+
+/* status codes (mapped to errors.py classes by paper_2605_07985_b200/errors.py) */
+#define DOOLY_OK 0
+#define DOOLY_ERR_INVALID_ARG 1
+#define DOOLY_ERR_INSUFFICIENT_DATA 2  /* errors.py:60 InsufficientData */
+#define DOOLY_ERR_UNKNOWN_SIGNATURE 3  /* errors.py:72 UnknownSignature */
+#define DOOLY_ERR_DUPLICATE_KEY 4      /* errors.py:52 DuplicateKey */
+#define DOOLY_ERR_NON_TERMINATION 5    /* errors.py:84 NonTermination */
+#define DOOLY_ERR_CUDA 6
+
+/* regression kinds (App. A.7 of SURVEY.md) */
+#define DOOLY_KIND_AFFINE 0 /* [1, f]                      num_toks-type feature  */
+#define DOOLY_KIND_ATTN 1   /* [1,f1,f2,f3,f1²,f2²,f3²,f1f2,f1f3,f2f3]  (prefill_toks, batch, kv_tokens) */
+
+/* Regressor tables are arrays of these rows, one per signature (AoS so one
+ * predict gathers exactly one 32-B sector / one 128-B line).  A row whose
+ * lo[0] > hi[0] is "not fitted" and yields UNKNOWN_SIGNATURE in predict. */
+typedef struct {
+  double c0, c1;     /* coefficients in the scaled basis f = x * inv_scale   */
+  double inv_scale;  /* 1 / max training x (1 if max == 0)                   */
+  uint32_t lo, hi;   /* training box (extrapolation flag outside it)         */
+} dooly_affine_row;  /* 32 bytes */
+
+typedef struct {
+  double c[10];
+  double inv_scale[3];
+  uint32_t lo[3], hi[3];
+} dooly_attn_row; /* 128 bytes */
+
+/* per-signature fit status */
+#define DOOLY_FIT_OK 0
+#define DOOLY_FIT_INSUFFICIENT 1
+
+/* predict flag planes (bit i of word i/32): plane 0 = extrapolated (outside
+ * training box), plane 1 = clamped at the 1e-7 s floor */
+#define DOOLY_FLAG_PLANES 2
+
+typedef struct dooly_ctx dooly_ctx;
+
+int dooly_version(void);
+int dooly_ctx_create(int device, dooly_ctx** out);
+void dooly_ctx_destroy(dooly_ctx* ctx);
+const char* dooly_last_error(const dooly_ctx* ctx);
+/* number of kernels this ctx has launched since creation (host counter) */
+int64_t dooly_launch_count(const dooly_ctx* ctx);
+
+/* ------------------------------------------------------------------ K1 dedup
+ * Replaces canonicalize, signature_hash
+ * and dedup.
+ *
+ * Packed record (u32 words, little-endian), starting at words[rec_off[i]]:
+ *   w0 op_id      index into the op-name table
+ *   w1 n_dims | n_sym << 16
+ *   w2 attr_id    index into attr-digest table, 0xFFFFFFFF = operator granularity
+ *   w3 repeat_count (carried for model_operations rows; not hashed)
+ *   n_dims x {pos, val_lo, val_hi}   MODEL_CONFIG dims/scalars, ascending pos
+ *   n_sym  x sym_id                  ascending; ids are ranks in bytewise order
+ * String tables are device byte arrays with int64 offsets (n+1 entries).
+ * The canonical message (sigfmt=1 layout) is rebuilt in registers and hashed;
+ * it is never materialised in HBM.
+ */
+int dooly_sha256_records(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off,
+                         int64_t n, const uint8_t* op_bytes, const int64_t* op_off,
+                         int64_t n_ops, const uint8_t* sym_bytes, const int64_t* sym_off,
+                         int64_t n_sym, const uint8_t* attr_digests, int64_t n_attr,
+                         uint8_t* out_digest, void* stream);
+
+/* Plain SHA-256 of n byte messages (msgs + off[i]..off[i+1]) — signature_hash(bytes). */
+int dooly_sha256_messages(dooly_ctx* ctx, const uint8_t* msgs, const int64_t* off, int64_t n,
+                          uint8_t* out_digest, void* stream);
+
+/* First-occurrence dedup of n 32-byte digests against an existing DB key set.
+ *   out_first[i]  = smallest j with digest[j] == digest[i]
+ *   out_uid[i]    = rank of out_first[i] among first occurrences (dense, ordered)
+ *   out_is_new[i] = 1 iff i is a first occurrence and its digest is not in db
+ *   out_in_db[i]  = 1 iff digest[i] is in db
+ *   out_n_unique  = device int64 scalar, number of distinct digests
+ * Exact and deterministic for any thread schedule (min-reduction per key). */
+size_t dooly_dedup_workspace_size(int64_t n, int64_t n_db);
+int dooly_dedup_digests(dooly_ctx* ctx, const uint8_t* digests, int64_t n,
+                        const uint8_t* db_digests, int64_t n_db, int64_t* out_first,
+                        uint32_t* out_uid, uint8_t* out_is_new, uint8_t* out_in_db,
+                        int64_t* out_n_unique, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
+/* -------------------------------------------------------------------- K2 fit
+ * Replaces fit.  Points of signature s are
+ * [pt_off[s], pt_off[s+1]); x is feature-major (kind==ATTN: 3 planes of n_pts
+ * u32, AFFINE: 1 plane), y is latency in seconds.  Writes one table row, the
+ * training MAPE and a status per signature. */
+int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
+              const int64_t* pt_off, int64_t n_sig, void* table, double* fit_err,
+              uint8_t* status, void* stream);
+
+/* ---------------------------------------------------------------- K3 predict
+ * Replaces predict.  sig[i] indexes the table; x is
+ * feature-major (planes of n_q u32).  out[i] = max(poly, 1e-7) evaluated
+ * mul-then-add without contraction; flag_bits holds DOOLY_FLAG_PLANES planes
+ * of ceil(n_q/32) words (may be NULL).  Queries on unknown/unfitted rows write
+ * NaN and atomically min their index into *err_first (device int64, caller
+ * initialises to INT64_MAX; may be NULL). */
+int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
+                  const uint32_t* sig, const uint32_t* x, int64_t n_q, double* out,
+                  uint32_t* flag_bits, int64_t* err_first, void* stream);
+
+/* ------------------------------------------------------------------- K4 sim
+ * Call-graph op list for one (model, backend, tp): iter_latency
+ *   lat = sum_e repeat_e * max(pred_e(x_it), 1e-7)   [in list order]
+ *       + sum_c repeat_c * comm(tp, num_toks * bytes_per_tok_c)
+ * HOST struct; the arrays it points to are HOST memory (copied to device
+ * constant memory at launch). */
+#define DOOLY_MAX_OPS 64
+#define DOOLY_FEAT_NUM_TOKS 0    /* affine on tokens scheduled this iteration     */
+#define DOOLY_FEAT_NUM_SEQS 1    /* affine on requests in the iteration (lm_head) */
+#define DOOLY_FEAT_ATTN 2        /* attention (prefill_toks, batch, kv_tokens[w]) */
+#define DOOLY_FEAT_COMM 3        /* ring all-reduce of num_toks*bytes_per_tok     */
+typedef struct {
+  int32_t n_ops;
+  int32_t tp;
+  double comm_alpha, comm_beta;
+  int32_t feat[DOOLY_MAX_OPS];      /* DOOLY_FEAT_*                                */
+  int32_t row[DOOLY_MAX_OPS];       /* table row (affine table or attention table) */
+  int32_t repeat[DOOLY_MAX_OPS];
+  int32_t window_slot[DOOLY_MAX_OPS]; /* ATTN: 0 = full kv, 1 = windowed kv       */
+  int64_t bytes_per_tok[DOOLY_MAX_OPS]; /* COMM                                   */
+} dooly_oplist;
+
+/* Per-iteration features, 5 planes of n_it u32 (feature-major):
+ *   0 num_toks, 1 prefill_toks, 2 batch, 3 kv_tokens (full), 4 kv_tokens (windowed) */
+#define DOOLY_IT_FEATS 5
+int dooly_iter_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_table,
+                    int64_t n_affine, const void* attn_table, int64_t n_attn,
+                    const uint32_t* it_feat, int64_t n_it, double* it_lat,
+                    int64_t* err_first, void* stream);
+
+/* Device-resident serving loop: one CTA per
+ * independent replica shard runs FCFS continuous batching with chunked
+ * prefill, the fused gather-evaluate-reduce iteration latency above, the f64
+ * clock, and stamps per-request first/last-token times. */
+typedef struct {
+  int32_t chunk;            /* prefill token budget per iteration (decodes count, D1) */
+  int32_t max_batch;
+  int32_t window;           /* sliding window of the windowed kv plane (0 = none)     */
+  int32_t pad_;
+  int64_t kv_bytes_per_token;
+  int64_t kv_capacity_bytes; /* admission cap on reserved (prompt+output) KV bytes    */
+  int64_t max_iterations;   /* per shard NonTermination guard                         */
+} dooly_sched;
+
+/* Requests of shard s are [shard_off[s], shard_off[s+1]), sorted by arrival.
+ * Outputs per request (device f64): ttft = first-token time - arrival, tpot =
+ * (last - first token time) / (output - 1) (NaN when output < 2).  Per shard:
+ * iteration count, final clock, status (DOOLY_OK, DOOLY_ERR_NON_TERMINATION
+ * when max_iterations is hit, DOOLY_ERR_INVALID_ARG when the head request can
+ * never fit the KV capacity, DOOLY_ERR_UNKNOWN_SIGNATURE for unfitted rows).
+ * Optional it_log (device, may be NULL): per shard up to it_log_cap rows of
+ * DOOLY_IT_FEATS u32 features + the f64 iteration latency, for verification.
+ * The workspace is currently unused (all scheduler state lives in shared
+ * memory; max_batch <= 1024). */
+size_t dooly_sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards);
+int dooly_sim_run(dooly_ctx* ctx, const dooly_oplist* ops, const dooly_sched* cfg,
+                  const void* affine_table, int64_t n_affine, const void* attn_table,
+                  int64_t n_attn, const double* arrival, const uint32_t* prompt,
+                  const uint32_t* output, const uint32_t* cached, const int64_t* shard_off,
+                  int64_t n_shards, double* ttft, double* tpot, int64_t* n_iter,
+                  double* final_clock, int32_t* shard_status, uint32_t* it_log_feat,
+                  double* it_log_lat, int64_t it_log_cap, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DOOLY_B200_H */

@@ -1,0 +1,137 @@
+"""ctypes binding of libdooly_b200.so (include/dooly_b200.h).
+
+The library is built in-tree (``make -C paper_2605_07985_b200/csrc``, or
+``__graft_entry__.build()``).  There is no fallback: if the shared object is
+missing or no CUDA device is present, every hot-path call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import torch
+
+from .errors import DeviceError, raise_for_status
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libdooly_b200.so"
+
+KIND_AFFINE = 0
+KIND_ATTN = 1
+FEAT_NUM_TOKS, FEAT_NUM_SEQS, FEAT_ATTN, FEAT_COMM = 0, 1, 2, 3
+MAX_OPS = 64
+IT_FEATS = 5
+AFFINE_ROW_BYTES = 32
+ATTN_ROW_BYTES = 128
+ROW_BYTES = {KIND_AFFINE: AFFINE_ROW_BYTES, KIND_ATTN: ATTN_ROW_BYTES}
+PLANES = {KIND_AFFINE: 1, KIND_ATTN: 3}
+
+
+class OpList(C.Structure):
+    _fields_ = [
+        ("n_ops", C.c_int32),
+        ("tp", C.c_int32),
+        ("comm_alpha", C.c_double),
+        ("comm_beta", C.c_double),
+        ("feat", C.c_int32 * MAX_OPS),
+        ("row", C.c_int32 * MAX_OPS),
+        ("repeat", C.c_int32 * MAX_OPS),
+        ("window_slot", C.c_int32 * MAX_OPS),
+        ("bytes_per_tok", C.c_int64 * MAX_OPS),
+    ]
+
+
+class Sched(C.Structure):
+    _fields_ = [
+        ("chunk", C.c_int32),
+        ("max_batch", C.c_int32),
+        ("window", C.c_int32),
+        ("pad_", C.c_int32),
+        ("kv_bytes_per_token", C.c_int64),
+        ("kv_capacity_bytes", C.c_int64),
+        ("max_iterations", C.c_int64),
+    ]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_SIGS = {
+    "dooly_version": (C.c_int, []),
+    "dooly_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "dooly_ctx_destroy": (None, [_P]),
+    "dooly_last_error": (C.c_char_p, [_P]),
+    "dooly_launch_count": (_I64, [_P]),
+    "dooly_sha256_records": (C.c_int, [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _I64,
+                                       _P, _P]),
+    "dooly_sha256_messages": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "dooly_dedup_workspace_size": (C.c_size_t, [_I64, _I64]),
+    "dooly_dedup_digests": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P,
+                                      C.c_size_t, _P]),
+    "dooly_fit": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
+    "dooly_predict": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
+    "dooly_iter_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _I64, _P, _P,
+                                  _P]),
+    "dooly_sim_workspace_size": (C.c_size_t, [C.POINTER(Sched), _I64, _I64]),
+    "dooly_sim_run": (C.c_int, [_P, C.POINTER(OpList), C.POINTER(Sched), _P, _I64, _P, _I64,
+                                _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
+                                C.c_size_t, _P]),
+}
+EXPORTS = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib = None
+_ctx: dict = {}
+
+
+def load_library() -> C.CDLL:
+    """Load and prototype the shared object (no CUDA device needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise DeviceError(
+                    f"{LIB_PATH} is missing: build it with `make -C paper_2605_07985_b200/csrc` "
+                    "(there is no CPU fallback)")
+            lib = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+        return _lib
+
+
+def ctx_for(device: torch.device) -> C.c_void_p:
+    """Per-device dooly_ctx, created on first use."""
+    if device.type != "cuda":
+        raise DeviceError(f"libdooly_b200 runs on CUDA devices only (got {device})")
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    with _lock:
+        pass
+    if idx not in _ctx:
+        lib = load_library()
+        h = C.c_void_p()
+        rc = lib.dooly_ctx_create(idx, C.byref(h))
+        if rc != 0:
+            raise DeviceError(f"dooly_ctx_create({idx}) failed with status {rc}")
+        _ctx[idx] = h
+    return _ctx[idx]
+
+
+def check(rc: int, ctx) -> None:
+    if rc:
+        msg = load_library().dooly_last_error(ctx)
+        raise_for_status(rc, msg.decode() if msg else f"status {rc}")
+
+
+def launch_count(device: torch.device) -> int:
+    return int(load_library().dooly_launch_count(ctx_for(device)))
+
+
+def stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()

@@ -1,0 +1,273 @@
+// extern "C" boundary of libdooly_b200 (include/dooly_b200.h).
+// Validates arguments, selects the kernel, launches on the caller's stream,
+// and records errors for dooly_last_error().  No allocation, no host sync.
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "common.cuh"
+
+namespace dooly {
+cudaError_t launch_predict(int kind, const void* table, int64_t n_sig, const uint32_t* sig,
+                           const uint32_t* x, int64_t n_q, double* out, uint32_t* flags,
+                           int64_t* err_first, cudaStream_t stream, int n_sm);
+cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double* y,
+                       const int64_t* off, int64_t n_sig, void* table, double* fit_err,
+                       uint8_t* status, cudaStream_t stream, int n_sm);
+cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off, int64_t n,
+                                  const uint8_t* op_bytes, const int64_t* op_off,
+                                  const uint8_t* sym_bytes, const int64_t* sym_off,
+                                  const uint8_t* attr_digests, uint8_t* out, cudaStream_t stream,
+                                  int n_sm, int64_t* launches);
+cudaError_t launch_sha256_messages(const uint8_t* msgs, const int64_t* off, int64_t n,
+                                   uint8_t* out, cudaStream_t stream, int n_sm);
+size_t dedup_workspace_size(int64_t n, int64_t n_db);
+cudaError_t launch_dedup(const uint8_t* digests, int64_t n, const uint8_t* db, int64_t n_db,
+                         int64_t* out_first, uint32_t* out_uid, uint8_t* out_is_new,
+                         uint8_t* out_in_db, int64_t* out_n_unique, void* ws, size_t ws_bytes,
+                         cudaStream_t stream, int n_sm, int64_t* launches);
+cudaError_t launch_iter_eval(const dooly_oplist* ops, const void* aff, int64_t n_aff,
+                             const void* attn, int64_t n_attn, const uint32_t* it_feat,
+                             int64_t n_it, double* it_lat, int64_t* err_first,
+                             cudaStream_t stream, int n_sm);
+size_t sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards);
+cudaError_t launch_sim(const dooly_oplist* ops, const dooly_sched* cfg, const void* aff,
+                       int64_t n_aff, const void* attn, int64_t n_attn, const double* arrival,
+                       const uint32_t* prompt, const uint32_t* output, const uint32_t* cached,
+                       const int64_t* shard_off, int64_t n_shards, double* ttft, double* tpot,
+                       int64_t* n_iter, double* final_clock, int32_t* shard_status,
+                       uint32_t* it_log_feat, double* it_log_lat, int64_t it_log_cap, void* ws,
+                       size_t ws_bytes, cudaStream_t stream, int n_sm);
+}  // namespace dooly
+
+struct dooly_ctx {
+  int device = 0;
+  int n_sm = 148;
+  int64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(dooly_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+int check_cuda(dooly_ctx* ctx, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return DOOLY_OK;
+  return fail(ctx, DOOLY_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Guard: every call runs on the ctx's device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int dooly_version(void) { return DOOLY_ABI_VERSION; }
+
+int dooly_ctx_create(int device, dooly_ctx** out) {
+  if (out == nullptr) return DOOLY_ERR_INVALID_ARG;
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || device < 0 || device >= n) return DOOLY_ERR_CUDA;
+  dooly_ctx* c = new dooly_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, device);
+  *out = c;
+  return DOOLY_OK;
+}
+
+void dooly_ctx_destroy(dooly_ctx* ctx) { delete ctx; }
+
+const char* dooly_last_error(const dooly_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+
+int64_t dooly_launch_count(const dooly_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
+                  const uint32_t* sig, const uint32_t* x, int64_t n_q, double* out,
+                  uint32_t* flag_bits, int64_t* err_first, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: unknown kind");
+  if (n_q < 0 || n_sig < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: negative size");
+  if (n_q > 0 && (!table && n_sig > 0 || !sig || !x || !out))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: null pointer");
+  DeviceGuard g(ctx->device);
+  if (n_q > 0) ctx->launches += 1;
+  return check_cuda(ctx,
+                    dooly::launch_predict(kind, table, n_sig, sig, x, n_q, out, flag_bits,
+                                          err_first, (cudaStream_t)stream, ctx->n_sm),
+                    "predict");
+}
+
+int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
+              const int64_t* pt_off, int64_t n_sig, void* table, double* fit_err,
+              uint8_t* status, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit: unknown kind");
+  if (n_sig < 0 || n_pts < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit: negative size");
+  if (n_sig > 0 && (!pt_off || !table || !fit_err || !status || (n_pts > 0 && (!x || !y))))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit: null pointer");
+  DeviceGuard g(ctx->device);
+  if (n_sig > 0) ctx->launches += 1;
+  return check_cuda(ctx,
+                    dooly::launch_fit(kind, x, n_pts, y, pt_off, n_sig, table, fit_err, status,
+                                      (cudaStream_t)stream, ctx->n_sm),
+                    "fit");
+}
+
+int dooly_sha256_records(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off,
+                         int64_t n, const uint8_t* op_bytes, const int64_t* op_off,
+                         int64_t n_ops, const uint8_t* sym_bytes, const int64_t* sym_off,
+                         int64_t n_sym, const uint8_t* attr_digests, int64_t n_attr,
+                         uint8_t* out_digest, void* stream) {
+  (void)n_ops;
+  (void)n_sym;
+  (void)n_attr;
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records: negative size");
+  if (n > 0 && (!words || !rec_off || !op_bytes || !op_off || !out_digest))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records: null pointer");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_sha256_records(words, rec_off, n, op_bytes, op_off, sym_bytes,
+                                                 sym_off, attr_digests, out_digest,
+                                                 (cudaStream_t)stream, ctx->n_sm,
+                                                 &ctx->launches),
+                    "sha256_records");
+}
+
+int dooly_sha256_messages(dooly_ctx* ctx, const uint8_t* msgs, const int64_t* off, int64_t n,
+                          uint8_t* out_digest, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_messages: negative size");
+  if (n > 0 && (!off || !out_digest))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_messages: null pointer");
+  DeviceGuard g(ctx->device);
+  if (n > 0) ctx->launches += 1;
+  return check_cuda(ctx,
+                    dooly::launch_sha256_messages(msgs, off, n, out_digest,
+                                                  (cudaStream_t)stream, ctx->n_sm),
+                    "sha256_messages");
+}
+
+size_t dooly_dedup_workspace_size(int64_t n, int64_t n_db) {
+  return dooly::dedup_workspace_size(n, n_db);
+}
+
+int dooly_dedup_digests(dooly_ctx* ctx, const uint8_t* digests, int64_t n,
+                        const uint8_t* db_digests, int64_t n_db, int64_t* out_first,
+                        uint32_t* out_uid, uint8_t* out_is_new, uint8_t* out_in_db,
+                        int64_t* out_n_unique, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n < 0 || n_db < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: negative size");
+  if (n + n_db >= (int64_t)0x7FFFFFFF)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: more than 2^31-1 digests per call");
+  if (!out_n_unique || (n > 0 && (!digests || !out_first || !out_uid || !out_is_new)) ||
+      (n_db > 0 && !db_digests))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: null pointer");
+  if (workspace_bytes < dooly::dedup_workspace_size(n, n_db))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: workspace too small");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_dedup(digests, n, db_digests, n_db, out_first, out_uid,
+                                        out_is_new, out_in_db, out_n_unique, workspace,
+                                        workspace_bytes, (cudaStream_t)stream, ctx->n_sm,
+                                        &ctx->launches),
+                    "dedup");
+}
+
+static int check_oplist(dooly_ctx* ctx, const dooly_oplist* ops, int64_t n_aff, int64_t n_attn) {
+  if (!ops || ops->n_ops < 0 || ops->n_ops > DOOLY_MAX_OPS)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "oplist: bad n_ops");
+  for (int e = 0; e < ops->n_ops; ++e) {
+    const int f = ops->feat[e];
+    if (f < DOOLY_FEAT_NUM_TOKS || f > DOOLY_FEAT_COMM)
+      return fail(ctx, DOOLY_ERR_INVALID_ARG, "oplist: bad feature selector");
+    if (f == DOOLY_FEAT_COMM) {
+      if (ops->tp < 2) return fail(ctx, DOOLY_ERR_INVALID_ARG, "oplist: comm entry needs tp>=2");
+      continue;
+    }
+    const int64_t lim = f == DOOLY_FEAT_ATTN ? n_attn : n_aff;
+    if (ops->row[e] < 0 || ops->row[e] >= lim)
+      return fail(ctx, DOOLY_ERR_UNKNOWN_SIGNATURE,
+                  "oplist: entry " + std::to_string(e) + " references row " +
+                      std::to_string(ops->row[e]) + " outside its regressor table");
+  }
+  return DOOLY_OK;
+}
+
+int dooly_iter_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_table,
+                    int64_t n_affine, const void* attn_table, int64_t n_attn,
+                    const uint32_t* it_feat, int64_t n_it, double* it_lat, int64_t* err_first,
+                    void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  int rc = check_oplist(ctx, ops, n_affine, n_attn);
+  if (rc) return rc;
+  if (n_it < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "iter_eval: negative size");
+  if (n_it > 0 && (!it_feat || !it_lat))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "iter_eval: null pointer");
+  DeviceGuard g(ctx->device);
+  if (n_it > 0) ctx->launches += 1;
+  return check_cuda(ctx,
+                    dooly::launch_iter_eval(ops, affine_table, n_affine, attn_table, n_attn,
+                                            it_feat, n_it, it_lat, err_first,
+                                            (cudaStream_t)stream, ctx->n_sm),
+                    "iter_eval");
+}
+
+size_t dooly_sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards) {
+  return dooly::sim_workspace_size(cfg, n_req, n_shards);
+}
+
+int dooly_sim_run(dooly_ctx* ctx, const dooly_oplist* ops, const dooly_sched* cfg,
+                  const void* affine_table, int64_t n_affine, const void* attn_table,
+                  int64_t n_attn, const double* arrival, const uint32_t* prompt,
+                  const uint32_t* output, const uint32_t* cached, const int64_t* shard_off,
+                  int64_t n_shards, double* ttft, double* tpot, int64_t* n_iter,
+                  double* final_clock, int32_t* shard_status, uint32_t* it_log_feat,
+                  double* it_log_lat, int64_t it_log_cap, void* workspace,
+                  size_t workspace_bytes, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  int rc = check_oplist(ctx, ops, n_affine, n_attn);
+  if (rc) return rc;
+  if (!cfg || cfg->chunk < 1 || cfg->max_batch < 1 || cfg->max_batch > 1024 ||
+      cfg->chunk < cfg->max_batch ||
+      cfg->max_iterations < 1 || cfg->kv_capacity_bytes < 0 || cfg->kv_bytes_per_token < 0)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG,
+                "sim: bad scheduler config (need chunk >= max_batch >= 1)");
+  if (n_shards < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "sim: negative shard count");
+  if (n_shards > 0 && (!shard_off || !n_iter || !final_clock || !shard_status))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sim: null pointer");
+  if (workspace_bytes < dooly::sim_workspace_size(cfg, 0, n_shards))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sim: workspace too small");
+  DeviceGuard g(ctx->device);
+  if (n_shards > 0) ctx->launches += 1;
+  return check_cuda(
+      ctx,
+      dooly::launch_sim(ops, cfg, affine_table, n_affine, attn_table, n_attn, arrival, prompt,
+                        output, cached, shard_off, n_shards, ttft, tpot, n_iter, final_clock,
+                        shard_status, it_log_feat, it_log_lat, it_log_cap, workspace,
+                        workspace_bytes, (cudaStream_t)stream, ctx->n_sm),
+      "sim_run");
+}
+
+}  // extern "C"

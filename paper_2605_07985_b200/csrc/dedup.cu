@@ -1,0 +1,183 @@
+// K1b — first-occurrence signature dedup against the DB key set
+// (replaces dedup; key lookup semantics of PAPER.md:333).
+//
+// Open-addressing table of 2^k u32 slots (load <= 0.5) keyed by the 256-bit
+// digest.  A slot stores a record index; it is claimed with atomicCAS and
+// then only ever holds indices of ONE digest, whose minimum is kept with
+// atomicMin — so "first occurrence" is exact and schedule-independent
+// (SURVEY H4).  DB digests are inserted first with indices n + j and mark
+// their slot; a batch record's atomicMin then wins the slot (i < n <= n + j)
+// while the DB mark stays.  Full-digest equality is always checked against
+// the immutable digest arrays, never against slot contents.
+// uids (rank among first occurrences, in index order) come from one
+// exclusive scan of the first-occurrence flags.
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+
+namespace dooly {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr int DEDUP_THREADS = 256;
+
+struct DedupWs {
+  uint32_t* slots;
+  uint8_t* mark;
+  uint32_t* slot_of;
+  uint32_t* first_flag;
+  uint32_t* rank;
+  void* cub_tmp;
+  size_t cub_bytes;
+  uint64_t cap;
+};
+
+static uint64_t table_cap(int64_t n, int64_t n_db) {
+  uint64_t need = 2 * (uint64_t)(n + n_db);
+  uint64_t cap = 1024;
+  while (cap < need) cap <<= 1;
+  return cap;
+}
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+static size_t cub_scan_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                (int)(n > 0 ? n : 1));
+  return bytes;
+}
+
+static DedupWs carve(void* base, int64_t n, int64_t n_db) {
+  DedupWs w;
+  w.cap = table_cap(n, n_db);
+  char* p = static_cast<char*>(base);
+  w.slots = reinterpret_cast<uint32_t*>(p);
+  p += align256(w.cap * 4);
+  w.mark = reinterpret_cast<uint8_t*>(p);
+  p += align256(w.cap);
+  w.slot_of = reinterpret_cast<uint32_t*>(p);
+  p += align256((size_t)n * 4);
+  w.first_flag = reinterpret_cast<uint32_t*>(p);
+  p += align256((size_t)n * 4);
+  w.rank = reinterpret_cast<uint32_t*>(p);
+  p += align256((size_t)n * 4);
+  w.cub_tmp = p;
+  w.cub_bytes = cub_scan_bytes(n);
+  return w;
+}
+
+size_t dedup_workspace_size(int64_t n, int64_t n_db) {
+  const uint64_t cap = table_cap(n, n_db);
+  return align256(cap * 4) + align256(cap) + 3 * align256((size_t)n * 4) +
+         align256(cub_scan_bytes(n)) + 256;
+}
+
+__device__ __forceinline__ void load_digest(const uint8_t* p, uint32_t d[8]) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4 a = __ldg(q), b = __ldg(q + 1);
+  d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w;
+  d[4] = b.x; d[5] = b.y; d[6] = b.z; d[7] = b.w;
+}
+
+__device__ __forceinline__ bool digest_eq(const uint8_t* p, const uint32_t d[8]) {
+  uint32_t e[8];
+  load_digest(p, e);
+  bool eq = true;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) eq &= e[k] == d[k];
+  return eq;
+}
+
+// Insert keys [0, m) of `keys` with slot values base + i.
+__global__ void __launch_bounds__(DEDUP_THREADS) dedup_insert_kernel(
+    const uint8_t* __restrict__ keys, int64_t m, uint32_t base, const uint8_t* __restrict__ batch,
+    int64_t n, const uint8_t* __restrict__ db, uint32_t* slots, uint8_t* mark,
+    uint32_t* slot_of, uint64_t mask) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    uint32_t d[8];
+    load_digest(keys + i * 32, d);
+    const uint32_t me = base + (uint32_t)i;
+    uint64_t slot = d[0] & mask;
+    while (true) {
+      const uint32_t cur = atomicCAS(slots + slot, kEmpty, me);
+      if (cur == kEmpty) break;
+      const uint8_t* other = cur < (uint32_t)n ? batch + (int64_t)cur * 32
+                                               : db + (int64_t)(cur - (uint32_t)n) * 32;
+      if (digest_eq(other, d)) {
+        if (me < cur) atomicMin(slots + slot, me);
+        break;
+      }
+      slot = (slot + 1) & mask;
+    }
+    if (slot_of != nullptr) slot_of[i] = (uint32_t)slot;
+    else mark[slot] = 1;  // DB pass
+  }
+}
+
+__global__ void __launch_bounds__(DEDUP_THREADS) dedup_resolve_kernel(
+    int64_t n, const uint32_t* __restrict__ slots, const uint8_t* __restrict__ mark,
+    const uint32_t* __restrict__ slot_of, int64_t* __restrict__ out_first,
+    uint8_t* __restrict__ out_is_new, uint8_t* __restrict__ out_in_db, uint32_t* first_flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t s = slot_of[i];
+    const uint32_t f = slots[s];
+    const uint8_t in_db = mark[s];
+    const bool first = f == (uint32_t)i;
+    out_first[i] = f;
+    out_is_new[i] = (first && !in_db) ? 1 : 0;
+    if (out_in_db) out_in_db[i] = in_db;
+    first_flag[i] = first ? 1u : 0u;
+  }
+}
+
+__global__ void __launch_bounds__(DEDUP_THREADS) dedup_uid_kernel(
+    int64_t n, const int64_t* __restrict__ out_first, const uint32_t* __restrict__ rank,
+    const uint32_t* __restrict__ first_flag, uint32_t* __restrict__ out_uid,
+    int64_t* __restrict__ out_n_unique) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    out_uid[i] = rank[out_first[i]];
+    if (i == n - 1) *out_n_unique = (int64_t)rank[i] + first_flag[i];
+  }
+}
+
+static unsigned grid_for(int64_t m, int n_sm) {
+  int64_t b = (m + DEDUP_THREADS - 1) / DEDUP_THREADS;
+  const int64_t cap = (int64_t)n_sm * 8;
+  if (b > cap) b = cap;
+  return (unsigned)(b > 0 ? b : 1);
+}
+
+cudaError_t launch_dedup(const uint8_t* digests, int64_t n, const uint8_t* db, int64_t n_db,
+                         int64_t* out_first, uint32_t* out_uid, uint8_t* out_is_new,
+                         uint8_t* out_in_db, int64_t* out_n_unique, void* ws, size_t ws_bytes,
+                         cudaStream_t stream, int n_sm, int64_t* launches) {
+  (void)ws_bytes;
+  cudaError_t e;
+  if (n == 0) return cudaMemsetAsync(out_n_unique, 0, sizeof(int64_t), stream);
+  DedupWs w = carve(ws, n, n_db);
+  if ((e = cudaMemsetAsync(w.slots, 0xFF, w.cap * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(w.mark, 0, w.cap, stream)) != cudaSuccess) return e;
+  const uint64_t mask = w.cap - 1;
+  if (n_db > 0) {
+    dedup_insert_kernel<<<grid_for(n_db, n_sm), DEDUP_THREADS, 0, stream>>>(
+        db, n_db, (uint32_t)n, digests, n, db, w.slots, w.mark, nullptr, mask);
+    *launches += 1;
+  }
+  dedup_insert_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
+      digests, n, 0u, digests, n, db, w.slots, w.mark, w.slot_of, mask);
+  dedup_resolve_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
+      n, w.slots, w.mark, w.slot_of, out_first, out_is_new, out_in_db, w.first_flag);
+  size_t tmp = w.cub_bytes;
+  if ((e = cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.first_flag, w.rank, (int)n, stream)) !=
+      cudaSuccess)
+    return e;
+  dedup_uid_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
+      n, out_first, w.rank, w.first_flag, out_uid, out_n_unique);
+  *launches += 4;  // insert, resolve, cub scan, uid
+  return cudaGetLastError();
+}
+
+}  // namespace dooly

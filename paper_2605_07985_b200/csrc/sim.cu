@@ -1,0 +1,426 @@
+// K4 — fused gather-evaluate-reduce iteration latency (iter_latency,
+// SPEC.md:586-594) and the device-resident serving loop (run, SPEC.md:596-604;
+// schedule_step).
+//
+// iter_eval: one thread per iteration; the op list's regressor rows are staged
+//   once per CTA in shared memory, so each iteration is a pure in-SM
+//   gather/evaluate/reduce over the call graph.
+//
+// sim_run: one WARP per independent replica shard (App. A.14).  Each shard's
+//   event loop is inherently sequential (the clock decides admissions), so the
+//   parallelism is across shards, and inside a shard across the running batch
+//   (lanes own running slots) and across op-list entries (lanes own entries).
+//   The scheduler state lives in shared memory; the per-iteration loop touches
+//   HBM only to read newly admitted requests and to write TTFT/TPOT.
+//
+// Parity: per-entry predictions use the same no-FMA evaluation as predict
+//   (common.cuh); the per-iteration sum runs in op-list order on lane 0 with
+//   separate mul/add, and the clock is a sequential f64 accumulation — the
+//   exact arithmetic sequence of oracle/sim.py, so iteration latencies, the
+//   clock, every admission decision and therefore TTFT/TPOT match bit-for-bit
+//   given the same regressor rows.
+//
+// Scheduler invariant used (proved in DESIGN.md "sim"): at the start of an
+// iteration the running list is [decode-phase ... | at most one prefill-phase
+// request], because prefill budget is granted in running order and admission
+// stops as soon as the budget is exhausted.
+#include "common.cuh"
+
+namespace dooly {
+
+constexpr int SIM_WARPS = 4;
+
+struct StagedOps {
+  AffineRow aff[DOOLY_MAX_OPS];
+  AttnRow attn[DOOLY_MAX_OPS];
+};
+
+__device__ __forceinline__ void stage_ops(const dooly_oplist& ops, const void* aff_t,
+                                          const void* attn_t, StagedOps* s, int tid, int nthr) {
+  for (int e = tid; e < ops.n_ops; e += nthr) {
+    const int f = ops.feat[e];
+    if (f == DOOLY_FEAT_ATTN)
+      s->attn[e] = load_attn(static_cast<const dooly_attn_row*>(attn_t), ops.row[e]);
+    else if (f != DOOLY_FEAT_COMM)
+      s->aff[e] = load_affine(static_cast<const dooly_affine_row*>(aff_t), ops.row[e]);
+  }
+}
+
+// comm_latency: 2(tp-1)/tp * (alpha + bytes/tp * beta), evaluated
+// in Python's operator order.
+__device__ __forceinline__ double comm_latency(int tp, double alpha, double beta, uint64_t bytes) {
+  const double a = __ddiv_rn((double)(2 * (tp - 1)), (double)tp);
+  const double b = mul(__ddiv_rn((double)bytes, (double)tp), beta);
+  return mul(a, add(alpha, b));
+}
+
+// One entry's clamped contribution before the repeat multiply; invalid rows -> NaN.
+__device__ __forceinline__ double entry_value(const dooly_oplist& ops, const StagedOps* s, int e,
+                                              uint32_t num_toks, uint32_t prefill, uint32_t batch,
+                                              uint32_t kv_full, uint32_t kv_win, bool& bad) {
+  const int f = ops.feat[e];
+  bool cl;
+  if (f == DOOLY_FEAT_COMM)
+    return comm_latency(ops.tp, ops.comm_alpha, ops.comm_beta,
+                        (uint64_t)num_toks * (uint64_t)ops.bytes_per_tok[e]);
+  if (f == DOOLY_FEAT_ATTN) {
+    const AttnRow& r = s->attn[e];
+    if (!attn_valid(r)) {
+      bad = true;
+      return nan64();
+    }
+    return clamp_floor(eval_attn(r, prefill, batch, ops.window_slot[e] ? kv_win : kv_full), cl);
+  }
+  const AffineRow& r = s->aff[e];
+  if (!affine_valid(r)) {
+    bad = true;
+    return nan64();
+  }
+  return clamp_floor(eval_affine(r, f == DOOLY_FEAT_NUM_SEQS ? batch : num_toks), cl);
+}
+
+__global__ void __launch_bounds__(256) iter_eval_kernel(
+    const dooly_oplist ops, const void* __restrict__ aff_t, const void* __restrict__ attn_t,
+    const uint32_t* __restrict__ feat, int64_t n_it, double* __restrict__ out,
+    int64_t* __restrict__ err_first) {
+  __shared__ StagedOps s;
+  stage_ops(ops, aff_t, attn_t, &s, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_it; i += stride) {
+    const uint32_t nt = feat[i], pf = feat[n_it + i], bt = feat[2 * n_it + i],
+                   kv = feat[3 * n_it + i], kw = feat[4 * n_it + i];
+    double lat = 0.0;
+    bool bad = false;
+    for (int e = 0; e < ops.n_ops; ++e) {
+      const double v = entry_value(ops, &s, e, nt, pf, bt, kv, kw, bad);
+      lat = add(lat, mul((double)ops.repeat[e], v));
+    }
+    out[i] = lat;
+    if (bad && err_first) atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)i);
+  }
+}
+
+cudaError_t launch_iter_eval(const dooly_oplist* ops, const void* aff, int64_t n_aff,
+                             const void* attn, int64_t n_attn, const uint32_t* it_feat,
+                             int64_t n_it, double* it_lat, int64_t* err_first,
+                             cudaStream_t stream, int n_sm) {
+  (void)n_aff;
+  (void)n_attn;
+  if (n_it == 0) return cudaSuccess;
+  int64_t blocks = (n_it + 255) / 256;
+  if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+  iter_eval_kernel<<<(unsigned)blocks, 256, 0, stream>>>(*ops, aff, attn, it_feat, n_it, it_lat,
+                                                         err_first);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ sim_run
+
+struct SlotArrays {  // per-warp views into dynamic shared memory
+  uint32_t* rq;      // request index within the shard
+  uint32_t* left;    // prefill tokens still to schedule
+  uint32_t* dec;     // output tokens produced
+  uint32_t* kv;      // tokens in the KV cache before this iteration
+  double* t_first;   // first-token time
+};
+
+size_t sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards) {
+  (void)cfg;
+  (void)n_req;
+  (void)n_shards;
+  return 0;  // all scheduler state is in shared memory
+}
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+  return __reduce_add_sync(0xFFFFFFFFu, v);
+}
+
+__global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
+    const dooly_oplist ops, const dooly_sched cfg, const void* __restrict__ aff_t,
+    const void* __restrict__ attn_t, const double* __restrict__ arrival,
+    const uint32_t* __restrict__ prompt, const uint32_t* __restrict__ output,
+    const uint32_t* __restrict__ cached, const int64_t* __restrict__ shard_off, int64_t n_shards,
+    double* __restrict__ ttft, double* __restrict__ tpot, int64_t* __restrict__ n_iter_out,
+    double* __restrict__ clock_out, int32_t* __restrict__ status_out,
+    uint32_t* __restrict__ log_feat, double* __restrict__ log_lat, int64_t log_cap) {
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ StagedOps s_ops;
+  stage_ops(ops, aff_t, attn_t, &s_ops, threadIdx.x, blockDim.x);
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int MB = cfg.max_batch;
+  SlotArrays sl;
+  {
+    unsigned char* p = dyn + (size_t)wid * MB * 24;
+    sl.t_first = reinterpret_cast<double*>(p);
+    sl.rq = reinterpret_cast<uint32_t*>(p + (size_t)MB * 8);
+    sl.left = sl.rq + MB;
+    sl.dec = sl.left + MB;
+    sl.kv = sl.dec + MB;
+  }
+  const uint32_t W = cfg.window > 0 ? (uint32_t)cfg.window : 0u;
+  const uint64_t kvb = (uint64_t)cfg.kv_bytes_per_token;
+  const uint64_t cap = (uint64_t)cfg.kv_capacity_bytes;
+
+  for (int64_t shard = (int64_t)blockIdx.x * SIM_WARPS + wid; shard < n_shards;
+       shard += (int64_t)gridDim.x * SIM_WARPS) {
+    const int64_t base = shard_off[shard];
+    const int64_t n = shard_off[shard + 1] - base;
+    const double* arr = arrival + base;
+    const uint32_t* pr = prompt + base;
+    const uint32_t* ou = output + base;
+    const uint32_t* ca = cached + base;
+    double clock = 0.0;
+    int64_t arrive = 0, admit = 0, it = 0;
+    int nrun = 0;
+    uint64_t reserved = 0;
+    int32_t status = DOOLY_OK;
+    double next_arr = n > 0 ? arr[0] : 0.0;
+
+    while (true) {
+      // ---- 1. arrivals with arrival <= clock (sorted: a ballot prefix)
+      if (arrive < n && next_arr <= clock) {
+        while (true) {
+          const int64_t idx = arrive + lane;
+          const bool in = idx < n && arr[idx] <= clock;
+          const uint32_t b = __ballot_sync(0xFFFFFFFFu, in);
+          const int cnt = __popc(b);  // prefix because arrivals are sorted
+          arrive += cnt;
+          if (cnt < 32) break;
+        }
+        next_arr = arrive < n ? arr[arrive] : 0.0;
+      }
+      if (nrun == 0 && admit == arrive) {
+        if (arrive == n) break;
+        clock = next_arr;  // idle: jump to the next arrival (exact copy)
+        continue;
+      }
+      if (it >= cfg.max_iterations) {  // work remains but the cap is reached
+        status = DOOLY_ERR_NON_TERMINATION;
+        break;
+      }
+      // ---- 2. schedule (decode prefix | <=1 prefill at the tail)
+      const bool has_p = nrun > 0 && sl.left[nrun - 1] > 0;
+      const int n_dec = nrun - (has_p ? 1 : 0);
+      int64_t budget = (int64_t)cfg.chunk - n_dec;
+      uint32_t take_p = 0;
+      if (has_p) {
+        const uint32_t l = sl.left[nrun - 1];
+        take_p = (int64_t)l < budget ? l : (uint32_t)budget;
+        budget -= take_p;
+      }
+      // admissions: lanes prefetch the next 32 waiting requests, lane 0 decides serially
+      const int nrun0 = nrun;
+      uint32_t adm_pf = 0, adm_tok = 0, adm_kv = 0, adm_kvw = 0;
+      int n_adm = 0;
+      while (admit < arrive && nrun < MB && budget > 0) {
+        const int64_t idx = admit + lane;
+        uint32_t p_l = 0, o_l = 0, c_l = 0;
+        if (idx < arrive) {
+          p_l = pr[idx];
+          o_l = ou[idx];
+          c_l = ca[idx];
+        }
+        int took = 0;  // admitted in this round (uniform after broadcast)
+        bool blocked = false;
+        for (int k = 0; k < 32; ++k) {
+          if (admit + k >= arrive || nrun + took >= MB || budget <= 0) break;
+          const uint32_t p = __shfl_sync(0xFFFFFFFFu, p_l, k);
+          const uint32_t o = __shfl_sync(0xFFFFFFFFu, o_l, k);
+          const uint32_t c = __shfl_sync(0xFFFFFFFFu, c_l, k);
+          const uint64_t need = (uint64_t)(p + o) * kvb;
+          if (reserved + need > cap) {
+            blocked = true;
+            break;
+          }
+          const uint32_t work = p - c;
+          const uint32_t take = work > 0 ? ((int64_t)work < budget ? work : (uint32_t)budget) : 1u;
+          budget -= take;
+          reserved += need;
+          if (lane == 0) {
+            const int j = nrun + took;
+            sl.rq[j] = (uint32_t)(admit + k);
+            sl.left[j] = work;   // updated after the iteration
+            sl.dec[j] = take;    // scratch: tokens scheduled this iteration
+            sl.kv[j] = c;
+            sl.t_first[j] = 0.0;
+          }
+          adm_tok += take;
+          if (work > 0) adm_pf += take;
+          adm_kv += c;
+          adm_kvw += W ? min(c, W) : 0u;
+          ++took;
+        }
+        nrun += took;
+        admit += took;
+        n_adm += took;
+        if (blocked || took < 32) break;
+      }
+      if (nrun == 0) {  // head request can never fit the KV capacity
+        status = DOOLY_ERR_INVALID_ARG;
+        break;
+      }
+      __syncwarp();
+      // ---- 3. iteration features
+      uint32_t kvs = 0, kvw = 0;
+      for (int j = lane; j < n_dec; j += 32) {
+        const uint32_t k = sl.kv[j];
+        kvs += k;
+        kvw += W ? min(k, W) : 0u;
+      }
+      kvs = warp_sum_u32(kvs);
+      kvw = warp_sum_u32(kvw);
+      if (take_p > 0) {
+        const uint32_t k = sl.kv[nrun0 - 1];
+        kvs += k;
+        kvw += W ? min(k, W) : 0u;
+      }
+      kvs += adm_kv;
+      kvw += adm_kvw;
+      const uint32_t num_toks = (uint32_t)n_dec + take_p + adm_tok;
+      const uint32_t prefill = take_p + adm_pf;
+      const uint32_t batch = (uint32_t)n_dec + (take_p > 0 ? 1u : 0u) + (uint32_t)n_adm;
+      // ---- 4. fused gather-evaluate-reduce over the call graph
+      bool bad = false;
+      double v0 = 0.0, v1 = 0.0;
+      if (lane < ops.n_ops) v0 = entry_value(ops, &s_ops, lane, num_toks, prefill, batch, kvs, kvw, bad);
+      if (lane + 32 < ops.n_ops)
+        v1 = entry_value(ops, &s_ops, lane + 32, num_toks, prefill, batch, kvs, kvw, bad);
+      double lat = 0.0;
+      for (int e = 0; e < ops.n_ops; ++e) {
+        const double v = __shfl_sync(0xFFFFFFFFu, e < 32 ? v0 : v1, e & 31);
+        lat = add(lat, mul((double)ops.repeat[e], v));
+      }
+      if (__any_sync(0xFFFFFFFFu, bad)) {
+        status = DOOLY_ERR_UNKNOWN_SIGNATURE;
+        break;
+      }
+      clock = add(clock, lat);
+      if (log_feat != nullptr && it < log_cap && lane == 0) {
+        const int64_t row = shard * log_cap + it;
+        uint32_t* lf = log_feat + row * DOOLY_IT_FEATS;
+        lf[0] = num_toks;
+        lf[1] = prefill;
+        lf[2] = batch;
+        lf[3] = kvs;
+        lf[4] = kvw;
+        log_lat[row] = lat;
+      }
+      ++it;
+      // ---- 5. advance request state, stamp tokens, release finished reservations
+      bool fin_any = false;
+      uint64_t freed = 0;
+      for (int j = lane; j < nrun; j += 32) {
+        bool fin = false;
+        const uint32_t r = sl.rq[j];
+        const uint32_t out_n = ou[r];
+        if (j < n_dec) {  // decode: one token
+          sl.kv[j] += 1;
+          const uint32_t d = sl.dec[j] + 1;
+          sl.dec[j] = d;
+          fin = d >= out_n;
+        } else {
+          const bool admitted = j >= nrun0;
+          const uint32_t take = admitted ? sl.dec[j] : take_p;
+          if (take > 0) {
+            const uint32_t l = sl.left[j];
+            if (l > 0) {  // prefill chunk
+              sl.left[j] = l - take;
+              sl.kv[j] += take;
+              sl.dec[j] = 0;
+              if (l == take) {  // last chunk: emits the first output token
+                sl.dec[j] = 1;
+                sl.t_first[j] = clock;
+                ttft[base + r] = clock - arr[r];
+                fin = out_n <= 1;
+              }
+            } else {  // fully cached request admitted this iteration: first decode step
+              sl.kv[j] += 1;
+              sl.dec[j] = 1;
+              sl.t_first[j] = clock;
+              ttft[base + r] = clock - arr[r];
+              fin = out_n <= 1;
+            }
+          }
+        }
+        if (fin) {
+          tpot[base + r] =
+              out_n >= 2 ? __ddiv_rn(clock - sl.t_first[j], (double)(out_n - 1)) : nan64();
+          freed += (uint64_t)(pr[r] + out_n) * kvb;
+          sl.rq[j] = 0xFFFFFFFFu;  // tombstone
+          fin_any = true;
+        }
+      }
+      if (__any_sync(0xFFFFFFFFu, fin_any)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) freed += __shfl_xor_sync(0xFFFFFFFFu, freed, o);
+        reserved -= freed;
+        // stable in-place compaction, 32 slots at a time (reads precede writes
+        // within a chunk and writes never reach the next chunk)
+        int w = 0;
+        for (int j0 = 0; j0 < nrun; j0 += 32) {
+          const int j = j0 + lane;
+          const bool valid = j < nrun;
+          uint32_t rq = 0xFFFFFFFFu, lf = 0, dc = 0, kv = 0;
+          double tf = 0.0;
+          if (valid) {
+            rq = sl.rq[j];
+            lf = sl.left[j];
+            dc = sl.dec[j];
+            kv = sl.kv[j];
+            tf = sl.t_first[j];
+          }
+          const bool keep = rq != 0xFFFFFFFFu;
+          const uint32_t km = __ballot_sync(0xFFFFFFFFu, keep);
+          __syncwarp();
+          if (keep) {
+            const int dst = w + __popc(km & ((1u << lane) - 1u));
+            sl.rq[dst] = rq;
+            sl.left[dst] = lf;
+            sl.dec[dst] = dc;
+            sl.kv[dst] = kv;
+            sl.t_first[dst] = tf;
+          }
+          w += __popc(km);
+          __syncwarp();
+        }
+        nrun = w;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      n_iter_out[shard] = it;
+      clock_out[shard] = clock;
+      status_out[shard] = status;
+    }
+  }
+}
+
+
+cudaError_t launch_sim(const dooly_oplist* ops, const dooly_sched* cfg, const void* aff,
+                       int64_t n_aff, const void* attn, int64_t n_attn, const double* arrival,
+                       const uint32_t* prompt, const uint32_t* output, const uint32_t* cached,
+                       const int64_t* shard_off, int64_t n_shards, double* ttft, double* tpot,
+                       int64_t* n_iter, double* final_clock, int32_t* shard_status,
+                       uint32_t* it_log_feat, double* it_log_lat, int64_t it_log_cap, void* ws,
+                       size_t ws_bytes, cudaStream_t stream, int n_sm) {
+  (void)n_aff;
+  (void)n_attn;
+  (void)ws;
+  (void)ws_bytes;
+  (void)n_sm;
+  if (n_shards == 0) return cudaSuccess;
+  const size_t smem = (size_t)SIM_WARPS * cfg->max_batch * 24;
+  cudaError_t e = cudaFuncSetAttribute(sim_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t blocks = (n_shards + SIM_WARPS - 1) / SIM_WARPS;
+  sim_run_kernel<<<(unsigned)blocks, SIM_WARPS * 32, smem, stream>>>(
+      *ops, *cfg, aff, attn, arrival, prompt, output, cached, shard_off, n_shards, ttft, tpot,
+      n_iter, final_clock, shard_status, it_log_feat, it_log_lat, it_log_cap);
+  return cudaGetLastError();
+}
+
+}  // namespace dooly

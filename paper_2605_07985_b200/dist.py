@@ -1,0 +1,122 @@
+"""Multi-GPU partitioning of the hot path: one process per GPU,
+``torch.distributed`` (NCCL over NVLink on the GPU box, gloo in CPU tests) for
+the plumbing.
+
+  dedup   records split contiguously by global index; each rank hashes its own
+          slice (the ALU-bound part), ONE all-gather of the 32-B digests, then
+          every rank resolves first occurrences over the full digest list (exact
+          for any world size) and keeps its slice.
+  fit     signatures split into contiguous ranges, no communication during the
+          fit, ONE all-gather of the fitted regressor rows (p*8 + box bytes per
+          signature) so every rank holds the full table.
+  predict queries split contiguously; no collective (each rank holds the table).
+  sim     S fixed replica shards, shard s on rank s mod world ("replicas only",
+          no data-path collective); per-request TTFT/TPOT gathered at the end.
+"""
+
+from __future__ import annotations
+
+import os
+from typing import Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def world() -> tuple:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def init_from_env(backend: Optional[str] = None) -> tuple:
+    """Initialise the default group from torchrun's env (127.0.0.1 rendezvous)."""
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group(backend=backend)
+    return world()
+
+
+def shard_range(n: int, rank: int, size: int) -> tuple:
+    """Contiguous split of [0, n): the first n % size ranks get one extra."""
+    q, r = divmod(n, size)
+    a = rank * q + min(rank, r)
+    return a, a + q + (1 if rank < r else 0)
+
+
+def all_gather_rows(local: torch.Tensor, n_total: int, group=None) -> torch.Tensor:
+    """Concatenate per-rank row blocks of a contiguous split of n_total rows.
+
+    Blocks differ by at most one row; they are padded to ceil(n/size) rows for
+    a single all_gather_into_tensor, then trimmed."""
+    rank, size = world()
+    if size == 1:
+        return local
+    per = -(-n_total // size)
+    pad = torch.zeros((per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    out = _gather_cat(pad, size, group)
+    keep = [out[r * per: r * per + (shard_range(n_total, r, size)[1] -
+                                    shard_range(n_total, r, size)[0])] for r in range(size)]
+    return torch.cat(keep, dim=0)
+
+
+def csr_slice(x: torch.Tensor, y: torch.Tensor, off: np.ndarray, a: int, b: int):
+    """Signatures [a, b) of a CSR batch -> (x, y, rebased offsets) views."""
+    p0, p1 = int(off[a]), int(off[b])
+    return x[:, p0:p1].contiguous(), y[p0:p1].contiguous(), off[a:b + 1] - off[a]
+
+
+def fit_sharded(kind: int, x: torch.Tensor, y: torch.Tensor, off: np.ndarray, group=None):
+    """Fit this rank's contiguous signature range, all-gather the regressor rows."""
+    from .sim import FitResult, fit_tables
+
+    rank, size = world()
+    n_sig = len(off) - 1
+    a, b = shard_range(n_sig, rank, size)
+    xs, ys, lo = csr_slice(x, y, off, a, b)
+    local = fit_tables(kind, xs, ys, torch.from_numpy(np.ascontiguousarray(lo)).to(y.device))
+    if size == 1:
+        return local
+    return FitResult(kind, all_gather_rows(local.table, n_sig, group),
+                     all_gather_rows(local.fit_err, n_sig, group),
+                     all_gather_rows(local.status, n_sig, group))
+
+
+def dedup_sharded(recs_local, n_total: int, db_digests: Optional[torch.Tensor] = None,
+                  workspace=None, group=None):
+    """Hash the local records, all-gather digests, dedup globally, keep local slice."""
+    from .profiler import DedupResult, dedup_digests, hash_records
+
+    rank, size = world()
+    local = hash_records(recs_local)
+    full = all_gather_rows(local, n_total, group) if size > 1 else local
+    res = dedup_digests(full, db_digests, workspace, sync=True)
+    a, b = shard_range(n_total, rank, size)
+    return DedupResult(res.digests[a:b], res.first[a:b], res.uid[a:b], res.is_new[a:b],
+                       res.in_db[a:b], res.n_unique)
+
+
+def gather_requests(values: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather equally sized per-rank vectors (e.g. padded TTFT blocks)."""
+    rank, size = world()
+    if size == 1:
+        return values
+    return _gather_cat(values.contiguous(), size, group).view((size,) + tuple(values.shape))
+
+
+def _gather_cat(t: torch.Tensor, size: int, group=None) -> torch.Tensor:
+    """all_gather of equal-shape tensors concatenated on dim 0 (one NCCL call)."""
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((t.shape[0] * size,) + tuple(t.shape[1:]), dtype=t.dtype,
+                          device=t.device)
+        dist.all_gather_into_tensor(out, t, group=group)
+        return out
+    parts = [torch.empty_like(t) for _ in range(size)]
+    dist.all_gather(parts, t, group=group)
+    return torch.cat(parts, dim=0)

@@ -1,0 +1,463 @@
+"""Duplication-aware profiler: the drop-in for the reference's `dooly.profiler`
+(module absent from pkg/src).
+
+Hot path (GPU, libdooly_b200):
+    canonicalize -> signature_hash -> dedup
+  ``dedup_packed`` hashes packed records on the device (K1a) and resolves
+  first occurrences against the DB key set (K1b).  ``dedup`` / ``signature_hash``
+  are thin wrappers over the same device path (no CPU fallback).
+
+Host side (inputs to the fit, SURVEY §8(f) row f1 is their GPU fusion):
+    sweep, oracle_latency, comm_latency
+  and a minimal in-memory ``LatencyDB`` with the Fig. 9 logical tables
+   — configurations, signatures, model_operations,
+  measurements — persisted as one .npz file.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DuplicateKey, OraclePanic, StoreUnavailable
+from .modelir import BackendSpec, HardwareSpec, ModelConfig, SweepGrid
+from .records import PackedRecords, RunnableEntry, canonical_bytes, pack_entries
+
+OVERHEAD_S = 5e-6  # fixed launch overhead of the analytical latency model
+
+
+def _device(device=None) -> torch.device:
+    if device is None:
+        if not torch.cuda.is_available():
+            raise StoreUnavailable("libdooly_b200 needs a CUDA device (no CPU fallback)")
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+# ------------------------------------------------------------------ signatures
+
+
+def canonicalize(entry: RunnableEntry) -> bytes:
+    """Canonical serialisation of one runnable entry."""
+    return canonical_bytes(entry)
+
+
+def signature_hash(canonical: bytes, device=None) -> bytes:
+    """SHA-256 of a canonical message, computed by the GPU kernel."""
+    return signature_hash_batch([canonical], device)[0]
+
+
+def signature_hash_batch(messages: Sequence[bytes], device=None) -> list:
+    dev = _device(device)
+    n = len(messages)
+    if n == 0:
+        return []
+    off = np.zeros(n + 1, dtype=np.int64)
+    off[1:] = np.cumsum([len(m) for m in messages])
+    data = np.frombuffer(b"".join(messages) or b"\0", dtype=np.uint8)
+    d_msgs = torch.from_numpy(data.copy()).to(dev)
+    d_off = torch.from_numpy(off).to(dev)
+    out = torch.empty((n, 32), dtype=torch.uint8, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_sha256_messages(
+        ctx, d_msgs.data_ptr(), d_off.data_ptr(), n, out.data_ptr(), _lib.stream_ptr(dev)), ctx)
+    host = out.cpu().numpy()
+    return [bytes(host[i]) for i in range(n)]
+
+
+@dataclass
+class DeviceRecords:
+    words: torch.Tensor
+    rec_off: torch.Tensor
+    op_bytes: torch.Tensor
+    op_off: torch.Tensor
+    sym_bytes: torch.Tensor
+    sym_off: torch.Tensor
+    attr_digests: torch.Tensor
+    n: int
+
+    @staticmethod
+    def from_packed(p: PackedRecords, device) -> "DeviceRecords":
+        dev = torch.device(device)
+
+        def t(a, dtype):
+            a = np.ascontiguousarray(a)
+            if a.size == 0:
+                a = np.zeros(1, dtype=a.dtype)
+            return torch.from_numpy(a.view(dtype) if a.dtype != dtype else a).to(dev)
+
+        return DeviceRecords(t(p.words.view(np.int32), np.int32), t(p.rec_off, np.int64),
+                             t(p.op_bytes, np.uint8), t(p.op_off, np.int64),
+                             t(p.sym_bytes, np.uint8), t(p.sym_off, np.int64),
+                             t(p.attr_digests.reshape(-1), np.uint8), p.n)
+
+
+def hash_records(recs: DeviceRecords, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """K1a: SHA-256 of every packed record's canonical message -> (n, 32) u8."""
+    dev = recs.words.device
+    if out is None:
+        out = torch.empty((recs.n, 32), dtype=torch.uint8, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_sha256_records(
+        ctx, recs.words.data_ptr(), recs.rec_off.data_ptr(), recs.n, recs.op_bytes.data_ptr(),
+        recs.op_off.data_ptr(), recs.op_off.numel() - 1, recs.sym_bytes.data_ptr(),
+        recs.sym_off.data_ptr(), recs.sym_off.numel() - 1, recs.attr_digests.data_ptr(),
+        recs.attr_digests.numel() // 32, out.data_ptr(), _lib.stream_ptr(dev)), ctx)
+    return out
+
+
+@dataclass
+class DedupResult:
+    digests: torch.Tensor     # (n, 32) u8
+    first: torch.Tensor       # (n,) i64 smallest index with the same digest
+    uid: torch.Tensor         # (n,) i32 rank of `first` among first occurrences
+    is_new: torch.Tensor      # (n,) u8  first occurrence and not in the DB -> profile it
+    in_db: torch.Tensor       # (n,) u8
+    n_unique: int
+
+    def to_profile_index(self) -> np.ndarray:
+        return np.nonzero(self.is_new.cpu().numpy())[0]
+
+
+class DedupWorkspace:
+    """Reusable device scratch for dedup_digests (no allocation in the hot call)."""
+
+    def __init__(self, device) -> None:
+        self.device = torch.device(device)
+        self.buf = torch.empty(0, dtype=torch.uint8, device=self.device)
+
+    def get(self, n: int, n_db: int) -> torch.Tensor:
+        need = int(_lib.load_library().dooly_dedup_workspace_size(n, n_db))
+        if self.buf.numel() < need:
+            self.buf = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def dedup_digests(digests: torch.Tensor, db_digests: Optional[torch.Tensor] = None,
+                  workspace: Optional[DedupWorkspace] = None, sync: bool = True) -> DedupResult:
+    """K1b: first-occurrence dedup of (n, 32) digests against a (n_db, 32) key set."""
+    dev = digests.device
+    n = digests.shape[0]
+    if db_digests is None:
+        db_digests = torch.empty((0, 32), dtype=torch.uint8, device=dev)
+    n_db = db_digests.shape[0]
+    ws = (workspace or DedupWorkspace(dev)).get(n, n_db)
+    first = torch.empty(n, dtype=torch.int64, device=dev)
+    uid = torch.empty(n, dtype=torch.int32, device=dev)
+    is_new = torch.empty(n, dtype=torch.uint8, device=dev)
+    in_db = torch.empty(n, dtype=torch.uint8, device=dev)
+    n_unique = torch.empty(1, dtype=torch.int64, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_dedup_digests(
+        ctx, digests.data_ptr() if n else 0, n, db_digests.data_ptr() if n_db else 0, n_db,
+        first.data_ptr(), uid.data_ptr(), is_new.data_ptr(), in_db.data_ptr(),
+        n_unique.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev)), ctx)
+    nu = int(n_unique.item()) if sync else -1
+    return DedupResult(digests, first, uid, is_new, in_db, nu)
+
+
+def dedup_packed(recs: DeviceRecords, db_digests: Optional[torch.Tensor] = None,
+                 workspace: Optional[DedupWorkspace] = None, sync: bool = True) -> DedupResult:
+    """Batch form of dedup: packed records in HBM -> digests + dedup table."""
+    return dedup_digests(hash_records(recs), db_digests, workspace, sync)
+
+
+# ------------------------------------------------------------------ LatencyDB
+
+
+def _kind_of(entry: RunnableEntry) -> int:
+    return _lib.KIND_ATTN if entry.feature == "attention" else _lib.KIND_AFFINE
+
+
+@dataclass
+class SignatureRow:
+    digest: bytes
+    op_name: str
+    granularity: str
+    kind: int
+    feature: str
+
+
+@dataclass
+class LatencyDB:
+    """In-memory store with the Fig. 9 logical schema (D5 :517)."""
+
+    configurations: list = field(default_factory=list)     # (hardware, model, backend, tp)
+    signatures: list = field(default_factory=list)         # SignatureRow, insertion order
+    model_operations: list = field(default_factory=list)   # (config_id, digest, repeat)
+    measurements: dict = field(default_factory=dict)       # digest -> (x (p, n) u32, y f64)
+    _index: dict = field(default_factory=dict)
+
+    SCHEMA = ("configurations(id, hardware, model, backend, tp_degree)\n"
+              "signatures(hash PRIMARY KEY, op_name, granularity, kind, feature)\n"
+              "model_operations(config_id -> configurations, signature_hash -> signatures, "
+              "repeat_count)\n"
+              "measurements(signature_hash -> signatures, features..., latency_s)\n")
+
+    def schema_dump(self) -> str:
+        return self.SCHEMA
+
+    def has(self, digest: bytes) -> bool:
+        return digest in self._index
+
+    def signature(self, digest: bytes) -> SignatureRow:
+        return self.signatures[self._index[digest]]
+
+    def add_configuration(self, hardware: str, model: str, backend: str, tp: int) -> int:
+        key = (hardware, model, backend, tp)
+        if key in self.configurations:
+            return self.configurations.index(key)
+        self.configurations.append(key)
+        return len(self.configurations) - 1
+
+    def add_signature(self, digest: bytes, entry: RunnableEntry) -> None:
+        if digest not in self._index:
+            self._index[digest] = len(self.signatures)
+            self.signatures.append(SignatureRow(digest, entry.name, entry.granularity,
+                                                _kind_of(entry), entry.feature))
+
+    def insert_measurements(self, digest: bytes, x: np.ndarray, y: np.ndarray) -> None:
+        """Insert a sweep; re-inserting an identical key with a different latency
+        raises DuplicateKey."""
+        if digest not in self._index:
+            raise StoreUnavailable("model_operations/measurements must reference a signature")
+        x = np.atleast_2d(np.asarray(x, dtype=np.uint32))
+        y = np.asarray(y, dtype=np.float64)
+        if digest in self.measurements:
+            ox, oy = self.measurements[digest]
+            old = {tuple(ox[:, i]): oy[i] for i in range(oy.shape[0])}
+            keep = []
+            for i in range(y.shape[0]):
+                k = tuple(x[:, i])
+                if k in old:
+                    if old[k] != y[i]:
+                        raise DuplicateKey(f"{digest.hex()[:12]} at {k}: {old[k]} != {y[i]}")
+                else:
+                    keep.append(i)
+            x = np.concatenate([ox, x[:, keep]], axis=1)
+            y = np.concatenate([oy, y[keep]])
+        self.measurements[digest] = (x, y)
+
+    def digest_tensor(self, device) -> torch.Tensor:
+        if not self.signatures:
+            return torch.empty((0, 32), dtype=torch.uint8, device=device)
+        arr = np.frombuffer(b"".join(s.digest for s in self.signatures), dtype=np.uint8)
+        return torch.from_numpy(arr.reshape(-1, 32).copy()).to(device)
+
+    def save(self, path) -> None:
+        sig = np.array([[s.digest.hex(), s.op_name, s.granularity, str(s.kind), s.feature]
+                        for s in self.signatures], dtype=object)
+        meas = {f"x_{d.hex()}": v[0] for d, v in self.measurements.items()}
+        meas.update({f"y_{d.hex()}": v[1] for d, v in self.measurements.items()})
+        np.savez(path, signatures=sig,
+                 configurations=np.array(self.configurations, dtype=object),
+                 model_operations=np.array([(c, d.hex(), r) for c, d, r in self.model_operations],
+                                           dtype=object), **meas)
+
+    @staticmethod
+    def load(path) -> "LatencyDB":
+        try:
+            z = np.load(path, allow_pickle=True)
+        except OSError as exc:
+            raise StoreUnavailable(str(exc)) from exc
+        db = LatencyDB()
+        db.configurations = [tuple(c) for c in z["configurations"].tolist()]
+        for h, name, gran, kind, feat in z["signatures"].tolist():
+            d = bytes.fromhex(h)
+            db._index[d] = len(db.signatures)
+            db.signatures.append(SignatureRow(d, name, gran, int(kind), feat))
+        db.model_operations = [(int(c), bytes.fromhex(h), int(r))
+                               for c, h, r in z["model_operations"].tolist()]
+        for key in z.files:
+            if key.startswith("x_"):
+                d = bytes.fromhex(key[2:])
+                db.measurements[d] = (z[key], z["y_" + key[2:]])
+        return db
+
+
+def dedup(entries: Sequence[RunnableEntry], db: LatencyDB, config_id: Optional[int] = None,
+          device=None, register: bool = True):
+    """Partition entries into (to_profile, skipped).
+
+    skipped <=> the signature is already in the DB, or an earlier entry of this
+    call has it.  model_operations rows are recorded for ALL entries when a
+    config id is given; new signatures are registered so a re-run profiles
+    nothing."""
+    to_profile, skipped, _ = dedup_with_digests(entries, db, config_id, device, register)
+    return to_profile, skipped
+
+
+def dedup_with_digests(entries: Sequence[RunnableEntry], db: LatencyDB,
+                       config_id: Optional[int] = None, device=None, register: bool = True):
+    """dedup that also returns the device-computed digest of every to_profile entry."""
+    if db is None:
+        raise StoreUnavailable("no latency database")
+    dev = _device(device)
+    entries = list(entries)
+    if not entries:
+        return [], [], []
+    recs = DeviceRecords.from_packed(pack_entries(entries), dev)
+    res = dedup_packed(recs, db.digest_tensor(dev))
+    is_new = res.is_new.cpu().numpy().astype(bool)
+    digs = res.digests.cpu().numpy()
+    to_profile, skipped, new_digests = [], [], []
+    for i, e in enumerate(entries):
+        d = bytes(digs[i])
+        if config_id is not None:
+            db.model_operations.append((config_id, d, e.repeat_count))
+        if is_new[i]:
+            to_profile.append(e)
+            new_digests.append(d)
+            if register:
+                db.add_signature(d, e)
+        else:
+            skipped.append(e)
+    return to_profile, skipped, new_digests
+
+
+# ------------------------------------------- analytical latency model (host, f1)
+
+
+def comm_latency(topology: str, tp: int, nbytes: int, hw: HardwareSpec) -> float:
+    """Ring all-reduce alpha-beta model, Python operator order."""
+    del topology  # keyed by (topology, tp) in the DB; the formula is topology-free
+    if tp < 2:
+        raise ValueError("comm_latency needs tp >= 2")
+    return 2 * (tp - 1) / tp * (hw.comm_alpha + nbytes / tp * hw.comm_beta)
+
+
+def _dims(entry: RunnableEntry) -> list:
+    return [[s for s, _ in a] for a in entry.arg_template]
+
+
+def op_cost(entry: RunnableEntry, point: dict, dtype_bytes: int) -> tuple:
+    """(flops, bytes) of one op instance at a sweep point."""
+    name = entry.name
+    a = _dims(entry)
+    t = point.get("num_toks", 1)
+    if name == "linear":
+        k, n = a[1][1], a[1][0]
+        m = point["num_reqs"] if entry.feature == "num_seqs" else t
+        return 2.0 * m * k * n, float((m * k + k * n + m * n) * dtype_bytes)
+    if name == "embedding":
+        h = a[1][1]
+        return 0.0, float(2 * t * h * dtype_bytes + 4 * t)
+    if name == "rms_norm":
+        h = a[0][1]
+        return 4.0 * t * h, float((2 * t * h + h) * dtype_bytes)
+    if name == "rotary_embedding":
+        w = a[0][1] * a[0][2] + a[1][1] * a[1][2]
+        return 3.0 * t * w, float(2 * t * w * dtype_bytes)
+    if name == "silu_and_mul":
+        i2 = a[0][1]
+        return 2.0 * t * i2, float((t * i2 + t * i2 // 2) * dtype_bytes)
+    if name == "topk_softmax":
+        e = a[0][1]
+        return 5.0 * t * e, float(t * e * (dtype_bytes + 8))
+    if name == "fused_moe":
+        e, i2, h = a[1]
+        k = entry.scalars[0][0]
+        touched = min(e, t * k)
+        return 2.0 * t * k * (i2 + i2 // 2) * h, float(
+            (touched * (i2 + i2 // 2) * h + 2 * t * h) * dtype_bytes)
+    if name == "attention":
+        hq, d = a[0][1], a[0][2]
+        hkv = a[1][1]
+        r = point["num_reqs"]
+        c = point["kv_len"]
+        if entry.window:
+            c = min(c, entry.window)
+        if point["phase"] == "prefill":
+            q = t / r
+        else:
+            q = 1.0
+        ctx = c + q
+        flops = 4.0 * hq * d * r * q * ctx
+        nbytes = float(dtype_bytes * (r * ctx * 2 * hkv * d + 2 * r * q * hq * d))
+        return flops, nbytes
+    if name == "reshape":
+        return 0.0, 0.0
+    raise OraclePanic(f"no cost formula for op kind {name!r} at {point}")
+
+
+def oracle_latency(entry: RunnableEntry, point: dict, hw: HardwareSpec, backend: BackendSpec,
+                   dtype_bytes: int = 2) -> float:
+    """overhead + multiplier * max(flops/peak, bytes/bw)."""
+    flops, nbytes = op_cost(entry, point, dtype_bytes)
+    syms = entry.kernel_symbols
+    if entry.feature == "attention":
+        syms = tuple(s.replace("_decode_attn_", f"_{point['phase']}_attn_") for s in syms)
+    mult = backend.multiplier(syms)
+    return OVERHEAD_S + mult * max(flops / hw.peak_flops, nbytes / hw.mem_bw)
+
+
+def sweep_points(entry: RunnableEntry, grid: SweepGrid, max_context: int) -> list:
+    """Training points of one signature (D3 :515, App. A.5)."""
+    cap_t = min(grid.prefill_chunk, max_context)
+    toks = [t for t in grid.token_counts if t <= cap_t]
+    reqs = [r for r in grid.request_counts if r <= grid.max_batch]
+    if entry.feature == "num_toks":
+        return [{"num_toks": t} for t in toks]
+    if entry.feature == "num_seqs":
+        return [{"num_reqs": r} for r in reqs]
+    pts = []
+    for t in toks:
+        for r in reqs:
+            if t < r:
+                continue
+            for c in grid.kv_lens:
+                if c + -(-t // r) <= max_context:
+                    pts.append({"phase": "prefill", "num_toks": t, "num_reqs": r, "kv_len": c})
+    for r in reqs:
+        for c in grid.kv_lens:
+            if c + 1 <= max_context:
+                pts.append({"phase": "decode", "num_toks": r, "num_reqs": r, "kv_len": c})
+    return pts
+
+
+def point_features(entry: RunnableEntry, p: dict) -> tuple:
+    """Regression features of a sweep point (App. A.6): affine -> (x,), attention ->
+    (prefill_toks, batch, kv_tokens) with kv capped by the sliding window."""
+    if entry.feature == "num_toks":
+        return (p["num_toks"],)
+    if entry.feature == "num_seqs":
+        return (p["num_reqs"],)
+    c = min(p["kv_len"], entry.window) if entry.window else p["kv_len"]
+    pre = p["num_toks"] if p["phase"] == "prefill" else 0
+    return (pre, p["num_reqs"], p["num_reqs"] * c)
+
+
+def sweep(entry: RunnableEntry, grid: SweepGrid, model: ModelConfig, hw: HardwareSpec,
+          backend: BackendSpec):
+    """Evaluate the analytical model over the signature's grid -> (x (p, n) u32, y f64)."""
+    pts = sweep_points(entry, grid, model.max_context)
+    x = np.array([point_features(entry, p) for p in pts], dtype=np.uint32).T
+    y = np.array([oracle_latency(entry, p, hw, backend, model.dtype_bytes) for p in pts])
+    return np.ascontiguousarray(x), y
+
+
+def profile_corpus(manifest, db: Optional[LatencyDB] = None, device=None,
+                   grid: Optional[SweepGrid] = None):
+    """cmd_profile without the CLI: dedup every (model, backend)
+    runnable set in manifest order against the DB, sweep the new signatures.
+    Returns (db, report) with per-config N/R counts."""
+    from .records import synthesize_entries
+
+    db = db if db is not None else LatencyDB()
+    grid = grid or manifest.grid
+    report = []
+    for m in manifest.models:
+        for b in manifest.backends:
+            cid = db.add_configuration(manifest.hardware.name, m.name, b.name, manifest.tp_degree)
+            entries = synthesize_entries(m, b, manifest.tp_degree)
+            to_profile, skipped, digests = dedup_with_digests(entries, db, cid, device)
+            for e, d in zip(to_profile, digests):
+                x, y = sweep(e, grid, m, manifest.hardware, b)
+                db.insert_measurements(d, x, y)
+            report.append({"model": m.name, "backend": b.name, "entries": len(entries),
+                           "profiled": len(to_profile), "skipped": len(skipped)})
+    return db, report

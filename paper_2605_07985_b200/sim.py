@@ -1,0 +1,526 @@
+"""Regression-backed serving simulation: the drop-in for the reference's
+`dooly.sim` (module absent from pkg/src).
+
+    fit(db)                 -> Regressors        K2
+    predict(regs, sig, x)   -> seconds           K3
+    iter_latency(batch, calltree, regs)          K4a
+    run(workload, model, backend, hw, regs, sched) -> Metrics   K4b
+    mape(pred, truth)                            (host utility)
+
+Every scalar form is a one-element call of the batch form (``fit_tables``,
+``predict_batch``, ``iter_latency_batch``, ``run_shards``), which launch the
+sm_100a kernels of libdooly_b200 on the current stream.  There is no CPU
+fallback: without the library or a CUDA device these raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import (InsufficientData, LengthMismatch, NonTermination, UnknownSignature,
+                     ValidationError, ZeroTruth)
+from .modelir import BackendSpec, HardwareSpec, ModelConfig, Request
+from .profiler import LatencyDB, _device, DeviceRecords, hash_records
+from .records import RunnableEntry, pack_entries, synthesize_entries
+
+NEED = {_lib.KIND_AFFINE: 4, _lib.KIND_ATTN: 11}          # max(4, p + 1), App. A.8
+FEATURE_NAMES = {_lib.KIND_AFFINE: ("num_toks",),
+                 _lib.KIND_ATTN: ("prefill_toks", "batch_size", "kv_tokens")}
+AFFINE_ROW = np.dtype([("c", "<f8", 2), ("inv", "<f8", 1), ("lo", "<u4", 1), ("hi", "<u4", 1)])
+ATTN_ROW = np.dtype([("c", "<f8", 10), ("inv", "<f8", 3), ("lo", "<u4", 3), ("hi", "<u4", 3)])
+ROW_DTYPE = {_lib.KIND_AFFINE: AFFINE_ROW, _lib.KIND_ATTN: ATTN_ROW}
+PERCENTILES = (25, 50, 75, 90, 95, 99)
+
+
+# ------------------------------------------------------------------------ fit
+
+
+@dataclass
+class FitResult:
+    kind: int
+    table: torch.Tensor        # (n_sig, row_bytes) u8 on device
+    fit_err: torch.Tensor      # (n_sig,) f64
+    status: torch.Tensor       # (n_sig,) u8 (0 ok, 1 insufficient)
+
+    def rows(self) -> np.ndarray:
+        return self.table.cpu().numpy().view(ROW_DTYPE[self.kind]).reshape(-1)
+
+
+def fit_tables(kind: int, x: torch.Tensor, y: torch.Tensor, pt_off: torch.Tensor,
+               out: Optional[FitResult] = None) -> FitResult:
+    """Batch fit (K2) of n_sig signatures whose points are CSR-ranged by pt_off.
+
+    x: (P, n_pts) int32/uint32 device tensor (P = 1 affine, 3 attention),
+    y: (n_pts,) f64, pt_off: (n_sig + 1,) i64.  Asynchronous; no exceptions
+    for per-signature shortfalls (see ``status``)."""
+    dev = y.device
+    n_sig = pt_off.numel() - 1
+    n_pts = y.numel()
+    if x.shape != (_lib.PLANES[kind], n_pts):
+        raise ValueError(f"x must have shape ({_lib.PLANES[kind]}, {n_pts}), got {tuple(x.shape)}")
+    if out is None:
+        out = FitResult(kind, torch.empty((n_sig, _lib.ROW_BYTES[kind]), dtype=torch.uint8,
+                                          device=dev),
+                        torch.empty(n_sig, dtype=torch.float64, device=dev),
+                        torch.empty(n_sig, dtype=torch.uint8, device=dev))
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_fit(
+        ctx, kind, x.data_ptr(), n_pts, y.data_ptr(), pt_off.data_ptr(), n_sig,
+        out.table.data_ptr(), out.fit_err.data_ptr(), out.status.data_ptr(),
+        _lib.stream_ptr(dev)), ctx)
+    return out
+
+
+@dataclass
+class Regressor:
+    """Host view of one fitted regressor."""
+
+    signature_hash: bytes
+    feature_names: tuple
+    coefficients: tuple          # scaled basis
+    inv_scale: tuple
+    box: tuple                   # ((lo, hi), ...) training box
+    fit_error: float
+
+
+@dataclass
+class Regressors:
+    """All fitted signatures: one device table per regression kind plus the
+    digest -> (kind, row) index."""
+
+    tables: dict                  # kind -> FitResult
+    index: dict                   # digest -> (kind, row)
+    device: torch.device
+
+    def n(self, kind: int) -> int:
+        fr = self.tables.get(kind)
+        return 0 if fr is None else fr.table.shape[0]
+
+    def table_ptr(self, kind: int) -> int:
+        fr = self.tables.get(kind)
+        return 0 if fr is None or fr.table.numel() == 0 else fr.table.data_ptr()
+
+    def regressor(self, digest: bytes) -> Regressor:
+        if digest not in self.index:
+            raise UnknownSignature(digest.hex())
+        kind, row = self.index[digest]
+        r = self.tables[kind].rows()[row]
+        return Regressor(digest, FEATURE_NAMES[kind], tuple(np.atleast_1d(r["c"]).tolist()),
+                         tuple(np.atleast_1d(r["inv"]).tolist()),
+                         tuple(zip(np.atleast_1d(r["lo"]).tolist(), np.atleast_1d(r["hi"]).tolist())),
+                         float(self.tables[kind].fit_err[row].item()))
+
+    def __contains__(self, digest: bytes) -> bool:
+        return digest in self.index
+
+
+def _csr(items: Sequence, planes: int):
+    """[(x (P, n_i), y (n_i,))] -> (x (P, N) u32, y (N,), off (n+1,))."""
+    off = np.zeros(len(items) + 1, dtype=np.int64)
+    if items:
+        off[1:] = np.cumsum([it[1].shape[0] for it in items])
+    x = np.zeros((planes, int(off[-1])), dtype=np.uint32)
+    y = np.zeros(int(off[-1]), dtype=np.float64)
+    for i, (xi, yi) in enumerate(items):
+        x[:, off[i]:off[i + 1]] = np.asarray(xi, dtype=np.uint32).reshape(planes, -1)
+        y[off[i]:off[i + 1]] = yi
+    return x, y, off
+
+
+def fit(db: LatencyDB, device=None, strict: bool = True) -> Regressors:
+    """One least-squares regressor per measured signature.
+
+    Raises InsufficientData(signature, have, need) for the first signature with
+    fewer than max(4, p + 1) measurements (App. A.8) when ``strict``."""
+    dev = _device(device)
+    tables, index = {}, {}
+    for kind in (_lib.KIND_AFFINE, _lib.KIND_ATTN):
+        sigs = [s for s in db.signatures if s.kind == kind and s.digest in db.measurements]
+        items = [db.measurements[s.digest] for s in sigs]
+        if strict:
+            for s, (_, y) in zip(sigs, items):
+                if y.shape[0] < NEED[kind]:
+                    raise InsufficientData(s.digest.hex(), int(y.shape[0]), NEED[kind])
+        x, y, off = _csr(items, _lib.PLANES[kind])
+        fr = fit_tables(kind, torch.from_numpy(x.view(np.int32)).to(dev),
+                        torch.from_numpy(y).to(dev), torch.from_numpy(off).to(dev))
+        tables[kind] = fr
+        for row, s in enumerate(sigs):
+            index[s.digest] = (kind, row)
+    torch.cuda.synchronize(dev)
+    return Regressors(tables, index, dev)
+
+
+# -------------------------------------------------------------------- predict
+
+
+def predict_batch(kind: int, table: torch.Tensor, sig: torch.Tensor, x: torch.Tensor,
+                  out: Optional[torch.Tensor] = None, flags: Optional[torch.Tensor] = None,
+                  err_first: Optional[torch.Tensor] = None, want_flags: bool = True):
+    """K3 over n_q queries: sig (n_q,) i32 rows of ``table`` (n_sig, row_bytes) u8,
+    x (P, n_q) i32/u32 features.  Returns (out f64 (n_q,), flag bits (2, ceil(n_q/32))
+    i32 or None, err_first i64 (1,): INT64_MAX unless some query hit an unknown row)."""
+    dev = sig.device
+    n_q = sig.numel()
+    n_sig = table.shape[0]
+    if out is None:
+        out = torch.empty(n_q, dtype=torch.float64, device=dev)
+    if flags is None and want_flags:
+        flags = torch.empty((2, (n_q + 31) // 32), dtype=torch.int32, device=dev)
+    if err_first is None:
+        err_first = torch.full((1,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_predict(
+        ctx, kind, table.data_ptr() if table.numel() else 0, n_sig, sig.data_ptr(), x.data_ptr(),
+        n_q, out.data_ptr(), _lib.ptr(flags), err_first.data_ptr(), _lib.stream_ptr(dev)), ctx)
+    return out, flags, err_first
+
+
+class Prediction(float):
+    """A latency (seconds) that also carries the SPEC.md:569 flags."""
+
+    def __new__(cls, value: float, extrapolated: bool = False, clamped: bool = False):
+        obj = float.__new__(cls, value)
+        obj.extrapolated = extrapolated
+        obj.clamped = clamped
+        return obj
+
+
+def predict(regs: Regressors, signature_hash: bytes, features: Sequence[int]) -> Prediction:
+    """Scalar predict: clamped at 1e-7 s, flags extrapolation."""
+    if signature_hash not in regs.index:
+        raise UnknownSignature(signature_hash.hex())
+    kind, row = regs.index[signature_hash]
+    feats = list(features)
+    if len(feats) != _lib.PLANES[kind]:
+        raise ValueError(f"expected {_lib.PLANES[kind]} features {FEATURE_NAMES[kind]}")
+    dev = regs.device
+    sig = torch.tensor([row], dtype=torch.int32, device=dev)
+    x = torch.tensor(np.asarray(feats, dtype=np.uint32).view(np.int32).reshape(-1, 1), device=dev)
+    out, flags, err = predict_batch(kind, regs.tables[kind].table, sig, x)
+    if int(err.item()) != torch.iinfo(torch.int64).max:
+        raise UnknownSignature(f"{signature_hash.hex()} has no fitted regressor")
+    f = flags.cpu().numpy()
+    return Prediction(float(out.item()), bool(f[0, 0] & 1), bool(f[1, 0] & 1))
+
+
+# ---------------------------------------------------------------- call graph
+
+
+@dataclass
+class CallTree:
+    """The op list the simulator walks per iteration."""
+
+    entries: list                 # RunnableEntry, list order = evaluation order
+    oplist: _lib.OpList
+    window: int                   # sliding window of the windowed kv plane (0 = none)
+
+    @property
+    def n_ops(self) -> int:
+        return int(self.oplist.n_ops)
+
+
+def build_calltree(model: ModelConfig, backend: BackendSpec, regs: Regressors,
+                   hw: Optional[HardwareSpec] = None, tp: int = 1,
+                   entries: Optional[list] = None) -> CallTree:
+    """Map a (model, backend, tp) runnable set onto regressor rows (digests are
+    computed by the GPU hash kernel) and append the TP all-reduces: 2 per
+    layer of num_toks * hidden * dtype bytes (App. A.16)."""
+    entries = synthesize_entries(model, backend, tp) if entries is None else list(entries)
+    recs = DeviceRecords.from_packed(pack_entries(entries), regs.device)
+    digs = hash_records(recs).cpu().numpy()
+    ol = _lib.OpList()
+    windows = {e.window for e in entries if e.feature == "attention" and e.window}
+    if len(windows) > 1:
+        raise ValidationError("model.layer_attention", "at most one sliding-window size supported")
+    window = windows.pop() if windows else 0
+    n = 0
+    for i, e in enumerate(entries):
+        d = bytes(digs[i])
+        if d not in regs.index:
+            raise UnknownSignature(f"{e.name} ({d.hex()[:12]}) has no fitted regressor; "
+                                   "profile it first")
+        kind, row = regs.index[d]
+        ol.feat[n] = {"num_toks": _lib.FEAT_NUM_TOKS, "num_seqs": _lib.FEAT_NUM_SEQS,
+                      "attention": _lib.FEAT_ATTN}[e.feature]
+        ol.row[n] = row
+        ol.repeat[n] = e.repeat_count
+        ol.window_slot[n] = 1 if (e.feature == "attention" and e.window) else 0
+        n += 1
+    ol.tp = tp
+    if tp > 1:
+        if hw is None:
+            raise ValueError("tp > 1 needs the hardware spec for comm_latency")
+        ol.comm_alpha, ol.comm_beta = hw.comm_alpha, hw.comm_beta
+        ol.feat[n] = _lib.FEAT_COMM
+        ol.repeat[n] = 2 * model.num_layers
+        ol.bytes_per_tok[n] = model.hidden_dim * model.dtype_bytes
+        n += 1
+    if n > _lib.MAX_OPS:
+        raise ValidationError("calltree", f"{n} entries exceed {_lib.MAX_OPS}")
+    ol.n_ops = n
+    return CallTree(entries, ol, window)
+
+
+@dataclass(frozen=True)
+class IterationBatch:
+    """Features of one scheduled iteration (App. A.6)."""
+
+    num_toks: int
+    prefill_toks: int
+    batch_size: int
+    kv_tokens: int
+    kv_tokens_window: int = 0
+
+    def as_row(self) -> list:
+        return [self.num_toks, self.prefill_toks, self.batch_size, self.kv_tokens,
+                self.kv_tokens_window]
+
+
+def iter_latency_batch(features: torch.Tensor, calltree: CallTree, regs: Regressors,
+                       out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """K4a: latency of n iterations; features (5, n) i32 device tensor."""
+    dev = features.device
+    n_it = features.shape[1]
+    if out is None:
+        out = torch.empty(n_it, dtype=torch.float64, device=dev)
+    err = torch.full((1,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_iter_eval(
+        ctx, C.byref(calltree.oplist), regs.table_ptr(_lib.KIND_AFFINE), regs.n(_lib.KIND_AFFINE),
+        regs.table_ptr(_lib.KIND_ATTN), regs.n(_lib.KIND_ATTN), features.data_ptr(), n_it,
+        out.data_ptr(), err.data_ptr(), _lib.stream_ptr(dev)), ctx)
+    return out
+
+
+def iter_latency(batch: IterationBatch, calltree: CallTree, regs: Regressors) -> float:
+    """Sum over the call graph of repeat x predict (+ comm) for one iteration."""
+    f = torch.tensor(np.asarray(batch.as_row(), dtype=np.uint32).view(np.int32).reshape(5, 1),
+                     device=regs.device)
+    return float(iter_latency_batch(f, calltree, regs).item())
+
+
+# ----------------------------------------------------------------------- run
+
+
+@dataclass(frozen=True)
+class SchedConfig:
+    """Continuous batching + chunked prefill."""
+
+    chunk: int = 8192
+    max_batch: int = 256
+    max_kv_memory: Optional[float] = None   # bytes; default tp*capacity - weights (App. A.13)
+    max_iterations: int = 50_000_000
+
+
+@dataclass
+class Metrics:
+    ttft: np.ndarray                  # per request, input order (s)
+    tpot: np.ndarray                  # NaN where output_tokens < 2
+    n_iterations: np.ndarray          # per shard
+    final_clock: np.ndarray           # per shard
+    percentiles: dict = field(default_factory=dict)
+
+    @staticmethod
+    def summarize(ttft, tpot, n_it, clock) -> "Metrics":
+        m = Metrics(ttft, tpot, n_it, clock)
+        for name, arr in (("ttft", ttft), ("tpot", tpot)):
+            v = arr[~np.isnan(arr)]
+            m.percentiles[name] = {f"p{p}": (float(np.percentile(v, p)) if v.size else math.nan)
+                                   for p in PERCENTILES}
+        return m
+
+
+def kv_capacity(model: ModelConfig, hw: HardwareSpec, tp: int, sched: SchedConfig) -> int:
+    if sched.max_kv_memory is not None:
+        return int(sched.max_kv_memory)
+    cap = int(tp * hw.memory_capacity) - model.weight_bytes()
+    if cap <= 0:
+        raise ValidationError("hardware.memory_capacity",
+                              f"{model.name} weights do not fit tp={tp} x {hw.memory_capacity:.3g} B")
+    return cap
+
+
+def make_sched(model: ModelConfig, hw: HardwareSpec, tp: int, sched: SchedConfig,
+               calltree: CallTree) -> _lib.Sched:
+    if sched.chunk < sched.max_batch:
+        raise ValidationError("sched.chunk", "chunk must be >= max_batch (decodes count, D1)")
+    if sched.max_batch > 1024:
+        raise ValidationError("sched.max_batch", "at most 1024 running requests per replica")
+    s = _lib.Sched()
+    s.chunk, s.max_batch, s.window = sched.chunk, sched.max_batch, calltree.window
+    s.kv_bytes_per_token = model.kv_bytes_per_token()
+    s.kv_capacity_bytes = kv_capacity(model, hw, tp, sched)
+    s.max_iterations = sched.max_iterations
+    return s
+
+
+@dataclass
+class ShardedTrace:
+    """Requests regrouped into S replica shards (request i -> shard i mod S, App. A.14)."""
+
+    arrival: torch.Tensor
+    prompt: torch.Tensor
+    output: torch.Tensor
+    cached: torch.Tensor
+    shard_off: torch.Tensor
+    order: np.ndarray            # position in the sharded layout -> original request index
+    n_shards: int
+
+    @staticmethod
+    def build(requests: Sequence[Request], n_shards: int, device) -> "ShardedTrace":
+        n = len(requests)
+        arr = np.fromiter((r.arrival_s for r in requests), dtype=np.float64, count=n)
+        pr = np.fromiter((r.prompt_tokens for r in requests), dtype=np.uint32, count=n)
+        ou = np.fromiter((r.output_tokens for r in requests), dtype=np.uint32, count=n)
+        ca = np.fromiter((r.cached_tokens for r in requests), dtype=np.uint32, count=n)
+        return ShardedTrace.from_arrays(arr, pr, ou, ca, n_shards, device)
+
+    @staticmethod
+    def from_arrays(arr, pr, ou, ca, n_shards: int, device) -> "ShardedTrace":
+        n = arr.shape[0]
+        if n and np.any(np.diff(arr) < 0):
+            raise ValidationError("workload", "requests must be sorted by arrival")
+        if np.any(ou < 1) or np.any(ca > pr):
+            raise ValidationError("workload", "need output_tokens >= 1 and cached <= prompt")
+        idx = np.arange(n)
+        order = np.concatenate([idx[s::n_shards] for s in range(n_shards)]) if n else idx
+        counts = np.array([len(range(s, n, n_shards)) for s in range(n_shards)], dtype=np.int64)
+        off = np.zeros(n_shards + 1, dtype=np.int64)
+        off[1:] = np.cumsum(counts)
+        dev = torch.device(device)
+
+        def t(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+        return ShardedTrace(t(arr[order]), t(pr[order].view(np.int32)), t(ou[order].view(np.int32)),
+                            t(ca[order].view(np.int32)), t(off), order, n_shards)
+
+
+@dataclass
+class SimOutputs:
+    ttft: torch.Tensor
+    tpot: torch.Tensor
+    n_iter: torch.Tensor
+    clock: torch.Tensor
+    status: torch.Tensor
+    log_feat: Optional[torch.Tensor] = None
+    log_lat: Optional[torch.Tensor] = None
+
+
+def run_sharded(trace: ShardedTrace, calltree: CallTree, sched: _lib.Sched, regs: Regressors,
+                log_cap: int = 0, out: Optional[SimOutputs] = None) -> SimOutputs:
+    """K4b: device-resident event loop over every shard (asynchronous)."""
+    dev = trace.arrival.device
+    n = trace.arrival.numel()
+    S = trace.n_shards
+    if out is None:
+        out = SimOutputs(torch.full((n,), math.nan, dtype=torch.float64, device=dev),
+                         torch.full((n,), math.nan, dtype=torch.float64, device=dev),
+                         torch.zeros(S, dtype=torch.int64, device=dev),
+                         torch.zeros(S, dtype=torch.float64, device=dev),
+                         torch.zeros(S, dtype=torch.int32, device=dev))
+        if log_cap:
+            out.log_feat = torch.zeros((S, log_cap, _lib.IT_FEATS), dtype=torch.int32, device=dev)
+            out.log_lat = torch.zeros((S, log_cap), dtype=torch.float64, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_sim_run(
+        ctx, C.byref(calltree.oplist), C.byref(sched), regs.table_ptr(_lib.KIND_AFFINE),
+        regs.n(_lib.KIND_AFFINE), regs.table_ptr(_lib.KIND_ATTN), regs.n(_lib.KIND_ATTN),
+        _lib.ptr(trace.arrival), _lib.ptr(trace.prompt), _lib.ptr(trace.output),
+        _lib.ptr(trace.cached), trace.shard_off.data_ptr(), S, _lib.ptr(out.ttft),
+        _lib.ptr(out.tpot), out.n_iter.data_ptr(), out.clock.data_ptr(), out.status.data_ptr(),
+        _lib.ptr(out.log_feat), _lib.ptr(out.log_lat), log_cap, 0, 0, _lib.stream_ptr(dev)), ctx)
+    return out
+
+
+def collect(trace: ShardedTrace, res: SimOutputs) -> Metrics:
+    """Sync, raise the reference's errors, and restore input order."""
+    status = res.status.cpu().numpy()
+    if np.any(status == 5):
+        raise NonTermination(f"shard {int(np.argmax(status == 5))} hit the iteration cap")
+    if np.any(status == 3):
+        raise UnknownSignature("call graph references an unfitted regressor row")
+    if np.any(status != 0):
+        raise ValidationError("workload", "a request can never fit the KV-memory capacity")
+    n = trace.order.shape[0]
+    ttft = np.empty(n)
+    tpot = np.empty(n)
+    ttft[trace.order] = res.ttft.cpu().numpy()
+    tpot[trace.order] = res.tpot.cpu().numpy()
+    return Metrics.summarize(ttft, tpot, res.n_iter.cpu().numpy(), res.clock.cpu().numpy())
+
+
+def run_shards(workload: Sequence[Request], n_shards: int, model: ModelConfig,
+               backend: BackendSpec, hw: HardwareSpec, regs: Regressors, sched: SchedConfig,
+               tp: int = 1, calltree: Optional[CallTree] = None) -> Metrics:
+    """S independent replicas (request i -> shard i mod S); identical results for
+    any device count because S is fixed."""
+    ct = calltree or build_calltree(model, backend, regs, hw, tp)
+    cfg = make_sched(model, hw, tp, sched, ct)
+    trace = ShardedTrace.build(workload, n_shards, regs.device)
+    return collect(trace, run_sharded(trace, ct, cfg, regs))
+
+
+def run(workload: Sequence[Request], model: ModelConfig, backend: BackendSpec,
+        hw: HardwareSpec, regs: Regressors, sched: SchedConfig, tp: int = 1) -> Metrics:
+    """End-to-end event loop of one serving replica."""
+    return run_shards(workload, 1, model, backend, hw, regs, sched, tp)
+
+
+def mape(pred: Sequence[float], truth: Sequence[float]) -> float:
+    """mean(|p - t| / t)."""
+    p = np.asarray(pred, dtype=np.float64)
+    t = np.asarray(truth, dtype=np.float64)
+    if p.shape != t.shape:
+        raise LengthMismatch(f"{p.shape} vs {t.shape}")
+    if np.any(t == 0):
+        raise ZeroTruth("truth series contains 0")
+    return float(np.mean(np.abs(p - t) / t)) if t.size else 0.0
+
+
+def predict_host(kind: int, table: torch.Tensor, sig: torch.Tensor, x: torch.Tensor,
+                 out: torch.Tensor, chunk: int = 1 << 24) -> torch.Tensor:
+    """Host-buffer entry point of K3: pinned host sig (n,) i32 and x (P, n) i32 in,
+    pinned host f64 latencies out.  The batch is cut into chunks pipelined over
+    two CUDA streams (H2D copy | kernel | D2H copy overlap); returns ``out``
+    after synchronising."""
+    dev = table.device
+    n = sig.numel()
+    P = x.shape[0]
+    cur = torch.cuda.current_stream(dev)
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    c = min(chunk, max(n, 1))
+    bufs = [(torch.empty(c, dtype=torch.int32, device=dev),
+             torch.empty((P, c), dtype=torch.int32, device=dev),
+             torch.empty(c, dtype=torch.float64, device=dev),
+             torch.empty((2, (c + 31) // 32), dtype=torch.int32, device=dev),
+             torch.full((1,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev))
+            for _ in streams]
+    for s in streams:
+        s.wait_stream(cur)
+    for i, q0 in enumerate(range(0, n, c)):
+        q1 = min(n, q0 + c)
+        m = q1 - q0
+        s = streams[i % 2]
+        d_sig, d_x, d_out, d_flags, d_err = bufs[i % 2]
+        with torch.cuda.stream(s):
+            d_sig[:m].copy_(sig[q0:q1], non_blocking=True)
+            xs = d_x[:, :m] if m == c else torch.empty((P, m), dtype=torch.int32, device=dev)
+            for p in range(P):
+                xs[p].copy_(x[p, q0:q1], non_blocking=True)
+            predict_batch(kind, table, d_sig[:m], xs, d_out[:m],
+                          d_flags if m == c else None, d_err, want_flags=m == c)
+            out[q0:q1].copy_(d_out[:m], non_blocking=True)
+    for s in streams:
+        s.synchronize()
+    if any(int(b[4].item()) != torch.iinfo(torch.int64).max for b in bufs):
+        raise UnknownSignature("a query references an unfitted regressor row")
+    return out

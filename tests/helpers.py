@@ -1,0 +1,81 @@
+"""Seeded synthetic inputs shared by the CPU and GPU tests (and bench.py)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+AFFINE, ATTN = 0, 1
+
+
+def synth_fit_data(kind: int, n_sig: int, n_pts, seed: int = 0, noise: float = 1e-3,
+                   ragged: bool = False):
+    """Per-signature points inside a random training box; y = positive
+    ground-truth polynomial x (1 + noise).  Returns x (P, N) u32, y (N,), off."""
+    rng = np.random.default_rng(seed)
+    counts = (rng.integers(max(1, n_pts // 2), n_pts + 1, size=n_sig) if ragged
+              else np.full(n_sig, n_pts))
+    off = np.zeros(n_sig + 1, dtype=np.int64)
+    off[1:] = np.cumsum(counts)
+    N = int(off[-1])
+    P = 1 if kind == AFFINE else 3
+    sig_of = np.repeat(np.arange(n_sig), counts)
+    if kind == AFFINE:
+        lo = rng.integers(1, 64, size=n_sig)
+        hi = lo + rng.integers(64, 32768, size=n_sig)
+        x = rng.integers(lo[sig_of], hi[sig_of] + 1).astype(np.uint32)[None, :]
+        a = rng.uniform(5e-6, 2e-5, size=n_sig)
+        b = rng.uniform(1e-9, 1e-7, size=n_sig)
+        y = a[sig_of] + b[sig_of] * x[0]
+    else:
+        hi = np.stack([rng.integers(256, 32768, size=n_sig),
+                       rng.integers(8, 256, size=n_sig),
+                       rng.integers(4096, 1 << 22, size=n_sig)], axis=1)
+        x = np.stack([rng.integers(0, hi[sig_of, k] + 1) for k in range(3)]).astype(np.uint32)
+        c = rng.uniform(1e-12, 1e-9, size=(n_sig, 3))
+        y = (1e-5 + c[sig_of, 0] * x[0] + c[sig_of, 1] * x[1] * 100 + c[sig_of, 2] * x[2]
+             + 1e-15 * x[0].astype(np.float64) ** 2 + 1e-16 * x[0].astype(np.float64) * x[2])
+    y = y * (1.0 + noise * rng.standard_normal(N))
+    return np.ascontiguousarray(x, dtype=np.uint32), np.abs(y) + 1e-9, off
+
+
+def rows_to_table(kind: int, rows: np.ndarray) -> dict:
+    """Product table rows (structured numpy) -> oracle table dict."""
+    P = 1 if kind == AFFINE else 3
+    return {"coef": np.asarray(rows["c"], dtype=np.float64).reshape(len(rows), -1),
+            "inv": np.asarray(rows["inv"], dtype=np.float64).reshape(len(rows), P),
+            "lo": np.asarray(rows["lo"], dtype=np.uint32).reshape(len(rows), P),
+            "hi": np.asarray(rows["hi"], dtype=np.uint32).reshape(len(rows), P)}
+
+
+def table_to_rows(kind: int, table: dict) -> np.ndarray:
+    """Oracle table dict -> product row bytes (structured numpy)."""
+    from paper_2605_07985_b200.sim import ROW_DTYPE
+
+    n = table["coef"].shape[0]
+    rows = np.zeros(n, dtype=ROW_DTYPE[kind])
+    if kind == AFFINE:
+        rows["c"] = table["coef"]
+        rows["inv"] = table["inv"][:, 0]
+        rows["lo"] = table["lo"][:, 0]
+        rows["hi"] = table["hi"][:, 0]
+    else:
+        rows["c"] = table["coef"]
+        rows["inv"] = table["inv"]
+        rows["lo"] = table["lo"]
+        rows["hi"] = table["hi"]
+    return rows
+
+
+def synth_queries(kind: int, table: dict, n_q: int, seed: int = 1, outside: float = 0.0):
+    """Uniform signature, features uniform inside that signature's box
+    (a fraction ``outside`` pushed beyond the box to exercise the flag)."""
+    rng = np.random.default_rng(seed)
+    n_sig = table["coef"].shape[0]
+    sig = rng.integers(0, n_sig, size=n_q).astype(np.int64)
+    lo = table["lo"][sig].astype(np.int64)
+    hi = table["hi"][sig].astype(np.int64)
+    x = (lo + (rng.random(lo.shape) * (hi - lo + 1)).astype(np.int64)).clip(lo, hi)
+    if outside:
+        m = rng.random(n_q) < outside
+        x[m] = hi[m] + 1 + rng.integers(0, 1000, size=(m.sum(), x.shape[1]))
+    return sig.astype(np.uint32), np.ascontiguousarray(x.T.astype(np.uint32))

@@ -1,0 +1,448 @@
+"""GPU parity of every libdooly_b200 kernel against the CPU oracle (C-ABI path).
+
+Bars (BASELINE.json north_star): dedup bit-exact; predictions bit-exact given
+the same regressor row (the evaluation order is the pinned contract) and
+within 1e-9 relative of the oracle's own fit; coefficients within 1e-9
+normwise in the scaled basis; TTFT/TPOT within 1e-6 relative (we assert
+bit-equality, which is stronger).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import ATTN, AFFINE, rows_to_table, synth_fit_data, synth_queries, table_to_rows
+from oracle import profiler as oprof
+from oracle import sim as osim
+
+pytestmark = pytest.mark.gpu
+
+COEF_TOL = 1e-9      # normwise, scaled basis
+PRED_TOL = 1e-9      # relative
+ERR_TOL = 1e-9
+
+
+def _i32(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32))
+
+
+# ------------------------------------------------------------------ fit (K2)
+
+
+def _fit_gpu(kind, x, y, off, dev):
+    from paper_2605_07985_b200.sim import fit_tables
+
+    fr = fit_tables(kind, _i32(x).to(dev), torch.from_numpy(y).to(dev),
+                    torch.from_numpy(off).to(dev))
+    torch.cuda.synchronize()
+    return fr
+
+
+@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+@pytest.mark.parametrize("ragged", [False, True])
+def test_fit_matches_oracle(kind, ragged, dev):
+    x, y, off = synth_fit_data(kind, 300, 512, seed=3 + kind, ragged=ragged)
+    fr = _fit_gpu(kind, x, y, off, dev)
+    ref = osim.fit(kind, x, y, off)
+    rows = fr.rows()
+    got = rows_to_table(kind, rows)
+    assert np.array_equal(fr.status.cpu().numpy(), ref["status"])
+    assert np.array_equal(got["lo"], ref["lo"]) and np.array_equal(got["hi"], ref["hi"])
+    assert np.array_equal(got["inv"], ref["inv"])          # IEEE 1/max on both sides
+    dc = np.abs(got["coef"] - ref["coef"]).max(axis=1) / np.abs(ref["coef"]).max(axis=1)
+    assert dc.max() <= COEF_TOL, dc.max()
+    fe = fr.fit_err.cpu().numpy()
+    assert np.allclose(fe, ref["fit_err"], rtol=ERR_TOL, atol=0)
+    # predictions of the two fits on the training points agree to 1e-9 relative
+    pg = osim.eval_poly(kind, got["coef"][np.repeat(np.arange(300), np.diff(off))],
+                        got["inv"][np.repeat(np.arange(300), np.diff(off))], x.T)
+    pr = osim.eval_poly(kind, ref["coef"][np.repeat(np.arange(300), np.diff(off))],
+                        ref["inv"][np.repeat(np.arange(300), np.diff(off))], x.T)
+    assert np.max(np.abs(pg - pr) / np.abs(pr)) <= PRED_TOL
+
+
+def test_fit_exact_linear_and_insufficient(dev):
+    # SPEC.md:562 exact linear data -> fit_error < 1e-6; SPEC.md:564 2 points -> insufficient
+    xs = np.array([[1, 16, 128, 512, 2048, 8192, 5, 7]], dtype=np.uint32)
+    y = 5e-6 + 1.25e-9 * xs[0].astype(np.float64)
+    off = np.array([0, 6, 8], dtype=np.int64)
+    fr = _fit_gpu(AFFINE, xs, y, off, dev)
+    st = fr.status.cpu().numpy()
+    assert st.tolist() == [0, 1]
+    assert fr.fit_err.cpu().numpy()[0] < 1e-6
+    rows = fr.rows()
+    assert rows["lo"][1] > rows["hi"][1]      # unfitted row marker
+
+
+def test_fit_rank_deficient_drops_columns(dev):
+    # chunk-constant style collinearity: batch fixed at 8 -> f2 == 1 == intercept
+    rng = np.random.default_rng(5)
+    n = 64
+    x = np.stack([rng.integers(0, 4096, n), np.full(n, 8), rng.integers(0, 1 << 16, n)]).astype(np.uint32)
+    y = 1e-5 + 1e-9 * x[0] + 3e-11 * x[2]
+    off = np.array([0, n], dtype=np.int64)
+    fr = _fit_gpu(ATTN, x, y, off, dev)
+    ref = osim.fit(ATTN, x, y, off)
+    got = rows_to_table(ATTN, fr.rows())
+    assert fr.status.cpu().numpy()[0] == 0
+    # same dropped set (exact zeros) and the same predictions
+    assert np.array_equal(got["coef"][0] == 0, ref["coef"][0] == 0)
+    pg = osim.eval_poly(ATTN, got["coef"][0], got["inv"][0], x.T)
+    pr = osim.eval_poly(ATTN, ref["coef"][0], ref["inv"][0], x.T)
+    assert np.max(np.abs(pg - pr) / pr) <= PRED_TOL
+
+
+# -------------------------------------------------------------- predict (K3)
+
+
+def _predict_gpu(kind, rows, sig, x, dev, offset=0):
+    from paper_2605_07985_b200.sim import predict_batch
+
+    table = torch.from_numpy(rows.view(np.uint8).reshape(len(rows), -1).copy()).to(dev)
+    n = sig.shape[0]
+    # `offset` elements of misalignment (offset % 4 != 0 exercises the scalar path)
+    sbuf = torch.zeros(n + offset, dtype=torch.int32, device=dev)
+    sbuf[offset:] = _i32(sig).to(dev)
+    xflat = torch.zeros(x.shape[0] * n + offset, dtype=torch.int32, device=dev)
+    xflat[offset:] = _i32(x).to(dev).reshape(-1)
+    out, flags, err = predict_batch(kind, table, sbuf[offset:], xflat[offset:])
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), flags.cpu().numpy().view(np.uint32), int(err.item())
+
+
+def _unpack_bits(words: np.ndarray, n: int) -> np.ndarray:
+    b = np.unpackbits(words.view(np.uint8), bitorder="little")
+    return b[:n].astype(bool)
+
+
+@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+@pytest.mark.parametrize("n_q,offset", [(1, 0), (127, 0), (4096 * 3 + 5, 0), (1000, 1), (99999, 3)])
+def test_predict_bit_exact(kind, n_q, offset, dev):
+    x, y, off = synth_fit_data(kind, 257, 64, seed=11 + kind)
+    ref_fit = osim.fit(kind, x, y, off)
+    table = {k: ref_fit[k] for k in ("coef", "inv", "lo", "hi")}
+    # force some clamping: shift one signature's intercept far negative
+    table["coef"][7, 0] = -1.0
+    rows = table_to_rows(kind, table)
+    sig, xq = synth_queries(kind, table, n_q, seed=n_q, outside=0.05)
+    out, flags, err = _predict_gpu(kind, rows, sig, xq, dev, offset)
+    ref = osim.predict(kind, table, sig, xq)
+    assert err == np.iinfo(np.int64).max
+    assert np.array_equal(out.view(np.uint64), ref["out"].view(np.uint64))   # bit-exact
+    nw = (n_q + 31) // 32
+    assert np.array_equal(_unpack_bits(flags[0, :nw], n_q), ref["extrap"])
+    assert np.array_equal(_unpack_bits(flags[1, :nw], n_q), ref["clamped"])
+
+
+@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+def test_predict_unknown_signature(kind, dev):
+    x, y, off = synth_fit_data(kind, 8, 32, seed=2)
+    x[:, : off[3]] = x[:, : off[3]]
+    ref_fit = osim.fit(kind, x, y, np.array([0, 2, *off[2:]], dtype=np.int64))  # sig 0: 2 pts
+    table = {k: ref_fit[k] for k in ("coef", "inv", "lo", "hi")}
+    rows = table_to_rows(kind, table)
+    sig = np.array([3, 0, 5, 100, 2], dtype=np.uint32)
+    xq = np.tile(table["lo"][3][:, None], (1, 5)).astype(np.uint32)
+    out, _, err = _predict_gpu(kind, rows, sig, xq, dev)
+    assert err == 1                               # first bad query: unfitted sig 0
+    assert np.isnan(out[1]) and np.isnan(out[3]) and np.isfinite(out[0])
+
+
+def test_predict_scalar_api_raises(dev):
+    from paper_2605_07985_b200.errors import UnknownSignature
+    from paper_2605_07985_b200.sim import FitResult, Regressors, predict
+
+    x, y, off = synth_fit_data(AFFINE, 4, 16, seed=9)
+    fr = _fit_gpu(AFFINE, x, y, off, dev)
+    regs = Regressors({AFFINE: fr}, {b"a" * 32: (AFFINE, 1)}, dev)
+    p = predict(regs, b"a" * 32, [int(x[0, off[1]])])
+    ref = osim.predict(AFFINE, rows_to_table(AFFINE, fr.rows()), np.array([1]), x[:, off[1]:off[1] + 1])
+    assert float(p) == ref["out"][0] and not p.extrapolated
+    with pytest.raises(UnknownSignature):
+        predict(regs, b"b" * 32, [1])
+
+
+# ------------------------------------------------------------- SHA-256 / dedup
+
+
+def test_sha256_messages_kat_and_random(dev):
+    from paper_2605_07985_b200.profiler import signature_hash, signature_hash_batch
+
+    assert signature_hash(b"").hex() == \
+        "e3b0c44298fc1c149afbf4c8996fb92427ae41e4649b934ca495991b7852b855"
+    rng = np.random.default_rng(0)
+    msgs = [rng.bytes(int(n)) for n in rng.integers(0, 700, size=3000)]
+    msgs += [b"a" * n for n in range(0, 130)]          # every padding boundary
+    got = signature_hash_batch(msgs)
+    assert got == [hashlib.sha256(m).digest() for m in msgs]
+
+
+def test_record_hash_matches_oracle_canonical(corpus, dev):
+    from paper_2605_07985_b200.profiler import DeviceRecords, hash_records
+    from paper_2605_07985_b200.records import corpus_entries, pack_entries
+
+    for tp in (1, 4):
+        ents = [e for _, _, es in corpus_entries(corpus, tp=tp) for e in es]
+        recs = DeviceRecords.from_packed(pack_entries(ents), dev)
+        got = hash_records(recs).cpu().numpy()
+        want = [oprof.signature_hash(oprof.canonicalize(e.to_json())) for e in ents]
+        assert [bytes(r) for r in got] == want
+
+
+def _dedup_gpu(digs: np.ndarray, db: np.ndarray, dev):
+    from paper_2605_07985_b200.profiler import dedup_digests
+
+    r = dedup_digests(torch.from_numpy(digs).to(dev),
+                      torch.from_numpy(db).to(dev) if db is not None else None)
+    return {"first": r.first.cpu().numpy().tolist(), "uid": r.uid.cpu().numpy().tolist(),
+            "is_new": r.is_new.cpu().numpy().astype(bool).tolist(),
+            "in_db": r.in_db.cpu().numpy().astype(bool).tolist(), "n_unique": r.n_unique}
+
+
+@pytest.mark.parametrize("n,n_distinct,n_db", [(1, 1, 0), (1000, 100, 0), (50000, 20000, 5000),
+                                               (200000, 150000, 0)])
+def test_dedup_bit_exact(n, n_distinct, n_db, dev):
+    rng = np.random.default_rng(n)
+    pool = rng.integers(0, 256, size=(n_distinct, 32), dtype=np.uint8)
+    # collisions on the probe word (first 4 bytes) but different digests
+    pool[1::7, :4] = pool[0, :4]
+    digs = pool[rng.integers(0, n_distinct, size=n)]
+    db = pool[rng.choice(n_distinct, size=n_db, replace=False)] if n_db else np.zeros((0, 32), np.uint8)
+    got = _dedup_gpu(digs, db, dev)
+    ref = oprof.dedup_digests([bytes(d) for d in digs], [bytes(d) for d in db])
+    assert got == ref
+
+
+def test_dedup_empty(dev):
+    got = _dedup_gpu(np.zeros((0, 32), np.uint8), None, dev)
+    assert got["n_unique"] == 0 and got["first"] == []
+
+
+def test_corpus_census_and_rerun(corpus, dev):
+    """Table 2: attention 42 occurrences, 27
+    reuses, groups 24/21, 6/3, 6/3, 3/0, 3/0; re-run profiles nothing."""
+    from paper_2605_07985_b200 import modelir
+    from paper_2605_07985_b200.profiler import LatencyDB, dedup
+    from paper_2605_07985_b200.records import corpus_entries
+
+    db = LatencyDB()
+    groups: dict = {}
+    for m, b, ents in corpus_entries(corpus):
+        att = [e for e in ents if e.name == "attention"]
+        to_profile, skipped = dedup(att, db, device=dev)
+        for e in att:
+            key = modelir.geometry_key(m, m.layer_attention.index(e.window))
+            g = groups.setdefault(key, [0, 0])
+            g[0] += 1
+        for e in skipped:
+            key = modelir.geometry_key(m, m.layer_attention.index(e.window))
+            groups[key][1] += 1
+    assert groups == {"q32/kv8/d128/full": [24, 21], "q28/kv4/d128/full": [6, 3],
+                      "q32/kv32/d128/full": [6, 3], "q32/kv8/d128/swa4096": [3, 0],
+                      "q32/kv8/d128/swa32768": [3, 0]}
+    assert len(db.signatures) == 42 - 27
+    again = [e for _, _, es in corpus_entries(corpus) for e in es if e.name == "attention"]
+    to_profile, skipped = dedup(again, db, device=dev)
+    assert to_profile == [] and len(skipped) == 42
+
+
+def test_dedup_packed_large_uniform(dev):
+    """C5-style bulk records (vectorised packer) vs oracle digests + dedup."""
+    from paper_2605_07985_b200.profiler import DeviceRecords, dedup_packed
+    from paper_2605_07985_b200.records import pack_uniform
+    from bench import synth_records
+
+    packed, n_dims = synth_records(200_000, seed=4)
+    recs = DeviceRecords.from_packed(packed, dev)
+    res = dedup_packed(recs)
+    digs = res.digests.cpu().numpy()
+    # spot-check digests against the oracle's canonical hash on a sample
+    rng = np.random.default_rng(0)
+    w = packed.words
+    for i in rng.choice(packed.n, size=300, replace=False):
+        o = int(packed.rec_off[i])
+        ent = _entry_from_words(packed, o)
+        assert bytes(digs[i]) == oprof.signature_hash(oprof.canonicalize(ent))
+    ref = oprof.dedup_digests([bytes(d) for d in digs])
+    assert res.n_unique == ref["n_unique"]
+    assert res.first.cpu().numpy().tolist() == ref["first"]
+    assert res.uid.cpu().numpy().tolist() == ref["uid"]
+
+
+def _entry_from_words(p, o):
+    w = p.words
+    op, nd, ns, attr = int(w[o]), int(w[o + 1]) & 0xFFFF, int(w[o + 1]) >> 16, int(w[o + 2])
+    flat = []
+    scal = []
+    pos_val = [(int(w[o + 4 + 3 * k]), int(w[o + 5 + 3 * k]) | (int(w[o + 6 + 3 * k]) << 32))
+               for k in range(nd)]
+    # rebuild an arg template whose MC positions are exactly pos_val (others NT)
+    maxpos = max([pv[0] for pv in pos_val if pv[0] < 65536], default=-1)
+    pm = dict(pos_val)
+    flat = [[pm.get(i, 7), "MC" if i in pm else "NT"] for i in range(maxpos + 1)]
+    for k in range(max([pv[0] - 65536 for pv in pos_val if pv[0] >= 65536], default=-1) + 1):
+        scal.append([pm.get(65536 + k, 3), "MC" if 65536 + k in pm else "NR"])
+    syms = []
+    for k in range(ns):
+        sid = int(w[o + 4 + 3 * nd + k])
+        syms.append(bytes(p.sym_bytes[p.sym_off[sid]:p.sym_off[sid + 1]]).decode())
+    name = bytes(p.op_bytes[p.op_off[op]:p.op_off[op + 1]]).decode()
+    ent = {"name": name, "granularity": "operator", "arg_template": [flat], "scalars": scal,
+           "kernel_symbols": syms, "attrs": {}}
+    assert attr == 0xFFFFFFFF
+    return ent
+
+
+# --------------------------------------------------------------- sim (K4)
+
+
+def _random_oplist(rng, n_aff, n_attn, window, tp):
+    from paper_2605_07985_b200 import _lib
+
+    ops = []
+    for e in range(12):
+        r = rng.random()
+        if r < 0.25:
+            ops.append({"feat": osim.FEAT_ATTN, "row": int(rng.integers(n_attn)),
+                        "window_slot": int(window > 0 and rng.random() < 0.5),
+                        "repeat": int(rng.integers(1, 40))})
+        elif r < 0.35:
+            ops.append({"feat": osim.FEAT_NUM_SEQS, "row": int(rng.integers(n_aff)),
+                        "window_slot": 0, "repeat": 1})
+        else:
+            ops.append({"feat": osim.FEAT_NUM_TOKS, "row": int(rng.integers(n_aff)),
+                        "window_slot": 0, "repeat": int(rng.integers(1, 80))})
+    if tp > 1:
+        ops.append({"feat": osim.FEAT_COMM, "row": 0, "window_slot": 0, "repeat": 160,
+                    "bytes_per_tok": 8192 * 2})
+    ol = _lib.OpList()
+    ol.n_ops = len(ops)
+    ol.tp = tp
+    ol.comm_alpha, ol.comm_beta = 5e-6, 5e-12
+    for i, o in enumerate(ops):
+        ol.feat[i], ol.row[i], ol.repeat[i] = o["feat"], o["row"], o["repeat"]
+        ol.window_slot[i] = o["window_slot"]
+        ol.bytes_per_tok[i] = o.get("bytes_per_tok", 0)
+    return ops, ol
+
+
+def _sim_setup(seed, window=0, tp=1):
+    from paper_2605_07985_b200.sim import CallTree, Regressors, FitResult
+
+    rng = np.random.default_rng(seed)
+    xa, ya, oa = synth_fit_data(AFFINE, 20, 24, seed=seed)
+    xt, yt, ot = synth_fit_data(ATTN, 6, 64, seed=seed + 1)
+    fa, ft = osim.fit(AFFINE, xa, ya, oa), osim.fit(ATTN, xt, yt, ot)
+    ta = {k: fa[k] for k in ("coef", "inv", "lo", "hi")}
+    tt = {k: ft[k] for k in ("coef", "inv", "lo", "hi")}
+    ops, ol = _random_oplist(rng, 20, 6, window, tp)
+    for o in ops:
+        if o["feat"] == osim.FEAT_ATTN:
+            o["coef"], o["inv"] = list(tt["coef"][o["row"]]), list(tt["inv"][o["row"]])
+        elif o["feat"] != osim.FEAT_COMM:
+            o["coef"], o["inv"] = list(ta["coef"][o["row"]]), list(ta["inv"][o["row"]])
+    return ta, tt, ops, ol
+
+
+def _regs(ta, tt, dev):
+    from paper_2605_07985_b200.sim import FitResult, Regressors
+
+    def fr(kind, t):
+        rows = table_to_rows(kind, t)
+        tab = torch.from_numpy(rows.view(np.uint8).reshape(len(rows), -1).copy()).to(dev)
+        n = len(rows)
+        return FitResult(kind, tab, torch.zeros(n, dtype=torch.float64, device=dev),
+                         torch.zeros(n, dtype=torch.uint8, device=dev))
+
+    return Regressors({AFFINE: fr(AFFINE, ta), ATTN: fr(ATTN, tt)}, {}, dev)
+
+
+@pytest.mark.parametrize("tp", [1, 4])
+def test_iter_eval_bit_exact(tp, dev):
+    from paper_2605_07985_b200.sim import CallTree, iter_latency_batch
+
+    ta, tt, ops, ol = _sim_setup(21 + tp, window=4096, tp=tp)
+    regs = _regs(ta, tt, dev)
+    rng = np.random.default_rng(tp)
+    n = 20000
+    feats = np.stack([rng.integers(1, 8192, n), rng.integers(0, 8192, n), rng.integers(1, 256, n),
+                      rng.integers(0, 1 << 21, n), rng.integers(0, 1 << 20, n)]).astype(np.uint32)
+    ct = CallTree([], ol, 4096)
+    got = iter_latency_batch(_i32(feats).to(dev), ct, regs).cpu().numpy()
+    want = np.array([osim.iter_latency(tuple(int(v) for v in feats[:, i]), ops, tp, 5e-6, 5e-12)
+                     for i in range(n)])
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+def _workload(n, seed, rate=4.0, cached_frac=0.0):
+    rng = np.random.default_rng(seed)
+    arr = np.cumsum(rng.exponential(1.0 / rate, size=n))
+    pr = rng.integers(1, 9000, size=n).astype(np.uint32)
+    ou = rng.integers(1, 300, size=n).astype(np.uint32)
+    ca = np.where(rng.random(n) < cached_frac, pr, 0).astype(np.uint32)
+    return arr, pr, ou, ca
+
+
+@pytest.mark.parametrize("seed,n,shards,window,tp,cap", [
+    (1, 400, 1, 0, 1, 10**15), (2, 3000, 8, 4096, 1, 10**15), (3, 2000, 4, 0, 4, 3 * 10**10),
+    (4, 1500, 3, 1024, 1, 4 * 10**9)])
+def test_sim_run_bit_exact(seed, n, shards, window, tp, cap, dev):
+    from paper_2605_07985_b200 import _lib
+    from paper_2605_07985_b200.sim import CallTree, ShardedTrace, collect, run_sharded
+
+    ta, tt, ops, ol = _sim_setup(seed, window=window, tp=tp)
+    regs = _regs(ta, tt, dev)
+    arr, pr, ou, ca = _workload(n, seed, cached_frac=0.1 if seed % 2 else 0.0)
+    sc = _lib.Sched()
+    sc.chunk, sc.max_batch, sc.window = 2048, 64, window
+    sc.kv_bytes_per_token, sc.kv_capacity_bytes, sc.max_iterations = 131072, cap, 10**7
+    trace = ShardedTrace.from_arrays(arr, pr, ou, ca, shards, dev)
+    res = run_sharded(trace, CallTree([], ol, window), sc, regs, log_cap=4000)
+    met = collect(trace, res)
+    ref = osim.run_shards(arr.tolist(), pr.tolist(), ou.tolist(), ca.tolist(), shards, ops=ops,
+                          chunk=2048, max_batch=64, kv_bytes_per_token=131072, kv_capacity=cap,
+                          window=window, tp=tp, alpha=5e-6, beta=5e-12)
+    assert res.n_iter.cpu().numpy().tolist() == ref["n_iter"]
+    assert np.array_equal(res.clock.cpu().numpy(), np.array(ref["clock"]))
+    assert np.array_equal(met.ttft.view(np.uint64), ref["ttft"].view(np.uint64))
+    assert np.array_equal(np.isnan(met.tpot), np.isnan(ref["tpot"]))
+    m = ~np.isnan(ref["tpot"])
+    assert np.array_equal(met.tpot[m], ref["tpot"][m])
+    # per-iteration features + latency of shard 0 (schedule compositions identical)
+    r0 = osim.run_shard(arr[0::shards].tolist(), pr[0::shards].tolist(), ou[0::shards].tolist(),
+                        ca[0::shards].tolist(), ops, 2048, 64, 131072, cap, window, tp, 5e-6,
+                        5e-12, log=True)
+    k = min(len(r0["lat"]), 4000)
+    lf = res.log_feat.cpu().numpy().view(np.uint32)[0, :k]
+    assert [tuple(int(v) for v in row) for row in lf] == [tuple(f) for f in r0["feats"][:k]]
+    assert np.array_equal(res.log_lat.cpu().numpy()[0, :k], np.array(r0["lat"][:k]))
+
+
+def test_sim_non_termination(dev):
+    from paper_2605_07985_b200 import _lib
+    from paper_2605_07985_b200.errors import NonTermination
+    from paper_2605_07985_b200.sim import CallTree, ShardedTrace, collect, run_sharded
+
+    ta, tt, ops, ol = _sim_setup(7)
+    regs = _regs(ta, tt, dev)
+    arr, pr, ou, ca = _workload(50, 7)
+    sc = _lib.Sched()
+    sc.chunk, sc.max_batch, sc.window = 2048, 64, 0
+    sc.kv_bytes_per_token, sc.kv_capacity_bytes, sc.max_iterations = 1, 10**12, 10
+    trace = ShardedTrace.from_arrays(arr, pr, ou, ca, 1, dev)
+    with pytest.raises(NonTermination):
+        collect(trace, run_sharded(trace, CallTree([], ol, 0), sc, regs))
+
+
+def test_library_launch_counter(dev):
+    from paper_2605_07985_b200 import _lib
+
+    before = _lib.launch_count(dev)
+    x, y, off = synth_fit_data(AFFINE, 4, 16, seed=1)
+    _fit_gpu(AFFINE, x, y, off, dev)
+    assert _lib.launch_count(dev) == before + 1
