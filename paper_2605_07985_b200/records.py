@@ -266,16 +266,15 @@ def synthesize_entries(cfg: ModelConfig, backend: BackendSpec, tp: int = 1) -> l
     linear, top-k softmax, expert module).  Embedding first, final norm and
     lm_head last.  Model-config dims are sharded by ``tp``.
     """
-    T = ("NT",)
     tok = (_DUMMY_REQS * _DUMMY_TOKS, "NT")
-    seq = (_DUMMY_REQS, "NR")
     h, d = cfg.hidden_dim, cfg.head_dim
     hq, hkv = cfg.num_q_heads // tp, cfg.num_kv_heads // tp
     inter = cfg.intermediate_size // tp
     vocab = cfg.vocab_size // tp
     gemm = (_gemm_symbol(cfg.dtype_bytes),)
-    mc = lambda v: (v, "MC")  # noqa: E731
-    del T
+
+    def mc(v):
+        return (v, "MC")
 
     def op(name, args, syms, rep, feature="num_toks", scalars=()):
         return RunnableEntry("operator", name, tuple(tuple(a) for a in args), tuple(scalars),
@@ -320,7 +319,8 @@ def synthesize_entries(cfg: ModelConfig, backend: BackendSpec, tp: int = 1) -> l
                 (("num_experts", m.num_experts), ("top_k", m.top_k)),
                 ("moe_align_block_size", "fused_moe_kernel", "moe_sum"), rep, "num_toks"))
     out.append(norm(1))
-    out.append(linear(h, vocab, 1, x=seq, feature="num_seqs"))
+    # Appendix F: every non-attention op regresses on the token count
+    out.append(linear(h, vocab, 1))
     return out
 
 

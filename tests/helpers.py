@@ -53,16 +53,8 @@ def table_to_rows(kind: int, table: dict) -> np.ndarray:
 
     n = table["coef"].shape[0]
     rows = np.zeros(n, dtype=ROW_DTYPE[kind])
-    if kind == AFFINE:
-        rows["c"] = table["coef"]
-        rows["inv"] = table["inv"][:, 0]
-        rows["lo"] = table["lo"][:, 0]
-        rows["hi"] = table["hi"][:, 0]
-    else:
-        rows["c"] = table["coef"]
-        rows["inv"] = table["inv"]
-        rows["lo"] = table["lo"]
-        rows["hi"] = table["hi"]
+    for field, key in (("c", "coef"), ("inv", "inv"), ("lo", "lo"), ("hi", "hi")):
+        rows[field] = np.asarray(table[key]).reshape(rows[field].shape)
     return rows
 
 
