@@ -430,7 +430,8 @@ def run_ours(args):
     if rank == 0 and world == 1 and args.cpu_sample > 0:
         tables_host = {}
         qh = {}
-        from tests.helpers import rows_to_table
+        sys.path.insert(0, str(ROOT / "tests"))
+        from helpers import rows_to_table
 
         for k in (AFFINE, ATTN):
             rows = tables[k].cpu().numpy().view(ROW_DTYPE[k]).reshape(-1)
@@ -574,7 +575,8 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import sim as osim
-    from tests.helpers import synth_fit_data, synth_queries
+    sys.path.insert(0, str(ROOT / "tests"))
+    from helpers import synth_fit_data, synth_queries
 
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     tables, qh = {}, {}

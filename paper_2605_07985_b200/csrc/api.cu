@@ -108,6 +108,8 @@ int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
   if (n_q < 0 || n_sig < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: negative size");
   if (n_q > 0 && (!table && n_sig > 0 || !sig || !x || !out))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: null pointer");
+  if ((uintptr_t)table % 32 != 0)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: table must be 32-byte aligned");
   DeviceGuard g(ctx->device);
   if (n_q > 0) ctx->launches += 1;
   return check_cuda(ctx,
@@ -195,7 +197,10 @@ int dooly_dedup_digests(dooly_ctx* ctx, const uint8_t* digests, int64_t n,
                     "dedup");
 }
 
-static int check_oplist(dooly_ctx* ctx, const dooly_oplist* ops, int64_t n_aff, int64_t n_attn) {
+static int check_oplist(dooly_ctx* ctx, const dooly_oplist* ops, int64_t n_aff, int64_t n_attn,
+                        const void* aff_t = nullptr, const void* attn_t = nullptr) {
+  if ((uintptr_t)aff_t % 32 != 0 || (uintptr_t)attn_t % 32 != 0)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "regressor tables must be 32-byte aligned");
   if (!ops || ops->n_ops < 0 || ops->n_ops > DOOLY_MAX_OPS)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "oplist: bad n_ops");
   for (int e = 0; e < ops->n_ops; ++e) {
@@ -220,7 +225,7 @@ int dooly_iter_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_
                     const uint32_t* it_feat, int64_t n_it, double* it_lat, int64_t* err_first,
                     void* stream) {
   if (!ctx) return DOOLY_ERR_INVALID_ARG;
-  int rc = check_oplist(ctx, ops, n_affine, n_attn);
+  int rc = check_oplist(ctx, ops, n_affine, n_attn, affine_table, attn_table);
   if (rc) return rc;
   if (n_it < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "iter_eval: negative size");
   if (n_it > 0 && (!it_feat || !it_lat))
@@ -247,7 +252,7 @@ int dooly_sim_run(dooly_ctx* ctx, const dooly_oplist* ops, const dooly_sched* cf
                   double* it_log_lat, int64_t it_log_cap, void* workspace,
                   size_t workspace_bytes, void* stream) {
   if (!ctx) return DOOLY_ERR_INVALID_ARG;
-  int rc = check_oplist(ctx, ops, n_affine, n_attn);
+  int rc = check_oplist(ctx, ops, n_affine, n_attn, affine_table, attn_table);
   if (rc) return rc;
   if (!cfg || cfg->chunk < 1 || cfg->max_batch < 1 || cfg->max_batch > 1024 ||
       cfg->chunk < cfg->max_batch ||
