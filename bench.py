@@ -165,55 +165,69 @@ def ncu_traffic(kernel_key: str):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled every ~5 ms through NVML in a
+    background thread, restricted to the timed region (mark_start/mark_end)."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, gpu_index: int):
-        self.proc = None
-        self.path = Path(os.environ.get("TMPDIR", "/tmp")) / f"dooly_clocks_{os.getpid()}.csv"
         self.gpu = gpu_index
+        self.samples = []
+        self.window = [None, None]
+        self.max_mhz = None
+        self._stop = False
+        self._thread = None
 
     def __enter__(self):
+        import threading
+
         try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
-                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=self.fh, stderr=subprocess.DEVNULL)
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def loop():
+                while not self._stop:
+                    try:
+                        self.samples.append((time.perf_counter(),
+                                             float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)),
+                                             int(get_reasons(h))))
+                    except pynvml.NVMLError:
+                        pass
+                    time.sleep(0.005)
+
+            self._thread = threading.Thread(target=loop, daemon=True)
+            self._thread.start()
+        except Exception:  # NVML unavailable: report it, never fake clocks
+            self._thread = None
         return self
 
+    def mark_start(self):
+        self.window[0] = time.perf_counter()
+
+    def mark_end(self):
+        self.window[1] = time.perf_counter()
+
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-            self.fh.close()
+        self._stop = True
+        if self._thread is not None:
+            self._thread.join(timeout=2)
 
     def summary(self):
-        if self.proc is None or not self.path.exists():
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.path.read_text().splitlines():
-            f = [t.strip() for t in line.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                smax = float(f[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        self.path.unlink(missing_ok=True)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self._thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        t0, t1 = self.window
+        inside = [s for s in self.samples if t0 is not None and t0 <= s[0] <= (t1 or t0)]
+        src = inside if inside else self.samples[-3:]
+        reasons = sorted({name for _, _, r in src for bit, name in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(np.median([s[1] for s in src])) if src else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
+                "source": "nvml, 5 ms sampling inside the timed region"}
 
 
 def barrier_sync(dist_on: bool):
@@ -381,6 +395,8 @@ def run_ours(args):
                for _ in range(args.steps)] for k in (AFFINE, ATTN)}
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        time.sleep(0.05)
+        clk.mark_start()
         start.record(stream)
         for s in range(args.steps):
             for k in (AFFINE, ATTN):
@@ -389,6 +405,7 @@ def run_ours(args):
                 pev[k][s][1].record(stream)
         end.record(stream)
         barrier_sync(dist_on)
+        clk.mark_end()
     launches = _lib.launch_count(dev) - launches0
     ms_step = max_over_ranks(start.elapsed_time(end) / args.steps, dist_on)
     k_ms = {k: sum(a.elapsed_time(b) for a, b in pev[k]) / args.steps for k in (AFFINE, ATTN)}

@@ -1,27 +1,33 @@
 // K2 — batched per-signature least-squares fit (replaces fit).
 //
-// Data path (B200): a persistent kernel, one 256-thread CTA per SM.  Thread 0
-// streams whole signatures (feature planes + latencies) from HBM into a ring
-// of shared-memory stages with the bulk-copy (1-D TMA) engine
-// (`cp.async.bulk` + mbarrier complete_tx), STAGES-1 signatures ahead of the
-// one being computed, so HBM streaming overlaps the FP64 work and the serial
-// reduce/solve phases.  Both passes over a signature then read shared memory:
-// every point is fetched from HBM exactly once.  Signatures larger than a
-// stage fall back to a direct global-memory path (same arithmetic).
+// Data path (B200): a persistent kernel with two 128-thread CTAs per SM.  In
+// each CTA thread 0 streams whole signatures (feature planes + latencies) from
+// HBM into a ring of shared-memory stages with the bulk-copy (1-D TMA) engine
+// (`cp.async.bulk` + mbarrier complete_tx), so both passes over a signature
+// read shared memory and every point is fetched from HBM exactly once.  The
+// two co-resident CTAs interleave: while one is in its short serial phase
+// (reduce + solve) or waiting for its next stage, the other keeps the FP64
+// pipes busy.  Signatures larger than a stage (or unaligned inputs) fall back
+// to a direct global-memory path with the same arithmetic.
 //
 // Per signature:
-//   pass 1  raw power moments sum x^a y^b z^c (a+b+c <= 4: 35 for attention,
-//           3 for affine), X^T y for the design monomials, and the training
-//           box.  All terms are non-negative so the raw sums are well
-//           conditioned; the scaled Gram G[i][j] = M[e_i+e_j] * prod inv^e is
-//           formed once per signature (35 moments replace 55 Gram products
-//           per point).
-//   reduce  warp shuffles -> shared memory -> 8-way column sums.
-//   solve   warp 0 factors G with a right-looking Cholesky, one lane per row;
-//           columns whose pivot falls to <= DROP_TOL x their diagonal are
-//           dropped (rank-deficient designs), then forward/back
-//           substitution by shuffles.
-//   pass 2  training MAPE (fit_error) of the clamped predictor.
+//   pass 1  raw power moments sum x^a y^b z^c (a+b+c <= 4: 34 non-trivial for
+//           attention, 2 for affine) and X^T y for the design monomials, plus
+//           the training box.  All terms are non-negative, so the raw sums are
+//           well conditioned; the scaled Gram G[i][j] = M[e_i+e_j] * prod inv^e
+//           is formed once per signature.  Degree-4 monomials are leaves and go
+//           straight into their accumulator with one FMA (63 FP64 instructions
+//           per attention point instead of ~130 for a direct 10x10 Gram).
+//           u32 -> f64 conversion uses the exact 2^52 bias trick (one DADD on
+//           the FP64 pipe instead of the quarter-rate I2F).
+//   reduce  warp shuffles -> shared memory -> warp 0.
+//   solve   warp 0 factors G with a right-looking Cholesky, one lane per row,
+//           reciprocal-multiply instead of FP64 division; columns whose pivot
+//           falls to <= DROP_TOL x their diagonal are dropped (rank-deficient
+//           designs), then forward/back substitution by shuffles.
+//   pass 2  training MAPE (fit_error) of the clamped predictor (FMA form; the
+//           bit-exact no-FMA form is only needed where predictions are
+//           returned, see common.cuh).
 // FP64 throughout; no tensor cores (B200's FP64 tensor peak equals the FP64
 // vector peak and lower precisions cannot meet the 1e-9 contract).
 #include "attn_moments.cuh"
@@ -30,28 +36,26 @@
 namespace dooly {
 
 constexpr double DROP_TOL = 1e-9;
-constexpr int FIT_THREADS = 256;
-constexpr int FIT_WARPS = FIT_THREADS / 32;
 constexpr int FIT_CAP = 4096;  // points per shared-memory stage
+constexpr int FIT_CTAS_PER_SM = 2;
 
 template <int KIND>
 struct FitTraits;
 
 template <>
 struct FitTraits<DOOLY_KIND_AFFINE> {
-  static constexpr int P = 1;     // features
-  static constexpr int NCOL = 2;  // design columns [1, f]
-  static constexpr int NMOM = 3;  // 1, x, x^2
-  static constexpr int NEED = 4;  // max(4, NCOL + 1)   (App. A.8)
-  static constexpr int STAGES = 3;
-  __device__ static __forceinline__ void monomials(const double* v, double* m) {
-    m[0] = 1.0;
-    m[1] = v[0];
-    m[2] = v[0] * v[0];
+  static constexpr int P = 1;      // features
+  static constexpr int NCOL = 2;   // design columns [1, f]
+  static constexpr int NMOM = 3;   // 1, x, x^2
+  static constexpr int NEED = 4;   // max(4, NCOL + 1)   (App. A.8)
+  static constexpr int STAGES = 2;
+  static constexpr int THREADS = 128;
+  __device__ static __forceinline__ void accumulate(const double* v, double y, double* acc) {
+    acc[0] += v[0];
+    acc[1] = fma(v[0], v[0], acc[1]);
+    acc[2] += y;
+    acc[3] = fma(y, v[0], acc[3]);
   }
-  __device__ static __forceinline__ int colmon(int i) { return i; }
-  __device__ static __forceinline__ int gidx(int i, int j) { return i + j; }
-  __device__ static __forceinline__ int exp(int m, int) { return m; }
 };
 
 template <>
@@ -60,14 +64,11 @@ struct FitTraits<DOOLY_KIND_ATTN> {
   static constexpr int NCOL = 10;
   static constexpr int NMOM = 35;
   static constexpr int NEED = 11;
-  static constexpr int STAGES = 2;
-  __device__ static __forceinline__ void monomials(const double* v, double* m) {
-    attn_monomials(v[0], v[1], v[2], m);
+  static constexpr int STAGES = 1;
+  static constexpr int THREADS = 128;
+  __device__ static __forceinline__ void accumulate(const double* v, double y, double* acc) {
+    attn_accumulate(v[0], v[1], v[2], y, acc);
   }
-  // dynamic-index lookups (Gram assembly, once per signature) use __constant__ tables
-  __device__ static __forceinline__ int colmon(int i) { return kAttnColmon[i]; }
-  __device__ static __forceinline__ int gidx(int i, int j) { return kAttnGidx[i][j]; }
-  __device__ static __forceinline__ int exp(int m, int k) { return kAttnExp[m][k]; }
 };
 
 // Stage layout in shared memory: y[FIT_CAP + 2] f64, then P planes of
@@ -90,6 +91,11 @@ __device__ __forceinline__ double rcp64(double y) {
   return fma(r, e, r);
 }
 
+// Exact u32 -> f64 on the FP64 pipe: 2^52 + x has x in its low mantissa bits.
+__device__ __forceinline__ double u2d(uint32_t x) {
+  return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -97,22 +103,22 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// FMA form of the predictor, used only for the training-MAPE diagnostic.
 template <int KIND>
-__device__ __forceinline__ double eval_row(const double* c, const double* inv,
-                                           const uint32_t* xs) {
+__device__ __forceinline__ double eval_fma(const double* c, const double* inv, const double* v) {
   if constexpr (KIND == DOOLY_KIND_AFFINE) {
-    AffineRow r;
-    r.c0 = c[0];
-    r.c1 = c[1];
-    r.inv = inv[0];
-    return eval_affine(r, xs[0]);
+    return fma(c[1], v[0] * inv[0], c[0]);
   } else {
-    AttnRow r;
-#pragma unroll
-    for (int i = 0; i < 10; ++i) r.c[i] = c[i];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) r.inv[k] = inv[k];
-    return eval_attn(r, xs[0], xs[1], xs[2]);
+    const double f1 = v[0] * inv[0], f2 = v[1] * inv[1], f3 = v[2] * inv[2];
+    double p = fma(c[1], f1, c[0]);
+    p = fma(c[2], f2, p);
+    p = fma(c[3], f3, p);
+    p = fma(c[4], f1 * f1, p);
+    p = fma(c[5], f2 * f2, p);
+    p = fma(c[6], f3 * f3, p);
+    p = fma(c[7], f1 * f2, p);
+    p = fma(c[8], f1 * f3, p);
+    return fma(c[9], f2 * f3, p);
   }
 }
 
@@ -145,17 +151,20 @@ struct SmemPoints {
 
 template <int KIND>
 struct FitScratch {
-  static constexpr int P = FitTraits<KIND>::P, NCOL = FitTraits<KIND>::NCOL,
-                       NACC = FitTraits<KIND>::NMOM - 1 + FitTraits<KIND>::NCOL;
-  double part[FIT_WARPS][NACC];
-  uint32_t mn[FIT_WARPS][P], mx[FIT_WARPS][P];
-  double mom[NACC];
-  double G[NCOL][NCOL + 1];
+  using T = FitTraits<KIND>;
+  static constexpr int P = T::P, NCOL = T::NCOL, NMOM = T::NMOM;
+  static constexpr int NACC = NMOM - 1 + NCOL, WARPS = T::THREADS / 32;
+  double part[WARPS][NACC];
+  uint32_t mn[WARPS][P], mx[WARPS][P];
+  double msc[NMOM];              // scaled moments, msc[0] = n
   double b[NCOL];
   double coef[NCOL];
   double inv[P];
   uint32_t lo[P], hi[P];
-  double err[FIT_WARPS];
+  double err[WARPS];
+  int8_t gidx[NCOL][NCOL];       // Gram entry -> moment index
+  int8_t colmon[NCOL];           // design column -> moment index
+  int8_t ex[NMOM][P];            // moment exponents
 };
 
 template <int KIND>
@@ -178,17 +187,35 @@ __device__ void write_unfitted(void* table, int64_t s, double* fit_err, uint8_t*
   status[s] = DOOLY_FIT_INSUFFICIENT;
 }
 
+template <int KIND>
+__device__ void init_tables(FitScratch<KIND>& sh) {
+  using T = FitTraits<KIND>;
+  for (int t = threadIdx.x; t < T::NCOL * T::NCOL; t += blockDim.x) {
+    const int i = t / T::NCOL, j = t % T::NCOL;
+    if constexpr (KIND == DOOLY_KIND_AFFINE)
+      sh.gidx[i][j] = (int8_t)(i + j);
+    else
+      sh.gidx[i][j] = kAttnGidx[i][j];
+  }
+  for (int t = threadIdx.x; t < T::NCOL; t += blockDim.x)
+    sh.colmon[t] = KIND == DOOLY_KIND_AFFINE ? (int8_t)t : kAttnColmon[t];
+  for (int t = threadIdx.x; t < T::NMOM * T::P; t += blockDim.x) {
+    const int m = t / T::P, k = t % T::P;
+    if constexpr (KIND == DOOLY_KIND_AFFINE)
+      sh.ex[m][k] = (int8_t)m;
+    else
+      sh.ex[m][k] = kAttnExp[m][k];
+  }
+}
+
 // Fit one signature with n >= NEED points; all threads of the CTA participate.
 template <int KIND, typename Pts>
 __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& sh, void* table,
                         double* fit_err, uint8_t* status) {
   using T = FitTraits<KIND>;
-  constexpr int P = T::P, NCOL = T::NCOL, NMOM = T::NMOM;
-  constexpr int NACC = (NMOM - 1) + NCOL;
+  constexpr int P = T::P, NCOL = T::NCOL, NMOM = T::NMOM, NT = T::THREADS;
+  constexpr int NACC = (NMOM - 1) + NCOL, WARPS = NT / 32;
   constexpr int UNR = 4;
-  constexpr int kAffineColmon[2] = {0, 1};
-  constexpr int kAttnColmonStatic[10] = DOOLY_ATTN_COLMON;
-  const int* kColmon = KIND == DOOLY_KIND_AFFINE ? kAffineColmon : kAttnColmonStatic;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
   // ---------------- pass 1: raw moments + box
@@ -201,12 +228,12 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
     mn[k] = 0xFFFFFFFFu;
     mx[k] = 0u;
   }
-  for (int64_t i0 = tid; i0 < n; i0 += FIT_THREADS * UNR) {
+  for (int64_t i0 = tid; i0 < n; i0 += NT * UNR) {
     uint32_t xv[UNR][P];
     double yv[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int64_t i = i0 + u * FIT_THREADS;
+      const int64_t i = i0 + u * NT;
       if (i < n) {
         pts.load(i, xv[u], yv[u]);
       } else {
@@ -217,21 +244,15 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      if (i0 + u * FIT_THREADS >= n) break;
-      double mon[NMOM];
+      if (i0 + u * NT >= n) break;
       double v[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        v[k] = (double)xv[u][k];
+        v[k] = u2d(xv[u][k]);
         mn[k] = min(mn[k], xv[u][k]);
         mx[k] = max(mx[k], xv[u][k]);
       }
-      T::monomials(v, mon);
-#pragma unroll
-      for (int m = 1; m < NMOM; ++m) acc[m - 1] += mon[m];
-#pragma unroll
-      for (int i = 0; i < NCOL; ++i)
-        acc[NMOM - 1 + i] = fma(yv[u], mon[kColmon[i]], acc[NMOM - 1 + i]);
+      T::accumulate(v, yv[u], acc);
     }
   }
 #pragma unroll
@@ -251,46 +272,53 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
     }
   }
   __syncthreads();
-  if (tid < NACC) {
-    double t = 0.0;
-#pragma unroll
-    for (int w = 0; w < FIT_WARPS; ++w) t += sh.part[w][tid];
-    sh.mom[tid] = t;
-  } else if (tid >= 64 && tid < 64 + P) {
-    const int k = tid - 64;
-    uint32_t a = 0xFFFFFFFFu, b = 0u;
-#pragma unroll
-    for (int w = 0; w < FIT_WARPS; ++w) {
-      a = min(a, sh.mn[w][k]);
-      b = max(b, sh.mx[w][k]);
-    }
-    sh.lo[k] = a;
-    sh.hi[k] = b;
-    sh.inv[k] = b > 0 ? 1.0 / (double)b : 1.0;  // IEEE division: bit-identical to the oracle
-  }
-  __syncthreads();
-  // ---------------- scaled Gram / rhs (one entry per thread)
-  if (tid < NCOL * NCOL + NCOL) {
-    const int i = tid < NCOL * NCOL ? tid / NCOL : tid - NCOL * NCOL;
-    const int j = tid < NCOL * NCOL ? tid % NCOL : -1;
-    const int m = j >= 0 ? T::gidx(i, j) : T::colmon(i);
-    double scl = 1.0;
-    for (int k = 0; k < P; ++k)
-      for (int r = 0; r < T::exp(m, k); ++r) scl *= sh.inv[k];
-    if (j >= 0)
-      sh.G[i][j] = (m == 0 ? (double)n : sh.mom[m - 1]) * scl;
-    else
-      sh.b[i] = sh.mom[NMOM - 1 + i] * scl;
-  }
-  __syncthreads();
-  // ---------------- solve: warp 0, lane i owns row i
+  // ---------------- warp 0: moments -> scaled Gram -> Cholesky solve
   if (wid == 0) {
+    if (lane < P) {
+      uint32_t a = 0xFFFFFFFFu, b = 0u;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        a = min(a, sh.mn[w][lane]);
+        b = max(b, sh.mx[w][lane]);
+      }
+      sh.lo[lane] = a;
+      sh.hi[lane] = b;
+      sh.inv[lane] = b > 0 ? 1.0 / (double)b : 1.0;  // IEEE division: bit-identical to the oracle
+    }
+    __syncwarp();
+    double inv[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) inv[k] = sh.inv[k];
+    auto scale_of = [&](int m) {
+      double scl = 1.0;
+#pragma unroll
+      for (int k = 0; k < P; ++k)
+        for (int r = 0; r < sh.ex[m][k]; ++r) scl *= inv[k];
+      return scl;
+    };
+    for (int m = lane; m < NMOM; m += 32) {
+      double raw = (double)n;
+      if (m > 0) {
+        raw = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) raw += sh.part[w][m - 1];
+      }
+      sh.msc[m] = raw * scale_of(m);
+    }
+    if (lane < NCOL) {
+      double raw = 0.0;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) raw += sh.part[w][NMOM - 1 + lane];
+      sh.b[lane] = raw * scale_of(sh.colmon[lane]);
+    }
+    __syncwarp();
     const int r = lane < NCOL ? lane : 0;
     double g[NCOL];
 #pragma unroll
-    for (int k = 0; k < NCOL; ++k) g[k] = sh.G[r][k];
-    const double diag = sh.G[r][r];
+    for (int k = 0; k < NCOL; ++k) g[k] = sh.msc[sh.gidx[r][k]];
+    const double diag = sh.msc[sh.gidx[r][r]];
     uint32_t keep = 0;
+    double rd = 0.0;  // lane j: 1 / L[j][j]
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) {
       const double piv = __shfl_sync(0xFFFFFFFFu, g[j], j);
@@ -298,39 +326,38 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
       const bool kj = piv > DROP_TOL * dj;
       keep |= (uint32_t)kj << j;
       const double d = kj ? sqrt(piv) : 0.0;
-      double lij = (kj && lane > j) ? g[j] / d : 0.0;
+      const double inv_d = kj ? rcp64(d) : 0.0;
+      if (lane == j) rd = inv_d;
+      double lij = lane > j ? g[j] * inv_d : 0.0;
       if (lane == j) lij = d;
       if (lane >= j) g[j] = lij;
 #pragma unroll
       for (int k = j + 1; k < NCOL; ++k) {
         const double lkj = __shfl_sync(0xFFFFFFFFu, lij, k);
-        g[k] -= lij * lkj;
+        g[k] = fma(-lij, lkj, g[k]);
       }
     }
     // forward: L z = b
     double t = lane < NCOL ? sh.b[lane] : 0.0, z = 0.0;
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) {
-      const bool kj = (keep >> j) & 1u;
-      const double zl = (kj && lane == j) ? t / g[j] : 0.0;
-      const double zj = __shfl_sync(0xFFFFFFFFu, zl, j);
-      if (lane > j) t -= g[j] * zj;
+      const double zj = __shfl_sync(0xFFFFFFFFu, t * rd, j);  // 0 for dropped columns
+      if (lane > j) t = fma(-g[j], zj, t);
       if (lane == j) z = zj;
     }
     // backward: L^T c = z
     double u = z, c = 0.0;
 #pragma unroll
     for (int j = NCOL - 1; j >= 0; --j) {
-      const bool kj = (keep >> j) & 1u;
-      const double cl = (kj && lane == j) ? u / g[j] : 0.0;
-      const double cj = __shfl_sync(0xFFFFFFFFu, cl, j);
+      const double cj = __shfl_sync(0xFFFFFFFFu, u * rd, j);
       if (lane == j) c = cj;
 #pragma unroll
       for (int m = 0; m < j; ++m) {
         const double ljm = __shfl_sync(0xFFFFFFFFu, g[m], j);  // L[j][m] from lane j
-        if (lane == m) u -= ljm * cj;
+        if (lane == m) u = fma(-ljm, cj, u);
       }
     }
+    (void)keep;
     if (lane < NCOL) sh.coef[lane] = c;
   }
   __syncthreads();
@@ -341,12 +368,12 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
 #pragma unroll
   for (int k = 0; k < P; ++k) inv[k] = sh.inv[k];
   double err = 0.0;
-  for (int64_t i0 = tid; i0 < n; i0 += FIT_THREADS * UNR) {
+  for (int64_t i0 = tid; i0 < n; i0 += NT * UNR) {
     uint32_t xv[UNR][P];
     double yv[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      const int64_t i = i0 + u * FIT_THREADS;
+      const int64_t i = i0 + u * NT;
       if (i < n) {
         pts.load(i, xv[u], yv[u]);
       } else {
@@ -357,10 +384,12 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
     }
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
-      if (i0 + u * FIT_THREADS >= n) break;
-      bool cl;
-      const double p = clamp_floor(eval_row<KIND>(coef, inv, xv[u]), cl);
-      err += fabs(p - yv[u]) * rcp64(yv[u]);
+      if (i0 + u * NT >= n) break;
+      double v[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) v[k] = u2d(xv[u][k]);
+      const double p = fmax(eval_fma<KIND>(coef, inv, v), DOOLY_CLAMP_FLOOR);
+      err = fma(fabs(p - yv[u]), rcp64(yv[u]), err);
     }
   }
   err = warp_sum(err);
@@ -369,7 +398,7 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
   if (tid == 0) {
     double e = 0.0;
 #pragma unroll
-    for (int w = 0; w < FIT_WARPS; ++w) e += sh.err[w];
+    for (int w = 0; w < WARPS; ++w) e += sh.err[w];
     fit_err[s] = e / (double)n;
     status[s] = DOOLY_FIT_OK;
     if constexpr (KIND == DOOLY_KIND_AFFINE) {
@@ -389,7 +418,8 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
       }
     }
   }
-  __syncthreads();  // shared scratch reused by the next signature
+  // the caller's next __syncthreads (or the next signature's first one)
+  // orders these smem reads before any rewrite of sh
 }
 
 // --------------------------------------------------------------- bulk copies
@@ -442,8 +472,8 @@ __device__ __forceinline__ Window make_window(int64_t beg, int64_t end, int64_t 
   return w;
 }
 
-// Issue the bulk copies of signature s into stage memory; returns nothing, the
-// tail elements beyond the aligned window are loaded by the consumers.
+// Issue the bulk copies of one signature into a stage; the (<4) tail elements
+// past the last aligned chunk of the arrays are loaded by the consumers.
 template <int KIND>
 __device__ void issue_stage(unsigned char* stage, uint64_t* bar, const uint32_t* x, int64_t n_pts,
                             const double* y, int64_t beg, int64_t end) {
@@ -462,7 +492,7 @@ __device__ void issue_stage(unsigned char* stage, uint64_t* bar, const uint32_t*
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(FIT_THREADS, 1) fit_bulk_kernel(
+__global__ void __launch_bounds__(FitTraits<KIND>::THREADS, FIT_CTAS_PER_SM) fit_bulk_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y,
     const int64_t* __restrict__ off, int64_t n_sig, void* __restrict__ table,
     double* __restrict__ fit_err, uint8_t* __restrict__ status, bool bulk_ok) {
@@ -480,6 +510,7 @@ __global__ void __launch_bounds__(FIT_THREADS, 1) fit_bulk_kernel(
     const int64_t n = off[s + 1] - off[s];
     return bulk_ok && n >= T::NEED && n <= FIT_CAP;
   };
+  init_tables<KIND>(sh);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -496,7 +527,7 @@ __global__ void __launch_bounds__(FIT_THREADS, 1) fit_bulk_kernel(
   for (int64_t k = 0;; ++k) {
     const int64_t s = sig_of(k);
     if (s >= n_sig) break;
-    // keep STAGES-1 signatures in flight: refill the stage freed at the end of k-1
+    // keep STAGES-1 signatures ahead: refill the stage freed by signature k-1
     if (tid == 0) {
       const int64_t kn = k + NST - 1;
       const int64_t sn = sig_of(kn);
@@ -514,6 +545,7 @@ __global__ void __launch_bounds__(FIT_THREADS, 1) fit_bulk_kernel(
     if (!stageable(s)) {  // oversized / unaligned inputs: stream straight from global memory
       GlobalPoints<T::P> gp{x, n_pts, y, beg};
       fit_one<KIND>(gp, n, s, sh, table, fit_err, status);
+      __syncthreads();
       continue;
     }
     const int st = (int)(k % NST);
@@ -534,7 +566,8 @@ __global__ void __launch_bounds__(FIT_THREADS, 1) fit_bulk_kernel(
     }
     __syncthreads();
     SmemPoints<T::P> sp{sx, S::X_LEN, wx.head, sy, wy.head};
-    fit_one<KIND>(sp, n, s, sh, table, fit_err, status);  // ends with __syncthreads
+    fit_one<KIND>(sp, n, s, sh, table, fit_err, status);
+    __syncthreads();  // stage and scratch free for reuse
   }
 }
 
@@ -549,9 +582,12 @@ static cudaError_t launch_kind(const uint32_t* x, int64_t n_pts, const double* y
   // 1-D TMA needs 16-B aligned sources: plane bases and the y array
   const bool bulk_ok = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
                        (FitTraits<KIND>::P == 1 || n_pts % 4 == 0);
-  int64_t blocks = n_sm;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_bulk_kernel<KIND>,
+                                                FitTraits<KIND>::THREADS, smem);
+  int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
   if (blocks > n_sig) blocks = n_sig;
-  fit_bulk_kernel<KIND><<<(unsigned)blocks, FIT_THREADS, smem, stream>>>(
+  fit_bulk_kernel<KIND><<<(unsigned)blocks, FitTraits<KIND>::THREADS, smem, stream>>>(
       x, n_pts, y, off, n_sig, table, fit_err, status, bulk_ok);
   return cudaGetLastError();
 }
