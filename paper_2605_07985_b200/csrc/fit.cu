@@ -30,6 +30,8 @@
 //           returned, see common.cuh).
 // FP64 throughout; no tensor cores (B200's FP64 tensor peak equals the FP64
 // vector peak and lower precisions cannot meet the 1e-9 contract).
+#include <stdlib.h>
+
 #include "attn_moments.cuh"
 #include "common.cuh"
 
@@ -48,8 +50,9 @@ struct FitTraits<DOOLY_KIND_AFFINE> {
   static constexpr int NCOL = 2;   // design columns [1, f]
   static constexpr int NMOM = 3;   // 1, x, x^2
   static constexpr int NEED = 4;   // max(4, NCOL + 1)   (App. A.8)
-  static constexpr int STAGES = 2;
+  static constexpr int STAGES = 1;  // 4 CTAs/SM x 1 stage beat 2x2 and 1x3 (profiles/)
   static constexpr int THREADS = 128;
+  static constexpr int SETS = 2;  // independent accumulator sets (breaks DADD chains)
   __device__ static __forceinline__ void accumulate(const double* v, double y, double* acc) {
     acc[0] += v[0];
     acc[1] = fma(v[0], v[0], acc[1]);
@@ -66,6 +69,7 @@ struct FitTraits<DOOLY_KIND_ATTN> {
   static constexpr int NEED = 11;
   static constexpr int STAGES = 1;
   static constexpr int THREADS = 128;
+  static constexpr int SETS = 1;  // 44 independent accumulators already give the ILP
   __device__ static __forceinline__ void accumulate(const double* v, double y, double* acc) {
     attn_accumulate(v[0], v[1], v[2], y, acc);
   }
@@ -219,9 +223,12 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
   // ---------------- pass 1: raw moments + box
-  double acc[NACC];
+  constexpr int SETS = T::SETS;
+  double accs[SETS][NACC];
 #pragma unroll
-  for (int i = 0; i < NACC; ++i) acc[i] = 0.0;
+  for (int q = 0; q < SETS; ++q)
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) accs[q][i] = 0.0;
   uint32_t mn[P], mx[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) {
@@ -252,11 +259,17 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
         mn[k] = min(mn[k], xv[u][k]);
         mx[k] = max(mx[k], xv[u][k]);
       }
-      T::accumulate(v, yv[u], acc);
+      T::accumulate(v, yv[u], accs[u % SETS]);
     }
   }
+  double acc[NACC];
 #pragma unroll
-  for (int i = 0; i < NACC; ++i) acc[i] = warp_sum(acc[i]);
+  for (int i = 0; i < NACC; ++i) {
+    acc[i] = accs[0][i];
+#pragma unroll
+    for (int q = 1; q < SETS; ++q) acc[i] += accs[q][i];
+    acc[i] = warp_sum(acc[i]);
+  }
 #pragma unroll
   for (int k = 0; k < P; ++k) {
     mn[k] = __reduce_min_sync(0xFFFFFFFFu, mn[k]);
@@ -495,12 +508,12 @@ template <int KIND>
 __global__ void __launch_bounds__(FitTraits<KIND>::THREADS, FIT_CTAS_PER_SM) fit_bulk_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y,
     const int64_t* __restrict__ off, int64_t n_sig, void* __restrict__ table,
-    double* __restrict__ fit_err, uint8_t* __restrict__ status, bool bulk_ok) {
+    double* __restrict__ fit_err, uint8_t* __restrict__ status, bool bulk_ok, int nst) {
   using T = FitTraits<KIND>;
   using S = Stage<KIND>;
-  constexpr int NST = T::STAGES;
+  const int NST = nst;  // 1..4 stages (runtime: tuned per kind at launch)
   extern __shared__ __align__(128) unsigned char dyn[];
-  __shared__ __align__(8) uint64_t bars[NST];
+  __shared__ __align__(8) uint64_t bars[4];
   __shared__ FitScratch<KIND> sh;
   const int tid = threadIdx.x;
 
@@ -523,26 +536,47 @@ __global__ void __launch_bounds__(FitTraits<KIND>::THREADS, FIT_CTAS_PER_SM) fit
         issue_stage<KIND>(dyn + (size_t)k * S::STRIDE, &bars[k], x, n_pts, y, off[s], off[s + 1]);
     }
   }
+  // CSR offsets are software-pipelined two signatures ahead so their global
+  // load latency never sits on the critical path (ncu: the refill's dependent
+  // off[] loads were stalling the whole CTA at the next barrier).
+  auto load_off = [&](int64_t kk, int64_t& b, int64_t& e) {
+    const int64_t ss = sig_of(kk);
+    b = ss < n_sig ? __ldg(off + ss) : 0;
+    e = ss < n_sig ? __ldg(off + ss + 1) : 0;
+  };
+  int64_t ob[4], oe[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) load_off(i, ob[i], oe[i]);
+  auto stageable_be = [&](int64_t b, int64_t e) {
+    return bulk_ok && e - b >= T::NEED && e - b <= FIT_CAP;
+  };
   uint32_t phase_bits = 0;  // per-stage parity
   for (int64_t k = 0;; ++k) {
     const int64_t s = sig_of(k);
     if (s >= n_sig) break;
+    const int64_t beg = ob[0], end = oe[0], n = end - beg;
     // keep STAGES-1 signatures ahead: refill the stage freed by signature k-1
     if (tid == 0) {
       const int64_t kn = k + NST - 1;
       const int64_t sn = sig_of(kn);
-      if (sn < n_sig && stageable(sn)) {
+      const int64_t nb = NST == 1 ? ob[0] : NST == 2 ? ob[1] : NST == 3 ? ob[2] : ob[3];
+      const int64_t ne = NST == 1 ? oe[0] : NST == 2 ? oe[1] : NST == 3 ? oe[2] : oe[3];
+      if (sn < n_sig && stageable_be(nb, ne)) {
         const int st = (int)(kn % NST);
-        issue_stage<KIND>(dyn + (size_t)st * S::STRIDE, &bars[st], x, n_pts, y, off[sn],
-                          off[sn + 1]);
+        issue_stage<KIND>(dyn + (size_t)st * S::STRIDE, &bars[st], x, n_pts, y, nb, ne);
       }
     }
-    const int64_t beg = off[s], end = off[s + 1], n = end - beg;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      ob[i] = ob[i + 1];
+      oe[i] = oe[i + 1];
+    }
+    load_off(k + 4, ob[3], oe[3]);
     if (n < T::NEED) {
       if (tid == 0) write_unfitted<KIND>(table, s, fit_err, status);
       continue;  // no stage was used (stageable() is false)
     }
-    if (!stageable(s)) {  // oversized / unaligned inputs: stream straight from global memory
+    if (!stageable_be(beg, end)) {  // oversized / unaligned inputs: stream from global memory
       GlobalPoints<T::P> gp{x, n_pts, y, beg};
       fit_one<KIND>(gp, n, s, sh, table, fit_err, status);
       __syncthreads();
@@ -575,7 +609,13 @@ template <int KIND>
 static cudaError_t launch_kind(const uint32_t* x, int64_t n_pts, const double* y,
                                const int64_t* off, int64_t n_sig, void* table, double* fit_err,
                                uint8_t* status, cudaStream_t stream, int n_sm) {
-  const size_t smem = (size_t)FitTraits<KIND>::STAGES * Stage<KIND>::STRIDE;
+  int nst = FitTraits<KIND>::STAGES;
+  if (const char* env = getenv(KIND == DOOLY_KIND_AFFINE ? "DOOLY_FIT_STAGES_AFFINE"
+                                                         : "DOOLY_FIT_STAGES_ATTN")) {
+    const int v = atoi(env);  // tuning knob (profiles/); 1..4
+    if (v >= 1 && v <= 4) nst = v;
+  }
+  const size_t smem = (size_t)nst * Stage<KIND>::STRIDE;
   cudaError_t e = cudaFuncSetAttribute(fit_bulk_kernel<KIND>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -588,7 +628,7 @@ static cudaError_t launch_kind(const uint32_t* x, int64_t n_pts, const double* y
   int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
   if (blocks > n_sig) blocks = n_sig;
   fit_bulk_kernel<KIND><<<(unsigned)blocks, FitTraits<KIND>::THREADS, smem, stream>>>(
-      x, n_pts, y, off, n_sig, table, fit_err, status, bulk_ok);
+      x, n_pts, y, off, n_sig, table, fit_err, status, bulk_ok, nst);
   return cudaGetLastError();
 }
 
