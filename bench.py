@@ -644,7 +644,7 @@ def main(argv=None):
     ap.add_argument("--ref-sample", type=int, default=40_000_000)
     ap.add_argument("--sim-requests", type=int, default=1_000_000)
     ap.add_argument("--sim-shards", type=int, default=1184)
-    ap.add_argument("--sim-rate", type=float, default=0.5)
+    ap.add_argument("--sim-rate", type=float, default=5.0)
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the bench contract requires --warmup >= 3", file=sys.stderr)
