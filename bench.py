@@ -153,14 +153,16 @@ def load_peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
-def ncu_traffic(kernel_key: str):
-    """DRAM bytes per launch from the committed ncu summary (profiles/), or None."""
+def ncu_traffic(kernel_key: str, units: dict):
+    """DRAM bytes per step from the committed ncu per-unit measurement
+    (profiles/ncu_summary.json x this step's units), or None."""
     p = ROOT / "profiles" / "ncu_summary.json"
     if not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(kernel_key, {}).get("dram_bytes_per_launch")
-    except ValueError:
+        per = json.loads(p.read_text())[kernel_key]["dram_bytes_per_unit"]
+        return sum(float(per[str(k)]) * n for k, n in units.items())
+    except (ValueError, KeyError):
         return None
 
 
@@ -366,7 +368,7 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": fit_bytes / (fit_dev_ms / 1e3) / 1e9,
                      "peak": hbm_peak, "unit": "GB/s",
                      "frac": fit_bytes / (fit_dev_ms / 1e3) / 1e9 / hbm_peak,
-                     "traffic": ncu_traffic("fit"),
+                     "traffic": ncu_traffic("fit", {k: n_sig[k] * args.points for k in (AFFINE, ATTN)}),
                      "note": "attention fit is FP64-bound (~100 FP64 instr/point); see DESIGN.md"},
         "all_fitted": status_ok,
     }
@@ -514,7 +516,8 @@ def run_ours(args):
                        "points_per_signature": args.points,
                        "l2": "inputs >> L2 (126 MB); no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": ncu_traffic("predict"),
+                         "frac": achieved / hbm_peak, "traffic": ncu_traffic("predict", nq),
+                         "alg_bytes": alg_bytes,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                          if peak_kind == "measured" else "fallback 6.65 TB/s",
                          "kernel_ms": {"affine": k_ms[AFFINE], "attention": k_ms[ATTN]},
@@ -644,7 +647,7 @@ def main(argv=None):
     ap.add_argument("--ref-sample", type=int, default=40_000_000)
     ap.add_argument("--sim-requests", type=int, default=1_000_000)
     ap.add_argument("--sim-shards", type=int, default=1184)
-    ap.add_argument("--sim-rate", type=float, default=5.0)
+    ap.add_argument("--sim-rate", type=float, default=4.0)
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the bench contract requires --warmup >= 3", file=sys.stderr)
