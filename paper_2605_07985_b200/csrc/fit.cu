@@ -1,14 +1,19 @@
 // K2 — batched per-signature least-squares fit (replaces fit).
 //
-// Data path (B200): a persistent kernel with two 128-thread CTAs per SM.  In
-// each CTA thread 0 streams whole signatures (feature planes + latencies) from
-// HBM into a ring of shared-memory stages with the bulk-copy (1-D TMA) engine
-// (`cp.async.bulk` + mbarrier complete_tx), so both passes over a signature
-// read shared memory and every point is fetched from HBM exactly once.  The
-// two co-resident CTAs interleave: while one is in its short serial phase
-// (reduce + solve) or waiting for its next stage, the other keeps the FP64
-// pipes busy.  Signatures larger than a stage (or unaligned inputs) fall back
-// to a direct global-memory path with the same arithmetic.
+// Data path (B200): a persistent kernel, several 128-thread CTAs per SM (4 for
+// affine, 2 for attention: the shared-memory stage is the limiter).  Each CTA
+// owns one stage that holds a whole signature (<= 4096 points) as two halves
+// of <= 2048 points, each filled by the bulk-copy (1-D TMA) engine
+// (`cp.async.bulk` + mbarrier complete_tx).  Both passes over a signature read
+// shared memory, so every point crosses HBM exactly once.  The halves are
+// refilled as soon as pass 2 has finished with them: the first half of the
+// next signature streams in underneath the second half of pass 2, the second
+// half underneath the write-out and the next signature's first-half pass 1.
+// (A finer chunk ring with a thread-0 producer was measured and was slower:
+// the per-chunk bookkeeping and producer imbalance cost more than the extra
+// overlap bought — profiles/r1_ncu_summary.md.)  Signatures larger than a
+// stage, or unaligned inputs, use a direct global-memory path with the same
+// arithmetic.
 //
 // Per signature:
 //   pass 1  raw power moments sum x^a y^b z^c (a+b+c <= 4: 34 non-trivial for
@@ -30,16 +35,16 @@
 //           returned, see common.cuh).
 // FP64 throughout; no tensor cores (B200's FP64 tensor peak equals the FP64
 // vector peak and lower precisions cannot meet the 1e-9 contract).
-#include <stdlib.h>
-
 #include "attn_moments.cuh"
 #include "common.cuh"
 
 namespace dooly {
 
 constexpr double DROP_TOL = 1e-9;
-constexpr int FIT_CAP = 4096;  // points per shared-memory stage
-constexpr int FIT_CTAS_PER_SM = 2;
+constexpr int FIT_THREADS = 128;
+constexpr int FIT_WARPS = FIT_THREADS / 32;
+constexpr int FIT_UNR = 4;
+constexpr int FIT_HALF = 2048;  // points per half stage; a stage holds 2 * FIT_HALF
 
 template <int KIND>
 struct FitTraits;
@@ -50,9 +55,7 @@ struct FitTraits<DOOLY_KIND_AFFINE> {
   static constexpr int NCOL = 2;   // design columns [1, f]
   static constexpr int NMOM = 3;   // 1, x, x^2
   static constexpr int NEED = 4;   // max(4, NCOL + 1)   (App. A.8)
-  static constexpr int STAGES = 1;  // 4 CTAs/SM x 1 stage beat 2x2 and 1x3 (profiles/)
-  static constexpr int THREADS = 128;
-  static constexpr int SETS = 2;  // independent accumulator sets (breaks DADD chains)
+  static constexpr int SETS = 2;   // independent accumulator sets (breaks DADD chains)
   __device__ static __forceinline__ void accumulate(const double* v, double y, double* acc) {
     acc[0] += v[0];
     acc[1] = fma(v[0], v[0], acc[1]);
@@ -67,23 +70,22 @@ struct FitTraits<DOOLY_KIND_ATTN> {
   static constexpr int NCOL = 10;
   static constexpr int NMOM = 35;
   static constexpr int NEED = 11;
-  static constexpr int STAGES = 1;
-  static constexpr int THREADS = 128;
-  static constexpr int SETS = 1;  // 44 independent accumulators already give the ILP
+  static constexpr int SETS = 1;   // 44 independent accumulators already give the ILP
   __device__ static __forceinline__ void accumulate(const double* v, double y, double* acc) {
     attn_accumulate(v[0], v[1], v[2], y, acc);
   }
 };
 
-// Stage layout in shared memory: y[FIT_CAP + 2] f64, then P planes of
-// x[FIT_CAP + 4] u32 (the +2/+4 hold the head misalignment of the window).
+// Half-stage layout: y[FIT_HALF + 2] f64, then P planes of x[FIT_HALF + 4] u32
+// (the +2/+4 hold the head misalignment of the aligned bulk window).
 template <int KIND>
-struct Stage {
+struct Half {
   static constexpr int P = FitTraits<KIND>::P;
-  static constexpr int Y_LEN = FIT_CAP + 2;
-  static constexpr int X_LEN = FIT_CAP + 4;
+  static constexpr int Y_LEN = FIT_HALF + 2;
+  static constexpr int X_LEN = FIT_HALF + 4;
   static constexpr size_t BYTES = (size_t)Y_LEN * 8 + (size_t)P * X_LEN * 4;
   static constexpr size_t STRIDE = (BYTES + 127) & ~(size_t)127;
+  static constexpr size_t STAGE_BYTES = 2 * STRIDE;
 };
 
 __device__ __forceinline__ double rcp64(double y) {
@@ -126,14 +128,14 @@ __device__ __forceinline__ double eval_fma(const double* c, const double* inv, c
   }
 }
 
-// Point sources -----------------------------------------------------------
+// Point sources ----------------------------------------------------------
 template <int P>
-struct GlobalPoints {
+struct GlobalPoints {  // points beg + i of the CSR arrays
   const uint32_t* x;
   int64_t n_pts;
   const double* y;
   int64_t beg;
-  __device__ __forceinline__ void load(int64_t i, uint32_t* xs, double& yv) const {
+  __device__ __forceinline__ void load(int i, uint32_t* xs, double& yv) const {
 #pragma unroll
     for (int k = 0; k < P; ++k) xs[k] = __ldg(x + k * n_pts + beg + i);
     yv = __ldg(y + beg + i);
@@ -141,15 +143,41 @@ struct GlobalPoints {
 };
 
 template <int P>
-struct SmemPoints {
-  const uint32_t* x;  // plane 0; plane k at + k * xlen
-  int xlen, xhead;
-  const double* y;
-  int yhead;
-  __device__ __forceinline__ void load(int64_t i, uint32_t* xs, double& yv) const {
+struct HalfPoints {  // one half stage; points past the bulk window come from global
+  const uint32_t* sx;
+  int xlen, xhead, xbulk;  // xbulk: points served from smem
+  const double* sy;
+  int yhead, ybulk;
+  GlobalPoints<P> g;       // global fallback for the (<4) array-end tail points
+  __device__ __forceinline__ void load(int i, uint32_t* xs, double& yv) const {
+    if (i < xbulk) {
 #pragma unroll
-    for (int k = 0; k < P; ++k) xs[k] = x[k * xlen + xhead + (int)i];
-    yv = y[yhead + (int)i];
+      for (int k = 0; k < P; ++k) xs[k] = sx[k * xlen + xhead + i];
+    } else {
+#pragma unroll
+      for (int k = 0; k < P; ++k) xs[k] = __ldg(g.x + k * g.n_pts + g.beg + i);
+    }
+    yv = i < ybulk ? sy[yhead + i] : __ldg(g.y + g.beg + i);
+  }
+  // Whole half in shared memory with 16-B aligned windows: 4-point vector loads.
+  __device__ __forceinline__ bool dense(int cnt) const {
+    return xhead == 0 && yhead == 0 && xbulk >= cnt && ybulk >= cnt;
+  }
+  __device__ __forceinline__ void load4(int i4, uint32_t (*xs)[P], double* yv) const {
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const uint4 v = *reinterpret_cast<const uint4*>(sx + k * xlen + i4);
+      xs[0][k] = v.x;
+      xs[1][k] = v.y;
+      xs[2][k] = v.z;
+      xs[3][k] = v.w;
+    }
+    const double2 a = *reinterpret_cast<const double2*>(sy + i4);
+    const double2 b = *reinterpret_cast<const double2*>(sy + i4 + 2);
+    yv[0] = a.x;
+    yv[1] = a.y;
+    yv[2] = b.x;
+    yv[3] = b.y;
   }
 };
 
@@ -157,15 +185,15 @@ template <int KIND>
 struct FitScratch {
   using T = FitTraits<KIND>;
   static constexpr int P = T::P, NCOL = T::NCOL, NMOM = T::NMOM;
-  static constexpr int NACC = NMOM - 1 + NCOL, WARPS = T::THREADS / 32;
-  double part[WARPS][NACC];
-  uint32_t mn[WARPS][P], mx[WARPS][P];
+  static constexpr int NACC = NMOM - 1 + NCOL;
+  double part[FIT_WARPS][NACC];
+  uint32_t mn[FIT_WARPS][P], mx[FIT_WARPS][P];
   double msc[NMOM];              // scaled moments, msc[0] = n
   double b[NCOL];
   double coef[NCOL];
   double inv[P];
   uint32_t lo[P], hi[P];
-  double err[WARPS];
+  double err[FIT_WARPS];
   int8_t gidx[NCOL][NCOL];       // Gram entry -> moment index
   int8_t colmon[NCOL];           // design column -> moment index
   int8_t ex[NMOM][P];            // moment exponents
@@ -212,36 +240,37 @@ __device__ void init_tables(FitScratch<KIND>& sh) {
   }
 }
 
-// Fit one signature with n >= NEED points; all threads of the CTA participate.
-template <int KIND, typename Pts>
-__device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& sh, void* table,
-                        double* fit_err, uint8_t* status) {
-  using T = FitTraits<KIND>;
-  constexpr int P = T::P, NCOL = T::NCOL, NMOM = T::NMOM, NT = T::THREADS;
-  constexpr int NACC = (NMOM - 1) + NCOL, WARPS = NT / 32;
-  constexpr int UNR = 4;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-
-  // ---------------- pass 1: raw moments + box
-  constexpr int SETS = T::SETS;
-  double accs[SETS][NACC];
+// --------------------------------------------------------------- fit phases
+template <int KIND>
+struct Pass1State {
+  static constexpr int NACC = FitTraits<KIND>::NMOM - 1 + FitTraits<KIND>::NCOL;
+  double accs[FitTraits<KIND>::SETS][NACC];
+  uint32_t mn[FitTraits<KIND>::P], mx[FitTraits<KIND>::P];
+  __device__ __forceinline__ void reset() {
 #pragma unroll
-  for (int q = 0; q < SETS; ++q)
+    for (int q = 0; q < FitTraits<KIND>::SETS; ++q)
 #pragma unroll
-    for (int i = 0; i < NACC; ++i) accs[q][i] = 0.0;
-  uint32_t mn[P], mx[P];
+      for (int i = 0; i < NACC; ++i) accs[q][i] = 0.0;
 #pragma unroll
-  for (int k = 0; k < P; ++k) {
-    mn[k] = 0xFFFFFFFFu;
-    mx[k] = 0u;
+    for (int k = 0; k < FitTraits<KIND>::P; ++k) {
+      mn[k] = 0xFFFFFFFFu;
+      mx[k] = 0u;
+    }
   }
-  for (int64_t i0 = tid; i0 < n; i0 += NT * UNR) {
-    uint32_t xv[UNR][P];
-    double yv[UNR];
+};
+
+// Accumulate points [0, cnt) of a source (threads stride over them).
+template <int KIND, typename Pts>
+__device__ __forceinline__ void pass1(const Pts& pts, int cnt, Pass1State<KIND>& st) {
+  using T = FitTraits<KIND>;
+  constexpr int P = T::P;
+  for (int i0 = threadIdx.x; i0 < cnt; i0 += FIT_THREADS * FIT_UNR) {
+    uint32_t xv[FIT_UNR][P];
+    double yv[FIT_UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int64_t i = i0 + u * NT;
-      if (i < n) {
+    for (int u = 0; u < FIT_UNR; ++u) {
+      const int i = i0 + u * FIT_THREADS;
+      if (i < cnt) {
         pts.load(i, xv[u], yv[u]);
       } else {
 #pragma unroll
@@ -250,47 +279,93 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
       }
     }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      if (i0 + u * NT >= n) break;
+    for (int u = 0; u < FIT_UNR; ++u) {
+      if (i0 + u * FIT_THREADS >= cnt) break;
       double v[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         v[k] = u2d(xv[u][k]);
-        mn[k] = min(mn[k], xv[u][k]);
-        mx[k] = max(mx[k], xv[u][k]);
+        st.mn[k] = min(st.mn[k], xv[u][k]);
+        st.mx[k] = max(st.mx[k], xv[u][k]);
       }
-      T::accumulate(v, yv[u], accs[u % SETS]);
+      T::accumulate(v, yv[u], st.accs[u % T::SETS]);
     }
   }
-  double acc[NACC];
+}
+
+template <int KIND>
+__device__ __forceinline__ void pass1_point(const uint32_t* xv, double yv, Pass1State<KIND>& st,
+                                            int set) {
+  constexpr int P = FitTraits<KIND>::P;
+  double v[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    v[k] = u2d(xv[k]);
+    st.mn[k] = min(st.mn[k], xv[k]);
+    st.mx[k] = max(st.mx[k], xv[k]);
+  }
+  FitTraits<KIND>::accumulate(v, yv, st.accs[set]);
+}
+
+// Half-stage pass 1: each thread takes 4 consecutive points with 16-B smem
+// loads when the half is dense and aligned, else the generic strided loop.
+template <int KIND>
+__device__ __forceinline__ void pass1_half(const HalfPoints<FitTraits<KIND>::P>& hp, int cnt,
+                                           Pass1State<KIND>& st) {
+  constexpr int P = FitTraits<KIND>::P, SETS = FitTraits<KIND>::SETS;
+  if (!hp.dense(cnt)) {
+    pass1<KIND>(hp, cnt, st);
+    return;
+  }
+  for (int i4 = 4 * threadIdx.x; i4 < cnt; i4 += 4 * FIT_THREADS) {
+    if (i4 + 4 <= cnt) {
+      uint32_t xv[4][P];
+      double yv[4];
+      hp.load4(i4, xv, yv);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pass1_point<KIND>(xv[u], yv[u], st, u % SETS);
+    } else {
+      for (int i = i4; i < cnt; ++i) {
+        uint32_t xv[P];
+        double yv;
+        hp.load(i, xv, yv);
+        pass1_point<KIND>(xv, yv, st, 0);
+      }
+    }
+  }
+}
+
+// Reduce pass-1 state, solve (warp 0); on return sh.coef/inv/lo/hi are valid
+// for every thread (ends with __syncthreads).
+template <int KIND>
+__device__ void reduce_and_solve(Pass1State<KIND>& st, int64_t n, FitScratch<KIND>& sh) {
+  using T = FitTraits<KIND>;
+  constexpr int P = T::P, NCOL = T::NCOL, NMOM = T::NMOM;
+  constexpr int NACC = (NMOM - 1) + NCOL;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 #pragma unroll
   for (int i = 0; i < NACC; ++i) {
-    acc[i] = accs[0][i];
+    double a = st.accs[0][i];
 #pragma unroll
-    for (int q = 1; q < SETS; ++q) acc[i] += accs[q][i];
-    acc[i] = warp_sum(acc[i]);
+    for (int q = 1; q < T::SETS; ++q) a += st.accs[q][i];
+    a = warp_sum(a);
+    if (lane == 0) sh.part[wid][i] = a;
   }
 #pragma unroll
   for (int k = 0; k < P; ++k) {
-    mn[k] = __reduce_min_sync(0xFFFFFFFFu, mn[k]);
-    mx[k] = __reduce_max_sync(0xFFFFFFFFu, mx[k]);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < NACC; ++i) sh.part[wid][i] = acc[i];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      sh.mn[wid][k] = mn[k];
-      sh.mx[wid][k] = mx[k];
+    const uint32_t a = __reduce_min_sync(0xFFFFFFFFu, st.mn[k]);
+    const uint32_t b = __reduce_max_sync(0xFFFFFFFFu, st.mx[k]);
+    if (lane == 0) {
+      sh.mn[wid][k] = a;
+      sh.mx[wid][k] = b;
     }
   }
   __syncthreads();
-  // ---------------- warp 0: moments -> scaled Gram -> Cholesky solve
   if (wid == 0) {
     if (lane < P) {
       uint32_t a = 0xFFFFFFFFu, b = 0u;
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
+      for (int w = 0; w < FIT_WARPS; ++w) {
         a = min(a, sh.mn[w][lane]);
         b = max(b, sh.mx[w][lane]);
       }
@@ -314,14 +389,14 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
       if (m > 0) {
         raw = 0.0;
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) raw += sh.part[w][m - 1];
+        for (int w = 0; w < FIT_WARPS; ++w) raw += sh.part[w][m - 1];
       }
       sh.msc[m] = raw * scale_of(m);
     }
     if (lane < NCOL) {
       double raw = 0.0;
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) raw += sh.part[w][NMOM - 1 + lane];
+      for (int w = 0; w < FIT_WARPS; ++w) raw += sh.part[w][NMOM - 1 + lane];
       sh.b[lane] = raw * scale_of(sh.colmon[lane]);
     }
     __syncwarp();
@@ -330,14 +405,12 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
 #pragma unroll
     for (int k = 0; k < NCOL; ++k) g[k] = sh.msc[sh.gidx[r][k]];
     const double diag = sh.msc[sh.gidx[r][r]];
-    uint32_t keep = 0;
-    double rd = 0.0;  // lane j: 1 / L[j][j]
+    double rd = 0.0;  // lane j: 1 / L[j][j] (0 for a dropped column)
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) {
       const double piv = __shfl_sync(0xFFFFFFFFu, g[j], j);
       const double dj = __shfl_sync(0xFFFFFFFFu, diag, j);
       const bool kj = piv > DROP_TOL * dj;
-      keep |= (uint32_t)kj << j;
       const double d = kj ? sqrt(piv) : 0.0;
       const double inv_d = kj ? rcp64(d) : 0.0;
       if (lane == j) rd = inv_d;
@@ -354,7 +427,7 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
     double t = lane < NCOL ? sh.b[lane] : 0.0, z = 0.0;
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) {
-      const double zj = __shfl_sync(0xFFFFFFFFu, t * rd, j);  // 0 for dropped columns
+      const double zj = __shfl_sync(0xFFFFFFFFu, t * rd, j);
       if (lane > j) t = fma(-g[j], zj, t);
       if (lane == j) z = zj;
     }
@@ -370,24 +443,22 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
         if (lane == m) u = fma(-ljm, cj, u);
       }
     }
-    (void)keep;
     if (lane < NCOL) sh.coef[lane] = c;
   }
   __syncthreads();
-  // ---------------- pass 2: training MAPE with the final (clamped) predictor
-  double coef[NCOL], inv[P];
+}
+
+template <int KIND, typename Pts>
+__device__ __forceinline__ void pass2(const Pts& pts, int cnt, const double* coef,
+                                      const double* inv, double& err) {
+  constexpr int P = FitTraits<KIND>::P;
+  for (int i0 = threadIdx.x; i0 < cnt; i0 += FIT_THREADS * FIT_UNR) {
+    uint32_t xv[FIT_UNR][P];
+    double yv[FIT_UNR];
 #pragma unroll
-  for (int i = 0; i < NCOL; ++i) coef[i] = sh.coef[i];
-#pragma unroll
-  for (int k = 0; k < P; ++k) inv[k] = sh.inv[k];
-  double err = 0.0;
-  for (int64_t i0 = tid; i0 < n; i0 += NT * UNR) {
-    uint32_t xv[UNR][P];
-    double yv[UNR];
-#pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      const int64_t i = i0 + u * NT;
-      if (i < n) {
+    for (int u = 0; u < FIT_UNR; ++u) {
+      const int i = i0 + u * FIT_THREADS;
+      if (i < cnt) {
         pts.load(i, xv[u], yv[u]);
       } else {
 #pragma unroll
@@ -396,8 +467,8 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
       }
     }
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) {
-      if (i0 + u * NT >= n) break;
+    for (int u = 0; u < FIT_UNR; ++u) {
+      if (i0 + u * FIT_THREADS >= cnt) break;
       double v[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) v[k] = u2d(xv[u][k]);
@@ -405,37 +476,84 @@ __device__ void fit_one(const Pts& pts, int64_t n, int64_t s, FitScratch<KIND>& 
       err = fma(fabs(p - yv[u]), rcp64(yv[u]), err);
     }
   }
+}
+
+template <int KIND>
+__device__ __forceinline__ double mape_term(const uint32_t* xv, double yv, const double* coef,
+                                            const double* inv) {
+  constexpr int P = FitTraits<KIND>::P;
+  double v[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) v[k] = u2d(xv[k]);
+  const double p = fmax(eval_fma<KIND>(coef, inv, v), DOOLY_CLAMP_FLOOR);
+  return fabs(p - yv) * rcp64(yv);
+}
+
+template <int KIND>
+__device__ __forceinline__ void pass2_half(const HalfPoints<FitTraits<KIND>::P>& hp, int cnt,
+                                           const double* coef, const double* inv, double& err) {
+  constexpr int P = FitTraits<KIND>::P;
+  if (!hp.dense(cnt)) {
+    pass2<KIND>(hp, cnt, coef, inv, err);
+    return;
+  }
+  double e2 = 0.0;
+  for (int i4 = 4 * threadIdx.x; i4 < cnt; i4 += 4 * FIT_THREADS) {
+    if (i4 + 4 <= cnt) {
+      uint32_t xv[4][P];
+      double yv[4];
+      hp.load4(i4, xv, yv);
+      err += mape_term<KIND>(xv[0], yv[0], coef, inv);
+      e2 += mape_term<KIND>(xv[1], yv[1], coef, inv);
+      err += mape_term<KIND>(xv[2], yv[2], coef, inv);
+      e2 += mape_term<KIND>(xv[3], yv[3], coef, inv);
+    } else {
+      for (int i = i4; i < cnt; ++i) {
+        uint32_t xv[P];
+        double yv;
+        hp.load(i, xv, yv);
+        err += mape_term<KIND>(xv, yv, coef, inv);
+      }
+    }
+  }
+  err += e2;
+}
+
+// Reduce the MAPE and write the row (ends with __syncthreads).
+template <int KIND>
+__device__ void finish(double err, int64_t n, int64_t s, FitScratch<KIND>& sh, void* table,
+                       double* fit_err, uint8_t* status) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   err = warp_sum(err);
   if (lane == 0) sh.err[wid] = err;
   __syncthreads();
   if (tid == 0) {
     double e = 0.0;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) e += sh.err[w];
+    for (int w = 0; w < FIT_WARPS; ++w) e += sh.err[w];
     fit_err[s] = e / (double)n;
     status[s] = DOOLY_FIT_OK;
     if constexpr (KIND == DOOLY_KIND_AFFINE) {
       dooly_affine_row* row = static_cast<dooly_affine_row*>(table) + s;
-      row->c0 = coef[0];
-      row->c1 = coef[1];
-      row->inv_scale = inv[0];
+      row->c0 = sh.coef[0];
+      row->c1 = sh.coef[1];
+      row->inv_scale = sh.inv[0];
       row->lo = sh.lo[0];
       row->hi = sh.hi[0];
     } else {
       dooly_attn_row* row = static_cast<dooly_attn_row*>(table) + s;
-      for (int i = 0; i < 10; ++i) row->c[i] = coef[i];
+      for (int i = 0; i < 10; ++i) row->c[i] = sh.coef[i];
       for (int k = 0; k < 3; ++k) {
-        row->inv_scale[k] = inv[k];
+        row->inv_scale[k] = sh.inv[k];
         row->lo[k] = sh.lo[k];
         row->hi[k] = sh.hi[k];
       }
     }
   }
-  // the caller's next __syncthreads (or the next signature's first one)
-  // orders these smem reads before any rewrite of sh
+  __syncthreads();
 }
 
-// --------------------------------------------------------------- bulk copies
+// --------------------------------------------------------------- mbarriers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -469,7 +587,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 struct Window {  // aligned bulk window of elements [beg, end) of an array
   int64_t abeg;  // aligned-down first element copied
-  int64_t aend;  // end of the bulk-copied range (aligned)
+  int64_t aend;  // end of the bulk-copied range (aligned, never past the array)
   int head;      // beg - abeg
 };
 
@@ -477,131 +595,152 @@ __device__ __forceinline__ Window make_window(int64_t beg, int64_t end, int64_t 
                                               int per16) {
   Window w;
   w.abeg = beg / per16 * per16;
-  int64_t e = (end + per16 - 1) / per16 * per16;
-  const int64_t cap = n_total / per16 * per16;  // never read past the array
+  const int64_t e = (end + per16 - 1) / per16 * per16;
+  const int64_t cap = n_total / per16 * per16;
   w.aend = e < cap ? e : cap;
   if (w.aend < w.abeg) w.aend = w.abeg;
   w.head = (int)(beg - w.abeg);
   return w;
 }
 
-// Issue the bulk copies of one signature into a stage; the (<4) tail elements
-// past the last aligned chunk of the arrays are loaded by the consumers.
+// Issue points [c0, c1) into one half stage (thread 0).
 template <int KIND>
-__device__ void issue_stage(unsigned char* stage, uint64_t* bar, const uint32_t* x, int64_t n_pts,
-                            const double* y, int64_t beg, int64_t end) {
-  using S = Stage<KIND>;
-  const Window wy = make_window(beg, end, n_pts, 2);
-  const Window wx = make_window(beg, end, n_pts, 4);
+__device__ void issue_half(unsigned char* half, uint64_t* bar, const uint32_t* x, int64_t n_pts,
+                           const double* y, int64_t c0, int64_t c1) {
+  using H = Half<KIND>;
+  const Window wy = make_window(c0, c1, n_pts, 2);
+  const Window wx = make_window(c0, c1, n_pts, 4);
   const uint32_t by = (uint32_t)((wy.aend - wy.abeg) * 8);
   const uint32_t bx = (uint32_t)((wx.aend - wx.abeg) * 4);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_expect_tx(bar, by + S::P * bx);
-  double* sy = reinterpret_cast<double*>(stage);
-  uint32_t* sx = reinterpret_cast<uint32_t*>(stage + (size_t)S::Y_LEN * 8);
-  if (by) bulk_g2s(sy, y + wy.abeg, by, bar);
-  if (bx)
-    for (int k = 0; k < S::P; ++k) bulk_g2s(sx + k * S::X_LEN, x + k * n_pts + wx.abeg, bx, bar);
+  mbar_expect_tx(bar, by + H::P * bx);
+  if (by) bulk_g2s(half, y + wy.abeg, by, bar);
+  if (bx) {
+    uint32_t* sx = reinterpret_cast<uint32_t*>(half + (size_t)H::Y_LEN * 8);
+    for (int k = 0; k < H::P; ++k) bulk_g2s(sx + k * H::X_LEN, x + k * n_pts + wx.abeg, bx, bar);
+  }
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(FitTraits<KIND>::THREADS, FIT_CTAS_PER_SM) fit_bulk_kernel(
+__device__ __forceinline__ HalfPoints<FitTraits<KIND>::P> half_points(
+    unsigned char* half, const uint32_t* x, int64_t n_pts, const double* y, int64_t c0,
+    int64_t c1) {
+  using H = Half<KIND>;
+  const Window wy = make_window(c0, c1, n_pts, 2);
+  const Window wx = make_window(c0, c1, n_pts, 4);
+  return HalfPoints<FitTraits<KIND>::P>{
+      reinterpret_cast<const uint32_t*>(half + (size_t)H::Y_LEN * 8), H::X_LEN, wx.head,
+      (int)(wx.aend - c0), reinterpret_cast<const double*>(half), wy.head, (int)(wy.aend - c0),
+      GlobalPoints<FitTraits<KIND>::P>{x, n_pts, y, c0}};
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(FIT_THREADS) fit_stage_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y,
     const int64_t* __restrict__ off, int64_t n_sig, void* __restrict__ table,
-    double* __restrict__ fit_err, uint8_t* __restrict__ status, bool bulk_ok, int nst) {
+    double* __restrict__ fit_err, uint8_t* __restrict__ status, bool bulk_ok) {
   using T = FitTraits<KIND>;
-  using S = Stage<KIND>;
-  const int NST = nst;  // 1..4 stages (runtime: tuned per kind at launch)
+  using H = Half<KIND>;
   extern __shared__ __align__(128) unsigned char dyn[];
-  __shared__ __align__(8) uint64_t bars[4];
+  __shared__ __align__(8) uint64_t bar[2];
   __shared__ FitScratch<KIND> sh;
   const int tid = threadIdx.x;
+  unsigned char* const half0 = dyn;
+  unsigned char* const half1 = dyn + H::STRIDE;
 
-  // signatures of this CTA: s_k = blockIdx.x + k * gridDim.x
   auto sig_of = [&](int64_t k) { return (int64_t)blockIdx.x + k * (int64_t)gridDim.x; };
-  auto stageable = [&](int64_t s) {
-    const int64_t n = off[s + 1] - off[s];
-    return bulk_ok && n >= T::NEED && n <= FIT_CAP;
+  auto staged = [&](int64_t b, int64_t e) {
+    return bulk_ok && e - b >= T::NEED && e - b <= 2 * FIT_HALF;
   };
+  auto split = [](int64_t b, int64_t e) { return e - b < FIT_HALF ? e - b : (int64_t)FIT_HALF; };
+
   init_tables<KIND>(sh);
   if (tid == 0) {
-    for (int i = 0; i < NST; ++i) mbar_init(&bars[i], 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int k = 0; k < NST - 1; ++k) {
-      const int64_t s = sig_of(k);
-      if (s < n_sig && stageable(s))
-        issue_stage<KIND>(dyn + (size_t)k * S::STRIDE, &bars[k], x, n_pts, y, off[s], off[s + 1]);
-    }
-  }
-  // CSR offsets are software-pipelined two signatures ahead so their global
-  // load latency never sits on the critical path (ncu: the refill's dependent
-  // off[] loads were stalling the whole CTA at the next barrier).
+
+  // CSR offsets software-pipelined two signatures ahead (all threads)
   auto load_off = [&](int64_t kk, int64_t& b, int64_t& e) {
     const int64_t ss = sig_of(kk);
     b = ss < n_sig ? __ldg(off + ss) : 0;
     e = ss < n_sig ? __ldg(off + ss + 1) : 0;
   };
-  int64_t ob[4], oe[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) load_off(i, ob[i], oe[i]);
-  auto stageable_be = [&](int64_t b, int64_t e) {
-    return bulk_ok && e - b >= T::NEED && e - b <= FIT_CAP;
-  };
-  uint32_t phase_bits = 0;  // per-stage parity
+  int64_t cb, ce, nb, ne, nnb, nne;
+  load_off(0, cb, ce);
+  load_off(1, nb, ne);
+  load_off(2, nnb, nne);
+  // producer (thread 0): the first signature's halves
+  if (tid == 0 && sig_of(0) < n_sig && staged(cb, ce)) {
+    const int64_t pa = split(cb, ce);
+    issue_half<KIND>(half0, &bar[0], x, n_pts, y, cb, cb + pa);
+    if (ce - cb > pa) issue_half<KIND>(half1, &bar[1], x, n_pts, y, cb + pa, ce);
+  }
+  uint32_t par0 = 0u, par1 = 0u;
+  Pass1State<KIND> st;
   for (int64_t k = 0;; ++k) {
     const int64_t s = sig_of(k);
     if (s >= n_sig) break;
-    const int64_t beg = ob[0], end = oe[0], n = end - beg;
-    // keep STAGES-1 signatures ahead: refill the stage freed by signature k-1
-    if (tid == 0) {
-      const int64_t kn = k + NST - 1;
-      const int64_t sn = sig_of(kn);
-      const int64_t nb = NST == 1 ? ob[0] : NST == 2 ? ob[1] : NST == 3 ? ob[2] : ob[3];
-      const int64_t ne = NST == 1 ? oe[0] : NST == 2 ? oe[1] : NST == 3 ? oe[2] : oe[3];
-      if (sn < n_sig && stageable_be(nb, ne)) {
-        const int st = (int)(kn % NST);
-        issue_stage<KIND>(dyn + (size_t)st * S::STRIDE, &bars[st], x, n_pts, y, nb, ne);
+    const int64_t beg = cb, end = ce, n = end - beg;
+    const int64_t nbeg = nb, nend = ne;
+    const bool next_staged = sig_of(k + 1) < n_sig && staged(nbeg, nend);
+    const int64_t npa = next_staged ? split(nbeg, nend) : 0;
+    cb = nb;
+    ce = ne;
+    nb = nnb;
+    ne = nne;
+    load_off(k + 3, nnb, nne);
+
+    if (!staged(beg, end)) {
+      // halves unused by this signature: start the next one's loads right away
+      if (tid == 0 && next_staged) {
+        issue_half<KIND>(half0, &bar[0], x, n_pts, y, nbeg, nbeg + npa);
+        if (nend - nbeg > npa) issue_half<KIND>(half1, &bar[1], x, n_pts, y, nbeg + npa, nend);
       }
-    }
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      ob[i] = ob[i + 1];
-      oe[i] = oe[i + 1];
-    }
-    load_off(k + 4, ob[3], oe[3]);
-    if (n < T::NEED) {
-      if (tid == 0) write_unfitted<KIND>(table, s, fit_err, status);
-      continue;  // no stage was used (stageable() is false)
-    }
-    if (!stageable_be(beg, end)) {  // oversized / unaligned inputs: stream from global memory
-      GlobalPoints<T::P> gp{x, n_pts, y, beg};
-      fit_one<KIND>(gp, n, s, sh, table, fit_err, status);
-      __syncthreads();
+      if (n < T::NEED) {
+        if (tid == 0) write_unfitted<KIND>(table, s, fit_err, status);
+        continue;
+      }
+      st.reset();  // oversized / unaligned: direct global path
+      const GlobalPoints<T::P> gp{x, n_pts, y, beg};
+      pass1<KIND>(gp, (int)n, st);
+      reduce_and_solve<KIND>(st, n, sh);
+      double err = 0.0;
+      pass2<KIND>(gp, (int)n, sh.coef, sh.inv, err);
+      finish<KIND>(err, n, s, sh, table, fit_err, status);
       continue;
     }
-    const int st = (int)(k % NST);
-    unsigned char* stage = dyn + (size_t)st * S::STRIDE;
-    mbar_wait(&bars[st], (phase_bits >> st) & 1u);
-    phase_bits ^= 1u << st;
-    const Window wy = make_window(beg, end, n_pts, 2);
-    const Window wx = make_window(beg, end, n_pts, 4);
-    double* sy = reinterpret_cast<double*>(stage);
-    uint32_t* sx = reinterpret_cast<uint32_t*>(stage + (size_t)S::Y_LEN * 8);
-    // tail elements past the last aligned chunk of the arrays (end of the data only)
-    if (tid < 4) {
-      const int64_t j = wx.aend + tid;
-      if (j < end)
-        for (int kk = 0; kk < T::P; ++kk) sx[kk * S::X_LEN + (j - wx.abeg)] = x[kk * n_pts + j];
-      const int64_t jy = wy.aend + tid;
-      if (jy < end) sy[jy - wy.abeg] = y[jy];
+    const int64_t pa = split(beg, end);
+    const bool has_b = n > pa;
+    const auto ha = half_points<KIND>(half0, x, n_pts, y, beg, beg + pa);
+    const auto hb = half_points<KIND>(half1, x, n_pts, y, beg + pa, end);
+    // ---- pass 1, half by half as they land
+    st.reset();
+    mbar_wait(&bar[0], par0);
+    par0 ^= 1u;
+    pass1_half<KIND>(ha, (int)pa, st);
+    if (has_b) {
+      mbar_wait(&bar[1], par1);
+      par1 ^= 1u;
+      pass1_half<KIND>(hb, (int)(n - pa), st);
     }
-    __syncthreads();
-    SmemPoints<T::P> sp{sx, S::X_LEN, wx.head, sy, wy.head};
-    fit_one<KIND>(sp, n, s, sh, table, fit_err, status);
-    __syncthreads();  // stage and scratch free for reuse
+    reduce_and_solve<KIND>(st, n, sh);
+    double coef[T::NCOL], inv[T::P];
+#pragma unroll
+    for (int i = 0; i < T::NCOL; ++i) coef[i] = sh.coef[i];
+#pragma unroll
+    for (int kk = 0; kk < T::P; ++kk) inv[kk] = sh.inv[kk];
+    // ---- pass 2; each half is refilled with the next signature once released
+    double err = 0.0;
+    pass2_half<KIND>(ha, (int)pa, coef, inv, err);
+    __syncthreads();  // half 0 free
+    if (tid == 0 && next_staged) issue_half<KIND>(half0, &bar[0], x, n_pts, y, nbeg, nbeg + npa);
+    if (has_b) pass2_half<KIND>(hb, (int)(n - pa), coef, inv, err);
+    finish<KIND>(err, n, s, sh, table, fit_err, status);  // ends with __syncthreads: half 1 free
+    if (tid == 0 && next_staged && nend - nbeg > npa)
+      issue_half<KIND>(half1, &bar[1], x, n_pts, y, nbeg + npa, nend);
   }
 }
 
@@ -609,26 +748,20 @@ template <int KIND>
 static cudaError_t launch_kind(const uint32_t* x, int64_t n_pts, const double* y,
                                const int64_t* off, int64_t n_sig, void* table, double* fit_err,
                                uint8_t* status, cudaStream_t stream, int n_sm) {
-  int nst = FitTraits<KIND>::STAGES;
-  if (const char* env = getenv(KIND == DOOLY_KIND_AFFINE ? "DOOLY_FIT_STAGES_AFFINE"
-                                                         : "DOOLY_FIT_STAGES_ATTN")) {
-    const int v = atoi(env);  // tuning knob (profiles/); 1..4
-    if (v >= 1 && v <= 4) nst = v;
-  }
-  const size_t smem = (size_t)nst * Stage<KIND>::STRIDE;
-  cudaError_t e = cudaFuncSetAttribute(fit_bulk_kernel<KIND>,
+  const size_t smem = Half<KIND>::STAGE_BYTES;
+  cudaError_t e = cudaFuncSetAttribute(fit_stage_kernel<KIND>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // 1-D TMA needs 16-B aligned sources: plane bases and the y array
   const bool bulk_ok = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) &&
                        (FitTraits<KIND>::P == 1 || n_pts % 4 == 0);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_bulk_kernel<KIND>,
-                                                FitTraits<KIND>::THREADS, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_stage_kernel<KIND>, FIT_THREADS,
+                                                smem);
   int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
   if (blocks > n_sig) blocks = n_sig;
-  fit_bulk_kernel<KIND><<<(unsigned)blocks, FitTraits<KIND>::THREADS, smem, stream>>>(
-      x, n_pts, y, off, n_sig, table, fit_err, status, bulk_ok, nst);
+  fit_stage_kernel<KIND><<<(unsigned)blocks, FIT_THREADS, smem, stream>>>(
+      x, n_pts, y, off, n_sig, table, fit_err, status, bulk_ok);
   return cudaGetLastError();
 }
 
