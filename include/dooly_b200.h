@@ -120,10 +120,13 @@ int dooly_dedup_digests(dooly_ctx* ctx, const uint8_t* digests, int64_t n,
  * Replaces fit.  Points of signature s are
  * [pt_off[s], pt_off[s+1]); x is feature-major (kind==ATTN: 3 planes of n_pts
  * u32, AFFINE: 1 plane), y is latency in seconds.  Writes one table row, the
- * training MAPE and a status per signature. */
+ * training MAPE and a status per signature.  The attention kind uses a
+ * moments workspace of dooly_fit_workspace_size(kind, n_sig) bytes (device,
+ * 256-B aligned); passing NULL selects the fused single-kernel path. */
+size_t dooly_fit_workspace_size(int kind, int64_t n_sig);
 int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
               const int64_t* pt_off, int64_t n_sig, void* table, double* fit_err,
-              uint8_t* status, void* stream);
+              uint8_t* status, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K3 predict
  * Replaces predict.  sig[i] indexes the table; x is

@@ -68,7 +68,9 @@ _SIGS = {
     "dooly_dedup_workspace_size": (C.c_size_t, [_I64, _I64]),
     "dooly_dedup_digests": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P,
                                       C.c_size_t, _P]),
-    "dooly_fit": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
+    "dooly_fit_workspace_size": (C.c_size_t, [C.c_int, _I64]),
+    "dooly_fit": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, C.c_size_t,
+                            _P]),
     "dooly_predict": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
     "dooly_iter_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _I64, _P, _P,
                                   _P]),

@@ -14,7 +14,9 @@ cudaError_t launch_predict(int kind, const void* table, int64_t n_sig, const uin
                            int64_t* err_first, cudaStream_t stream, int n_sm);
 cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double* y,
                        const int64_t* off, int64_t n_sig, void* table, double* fit_err,
-                       uint8_t* status, cudaStream_t stream, int n_sm);
+                       uint8_t* status, void* ws, cudaStream_t stream, int n_sm,
+                       int64_t* launches);
+size_t fit_workspace_size(int kind, int64_t n_sig);
 cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off, int64_t n,
                                   const uint8_t* op_bytes, const int64_t* op_off,
                                   const uint8_t* sym_bytes, const int64_t* sym_off,
@@ -118,20 +120,27 @@ int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
                     "predict");
 }
 
+size_t dooly_fit_workspace_size(int kind, int64_t n_sig) {
+  return dooly::fit_workspace_size(kind, n_sig);
+}
+
 int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
               const int64_t* pt_off, int64_t n_sig, void* table, double* fit_err,
-              uint8_t* status, void* stream) {
+              uint8_t* status, void* workspace, size_t workspace_bytes, void* stream) {
   if (!ctx) return DOOLY_ERR_INVALID_ARG;
   if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit: unknown kind");
   if (n_sig < 0 || n_pts < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit: negative size");
   if (n_sig > 0 && (!pt_off || !table || !fit_err || !status || (n_pts > 0 && (!x || !y))))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit: null pointer");
+  if (workspace != nullptr &&
+      (workspace_bytes < dooly::fit_workspace_size(kind, n_sig) || (uintptr_t)workspace % 256))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit: workspace too small or misaligned");
   DeviceGuard g(ctx->device);
-  if (n_sig > 0) ctx->launches += 1;
   return check_cuda(ctx,
                     dooly::launch_fit(kind, x, n_pts, y, pt_off, n_sig, table, fit_err, status,
-                                      (cudaStream_t)stream, ctx->n_sm),
+                                      workspace, (cudaStream_t)stream, ctx->n_sm,
+                                      &ctx->launches),
                     "fit");
 }
 

@@ -765,15 +765,383 @@ static cudaError_t launch_kind(const uint32_t* x, int64_t n_pts, const double* y
   return cudaGetLastError();
 }
 
+// ====================================================================
+// Attention (10-column) path: three kernels.
+//
+// ncu showed the fused stage kernel spending ~a third of its warp time in the
+// per-signature serial phase (the 10x10 solve on warp 0 while three warps wait
+// at the barrier) and FP64 pipes only ~40% busy.  For the FP64-bound attention
+// kind the solve is therefore taken off the streaming path:
+//   A  fit_moments_attn: one WARP per signature streams its points once
+//      (16-B vector loads, two blocks in flight per lane), accumulates the 44
+//      raw moments + box, butterfly-reduces in registers (no CTA barrier) and
+//      stores them moment-major to a workspace (352 B + 24 B per signature);
+//   B  fit_solve_attn: one THREAD per signature scales the moments, builds the
+//      10x10 Gram, Cholesky-with-drop + substitution in registers, writes the
+//      row (0.5M independent solves: latency fully hidden by parallelism);
+//   C  fit_mape_attn: one warp per signature re-streams the points with the
+//      final row for the training MAPE.
+// Points cross HBM twice (40 B/point instead of 20) but both streaming kernels
+// run at the FP64 or HBM roofline instead of stalling on a serial solve.
+// ====================================================================
+constexpr int ATTN_NACC = 44;  // 34 moments (degree 1..4) + 10 X^T y sums
+constexpr int FA_THREADS = 128;
+
+struct AttnPoints4 {  // 4 consecutive points
+  uint32_t x[4][3];
+  double y[4];
+};
+
+__device__ __forceinline__ void ld_points4(const uint32_t* x, int64_t n_pts, const double* y,
+                                           int64_t i, AttnPoints4& p) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const uint4 v = ld_stream_u4(x + k * n_pts + i);
+    p.x[0][k] = v.x;
+    p.x[1][k] = v.y;
+    p.x[2][k] = v.z;
+    p.x[3][k] = v.w;
+  }
+  const uint4 a = ld_stream_u4(y + i);
+  const uint4 b = ld_stream_u4(y + i + 2);
+  p.y[0] = __hiloint2double((int)a.y, (int)a.x);
+  p.y[1] = __hiloint2double((int)a.w, (int)a.z);
+  p.y[2] = __hiloint2double((int)b.y, (int)b.x);
+  p.y[3] = __hiloint2double((int)b.w, (int)b.z);
+}
+
+__device__ __forceinline__ void attn_point(const uint32_t* xv, double yv, double* acc,
+                                           uint32_t* mn, uint32_t* mx) {
+  double v[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    v[k] = u2d(xv[k]);
+    mn[k] = min(mn[k], xv[k]);
+    mx[k] = max(mx[k], xv[k]);
+  }
+  attn_accumulate(v[0], v[1], v[2], yv, acc);
+}
+
+// Visit every point of [beg, end) once per lane-strided schedule; `vec` selects
+// 16-B vector loads (4 points per lane per block of 128).
+template <typename F4, typename F1>
+__device__ __forceinline__ void warp_stream_points(const uint32_t* x, int64_t n_pts,
+                                                   const double* y, int64_t beg, int64_t n,
+                                                   bool vec, F4&& f4, F1&& f1) {
+  const int lane = threadIdx.x & 31;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t full = n / 128 * 128;
+    int64_t i = 0;
+    for (; i + 256 <= full; i += 256) {  // two blocks of loads in flight per lane
+      AttnPoints4 p0, p1;
+      ld_points4(x, n_pts, y, beg + i + 4 * lane, p0);
+      ld_points4(x, n_pts, y, beg + i + 128 + 4 * lane, p1);
+      f4(p0);
+      f4(p1);
+    }
+    for (; i < full; i += 128) {
+      AttnPoints4 p0;
+      ld_points4(x, n_pts, y, beg + i + 4 * lane, p0);
+      f4(p0);
+    }
+    done = full;
+  }
+  for (int64_t i = done + lane; i < n; i += 32) {
+    uint32_t xv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) xv[k] = __ldg(x + k * n_pts + beg + i);
+    f1(xv, __ldg(y + beg + i));
+  }
+}
+
+// Per-lane cp.async pipeline: each lane copies exactly the 16-B pieces it
+// later consumes (3 x-plane chunks + 2 y chunks per 128-point block), so the
+// ring needs no cross-lane synchronisation, only cp.async.wait_group; D blocks
+// are in flight per warp without holding any registers.
+constexpr int FA_DEPTH = 4;                      // blocks in flight per warp
+constexpr int FA_BLOCK_BYTES = 3 * 128 * 4 + 128 * 8;  // 2560 B per 128-point block
+constexpr size_t FA_SMEM = (size_t)(FA_THREADS / 32) * FA_DEPTH * FA_BLOCK_BYTES;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename F4, typename F1>
+__device__ __forceinline__ void warp_stream_points_async(unsigned char* ring, const uint32_t* x,
+                                                         int64_t n_pts, const double* y,
+                                                         int64_t beg, int64_t n, bool vec,
+                                                         F4&& f4, F1&& f1) {
+  const int lane = threadIdx.x & 31;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nb = n / 128;
+    auto issue = [&](int64_t b) {
+      unsigned char* st = ring + (size_t)(b % FA_DEPTH) * FA_BLOCK_BYTES;
+      const int64_t i = beg + b * 128 + 4 * lane;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cp_async16(st + k * 512 + 16 * lane, x + k * n_pts + i);
+      cp_async16(st + 1536 + 32 * lane, y + i);
+      cp_async16(st + 1536 + 32 * lane + 16, y + i + 2);
+    };
+#pragma unroll
+    for (int d = 0; d < FA_DEPTH - 1; ++d) {
+      if (d < nb) issue(d);
+      cp_async_commit();
+    }
+    for (int64_t b = 0; b < nb; ++b) {
+      if (b + FA_DEPTH - 1 < nb) issue(b + FA_DEPTH - 1);
+      cp_async_commit();
+      cp_async_wait<FA_DEPTH - 1>();
+      const unsigned char* st = ring + (size_t)(b % FA_DEPTH) * FA_BLOCK_BYTES;
+      AttnPoints4 p;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const uint4 v = *reinterpret_cast<const uint4*>(st + k * 512 + 16 * lane);
+        p.x[0][k] = v.x;
+        p.x[1][k] = v.y;
+        p.x[2][k] = v.z;
+        p.x[3][k] = v.w;
+      }
+      const double2 a = *reinterpret_cast<const double2*>(st + 1536 + 32 * lane);
+      const double2 c = *reinterpret_cast<const double2*>(st + 1536 + 32 * lane + 16);
+      p.y[0] = a.x;
+      p.y[1] = a.y;
+      p.y[2] = c.x;
+      p.y[3] = c.y;
+      f4(p);
+    }
+    cp_async_wait<0>();
+    done = nb * 128;
+  }
+  for (int64_t i = done + lane; i < n; i += 32) {
+    uint32_t xv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) xv[k] = __ldg(x + k * n_pts + beg + i);
+    f1(xv, __ldg(y + beg + i));
+  }
+}
+
+__global__ void __launch_bounds__(FA_THREADS) fit_moments_attn_kernel(
+    const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y,
+    const int64_t* __restrict__ off, int64_t n_sig, double* __restrict__ mom,
+    uint32_t* __restrict__ box, bool vec_ok) {
+  extern __shared__ __align__(16) unsigned char fa_dyn[];
+  unsigned char* ring = fa_dyn + (size_t)(threadIdx.x >> 5) * FA_DEPTH * FA_BLOCK_BYTES;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < n_sig; s += n_warps) {
+    const int64_t beg = __ldg(off + s), n = __ldg(off + s + 1) - beg;
+    if (n < FitTraits<DOOLY_KIND_ATTN>::NEED) continue;  // the solve kernel marks it
+    double acc[ATTN_NACC];
+#pragma unroll
+    for (int i = 0; i < ATTN_NACC; ++i) acc[i] = 0.0;
+    uint32_t mn[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, mx[3] = {0u, 0u, 0u};
+    warp_stream_points_async(
+        ring, x, n_pts, y, beg, n, vec_ok && (beg % 4 == 0),
+        [&](const AttnPoints4& p) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) attn_point(p.x[u], p.y[u], acc, mn, mx);
+        },
+        [&](const uint32_t* xv, double yv) { attn_point(xv, yv, acc, mn, mx); });
+#pragma unroll
+    for (int i = 0; i < ATTN_NACC; ++i) acc[i] = warp_sum(acc[i]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = __reduce_min_sync(0xFFFFFFFFu, mn[k]);
+      mx[k] = __reduce_max_sync(0xFFFFFFFFu, mx[k]);
+    }
+    // moment-major stores, spread over lanes (every lane holds every sum)
+#pragma unroll
+    for (int i = 0; i < ATTN_NACC; ++i)
+      if (lane == (i & 31)) mom[(int64_t)i * n_sig + s] = acc[i];
+    if (lane < 3) {
+      box[(int64_t)lane * n_sig + s] = lane == 0 ? mn[0] : lane == 1 ? mn[1] : mn[2];
+      box[(int64_t)(3 + lane) * n_sig + s] = lane == 0 ? mx[0] : lane == 1 ? mx[1] : mx[2];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) fit_solve_attn_kernel(
+    const int64_t* __restrict__ off, int64_t n_sig, const double* __restrict__ mom,
+    const uint32_t* __restrict__ box, dooly_attn_row* __restrict__ table,
+    double* __restrict__ fit_err, uint8_t* __restrict__ status) {
+  constexpr int NC = 10;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_sig;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = __ldg(off + s + 1) - __ldg(off + s);
+    if (n < FitTraits<DOOLY_KIND_ATTN>::NEED) {
+      write_unfitted<DOOLY_KIND_ATTN>(table, s, fit_err, status);
+      continue;
+    }
+    uint32_t lo[3], hi[3];
+    double inv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = __ldg(box + (int64_t)k * n_sig + s);
+      hi[k] = __ldg(box + (int64_t)(3 + k) * n_sig + s);
+      inv[k] = hi[k] > 0 ? 1.0 / (double)hi[k] : 1.0;  // IEEE division (oracle parity)
+    }
+    // scaled moment m: raw * prod inv^e (m = 0 is the point count)
+    auto msc = [&](int m) {
+      double v = m == 0 ? (double)n : __ldg(mom + (int64_t)(m - 1) * n_sig + s);
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        for (int r = 0; r < kAttnExp[m][k]; ++r) v *= inv[k];
+      return v;
+    };
+    double L[NC][NC];  // lower triangle used
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j) L[i][j] = msc(kAttnGidx[i][j]);
+    double b[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      double v = __ldg(mom + (int64_t)(34 + i) * n_sig + s);
+      const int m = kAttnColmon[i];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        for (int r = 0; r < kAttnExp[m][k]; ++r) v *= inv[k];
+      b[i] = v;
+    }
+    // Cholesky with drop (same rule as the oracle): L overwrites G
+    double rd[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const double gjj = L[j][j];
+      double d2 = gjj;
+#pragma unroll
+      for (int k = 0; k < j; ++k) d2 = fma(-L[j][k], L[j][k], d2);
+      const bool keep = d2 > DROP_TOL * gjj;
+      const double d = keep ? sqrt(d2) : 0.0;
+      rd[j] = keep ? rcp64(d) : 0.0;
+      L[j][j] = d;
+#pragma unroll
+      for (int i = j + 1; i < NC; ++i) {
+        double t = L[i][j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) t = fma(-L[i][k], L[j][k], t);
+        L[i][j] = t * rd[j];
+      }
+    }
+    double z[NC], c[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      double t = b[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t = fma(-L[j][k], z[k], t);
+      z[j] = t * rd[j];
+    }
+#pragma unroll
+    for (int j = NC - 1; j >= 0; --j) {
+      double t = z[j];
+#pragma unroll
+      for (int k = j + 1; k < NC; ++k) t = fma(-L[k][j], c[k], t);
+      c[j] = t * rd[j];
+    }
+    dooly_attn_row* row = table + s;
+#pragma unroll
+    for (int i = 0; i < NC; ++i) row->c[i] = c[i];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      row->inv_scale[k] = inv[k];
+      row->lo[k] = lo[k];
+      row->hi[k] = hi[k];
+    }
+    status[s] = DOOLY_FIT_OK;
+  }
+}
+
+__global__ void __launch_bounds__(FA_THREADS) fit_mape_attn_kernel(
+    const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y,
+    const int64_t* __restrict__ off, int64_t n_sig, const dooly_attn_row* __restrict__ table,
+    double* __restrict__ fit_err, bool vec_ok) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < n_sig; s += n_warps) {
+    const int64_t beg = __ldg(off + s), n = __ldg(off + s + 1) - beg;
+    if (n < FitTraits<DOOLY_KIND_ATTN>::NEED) continue;
+    const AttnRow r = load_attn(table, (uint32_t)s);
+    double e0 = 0.0, e1 = 0.0;
+    auto term = [&](const uint32_t* xv, double yv) {
+      double v[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) v[k] = u2d(xv[k]);
+      const double p = fmax(eval_fma<DOOLY_KIND_ATTN>(r.c, r.inv, v), DOOLY_CLAMP_FLOOR);
+      return fabs(p - yv) * rcp64(yv);
+    };
+    warp_stream_points(
+        x, n_pts, y, beg, n, vec_ok && (beg % 4 == 0),
+        [&](const AttnPoints4& p) {
+          e0 += term(p.x[0], p.y[0]);
+          e1 += term(p.x[1], p.y[1]);
+          e0 += term(p.x[2], p.y[2]);
+          e1 += term(p.x[3], p.y[3]);
+        },
+        [&](const uint32_t* xv, double yv) { e0 += term(xv, yv); });
+    const double e = warp_sum(e0 + e1);
+    if (lane == 0) fit_err[s] = e / (double)n;
+  }
+}
+
+size_t fit_workspace_size(int kind, int64_t n_sig) {
+  if (kind != DOOLY_KIND_ATTN) return 0;
+  return (size_t)n_sig * (ATTN_NACC * 8 + 6 * 4) + 256;
+}
+
+static cudaError_t launch_attn(const uint32_t* x, int64_t n_pts, const double* y,
+                               const int64_t* off, int64_t n_sig, void* table, double* fit_err,
+                               uint8_t* status, void* ws, cudaStream_t stream, int n_sm) {
+  double* mom = static_cast<double*>(ws);
+  uint32_t* box = reinterpret_cast<uint32_t*>(mom + (size_t)ATTN_NACC * n_sig);
+  const bool vec_ok = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && (n_pts % 4 == 0);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_moments_attn_kernel, FA_THREADS,
+                                                FA_SMEM);
+  int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+  const int64_t need = (n_sig + FA_THREADS / 32 - 1) / (FA_THREADS / 32);
+  if (blocks > need) blocks = need;
+  fit_moments_attn_kernel<<<(unsigned)blocks, FA_THREADS, FA_SMEM, stream>>>(
+      x, n_pts, y, off, n_sig, mom, box, vec_ok);
+  int64_t sb = (n_sig + 127) / 128;
+  fit_solve_attn_kernel<<<(unsigned)sb, 128, 0, stream>>>(
+      off, n_sig, mom, box, static_cast<dooly_attn_row*>(table), fit_err, status);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_mape_attn_kernel, FA_THREADS, 0);
+  blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+  if (blocks > need) blocks = need;
+  fit_mape_attn_kernel<<<(unsigned)blocks, FA_THREADS, 0, stream>>>(
+      x, n_pts, y, off, n_sig, static_cast<const dooly_attn_row*>(table), fit_err, vec_ok);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double* y,
                        const int64_t* off, int64_t n_sig, void* table, double* fit_err,
-                       uint8_t* status, cudaStream_t stream, int n_sm) {
+                       uint8_t* status, void* ws, cudaStream_t stream, int n_sm,
+                       int64_t* launches) {
   if (n_sig == 0) return cudaSuccess;
-  if (kind == DOOLY_KIND_AFFINE)
+  if (kind == DOOLY_KIND_AFFINE) {
+    *launches += 1;
     return launch_kind<DOOLY_KIND_AFFINE>(x, n_pts, y, off, n_sig, table, fit_err, status,
                                           stream, n_sm);
-  return launch_kind<DOOLY_KIND_ATTN>(x, n_pts, y, off, n_sig, table, fit_err, status, stream,
-                                      n_sm);
+  }
+  if (ws == nullptr) {  // no workspace: fused single-kernel path
+    *launches += 1;
+    return launch_kind<DOOLY_KIND_ATTN>(x, n_pts, y, off, n_sig, table, fit_err, status, stream,
+                                        n_sm);
+  }
+  *launches += 3;
+  return launch_attn(x, n_pts, y, off, n_sig, table, fit_err, status, ws, stream, n_sm);
 }
 
 }  // namespace dooly

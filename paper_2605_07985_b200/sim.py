@@ -53,13 +53,28 @@ class FitResult:
         return self.table.cpu().numpy().view(ROW_DTYPE[self.kind]).reshape(-1)
 
 
+_FIT_WS: dict = {}
+
+
+def _fit_workspace(kind: int, n_sig: int, device) -> torch.Tensor:
+    """Cached device scratch for the attention fit's moment buffers."""
+    need = int(_lib.load_library().dooly_fit_workspace_size(kind, n_sig))
+    key = (str(device), kind)
+    buf = _FIT_WS.get(key)
+    if buf is None or buf.numel() < need:
+        buf = torch.empty(max(need, 256), dtype=torch.uint8, device=device)
+        _FIT_WS[key] = buf
+    return buf
+
+
 def fit_tables(kind: int, x: torch.Tensor, y: torch.Tensor, pt_off: torch.Tensor,
-               out: Optional[FitResult] = None) -> FitResult:
+               out: Optional[FitResult] = None, fused: bool = False) -> FitResult:
     """Batch fit (K2) of n_sig signatures whose points are CSR-ranged by pt_off.
 
     x: (P, n_pts) int32/uint32 device tensor (P = 1 affine, 3 attention),
     y: (n_pts,) f64, pt_off: (n_sig + 1,) i64.  Asynchronous; no exceptions
-    for per-signature shortfalls (see ``status``)."""
+    for per-signature shortfalls (see ``status``).  ``fused`` forces the
+    single-kernel attention path (no workspace)."""
     dev = y.device
     n_sig = pt_off.numel() - 1
     n_pts = y.numel()
@@ -70,11 +85,12 @@ def fit_tables(kind: int, x: torch.Tensor, y: torch.Tensor, pt_off: torch.Tensor
                                           device=dev),
                         torch.empty(n_sig, dtype=torch.float64, device=dev),
                         torch.empty(n_sig, dtype=torch.uint8, device=dev))
+    ws = None if (fused or kind == _lib.KIND_AFFINE) else _fit_workspace(kind, n_sig, dev)
     ctx = _lib.ctx_for(dev)
     _lib.check(_lib.load_library().dooly_fit(
         ctx, kind, x.data_ptr(), n_pts, y.data_ptr(), pt_off.data_ptr(), n_sig,
         out.table.data_ptr(), out.fit_err.data_ptr(), out.status.data_ptr(),
-        _lib.stream_ptr(dev)), ctx)
+        _lib.ptr(ws), 0 if ws is None else ws.numel(), _lib.stream_ptr(dev)), ctx)
     return out
 
 
