@@ -1,0 +1,156 @@
+"""End-to-end GPU pipeline vs the CPU oracle on the BASELINE.json configs that
+run on the reference CPU path (C1, C2, C3): dedup -> sweep -> fit -> call graph ->
+device serving loop -> TTFT/TPOT."""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from helpers import rows_to_table
+from oracle import profiler as oprof
+from oracle import sim as osim
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_fit_db(db):
+    """Oracle fit of every measured signature -> {digest: (kind, coef, inv, lo, hi)}."""
+    out = {}
+    for s in db.signatures:
+        if s.digest not in db.measurements:
+            continue
+        x, y = db.measurements[s.digest]
+        r = osim.fit(s.kind, x, y, np.array([0, y.shape[0]], dtype=np.int64))
+        out[s.digest] = (s.kind, r)
+    return out
+
+
+def _profile(manifest, dev):
+    from paper_2605_07985_b200.profiler import profile_corpus
+
+    return profile_corpus(manifest, device=dev)
+
+
+def test_c1_llama3_8b_end_to_end(corpus, dev):
+    from paper_2605_07985_b200 import modelir
+    from paper_2605_07985_b200.records import synthesize_entries
+    from paper_2605_07985_b200.sim import (SchedConfig, build_calltree, fit, run,
+                                           ShardedTrace, make_sched, run_sharded, collect)
+
+    model = corpus.model("llama-3-8b-like")
+    backend = corpus.backend("flashattention-like")
+    man = modelir.CorpusManifest((model,), (backend,), corpus.hardware, 1, corpus.grid)
+    db, report = _profile(man, dev)
+    ents = synthesize_entries(model, backend, 1)
+    # dedup: the GPU to_profile set equals the oracle's first occurrences
+    ref_tp, _ = oprof.dedup([e.to_json() for e in ents])
+    assert report[0]["profiled"] == len(ref_tp) == len(db.signatures)
+    regs = fit(db, dev)
+    ref = _oracle_fit_db(db)
+    for d, (kind, r) in ref.items():
+        got = regs.regressor(d)
+        c = np.array(got.coefficients)
+        assert np.max(np.abs(c - r["coef"][0])) <= 1e-9 * np.max(np.abs(r["coef"][0]))
+        # MAPE of an exactly-affine sweep is rounding noise (~1e-16): relative 1e-9 or 1e-12 absolute
+        assert abs(got.fit_error - r["fit_err"][0]) <= 1e-9 * r["fit_err"][0] + 1e-12
+    # TTFT/TPOT on the reference's own C1 trace (tests/golden/workload_c1.json)
+    g = json.loads((GOLDEN / "workload_c1.json").read_text())
+    reqs = [modelir.Request(*r) for r in g["requests"]]
+    sched = SchedConfig(chunk=8192, max_batch=256)
+    m = run(reqs, model, backend, corpus.hardware, regs, sched)
+    ct = build_calltree(model, backend, regs, corpus.hardware, 1)
+    cfg = make_sched(model, corpus.hardware, 1, sched, ct)
+    # oracle run with the oracle's own coefficients (independent fit): 1e-6 relative
+    ops, ops_same = [], []
+    rows_by_kind = {k: rows_to_table(k, regs.tables[k].rows()) for k in regs.tables}
+    for i in range(ct.n_ops):
+        feat, row = ct.oplist.feat[i], ct.oplist.row[i]
+        kind = 1 if feat == osim.FEAT_ATTN else 0
+        digest = [dd for dd, (kk, rr) in regs.index.items() if kk == kind and rr == row][0]
+        _, r = ref[digest]
+        base = {"feat": feat, "repeat": ct.oplist.repeat[i], "window_slot": ct.oplist.window_slot[i]}
+        ops.append(dict(base, coef=list(r["coef"][0]), inv=list(r["inv"][0])))
+        t = rows_by_kind[kind]
+        ops_same.append(dict(base, coef=list(t["coef"][row]), inv=list(t["inv"][row])))
+    arr = [r.arrival_s for r in reqs]
+    pr = [r.prompt_tokens for r in reqs]
+    ou = [r.output_tokens for r in reqs]
+    ca = [r.cached_tokens for r in reqs]
+    kw = dict(chunk=8192, max_batch=256, kv_bytes_per_token=cfg.kv_bytes_per_token,
+              kv_capacity=cfg.kv_capacity_bytes, window=ct.window)
+    r_ind = osim.run_shard(arr, pr, ou, ca, ops, **kw)
+    r_same = osim.run_shard(arr, pr, ou, ca, ops_same, **kw)
+    # same regressor rows -> bit-identical TTFT/TPOT
+    assert np.array_equal(m.ttft, r_same["ttft"])
+    mask = ~np.isnan(r_same["tpot"])
+    assert np.array_equal(np.isnan(m.tpot), ~mask) and np.array_equal(m.tpot[mask], r_same["tpot"][mask])
+    # independent oracle fit -> within the 1e-6 relative TTFT/TPOT bar
+    assert np.allclose(m.ttft, r_ind["ttft"], rtol=1e-6, atol=0)
+    assert np.allclose(m.tpot[mask], r_ind["tpot"][mask], rtol=1e-6, atol=0)
+    assert m.n_iterations[0] == r_same["n_iter"]
+
+
+def test_c2_zoo_joint_fit(corpus, dev):
+    from paper_2605_07985_b200.sim import fit
+
+    db, report = _profile(corpus, dev)
+    assert len(report) == 36
+    # attention signatures: 15 unique (Table 2)
+    att = [s for s in db.signatures if s.op_name == "attention"]
+    assert len(att) == 15
+    regs = fit(db, dev)
+    ref = _oracle_fit_db(db)
+    worst = 0.0
+    for d, (kind, r) in ref.items():
+        c = np.array(regs.regressor(d).coefficients)
+        worst = max(worst, np.max(np.abs(c - r["coef"][0])) / np.max(np.abs(r["coef"][0])))
+    assert worst <= 1e-9, worst
+
+
+def test_c3_mixtral_moe_dedup_fit(dev):
+    from paper_2605_07985_b200 import modelir
+    from paper_2605_07985_b200.records import synthesize_entries
+    from paper_2605_07985_b200.sim import fit
+
+    man = modelir.load_manifest(modelir.builtin_manifest_path("mixtral"))
+    db, report = _profile(man, dev)
+    names = {s.op_name for s in db.signatures}
+    assert {"fused_moe", "topk_softmax", "attention", "linear"} <= names
+    ents = [e for b in man.backends for e in synthesize_entries(man.models[0], b, 1)]
+    ref_tp, _ = oprof.dedup([e.to_json() for e in ents])
+    assert len(db.signatures) == len(ref_tp)
+    regs = fit(db, dev)
+    att = [s for s in db.signatures if s.op_name == "attention"][0]
+    x, y = db.measurements[att.digest]
+    # 7 x 4 x 4 x 2 grid minus invalid points (prefill needs t >= r,
+    # t/r + kv within max_context; App. A.5)
+    valid = sum(1 for t in man.grid.token_counts for r in man.grid.request_counts
+                for c in man.grid.kv_lens if t >= r and c + -(-t // r) <= 32768)
+    valid += sum(1 for r in man.grid.request_counts for c in man.grid.kv_lens if c + 1 <= 32768)
+    assert x.shape[1] == valid and valid > 100
+    ref = _oracle_fit_db(db)[att.digest][1]
+    c = np.array(regs.regressor(att.digest).coefficients)
+    assert np.max(np.abs(c - ref["coef"][0])) <= 1e-9 * np.max(np.abs(ref["coef"][0]))
+
+
+def test_tp4_calltree_comm_entries(dev):
+    from paper_2605_07985_b200 import modelir
+    from paper_2605_07985_b200.sim import build_calltree, fit, iter_latency, IterationBatch
+
+    man = modelir.load_manifest(modelir.builtin_manifest_path("llama70b"))
+    model, backend = man.models[0], man.backends[1]
+    sub = modelir.CorpusManifest((model,), (backend,), man.hardware, 4, man.grid)
+    db, _ = _profile(sub, dev)
+    regs = fit(db, dev)
+    ct = build_calltree(model, backend, regs, man.hardware, 4)
+    assert ct.oplist.feat[ct.n_ops - 1] == osim.FEAT_COMM
+    assert ct.oplist.repeat[ct.n_ops - 1] == 2 * model.num_layers
+    lat = iter_latency(IterationBatch(512, 256, 8, 8192), ct, regs)
+    comm = oprof.comm_latency(4, 512 * model.hidden_dim * 2, man.hardware.comm_alpha,
+                              man.hardware.comm_beta)
+    assert lat > 2 * model.num_layers * comm
