@@ -310,9 +310,9 @@ def run_ours(args):
 
     rank, world = ddist.init_from_env()
     dist_on = world > 1
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = ddist.local_device()
+    local = dev.index
+    torch.cuda.set_device(dev)
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     _lib.ctx_for(dev)

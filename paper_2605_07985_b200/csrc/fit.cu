@@ -991,29 +991,18 @@ __global__ void __launch_bounds__(128) fit_solve_attn_kernel(
       hi[k] = __ldg(box + (int64_t)(3 + k) * n_sig + s);
       inv[k] = hi[k] > 0 ? 1.0 / (double)hi[k] : 1.0;  // IEEE division (oracle parity)
     }
-    // scaled moment m: raw * prod inv^e (m = 0 is the point count)
-    auto msc = [&](int m) {
-      double v = m == 0 ? (double)n : __ldg(mom + (int64_t)(m - 1) * n_sig + s);
+    // scaled moments: raw sum * prod inv^e; the scales follow the same
+    // degree-<=4 monomial recurrence as the moments themselves
+    double sc[35], msc[35];
+    attn_monomials(inv[0], inv[1], inv[2], sc);
+    msc[0] = (double)n;
 #pragma unroll
-      for (int k = 0; k < 3; ++k)
-        for (int r = 0; r < kAttnExp[m][k]; ++r) v *= inv[k];
-      return v;
-    };
+    for (int m = 1; m < 35; ++m) msc[m] = __ldg(mom + (int64_t)(m - 1) * n_sig + s) * sc[m];
     double L[NC][NC];  // lower triangle used
-#pragma unroll
-    for (int i = 0; i < NC; ++i)
-#pragma unroll
-      for (int j = 0; j <= i; ++j) L[i][j] = msc(kAttnGidx[i][j]);
+    attn_gram(msc, L);
     double b[NC];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      double v = __ldg(mom + (int64_t)(34 + i) * n_sig + s);
-      const int m = kAttnColmon[i];
-#pragma unroll
-      for (int k = 0; k < 3; ++k)
-        for (int r = 0; r < kAttnExp[m][k]; ++r) v *= inv[k];
-      b[i] = v;
-    }
+    for (int i = 0; i < NC; ++i) b[i] = __ldg(mom + (int64_t)(34 + i) * n_sig + s) * sc[attn_colmon(i)];
     // Cholesky with drop (same rule as the oracle): L overwrites G
     double rd[NC];
 #pragma unroll

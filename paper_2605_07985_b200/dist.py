@@ -30,14 +30,24 @@ def world() -> tuple:
     return 0, 1
 
 
+def local_device() -> torch.device:
+    """This rank's GPU: LOCAL_RANK, folded onto the visible devices (so a
+    multi-rank smoke test can share one GPU under the gloo backend)."""
+    n = max(1, torch.cuda.device_count())
+    return torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")) % n)
+
+
 def init_from_env(backend: Optional[str] = None) -> tuple:
-    """Initialise the default group from torchrun's env (127.0.0.1 rendezvous)."""
+    """Initialise the default group from torchrun's env (127.0.0.1 rendezvous).
+
+    Backend: NCCL on GPUs unless DOOLY_DIST_BACKEND overrides it (gloo is used
+    by the CPU tests and for several ranks sharing one GPU)."""
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        backend = backend or os.environ.get("DOOLY_DIST_BACKEND") or (
+            "nccl" if torch.cuda.is_available() else "gloo")
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local_device())
         dist.init_process_group(backend=backend)
     return world()
 
