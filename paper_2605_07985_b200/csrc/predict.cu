@@ -116,7 +116,7 @@ __device__ __forceinline__ double eval_query(const void* table, int64_t n_sig, u
 // Vector path: 256-query tiles, sig / planes / out 32-B aligned, n_q % 8 == 0
 // when there is more than one plane.
 template <int KIND>
-__global__ void __launch_bounds__(256, KIND == DOOLY_KIND_AFFINE ? 4 : 1) predict_vec_kernel(
+__global__ void __launch_bounds__(256) predict_vec_kernel(
     const void* __restrict__ table, int64_t n_sig, const uint32_t* __restrict__ sig,
     const uint32_t* __restrict__ x, int64_t n_q, double* __restrict__ out,
     uint32_t* __restrict__ flags, int64_t* __restrict__ err_first) {
