@@ -139,6 +139,43 @@ int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
                   const uint32_t* sig, const uint32_t* x, int64_t n_q, double* out,
                   uint32_t* flag_bits, int64_t* err_first, void* stream);
 
+/* ------------------------------------------------------- K5 fused sweep -> fit
+ * evaluates the analytical latency model (SPEC.md:476-484,
+ * op formulas of profiler.op_cost) over each signature's sweep grid
+ * (App. A.5) in registers and fits it (K2 semantics) without
+ * materialising measurements.  descs is DEVICE memory (n_sig entries), grid
+ * is a HOST struct passed by value.  out_x/out_y/out_off (device, optional)
+ * receive the generated points (feature-major planes of out_n) for checking. */
+#define DOOLY_OP_RESHAPE 0
+#define DOOLY_OP_LINEAR 1     /* dim: K, N                        */
+#define DOOLY_OP_EMBEDDING 2  /* dim: hidden                      */
+#define DOOLY_OP_RMSNORM 3    /* dim: hidden                      */
+#define DOOLY_OP_ROTARY 4     /* dim: hq*d + hkv*d                */
+#define DOOLY_OP_ACT_MUL 5    /* dim: 2*intermediate              */
+#define DOOLY_OP_TOPK 6       /* dim: experts                     */
+#define DOOLY_OP_MOE 7        /* dim: experts, 2*expert_inter, hidden, top_k */
+#define DOOLY_OP_ATTENTION 8  /* dim: hq, head_dim, hkv           */
+#define DOOLY_SWEEP_MAX 16
+typedef struct {
+  int32_t op;           /* DOOLY_OP_*                                         */
+  int32_t feature;      /* DOOLY_FEAT_NUM_TOKS / NUM_SEQS / ATTN               */
+  int64_t dim[4];
+  int32_t window;       /* attention sliding window, 0 = full                  */
+  int32_t dtype_bytes;
+  int64_t max_context;
+  double mult[2];       /* cost multiplier: [prefill or all, decode]           */
+} dooly_sweep_desc;
+typedef struct {
+  int32_t n_tok, n_req, n_kv, pad_;
+  int64_t chunk, max_batch;
+  uint32_t tok[DOOLY_SWEEP_MAX], req[DOOLY_SWEEP_MAX], kv[DOOLY_SWEEP_MAX];
+  double peak_flops, mem_bw, overhead;
+} dooly_sweep_grid;
+int dooly_profile_fit(dooly_ctx* ctx, int kind, const dooly_sweep_desc* descs, int64_t n_sig,
+                      const dooly_sweep_grid* grid, void* table, double* fit_err,
+                      uint8_t* status, uint32_t* out_x, double* out_y, const int64_t* out_off,
+                      int64_t out_n, void* stream);
+
 /* ------------------------------------------------------------------- K4 sim
  * Call-graph op list for one (model, backend, tp): iter_latency
  *   lat = sum_e repeat_e * max(pred_e(x_it), 1e-7)   [in list order]

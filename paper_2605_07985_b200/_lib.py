@@ -42,6 +42,33 @@ class OpList(C.Structure):
     ]
 
 
+SWEEP_MAX = 16
+OP_CODES = {"reshape": 0, "linear": 1, "embedding": 2, "rms_norm": 3, "rotary_embedding": 4,
+            "silu_and_mul": 5, "topk_softmax": 6, "fused_moe": 7, "attention": 8}
+
+
+class SweepDesc(C.Structure):
+    _fields_ = [
+        ("op", C.c_int32),
+        ("feature", C.c_int32),
+        ("dim", C.c_int64 * 4),
+        ("window", C.c_int32),
+        ("dtype_bytes", C.c_int32),
+        ("max_context", C.c_int64),
+        ("mult", C.c_double * 2),
+    ]
+
+
+class SweepGrid(C.Structure):
+    _fields_ = [
+        ("n_tok", C.c_int32), ("n_req", C.c_int32), ("n_kv", C.c_int32), ("pad_", C.c_int32),
+        ("chunk", C.c_int64), ("max_batch", C.c_int64),
+        ("tok", C.c_uint32 * SWEEP_MAX), ("req", C.c_uint32 * SWEEP_MAX),
+        ("kv", C.c_uint32 * SWEEP_MAX),
+        ("peak_flops", C.c_double), ("mem_bw", C.c_double), ("overhead", C.c_double),
+    ]
+
+
 class Sched(C.Structure):
     _fields_ = [
         ("chunk", C.c_int32),
@@ -74,6 +101,8 @@ _SIGS = {
     "dooly_predict": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
     "dooly_iter_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _I64, _P, _P,
                                   _P]),
+    "dooly_profile_fit": (C.c_int, [_P, C.c_int, _P, _I64, C.POINTER(SweepGrid), _P, _P, _P, _P,
+                                    _P, _P, _I64, _P]),
     "dooly_sim_workspace_size": (C.c_size_t, [C.POINTER(Sched), _I64, _I64]),
     "dooly_sim_run": (C.c_int, [_P, C.POINTER(OpList), C.POINTER(Sched), _P, _I64, _P, _I64,
                                 _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _I64, _P,

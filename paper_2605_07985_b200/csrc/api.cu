@@ -34,6 +34,11 @@ cudaError_t launch_iter_eval(const dooly_oplist* ops, const void* aff, int64_t n
                              int64_t n_it, double* it_lat, int64_t* err_first,
                              cudaStream_t stream, int n_sm);
 size_t sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards);
+cudaError_t launch_profile_fit(int kind, const dooly_sweep_desc* descs, int64_t n_sig,
+                               const dooly_sweep_grid* grid, void* table, double* fit_err,
+                               uint8_t* status, uint32_t* out_x, double* out_y,
+                               const int64_t* out_off, int64_t out_n, cudaStream_t stream,
+                               int n_sm);
 cudaError_t launch_sim(const dooly_oplist* ops, const dooly_sched* cfg, const void* aff,
                        int64_t n_aff, const void* attn, int64_t n_attn, const double* arrival,
                        const uint32_t* prompt, const uint32_t* output, const uint32_t* cached,
@@ -246,6 +251,31 @@ int dooly_iter_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_
                                             it_feat, n_it, it_lat, err_first,
                                             (cudaStream_t)stream, ctx->n_sm),
                     "iter_eval");
+}
+
+int dooly_profile_fit(dooly_ctx* ctx, int kind, const dooly_sweep_desc* descs, int64_t n_sig,
+                      const dooly_sweep_grid* grid, void* table, double* fit_err,
+                      uint8_t* status, uint32_t* out_x, double* out_y, const int64_t* out_off,
+                      int64_t out_n, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "profile_fit: unknown kind");
+  if (n_sig < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "profile_fit: negative size");
+  if (!grid || grid->n_tok < 0 || grid->n_tok > DOOLY_SWEEP_MAX || grid->n_req < 0 ||
+      grid->n_req > DOOLY_SWEEP_MAX || grid->n_kv < 0 || grid->n_kv > DOOLY_SWEEP_MAX ||
+      grid->peak_flops <= 0 || grid->mem_bw <= 0)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "profile_fit: bad sweep grid");
+  if (n_sig > 0 && (!descs || !table || !fit_err || !status))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "profile_fit: null pointer");
+  if ((out_x != nullptr) != (out_y != nullptr) || (out_x != nullptr && out_off == nullptr))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "profile_fit: out_x/out_y/out_off go together");
+  DeviceGuard g(ctx->device);
+  if (n_sig > 0) ctx->launches += 1;
+  return check_cuda(ctx,
+                    dooly::launch_profile_fit(kind, descs, n_sig, grid, table, fit_err, status,
+                                              out_x, out_y, out_off, out_n,
+                                              (cudaStream_t)stream, ctx->n_sm),
+                    "profile_fit");
 }
 
 size_t dooly_sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards) {

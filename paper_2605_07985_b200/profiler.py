@@ -16,6 +16,7 @@ Host side (inputs to the fit, SURVEY §8(f) row f1 is their GPU fusion):
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -461,3 +462,127 @@ def profile_corpus(manifest, db: Optional[LatencyDB] = None, device=None,
             report.append({"model": m.name, "backend": b.name, "entries": len(entries),
                            "profiled": len(to_profile), "skipped": len(skipped)})
     return db, report
+
+
+# ------------------------------------------------- K5: fused sweep -> fit (f1)
+
+
+def sweep_descriptor(entry: RunnableEntry, model: ModelConfig, backend: BackendSpec):
+    """Device descriptor of one signature's sweep for dooly_profile_fit (the
+    dims op_cost reads, the backend multipliers of both attention phases)."""
+    d = _lib.SweepDesc()
+    if entry.name not in _lib.OP_CODES:
+        raise OraclePanic(f"no cost formula for op kind {entry.name!r}")
+    d.op = _lib.OP_CODES[entry.name]
+    d.feature = {"num_toks": _lib.FEAT_NUM_TOKS, "num_seqs": _lib.FEAT_NUM_SEQS,
+                 "attention": _lib.FEAT_ATTN}[entry.feature]
+    a = _dims(entry)
+    dims = {
+        "linear": lambda: (a[1][1], a[1][0]),
+        "embedding": lambda: (a[1][1],),
+        "rms_norm": lambda: (a[0][1],),
+        "rotary_embedding": lambda: (a[0][1] * a[0][2] + a[1][1] * a[1][2],),
+        "silu_and_mul": lambda: (a[0][1],),
+        "topk_softmax": lambda: (a[0][1],),
+        "fused_moe": lambda: (a[1][0], a[1][1], a[1][2], entry.scalars[0][0]),
+        "attention": lambda: (a[0][1], a[0][2], a[1][1]),
+        "reshape": lambda: (),
+    }[entry.name]()
+    for i, v in enumerate(dims):
+        d.dim[i] = int(v)
+    d.window = int(entry.window or 0)
+    d.dtype_bytes = model.dtype_bytes
+    d.max_context = model.max_context
+    if entry.feature == "attention":
+        for i, phase in enumerate(("prefill", "decode")):
+            syms = tuple(s.replace("_decode_attn_", f"_{phase}_attn_") for s in entry.kernel_symbols)
+            d.mult[i] = backend.multiplier(syms)
+    else:
+        d.mult[0] = d.mult[1] = backend.multiplier(entry.kernel_symbols)
+    return d
+
+
+def sweep_grid_struct(grid: SweepGrid, hw: HardwareSpec):
+    g = _lib.SweepGrid()
+    for name, vals in (("tok", grid.token_counts), ("req", grid.request_counts),
+                       ("kv", grid.kv_lens)):
+        if len(vals) > _lib.SWEEP_MAX:
+            raise ValueError(f"sweep grid axis {name} longer than {_lib.SWEEP_MAX}")
+        arr = getattr(g, name)
+        for i, v in enumerate(vals):
+            arr[i] = int(v)
+    g.n_tok, g.n_req, g.n_kv = len(grid.token_counts), len(grid.request_counts), len(grid.kv_lens)
+    g.chunk, g.max_batch = grid.prefill_chunk, grid.max_batch
+    g.peak_flops, g.mem_bw, g.overhead = hw.peak_flops, hw.mem_bw, OVERHEAD_S
+    return g
+
+
+def profile_fit(items: Sequence, hw: HardwareSpec, grid: SweepGrid, device=None,
+                emit_points: bool = False):
+    """K5: sweep + fit (entry, model, backend) triples on the device, one launch
+    per regression kind (descriptors carry each model's caps and each backend's
+    multipliers; the grid and hardware are shared).  Returns
+    {kind: (FitResult, item indices, (x, y, off) | None)}."""
+    from .sim import FitResult
+
+    dev = _device(device)
+    g = sweep_grid_struct(grid, hw)
+    out = {}
+    for kind in (_lib.KIND_AFFINE, _lib.KIND_ATTN):
+        idx = [i for i, it in enumerate(items) if _kind_of(it[0]) == kind]
+        if not idx:
+            continue
+        descs = (_lib.SweepDesc * len(idx))(*[sweep_descriptor(*items[i]) for i in idx])
+        d_desc = torch.frombuffer(bytearray(descs), dtype=torch.uint8).to(dev)
+        n = len(idx)
+        fr = FitResult(kind, torch.empty((n, _lib.ROW_BYTES[kind]), dtype=torch.uint8, device=dev),
+                       torch.empty(n, dtype=torch.float64, device=dev),
+                       torch.empty(n, dtype=torch.uint8, device=dev))
+        px = py = poff = None
+        if emit_points:
+            counts = [len(sweep_points(items[i][0], grid, items[i][1].max_context)) for i in idx]
+            off = np.zeros(n + 1, dtype=np.int64)
+            off[1:] = np.cumsum(counts)
+            total = int(off[-1])
+            px = torch.zeros((_lib.PLANES[kind], max(total, 1)), dtype=torch.int32, device=dev)
+            py = torch.zeros(max(total, 1), dtype=torch.float64, device=dev)
+            poff = torch.from_numpy(off).to(dev)
+        ctx = _lib.ctx_for(dev)
+        _lib.check(_lib.load_library().dooly_profile_fit(
+            ctx, kind, d_desc.data_ptr(), n, C.byref(g), fr.table.data_ptr(),
+            fr.fit_err.data_ptr(), fr.status.data_ptr(), _lib.ptr(px), _lib.ptr(py),
+            _lib.ptr(poff), 0 if px is None else px.shape[1], _lib.stream_ptr(dev)), ctx)
+        out[kind] = (fr, idx, (px, py, poff) if emit_points else None)
+    return out
+
+
+def profile_and_fit(manifest, db: Optional[LatencyDB] = None, device=None,
+                    grid: Optional[SweepGrid] = None):
+    """cmd_profile + fit with the fused K5 path: GPU dedup of every runnable set
+    (model_operations rows for all entries), then one sweep+fit launch per
+    regression kind for all new signatures.  Measurements are never
+    materialised; returns (db, Regressors, report)."""
+    from .records import synthesize_entries
+    from .sim import Regressors
+
+    dev = _device(device)
+    db = db if db is not None else LatencyDB()
+    grid = grid or manifest.grid
+    items, digests, report = [], [], []
+    for m in manifest.models:
+        for b in manifest.backends:
+            cid = db.add_configuration(manifest.hardware.name, m.name, b.name, manifest.tp_degree)
+            entries = synthesize_entries(m, b, manifest.tp_degree)
+            to_profile, skipped, digs = dedup_with_digests(entries, db, cid, dev)
+            items += [(e, m, b) for e in to_profile]
+            digests += digs
+            report.append({"model": m.name, "backend": b.name, "entries": len(entries),
+                           "profiled": len(to_profile), "skipped": len(skipped)})
+    res = profile_fit(items, manifest.hardware, grid, dev)
+    tables, index = {}, {}
+    for kind, (fr, idx, _) in res.items():
+        tables[kind] = fr
+        for row, i in enumerate(idx):
+            index[digests[i]] = (kind, row)
+    torch.cuda.synchronize(dev)
+    return db, Regressors(tables, index, dev), report
