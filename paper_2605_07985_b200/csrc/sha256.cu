@@ -30,50 +30,70 @@ __device__ __forceinline__ uint32_t rotr(uint32_t x, int n) { return __funnelshi
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 // One 64-byte block; w points at 16 big-endian words in shared memory.
-__device__ __forceinline__ void sha256_compress(uint32_t h[8], const uint32_t* w_in) {
+// 16 rounds are unrolled (the a..h roles rotate back every 8 rounds) inside a
+// 4-trip loop: ncu showed the fully unrolled 64-round body, inlined at two call
+// sites, thrashing the instruction cache (`no_instruction` was the top stall).
+#define SHA_S0(x) (rotr(x, 2) ^ rotr(x, 13) ^ rotr(x, 22))
+#define SHA_S1(x) (rotr(x, 6) ^ rotr(x, 11) ^ rotr(x, 25))
+#define SHA_s0(x) (rotr(x, 7) ^ rotr(x, 18) ^ ((x) >> 3))
+#define SHA_s1(x) (rotr(x, 17) ^ rotr(x, 19) ^ ((x) >> 10))
+#define SHA_RND(a, b, c, d, e, f, g, h, i)                                          \
+  {                                                                                 \
+    const uint32_t t1 = h + SHA_S1(e) + ((e & f) ^ (~e & g)) + kSha256K[r + i] + w[i]; \
+    const uint32_t t2 = SHA_S0(a) + ((a & b) ^ (a & c) ^ (b & c));                   \
+    d += t1;                                                                        \
+    h = t1 + t2;                                                                    \
+  }
+#define SHA_SCHED(i) \
+  w[i] += SHA_s0(w[((i) + 1) & 15]) + w[((i) + 9) & 15] + SHA_s1(w[((i) + 14) & 15])
+#define SHA_16(sched)                                                              \
+  sched(0); SHA_RND(a, b, c, d, e, f, g, k, 0);                                    \
+  sched(1); SHA_RND(k, a, b, c, d, e, f, g, 1);                                    \
+  sched(2); SHA_RND(g, k, a, b, c, d, e, f, 2);                                    \
+  sched(3); SHA_RND(f, g, k, a, b, c, d, e, 3);                                    \
+  sched(4); SHA_RND(e, f, g, k, a, b, c, d, 4);                                    \
+  sched(5); SHA_RND(d, e, f, g, k, a, b, c, 5);                                    \
+  sched(6); SHA_RND(c, d, e, f, g, k, a, b, 6);                                    \
+  sched(7); SHA_RND(b, c, d, e, f, g, k, a, 7);                                    \
+  sched(8); SHA_RND(a, b, c, d, e, f, g, k, 8);                                    \
+  sched(9); SHA_RND(k, a, b, c, d, e, f, g, 9);                                    \
+  sched(10); SHA_RND(g, k, a, b, c, d, e, f, 10);                                  \
+  sched(11); SHA_RND(f, g, k, a, b, c, d, e, 11);                                  \
+  sched(12); SHA_RND(e, f, g, k, a, b, c, d, 12);                                  \
+  sched(13); SHA_RND(d, e, f, g, k, a, b, c, 13);                                  \
+  sched(14); SHA_RND(c, d, e, f, g, k, a, b, 14);                                  \
+  sched(15); SHA_RND(b, c, d, e, f, g, k, a, 15);
+#define SHA_NOSCHED(i) (void)0
+
+__device__ __forceinline__ void sha256_compress(uint32_t hs[8], const uint32_t* w_in) {
   uint32_t w[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) w[i] = w_in[i];
-  uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], k = h[7];
-#pragma unroll
-  for (int t = 0; t < 64; ++t) {
-    uint32_t wt;
-    if (t < 16) {
-      wt = w[t];
-    } else {
-      const uint32_t w15 = w[(t - 15) & 15], w2 = w[(t - 2) & 15];
-      const uint32_t s0 = rotr(w15, 7) ^ rotr(w15, 18) ^ (w15 >> 3);
-      const uint32_t s1 = rotr(w2, 17) ^ rotr(w2, 19) ^ (w2 >> 10);
-      wt = w[t & 15] + s0 + w[(t - 7) & 15] + s1;
-      w[t & 15] = wt;
-    }
-    const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
-    const uint32_t ch = (e & f) ^ (~e & g);
-    const uint32_t t1 = k + S1 + ch + kSha256K[t] + wt;
-    const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
-    const uint32_t maj = (a & b) ^ (a & c) ^ (b & c);
-    const uint32_t t2 = S0 + maj;
-    k = g;
-    g = f;
-    f = e;
-    e = d + t1;
-    d = c;
-    c = b;
-    b = a;
-    a = t1 + t2;
+  uint32_t a = hs[0], b = hs[1], c = hs[2], d = hs[3], e = hs[4], f = hs[5], g = hs[6],
+           k = hs[7];
+  int r = 0;
+  SHA_16(SHA_NOSCHED)
+#pragma unroll 1
+  for (r = 16; r < 64; r += 16) {
+    SHA_16(SHA_SCHED)
   }
-  h[0] += a;
-  h[1] += b;
-  h[2] += c;
-  h[3] += d;
-  h[4] += e;
-  h[5] += f;
-  h[6] += g;
-  h[7] += k;
+  hs[0] += a;
+  hs[1] += b;
+  hs[2] += c;
+  hs[3] += d;
+  hs[4] += e;
+  hs[5] += f;
+  hs[6] += g;
+  hs[7] += k;
+}
+
+// Out-of-line copy for the rare long-message drain inside the byte writer.
+__device__ __noinline__ void sha256_compress_blocks(uint32_t hs[8], const uint32_t* w, int nb) {
+  for (int b = 0; b < nb; ++b) sha256_compress(hs, w + 16 * b);
 }
 
 constexpr int SHA_THREADS = 128;
-constexpr int SHA_BUF_BLOCKS = 5;                     // 320 B: typical canonical messages fit
+constexpr int SHA_BUF_BLOCKS = 3;  // 192 B: C1-C5 canonical messages fit (longer ones drain)
 constexpr int SHA_STRIDE = SHA_BUF_BLOCKS * 16 + 1;   // odd word stride: conflict-free reads
 
 // Byte-stream writer into a per-thread shared-memory block buffer.
@@ -103,7 +123,7 @@ struct ShaStream {
   __device__ __forceinline__ void emit(uint32_t w) {
     buf[nw++] = w;
     if (nw == SHA_BUF_BLOCKS * 16) {  // long message: drain (rare, divergent)
-      for (int b = 0; b < SHA_BUF_BLOCKS; ++b) sha256_compress(h, buf + 16 * b);
+      sha256_compress_blocks(h, buf, SHA_BUF_BLOCKS);
       nw = 0;
     }
   }
@@ -128,10 +148,9 @@ struct ShaStream {
   }
   __device__ void put_bytes(const uint8_t* p, int64_t len) {
     int64_t i = 0;
-    while (i < len && pn != 0) put_byte(p[i++]);
-    for (; i + 4 <= len; i += 4)
-      put_be32(((uint32_t)p[i] << 24) | ((uint32_t)p[i + 1] << 16) | ((uint32_t)p[i + 2] << 8) |
-               (uint32_t)p[i + 3]);
+    // bytes until the source is 4-aligned, then whole little-endian words
+    while (i < len && (((uintptr_t)(p + i)) & 3u) != 0) put_byte(p[i++]);
+    for (; i + 4 <= len; i += 4) put_be32(bswap32(__ldg(reinterpret_cast<const uint32_t*>(p + i))));
     for (; i < len; ++i) put_byte(p[i]);
   }
   // FIPS 180-4 padding, then lock-step compression of the buffered blocks.
