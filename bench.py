@@ -323,10 +323,12 @@ def run_ours(args):
     n_sig = {AFFINE: args.sigs // 2, ATTN: args.sigs - args.sigs // 2}
     fit_in = {k: gen_fit_data(k, n_sig[k], args.points, dev, seed + k) for k in (AFFINE, ATTN)}
     torch.cuda.synchronize()
-    from paper_2605_07985_b200.sim import fit_tables
+    from paper_2605_07985_b200._lib import KIND_ATTN_PACKED
+    from paper_2605_07985_b200.sim import fit_tables, pack_attn
 
     offs = {k: torch.from_numpy(fit_in[k][2]).to(dev) for k in (AFFINE, ATTN)}
     fit_out = {}
+    packed96 = None
     for _ in range(max(1, args.warmup)):
         for k in (AFFINE, ATTN):
             fit_out[k] = fit_tables(k, fit_in[k][0], fit_in[k][1], offs[k], fit_out.get(k))
@@ -345,6 +347,8 @@ def run_ours(args):
         for k in (AFFINE, ATTN):
             ev[k][0].record(stream)
             fit_out[k] = fit_tables(k, fit_in[k][0], fit_in[k][1], offs[k], fit_out[k])
+            if k == ATTN:   # serving form of the attention table (96-B rows), part of the fit output
+                packed96 = pack_attn(fit_out[k].table, packed96, check=False)
             ev[k][1].record(stream)
         ag0.record(stream)
         if dist_on:   # the one exchange step: every rank gets every rank's regressor rows
@@ -373,12 +377,15 @@ def run_ours(args):
         "all_fitted": status_ok,
     }
     del fit_in
-    tables = {k: fit_out[k].table for k in (AFFINE, ATTN)}
+    pack_attn(fit_out[ATTN].table, packed96, check=True)   # raises if not representable
+    rows128 = {k: fit_out[k].table for k in (AFFINE, ATTN)}
+    tables = {AFFINE: fit_out[AFFINE].table, ATTN: packed96}
+    pkind = {AFFINE: AFFINE, ATTN: KIND_ATTN_PACKED}
     torch.cuda.empty_cache()
 
     # ---------------- headline: predict
     nq = {AFFINE: args.queries // 2, ATTN: args.queries - args.queries // 2}
-    qs = {k: gen_queries(k, tables[k], nq[k], dev, seed + 7 + k) for k in (AFFINE, ATTN)}
+    qs = {k: gen_queries(k, rows128[k], nq[k], dev, seed + 7 + k) for k in (AFFINE, ATTN)}
     outs = {k: torch.empty(nq[k], dtype=torch.float64, device=dev) for k in (AFFINE, ATTN)}
     flags = {k: torch.empty((2, (nq[k] + 31) // 32), dtype=torch.int32, device=dev)
              for k in (AFFINE, ATTN)}
@@ -387,7 +394,7 @@ def run_ours(args):
 
     def predict_step():
         for k in (AFFINE, ATTN):
-            predict_batch(k, tables[k], qs[k][0], qs[k][1], outs[k], flags[k], errs[k])
+            predict_batch(pkind[k], tables[k], qs[k][0], qs[k][1], outs[k], flags[k], errs[k])
 
     for _ in range(args.warmup):
         predict_step()
@@ -403,7 +410,7 @@ def run_ours(args):
         for s in range(args.steps):
             for k in (AFFINE, ATTN):
                 pev[k][s][0].record(stream)
-                predict_batch(k, tables[k], qs[k][0], qs[k][1], outs[k], flags[k], errs[k])
+                predict_batch(pkind[k], tables[k], qs[k][0], qs[k][1], outs[k], flags[k], errs[k])
                 pev[k][s][1].record(stream)
         end.record(stream)
         barrier_sync(dist_on)
@@ -427,13 +434,13 @@ def run_ours(args):
                          torch.empty(n_e[k], dtype=torch.float64).pin_memory())
         for _ in range(2):
             for k in (AFFINE, ATTN):
-                predict_host(k, tables[k], *host_q[k])
+                predict_host(pkind[k], tables[k], *host_q[k])
         barrier_sync(dist_on)
         e_steps = max(1, min(args.steps, 3))
         t0 = time.perf_counter()
         for _ in range(e_steps):
             for k in (AFFINE, ATTN):
-                predict_host(k, tables[k], *host_q[k])
+                predict_host(pkind[k], tables[k], *host_q[k])
         barrier_sync(dist_on)
         e_s = max_over_ranks((time.perf_counter() - t0) / e_steps, dist_on)
         h2d = sum(host_q[k][0].numel() * 4 + host_q[k][1].numel() * 4 for k in (AFFINE, ATTN))
@@ -453,7 +460,7 @@ def run_ours(args):
         from helpers import rows_to_table
 
         for k in (AFFINE, ATTN):
-            rows = tables[k].cpu().numpy().view(ROW_DTYPE[k]).reshape(-1)
+            rows = rows128[k].cpu().numpy().view(ROW_DTYPE[k]).reshape(-1)
             tables_host[k] = rows_to_table(k, rows)
             m = args.cpu_sample // 2
             qh[k] = (qs[k][0][:m].cpu().numpy().view(np.uint32),

@@ -60,6 +60,33 @@ typedef struct {
   uint32_t lo[3], hi[3];
 } dooly_attn_row; /* 128 bytes */
 
+/* Packed attention table (DOOLY_KIND_ATTN_PACKED): the predict-side form of a
+ * dooly_attn_row table, 96 B = 3 sectors per row instead of 4.  inv_scale is
+ * not stored: it is a pure function of the box (inv = 1/hi by IEEE division,
+ * 1 if hi == 0; oracle/sim.py inv_scale), recomputed with a correctly-rounded
+ * reciprocal, so predictions stay bit-identical to the 128-B row.  The box is
+ * bit-packed with per-table field widths w[k] (w0+w1+w2 <= 64):
+ *   lo_bits = lo0 | lo1 << w0 | lo2 << (w0+w1)   (hi_bits likewise)
+ * Unfitted rows: lo_bits = all ones, hi_bits = 0.  Row s lives at
+ * packed + 96 * (s + 1); the first 96 B are the header below. */
+#define DOOLY_KIND_ATTN_PACKED 2
+#define DOOLY_PACK_MAGIC 0x6b504144u /* "DAPk" */
+typedef struct {
+  double c[10];
+  uint64_t lo_bits, hi_bits;
+} dooly_attn_row96; /* 96 bytes */
+
+typedef struct {
+  uint32_t magic;      /* DOOLY_PACK_MAGIC once packed                          */
+  uint32_t ok;         /* 1 = packable (widths fit, inv == 1/hi on every row)   */
+  uint32_t width[3];   /* box field widths, bits                                */
+  uint32_t max_hi[3];  /* per-feature max of hi over fitted rows                */
+  uint32_t bad_inv;    /* number of fitted rows whose inv_scale != 1/hi         */
+  uint32_t pad_;
+  int64_t n_sig;
+  uint8_t reserved[48];
+} dooly_attn_pack_header; /* 96 bytes */
+
 /* per-signature fit status */
 #define DOOLY_FIT_OK 0
 #define DOOLY_FIT_INSUFFICIENT 1
@@ -138,6 +165,15 @@ int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const 
 int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
                   const uint32_t* sig, const uint32_t* x, int64_t n_q, double* out,
                   uint32_t* flag_bits, int64_t* err_first, void* stream);
+
+/* Convert an attention table (n_sig dooly_attn_row) into the packed predict
+ * form (DOOLY_KIND_ATTN_PACKED) at `packed` (dooly_attn_pack_bytes(n_sig)
+ * bytes, 32-B aligned).  Asynchronous; the caller reads header.ok after the
+ * stream syncs.  dooly_predict on a header with ok != 1 flags every query as
+ * unknown (NaN + err_first), never silently mispredicts. */
+size_t dooly_attn_pack_bytes(int64_t n_sig);
+int dooly_attn_pack(dooly_ctx* ctx, const void* table, int64_t n_sig, void* packed,
+                    void* stream);
 
 /* ------------------------------------------------------- K5 fused sweep -> fit
  * evaluates the analytical latency model (SPEC.md:476-484,

@@ -19,13 +19,17 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libdooly_b200.so"
 
 KIND_AFFINE = 0
 KIND_ATTN = 1
+KIND_ATTN_PACKED = 2   # predict-only 96-B rows (dooly_attn_pack), see include/dooly_b200.h
+PACK_MAGIC = 0x6B504144
 FEAT_NUM_TOKS, FEAT_NUM_SEQS, FEAT_ATTN, FEAT_COMM = 0, 1, 2, 3
 MAX_OPS = 64
 IT_FEATS = 5
 AFFINE_ROW_BYTES = 32
 ATTN_ROW_BYTES = 128
-ROW_BYTES = {KIND_AFFINE: AFFINE_ROW_BYTES, KIND_ATTN: ATTN_ROW_BYTES}
-PLANES = {KIND_AFFINE: 1, KIND_ATTN: 3}
+ATTN96_ROW_BYTES = 96
+ROW_BYTES = {KIND_AFFINE: AFFINE_ROW_BYTES, KIND_ATTN: ATTN_ROW_BYTES,
+             KIND_ATTN_PACKED: ATTN96_ROW_BYTES}
+PLANES = {KIND_AFFINE: 1, KIND_ATTN: 3, KIND_ATTN_PACKED: 3}
 
 
 class OpList(C.Structure):
@@ -99,6 +103,8 @@ _SIGS = {
     "dooly_fit": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, C.c_size_t,
                             _P]),
     "dooly_predict": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
+    "dooly_attn_pack_bytes": (C.c_size_t, [_I64]),
+    "dooly_attn_pack": (C.c_int, [_P, _P, _I64, _P, _P]),
     "dooly_iter_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _I64, _P, _P,
                                   _P]),
     "dooly_profile_fit": (C.c_int, [_P, C.c_int, _P, _I64, C.POINTER(SweepGrid), _P, _P, _P, _P,

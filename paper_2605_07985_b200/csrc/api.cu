@@ -17,6 +17,8 @@ cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double*
                        uint8_t* status, void* ws, cudaStream_t stream, int n_sm,
                        int64_t* launches);
 size_t fit_workspace_size(int kind, int64_t n_sig);
+cudaError_t launch_attn_pack(const void* table, int64_t n_sig, void* packed, cudaStream_t stream,
+                             int n_sm, int64_t* launches);
 cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off, int64_t n,
                                   const uint8_t* op_bytes, const int64_t* op_off,
                                   const uint8_t* sym_bytes, const int64_t* sym_off,
@@ -110,8 +112,10 @@ int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
                   const uint32_t* sig, const uint32_t* x, int64_t n_q, double* out,
                   uint32_t* flag_bits, int64_t* err_first, void* stream) {
   if (!ctx) return DOOLY_ERR_INVALID_ARG;
-  if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
+  if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN && kind != DOOLY_KIND_ATTN_PACKED)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: unknown kind");
+  if (kind == DOOLY_KIND_ATTN_PACKED && !table)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: packed table needs its header");
   if (n_q < 0 || n_sig < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: negative size");
   if (n_q > 0 && (!table && n_sig > 0 || !sig || !x || !out))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: null pointer");
@@ -123,6 +127,27 @@ int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
                     dooly::launch_predict(kind, table, n_sig, sig, x, n_q, out, flag_bits,
                                           err_first, (cudaStream_t)stream, ctx->n_sm),
                     "predict");
+}
+
+size_t dooly_attn_pack_bytes(int64_t n_sig) {
+  return n_sig < 0 ? 0 : (size_t)(n_sig + 1) * sizeof(dooly_attn_row96);
+}
+
+int dooly_attn_pack(dooly_ctx* ctx, const void* table, int64_t n_sig, void* packed,
+                    void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n_sig < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "attn_pack: negative size");
+  if (!packed || (n_sig > 0 && !table))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "attn_pack: null pointer");
+  if ((uintptr_t)packed % 32 != 0 || (uintptr_t)table % 16 != 0)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "attn_pack: packed must be 32-B, table 16-B aligned");
+  if (n_sig > 0xFFFFFFFFll)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "attn_pack: more than 2^32 rows");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_attn_pack(table, n_sig, packed, (cudaStream_t)stream,
+                                            ctx->n_sm, &ctx->launches),
+                    "attn_pack");
 }
 
 size_t dooly_fit_workspace_size(int kind, int64_t n_sig) {

@@ -23,8 +23,40 @@ namespace dooly {
 
 template <int KIND>
 struct Planes {
-  static constexpr int P = KIND == DOOLY_KIND_ATTN ? 3 : 1;
+  static constexpr int P = KIND == DOOLY_KIND_AFFINE ? 1 : 3;
 };
+
+static_assert(sizeof(dooly_attn_row96) == 96, "packed attention row must be 3 sectors");
+static_assert(sizeof(dooly_attn_pack_header) == 96, "pack header must be one row");
+
+// Box field layout of a packed attention table, read from its header once per
+// thread (uniform across the grid; ok == false makes every query unknown).
+struct PackInfo {
+  uint64_t m0, m1, m2;
+  uint32_t s1, s2;
+  bool ok;
+};
+
+__device__ __forceinline__ PackInfo read_pack_header(const void* table, int64_t n_sig) {
+  PackInfo pk{};
+  const dooly_attn_pack_header* h = static_cast<const dooly_attn_pack_header*>(table);
+  const uint32_t magic = __ldg(&h->magic), ok = __ldg(&h->ok);
+  const uint32_t w0 = __ldg(&h->width[0]), w1 = __ldg(&h->width[1]), w2 = __ldg(&h->width[2]);
+  pk.ok = magic == DOOLY_PACK_MAGIC && ok == 1u && __ldg(&h->n_sig) == n_sig &&
+          w0 >= 1 && w1 >= 1 && w2 >= 1 && w0 + w1 + w2 <= 64;
+  pk.m0 = (1ull << (w0 & 63)) - 1;
+  pk.m1 = (1ull << (w1 & 63)) - 1;
+  pk.m2 = (1ull << (w2 & 63)) - 1;
+  pk.s1 = w0 & 63;
+  pk.s2 = (w0 + w1) & 63;
+  return pk;
+}
+
+// inv_scale of a packed row, recomputed exactly as oracle/sim.py inv_scale:
+// RN(1 / hi) (correctly-rounded reciprocal == IEEE 1.0 / hi) or 1 when hi == 0.
+__device__ __forceinline__ double inv_of(uint32_t hi) {
+  return hi != 0u ? __drcp_rn((double)hi) : 1.0;
+}
 
 struct U8 {
   uint32_t v[8];
@@ -84,16 +116,46 @@ __device__ __forceinline__ AttnRow gather_attn(const dooly_attn_row* t, uint32_t
   return r;
 }
 
+__device__ __forceinline__ AttnRow gather_attn96(const dooly_attn_row96* t, uint32_t s,
+                                                const PackInfo& pk) {
+  const double* p = reinterpret_cast<const double*>(t + s);
+  AttnRow r;
+  double wl, wh;
+  ld_row_256(p, r.c[0], r.c[1], r.c[2], r.c[3]);
+  ld_row_256(p + 4, r.c[4], r.c[5], r.c[6], r.c[7]);
+  ld_row_256(p + 8, r.c[8], r.c[9], wl, wh);
+  const uint64_t lb = (uint64_t)__double_as_longlong(wl), hb = (uint64_t)__double_as_longlong(wh);
+  r.lo[0] = (uint32_t)(lb & pk.m0);
+  r.lo[1] = (uint32_t)((lb >> pk.s1) & pk.m1);
+  r.lo[2] = (uint32_t)((lb >> pk.s2) & pk.m2);
+  r.hi[0] = (uint32_t)(hb & pk.m0);
+  r.hi[1] = (uint32_t)((hb >> pk.s1) & pk.m1);
+  r.hi[2] = (uint32_t)((hb >> pk.s2) & pk.m2);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r.inv[k] = inv_of(r.hi[k]);
+  return r;
+}
+
 template <int KIND>
 __device__ __forceinline__ double eval_query(const void* table, int64_t n_sig, uint32_t s,
                                              const uint32_t* xs, bool& extrap, bool& clamped,
-                                             bool& bad) {
+                                             bool& bad, const PackInfo& pk) {
   extrap = clamped = false;
   if (s >= (uint64_t)n_sig) {
     bad = true;
     return nan64();
   }
-  if constexpr (KIND == DOOLY_KIND_AFFINE) {
+  if constexpr (KIND == DOOLY_KIND_ATTN_PACKED) {
+    const AttnRow r =
+        gather_attn96(static_cast<const dooly_attn_row96*>(table) + 1, s, pk);
+    if (!attn_valid(r)) {
+      bad = true;
+      return nan64();
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) extrap |= xs[k] < r.lo[k] || xs[k] > r.hi[k];
+    return clamp_floor(eval_attn(r, xs[0], xs[1], xs[2]), clamped);
+  } else if constexpr (KIND == DOOLY_KIND_AFFINE) {
     const AffineRow r = gather_affine(static_cast<const dooly_affine_row*>(table), s);
     if (!affine_valid(r)) {
       bad = true;
@@ -121,6 +183,11 @@ __global__ void __launch_bounds__(256) predict_vec_kernel(
     const uint32_t* __restrict__ x, int64_t n_q, double* __restrict__ out,
     uint32_t* __restrict__ flags, int64_t* __restrict__ err_first) {
   constexpr int P = Planes<KIND>::P;
+  PackInfo pk{};
+  if constexpr (KIND == DOOLY_KIND_ATTN_PACKED) {
+    pk = read_pack_header(table, n_sig);
+    if (!pk.ok) n_sig = 0;
+  }
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -154,7 +221,7 @@ __global__ void __launch_bounds__(256) predict_vec_kernel(
       for (int p = 0; p < P; ++p) xs[p] = xv[p].v[j];
       bool e = false, c = false, bad = false;
       if (q + j < n_q) {
-        r[j] = eval_query<KIND>(table, n_sig, sv.v[j], xs, e, c, bad);
+        r[j] = eval_query<KIND>(table, n_sig, sv.v[j], xs, e, c, bad, pk);
         if (bad && q + j < bad_min) bad_min = q + j;
       } else {
         r[j] = 0.0;
@@ -195,6 +262,11 @@ __global__ void __launch_bounds__(256) predict_scalar_kernel(
     const uint32_t* __restrict__ x, int64_t n_q, double* __restrict__ out,
     uint32_t* __restrict__ flags, int64_t* __restrict__ err_first) {
   constexpr int P = Planes<KIND>::P;
+  PackInfo pk{};
+  if constexpr (KIND == DOOLY_KIND_ATTN_PACKED) {
+    pk = read_pack_header(table, n_sig);
+    if (!pk.ok) n_sig = 0;
+  }
   const int64_t n_words = (n_q + 31) >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n_q; base += stride) {
@@ -204,7 +276,7 @@ __global__ void __launch_bounds__(256) predict_scalar_kernel(
       uint32_t xs[P];
 #pragma unroll
       for (int p = 0; p < P; ++p) xs[p] = x[p * n_q + q];
-      out[q] = eval_query<KIND>(table, n_sig, sig[q], xs, e, c, bad);
+      out[q] = eval_query<KIND>(table, n_sig, sig[q], xs, e, c, bad, pk);
       if (bad && err_first != nullptr)
         atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)q);
     }
@@ -248,8 +320,105 @@ cudaError_t launch_predict(int kind, const void* table, int64_t n_sig, const uin
   if (kind == DOOLY_KIND_AFFINE)
     return launch_predict_kind<DOOLY_KIND_AFFINE>(table, n_sig, sig, x, n_q, out, flags,
                                                   err_first, stream, n_sm);
+  if (kind == DOOLY_KIND_ATTN_PACKED)
+    return launch_predict_kind<DOOLY_KIND_ATTN_PACKED>(table, n_sig, sig, x, n_q, out, flags,
+                                                       err_first, stream, n_sm);
   return launch_predict_kind<DOOLY_KIND_ATTN>(table, n_sig, sig, x, n_q, out, flags, err_first,
                                               stream, n_sm);
+}
+
+// ---- attention table -> packed predict form ------------------------------
+// Pass 1: per-feature max of hi over fitted rows and a count of rows the
+// packed form cannot represent exactly (inv_scale != 1/hi, or lo > hi in a
+// feature) — block-reduced, one atomic per CTA per field.
+__global__ void __launch_bounds__(256) attn_pack_scan_kernel(const dooly_attn_row* __restrict__ t,
+                                                             int64_t n_sig,
+                                                             dooly_attn_pack_header* h) {
+  uint32_t mx[3] = {0u, 0u, 0u}, bad = 0u;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_sig;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const AttnRow r = load_attn(t, (uint32_t)s);
+    if (!attn_valid(r)) continue;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      mx[k] = max(mx[k], r.hi[k]);
+      bad += (r.lo[k] > r.hi[k]) ||
+             (__double_as_longlong(r.inv[k]) != __double_as_longlong(inv_of(r.hi[k])));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mx[k] = max(mx[k], __shfl_xor_sync(0xFFFFFFFFu, mx[k], o));
+    bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+  }
+  __shared__ uint32_t sm[8][4];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sm[w][0] = mx[0];
+    sm[w][1] = mx[1];
+    sm[w][2] = mx[2];
+    sm[w][3] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    uint32_t v = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i)
+      v = threadIdx.x == 3 ? v + sm[i][3] : max(v, sm[i][threadIdx.x]);
+    if (threadIdx.x == 3) {
+      if (v) atomicAdd(&h->bad_inv, v);
+    } else if (v) {
+      atomicMax(&h->max_hi[threadIdx.x], v);
+    }
+  }
+}
+
+// Pass 2: widths from the maxima, rows re-encoded; CTA 0 publishes the header.
+__global__ void __launch_bounds__(256) attn_pack_write_kernel(const dooly_attn_row* __restrict__ t,
+                                                              int64_t n_sig,
+                                                              dooly_attn_pack_header* h) {
+  uint32_t w[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) w[k] = max(1, 32 - __clz((int)h->max_hi[k]));
+  const uint32_t s1 = w[0], s2 = w[0] + w[1];
+  const bool fits = w[0] + w[1] + w[2] <= 64;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    h->width[0] = w[0];
+    h->width[1] = w[1];
+    h->width[2] = w[2];
+    h->n_sig = n_sig;
+    h->ok = (fits && h->bad_inv == 0u) ? 1u : 0u;
+    h->magic = DOOLY_PACK_MAGIC;
+  }
+  dooly_attn_row96* out = reinterpret_cast<dooly_attn_row96*>(h) + 1;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_sig;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const AttnRow r = load_attn(t, (uint32_t)s);
+    uint64_t lb = ~0ull, hb = 0ull;
+    if (attn_valid(r) && fits) {
+      lb = (uint64_t)r.lo[0] | ((uint64_t)r.lo[1] << s1) | ((uint64_t)r.lo[2] << s2);
+      hb = (uint64_t)r.hi[0] | ((uint64_t)r.hi[1] << s1) | ((uint64_t)r.hi[2] << s2);
+    }
+    double2* o = reinterpret_cast<double2*>(out + s);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) o[i] = make_double2(r.c[2 * i], r.c[2 * i + 1]);
+    o[5] = make_double2(__longlong_as_double((long long)lb), __longlong_as_double((long long)hb));
+  }
+}
+
+cudaError_t launch_attn_pack(const void* table, int64_t n_sig, void* packed, cudaStream_t stream,
+                             int n_sm, int64_t* launches) {
+  dooly_attn_pack_header* h = static_cast<dooly_attn_pack_header*>(packed);
+  cudaError_t e = cudaMemsetAsync(h, 0, sizeof(dooly_attn_pack_header), stream);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (n_sig + 255) / 256;
+  if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+  if (blocks < 1) blocks = 1;
+  const dooly_attn_row* t = static_cast<const dooly_attn_row*>(table);
+  attn_pack_scan_kernel<<<(unsigned)blocks, 256, 0, stream>>>(t, n_sig, h);
+  attn_pack_write_kernel<<<(unsigned)blocks, 256, 0, stream>>>(t, n_sig, h);
+  *launches += 2;
+  return cudaGetLastError();
 }
 
 }  // namespace dooly

@@ -177,15 +177,46 @@ def fit(db: LatencyDB, device=None, strict: bool = True) -> Regressors:
 # -------------------------------------------------------------------- predict
 
 
+PACK_HEADER = np.dtype([("magic", "<u4"), ("ok", "<u4"), ("width", "<u4", 3), ("max_hi", "<u4", 3),
+                        ("bad_inv", "<u4"), ("pad_", "<u4"), ("n_sig", "<i8"),
+                        ("reserved", "u1", 48)])
+
+
+def pack_attn(table: torch.Tensor, out: Optional[torch.Tensor] = None,
+              check: bool = True) -> torch.Tensor:
+    """Attention table (n_sig, 128) u8 -> packed predict table (n_sig + 1, 96) u8
+    (``KIND_ATTN_PACKED``: 3 sectors per row, inv_scale recomputed as 1/hi, box
+    bit-packed; include/dooly_b200.h).  Bit-identical predictions.  ``check``
+    syncs and raises ValueError when the table is not representable (box widths
+    over 64 bits, or an inv_scale that is not 1/hi); unchecked, a bad header
+    makes predict flag every query unknown."""
+    if table.dim() != 2 or table.shape[1] != _lib.ATTN_ROW_BYTES:
+        raise ValueError(f"expected an (n_sig, {_lib.ATTN_ROW_BYTES}) attention table")
+    dev = table.device
+    n_sig = table.shape[0]
+    if out is None:
+        out = torch.empty((n_sig + 1, _lib.ATTN96_ROW_BYTES), dtype=torch.uint8, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_attn_pack(
+        ctx, table.data_ptr() if n_sig else 0, n_sig, out.data_ptr(), _lib.stream_ptr(dev)), ctx)
+    if check:
+        h = out[0].cpu().numpy().view(PACK_HEADER)[0]
+        if int(h["ok"]) != 1:
+            raise ValueError(f"attention table not packable: widths {list(h['width'])}, "
+                             f"{int(h['bad_inv'])} rows with inv_scale != 1/hi")
+    return out
+
+
 def predict_batch(kind: int, table: torch.Tensor, sig: torch.Tensor, x: torch.Tensor,
                   out: Optional[torch.Tensor] = None, flags: Optional[torch.Tensor] = None,
                   err_first: Optional[torch.Tensor] = None, want_flags: bool = True):
-    """K3 over n_q queries: sig (n_q,) i32 rows of ``table`` (n_sig, row_bytes) u8,
+    """K3 over n_q queries: sig (n_q,) i32 rows of ``table`` (n_sig, row_bytes) u8
+    (or a ``pack_attn`` table for ``KIND_ATTN_PACKED``),
     x (P, n_q) i32/u32 features.  Returns (out f64 (n_q,), flag bits (2, ceil(n_q/32))
     i32 or None, err_first i64 (1,): INT64_MAX unless some query hit an unknown row)."""
     dev = sig.device
     n_q = sig.numel()
-    n_sig = table.shape[0]
+    n_sig = table.shape[0] - (1 if kind == _lib.KIND_ATTN_PACKED else 0)
     if out is None:
         out = torch.empty(n_q, dtype=torch.float64, device=dev)
     if flags is None and want_flags:

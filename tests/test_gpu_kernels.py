@@ -100,10 +100,15 @@ def test_fit_rank_deficient_drops_columns(dev):
 # -------------------------------------------------------------- predict (K3)
 
 
-def _predict_gpu(kind, rows, sig, x, dev, offset=0):
-    from paper_2605_07985_b200.sim import predict_batch
+PACKED = 2   # KIND_ATTN_PACKED: attention rows repacked to 96 B by dooly_attn_pack
+
+
+def _predict_gpu(kind, rows, sig, x, dev, offset=0, packed=False):
+    from paper_2605_07985_b200.sim import pack_attn, predict_batch
 
     table = torch.from_numpy(rows.view(np.uint8).reshape(len(rows), -1).copy()).to(dev)
+    if packed:
+        table, kind = pack_attn(table), PACKED
     n = sig.shape[0]
     # `offset` elements of misalignment (offset % 4 != 0 exercises the scalar path)
     sbuf = torch.zeros(n + offset, dtype=torch.int32, device=dev)
@@ -120,9 +125,11 @@ def _unpack_bits(words: np.ndarray, n: int) -> np.ndarray:
     return b[:n].astype(bool)
 
 
-@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+@pytest.mark.parametrize("kind", [AFFINE, ATTN, PACKED])
 @pytest.mark.parametrize("n_q,offset", [(1, 0), (127, 0), (4096 * 3 + 5, 0), (1000, 1), (99999, 3)])
 def test_predict_bit_exact(kind, n_q, offset, dev):
+    packed = kind == PACKED
+    kind = ATTN if packed else kind
     x, y, off = synth_fit_data(kind, 257, 64, seed=11 + kind)
     ref_fit = osim.fit(kind, x, y, off)
     table = {k: ref_fit[k] for k in ("coef", "inv", "lo", "hi")}
@@ -130,7 +137,7 @@ def test_predict_bit_exact(kind, n_q, offset, dev):
     table["coef"][7, 0] = -1.0
     rows = table_to_rows(kind, table)
     sig, xq = synth_queries(kind, table, n_q, seed=n_q, outside=0.05)
-    out, flags, err = _predict_gpu(kind, rows, sig, xq, dev, offset)
+    out, flags, err = _predict_gpu(kind, rows, sig, xq, dev, offset, packed)
     ref = osim.predict(kind, table, sig, xq)
     assert err == np.iinfo(np.int64).max
     assert np.array_equal(out.view(np.uint64), ref["out"].view(np.uint64))   # bit-exact
@@ -139,8 +146,10 @@ def test_predict_bit_exact(kind, n_q, offset, dev):
     assert np.array_equal(_unpack_bits(flags[1, :nw], n_q), ref["clamped"])
 
 
-@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+@pytest.mark.parametrize("kind", [AFFINE, ATTN, PACKED])
 def test_predict_unknown_signature(kind, dev):
+    packed = kind == PACKED
+    kind = ATTN if packed else kind
     x, y, off = synth_fit_data(kind, 8, 32, seed=2)
     x[:, : off[3]] = x[:, : off[3]]
     ref_fit = osim.fit(kind, x, y, np.array([0, 2, *off[2:]], dtype=np.int64))  # sig 0: 2 pts
@@ -148,9 +157,39 @@ def test_predict_unknown_signature(kind, dev):
     rows = table_to_rows(kind, table)
     sig = np.array([3, 0, 5, 100, 2], dtype=np.uint32)
     xq = np.tile(table["lo"][3][:, None], (1, 5)).astype(np.uint32)
-    out, _, err = _predict_gpu(kind, rows, sig, xq, dev)
+    out, _, err = _predict_gpu(kind, rows, sig, xq, dev, packed=packed)
     assert err == 1                               # first bad query: unfitted sig 0
     assert np.isnan(out[1]) and np.isnan(out[3]) and np.isfinite(out[0])
+
+
+def test_attn_pack_header_and_refusals(dev):
+    """Pack header fields; tables the 96-B form cannot represent exactly are refused,
+    and an unchecked refused table makes predict flag every query (never mispredict)."""
+    from paper_2605_07985_b200.sim import PACK_HEADER, pack_attn, predict_batch
+
+    x, y, off = synth_fit_data(ATTN, 64, 32, seed=5)
+    ref_fit = osim.fit(ATTN, x, y, off)
+    table = {k: ref_fit[k].copy() for k in ("coef", "inv", "lo", "hi")}
+    t = lambda tb: torch.from_numpy(table_to_rows(ATTN, tb).view(np.uint8).reshape(64, -1).copy()).to(dev)
+    pk = pack_attn(t(table))
+    h = pk[0].cpu().numpy().view(PACK_HEADER)[0]
+    assert int(h["ok"]) == 1 and int(h["n_sig"]) == 64 and int(h["magic"]) == 0x6B504144
+    assert list(h["max_hi"]) == list(table["hi"].max(axis=0))
+    assert list(h["width"]) == [int(v).bit_length() for v in table["hi"].max(axis=0)]
+    bad = {k: v.copy() for k, v in table.items()}
+    bad["inv"][3, 1] = np.nextafter(bad["inv"][3, 1], 1.0)       # not 1/hi
+    with pytest.raises(ValueError):
+        pack_attn(t(bad))
+    wide = {k: v.copy() for k, v in table.items()}
+    wide["hi"][5] = [0xFFFFFFF0, 0xFFFFFFF0, 0xFFFFFFF0]            # 96 box bits > 64
+    wide["inv"][5] = 1.0 / wide["hi"][5].astype(np.float64)
+    with pytest.raises(ValueError):
+        pack_attn(t(wide))
+    pk = pack_attn(t(wide), check=False)
+    sig = torch.zeros(40, dtype=torch.int32, device=dev)
+    xq = torch.zeros((3, 40), dtype=torch.int32, device=dev)
+    out, _, err = predict_batch(PACKED, pk, sig, xq)
+    assert int(err.item()) == 0 and torch.isnan(out).all()
 
 
 def test_predict_scalar_api_raises(dev):
