@@ -1,0 +1,279 @@
+// Ceiling probe for K3 predict: how fast can a B200 gather random table rows
+// when nothing else (no query streams, no evaluation) is in the way?
+//
+//   l2_stream:  every warp streams a small L2-resident buffer (LTS read cap)
+//   gather:     each lane hashes (query index) -> row, loads the row with
+//               LDG.256 (L2::evict_last, L1::no_allocate) exactly like
+//               predict_vec_kernel, and folds it into a checksum
+//
+// Built by tools/gather_probe.py (nvcc -shared); not part of libdooly_b200.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+__device__ __forceinline__ void ld256(const void* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p));
+}
+
+__device__ __forceinline__ uint32_t mix(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return (uint32_t)x;
+}
+
+template <int SECTORS>
+__global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__ table,
+                                                     uint32_t n_rows, int64_t n_q,
+                                                     unsigned long long* sink) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int64_t q = tid; q < n_q; q += stride * 8) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t qq = q + j * stride;
+      const uint32_t r = mix((uint64_t)qq) % n_rows;
+      const uint8_t* p = table + (uint64_t)r * (32 * SECTORS);
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < SECTORS; ++k) {
+        double a, b, c, d;
+        ld256(p + 32 * k, a, b, c, d);
+        s += a + b + c + d;
+      }
+      v[j] = qq < n_q ? s : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc += v[j];
+  }
+  if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+__global__ void __launch_bounds__(256) l2_stream_kernel(const double4* __restrict__ buf,
+                                                        int64_t n4, int reps,
+                                                        unsigned long long* sink) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int r = 0; r < reps; ++r)
+    for (int64_t i = (tid + r * 7919) % n4; i < n4; i += stride) {
+      double a, b, c, d;
+      ld256(buf + i, a, b, c, d);
+      acc += a + b + c + d;
+    }
+  if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+// TMA variant: each lane issues one cp.async.bulk (global -> shared) of its
+// row; one mbarrier per warp-stage counts the bytes; D stages in flight.
+template <int ROW, int D>
+__global__ void __launch_bounds__(128) tma_gather_kernel(const uint8_t* __restrict__ table,
+                                                         uint32_t n_rows, int64_t n_q,
+                                                         unsigned long long* sink) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_warps_cta = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * D;
+  uint8_t* slots = smem + 8 * D * n_warps_cta + (size_t)warp * D * 32 * ROW;
+  if (lane == 0)
+    for (int b = 0; b < D; ++b)
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bars + b)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t gwarp = (blockIdx.x * (int64_t)n_warps_cta + warp);
+  const int64_t n_gwarps = (int64_t)gridDim.x * n_warps_cta;
+  const int64_t n_rounds = (n_q + 31) / 32;
+  double acc = 0.0;
+  auto issue = [&](int64_t round, int b) {
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(bars + b);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(32 * ROW) : "memory");
+    __syncwarp();
+    const int64_t q = round * 32 + lane;
+    const uint32_t r = mix((uint64_t)q) % n_rows;
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(slots + (size_t)b * 32 * ROW + lane * ROW);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(table + (uint64_t)r * ROW), "r"(ROW), "r"(bar)
+        : "memory");
+  };
+  int64_t round = gwarp;
+  for (int b = 0; b < D && round + (int64_t)b * n_gwarps < n_rounds; ++b) issue(round + (int64_t)b * n_gwarps, b);
+  uint32_t phase = 0;
+  for (int b = 0; round < n_rounds; round += n_gwarps) {
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(bars + b);
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(bar), "r"((phase >> b) & 1u) : "memory");
+    phase ^= 1u << b;
+    const double2* row = reinterpret_cast<const double2*>(slots + (size_t)b * 32 * ROW + lane * ROW);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < ROW / 16; ++k) {
+      const double2 v = row[k];
+      s += v.x + v.y;
+    }
+    acc += s;
+    __syncwarp();
+    const int64_t nxt = round + (int64_t)D * n_gwarps;
+    if (nxt < n_rounds) issue(nxt, b);
+    b = (b + 1) % D;
+  }
+  if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+extern "C" int probe_tma_gather(const void* table, uint32_t n_rows, int row_bytes, int depth,
+                                int64_t n_q, void* sink, int blocks, void* stream) {
+  const int warps = 4;
+  const size_t smem = (size_t)warps * depth * (8 + 32 * row_bytes);
+  cudaStream_t s = (cudaStream_t)stream;
+  auto t = static_cast<const uint8_t*>(table);
+  auto k = static_cast<unsigned long long*>(sink);
+#define PROBE_TMA(RB, DD)                                                                   \
+  if (row_bytes == RB && depth == DD) {                                                     \
+    cudaFuncSetAttribute(tma_gather_kernel<RB, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem);                                                        \
+    tma_gather_kernel<RB, DD><<<blocks, 32 * warps, smem, s>>>(t, n_rows, n_q, k);         \
+    return (int)cudaGetLastError();                                                         \
+  }
+  PROBE_TMA(96, 2) PROBE_TMA(96, 4) PROBE_TMA(96, 8) PROBE_TMA(32, 4) PROBE_TMA(32, 8)
+  PROBE_TMA(128, 4)
+#undef PROBE_TMA
+  return 1;
+}
+
+// TMA tile::gather4 variant (sm_100a): lanes 0..7 each fetch 4 rows (those of
+// lanes 4i..4i+3) with ONE bulk-tensor op over a 2-D map {row_words, n_rows}.
+template <int ROW, int D>
+__global__ void __launch_bounds__(128) tma_gather4_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                          uint32_t n_rows, int64_t n_q,
+                                                          unsigned long long* sink) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_warps_cta = blockDim.x >> 5;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * D;
+  uint8_t* slots = smem + 128 * ((8 * D * n_warps_cta + 127) / 128) + (size_t)warp * D * 32 * ROW;
+  if (lane == 0)
+    for (int b = 0; b < D; ++b)
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bars + b)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t gwarp = (blockIdx.x * (int64_t)n_warps_cta + warp);
+  const int64_t n_gwarps = (int64_t)gridDim.x * n_warps_cta;
+  const int64_t n_rounds = (n_q + 31) / 32;
+  double acc = 0.0;
+  auto issue = [&](int64_t round, int b) {
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(bars + b);
+    const int64_t q = round * 32 + lane;
+    const int32_t r = (int32_t)(mix((uint64_t)q) % n_rows);
+    const int32_t r0 = __shfl_sync(0xFFFFFFFFu, r, (lane * 4) & 31);
+    const int32_t r1 = __shfl_sync(0xFFFFFFFFu, r, (lane * 4 + 1) & 31);
+    const int32_t r2 = __shfl_sync(0xFFFFFFFFu, r, (lane * 4 + 2) & 31);
+    const int32_t r3 = __shfl_sync(0xFFFFFFFFu, r, (lane * 4 + 3) & 31);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(32 * ROW) : "memory");
+    __syncwarp();
+    if (lane < 8) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(slots + (size_t)b * 32 * ROW + lane * 4 * ROW);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+          : "memory");
+    }
+  };
+  int64_t round = gwarp;
+  for (int b = 0; b < D && round + (int64_t)b * n_gwarps < n_rounds; ++b) issue(round + (int64_t)b * n_gwarps, b);
+  uint32_t phase = 0;
+  for (int b = 0; round < n_rounds; round += n_gwarps) {
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(bars + b);
+    uint32_t done = 0;
+    for (int spin = 0; !done; ++spin) {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(bar), "r"((phase >> b) & 1u) : "memory");
+      if (spin > 2000000) {   // bounded: a byte-count mismatch must not hang the GPU
+        atomicAdd(sink + 1, 1ull);
+        return;
+      }
+    }
+    phase ^= 1u << b;
+    const double2* row = reinterpret_cast<const double2*>(slots + (size_t)b * 32 * ROW + lane * ROW);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < ROW / 16; ++k) {
+      const double2 v = row[k];
+      s += v.x + v.y;
+    }
+    acc += s;
+    __syncwarp();
+    const int64_t nxt = round + (int64_t)D * n_gwarps;
+    if (nxt < n_rounds) issue(nxt, b);
+    b = (b + 1) % D;
+  }
+  if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+
+extern "C" int probe_tma_gather4(const void* table, uint32_t n_rows, int row_bytes, int depth,
+                                 int64_t n_q, void* sink, int blocks, void* stream) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+    return 100;
+  CUtensorMap tmap;
+  cuuint64_t dims[2] = {(cuuint64_t)(row_bytes / 4), n_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)(row_bytes / 4), 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = ((EncodeTiled)fn)(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(table), dims,
+                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return 200 + (int)cr;
+  const int warps = 4;
+  const size_t smem = 128 * ((8 * depth * warps + 127) / 128) + (size_t)warps * depth * 32 * row_bytes;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto k = static_cast<unsigned long long*>(sink);
+#define PROBE_G4(RB, DD)                                                                    \
+  if (row_bytes == RB && depth == DD) {                                                     \
+    cudaFuncSetAttribute(tma_gather4_kernel<RB, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                         (int)smem);                                                        \
+    tma_gather4_kernel<RB, DD><<<blocks, 32 * warps, smem, s>>>(tmap, n_rows, n_q, k);     \
+    return (int)cudaGetLastError();                                                         \
+  }
+  PROBE_G4(96, 2) PROBE_G4(96, 4) PROBE_G4(32, 4) PROBE_G4(128, 4)
+#undef PROBE_G4
+  return 1;
+}
+
+extern "C" int probe_gather(const void* table, uint32_t n_rows, int sectors, int64_t n_q,
+                            void* sink, int blocks, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  auto t = static_cast<const uint8_t*>(table);
+  auto k = static_cast<unsigned long long*>(sink);
+  switch (sectors) {
+    case 1: gather_kernel<1><<<blocks, 256, 0, s>>>(t, n_rows, n_q, k); break;
+    case 3: gather_kernel<3><<<blocks, 256, 0, s>>>(t, n_rows, n_q, k); break;
+    case 4: gather_kernel<4><<<blocks, 256, 0, s>>>(t, n_rows, n_q, k); break;
+    default: return 1;
+  }
+  return (int)cudaGetLastError();
+}
+
+extern "C" int probe_l2_stream(const void* buf, int64_t bytes, int reps, void* sink, int blocks,
+                               void* stream) {
+  l2_stream_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const double4*>(buf), bytes / 32, reps, static_cast<unsigned long long*>(sink));
+  return (int)cudaGetLastError();
+}

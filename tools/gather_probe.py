@@ -1,0 +1,131 @@
+"""Measure the random-row gather ceiling that bounds K3 predict (and the L2
+read cap) on this B200.
+
+    python tools/gather_probe.py            # builds tools/_build/gather_probe.so first if needed
+
+For each row size used by the predict tables (32 B affine, 96 B packed
+attention, 128 B attention) and table sizes matching the C5 bench, prints
+rows/s and gathered bytes/s.  Compare with bench.py's per-kind kernel_ms."""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "_build", "gather_probe.so")
+
+
+def build() -> None:
+    os.makedirs(os.path.dirname(SO), exist_ok=True)
+    src = os.path.join(HERE, "gather_probe.cu")
+    if os.path.exists(SO) and os.path.getmtime(SO) >= os.path.getmtime(src):
+        return
+    subprocess.check_call(["nvcc", "-O3", "-gencode", "arch=compute_100a,code=sm_100a",
+                           "-shared", "-Xcompiler", "-fPIC", "--cudart", "static", "-o", SO, src])
+
+
+def main() -> None:
+    build()
+    lib = C.CDLL(SO)
+    lib.probe_gather.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_int64, C.c_void_p, C.c_int,
+                                 C.c_void_p]
+    lib.probe_tma_gather.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_int, C.c_int64,
+                                     C.c_void_p, C.c_int, C.c_void_p]
+    lib.probe_tma_gather4.argtypes = lib.probe_tma_gather.argtypes
+    lib.probe_l2_stream.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
+    dev = torch.device("cuda", 0)
+    only = set(sys.argv[1:])
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.zeros(2, dtype=torch.int64, device=dev)   # [checksum hits, timeouts]
+    st = torch.cuda.current_stream().cuda_stream
+
+    def timed(fn, reps=5):
+        fn()
+        ms = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        return sorted(ms)[len(ms) // 2]
+
+    if "gather4" in only:
+        gather4(lib, dev, n_sm, sink, st, timed)
+        return
+    for mb in (16, 48):
+        buf = torch.rand((mb << 20) // 8, dtype=torch.float64, device=dev)
+        reps = 20
+        for blocks in (n_sm * 4, n_sm * 8):
+            ms = timed(lambda: lib.probe_l2_stream(buf.data_ptr(), buf.numel() * 8, reps,
+                                                   sink.data_ptr(), blocks, st))
+            print(json.dumps({"probe": "l2_stream", "buffer_mb": mb, "blocks": blocks,
+                              "gb_per_s": buf.numel() * 8 * reps / ms / 1e6}), flush=True)
+        del buf
+    n_q = 500_000_000
+    for sectors, rows in ((1, 500_000), (3, 500_000), (4, 500_000), (3, 1_000_000),
+                          (4, 1_000_000), (3, 250_000)):
+        table = torch.rand((rows * sectors * 32) // 8, dtype=torch.float64, device=dev)
+        for blocks in (n_sm * 8,):
+            ms = timed(lambda: lib.probe_gather(table.data_ptr(), rows, sectors, n_q,
+                                                sink.data_ptr(), blocks, st))
+            print(json.dumps({"probe": "gather", "row_bytes": 32 * sectors, "rows": rows,
+                              "table_mb": rows * sectors * 32 / 2**20, "ms": ms,
+                              "g_rows_per_s": n_q / ms / 1e6,
+                              "gb_per_s": n_q * 32 * sectors / ms / 1e6}), flush=True)
+        del table
+    for rb, rows in ((96, 500_000), (32, 500_000), (128, 500_000)):
+        table = torch.rand((rows * rb) // 8, dtype=torch.float64, device=dev)
+        for depth in (2, 4, 8):
+            for per_sm in (2, 4, 8):
+                smem = 4 * depth * (8 + 32 * rb)
+                if smem * per_sm > 220 * 1024:
+                    continue
+                rc = lib.probe_tma_gather(table.data_ptr(), rows, rb, depth, n_q, sink.data_ptr(),
+                                          n_sm * per_sm, st)
+                if rc != 0:
+                    continue
+                ms = timed(lambda: lib.probe_tma_gather(table.data_ptr(), rows, rb, depth, n_q,
+                                                        sink.data_ptr(), n_sm * per_sm, st))
+                print(json.dumps({"probe": "tma_gather", "row_bytes": rb, "rows": rows,
+                                  "depth": depth, "ctas_per_sm": per_sm, "ms": ms,
+                                  "g_rows_per_s": n_q / ms / 1e6,
+                                  "gb_per_s": n_q * rb / ms / 1e6}), flush=True)
+        del table
+
+
+def gather4(lib, dev, n_sm, sink, st, timed):
+    n_q = 500_000_000
+    for rb, rows in ((96, 500_000), (32, 500_000), (128, 500_000)):
+        table = torch.rand((rows * rb) // 8, dtype=torch.float64, device=dev)
+        for depth in (2, 4):
+            for per_sm in (2, 4, 8):
+                smem = 4 * depth * 32 * rb + 128
+                if smem * per_sm > 220 * 1024:
+                    continue
+                rc = lib.probe_tma_gather4(table.data_ptr(), rows, rb, depth, 1 << 20,
+                                           sink.data_ptr(), n_sm * per_sm, st)
+                torch.cuda.synchronize()
+                if rc != 0 or int(sink[1].item()):
+                    print(json.dumps({"probe": "tma_gather4", "row_bytes": rb, "depth": depth,
+                                      "rc": rc, "timeouts": int(sink[1].item())}), flush=True)
+                    sink.zero_()
+                    continue
+                ms = timed(lambda: lib.probe_tma_gather4(table.data_ptr(), rows, rb, depth, n_q,
+                                                         sink.data_ptr(), n_sm * per_sm, st))
+                print(json.dumps({"probe": "tma_gather4", "row_bytes": rb, "rows": rows,
+                                  "depth": depth, "ctas_per_sm": per_sm, "ms": ms,
+                                  "g_rows_per_s": n_q / ms / 1e6, "timeouts": int(sink[1].item()),
+                                  "gb_per_s": n_q * rb / ms / 1e6}), flush=True)
+        del table
+
+
+if __name__ == "__main__":
+    sys.exit(main())

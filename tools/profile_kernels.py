@@ -1,6 +1,6 @@
 """Launch every libdooly_b200 hot kernel on C5-shaped inputs, for ncu.
 
-    ncu --set full --import-source on -k regex:'fit_bulk|predict_vec|sha256_rec|dedup_insert|sim_run' \
+    ncu --set full --import-source on -k regex:'fit_stage|fit_moments_attn|fit_mape_attn|predict_vec|sha256_rec|dedup_insert|sim_run' \
         -c 16 -o gpurun_out/prof python tools/profile_kernels.py
 
 Sizes are scaled down from bench.py (same shapes per unit) so a full ncu
@@ -32,7 +32,7 @@ def main() -> None:
 
     import bench
     from paper_2605_07985_b200.profiler import DedupWorkspace, DeviceRecords, dedup_packed
-    from paper_2605_07985_b200.sim import fit_tables, predict_batch
+    from paper_2605_07985_b200.sim import fit_tables, pack_attn, predict_batch
 
     dev = torch.device("cuda", 0)
     only = set(args.only.split(","))
@@ -52,9 +52,12 @@ def main() -> None:
             reps = max(1, 500_000 // tables[kind].shape[0])
             table = tables[kind].repeat(reps, 1)
             sig, xq = bench.gen_queries(kind, table, args.queries // 2, dev, seed=7)
+            pk = kind
+            if kind == 1:   # the serving form bench.py times (96-B packed rows)
+                table, pk = pack_attn(table), 2
             out = torch.empty(sig.numel(), dtype=torch.float64, device=dev)
             for _ in range(args.repeat):
-                predict_batch(kind, table, sig, xq, out)
+                predict_batch(pk, table, sig, xq, out)
             del sig, xq, out
     if "dedup" in only:
         packed, _ = bench.synth_records(args.records, seed=1)
