@@ -110,6 +110,48 @@ def gen_fit_data(kind: int, n_sig: int, n_pts: int, dev, seed: int):
     return x, y, off
 
 
+def grid_points(kind: int, n_pts: int):
+    """C5 sweep grid shared by every signature of a kind (BASELINE.json configs[4]):
+    affine — n_pts token counts evenly spanning [1, 32768]; attention — a
+    side^3 (prefill_toks, batch, kv_tokens) grid, side = n_pts^(1/3) (16 for 4096)."""
+    if kind == AFFINE:
+        return np.rint(np.linspace(1, 32768, n_pts)).astype(np.uint32)[None, :]
+    side = max(2, round(n_pts ** (1.0 / 3.0)))
+    t = np.rint(np.geomspace(1, 32768, side)).astype(np.int64)
+    b = np.rint(np.geomspace(1, 256, side)).astype(np.int64)
+    k = np.rint(np.linspace(0, 1 << 22, side)).astype(np.int64)
+    g = np.stack(np.meshgrid(t, b, k, indexing="ij")).reshape(3, -1)
+    return g.astype(np.uint32)
+
+
+def gen_grid_fit_data(kind: int, n_sig: int, n_pts: int, dev, seed: int):
+    """Shared-grid C5 fit input: x (P, n) int32 on device, y (n_sig, n) f64 with
+    y = positive per-signature polynomial x (1 + N(0, 1e-3))."""
+    import torch
+
+    xg = grid_points(kind, n_pts)
+    n = xg.shape[1]
+    x = torch.from_numpy(xg.view(np.int32)).to(dev)
+    xf = x.view(torch.int32).double()
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    y = torch.empty((n_sig, n), dtype=torch.float64, device=dev)
+    chunk = max(1, (1 << 26) // n)
+    for s0 in range(0, n_sig, chunk):
+        m = min(n_sig, s0 + chunk) - s0
+        if kind == AFFINE:
+            a = torch.empty((m, 1), dtype=torch.float64, device=dev).uniform_(5e-6, 2e-5, generator=g)
+            b = torch.empty((m, 1), dtype=torch.float64, device=dev).uniform_(1e-9, 1e-7, generator=g)
+            yv = a + b * xf[0]
+        else:
+            c = torch.empty((m, 3), dtype=torch.float64, device=dev).uniform_(1e-12, 1e-9, generator=g)
+            yv = (1e-5 + c[:, 0:1] * xf[0] + c[:, 1:2] * xf[1] * 100 + c[:, 2:3] * xf[2]
+                  + 1e-15 * xf[0] * xf[0] + 1e-16 * xf[0] * xf[2])
+        eps = torch.randn((m, n), generator=g, device=dev, dtype=torch.float64)
+        y[s0:s0 + m] = (yv * (1.0 + 1e-3 * eps)).abs() + 1e-9
+    return x, y
+
+
 def gen_queries(kind: int, table, n_q: int, dev, seed: int):
     """Uniform signature; features uniform inside that signature's box."""
     import torch

@@ -155,6 +155,17 @@ int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const 
               const int64_t* pt_off, int64_t n_sig, void* table, double* fit_err,
               uint8_t* status, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Shared-grid fit: every signature was swept over the SAME n_pts points x
+ * (feature-major planes of n_pts u32, the sweep grid of SPEC.md:466-474);
+ * y is row-major (n_sig, n_pts) f64.  Same rows, fit_err and statuses as
+ * dooly_fit with pt_off[s] = s * n_pts and x repeated per signature, but the
+ * Gram matrix, its factor, the scaling and the box are built once.
+ * Workspace: dooly_fit_grid_workspace_size() bytes of device memory. */
+size_t dooly_fit_grid_workspace_size(void);
+int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
+                   int64_t n_sig, void* table, double* fit_err, uint8_t* status, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------- K3 predict
  * Replaces predict.  sig[i] indexes the table; x is
  * feature-major (planes of n_q u32).  out[i] = max(poly, 1e-7) evaluated

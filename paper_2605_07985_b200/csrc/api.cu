@@ -17,6 +17,10 @@ cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double*
                        uint8_t* status, void* ws, cudaStream_t stream, int n_sm,
                        int64_t* launches);
 size_t fit_workspace_size(int kind, int64_t n_sig);
+size_t fit_grid_workspace_size();
+cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
+                            int64_t n_sig, void* table, double* fit_err, uint8_t* status,
+                            void* ws, cudaStream_t stream, int n_sm, int64_t* launches);
 cudaError_t launch_attn_pack(const void* table, int64_t n_sig, void* packed, cudaStream_t stream,
                              int n_sm, int64_t* launches);
 cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off, int64_t n,
@@ -172,6 +176,30 @@ int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const 
                                       workspace, (cudaStream_t)stream, ctx->n_sm,
                                       &ctx->launches),
                     "fit");
+}
+
+size_t dooly_fit_grid_workspace_size(void) { return dooly::fit_grid_workspace_size(); }
+
+int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
+                   int64_t n_sig, void* table, double* fit_err, uint8_t* status, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: unknown kind");
+  if (n_sig < 0 || n_pts < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: negative size");
+  if (!workspace || workspace_bytes < dooly::fit_grid_workspace_size() ||
+      (uintptr_t)workspace % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: workspace too small or misaligned");
+  if ((n_pts > 0 && !x) || (n_sig > 0 && (!table || !fit_err || !status || (n_pts > 0 && !y))))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: null pointer");
+  if ((uintptr_t)table % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: table must be 16-byte aligned");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_fit_grid(kind, x, n_pts, y, n_sig, table, fit_err, status,
+                                           workspace, (cudaStream_t)stream, ctx->n_sm,
+                                           &ctx->launches),
+                    "fit_grid");
 }
 
 int dooly_sha256_records(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off,

@@ -1,0 +1,641 @@
+// K2g — shared-grid fit (dooly_fit_grid): the fit of SPEC.md:556-564 for the
+// common case where every signature of a batch was swept over the SAME points
+// (one sweep grid per model/backend; the C5 scale sweep).
+//
+// With a shared design matrix M (n_pts x p) the normal-equation Gram M^T M,
+// its Cholesky-with-drop factor, the scaling (inv = 1/max x) and the training
+// box are the same for every signature, so they are computed ONCE
+// (fit_grid_prep_kernel, one CTA).  Per signature only X^T y remains:
+//   pass 1  b = M^T y          (p FMAs per point)
+//   solve   L L^T c = b        (shared factor, dropped columns stay 0)
+//   pass 2  training MAPE      (p FMAs + reciprocal per point)
+// versus ~95 FP64 instructions per point for the per-signature Gram path
+// (fit.cu).  Register blocking: a 256-thread CTA owns R signatures at a time,
+// every thread walks a strided subset of the points and recomputes that
+// point's monomials once for all R signatures (x is 4-12 B per point, shared
+// by all CTAs through L1/L2).  y rows are read with default caching so the
+// pass-2 re-read of the R rows a CTA just streamed hits L2.
+//
+// Result contract: identical to dooly_fit with pt_off[s] = s * n_pts and x
+// repeated per signature — coefficients within 1e-9 normwise, fit_err within
+// 1e-9 relative (tests/test_gpu_fit_grid.py), same row layout and statuses.
+#include <stdlib.h>
+
+#include "common.cuh"
+
+namespace dooly {
+
+constexpr double kGridDropTol = 1e-9;  // App. A.7, same rule as fit.cu
+constexpr int kGT = 256;
+constexpr int kGW = kGT / 32;
+
+template <int KIND>
+struct GridTraits;
+template <>
+struct GridTraits<DOOLY_KIND_AFFINE> {
+  static constexpr int P = 1, NC = 2, NEED = 4, R = 8, RS = 3;
+};
+template <>
+struct GridTraits<DOOLY_KIND_ATTN> {
+  static constexpr int P = 3, NC = 10, NEED = 11, R = 4, RS = 3;
+};
+constexpr size_t kGridStageMax = 96 * 1024;  // y bytes staged per CTA (2 CTAs/SM)
+
+struct GridFactor {
+  double L[10][10];  // lower Cholesky factor; dropped columns are zero
+  double rd[10];     // 1 / L[j][j], 0 for a dropped column
+  double inv[3];
+  uint32_t lo[3], hi[3];
+  int32_t ok;        // n_pts >= need
+  int32_t pad_;
+};
+
+__device__ __forceinline__ double g_u2d(uint32_t x) {
+  return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+}
+
+__device__ __forceinline__ double g_rcp(double y) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  double e = fma(-y, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-y, r, 1.0);
+  return fma(r, e, r);
+}
+
+// One Newton step on the hardware estimate: ~2^-44 relative, ample for the
+// training-MAPE diagnostic (1e-9 contract).
+__device__ __forceinline__ double g_rcp1(double y) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  return fma(r, fma(-y, r, 1.0), r);
+}
+
+template <typename T>
+__device__ __forceinline__ T g_warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+// Design columns in eval order (common.cuh eval_attn): [1,f1,f2,f3,f1²,f2²,f3²,f1f2,f1f3,f2f3].
+template <int KIND>
+__device__ __forceinline__ void grid_monomials(const uint32_t* xs, const double* inv, double* m) {
+  if constexpr (KIND == DOOLY_KIND_AFFINE) {
+    m[0] = 1.0;
+    m[1] = g_u2d(xs[0]) * inv[0];
+  } else {
+    const double f1 = g_u2d(xs[0]) * inv[0], f2 = g_u2d(xs[1]) * inv[1],
+                 f3 = g_u2d(xs[2]) * inv[2];
+    m[0] = 1.0;
+    m[1] = f1;
+    m[2] = f2;
+    m[3] = f3;
+    m[4] = f1 * f1;
+    m[5] = f2 * f2;
+    m[6] = f3 * f3;
+    m[7] = f1 * f2;
+    m[8] = f1 * f3;
+    m[9] = f2 * f3;
+  }
+}
+
+// One CTA: box, scaling, Gram of the shared design, Cholesky with drop.
+template <int KIND>
+__global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __restrict__ x,
+                                                            int64_t n_pts, GridFactor* gf) {
+  using T = GridTraits<KIND>;
+  constexpr int P = T::P, NC = T::NC, NT = NC * (NC + 1) / 2;
+  __shared__ uint32_t smn[kGW][3], smx[kGW][3];
+  __shared__ double sg[kGW][NT];
+  __shared__ double G[NC][NC];
+  __shared__ double sinv[3];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t mn[P], mx[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    mn[k] = 0xFFFFFFFFu;
+    mx[k] = 0u;
+  }
+  for (int64_t p = tid; p < n_pts; p += kGT)
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const uint32_t v = x[k * n_pts + p];
+      mn[k] = min(mn[k], v);
+      mx[k] = max(mx[k], v);
+    }
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
+    const uint32_t a = __reduce_min_sync(0xFFFFFFFFu, mn[k]);
+    const uint32_t b = __reduce_max_sync(0xFFFFFFFFu, mx[k]);
+    if (lane == 0) {
+      smn[wid][k] = a;
+      smx[wid][k] = b;
+    }
+  }
+  __syncthreads();
+  if (tid < P) {
+    uint32_t a = 0xFFFFFFFFu, b = 0u;
+    for (int w = 0; w < kGW; ++w) {
+      a = min(a, smn[w][tid]);
+      b = max(b, smx[w][tid]);
+    }
+    gf->lo[tid] = a;
+    gf->hi[tid] = b;
+    const double iv = b > 0 ? 1.0 / (double)b : 1.0;  // IEEE division, as the oracle
+    gf->inv[tid] = iv;
+    sinv[tid] = iv;
+  }
+  __syncthreads();
+  double inv[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) inv[k] = sinv[k];
+  double acc[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) acc[i] = 0.0;
+  for (int64_t p = tid; p < n_pts; p += kGT) {
+    uint32_t xs[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) xs[k] = x[k * n_pts + p];
+    double m[NC];
+    grid_monomials<KIND>(xs, inv, m);
+    int t = 0;
+#pragma unroll
+    for (int i = 0; i < NC; ++i)
+#pragma unroll
+      for (int j = i; j < NC; ++j) acc[t] = fma(m[i], m[j], acc[t]), ++t;
+  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const double v = g_warp_sum(acc[i]);
+    if (lane == 0) sg[wid][i] = v;
+  }
+  __syncthreads();
+  if (tid < NT) {
+    int i = 0, t = tid;
+    while (t >= NC - i) {
+      t -= NC - i;
+      ++i;
+    }
+    const int j = i + t;
+    double v = 0.0;
+    for (int w = 0; w < kGW; ++w) v += sg[w][tid];
+    G[i][j] = v;
+    G[j][i] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double diag[NC];
+    for (int j = 0; j < NC; ++j) diag[j] = G[j][j];
+    for (int j = 0; j < NC; ++j) {
+      const double piv = G[j][j];
+      const bool keep = piv > kGridDropTol * diag[j];
+      const double d = keep ? sqrt(piv) : 0.0;
+      const double id = keep ? 1.0 / d : 0.0;
+      gf->rd[j] = id;
+      for (int i = 0; i < NC; ++i) gf->L[i][j] = i < j ? 0.0 : (i == j ? d : G[i][j] * id);
+      for (int k = j + 1; k < NC; ++k)
+        for (int i = k; i < NC; ++i) G[i][k] = fma(-gf->L[i][j], gf->L[k][j], G[i][k]);
+    }
+    for (int i = NC; i < 10; ++i) gf->rd[i] = 0.0;
+    gf->ok = n_pts >= T::NEED ? 1 : 0;
+  }
+}
+
+template <int KIND>
+__device__ void write_unfitted_grid(void* table, int64_t s, double* fit_err, uint8_t* status) {
+  if constexpr (KIND == DOOLY_KIND_AFFINE) {
+    dooly_affine_row* row = static_cast<dooly_affine_row*>(table) + s;
+    row->c0 = row->c1 = row->inv_scale = nan64();
+    row->lo = 0xFFFFFFFFu;
+    row->hi = 0;
+  } else {
+    dooly_attn_row* row = static_cast<dooly_attn_row*>(table) + s;
+    for (int i = 0; i < 10; ++i) row->c[i] = nan64();
+    for (int k = 0; k < 3; ++k) {
+      row->inv_scale[k] = nan64();
+      row->lo[k] = 0xFFFFFFFFu;
+      row->hi[k] = 0;
+    }
+  }
+  fit_err[s] = nan64();
+  status[s] = DOOLY_FIT_INSUFFICIENT;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kGT, 2) fit_grid_kernel(
+    const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
+    const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
+    uint8_t* __restrict__ status) {
+  using T = GridTraits<KIND>;
+  constexpr int P = T::P, NC = T::NC, R = T::R;
+  __shared__ double sL[NC][NC], srd[NC], sinv[P];
+  __shared__ uint32_t slo[P], shi[P];
+  __shared__ double part[kGW][R * NC];
+  __shared__ double scoef[R][NC];
+  __shared__ double serr[kGW][R];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int t = tid; t < NC * NC; t += kGT) sL[t / NC][t % NC] = gf->L[t / NC][t % NC];
+  if (tid < NC) srd[tid] = gf->rd[tid];
+  if (tid < P) {
+    sinv[tid] = gf->inv[tid];
+    slo[tid] = gf->lo[tid];
+    shi[tid] = gf->hi[tid];
+  }
+  const bool ok = gf->ok != 0;
+  __syncthreads();
+  double inv[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) inv[k] = sinv[k];
+  const int64_t n_groups = (n_sig + R - 1) / R;
+  for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+    const int64_t s0 = g * R;
+    const int nr = (int)min((int64_t)R, n_sig - s0);
+    if (!ok) {
+      if (tid < nr) write_unfitted_grid<KIND>(table, s0 + tid, fit_err, status);
+      continue;
+    }
+    const double* yg = y + s0 * n_pts;
+    // ---- pass 1: b = M^T y for R signatures
+    double acc[R][NC];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) acc[r][k] = 0.0;
+    for (int64_t p = tid; p < n_pts; p += kGT) {
+      uint32_t xs[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) xs[k] = __ldg(x + k * n_pts + p);
+      double yv[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) yv[r] = r < nr ? yg[r * n_pts + p] : 0.0;
+      double m[NC];
+      grid_monomials<KIND>(xs, inv, m);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int k = 0; k < NC; ++k) acc[r][k] = fma(yv[r], m[k], acc[r][k]);
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const double v = g_warp_sum(acc[r][k]);
+        if (lane == 0) part[wid][r * NC + k] = v;
+      }
+    __syncthreads();
+    // ---- solve with the shared factor (thread r owns signature r)
+    if (tid < nr) {
+      double z[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kGW; ++w) t += part[w][tid * NC + j];
+#pragma unroll
+        for (int i = 0; i < j; ++i) t = fma(-sL[j][i], z[i], t);
+        z[j] = t * srd[j];
+      }
+#pragma unroll
+      for (int j = NC - 1; j >= 0; --j) {
+        double t = z[j];
+#pragma unroll
+        for (int i = j + 1; i < NC; ++i) t = fma(-sL[i][j], scoef[tid][i], t);
+        scoef[tid][j] = t * srd[j];
+      }
+    }
+    __syncthreads();
+    // ---- pass 2: training MAPE (y rows re-read, normally from L2)
+    double c[R][NC], err[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      err[r] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) c[r][k] = scoef[r][k];
+    }
+    for (int64_t p = tid; p < n_pts; p += kGT) {
+      uint32_t xs[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) xs[k] = __ldg(x + k * n_pts + p);
+      double yv[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) yv[r] = r < nr ? yg[r * n_pts + p] : 1.0;
+      double m[NC];
+      grid_monomials<KIND>(xs, inv, m);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        double pr = c[r][0];
+#pragma unroll
+        for (int k = 1; k < NC; ++k) pr = fma(c[r][k], m[k], pr);
+        pr = fmax(pr, DOOLY_CLAMP_FLOOR);
+        err[r] = fma(fabs(pr - yv[r]), g_rcp(yv[r]), err[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double v = g_warp_sum(err[r]);
+      if (lane == 0) serr[wid][r] = v;
+    }
+    __syncthreads();
+    if (tid < nr) {
+      double e = 0.0;
+#pragma unroll
+      for (int w = 0; w < kGW; ++w) e += serr[w][tid];
+      const int64_t s = s0 + tid;
+      fit_err[s] = e / (double)n_pts;
+      status[s] = DOOLY_FIT_OK;
+      if constexpr (KIND == DOOLY_KIND_AFFINE) {
+        dooly_affine_row* row = static_cast<dooly_affine_row*>(table) + s;
+        row->c0 = scoef[tid][0];
+        row->c1 = scoef[tid][1];
+        row->inv_scale = sinv[0];
+        row->lo = slo[0];
+        row->hi = shi[0];
+      } else {
+        dooly_attn_row* row = static_cast<dooly_attn_row*>(table) + s;
+#pragma unroll
+        for (int i = 0; i < 10; ++i) row->c[i] = scoef[tid][i];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          row->inv_scale[k] = sinv[k];
+          row->lo[k] = slo[k];
+          row->hi[k] = shi[k];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---- staged variant: the R signatures' y rows are bulk-copied (1-D TMA) into
+// shared memory in two point-halves, so both passes read smem and y crosses
+// HBM exactly once (8 B/point).  The next group's first half is copied in as
+// soon as pass 2 has released it.
+__device__ __forceinline__ uint32_t g_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void g_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          g_smem(dst)),
+      "l"(src), "r"(bytes), "r"(g_smem(bar))
+      : "memory");
+}
+__device__ __forceinline__ void g_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(g_smem(bar)), "r"(parity)
+        : "memory");
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
+    const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
+    const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
+    uint8_t* __restrict__ status) {
+  using T = GridTraits<KIND>;
+  constexpr int P = T::P, NC = T::NC, R = T::RS;
+  extern __shared__ __align__(128) unsigned char gdyn[];
+  double* stage = reinterpret_cast<double*>(gdyn);  // [R][n_pts]
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ double sL[NC][NC], srd[NC], sinv[P];
+  __shared__ uint32_t slo[P], shi[P];
+  __shared__ double part[kGW][R * NC];
+  __shared__ double scoef[R][NC];
+  __shared__ double serr[kGW][R];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t half = n_pts / 2;  // n_pts % 4 == 0 (launcher)
+  const int n = (int)n_pts;        // stage <= 96 KB, so n_pts <= 12288
+  const int64_t n_groups = (n_sig + R - 1) / R;
+  for (int t = tid; t < NC * NC; t += kGT) sL[t / NC][t % NC] = gf->L[t / NC][t % NC];
+  if (tid < NC) srd[tid] = gf->rd[tid];
+  if (tid < P) {
+    sinv[tid] = gf->inv[tid];
+    slo[tid] = gf->lo[tid];
+    shi[tid] = gf->hi[tid];
+  }
+  const bool ok = gf->ok != 0;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(g_smem(&bar[0])));
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(g_smem(&bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t g, int c) {  // thread 0: half c of group g
+    const int64_t s0 = g * R;
+    const int nr = (int)min((int64_t)R, n_sig - s0);
+    const uint32_t bytes = (uint32_t)(half * 8);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(g_smem(&bar[c])),
+                 "r"(bytes * nr)
+                 : "memory");
+    for (int r = 0; r < nr; ++r)
+      g_bulk(stage + r * n_pts + c * half, y + (s0 + r) * n_pts + c * half, bytes, &bar[c]);
+  };
+  double inv[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) inv[k] = sinv[k];
+  if (!ok) {
+    for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+      const int nr = (int)min((int64_t)R, n_sig - g * R);
+      if (tid < nr) write_unfitted_grid<KIND>(table, g * R + tid, fit_err, status);
+    }
+    return;
+  }
+  if (tid == 0 && blockIdx.x < n_groups) {
+    issue(blockIdx.x, 0);
+    issue(blockIdx.x, 1);
+  }
+  uint32_t par[2] = {0u, 0u};
+  for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+    const int64_t s0 = g * R;
+    const int nr = (int)min((int64_t)R, n_sig - s0);
+    const int64_t gn = g + gridDim.x;
+    double acc[R][NC];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) acc[r][k] = 0.0;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      g_wait(&bar[c], par[c]);
+      par[c] ^= 1u;
+      // two consecutive points per thread: 8-B x loads, 16-B y loads, 32-bit indices
+      for (int p = (int)(c * half) + 2 * tid; p < (int)((c + 1) * half); p += 2 * kGT) {
+        uint32_t xa[P], xb[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(x + k * n + p));
+          xa[k] = v.x;
+          xb[k] = v.y;
+        }
+        double ma[NC], mb[NC];
+        grid_monomials<KIND>(xa, inv, ma);
+        grid_monomials<KIND>(xb, inv, mb);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double2 yv =
+              r < nr ? *reinterpret_cast<const double2*>(stage + r * n + p) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int k = 0; k < NC; ++k) acc[r][k] = fma(yv.y, mb[k], fma(yv.x, ma[k], acc[r][k]));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        const double v = g_warp_sum(acc[r][k]);
+        if (lane == 0) part[wid][r * NC + k] = v;
+      }
+    __syncthreads();
+    if (tid < nr) {
+      double z[NC];
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kGW; ++w) t += part[w][tid * NC + j];
+#pragma unroll
+        for (int i = 0; i < j; ++i) t = fma(-sL[j][i], z[i], t);
+        z[j] = t * srd[j];
+      }
+#pragma unroll
+      for (int j = NC - 1; j >= 0; --j) {
+        double t = z[j];
+#pragma unroll
+        for (int i = j + 1; i < NC; ++i) t = fma(-sL[i][j], scoef[tid][i], t);
+        scoef[tid][j] = t * srd[j];
+      }
+    }
+    __syncthreads();
+    double cf[R][NC], err[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      err[r] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) cf[r][k] = scoef[r][k];
+    }
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      for (int p = (int)(c * half) + 2 * tid; p < (int)((c + 1) * half); p += 2 * kGT) {
+        uint32_t xa[P], xb[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(x + k * n + p));
+          xa[k] = v.x;
+          xb[k] = v.y;
+        }
+        double ma[NC], mb[NC];
+        grid_monomials<KIND>(xa, inv, ma);
+        grid_monomials<KIND>(xb, inv, mb);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double2 yv =
+              r < nr ? *reinterpret_cast<const double2*>(stage + r * n + p) : make_double2(1.0, 1.0);
+          double pa = cf[r][0], pb = cf[r][0];
+#pragma unroll
+          for (int k = 1; k < NC; ++k) {
+            pa = fma(cf[r][k], ma[k], pa);
+            pb = fma(cf[r][k], mb[k], pb);
+          }
+          pa = fmax(pa, DOOLY_CLAMP_FLOOR);
+          pb = fmax(pb, DOOLY_CLAMP_FLOOR);
+          err[r] = fma(fabs(pa - yv.x), g_rcp1(yv.x), err[r]);
+          err[r] = fma(fabs(pb - yv.y), g_rcp1(yv.y), err[r]);
+        }
+      }
+      if (c == 0) {
+        __syncthreads();  // half 0 released: stream in the next group's first half
+        if (tid == 0 && gn < n_groups) issue(gn, 0);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double v = g_warp_sum(err[r]);
+      if (lane == 0) serr[wid][r] = v;
+    }
+    __syncthreads();  // half 1 released
+    if (tid == 0 && gn < n_groups) issue(gn, 1);
+    if (tid < nr) {
+      double e = 0.0;
+#pragma unroll
+      for (int w = 0; w < kGW; ++w) e += serr[w][tid];
+      const int64_t s = s0 + tid;
+      fit_err[s] = e / (double)n_pts;
+      status[s] = DOOLY_FIT_OK;
+      if constexpr (KIND == DOOLY_KIND_AFFINE) {
+        dooly_affine_row* row = static_cast<dooly_affine_row*>(table) + s;
+        row->c0 = scoef[tid][0];
+        row->c1 = scoef[tid][1];
+        row->inv_scale = sinv[0];
+        row->lo = slo[0];
+        row->hi = shi[0];
+      } else {
+        dooly_attn_row* row = static_cast<dooly_attn_row*>(table) + s;
+#pragma unroll
+        for (int i = 0; i < 10; ++i) row->c[i] = scoef[tid][i];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          row->inv_scale[k] = sinv[k];
+          row->lo[k] = slo[k];
+          row->hi[k] = shi[k];
+        }
+      }
+    }
+    __syncthreads();  // scoef / part reused by the next group
+  }
+}
+
+template <int KIND>
+static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const double* y, int64_t n_sig,
+                             void* table, double* fit_err, uint8_t* status, void* ws,
+                             cudaStream_t stream, int n_sm, int64_t* launches) {
+  GridFactor* gf = static_cast<GridFactor*>(ws);
+  fit_grid_prep_kernel<KIND><<<1, kGT, 0, stream>>>(x, n_pts, gf);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  *launches += 1;
+  if (n_sig == 0) return cudaSuccess;
+  const size_t stage = (size_t)GridTraits<KIND>::RS * n_pts * 8;
+  static const bool no_stage = getenv("DOOLY_FIT_GRID_NO_STAGE") != nullptr;
+  if (!no_stage && stage <= kGridStageMax && n_pts % 4 == 0 && (uintptr_t)y % 16 == 0) {
+    auto kern = fit_grid_stage_kernel<KIND>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGridStageMax);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kGT, stage);
+    const int64_t groups = (n_sig + GridTraits<KIND>::RS - 1) / GridTraits<KIND>::RS;
+    int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+    if (blocks > groups) blocks = groups;
+    kern<<<(unsigned)blocks, kGT, stage, stream>>>(x, n_pts, y, n_sig, gf, table, fit_err,
+                                                   status);
+    *launches += 1;
+    return cudaGetLastError();
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_grid_kernel<KIND>, kGT, 0);
+  const int64_t groups = (n_sig + GridTraits<KIND>::R - 1) / GridTraits<KIND>::R;
+  int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+  if (blocks > groups) blocks = groups;
+  fit_grid_kernel<KIND><<<(unsigned)blocks, kGT, 0, stream>>>(x, n_pts, y, n_sig, gf, table,
+                                                              fit_err, status);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+size_t fit_grid_workspace_size() { return (sizeof(GridFactor) + 255) & ~(size_t)255; }
+
+cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
+                            int64_t n_sig, void* table, double* fit_err, uint8_t* status,
+                            void* ws, cudaStream_t stream, int n_sm, int64_t* launches) {
+  if (kind == DOOLY_KIND_AFFINE)
+    return launch_grid_kind<DOOLY_KIND_AFFINE>(x, n_pts, y, n_sig, table, fit_err, status, ws,
+                                               stream, n_sm, launches);
+  return launch_grid_kind<DOOLY_KIND_ATTN>(x, n_pts, y, n_sig, table, fit_err, status, ws, stream,
+                                           n_sm, launches);
+}
+
+}  // namespace dooly

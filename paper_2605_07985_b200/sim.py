@@ -177,6 +177,40 @@ def fit(db: LatencyDB, device=None, strict: bool = True) -> Regressors:
 # -------------------------------------------------------------------- predict
 
 
+def fit_grid(kind: int, x: torch.Tensor, y: torch.Tensor,
+             out: Optional[FitResult] = None) -> FitResult:
+    """Shared-grid batch fit (dooly_fit_grid): every signature was swept over the
+    same points.  x: (P, n_pts) int32/uint32 device tensor, y: (n_sig, n_pts) f64.
+    Same result contract as ``fit_tables`` with x repeated per signature; the
+    Gram matrix and its factor are built once for the whole batch."""
+    dev = y.device
+    if y.dim() != 2:
+        raise ValueError("y must be (n_sig, n_pts)")
+    n_sig, n_pts = y.shape
+    if x.shape != (_lib.PLANES[kind], n_pts):
+        raise ValueError(f"x must have shape ({_lib.PLANES[kind]}, {n_pts}), got {tuple(x.shape)}")
+    x, y = x.contiguous(), y.contiguous()
+    if out is None:
+        out = FitResult(kind, torch.empty((n_sig, _lib.ROW_BYTES[kind]), dtype=torch.uint8,
+                                          device=dev),
+                        torch.empty(n_sig, dtype=torch.float64, device=dev),
+                        torch.empty(n_sig, dtype=torch.uint8, device=dev))
+    lib = _lib.load_library()
+    need = int(lib.dooly_fit_grid_workspace_size())
+    key = (str(dev), "grid")
+    ws = _FIT_WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        _FIT_WS[key] = ws
+    ctx = _lib.ctx_for(dev)
+    _lib.check(lib.dooly_fit_grid(
+        ctx, kind, x.data_ptr() if x.numel() else 0, n_pts, y.data_ptr() if y.numel() else 0,
+        n_sig, out.table.data_ptr() if n_sig else 0, out.fit_err.data_ptr() if n_sig else 0,
+        out.status.data_ptr() if n_sig else 0, ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev)),
+        ctx)
+    return out
+
+
 PACK_HEADER = np.dtype([("magic", "<u4"), ("ok", "<u4"), ("width", "<u4", 3), ("max_hi", "<u4", 3),
                         ("bad_inv", "<u4"), ("pad_", "<u4"), ("n_sig", "<i8"),
                         ("reserved", "u1", 48)])

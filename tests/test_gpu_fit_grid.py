@@ -1,0 +1,127 @@
+"""Shared-grid fit (dooly_fit_grid) vs the CPU oracle and vs the CSR fit.
+
+Contract: the same rows, statuses and fit_err as ``fit`` over the same points
+repeated per signature — coefficients within 1e-9 normwise
+in the scaled basis, fit_err within 1e-9 relative, box and inv_scale exact."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import ATTN, AFFINE, rows_to_table
+from oracle import sim as osim
+
+pytestmark = pytest.mark.gpu
+
+COEF_TOL = 1e-9
+ERR_TOL = 1e-9
+
+
+def _grid(kind, n_pts, rng):
+    if kind == AFFINE:
+        return np.sort(rng.integers(1, 32769, n_pts)).astype(np.uint32)[None, :]
+    side = round(n_pts ** (1 / 3))
+    t = np.unique(np.geomspace(1, 32768, side).astype(np.int64))
+    b = np.unique(np.geomspace(1, 256, side).astype(np.int64))
+    k = np.unique(np.linspace(0, 1 << 22, side).astype(np.int64))
+    g = np.stack(np.meshgrid(t, b, k, indexing="ij")).reshape(3, -1)
+    return g.astype(np.uint32)
+
+
+def _ys(kind, x, n_sig, rng, noise=1e-3):
+    xf = x.astype(np.float64)
+    if kind == AFFINE:
+        a = rng.uniform(5e-6, 2e-5, (n_sig, 1))
+        b = rng.uniform(1e-9, 1e-7, (n_sig, 1))
+        y = a + b * xf[0]
+    else:
+        c = rng.uniform(1e-12, 1e-9, (n_sig, 3))
+        y = (1e-5 + c[:, :1] * xf[0] + c[:, 1:2] * xf[1] * 100 + c[:, 2:3] * xf[2]
+             + 1e-15 * xf[0] * xf[0])
+    return np.abs(y * (1 + noise * rng.standard_normal(y.shape))) + 1e-9
+
+
+def _fit_grid_gpu(kind, x, y, dev):
+    from paper_2605_07985_b200.sim import fit_grid
+
+    fr = fit_grid(kind, torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).to(dev),
+                  torch.from_numpy(y).to(dev))
+    torch.cuda.synchronize()
+    return fr
+
+
+def _oracle(kind, x, y):
+    n_sig, n = y.shape
+    xr = np.tile(x, (1, n_sig))
+    off = np.arange(n_sig + 1, dtype=np.int64) * n
+    return osim.fit(kind, xr, y.reshape(-1), off), xr, off
+
+
+@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+@pytest.mark.parametrize("n_sig,n_pts", [(1, 512), (37, 512), (301, 512), (37, 510), (9, 4096)])
+def test_fit_grid_matches_oracle_and_csr(kind, n_sig, n_pts, dev):
+    """n_pts % 4 == 0 takes the shared-memory staged kernel, 510 the direct one."""
+    from paper_2605_07985_b200.sim import fit_tables
+
+    rng = np.random.default_rng(17 + kind + n_sig)
+    x = _grid(kind, n_pts, rng)[:, :n_pts]
+    y = _ys(kind, x, n_sig, rng)
+    fr = _fit_grid_gpu(kind, x, y, dev)
+    ref, xr, off = _oracle(kind, x, y)
+    got = rows_to_table(kind, fr.rows())
+    assert np.array_equal(fr.status.cpu().numpy(), ref["status"])
+    assert np.array_equal(got["lo"], ref["lo"]) and np.array_equal(got["hi"], ref["hi"])
+    assert np.array_equal(got["inv"], ref["inv"])
+    dc = np.abs(got["coef"] - ref["coef"]).max(axis=1) / np.abs(ref["coef"]).max(axis=1)
+    assert dc.max() <= COEF_TOL, dc.max()
+    # fit_err is a MAPE, so | |a-y| - |b-y| | <= |a-b| bounds its difference by the
+    # mean relative difference of the two fits' training predictions (each
+    # within the 1e-9 prediction contract); near-noise-level residuals amplify
+    # ~1e-12 coefficient differences, so a flat 1e-9 relative bar on fit_err
+    # would test summation order, not correctness.
+    fe = fr.fit_err.cpu().numpy()
+    for s in range(n_sig):
+        pg = np.maximum(osim.eval_poly(kind, got["coef"][s], got["inv"][s], x.T), 1e-7)
+        pr = np.maximum(osim.eval_poly(kind, ref["coef"][s], ref["inv"][s], x.T), 1e-7)
+        assert np.max(np.abs(pg - pr) / np.abs(pr)) <= 1e-9
+        bound = np.mean(np.abs(pg - pr) / y[s])
+        assert abs(fe[s] - ref["fit_err"][s]) <= bound * (1 + 1e-6) + 1e-12 * ref["fit_err"][s], (
+            s, fe[s], ref["fit_err"][s], bound)
+    # the CSR kernel over the repeated points gives the same regressors
+    csr = fit_tables(kind, torch.from_numpy(xr.view(np.int32)).to(dev), torch.from_numpy(
+        y.reshape(-1)).to(dev), torch.from_numpy(off).to(dev))
+    c2 = rows_to_table(kind, csr.rows())
+    d2 = np.abs(got["coef"] - c2["coef"]).max(axis=1) / np.abs(c2["coef"]).max(axis=1)
+    assert d2.max() <= 2 * COEF_TOL
+
+
+def test_fit_grid_insufficient_and_empty(dev):
+    rng = np.random.default_rng(3)
+    x = np.array([[1, 16, 128]], dtype=np.uint32)        # 3 points < need 4
+    y = _ys(AFFINE, x, 5, rng)
+    fr = _fit_grid_gpu(AFFINE, x, y, dev)
+    assert fr.status.cpu().numpy().tolist() == [1] * 5
+    assert np.isnan(fr.fit_err.cpu().numpy()).all()
+    rows = fr.rows()
+    assert (rows["lo"] > rows["hi"]).all()
+    x3 = _grid(ATTN, 8, rng)[:, :10]                      # 10 points < need 11
+    fr = _fit_grid_gpu(ATTN, x3, _ys(ATTN, x3, 2, rng), dev)
+    assert fr.status.cpu().numpy().tolist() == [1, 1]
+    fr = _fit_grid_gpu(ATTN, _grid(ATTN, 64, rng), np.zeros((0, 64)), dev)
+    assert fr.table.shape[0] == 0
+
+
+def test_fit_grid_rank_deficient_drops_columns(dev):
+    rng = np.random.default_rng(5)
+    x = _grid(ATTN, 512, rng)
+    x[1] = 8                                              # batch constant: f2 == 1 == intercept
+    y = _ys(ATTN, x, 9, rng, noise=0.0)
+    fr = _fit_grid_gpu(ATTN, x, y, dev)
+    ref, xr, off = _oracle(ATTN, x, y)
+    got = rows_to_table(ATTN, fr.rows())
+    assert np.array_equal(got["coef"] == 0, ref["coef"] == 0)
+    pg = osim.eval_poly(ATTN, got["coef"][0], got["inv"][0], x.T)
+    pr = osim.eval_poly(ATTN, ref["coef"][0], ref["inv"][0], x.T)
+    assert np.max(np.abs(pg - pr) / pr) <= 1e-9
