@@ -38,6 +38,7 @@ sys.path.insert(0, str(ROOT))
 AFFINE, ATTN = 0, 1
 BYTES_PER_QUERY = {AFFINE: 4 + 4 + 8 + 0.25, ATTN: 4 + 12 + 8 + 0.25}   # sig + x + out + 2 flag bits
 BYTES_PER_POINT = {AFFINE: 4 + 8, ATTN: 12 + 8}                          # x u32 planes + y f64
+BYTES_PER_GRID_POINT = 8                     # shared grid: y f64 per point (x counted once per kind)
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -361,19 +362,19 @@ def run_ours(args):
     hbm_peak, peak_kind = load_peaks()
     seed = 1000 * rank
 
-    # ---------------- fit inputs (C5) and the fit sub-benchmark
+    # ---------------- fit inputs (C5: one shared sweep grid per kind) and the fit sub-benchmark
     n_sig = {AFFINE: args.sigs // 2, ATTN: args.sigs - args.sigs // 2}
-    fit_in = {k: gen_fit_data(k, n_sig[k], args.points, dev, seed + k) for k in (AFFINE, ATTN)}
+    fit_in = {k: gen_grid_fit_data(k, n_sig[k], args.points, dev, seed + k) for k in (AFFINE, ATTN)}
+    n_pts = {k: fit_in[k][0].shape[1] for k in (AFFINE, ATTN)}
     torch.cuda.synchronize()
     from paper_2605_07985_b200._lib import KIND_ATTN_PACKED
-    from paper_2605_07985_b200.sim import fit_tables, pack_attn
+    from paper_2605_07985_b200.sim import fit_grid, fit_tables, pack_attn
 
-    offs = {k: torch.from_numpy(fit_in[k][2]).to(dev) for k in (AFFINE, ATTN)}
     fit_out = {}
     packed96 = None
     for _ in range(max(1, args.warmup)):
         for k in (AFFINE, ATTN):
-            fit_out[k] = fit_tables(k, fit_in[k][0], fit_in[k][1], offs[k], fit_out.get(k))
+            fit_out[k] = fit_grid(k, fit_in[k][0], fit_in[k][1], fit_out.get(k))
     barrier_sync(dist_on)
     stream = torch.cuda.current_stream()
     ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -384,11 +385,12 @@ def run_ours(args):
     fit_steps = max(1, min(args.steps, 3))
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    fit_launches0 = _lib.launch_count(dev)
     t_start.record(stream)
     for _ in range(fit_steps):
         for k in (AFFINE, ATTN):
             ev[k][0].record(stream)
-            fit_out[k] = fit_tables(k, fit_in[k][0], fit_in[k][1], offs[k], fit_out[k])
+            fit_out[k] = fit_grid(k, fit_in[k][0], fit_in[k][1], fit_out[k])
             if k == ATTN:   # serving form of the attention table (96-B rows), part of the fit output
                 packed96 = pack_attn(fit_out[k].table, packed96, check=False)
             ev[k][1].record(stream)
@@ -402,22 +404,55 @@ def run_ours(args):
         ag_ms += ag0.elapsed_time(ag1)
     t_end.record(stream)
     barrier_sync(dist_on)
+    fit_launches = (_lib.launch_count(dev) - fit_launches0) // fit_steps
     fit_total_ms = max_over_ranks(t_start.elapsed_time(t_end) / fit_steps, dist_on)
     status_ok = all(int((fit_out[k].status != 0).sum().item()) == 0 for k in (AFFINE, ATTN))
-    fit_bytes = sum(n_sig[k] * args.points * BYTES_PER_POINT[k] for k in (AFFINE, ATTN))
+    fit_bytes = sum(n_sig[k] * n_pts[k] * BYTES_PER_GRID_POINT for k in (AFFINE, ATTN))
     fit_dev_ms = sum(fit_ms.values()) / fit_steps
     fits = {
         "value": world * args.sigs / (fit_total_ms / 1e3), "unit": "fits/s",
-        "ms_per_step": fit_total_ms, "signatures_per_gpu": args.sigs, "points": args.points,
+        "ms_per_step": fit_total_ms, "signatures_per_gpu": args.sigs, "points": n_pts,
+        "workload": "C5 shared sweep grid per kind (affine: 4096 token counts in [1, 32768]; "
+                    "attention: 16x16x16 (prefill_toks, batch, kv_tokens)); sim.fit_grid",
         "kernel_ms": {"affine": fit_ms[AFFINE] / fit_steps, "attention": fit_ms[ATTN] / fit_steps,
                       "allgather": ag_ms / fit_steps},
+        "launches_per_step": fit_launches,
         "roofline": {"bound": "hbm", "achieved": fit_bytes / (fit_dev_ms / 1e3) / 1e9,
                      "peak": hbm_peak, "unit": "GB/s",
                      "frac": fit_bytes / (fit_dev_ms / 1e3) / 1e9 / hbm_peak,
-                     "traffic": ncu_traffic("fit", {k: n_sig[k] * args.points for k in (AFFINE, ATTN)}),
-                     "note": "attention fit is FP64-bound (~100 FP64 instr/point); see DESIGN.md"},
+                     "traffic": ncu_traffic("fit_grid", {k: n_sig[k] * n_pts[k] for k in (AFFINE, ATTN)}),
+                     "alg_bytes_per_point": BYTES_PER_GRID_POINT,
+                     "note": "y crosses HBM once (8 B/point); the attention kind is FP64-bound "
+                             "(~32 FP64 instr/point); see DESIGN.md"},
         "all_fitted": status_ok,
     }
+    # the general per-signature (CSR) kernel on the same points, x materialised per signature
+    fits_csr = None
+    if args.csr_fit:
+        csr_ms = {}
+        worst = 0.0
+        for k in (AFFINE, ATTN):
+            xr = fit_in[k][0].repeat(1, n_sig[k])
+            off = torch.arange(n_sig[k] + 1, dtype=torch.int64, device=dev) * n_pts[k]
+            fc = fit_tables(k, xr, fit_in[k][1].reshape(-1), off)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fc = fit_tables(k, xr, fit_in[k][1].reshape(-1), off, fc)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            csr_ms[k] = e0.elapsed_time(e1)
+            nc = 2 if k == AFFINE else 10
+            ga, gc = fit_out[k].table.view(torch.float64)[:, :nc], fc.table.view(torch.float64)[:, :nc]
+            worst = max(worst, float(((ga - gc).abs().amax(1) / gc.abs().amax(1)).max().item()))
+            del xr, fc
+        torch.cuda.empty_cache()
+        csr_bytes = sum(n_sig[k] * n_pts[k] * BYTES_PER_POINT[k] for k in (AFFINE, ATTN))
+        fits_csr = {"value": args.sigs / (sum(csr_ms.values()) / 1e3), "unit": "fits/s",
+                    "kernel_ms": {"affine": csr_ms[AFFINE], "attention": csr_ms[ATTN]},
+                    "achieved_gbs": csr_bytes / (sum(csr_ms.values()) / 1e3) / 1e9,
+                    "alg_bytes_per_point": BYTES_PER_POINT,
+                    "max_coef_rel_diff_vs_grid": worst,
+                    "path": "sim.fit_tables (dooly_fit): per-signature points, Gram per signature"}
     del fit_in
     pack_attn(fit_out[ATTN].table, packed96, check=True)   # raises if not representable
     rows128 = {k: fit_out[k].table for k in (AFFINE, ATTN)}
@@ -572,7 +607,7 @@ def run_ours(args):
                          "kernel_ms": {"affine": k_ms[AFFINE], "attention": k_ms[ATTN]},
                          "alg_bytes_per_query": BYTES_PER_QUERY},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-            "fits": fits, "dedup": dedup, "sim": sim, "unknown_signature_errors": bad,
+            "fits": fits, "fits_csr": fits_csr, "dedup": dedup, "sim": sim, "unknown_signature_errors": bad,
         }
         print(json.dumps(line))
     if dist_on:
@@ -690,6 +725,7 @@ def main(argv=None):
     ap.add_argument("--queries", type=int, default=1_000_000_000)
     ap.add_argument("--sigs", type=int, default=1_000_000)
     ap.add_argument("--points", type=int, default=4096)
+    ap.add_argument("--csr-fit", type=int, default=1, help="also time the per-signature CSR fit")
     ap.add_argument("--records", type=int, default=4_000_000)
     ap.add_argument("--e2e-queries", type=int, default=200_000_000)
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)

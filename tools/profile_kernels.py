@@ -1,6 +1,6 @@
 """Launch every libdooly_b200 hot kernel on C5-shaped inputs, for ncu.
 
-    ncu --set full --import-source on -k regex:'fit_stage|fit_moments_attn|fit_mape_attn|predict_vec|sha256_rec|dedup_insert|sim_run' \
+    ncu --set full --import-source on -k regex:'fit_grid_stage|fit_stage|fit_moments_attn|fit_mape_attn|predict_vec|sha256_rec|dedup_insert|sim_run' \
         -c 16 -o gpurun_out/prof python tools/profile_kernels.py
 
 Sizes are scaled down from bench.py (same shapes per unit) so a full ncu
@@ -25,14 +25,14 @@ def main() -> None:
     ap.add_argument("--queries", type=int, default=100_000_000)
     ap.add_argument("--records", type=int, default=1_000_000)
     ap.add_argument("--repeat", type=int, default=2)
-    ap.add_argument("--only", default="fit,predict,dedup,sim")
+    ap.add_argument("--only", default="fit,fitgrid,predict,dedup,sim")
     args = ap.parse_args()
 
     import torch
 
     import bench
     from paper_2605_07985_b200.profiler import DedupWorkspace, DeviceRecords, dedup_packed
-    from paper_2605_07985_b200.sim import fit_tables, pack_attn, predict_batch
+    from paper_2605_07985_b200.sim import fit_grid, fit_tables, pack_attn, predict_batch
 
     dev = torch.device("cuda", 0)
     only = set(args.only.split(","))
@@ -46,6 +46,13 @@ def main() -> None:
         tables[kind] = fr.table
         del x, y
     torch.cuda.synchronize()
+    if "fitgrid" in only:
+        for kind in (0, 1):
+            xg, yg = bench.gen_grid_fit_data(kind, args.sigs, args.points, dev, seed=kind)
+            fg = None
+            for _ in range(args.repeat):
+                fg = fit_grid(kind, xg, yg, fg)
+            del xg, yg
     if "predict" in only:
         for kind in (0, 1):
             # table sized like C5 (0.5M rows) by tiling the fitted rows
