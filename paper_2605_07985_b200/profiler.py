@@ -9,9 +9,11 @@ Hot path (GPU, libdooly_b200):
 
 Host side (inputs to the fit, SURVEY §8(f) row f1 is their GPU fusion):
     sweep, oracle_latency, comm_latency          (SPEC.md:466-494)
-  and a minimal in-memory ``LatencyDB`` with the Fig. 9 logical tables
+  and the in-memory ``LatencyDB`` working set with the Fig. 9 logical tables
   (SPEC.md:430-435) — configurations, signatures, model_operations,
-  measurements — persisted as one .npz file.
+  measurements, comm_measurements.  ``store.py`` persists it as one SQLite file
+  (D5, SPEC.md:517) with JSON-lines import/export (D4) and a schema dump;
+  ``.npz`` snapshots remain for quick round trips.
 """
 
 from __future__ import annotations
@@ -181,6 +183,14 @@ class SignatureRow:
     granularity: str
     kind: int
     feature: str
+    components: str = "{}"   # JSON: model_dims, kernel_symbols, attrs, window
+
+
+def _components(entry: RunnableEntry) -> str:
+    import json
+
+    return json.dumps({"model_dims": entry.model_dims(), "kernel_symbols": list(entry.kernel_symbols),
+                       "attrs": dict(entry.attrs), "window": entry.window}, sort_keys=True)
 
 
 @dataclass
@@ -191,16 +201,16 @@ class LatencyDB:
     signatures: list = field(default_factory=list)         # SignatureRow, insertion order
     model_operations: list = field(default_factory=list)   # (config_id, digest, repeat)
     measurements: dict = field(default_factory=dict)       # digest -> (x (p, n) u32, y f64)
+    workloads: dict = field(default_factory=dict)          # digest -> [workload dict | None] per point
+    sources: dict = field(default_factory=dict)            # digest -> "oracle" | "imported"
+    comm_measurements: dict = field(default_factory=dict)  # (topology, tp, bytes) -> latency_s
     _index: dict = field(default_factory=dict)
 
-    SCHEMA = ("configurations(id, hardware, model, backend, tp_degree)\n"
-              "signatures(hash PRIMARY KEY, op_name, granularity, kind, feature)\n"
-              "model_operations(config_id -> configurations, signature_hash -> signatures, "
-              "repeat_count)\n"
-              "measurements(signature_hash -> signatures, features..., latency_s)\n")
-
     def schema_dump(self) -> str:
-        return self.SCHEMA
+        """The logical schema (D5 conformance dump), identical to the SQLite DDL."""
+        from .store import schema_dump
+
+        return schema_dump()
 
     def has(self, digest: bytes) -> bool:
         return digest in self._index
@@ -219,15 +229,29 @@ class LatencyDB:
         if digest not in self._index:
             self._index[digest] = len(self.signatures)
             self.signatures.append(SignatureRow(digest, entry.name, entry.granularity,
-                                                _kind_of(entry), entry.feature))
+                                                _kind_of(entry), entry.feature,
+                                                _components(entry)))
 
-    def insert_measurements(self, digest: bytes, x: np.ndarray, y: np.ndarray) -> None:
+    def add_model_operation(self, config_id: int, digest: bytes, repeat_count: int) -> None:
+        """model_operations row; must reference an existing configuration and
+        signature (referential integrity)."""
+        if not 0 <= config_id < len(self.configurations) or digest not in self._index:
+            raise StoreUnavailable("model_operations must reference an existing configuration "
+                                   "and signature")
+        self.model_operations.append((int(config_id), digest, int(repeat_count)))
+
+    def insert_measurements(self, digest: bytes, x: np.ndarray, y: np.ndarray,
+                            workloads: Optional[Sequence] = None, source: str = "oracle") -> None:
         """Insert a sweep; re-inserting an identical key with a different latency
-        raises DuplicateKey."""
+        raises DuplicateKey.  ``workloads`` optionally carries the
+        LatencyRecord workload of every point."""
         if digest not in self._index:
             raise StoreUnavailable("model_operations/measurements must reference a signature")
         x = np.atleast_2d(np.asarray(x, dtype=np.uint32))
         y = np.asarray(y, dtype=np.float64)
+        if np.any(~(y > 0)):
+            raise OraclePanic(f"{digest.hex()[:12]}: latency_s must be > 0 (SPEC.md:427)")
+        wl = list(workloads) if workloads is not None else [None] * y.shape[0]
         if digest in self.measurements:
             ox, oy = self.measurements[digest]
             old = {tuple(ox[:, i]): oy[i] for i in range(oy.shape[0])}
@@ -241,7 +265,18 @@ class LatencyDB:
                     keep.append(i)
             x = np.concatenate([ox, x[:, keep]], axis=1)
             y = np.concatenate([oy, y[keep]])
+            wl = self.workloads.get(digest, [None] * oy.shape[0]) + [wl[i] for i in keep]
         self.measurements[digest] = (x, y)
+        self.workloads[digest] = wl
+        self.sources.setdefault(digest, source)
+
+    def insert_comm(self, topology: str, tp_degree: int, nbytes: int, latency_s: float) -> None:
+        """comm sub-schema keyed by hardware topology (Appendix E)."""
+        key = (topology, int(tp_degree), int(nbytes))
+        old = self.comm_measurements.get(key)
+        if old is not None and old != latency_s:
+            raise DuplicateKey(f"comm {key}: {old} != {latency_s}")
+        self.comm_measurements[key] = float(latency_s)
 
     def digest_tensor(self, device) -> torch.Tensor:
         if not self.signatures:
@@ -250,6 +285,13 @@ class LatencyDB:
         return torch.from_numpy(arr.reshape(-1, 32).copy()).to(device)
 
     def save(self, path) -> None:
+        """Persist: ``.npz`` snapshot, or the single-file SQLite store (D5) for any
+        other suffix (``store.save``)."""
+        if not str(path).endswith(".npz"):
+            from .store import save
+
+            save(self, path)
+            return
         sig = np.array([[s.digest.hex(), s.op_name, s.granularity, str(s.kind), s.feature]
                         for s in self.signatures], dtype=object)
         meas = {f"x_{d.hex()}": v[0] for d, v in self.measurements.items()}
@@ -261,6 +303,10 @@ class LatencyDB:
 
     @staticmethod
     def load(path) -> "LatencyDB":
+        if not str(path).endswith(".npz"):
+            from .store import load
+
+            return load(path)
         try:
             z = np.load(path, allow_pickle=True)
         except OSError as exc:
@@ -308,13 +354,13 @@ def dedup_with_digests(entries: Sequence[RunnableEntry], db: LatencyDB,
     to_profile, skipped, new_digests = [], [], []
     for i, e in enumerate(entries):
         d = bytes(digs[i])
-        if config_id is not None:
-            db.model_operations.append((config_id, d, e.repeat_count))
+        if is_new[i] and register:
+            db.add_signature(d, e)
+        if config_id is not None and db.has(d):   # dry runs (register=False) record nothing new
+            db.add_model_operation(config_id, d, e.repeat_count)
         if is_new[i]:
             to_profile.append(e)
             new_digests.append(d)
-            if register:
-                db.add_signature(d, e)
         else:
             skipped.append(e)
     return to_profile, skipped, new_digests
@@ -458,7 +504,7 @@ def profile_corpus(manifest, db: Optional[LatencyDB] = None, device=None,
             to_profile, skipped, digests = dedup_with_digests(entries, db, cid, device)
             for e, d in zip(to_profile, digests):
                 x, y = sweep(e, grid, m, manifest.hardware, b)
-                db.insert_measurements(d, x, y)
+                db.insert_measurements(d, x, y, sweep_points(e, grid, m.max_context))
             report.append({"model": m.name, "backend": b.name, "entries": len(entries),
                            "profiled": len(to_profile), "skipped": len(skipped)})
     return db, report
