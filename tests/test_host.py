@@ -220,7 +220,7 @@ def test_latency_db_roundtrip_and_duplicate_key(tmp_path):
     assert back.has(d) and back.configurations == db.configurations
     assert np.array_equal(back.measurements[d][0], db.measurements[d][0])
     assert back.model_operations == db.model_operations
-    assert "signatures(hash PRIMARY KEY" in back.schema_dump()
+    assert "CREATE TABLE signatures(\n  hash BLOB PRIMARY KEY" in back.schema_dump()
 
 
 def test_sweep_points_cardinality(corpus):
