@@ -287,6 +287,41 @@ int dooly_sim_run(dooly_ctx* ctx, const dooly_oplist* ops, const dooly_sched* cf
                   double* it_log_lat, int64_t it_log_cap, void* workspace,
                   size_t workspace_bytes, void* stream);
 
+/* Host-scheduled evaluation (SURVEY §8(b) dooly_sim_eval): an external
+ * scheduler supplies the iterations; the device evaluates them and derives the
+ * request metrics.
+ *   it_feat   DOOLY_IT_FEATS planes of n_it u32 (as dooly_iter_eval)
+ *   it_start  per iteration, the earliest start (the arrival an idle replica
+ *             jumps to), 0 when the replica was busy; NULL = 0
+ *   it_off    n_shards + 1 offsets of independent replica shards (NULL: one)
+ *   clock[i]  = max(clock[i-1], it_start[i]) + it_lat[i], sequential f64 per
+ *               shard, bit-identical to the event loop's clock
+ *   first_it / last_it  global iteration that produced a request's first /
+ *             last token (0xFFFFFFFF = never)
+ *   ttft      = clock[first_it] - arrival;  tpot = (clock[last_it] -
+ *               clock[first_it]) / (out_tok - 1), NaN when out_tok < 2
+ * err_first  (optional) first iteration on an unknown regressor row
+ * req_err_first (optional) first request with an out-of-range iteration index
+ * it_lat and clock are caller-owned device outputs of n_it f64. */
+int dooly_sim_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_table,
+                   int64_t n_affine, const void* attn_table, int64_t n_attn,
+                   const uint32_t* it_feat, const double* it_start, const int64_t* it_off,
+                   int64_t n_shards, int64_t n_it, const double* arrival,
+                   const uint32_t* first_it, const uint32_t* last_it, const uint32_t* out_tok,
+                   int64_t n_req, double* it_lat, double* clock, double* ttft, double* tpot,
+                   int64_t* err_first, int64_t* req_err_first, void* stream);
+
+/* canonicalize + signature_hash + dedup in one call (SURVEY §8(b) dooly_dedup):
+ * dooly_sha256_records into out_digest, then dooly_dedup_digests.  The
+ * workspace is dooly_dedup_workspace_size(n, n_db) bytes. */
+int dooly_dedup(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off, int64_t n,
+                const uint8_t* op_bytes, const int64_t* op_off, int64_t n_ops,
+                const uint8_t* sym_bytes, const int64_t* sym_off, int64_t n_sym,
+                const uint8_t* attr_digests, int64_t n_attr, const uint8_t* db_digests,
+                int64_t n_db, uint8_t* out_digest, int64_t* out_first, uint32_t* out_uid,
+                uint8_t* out_is_new, uint8_t* out_in_db, int64_t* out_n_unique,
+                void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

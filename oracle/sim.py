@@ -247,6 +247,9 @@ def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch:
     running: list = []
     reserved = 0
     feats_log, lat_log = [], []
+    start_log, clock_log = [], []          # idle jump target (0.0 if busy), clock after it
+    first_it, last_it = [-1] * n, [-1] * n
+    jump = 0.0
     status = "ok"
 
     def make(i):
@@ -261,6 +264,7 @@ def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch:
             if arrive == n:
                 break
             clock = float(arrival[arrive])          # idle: jump to the next arrival
+            jump = clock
             continue
         if it >= max_iterations:
             status = "non_termination"
@@ -298,6 +302,9 @@ def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch:
         if log:
             feats_log.append(feats)
             lat_log.append(lat)
+            start_log.append(jump)
+            clock_log.append(clock)
+        jump = 0.0
         done = []
         for r, t, pf in active:
             r["kv"] += t
@@ -309,7 +316,9 @@ def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch:
             if r["dec"] == 1:
                 r["t_first"] = clock
                 ttft[r["i"]] = clock - arrival[r["i"]]
+                first_it[r["i"]] = it - 1
             if r["dec"] >= r["output"]:
+                last_it[r["i"]] = it - 1
                 if r["output"] >= 2:
                     tpot[r["i"]] = (clock - r["t_first"]) / (r["output"] - 1)
                 done.append(r)
@@ -319,7 +328,8 @@ def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch:
                 reserved -= (r["prompt"] + r["output"]) * kv_bytes_per_token
             running = [r for r in running if id(r) not in ids]
     return {"ttft": np.array(ttft), "tpot": np.array(tpot), "n_iter": it, "clock": clock,
-            "status": status, "feats": feats_log, "lat": lat_log}
+            "status": status, "feats": feats_log, "lat": lat_log, "start": start_log,
+            "clocks": clock_log, "first_it": first_it, "last_it": last_it}
 
 
 def run_shards(arrival, prompt, output, cached, n_shards: int, **kw) -> dict:

@@ -105,6 +105,10 @@ _SIGS = {
     "dooly_predict": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
     "dooly_attn_pack_bytes": (C.c_size_t, [_I64]),
     "dooly_fit_grid_workspace_size": (C.c_size_t, []),
+    "dooly_dedup": (C.c_int, [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _I64, _P, _I64,
+                              _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
+    "dooly_sim_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
+                                 _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "dooly_fit_grid": (C.c_int, [_P, C.c_int, _P, _I64, _P, _I64, _P, _P, _P, _P, C.c_size_t, _P]),
     "dooly_attn_pack": (C.c_int, [_P, _P, _I64, _P, _P]),
     "dooly_iter_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _I64, _P, _P,

@@ -40,6 +40,12 @@ cudaError_t launch_iter_eval(const dooly_oplist* ops, const void* aff, int64_t n
                              int64_t n_it, double* it_lat, int64_t* err_first,
                              cudaStream_t stream, int n_sm);
 size_t sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards);
+cudaError_t launch_sim_eval(const double* it_lat, const double* it_start, const int64_t* it_off,
+                            int64_t n_shards, int64_t n_it, double* clock, const double* arrival,
+                            const uint32_t* first_it, const uint32_t* last_it,
+                            const uint32_t* out_tok, int64_t n_req, double* ttft, double* tpot,
+                            int64_t* err_first, cudaStream_t stream, int n_sm,
+                            int64_t* launches);
 cudaError_t launch_profile_fit(int kind, const dooly_sweep_desc* descs, int64_t n_sig,
                                const dooly_sweep_grid* grid, void* table, double* fit_err,
                                uint8_t* status, uint32_t* out_x, double* out_y,
@@ -304,6 +310,47 @@ int dooly_iter_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_
                                             it_feat, n_it, it_lat, err_first,
                                             (cudaStream_t)stream, ctx->n_sm),
                     "iter_eval");
+}
+
+int dooly_sim_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_table,
+                   int64_t n_affine, const void* attn_table, int64_t n_attn,
+                   const uint32_t* it_feat, const double* it_start, const int64_t* it_off,
+                   int64_t n_shards, int64_t n_it, const double* arrival,
+                   const uint32_t* first_it, const uint32_t* last_it, const uint32_t* out_tok,
+                   int64_t n_req, double* it_lat, double* clock, double* ttft, double* tpot,
+                   int64_t* err_first, int64_t* req_err_first, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n_req < 0 || n_shards < 0)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sim_eval: negative size");
+  if (!it_off) n_shards = n_it > 0 ? 1 : 0;
+  if (n_it > 0 && !clock) return fail(ctx, DOOLY_ERR_INVALID_ARG, "sim_eval: null clock");
+  if (n_req > 0 && (!arrival || !first_it || !last_it || !out_tok || !ttft || !tpot))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sim_eval: null request pointer");
+  int rc = dooly_iter_eval(ctx, ops, affine_table, n_affine, attn_table, n_attn, it_feat, n_it,
+                           it_lat, err_first, stream);
+  if (rc) return rc;
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_sim_eval(it_lat, it_start, it_off, n_shards, n_it, clock,
+                                           arrival, first_it, last_it, out_tok, n_req, ttft,
+                                           tpot, req_err_first, (cudaStream_t)stream, ctx->n_sm,
+                                           &ctx->launches),
+                    "sim_eval");
+}
+
+int dooly_dedup(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off, int64_t n,
+                const uint8_t* op_bytes, const int64_t* op_off, int64_t n_ops,
+                const uint8_t* sym_bytes, const int64_t* sym_off, int64_t n_sym,
+                const uint8_t* attr_digests, int64_t n_attr, const uint8_t* db_digests,
+                int64_t n_db, uint8_t* out_digest, int64_t* out_first, uint32_t* out_uid,
+                uint8_t* out_is_new, uint8_t* out_in_db, int64_t* out_n_unique,
+                void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = dooly_sha256_records(ctx, words, rec_off, n, op_bytes, op_off, n_ops, sym_bytes,
+                                sym_off, n_sym, attr_digests, n_attr, out_digest, stream);
+  if (rc) return rc;
+  return dooly_dedup_digests(ctx, out_digest, n, db_digests, n_db, out_first, out_uid,
+                             out_is_new, out_in_db, out_n_unique, workspace, workspace_bytes,
+                             stream);
 }
 
 int dooly_profile_fit(dooly_ctx* ctx, int kind, const dooly_sweep_desc* descs, int64_t n_sig,

@@ -424,3 +424,90 @@ cudaError_t launch_sim(const dooly_oplist* ops, const dooly_sched* cfg, const vo
 }
 
 }  // namespace dooly
+
+// ===================================================================
+// dooly_sim_eval: host-scheduled iterations (an external simulator's own
+// scheduler, "drop-in profiling backend") evaluated on the
+// device.  iter_eval gives it_lat; then one warp per shard scans
+// clock[i] = max(clock[i-1], it_start[i]) + it_lat[i] sequentially (the same
+// f64 operation order as the event loop: an idle replica
+// jumps to the next arrival, else iterations run back to back); then one
+// thread per request reads its first/last-token clocks.
+namespace dooly {
+
+__global__ void __launch_bounds__(128) sim_clock_kernel(const double* __restrict__ it_lat,
+                                                        const double* __restrict__ it_start,
+                                                        const int64_t* __restrict__ it_off,
+                                                        int64_t n_shards, int64_t n_it,
+                                                        double* __restrict__ clock) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (w >= n_shards) return;
+  const int64_t b = it_off ? it_off[w] : 0, e = it_off ? it_off[w + 1] : n_it;
+  double c = 0.0;
+  for (int64_t i0 = b; i0 < e; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const double l = i < e ? it_lat[i] : 0.0;
+    const double s = (i < e && it_start) ? it_start[i] : 0.0;
+    double mine = 0.0;
+    const int m = (int)min((int64_t)32, e - i0);
+    for (int j = 0; j < m; ++j) {
+      const double lj = __shfl_sync(0xFFFFFFFFu, l, j);
+      const double sj = __shfl_sync(0xFFFFFFFFu, s, j);
+      c = __dadd_rn(c < sj ? sj : c, lj);
+      if (lane == j) mine = c;
+    }
+    if (i < e) clock[i] = mine;
+  }
+}
+
+__global__ void __launch_bounds__(256) sim_request_kernel(
+    const double* __restrict__ clock, int64_t n_it, const double* __restrict__ arrival,
+    const uint32_t* __restrict__ first_it, const uint32_t* __restrict__ last_it,
+    const uint32_t* __restrict__ out_tok, int64_t n_req, double* __restrict__ ttft,
+    double* __restrict__ tpot, int64_t* __restrict__ err_first) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_req;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = first_it[r], l = last_it[r], o = out_tok[r];
+    double t1 = nan64(), t2 = nan64();
+    if (f != 0xFFFFFFFFu) {
+      if (f >= n_it || (l != 0xFFFFFFFFu && (l >= n_it || l < f))) {
+        if (err_first)
+          atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)r);
+      } else {
+        const double cf = clock[f];
+        t1 = __dsub_rn(cf, arrival[r]);
+        if (o >= 2 && l != 0xFFFFFFFFu) t2 = __ddiv_rn(__dsub_rn(clock[l], cf), (double)(o - 1));
+      }
+    }
+    ttft[r] = t1;
+    tpot[r] = t2;
+  }
+}
+
+cudaError_t launch_sim_eval(const double* it_lat, const double* it_start, const int64_t* it_off,
+                            int64_t n_shards, int64_t n_it, double* clock, const double* arrival,
+                            const uint32_t* first_it, const uint32_t* last_it,
+                            const uint32_t* out_tok, int64_t n_req, double* ttft, double* tpot,
+                            int64_t* err_first, cudaStream_t stream, int n_sm,
+                            int64_t* launches) {
+  if (n_it > 0 && n_shards > 0) {
+    const int64_t blocks = (n_shards * 32 + 127) / 128;
+    sim_clock_kernel<<<(unsigned)blocks, 128, 0, stream>>>(it_lat, it_start, it_off, n_shards,
+                                                           n_it, clock);
+    *launches += 1;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (n_req > 0) {
+    int64_t blocks = (n_req + 255) / 256;
+    if (blocks > (int64_t)n_sm * 8) blocks = (int64_t)n_sm * 8;
+    sim_request_kernel<<<(unsigned)blocks, 256, 0, stream>>>(clock, n_it, arrival, first_it,
+                                                             last_it, out_tok, n_req, ttft, tpot,
+                                                             err_first);
+    *launches += 1;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace dooly

@@ -165,8 +165,30 @@ def dedup_digests(digests: torch.Tensor, db_digests: Optional[torch.Tensor] = No
 
 def dedup_packed(recs: DeviceRecords, db_digests: Optional[torch.Tensor] = None,
                  workspace: Optional[DedupWorkspace] = None, sync: bool = True) -> DedupResult:
-    """Batch form of dedup: packed records in HBM -> digests + dedup table."""
-    return dedup_digests(hash_records(recs), db_digests, workspace, sync)
+    """Batch form of dedup: packed records in HBM -> digests + dedup table, one
+    C-ABI call (dooly_dedup = K1a SHA-256 + K1b first-occurrence resolve)."""
+    dev = recs.words.device
+    n = recs.n
+    if db_digests is None:
+        db_digests = torch.empty((0, 32), dtype=torch.uint8, device=dev)
+    n_db = db_digests.shape[0]
+    ws = (workspace or DedupWorkspace(dev)).get(n, n_db)
+    dig = torch.empty((n, 32), dtype=torch.uint8, device=dev)
+    first = torch.empty(n, dtype=torch.int64, device=dev)
+    uid = torch.empty(n, dtype=torch.int32, device=dev)
+    is_new = torch.empty(n, dtype=torch.uint8, device=dev)
+    in_db = torch.empty(n, dtype=torch.uint8, device=dev)
+    n_unique = torch.empty(1, dtype=torch.int64, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_dedup(
+        ctx, recs.words.data_ptr(), recs.rec_off.data_ptr(), n, recs.op_bytes.data_ptr(),
+        recs.op_off.data_ptr(), recs.op_off.numel() - 1, recs.sym_bytes.data_ptr(),
+        recs.sym_off.data_ptr(), recs.sym_off.numel() - 1, recs.attr_digests.data_ptr(),
+        recs.attr_digests.numel() // 32, db_digests.data_ptr() if n_db else 0, n_db,
+        dig.data_ptr(), first.data_ptr(), uid.data_ptr(), is_new.data_ptr(), in_db.data_ptr(),
+        n_unique.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev)), ctx)
+    nu = int(n_unique.item()) if sync else -1
+    return DedupResult(dig, first, uid, is_new, in_db, nu)
 
 
 # ------------------------------------------------------------------ LatencyDB

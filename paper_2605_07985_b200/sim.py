@@ -388,6 +388,40 @@ def iter_latency(batch: IterationBatch, calltree: CallTree, regs: Regressors) ->
     return float(iter_latency_batch(f, calltree, regs).item())
 
 
+def sim_eval(calltree: CallTree, regs: Regressors, it_feat: torch.Tensor,
+             arrival: torch.Tensor, first_it: torch.Tensor, last_it: torch.Tensor,
+             out_tok: torch.Tensor, it_start: Optional[torch.Tensor] = None,
+             it_off: Optional[torch.Tensor] = None):
+    """Host-scheduled evaluation (dooly_sim_eval): an external scheduler's
+    iterations (5, n_it) i32 -> (it_lat, clock, ttft, tpot) f64 device tensors.
+    clock[i] = max(clock[i-1], it_start[i]) + it_lat[i] per shard (it_off), the
+    event loop's clock bit for bit; first_it / last_it are the global iterations
+    that produced a request's first / last token (-1 = never)."""
+    dev = it_feat.device
+    n_it = it_feat.shape[1]
+    n_req = arrival.numel()
+    n_shards = 0 if it_off is None else it_off.numel() - 1
+    it_lat = torch.empty(n_it, dtype=torch.float64, device=dev)
+    clock = torch.empty(n_it, dtype=torch.float64, device=dev)
+    ttft = torch.empty(n_req, dtype=torch.float64, device=dev)
+    tpot = torch.empty(n_req, dtype=torch.float64, device=dev)
+    errs = torch.full((2,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+    ctx = _lib.ctx_for(dev)
+    _lib.check(_lib.load_library().dooly_sim_eval(
+        ctx, C.byref(calltree.oplist), regs.table_ptr(_lib.KIND_AFFINE), regs.n(_lib.KIND_AFFINE),
+        regs.table_ptr(_lib.KIND_ATTN), regs.n(_lib.KIND_ATTN), _lib.ptr(it_feat),
+        _lib.ptr(it_start), _lib.ptr(it_off), n_shards, n_it, _lib.ptr(arrival),
+        _lib.ptr(first_it), _lib.ptr(last_it), _lib.ptr(out_tok), n_req,
+        _lib.ptr(it_lat), _lib.ptr(clock), _lib.ptr(ttft), _lib.ptr(tpot),
+        errs.data_ptr(), errs.data_ptr() + 8, _lib.stream_ptr(dev)), ctx)
+    e = errs.cpu().numpy()
+    if e[0] != np.iinfo(np.int64).max:
+        raise UnknownSignature(f"iteration {int(e[0])} evaluates an unfitted regressor row")
+    if e[1] != np.iinfo(np.int64).max:
+        raise ValueError(f"request {int(e[1])}: first/last iteration index out of range")
+    return it_lat, clock, ttft, tpot
+
+
 # ----------------------------------------------------------------------- run
 
 

@@ -462,6 +462,77 @@ def test_sim_run_bit_exact(seed, n, shards, window, tp, cap, dev):
     assert np.array_equal(res.log_lat.cpu().numpy()[0, :k], np.array(r0["lat"][:k]))
 
 
+@pytest.mark.parametrize("seed,n,shards,window,tp", [(5, 600, 1, 0, 1), (6, 2500, 5, 4096, 4)])
+def test_sim_eval_host_schedule_bit_exact(seed, n, shards, window, tp, dev):
+    """dooly_sim_eval on the oracle event loop's own schedule: identical iteration
+    latencies, clocks (idle jumps included) and TTFT/TPOT, bit for bit."""
+    from paper_2605_07985_b200.sim import CallTree, sim_eval
+
+    ta, tt, ops, ol = _sim_setup(seed, window=window, tp=tp)
+    regs = _regs(ta, tt, dev)
+    arr, pr, ou, ca = _workload(n, seed, rate=2.0, cached_frac=0.1)
+    feats, start, clocks, lat, off = [], [], [], [], [0]
+    first = np.full(n, -1, dtype=np.int64)
+    last = np.full(n, -1, dtype=np.int64)
+    ttft_ref = np.full(n, np.nan)
+    tpot_ref = np.full(n, np.nan)
+    for s in range(shards):
+        idx = np.arange(s, n, shards)
+        r = osim.run_shard(arr[idx].tolist(), pr[idx].tolist(), ou[idx].tolist(),
+                           ca[idx].tolist(), ops, 2048, 64, 131072, 10**15, window, tp, 5e-6,
+                           5e-12, log=True)
+        base = off[-1]
+        feats += r["feats"]
+        start += r["start"]
+        clocks += r["clocks"]
+        lat += r["lat"]
+        off.append(base + len(r["lat"]))
+        f, l = np.array(r["first_it"]), np.array(r["last_it"])
+        first[idx] = np.where(f >= 0, f + base, -1)
+        last[idx] = np.where(l >= 0, l + base, -1)
+        ttft_ref[idx], tpot_ref[idx] = r["ttft"], r["tpot"]
+    assert any(v > 0 for v in start)                       # idle jumps are exercised
+    it_feat = _i32(np.array(feats, dtype=np.uint32).T.copy()).to(dev)
+    t = lambda a, dt: torch.from_numpy(np.asarray(a, dtype=dt)).to(dev)
+    it_lat, clock, ttft, tpot = sim_eval(
+        CallTree([], ol, window), regs, it_feat, t(arr, np.float64),
+        t(first.astype(np.int32), np.int32), t(last.astype(np.int32), np.int32),
+        _i32(ou.astype(np.uint32)).to(dev), it_start=t(start, np.float64),
+        it_off=t(off, np.int64))
+    assert np.array_equal(it_lat.cpu().numpy(), np.array(lat))
+    assert np.array_equal(clock.cpu().numpy(), np.array(clocks))
+    g1, g2 = ttft.cpu().numpy(), tpot.cpu().numpy()
+    assert np.array_equal(g1.view(np.uint64), ttft_ref.view(np.uint64))
+    assert np.array_equal(np.isnan(g2), np.isnan(tpot_ref))
+    m = ~np.isnan(tpot_ref)
+    assert np.array_equal(g2[m], tpot_ref[m])
+    with pytest.raises(ValueError):                        # out-of-range iteration index
+        bad = first.copy()
+        bad[0] = len(lat) + 5
+        sim_eval(CallTree([], ol, window), regs, it_feat, t(arr, np.float64),
+                 t(bad.astype(np.int32), np.int32), t(last.astype(np.int32), np.int32),
+                 _i32(ou.astype(np.uint32)).to(dev), it_start=t(start, np.float64),
+                 it_off=t(off, np.int64))
+
+
+def test_dedup_single_call_matches_two_calls(corpus, dev):
+    from paper_2605_07985_b200.profiler import (DeviceRecords, dedup_digests, dedup_packed,
+                                                hash_records)
+    from paper_2605_07985_b200.records import pack_entries, synthesize_entries
+
+    ents = [e for m in corpus.models for b in corpus.backends for e in synthesize_entries(m, b)]
+    recs = DeviceRecords.from_packed(pack_entries(ents), dev)
+    one = dedup_packed(recs)
+    dig = hash_records(recs)
+    two = dedup_digests(dig, one.digests[:7].clone())
+    one_db = dedup_packed(recs, one.digests[:7].clone())
+    assert torch.equal(one.digests, dig)
+    for a, b in ((one_db.first, two.first), (one_db.uid, two.uid), (one_db.is_new, two.is_new),
+                 (one_db.in_db, two.in_db)):
+        assert torch.equal(a, b)
+    assert one_db.n_unique == two.n_unique == one.n_unique
+
+
 def test_sim_non_termination(dev):
     from paper_2605_07985_b200 import _lib
     from paper_2605_07985_b200.errors import NonTermination
