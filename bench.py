@@ -196,6 +196,26 @@ def load_peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
+def gather_ceiling(nq: dict, k_ms: dict):
+    """The binding limit of random-row predict on this hardware: the measured
+    LDG.256 gather rate of bare 32-B / 96-B rows (tools/gather_probe.py,
+    profiles/r1_gather_probe.jsonl).  frac = time at that rate / measured time."""
+    p = ROOT / "profiles" / "r1_gather_probe.jsonl"
+    if not p.exists():
+        return None
+    rate = {}
+    for ln in p.read_text().splitlines():
+        r = json.loads(ln)
+        if r.get("probe") == "gather" and r.get("rows") == 500_000:
+            rate[r["row_bytes"]] = r["g_rows_per_s"] * 1e9
+    if 32 not in rate or 96 not in rate:
+        return None
+    ideal_ms = (nq[AFFINE] / rate[32] + nq[ATTN] / rate[96]) * 1e3
+    return {"rows_per_s": {"affine_32B": rate[32], "attention_96B": rate[96]},
+            "ideal_ms": ideal_ms, "frac": ideal_ms / (k_ms[AFFINE] + k_ms[ATTN]),
+            "source": "profiles/r1_gather_probe.jsonl (bare LDG.256 row gathers, 500k rows)"}
+
+
 def ncu_traffic(kernel_key: str, units: dict):
     """DRAM bytes per step from the committed ncu per-unit measurement
     (profiles/ncu_summary.json x this step's units), or None."""
@@ -341,6 +361,16 @@ def cpu_predict_baseline(tables_host, queries_host, threads: int, budget_s: floa
 
 
 # ------------------------------------------------------------------- main arm
+
+
+def arm_config(args) -> dict:
+    """The workload both arms report (the reference arm times a bounded sample of it)."""
+    return {"workload": f"C5 scale sweep: {args.sigs:.3g} signatures x {args.points} points "
+                        f"fitted on the shared sweep grid, then {args.queries:.3g} queries "
+                        "per GPU per step (half affine, half attention)",
+            "queries_per_gpu": args.queries, "signatures_per_gpu": args.sigs,
+            "points_per_signature": args.points,
+            "l2": "inputs >> L2 (126 MB); no flush"}
 
 
 def run_ours(args):
@@ -594,18 +624,15 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (C5: seeded device-generated regressor tables and queries)",
-            "config": {"workload": "C5 scale sweep: 1M signatures x 4096 points fitted, then "
-                                   f"{args.queries:.3g} queries per GPU per step",
-                       "queries_per_gpu": args.queries, "signatures_per_gpu": args.sigs,
-                       "points_per_signature": args.points,
-                       "l2": "inputs >> L2 (126 MB); no flush"},
+            "config": arm_config(args),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": ncu_traffic("predict", nq),
                          "alg_bytes": alg_bytes,
                          "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                          if peak_kind == "measured" else "fallback 6.65 TB/s",
                          "kernel_ms": {"affine": k_ms[AFFINE], "attention": k_ms[ATTN]},
-                         "alg_bytes_per_query": BYTES_PER_QUERY},
+                         "alg_bytes_per_query": BYTES_PER_QUERY,
+                         "gather_ceiling": gather_ceiling(nq, k_ms)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "fits": fits, "fits_csr": fits_csr, "dedup": dedup, "sim": sim, "unknown_signature_errors": bad,
         }
@@ -705,7 +732,8 @@ def run_reference(args):
             "value": value, "unit": "predictions/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C5 predict batch (bounded CPU sample)",
+            "config": arm_config(args),
+            "config_sample": {"workload": "C5 predict batch (bounded CPU sample)",
                        "queries_per_step": args.ref_sample},
             "cpu_baseline": {"value": value, "unit": "predictions/s", "cores": threads,
                              "kind": "port",
