@@ -124,7 +124,7 @@ EXPORTS = tuple(_SIGS)
 
 _lock = threading.Lock()
 _lib = None
-_ctx: dict = {}
+_tls = threading.local()
 
 
 def load_library() -> C.CDLL:
@@ -146,20 +146,24 @@ def load_library() -> C.CDLL:
 
 
 def ctx_for(device: torch.device) -> C.c_void_p:
-    """Per-device dooly_ctx, created on first use."""
+    """This thread's dooly_ctx for ``device``, created on first use.
+
+    A dooly_ctx is not thread-safe (include/dooly_b200.h) and ctypes releases
+    the GIL during the call, so every host thread gets its own context."""
     if device.type != "cuda":
         raise DeviceError(f"libdooly_b200 runs on CUDA devices only (got {device})")
     idx = device.index if device.index is not None else torch.cuda.current_device()
-    with _lock:
-        pass
-    if idx not in _ctx:
+    ctxs = getattr(_tls, "ctx", None)
+    if ctxs is None:
+        ctxs = _tls.ctx = {}
+    if idx not in ctxs:
         lib = load_library()
         h = C.c_void_p()
         rc = lib.dooly_ctx_create(idx, C.byref(h))
         if rc != 0:
             raise DeviceError(f"dooly_ctx_create({idx}) failed with status {rc}")
-        _ctx[idx] = h
-    return _ctx[idx]
+        ctxs[idx] = h
+    return ctxs[idx]
 
 
 def check(rc: int, ctx) -> None:
