@@ -602,16 +602,16 @@ def mape(pred: Sequence[float], truth: Sequence[float]) -> float:
 
 
 def predict_host(kind: int, table: torch.Tensor, sig: torch.Tensor, x: torch.Tensor,
-                 out: torch.Tensor, chunk: int = 1 << 24) -> torch.Tensor:
+                 out: torch.Tensor, chunk: int = 1 << 24, n_streams: int = 2) -> torch.Tensor:
     """Host-buffer entry point of K3: pinned host sig (n,) i32 and x (P, n) i32 in,
     pinned host f64 latencies out.  The batch is cut into chunks pipelined over
-    two CUDA streams (H2D copy | kernel | D2H copy overlap); returns ``out``
-    after synchronising."""
+    ``n_streams`` CUDA streams (H2D copy | kernel | D2H copy overlap); returns
+    ``out`` after synchronising."""
     dev = table.device
     n = sig.numel()
     P = x.shape[0]
     cur = torch.cuda.current_stream(dev)
-    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    streams = [torch.cuda.Stream(dev) for _ in range(max(1, n_streams))]
     c = min(chunk, max(n, 1))
     bufs = [(torch.empty(c, dtype=torch.int32, device=dev),
              torch.empty((P, c), dtype=torch.int32, device=dev),
@@ -624,8 +624,8 @@ def predict_host(kind: int, table: torch.Tensor, sig: torch.Tensor, x: torch.Ten
     for i, q0 in enumerate(range(0, n, c)):
         q1 = min(n, q0 + c)
         m = q1 - q0
-        s = streams[i % 2]
-        d_sig, d_x, d_out, d_flags, d_err = bufs[i % 2]
+        s = streams[i % len(streams)]
+        d_sig, d_x, d_out, d_flags, d_err = bufs[i % len(streams)]
         with torch.cuda.stream(s):
             d_sig[:m].copy_(sig[q0:q1], non_blocking=True)
             xs = d_x[:, :m] if m == c else torch.empty((P, m), dtype=torch.int32, device=dev)
