@@ -602,40 +602,59 @@ def mape(pred: Sequence[float], truth: Sequence[float]) -> float:
 
 
 def predict_host(kind: int, table: torch.Tensor, sig: torch.Tensor, x: torch.Tensor,
-                 out: torch.Tensor, chunk: int = 1 << 24, n_streams: int = 2) -> torch.Tensor:
+                 out: torch.Tensor, chunk: int = 1 << 23, n_streams: int = 3) -> torch.Tensor:
     """Host-buffer entry point of K3: pinned host sig (n,) i32 and x (P, n) i32 in,
-    pinned host f64 latencies out.  The batch is cut into chunks pipelined over
-    ``n_streams`` CUDA streams (H2D copy | kernel | D2H copy overlap); returns
-    ``out`` after synchronising."""
-    dev = table.device
-    n = sig.numel()
-    P = x.shape[0]
+    pinned host f64 latencies out (see ``predict_host_many``); returns ``out``."""
+    predict_host_many([(kind, table, sig, x, out)], chunk, n_streams)
+    return out
+
+
+def predict_host_many(batches: Sequence, chunk: int = 1 << 23, n_streams: int = 3) -> None:
+    """Several host-buffer query batches ``(kind, table, sig, x, out)`` (pinned host
+    tensors; tables on the device) through one copy/compute pipeline.  Chunks
+    of all batches are interleaved over ``n_streams`` CUDA streams, so the H2D
+    copy engine, the kernels and the D2H copy engine overlap.  Mixing kinds
+    also balances the link: attention queries are H2D-heavy (16 B in, 8 B
+    out), affine ones symmetric (8 B in, 8 B out).  Synchronises; raises
+    UnknownSignature if any query hit an unfitted row."""
+    if not batches:
+        return
+    dev = batches[0][1].device
     cur = torch.cuda.current_stream(dev)
     streams = [torch.cuda.Stream(dev) for _ in range(max(1, n_streams))]
-    c = min(chunk, max(n, 1))
+    pmax = max(b[3].shape[0] for b in batches)
+    c = min(chunk, max(max(b[2].numel() for b in batches), 1))
     bufs = [(torch.empty(c, dtype=torch.int32, device=dev),
-             torch.empty((P, c), dtype=torch.int32, device=dev),
+             torch.empty((pmax, c), dtype=torch.int32, device=dev),
              torch.empty(c, dtype=torch.float64, device=dev),
              torch.empty((2, (c + 31) // 32), dtype=torch.int32, device=dev),
              torch.full((1,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev))
             for _ in streams]
     for s in streams:
         s.wait_stream(cur)
-    for i, q0 in enumerate(range(0, n, c)):
-        q1 = min(n, q0 + c)
+    work = []                                  # round-robin chunks of every batch
+    cursors = [0] * len(batches)
+    while any(cursors[i] < batches[i][2].numel() for i in range(len(batches))):
+        for i, bt in enumerate(batches):
+            n = bt[2].numel()
+            if cursors[i] < n:
+                work.append((i, cursors[i], min(n, cursors[i] + c)))
+                cursors[i] += c
+    for j, (i, q0, q1) in enumerate(work):
+        kind, table, sig, x, out = batches[i]
+        P = x.shape[0]
         m = q1 - q0
-        s = streams[i % len(streams)]
-        d_sig, d_x, d_out, d_flags, d_err = bufs[i % len(streams)]
+        s = streams[j % len(streams)]
+        d_sig, d_x, d_out, d_flags, d_err = bufs[j % len(streams)]
         with torch.cuda.stream(s):
             d_sig[:m].copy_(sig[q0:q1], non_blocking=True)
-            xs = d_x[:, :m] if m == c else torch.empty((P, m), dtype=torch.int32, device=dev)
+            xs = d_x[:P, :m] if m == c else torch.empty((P, m), dtype=torch.int32, device=dev)
             for p in range(P):
                 xs[p].copy_(x[p, q0:q1], non_blocking=True)
-            predict_batch(kind, table, d_sig[:m], xs, d_out[:m],
-                          d_flags if m == c else None, d_err, want_flags=m == c)
+            predict_batch(kind, table, d_sig[:m], xs, d_out[:m], d_flags if m == c else None,
+                          d_err, want_flags=m == c)
             out[q0:q1].copy_(d_out[:m], non_blocking=True)
     for s in streams:
         s.synchronize()
     if any(int(b[4].item()) != torch.iinfo(torch.int64).max for b in bufs):
         raise UnknownSignature("a query references an unfitted regressor row")
-    return out

@@ -162,6 +162,36 @@ def test_predict_unknown_signature(kind, dev):
     assert np.isnan(out[1]) and np.isnan(out[3]) and np.isfinite(out[0])
 
 
+def test_predict_host_pipeline_matches_device(dev):
+    """Pinned-host entry points (chunked multi-stream pipeline, mixed kinds and a
+    ragged last chunk) return exactly what the device call returns."""
+    from paper_2605_07985_b200.sim import pack_attn, predict_batch, predict_host, predict_host_many
+
+    outs = []
+    batches = []
+    for kind in (AFFINE, ATTN):
+        x, y, off = synth_fit_data(kind, 97, 40, seed=31 + kind)
+        ref_fit = osim.fit(kind, x, y, off)
+        table = {k: ref_fit[k] for k in ("coef", "inv", "lo", "hi")}
+        rows = table_to_rows(kind, table)
+        t = torch.from_numpy(rows.view(np.uint8).reshape(len(rows), -1).copy()).to(dev)
+        k = kind
+        if kind == ATTN:
+            t, k = pack_attn(t), PACKED
+        n = 100_003 + 8 * kind
+        sig, xq = synth_queries(kind, table, n, seed=5 + kind, outside=0.02)
+        dev_out, _, _ = predict_batch(k, t, _i32(sig).to(dev), _i32(xq).to(dev))
+        hs, hx = _i32(sig).pin_memory(), _i32(xq).pin_memory()
+        ho = torch.empty(n, dtype=torch.float64).pin_memory()
+        predict_host(k, t, hs, hx, ho, chunk=4096 * 3, n_streams=2)
+        assert torch.equal(ho, dev_out.cpu())
+        outs.append(dev_out.cpu())
+        batches.append((k, t, hs, hx, torch.empty(n, dtype=torch.float64).pin_memory()))
+    predict_host_many(batches, chunk=8192, n_streams=3)
+    for (_, _, _, _, o), want in zip(batches, outs):
+        assert torch.equal(o, want)
+
+
 def test_attn_pack_header_and_refusals(dev):
     """Pack header fields; tables the 96-B form cannot represent exactly are refused,
     and an unchecked refused table makes predict flag every query (never mispredict)."""
