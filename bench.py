@@ -196,6 +196,29 @@ def load_peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
+def link_ceiling(pinned, dev, h2d: int, d2h: int, step_s: float) -> dict:
+    """Measured pinned-copy bandwidth of this GPU's host link (one copy engine per
+    direction, full duplex) and the e2e step time it allows for these bytes."""
+    import torch
+
+    buf = pinned.view(torch.uint8)
+    d = torch.empty_like(buf, device=dev)
+    bw = {}
+    for name, fn in (("h2d", lambda: d.copy_(buf, non_blocking=True)),
+                     ("d2h", lambda: buf.copy_(d, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        bw[name] = 3 * buf.numel() / (time.perf_counter() - t)
+    del d
+    ideal = max(h2d / bw["h2d"], d2h / bw["d2h"])
+    return {"h2d_gb_s": bw["h2d"] / 1e9, "d2h_gb_s": bw["d2h"] / 1e9, "ideal_step_s": ideal,
+            "frac": ideal / step_s}
+
+
 def gather_ceiling(nq: dict, k_ms: dict):
     """The binding limit of random-row predict on this hardware: the measured
     LDG.256 gather rate of bare 32-B / 96-B rows (tools/gather_probe.py,
@@ -555,7 +578,8 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "queries_per_step_per_gpu": args.e2e_queries,
                "path": "sim.predict_host_many: pinned host -> device -> kernel -> host, both kinds' "
-                       "chunks interleaved over 3 streams"}
+                       "chunks interleaved over 3 streams",
+               "link_ceiling": link_ceiling(host_q[AFFINE][2], dev, h2d, d2h, e_s)}
         del host_q
 
     # ---------------- CPU baseline (rank 0, N=1 only)
