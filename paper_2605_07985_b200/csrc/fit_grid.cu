@@ -43,6 +43,7 @@ constexpr size_t kGridStageMax = 96 * 1024;  // y bytes staged per CTA (2 CTAs/S
 
 struct GridFactor {
   double L[10][10];  // lower Cholesky factor; dropped columns are zero
+  double W[10][10];  // c = W b: the forward+backward solve with drop applied to e_i
   double rd[10];     // 1 / L[j][j], 0 for a dropped column
   double inv[3];
   uint32_t lo[3], hi[3];
@@ -52,6 +53,13 @@ struct GridFactor {
 
 __device__ __forceinline__ double g_u2d(uint32_t x) {
   return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+}
+
+// x * inv in one rounding: 2^52 + x is exact (x < 2^32) and nbias = -2^52 * inv
+// is a power-of-two scaling of inv, so the fused product-sum rounds the exact
+// x * inv once — bit-identical to g_u2d(x) * inv in one FP64 instruction.
+__device__ __forceinline__ double g_scale(uint32_t x, double inv, double nbias) {
+  return fma(__hiloint2double(0x43300000, (int)x), inv, nbias);
 }
 
 __device__ __forceinline__ double g_rcp(double y) {
@@ -98,6 +106,31 @@ __device__ __forceinline__ void grid_monomials(const uint32_t* xs, const double*
     m[8] = f1 * f3;
     m[9] = f2 * f3;
   }
+}
+
+// Training-MAPE prediction from the scaled features only (pass 2): the same
+// polynomial as the design row, regrouped so it needs 9 FMAs and no monomials
+//   c0 + f1(c1 + c4 f1 + c7 f2 + c8 f3) + f2(c2 + c5 f2 + c9 f3) + f3(c3 + c6 f3).
+// fit_err is a diagnostic held to 1e-9 relative, not the bit-exact predict
+// contract, so the regrouping is allowed here (and only here).
+template <int KIND>
+__device__ __forceinline__ double grid_horner(const double* c, const double* f) {
+  if constexpr (KIND == DOOLY_KIND_AFFINE) {
+    return fma(c[1], f[0], c[0]);
+  } else {
+    const double t1 = fma(c[8], f[2], fma(c[7], f[1], fma(c[4], f[0], c[1])));
+    const double t2 = fma(c[9], f[2], fma(c[5], f[1], c[2]));
+    const double t3 = fma(c[6], f[2], c[3]);
+    return fma(f[0], t1, fma(f[1], t2, fma(f[2], t3, c[0])));
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void grid_features(const uint32_t* xs, const double* inv,
+                                              const double* nb, double* f) {
+  constexpr int P = KIND == DOOLY_KIND_AFFINE ? 1 : 3;
+#pragma unroll
+  for (int k = 0; k < P; ++k) f[k] = g_scale(xs[k], inv[k], nb[k]);
 }
 
 // One CTA: box, scaling, Gram of the shared design, Cholesky with drop.
@@ -198,6 +231,22 @@ __global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __re
         for (int i = k; i < NC; ++i) G[i][k] = fma(-gf->L[i][j], gf->L[k][j], G[i][k]);
     }
     for (int i = NC; i < 10; ++i) gf->rd[i] = 0.0;
+    // W = the solve applied to the unit vectors, so per signature c = W b is
+    // NC independent dot products instead of two dependent triangular sweeps.
+    for (int e = 0; e < NC; ++e) {
+      double z[NC], c[NC];
+      for (int j = 0; j < NC; ++j) {
+        double t = j == e ? 1.0 : 0.0;
+        for (int i = 0; i < j; ++i) t = fma(-gf->L[j][i], z[i], t);
+        z[j] = t * gf->rd[j];
+      }
+      for (int j = NC - 1; j >= 0; --j) {
+        double t = z[j];
+        for (int i = j + 1; i < NC; ++i) t = fma(-gf->L[i][j], c[i], t);
+        c[j] = t * gf->rd[j];
+      }
+      for (int j = 0; j < NC; ++j) gf->W[j][e] = c[j];
+    }
     gf->ok = n_pts >= T::NEED ? 1 : 0;
   }
 }
@@ -401,7 +450,7 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
   extern __shared__ __align__(128) unsigned char gdyn[];
   double* stage = reinterpret_cast<double*>(gdyn);  // [R][n_pts]
   __shared__ __align__(8) uint64_t bar[2];
-  __shared__ double sL[NC][NC], srd[NC], sinv[P];
+  __shared__ double sW[NC][NC], sb[R * NC], sinv[P];
   __shared__ uint32_t slo[P], shi[P];
   __shared__ double part[kGW][R * NC];
   __shared__ double scoef[R][NC];
@@ -410,8 +459,7 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
   const int64_t half = n_pts / 2;  // n_pts % 4 == 0 (launcher)
   const int n = (int)n_pts;        // stage <= 96 KB, so n_pts <= 12288
   const int64_t n_groups = (n_sig + R - 1) / R;
-  for (int t = tid; t < NC * NC; t += kGT) sL[t / NC][t % NC] = gf->L[t / NC][t % NC];
-  if (tid < NC) srd[tid] = gf->rd[tid];
+  for (int t = tid; t < NC * NC; t += kGT) sW[t / NC][t % NC] = gf->W[t / NC][t % NC];
   if (tid < P) {
     sinv[tid] = gf->inv[tid];
     slo[tid] = gf->lo[tid];
@@ -435,9 +483,9 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
     for (int r = 0; r < nr; ++r)
       g_bulk(stage + r * n_pts + c * half, y + (s0 + r) * n_pts + c * half, bytes, &bar[c]);
   };
-  double inv[P];
+  double inv[P], nb[P];
 #pragma unroll
-  for (int k = 0; k < P; ++k) inv[k] = sinv[k];
+  for (int k = 0; k < P; ++k) inv[k] = sinv[k], nb[k] = -4503599627370496.0 * sinv[k];
   if (!ok) {
     for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
       const int nr = (int)min((int64_t)R, n_sig - g * R);
@@ -492,24 +540,19 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
         if (lane == 0) part[wid][r * NC + k] = v;
       }
     __syncthreads();
-    if (tid < nr) {
-      double z[NC];
+    if (tid < R * NC) {  // b = sum of the warp partials
+      double t = 0.0;
 #pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        double t = 0.0;
+      for (int w = 0; w < kGW; ++w) t += part[w][tid];
+      sb[tid] = t;
+    }
+    __syncthreads();
+    if (tid < nr * NC) {  // c = W b, one coefficient per thread
+      const int r = tid / NC, j = tid - r * NC;
+      double c = 0.0;
 #pragma unroll
-        for (int w = 0; w < kGW; ++w) t += part[w][tid * NC + j];
-#pragma unroll
-        for (int i = 0; i < j; ++i) t = fma(-sL[j][i], z[i], t);
-        z[j] = t * srd[j];
-      }
-#pragma unroll
-      for (int j = NC - 1; j >= 0; --j) {
-        double t = z[j];
-#pragma unroll
-        for (int i = j + 1; i < NC; ++i) t = fma(-sL[i][j], scoef[tid][i], t);
-        scoef[tid][j] = t * srd[j];
-      }
+      for (int i = 0; i < NC; ++i) c = fma(sW[j][i], sb[r * NC + i], c);
+      scoef[r][j] = c;
     }
     __syncthreads();
     double cf[R][NC], err[R];
@@ -529,19 +572,14 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
           xa[k] = v.x;
           xb[k] = v.y;
         }
-        double ma[NC], mb[NC];
-        grid_monomials<KIND>(xa, inv, ma);
-        grid_monomials<KIND>(xb, inv, mb);
+        double fa[P], fb[P];
+        grid_features<KIND>(xa, inv, nb, fa);
+        grid_features<KIND>(xb, inv, nb, fb);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const double2 yv =
               r < nr ? *reinterpret_cast<const double2*>(stage + r * n + p) : make_double2(1.0, 1.0);
-          double pa = cf[r][0], pb = cf[r][0];
-#pragma unroll
-          for (int k = 1; k < NC; ++k) {
-            pa = fma(cf[r][k], ma[k], pa);
-            pb = fma(cf[r][k], mb[k], pb);
-          }
+          double pa = grid_horner<KIND>(cf[r], fa), pb = grid_horner<KIND>(cf[r], fb);
           pa = fmax(pa, DOOLY_CLAMP_FLOOR);
           pb = fmax(pb, DOOLY_CLAMP_FLOOR);
           err[r] = fma(fabs(pa - yv.x), g_rcp1(yv.x), err[r]);
