@@ -334,7 +334,8 @@ def max_over_ranks(v: float, dist_on: bool) -> float:
 
     if not dist_on:
         return v
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64,
+                     device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -617,21 +618,26 @@ def run_ours(args):
         sha_ms = 0.0
         tot_ms = 0.0
         dig = torch.empty((recs.n, 32), dtype=torch.uint8, device=dev)
+        n_total = world * recs.n   # global record list = the ranks' slices in rank order
         for _ in range(d_steps):
             e0.record(stream)
             hash_records(recs, dig)
             e1.record(stream)
-            r = dedup_digests(dig, None, ws, sync=False)
+            # N > 1: the one exchange step (all-gather of the 32-B digests), then a
+            # global first-occurrence resolve on every rank (dist.dedup_sharded)
+            full = ddist.all_gather_rows(dig, n_total) if dist_on else dig
+            r = dedup_digests(full, None, ws, sync=False)
             e2.record(stream)
             torch.cuda.synchronize()
             sha_ms += e0.elapsed_time(e1)
             tot_ms += e0.elapsed_time(e2)
         barrier_sync(dist_on)
         tot_ms = max_over_ranks(tot_ms / d_steps, dist_on)
-        n_unique = int(dedup_digests(dig, None, ws).n_unique)
+        n_unique = int(dedup_digests(full, None, ws).n_unique)
         msg_len = 8 + 4 + 6 + 4 + 3 * 12 + 4 + 2 * (4 + 16)  # approx canonical length
         dedup = {"value": world * recs.n / (tot_ms / 1e3), "unit": "records/s",
                  "records_per_gpu": recs.n, "unique": n_unique, "ms_per_step": tot_ms,
+                 "exchange": "all-gather of 32-B digests, global resolve" if dist_on else None,
                  "sha_ms": sha_ms / d_steps,
                  "sha_blocks_per_s": recs.n * 2 / (sha_ms / d_steps / 1e3),
                  "bound": "int32 ALU (SHA-256 rounds)"}
@@ -670,6 +676,7 @@ def bench_sim(args, dev, dist_on, rank, world):
     """C4: Llama-3-70B-like tp=4 replicas; regressors from the C4 manifest's sweep."""
     import torch
 
+    from paper_2605_07985_b200 import dist as ddist
     from paper_2605_07985_b200 import modelir
     from paper_2605_07985_b200.profiler import profile_corpus
     from paper_2605_07985_b200.sim import (SchedConfig, ShardedTrace, build_calltree, fit,
@@ -709,7 +716,14 @@ def bench_sim(args, dev, dist_on, rank, world):
     ms = max_over_ranks(e0.elapsed_time(e1), dist_on)
     n_it = int(res.n_iter.sum().item())
     ok = int((res.status != 0).sum().item()) == 0
-    ttft = res.ttft.cpu().numpy()
+    ttft = res.ttft.cpu()
+    if dist_on:   # global percentiles: every rank's TTFTs, NaN-padded to a common length
+        m = int(max_over_ranks(float(ttft.numel()), dist_on))
+        pad = torch.full((m,), float("nan"), dtype=torch.float64)
+        pad[: ttft.numel()] = ttft
+        ttft = ddist.gather_requests(pad.to(dev)).reshape(-1).cpu()
+        ok = max_over_ranks(0.0 if ok else 1.0, dist_on) == 0.0
+    ttft = ttft.numpy()
     return {"value": n / (ms / 1e3), "unit": "requests/s", "ms": ms, "requests": n,
             "shards": S, "iterations_rank0": n_it,
             "iterations_per_s": n_it / (ms / 1e3), "all_ok": ok,

@@ -127,6 +127,8 @@ def _gather_cat(t: torch.Tensor, size: int, group=None) -> torch.Tensor:
                           device=t.device)
         dist.all_gather_into_tensor(out, t, group=group)
         return out
-    parts = [torch.empty_like(t) for _ in range(size)]
-    dist.all_gather(parts, t, group=group)
-    return torch.cat(parts, dim=0)
+    # gloo (CPU tests; several ranks sharing one GPU): exchange through host memory
+    h = t.cpu()
+    parts = [torch.empty_like(h) for _ in range(size)]
+    dist.all_gather(parts, h, group=group)
+    return torch.cat(parts, dim=0).to(t.device)

@@ -1,0 +1,133 @@
+"""N > 1 path on the GPU box: two ranks sharing cuda:0 over gloo (gpurun hands out
+one GPU, and NCCL refuses two ranks on one device).  The sharded dedup and fit
+(paper_2605_07985_b200.dist) run the real sm_100a kernels on each rank's slice,
+exchange through the same collective calls the NCCL path makes, and must equal
+the single-rank results; then bench.py runs under torchrun at --gpus 2."""
+
+from __future__ import annotations
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, world: int, port: int, q) -> None:
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank), DOOLY_DIST_BACKEND="gloo")
+    import torch.distributed as dist
+
+    try:
+        import bench
+        from helpers import AFFINE, ATTN, synth_fit_data
+        from paper_2605_07985_b200 import dist as ddist
+        from paper_2605_07985_b200.profiler import DeviceRecords, dedup_packed
+        from paper_2605_07985_b200.records import pack_uniform  # noqa: F401 (bench uses it)
+        from paper_2605_07985_b200.sim import fit_tables
+
+        assert ddist.init_from_env() == (rank, world)
+        dev = ddist.local_device()
+        assert dev == torch.device("cuda", 0)
+        # ---- dedup: global record list split contiguously, digests all-gathered
+        n_total = 20_011
+        packed, _ = bench.synth_records(n_total, seed=5)
+        whole = dedup_packed(DeviceRecords.from_packed(packed, dev))
+        a, b = ddist.shard_range(n_total, rank, world)
+        mine, _ = bench.synth_records(n_total, seed=5)
+        sl = _slice_packed(mine, a, b)
+        got = ddist.dedup_sharded(DeviceRecords.from_packed(sl, dev), n_total)
+        assert got.n_unique == whole.n_unique
+        for name in ("first", "uid", "is_new", "in_db"):
+            assert torch.equal(getattr(got, name), getattr(whole, name)[a:b]), name
+        assert torch.equal(got.digests, whole.digests[a:b])
+        # ---- fit: contiguous signature ranges, regressor rows all-gathered
+        for kind in (AFFINE, ATTN):
+            x, y, off = synth_fit_data(kind, 301, 64, seed=kind, ragged=True)
+            xt = torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).to(dev)
+            yt = torch.from_numpy(y).to(dev)
+            ref = fit_tables(kind, xt, yt, torch.from_numpy(off).to(dev))
+            shard = ddist.fit_sharded(kind, xt, yt, off)
+            # same kernels, but a signature's points sit at a different alignment
+            # in the rank's slice (TMA head/tail peeling changes the summation
+            # order), so rows agree to the fit contract, not bit for bit
+            nc = 2 if kind == AFFINE else 10
+            ga, gr = shard.table.view(torch.float64), ref.table.view(torch.float64)
+            d = (ga[:, :nc] - gr[:, :nc]).abs().amax(1) / gr[:, :nc].abs().amax(1)
+            assert float(d.max()) <= 1e-11, (kind, float(d.max()))
+            assert torch.equal(ga[:, nc:], gr[:, nc:]), kind        # scaling + box exact
+            assert torch.equal(shard.status, ref.status), kind
+            assert torch.allclose(shard.fit_err, ref.fit_err, rtol=1e-11, atol=0), kind
+        dist.barrier()
+        q.put((rank, "ok"))
+    except Exception as exc:  # surface the failure to the parent
+        import traceback
+
+        q.put((rank, repr(exc) + traceback.format_exc()[-1500:]))
+        raise
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def _slice_packed(packed, a: int, b: int):
+    """Records [a, b) of a packed batch (the string/digest tables are shared)."""
+    from dataclasses import replace
+
+    off = packed.rec_off                      # n start offsets into words
+    w0 = int(off[a])
+    w1 = int(off[b]) if b < packed.n else packed.words.shape[0]
+    return replace(packed, words=packed.words[w0:w1].copy(), rec_off=(off[a:b] - w0).copy(),
+                   repeat=packed.repeat[a:b].copy())
+
+
+def test_two_ranks_one_gpu_sharded_dedup_and_fit():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    results = dict(q.get(timeout=5) for _ in range(2))
+    assert results == {0: "ok", 1: "ok"}, results
+    assert all(p.exitcode == 0 for p in procs)
+
+
+def test_bench_two_ranks_torchrun():
+    """bench.py's N > 1 path end to end (barriers, max-over-ranks timing, the
+    fit-table and digest all-gathers, replica-sharded sim) at small sizes."""
+    env = dict(os.environ, DOOLY_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--queries", "4000000",
+           "--sigs", "20000", "--points", "512", "--records", "100000",
+           "--e2e-queries", "2000000", "--sim-requests", "20000", "--sim-shards", "16",
+           "--csr-fit", "0"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["fits"]["all_fitted"] and not d["unknown_signature_errors"]
+    assert d["dedup"]["exchange"] and d["dedup"]["records_per_gpu"] == 100_000
+    assert d["sim"]["all_ok"] and d["sim"]["requests"] == 20_000
