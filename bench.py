@@ -424,11 +424,29 @@ def run_ours(args):
     from paper_2605_07985_b200._lib import KIND_ATTN_PACKED
     from paper_2605_07985_b200.sim import fit_grid, fit_tables, pack_attn
 
+    from paper_2605_07985_b200.sim import FitResult
+
+    # N > 1: the regressor all-gather fused into the fit (peer stores from the
+    # fit epilogue + a device arrival counter) when every GPU pair has peer
+    # access; otherwise one NCCL all-gather of the rows after the fit
+    peer = None
+    if dist_on and os.environ.get("DOOLY_FIT_ALLGATHER", "fused") == "fused" and \
+            ddist.PeerFitTable.available(world):
+        peer = {k: ddist.PeerFitTable(k, world * n_sig[k], dev) for k in (AFFINE, ATTN)}
+
+    def do_fit(k):
+        if peer is None:
+            return fit_grid(k, fit_in[k][0], fit_in[k][1], fit_out.get(k))
+        r0 = rank * n_sig[k]
+        pt = peer[k].fit_grid(fit_in[k][0], fit_in[k][1], r0)
+        sl = slice(r0, r0 + n_sig[k])
+        return FitResult(k, pt.table[sl], pt.fit_err[sl], pt.status[sl])
+
     fit_out = {}
     packed96 = None
     for _ in range(max(1, args.warmup)):
         for k in (AFFINE, ATTN):
-            fit_out[k] = fit_grid(k, fit_in[k][0], fit_in[k][1], fit_out.get(k))
+            fit_out[k] = do_fit(k)
     barrier_sync(dist_on)
     stream = torch.cuda.current_stream()
     ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -444,12 +462,12 @@ def run_ours(args):
     for _ in range(fit_steps):
         for k in (AFFINE, ATTN):
             ev[k][0].record(stream)
-            fit_out[k] = fit_grid(k, fit_in[k][0], fit_in[k][1], fit_out[k])
+            fit_out[k] = do_fit(k)
             if k == ATTN:   # serving form of the attention table (96-B rows), part of the fit output
                 packed96 = pack_attn(fit_out[k].table, packed96, check=False)
             ev[k][1].record(stream)
         ag0.record(stream)
-        if dist_on:   # the one exchange step: every rank gets every rank's regressor rows
+        if dist_on and peer is None:   # the one exchange step: every rank gets every rank's rows
             full = {k: ddist.gather_requests(fit_out[k].table) for k in (AFFINE, ATTN)}
         ag1.record(stream)
         torch.cuda.synchronize()
@@ -461,6 +479,10 @@ def run_ours(args):
     fit_launches = (_lib.launch_count(dev) - fit_launches0) // fit_steps
     fit_total_ms = max_over_ranks(t_start.elapsed_time(t_end) / fit_steps, dist_on)
     status_ok = all(int((fit_out[k].status != 0).sum().item()) == 0 for k in (AFFINE, ATTN))
+    if peer is not None:   # every rank's rows landed in this rank's full tables
+        for k in (AFFINE, ATTN):
+            peer[k].check()
+            status_ok &= int((peer[k].status != 0).sum().item()) == 0
     fit_bytes = sum(n_sig[k] * n_pts[k] * BYTES_PER_GRID_POINT for k in (AFFINE, ATTN))
     fit_dev_ms = sum(fit_ms.values()) / fit_steps
     fits = {
@@ -471,6 +493,9 @@ def run_ours(args):
         "kernel_ms": {"affine": fit_ms[AFFINE] / fit_steps, "attention": fit_ms[ATTN] / fit_steps,
                       "allgather": ag_ms / fit_steps},
         "launches_per_step": fit_launches,
+        "allgather_path": None if not dist_on else (
+            "fused: peer-memory row stores in the fit epilogue + device arrival counter"
+            if peer is not None else "NCCL all_gather of the regressor rows"),
         "roofline": {"bound": "hbm", "achieved": fit_bytes / (fit_dev_ms / 1e3) / 1e9,
                      "peak": hbm_peak, "unit": "GB/s",
                      "frac": fit_bytes / (fit_dev_ms / 1e3) / 1e9 / hbm_peak,

@@ -166,6 +166,34 @@ int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, c
                    int64_t n_sig, void* table, double* fit_err, uint8_t* status, void* workspace,
                    size_t workspace_bytes, void* stream);
 
+/* Fused fit + all-gather (SURVEY §8(e) "ONE all-gather of the fitted
+ * coefficients", done inside the fit instead of as a separate NCCL call).
+ * Each rank fits its contiguous signature range [row0, row0 + n_sig) of the
+ * global table and its epilogue stores every row, fit_err and status both into
+ * the local full-size arrays and into every peer rank's arrays over peer memory
+ * (CUDA IPC mappings of the peers' buffers, peer access enabled; NVLink P2P
+ * stores on an NVSwitch box).  Then it adds 1 to every rank's arrival counter
+ * (flag, system-scope release) and waits, on the stream, until its own
+ * counter reaches `target` (= world size x call number): after that the full
+ * table is valid on this rank.  The wait gives up after ~20 s and sets
+ * *timed_out (device int32) instead of hanging.  table / fit_err / status are
+ * the LOCAL full arrays (row0 + s addressing); peers.table[p] etc. the peers'. */
+#define DOOLY_MAX_PEERS 7
+typedef struct {
+  int32_t n_peers; /* other ranks, 0..DOOLY_MAX_PEERS */
+  int32_t pad_;
+  int64_t row0;    /* global row of this rank's signature 0 */
+  void* table[DOOLY_MAX_PEERS];
+  double* fit_err[DOOLY_MAX_PEERS];
+  uint8_t* status[DOOLY_MAX_PEERS];
+  uint32_t* flag[DOOLY_MAX_PEERS];
+} dooly_grid_peers;
+int dooly_fit_grid_bcast(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts,
+                         const double* y, int64_t n_sig, void* table, double* fit_err,
+                         uint8_t* status, const dooly_grid_peers* peers, uint32_t* flag,
+                         uint32_t target, int32_t* timed_out, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
 /* ---------------------------------------------------------------- K3 predict
  * Replaces predict.  sig[i] indexes the table; x is
  * feature-major (planes of n_q u32).  out[i] = max(poly, 1e-7) evaluated

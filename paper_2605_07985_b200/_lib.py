@@ -85,6 +85,22 @@ class Sched(C.Structure):
     ]
 
 
+MAX_PEERS = 7
+
+
+class GridPeers(C.Structure):
+    """dooly_grid_peers: the other ranks' buffers for dooly_fit_grid_bcast."""
+    _fields_ = [
+        ("n_peers", C.c_int32),
+        ("pad_", C.c_int32),
+        ("row0", C.c_int64),
+        ("table", C.c_void_p * MAX_PEERS),
+        ("fit_err", C.c_void_p * MAX_PEERS),
+        ("status", C.c_void_p * MAX_PEERS),
+        ("flag", C.c_void_p * MAX_PEERS),
+    ]
+
+
 _P = C.c_void_p
 _I64 = C.c_int64
 _SIGS = {
@@ -110,6 +126,9 @@ _SIGS = {
     "dooly_sim_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
                                  _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "dooly_fit_grid": (C.c_int, [_P, C.c_int, _P, _I64, _P, _I64, _P, _P, _P, _P, C.c_size_t, _P]),
+    "dooly_fit_grid_bcast": (C.c_int, [_P, C.c_int, _P, _I64, _P, _I64, _P, _P, _P,
+                                       C.POINTER(GridPeers), _P, C.c_uint32, _P, _P, C.c_size_t,
+                                       _P]),
     "dooly_attn_pack": (C.c_int, [_P, _P, _I64, _P, _P]),
     "dooly_iter_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _I64, _P, _P,
                                   _P]),

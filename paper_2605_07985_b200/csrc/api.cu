@@ -20,7 +20,10 @@ size_t fit_workspace_size(int kind, int64_t n_sig);
 size_t fit_grid_workspace_size();
 cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
                             int64_t n_sig, void* table, double* fit_err, uint8_t* status,
-                            void* ws, cudaStream_t stream, int n_sm, int64_t* launches);
+                            const dooly_grid_peers* peers, void* ws, cudaStream_t stream,
+                            int n_sm, int64_t* launches);
+cudaError_t launch_grid_peer_sync(const dooly_grid_peers* peers, uint32_t* flag, uint32_t target,
+                                  int32_t* timed_out, cudaStream_t stream, int64_t* launches);
 cudaError_t launch_attn_pack(const void* table, int64_t n_sig, void* packed, cudaStream_t stream,
                              int n_sm, int64_t* launches);
 cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off, int64_t n,
@@ -203,9 +206,42 @@ int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, c
   DeviceGuard g(ctx->device);
   return check_cuda(ctx,
                     dooly::launch_fit_grid(kind, x, n_pts, y, n_sig, table, fit_err, status,
-                                           workspace, (cudaStream_t)stream, ctx->n_sm,
+                                           nullptr, workspace, (cudaStream_t)stream, ctx->n_sm,
                                            &ctx->launches),
                     "fit_grid");
+}
+
+int dooly_fit_grid_bcast(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts,
+                         const double* y, int64_t n_sig, void* table, double* fit_err,
+                         uint8_t* status, const dooly_grid_peers* peers, uint32_t* flag,
+                         uint32_t target, int32_t* timed_out, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (!peers || peers->n_peers < 0 || peers->n_peers > DOOLY_MAX_PEERS || peers->row0 < 0 ||
+      !flag || !timed_out)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: bad peer set");
+  for (int p = 0; p < peers->n_peers; ++p)
+    if (!peers->table[p] || !peers->fit_err[p] || !peers->status[p] || !peers->flag[p] ||
+        (uintptr_t)peers->table[p] % 16)
+      return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: null or misaligned peer buffer");
+  if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: unknown kind");
+  if (n_sig < 0 || n_pts < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: negative size");
+  if (!workspace || workspace_bytes < dooly::fit_grid_workspace_size() ||
+      (uintptr_t)workspace % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: workspace too small or misaligned");
+  if ((n_pts > 0 && !x) || (n_sig > 0 && (!table || !fit_err || !status || (n_pts > 0 && !y))))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: null pointer");
+  if ((uintptr_t)table % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: table must be 16-byte aligned");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = dooly::launch_fit_grid(kind, x, n_pts, y, n_sig, table, fit_err, status, peers,
+                                         workspace, (cudaStream_t)stream, ctx->n_sm,
+                                         &ctx->launches);
+  if (e == cudaSuccess)
+    e = dooly::launch_grid_peer_sync(peers, flag, target, timed_out, (cudaStream_t)stream,
+                                     &ctx->launches);
+  return check_cuda(ctx, e, "fit_grid_bcast");
 }
 
 int dooly_sha256_records(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off,

@@ -251,31 +251,78 @@ __global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __re
   }
 }
 
+// Row emission.  Rows go to the local table at global row pe.row0 + s and,
+// for the fused fit + all-gather (dooly_fit_grid_bcast), to every peer rank's
+// table at the same row over peer memory (NVLink P2P stores): the regressor
+// all-gather of SURVEY §8(e) happens in the fit's own epilogue.  A row is
+// assembled in registers and written as 16-B stores.
 template <int KIND>
-__device__ void write_unfitted_grid(void* table, int64_t s, double* fit_err, uint8_t* status) {
+struct RowBuf {
+  static constexpr int N2 = KIND == DOOLY_KIND_AFFINE ? 2 : 8;  // double2 per row
+  double2 v[N2];
+};
+
+template <int KIND>
+__device__ __forceinline__ RowBuf<KIND> make_row(const double* c, const double* inv,
+                                                 const uint32_t* lo, const uint32_t* hi) {
+  RowBuf<KIND> r;
   if constexpr (KIND == DOOLY_KIND_AFFINE) {
-    dooly_affine_row* row = static_cast<dooly_affine_row*>(table) + s;
-    row->c0 = row->c1 = row->inv_scale = nan64();
-    row->lo = 0xFFFFFFFFu;
-    row->hi = 0;
+    r.v[0] = make_double2(c[0], c[1]);
+    r.v[1] = make_double2(inv[0], __longlong_as_double((long long)(((uint64_t)hi[0] << 32) | lo[0])));
   } else {
-    dooly_attn_row* row = static_cast<dooly_attn_row*>(table) + s;
-    for (int i = 0; i < 10; ++i) row->c[i] = nan64();
-    for (int k = 0; k < 3; ++k) {
-      row->inv_scale[k] = nan64();
-      row->lo[k] = 0xFFFFFFFFu;
-      row->hi[k] = 0;
-    }
+#pragma unroll
+    for (int i = 0; i < 5; ++i) r.v[i] = make_double2(c[2 * i], c[2 * i + 1]);
+    r.v[5] = make_double2(inv[0], inv[1]);
+    r.v[6] = make_double2(inv[2], __longlong_as_double((long long)(((uint64_t)lo[1] << 32) | lo[0])));
+    r.v[7] = make_double2(__longlong_as_double((long long)(((uint64_t)hi[0] << 32) | lo[2])),
+                          __longlong_as_double((long long)(((uint64_t)hi[2] << 32) | hi[1])));
   }
-  fit_err[s] = nan64();
-  status[s] = DOOLY_FIT_INSUFFICIENT;
+  return r;
+}
+
+template <int KIND>
+__device__ __forceinline__ void put_row(void* table, int64_t row, const RowBuf<KIND>& r) {
+  double2* d = reinterpret_cast<double2*>(table) + row * RowBuf<KIND>::N2;
+#pragma unroll
+  for (int i = 0; i < RowBuf<KIND>::N2; ++i) d[i] = r.v[i];
+}
+
+template <int KIND>
+__device__ __forceinline__ void emit_row(const dooly_grid_peers& pe, void* table, double* fit_err,
+                                         uint8_t* status, int64_t s, const RowBuf<KIND>& r,
+                                         double err, uint8_t st) {
+  const int64_t g = pe.row0 + s;
+  put_row<KIND>(table, g, r);
+  fit_err[g] = err;
+  status[g] = st;
+  for (int p = 0; p < pe.n_peers; ++p) {
+    put_row<KIND>(pe.table[p], g, r);
+    pe.fit_err[p][g] = err;
+    pe.status[p][g] = st;
+  }
+  if (pe.n_peers > 0) __threadfence_system();  // peer stores ordered before the arrival signal
+}
+
+template <int KIND>
+__device__ void write_unfitted_grid(const dooly_grid_peers& pe, void* table, int64_t s,
+                                    double* fit_err, uint8_t* status) {
+  double c[10], inv[3];
+  uint32_t lo[3], hi[3];
+  for (int i = 0; i < 10; ++i) c[i] = nan64();
+  for (int k = 0; k < 3; ++k) {
+    inv[k] = nan64();
+    lo[k] = 0xFFFFFFFFu;
+    hi[k] = 0;
+  }
+  emit_row<KIND>(pe, table, fit_err, status, s, make_row<KIND>(c, inv, lo, hi), nan64(),
+                 DOOLY_FIT_INSUFFICIENT);
 }
 
 template <int KIND>
 __global__ void __launch_bounds__(kGT, 2) fit_grid_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
-    uint8_t* __restrict__ status) {
+    uint8_t* __restrict__ status, const dooly_grid_peers pe) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC, R = T::R;
   __shared__ double sL[NC][NC], srd[NC], sinv[P];
@@ -301,7 +348,7 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_kernel(
     const int64_t s0 = g * R;
     const int nr = (int)min((int64_t)R, n_sig - s0);
     if (!ok) {
-      if (tid < nr) write_unfitted_grid<KIND>(table, s0 + tid, fit_err, status);
+      if (tid < nr) write_unfitted_grid<KIND>(pe, table, s0 + tid, fit_err, status);
       continue;
     }
     const double* yg = y + s0 * n_pts;
@@ -390,27 +437,9 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_kernel(
       double e = 0.0;
 #pragma unroll
       for (int w = 0; w < kGW; ++w) e += serr[w][tid];
-      const int64_t s = s0 + tid;
-      fit_err[s] = e / (double)n_pts;
-      status[s] = DOOLY_FIT_OK;
-      if constexpr (KIND == DOOLY_KIND_AFFINE) {
-        dooly_affine_row* row = static_cast<dooly_affine_row*>(table) + s;
-        row->c0 = scoef[tid][0];
-        row->c1 = scoef[tid][1];
-        row->inv_scale = sinv[0];
-        row->lo = slo[0];
-        row->hi = shi[0];
-      } else {
-        dooly_attn_row* row = static_cast<dooly_attn_row*>(table) + s;
-#pragma unroll
-        for (int i = 0; i < 10; ++i) row->c[i] = scoef[tid][i];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          row->inv_scale[k] = sinv[k];
-          row->lo[k] = slo[k];
-          row->hi[k] = shi[k];
-        }
-      }
+      emit_row<KIND>(pe, table, fit_err, status, s0 + tid,
+                     make_row<KIND>(scoef[tid], sinv, slo, shi), e / (double)n_pts,
+                     DOOLY_FIT_OK);
     }
     __syncthreads();
   }
@@ -444,7 +473,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
-    uint8_t* __restrict__ status) {
+    uint8_t* __restrict__ status, const dooly_grid_peers pe) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC, R = T::RS;
   extern __shared__ __align__(128) unsigned char gdyn[];
@@ -489,7 +518,7 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
   if (!ok) {
     for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
       const int nr = (int)min((int64_t)R, n_sig - g * R);
-      if (tid < nr) write_unfitted_grid<KIND>(table, g * R + tid, fit_err, status);
+      if (tid < nr) write_unfitted_grid<KIND>(pe, table, g * R + tid, fit_err, status);
     }
     return;
   }
@@ -602,27 +631,9 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
       double e = 0.0;
 #pragma unroll
       for (int w = 0; w < kGW; ++w) e += serr[w][tid];
-      const int64_t s = s0 + tid;
-      fit_err[s] = e / (double)n_pts;
-      status[s] = DOOLY_FIT_OK;
-      if constexpr (KIND == DOOLY_KIND_AFFINE) {
-        dooly_affine_row* row = static_cast<dooly_affine_row*>(table) + s;
-        row->c0 = scoef[tid][0];
-        row->c1 = scoef[tid][1];
-        row->inv_scale = sinv[0];
-        row->lo = slo[0];
-        row->hi = shi[0];
-      } else {
-        dooly_attn_row* row = static_cast<dooly_attn_row*>(table) + s;
-#pragma unroll
-        for (int i = 0; i < 10; ++i) row->c[i] = scoef[tid][i];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          row->inv_scale[k] = sinv[k];
-          row->lo[k] = slo[k];
-          row->hi[k] = shi[k];
-        }
-      }
+      emit_row<KIND>(pe, table, fit_err, status, s0 + tid,
+                     make_row<KIND>(scoef[tid], sinv, slo, shi), e / (double)n_pts,
+                     DOOLY_FIT_OK);
     }
     __syncthreads();  // scoef / part reused by the next group
   }
@@ -630,8 +641,9 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
 
 template <int KIND>
 static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const double* y, int64_t n_sig,
-                             void* table, double* fit_err, uint8_t* status, void* ws,
-                             cudaStream_t stream, int n_sm, int64_t* launches) {
+                                    void* table, double* fit_err, uint8_t* status,
+                                    const dooly_grid_peers& pe, void* ws, cudaStream_t stream,
+                                    int n_sm, int64_t* launches) {
   GridFactor* gf = static_cast<GridFactor*>(ws);
   fit_grid_prep_kernel<KIND><<<1, kGT, 0, stream>>>(x, n_pts, gf);
   cudaError_t e = cudaGetLastError();
@@ -649,7 +661,7 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
     int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
     if (blocks > groups) blocks = groups;
     kern<<<(unsigned)blocks, kGT, stage, stream>>>(x, n_pts, y, n_sig, gf, table, fit_err,
-                                                   status);
+                                                   status, pe);
     *launches += 1;
     return cudaGetLastError();
   }
@@ -659,21 +671,64 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
   if (blocks > groups) blocks = groups;
   fit_grid_kernel<KIND><<<(unsigned)blocks, kGT, 0, stream>>>(x, n_pts, y, n_sig, gf, table,
-                                                              fit_err, status);
+                                                              fit_err, status, pe);
   *launches += 1;
   return cudaGetLastError();
+}
+
+// Arrival signal of the fused all-gather: one increment of every rank's
+// counter (peers over NVLink, system-scope release after this rank's rows).
+__global__ void grid_peer_signal_kernel(const dooly_grid_peers pe, uint32_t* flag) {
+  const int t = threadIdx.x;
+  __threadfence_system();
+  if (t < pe.n_peers) {
+    atomicAdd_system(pe.flag[t], 1u);
+  } else if (t == pe.n_peers) {
+    atomicAdd_system(flag, 1u);
+  }
+}
+
+// Wait until every rank has signalled (counter >= target).  Bounded: after
+// ~20 s it gives up and raises *timed_out instead of hanging the GPU.
+__global__ void grid_peer_wait_kernel(const uint32_t* flag, uint32_t target, int32_t* timed_out) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if ((int32_t)(v - target) >= 0) break;
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > 20ull * 1000000000ull) {
+      *timed_out = 1;
+      break;
+    }
+    __nanosleep(256);
+  }
+  __threadfence_system();
 }
 
 size_t fit_grid_workspace_size() { return (sizeof(GridFactor) + 255) & ~(size_t)255; }
 
 cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
                             int64_t n_sig, void* table, double* fit_err, uint8_t* status,
-                            void* ws, cudaStream_t stream, int n_sm, int64_t* launches) {
+                            const dooly_grid_peers* peers, void* ws, cudaStream_t stream,
+                            int n_sm, int64_t* launches) {
+  dooly_grid_peers pe{};
+  if (peers) pe = *peers;
   if (kind == DOOLY_KIND_AFFINE)
-    return launch_grid_kind<DOOLY_KIND_AFFINE>(x, n_pts, y, n_sig, table, fit_err, status, ws,
+    return launch_grid_kind<DOOLY_KIND_AFFINE>(x, n_pts, y, n_sig, table, fit_err, status, pe, ws,
                                                stream, n_sm, launches);
-  return launch_grid_kind<DOOLY_KIND_ATTN>(x, n_pts, y, n_sig, table, fit_err, status, ws, stream,
-                                           n_sm, launches);
+  return launch_grid_kind<DOOLY_KIND_ATTN>(x, n_pts, y, n_sig, table, fit_err, status, pe, ws,
+                                           stream, n_sm, launches);
+}
+
+cudaError_t launch_grid_peer_sync(const dooly_grid_peers* peers, uint32_t* flag, uint32_t target,
+                                  int32_t* timed_out, cudaStream_t stream, int64_t* launches) {
+  grid_peer_signal_kernel<<<1, 32, 0, stream>>>(*peers, flag);
+  grid_peer_wait_kernel<<<1, 1, 0, stream>>>(flag, target, timed_out);
+  *launches += 2;
+  return cudaGetLastError();
 }
 
 }  // namespace dooly

@@ -8,7 +8,11 @@ the plumbing.
           for any world size) and keeps its slice.
   fit     signatures split into contiguous ranges, no communication during the
           fit, ONE all-gather of the fitted regressor rows (p*8 + box bytes per
-          signature) so every rank holds the full table.
+          signature) so every rank holds the full table.  On GPUs with peer
+          access (NVLink/NVSwitch) the all-gather is fused into the fit:
+          ``PeerFitTable`` maps every rank's table into every other rank (CUDA
+          IPC) and dooly_fit_grid_bcast's epilogue stores each row into all of
+          them, then a device-side arrival counter replaces the collective.
   predict queries split contiguously; no collective (each rank holds the table).
   sim     S fixed replica shards, shard s on rank s mod world ("replicas only",
           no data-path collective); per-request TTFT/TPOT gathered at the end.
@@ -16,6 +20,7 @@ the plumbing.
 
 from __future__ import annotations
 
+import ctypes as C
 import os
 from typing import Optional
 
@@ -132,3 +137,94 @@ def _gather_cat(t: torch.Tensor, size: int, group=None) -> torch.Tensor:
     parts = [torch.empty_like(h) for _ in range(size)]
     dist.all_gather(parts, h, group=group)
     return torch.cat(parts, dim=0).to(t.device)
+
+
+class PeerFitTable:
+    """Full regressor table replicated on every rank and written in place by every
+    rank's fit (dooly_fit_grid_bcast): the fused fit + all-gather.
+
+    Each rank allocates the full (n_total rows) table, fit_err, status and a u32
+    arrival counter, shares them with the other ranks through CUDA IPC (torch's
+    tensor-sharing reductions, handles exchanged once with all_gather_object),
+    and hands the peers' mapped device pointers to the kernel.  ``fit_grid``
+    fits this rank's rows [row0, row0 + n) and returns when (on the stream) all
+    ranks' rows have landed.  Needs peer access between every pair of GPUs
+    (``available``); callers use ``fit_sharded``/NCCL otherwise."""
+
+    def __init__(self, kind: int, n_total: int, device: torch.device, group=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        from . import _lib
+
+        self.kind, self.n_total, self.device = kind, n_total, device
+        rank, size = world()
+        self.rank, self.size = rank, size
+        if size - 1 > _lib.MAX_PEERS:
+            raise ValueError(f"at most {_lib.MAX_PEERS + 1} ranks per fused fit")
+        self.table = torch.zeros((n_total, _lib.ROW_BYTES[kind]), dtype=torch.uint8, device=device)
+        self.fit_err = torch.zeros(n_total, dtype=torch.float64, device=device)
+        self.status = torch.zeros(n_total, dtype=torch.uint8, device=device)
+        self.flag = torch.zeros(4, dtype=torch.int32, device=device)   # [0] arrivals
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        mine = [reduce_tensor(t) for t in (self.table, self.fit_err, self.status, self.flag)]
+        handles = [None] * size
+        if size > 1:
+            dist.all_gather_object(handles, mine, group=group)
+        self._peer_tensors = []          # keep the IPC mappings alive
+        pe = _lib.GridPeers()
+        pe.n_peers = size - 1
+        j = 0
+        for r in range(size):
+            if r == rank:
+                continue
+            ts = [fn(*args) for fn, args in handles[r]]
+            self._peer_tensors.append(ts)
+            pe.table[j], pe.fit_err[j], pe.status[j], pe.flag[j] = (t.data_ptr() for t in ts)
+            j += 1
+        self._peers = pe
+        self.calls = 0
+        if size > 1:
+            dist.barrier(group=group)
+
+    @staticmethod
+    def available(size: int) -> bool:
+        """Peer access between every pair of the first ``size`` visible GPUs (a
+        single GPU shared by several ranks maps its own memory and qualifies)."""
+        n = torch.cuda.device_count()
+        if n == 0:
+            return False
+        devs = sorted({r % n for r in range(size)})
+        return all(torch.cuda.can_device_access_peer(a, b)
+                   for a in devs for b in devs if a != b)
+
+    def fit_grid(self, x: torch.Tensor, y: torch.Tensor, row0: int):
+        """Fit y's signatures as global rows [row0, row0 + len(y)) into every
+        rank's table; returns self once the stream has seen all ranks arrive."""
+        from . import _lib
+        from .sim import _grid_workspace
+
+        n_sig, n_pts = y.shape
+        if row0 < 0 or row0 + n_sig > self.n_total:
+            raise ValueError("rows outside the shared table")
+        if x.shape != (_lib.PLANES[self.kind], n_pts):
+            raise ValueError(f"x must have shape ({_lib.PLANES[self.kind]}, {n_pts})")
+        x, y = x.contiguous(), y.contiguous()
+        self.calls += 1
+        self._peers.row0 = row0
+        lib = _lib.load_library()
+        ws = _grid_workspace(self.device)
+        ctx = _lib.ctx_for(self.device)
+        _lib.check(lib.dooly_fit_grid_bcast(
+            ctx, self.kind, x.data_ptr() if x.numel() else 0, n_pts,
+            y.data_ptr() if y.numel() else 0, n_sig, self.table.data_ptr(),
+            self.fit_err.data_ptr(), self.status.data_ptr(), C.byref(self._peers),
+            self.flag.data_ptr(), (self.calls * self.size) & 0xFFFFFFFF,
+            self.timed_out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr(self.device)),
+            ctx)
+        return self
+
+    def check(self) -> None:
+        """Raise if a wait gave up (a peer never arrived); synchronises."""
+        if int(self.timed_out.item()):
+            raise RuntimeError("fused fit all-gather: a peer rank never signalled (timeout)")

@@ -196,12 +196,7 @@ def fit_grid(kind: int, x: torch.Tensor, y: torch.Tensor,
                         torch.empty(n_sig, dtype=torch.float64, device=dev),
                         torch.empty(n_sig, dtype=torch.uint8, device=dev))
     lib = _lib.load_library()
-    need = int(lib.dooly_fit_grid_workspace_size())
-    key = (str(dev), "grid")
-    ws = _FIT_WS.get(key)
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
-        _FIT_WS[key] = ws
+    ws = _grid_workspace(dev)
     ctx = _lib.ctx_for(dev)
     _lib.check(lib.dooly_fit_grid(
         ctx, kind, x.data_ptr() if x.numel() else 0, n_pts, y.data_ptr() if y.numel() else 0,
@@ -209,6 +204,16 @@ def fit_grid(kind: int, x: torch.Tensor, y: torch.Tensor,
         out.status.data_ptr() if n_sig else 0, ws.data_ptr(), ws.numel(), _lib.stream_ptr(dev)),
         ctx)
     return out
+
+
+def _grid_workspace(dev: torch.device) -> torch.Tensor:
+    need = int(_lib.load_library().dooly_fit_grid_workspace_size())
+    key = (str(dev), "grid")
+    ws = _FIT_WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
+        _FIT_WS[key] = ws
+    return ws
 
 
 PACK_HEADER = np.dtype([("magic", "<u4"), ("ok", "<u4"), ("width", "<u4", 3), ("max_hi", "<u4", 3),

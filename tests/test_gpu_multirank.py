@@ -2,7 +2,11 @@
 one GPU, and NCCL refuses two ranks on one device).  The sharded dedup and fit
 (paper_2605_07985_b200.dist) run the real sm_100a kernels on each rank's slice,
 exchange through the same collective calls the NCCL path makes, and must equal
-the single-rank results; then bench.py runs under torchrun at --gpus 2."""
+the single-rank results.  The fused fit + all-gather (PeerFitTable,
+dooly_fit_grid_bcast) maps each rank's table into the other through CUDA IPC —
+the same mechanism as across NVLink peers, minus the link — and must reproduce
+the single-rank table bit for bit.  Then bench.py runs under torchrun at
+--gpus 2."""
 
 from __future__ import annotations
 
@@ -41,7 +45,7 @@ def _worker(rank: int, world: int, port: int, q) -> None:
         from paper_2605_07985_b200 import dist as ddist
         from paper_2605_07985_b200.profiler import DeviceRecords, dedup_packed
         from paper_2605_07985_b200.records import pack_uniform  # noqa: F401 (bench uses it)
-        from paper_2605_07985_b200.sim import fit_tables
+        from paper_2605_07985_b200.sim import fit_grid, fit_tables
 
         assert ddist.init_from_env() == (rank, world)
         dev = ddist.local_device()
@@ -75,6 +79,23 @@ def _worker(rank: int, world: int, port: int, q) -> None:
             assert torch.equal(ga[:, nc:], gr[:, nc:]), kind        # scaling + box exact
             assert torch.equal(shard.status, ref.status), kind
             assert torch.allclose(shard.fit_err, ref.fit_err, rtol=1e-11, atol=0), kind
+        # ---- fused fit + all-gather: rows stored into every rank's table by the
+        # fit epilogue over peer (IPC-mapped) memory, device arrival counter
+        assert ddist.PeerFitTable.available(world)
+        for kind in (AFFINE, ATTN):
+            n_total = 601
+            xg, yg = bench.gen_grid_fit_data(kind, n_total, 512, dev, seed=7 + kind)
+            ref = fit_grid(kind, xg, yg)
+            pt = ddist.PeerFitTable(kind, n_total, dev)
+            a, b = ddist.shard_range(n_total, rank, world)
+            for _ in range(3):                      # repeated calls: counter targets advance
+                pt.fit_grid(xg, yg[a:b], a)
+            torch.cuda.synchronize()
+            pt.check()
+            assert torch.equal(pt.table, ref.table), kind
+            assert torch.equal(pt.status, ref.status), kind
+            assert torch.equal(pt.fit_err, ref.fit_err), kind
+            dist.barrier()
         dist.barrier()
         q.put((rank, "ok"))
     except Exception as exc:  # surface the failure to the parent
@@ -129,5 +150,6 @@ def test_bench_two_ranks_torchrun():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
     assert d["fits"]["all_fitted"] and not d["unknown_signature_errors"]
+    assert d["fits"]["allgather_path"].startswith("fused")
     assert d["dedup"]["exchange"] and d["dedup"]["records_per_gpu"] == 100_000
     assert d["sim"]["all_ok"] and d["sim"]["requests"] == 20_000
