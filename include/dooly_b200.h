@@ -41,6 +41,9 @@ extern "C" {
 #define DOOLY_ERR_NON_TERMINATION 5    /* errors.py:84 NonTermination */
 #define DOOLY_ERR_CUDA 6
 
+/* peer ranks a fused compute + all-gather call can write (8-GPU box) */
+#define DOOLY_MAX_PEERS 7
+
 /* regression kinds (App. A.7 of SURVEY.md) */
 #define DOOLY_KIND_AFFINE 0 /* [1, f]                      num_toks-type feature  */
 #define DOOLY_KIND_ATTN 1   /* [1,f1,f2,f3,f1²,f2²,f3²,f1f2,f1f3,f2f3]  (prefill_toks, batch, kv_tokens) */
@@ -125,6 +128,26 @@ int dooly_sha256_records(dooly_ctx* ctx, const uint32_t* words, const int64_t* r
                          int64_t n_sym, const uint8_t* attr_digests, int64_t n_attr,
                          uint8_t* out_digest, void* stream);
 
+/* Fused hash + all-gather for the multi-GPU dedup: as
+ * dooly_sha256_records, but record i's digest goes to out_digest[row0 + i] (the
+ * LOCAL full-size gathered array) and to every peer rank's gathered array at
+ * the same row over peer memory; then the arrival counter handshake of
+ * dooly_fit_grid_bcast (flag / target / timed_out).  After it every rank holds
+ * all ranks' digests in global record order, ready for dooly_dedup_digests. */
+typedef struct {
+  int32_t n_peers; /* other ranks, 0..DOOLY_MAX_PEERS */
+  int32_t pad_;
+  int64_t row0;    /* global index of this rank's record 0 */
+  uint8_t* digest[DOOLY_MAX_PEERS];
+  uint32_t* flag[DOOLY_MAX_PEERS];
+} dooly_digest_peers;
+int dooly_sha256_records_bcast(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off,
+                               int64_t n, const uint8_t* op_bytes, const int64_t* op_off,
+                               int64_t n_ops, const uint8_t* sym_bytes, const int64_t* sym_off,
+                               int64_t n_sym, const uint8_t* attr_digests, int64_t n_attr,
+                               uint8_t* out_digest, const dooly_digest_peers* peers,
+                               uint32_t* flag, uint32_t target, int32_t* timed_out, void* stream);
+
 /* Plain SHA-256 of n byte messages (msgs + off[i]..off[i+1]) — signature_hash(bytes). */
 int dooly_sha256_messages(dooly_ctx* ctx, const uint8_t* msgs, const int64_t* off, int64_t n,
                           uint8_t* out_digest, void* stream);
@@ -178,7 +201,6 @@ int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, c
  * table is valid on this rank.  The wait gives up after ~20 s and sets
  * *timed_out (device int32) instead of hanging.  table / fit_err / status are
  * the LOCAL full arrays (row0 + s addressing); peers.table[p] etc. the peers'. */
-#define DOOLY_MAX_PEERS 7
 typedef struct {
   int32_t n_peers; /* other ranks, 0..DOOLY_MAX_PEERS */
   int32_t pad_;

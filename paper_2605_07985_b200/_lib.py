@@ -101,6 +101,17 @@ class GridPeers(C.Structure):
     ]
 
 
+class DigestPeers(C.Structure):
+    """dooly_digest_peers: the other ranks' gathered digest arrays."""
+    _fields_ = [
+        ("n_peers", C.c_int32),
+        ("pad_", C.c_int32),
+        ("row0", C.c_int64),
+        ("digest", C.c_void_p * MAX_PEERS),
+        ("flag", C.c_void_p * MAX_PEERS),
+    ]
+
+
 _P = C.c_void_p
 _I64 = C.c_int64
 _SIGS = {
@@ -112,6 +123,9 @@ _SIGS = {
     "dooly_sha256_records": (C.c_int, [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _I64,
                                        _P, _P]),
     "dooly_sha256_messages": (C.c_int, [_P, _P, _P, _I64, _P, _P]),
+    "dooly_sha256_records_bcast": (C.c_int, [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P,
+                                             _I64, _P, C.POINTER(DigestPeers), _P, C.c_uint32, _P,
+                                             _P]),
     "dooly_dedup_workspace_size": (C.c_size_t, [_I64, _I64]),
     "dooly_dedup_digests": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P,
                                       C.c_size_t, _P]),

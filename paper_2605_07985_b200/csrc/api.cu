@@ -22,15 +22,17 @@ cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const do
                             int64_t n_sig, void* table, double* fit_err, uint8_t* status,
                             const dooly_grid_peers* peers, void* ws, cudaStream_t stream,
                             int n_sm, int64_t* launches);
-cudaError_t launch_grid_peer_sync(const dooly_grid_peers* peers, uint32_t* flag, uint32_t target,
-                                  int32_t* timed_out, cudaStream_t stream, int64_t* launches);
 cudaError_t launch_attn_pack(const void* table, int64_t n_sig, void* packed, cudaStream_t stream,
                              int n_sm, int64_t* launches);
 cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off, int64_t n,
                                   const uint8_t* op_bytes, const int64_t* op_off,
                                   const uint8_t* sym_bytes, const int64_t* sym_off,
                                   const uint8_t* attr_digests, uint8_t* out, cudaStream_t stream,
-                                  int n_sm, int64_t* launches);
+                                  int n_sm, int64_t* launches,
+                                  const dooly_digest_peers* peers = nullptr);
+cudaError_t launch_peer_sync(int n_peers, uint32_t* const* peer_flags, uint32_t* flag,
+                             uint32_t target, int32_t* timed_out, cudaStream_t stream,
+                             int64_t* launches);
 cudaError_t launch_sha256_messages(const uint8_t* msgs, const int64_t* off, int64_t n,
                                    uint8_t* out, cudaStream_t stream, int n_sm);
 size_t dedup_workspace_size(int64_t n, int64_t n_db);
@@ -239,8 +241,8 @@ int dooly_fit_grid_bcast(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_
                                          workspace, (cudaStream_t)stream, ctx->n_sm,
                                          &ctx->launches);
   if (e == cudaSuccess)
-    e = dooly::launch_grid_peer_sync(peers, flag, target, timed_out, (cudaStream_t)stream,
-                                     &ctx->launches);
+    e = dooly::launch_peer_sync(peers->n_peers, peers->flag, flag, target, timed_out,
+                                (cudaStream_t)stream, &ctx->launches);
   return check_cuda(ctx, e, "fit_grid_bcast");
 }
 
@@ -263,6 +265,40 @@ int dooly_sha256_records(dooly_ctx* ctx, const uint32_t* words, const int64_t* r
                                                  (cudaStream_t)stream, ctx->n_sm,
                                                  &ctx->launches),
                     "sha256_records");
+}
+
+int dooly_sha256_records_bcast(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off,
+                               int64_t n, const uint8_t* op_bytes, const int64_t* op_off,
+                               int64_t n_ops, const uint8_t* sym_bytes, const int64_t* sym_off,
+                               int64_t n_sym, const uint8_t* attr_digests, int64_t n_attr,
+                               uint8_t* out_digest, const dooly_digest_peers* peers,
+                               uint32_t* flag, uint32_t target, int32_t* timed_out,
+                               void* stream) {
+  (void)n_ops;
+  (void)n_sym;
+  (void)n_attr;
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records_bcast: negative size");
+  if (n > 0 && (!words || !rec_off || !op_bytes || !op_off || !out_digest))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records_bcast: null pointer");
+  if (!peers || peers->n_peers < 0 || peers->n_peers > DOOLY_MAX_PEERS || peers->row0 < 0 ||
+      !flag || !timed_out)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records_bcast: bad peer set");
+  for (int p = 0; p < peers->n_peers; ++p)
+    if (!peers->digest[p] || !peers->flag[p] || (uintptr_t)peers->digest[p] % 16)
+      return fail(ctx, DOOLY_ERR_INVALID_ARG,
+                  "sha256_records_bcast: null or misaligned peer buffer");
+  if ((uintptr_t)out_digest % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records_bcast: digests must be 16-B aligned");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = dooly::launch_sha256_records(words, rec_off, n, op_bytes, op_off, sym_bytes,
+                                               sym_off, attr_digests, out_digest,
+                                               (cudaStream_t)stream, ctx->n_sm, &ctx->launches,
+                                               peers);
+  if (e == cudaSuccess)
+    e = dooly::launch_peer_sync(peers->n_peers, peers->flag, flag, target, timed_out,
+                                (cudaStream_t)stream, &ctx->launches);
+  return check_cuda(ctx, e, "sha256_records_bcast");
 }
 
 int dooly_sha256_messages(dooly_ctx* ctx, const uint8_t* msgs, const int64_t* off, int64_t n,

@@ -676,38 +676,6 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   return cudaGetLastError();
 }
 
-// Arrival signal of the fused all-gather: one increment of every rank's
-// counter (peers over NVLink, system-scope release after this rank's rows).
-__global__ void grid_peer_signal_kernel(const dooly_grid_peers pe, uint32_t* flag) {
-  const int t = threadIdx.x;
-  __threadfence_system();
-  if (t < pe.n_peers) {
-    atomicAdd_system(pe.flag[t], 1u);
-  } else if (t == pe.n_peers) {
-    atomicAdd_system(flag, 1u);
-  }
-}
-
-// Wait until every rank has signalled (counter >= target).  Bounded: after
-// ~20 s it gives up and raises *timed_out instead of hanging the GPU.
-__global__ void grid_peer_wait_kernel(const uint32_t* flag, uint32_t target, int32_t* timed_out) {
-  uint64_t t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (;;) {
-    uint32_t v;
-    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if ((int32_t)(v - target) >= 0) break;
-    uint64_t t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    if (t1 - t0 > 20ull * 1000000000ull) {
-      *timed_out = 1;
-      break;
-    }
-    __nanosleep(256);
-  }
-  __threadfence_system();
-}
-
 size_t fit_grid_workspace_size() { return (sizeof(GridFactor) + 255) & ~(size_t)255; }
 
 cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
@@ -721,14 +689,6 @@ cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const do
                                                stream, n_sm, launches);
   return launch_grid_kind<DOOLY_KIND_ATTN>(x, n_pts, y, n_sig, table, fit_err, status, pe, ws,
                                            stream, n_sm, launches);
-}
-
-cudaError_t launch_grid_peer_sync(const dooly_grid_peers* peers, uint32_t* flag, uint32_t target,
-                                  int32_t* timed_out, cudaStream_t stream, int64_t* launches) {
-  grid_peer_signal_kernel<<<1, 32, 0, stream>>>(*peers, flag);
-  grid_peer_wait_kernel<<<1, 1, 0, stream>>>(flag, target, timed_out);
-  *launches += 2;
-  return cudaGetLastError();
 }
 
 }  // namespace dooly

@@ -176,13 +176,25 @@ struct ShaStream {
     o4[0] = make_uint4(bswap32(h[0]), bswap32(h[1]), bswap32(h[2]), bswap32(h[3]));
     o4[1] = make_uint4(bswap32(h[4]), bswap32(h[5]), bswap32(h[6]), bswap32(h[7]));
   }
+  // The same digest into every peer rank's gathered array (fused all-gather).
+  __device__ void broadcast(const dooly_digest_peers& pe, int64_t row) const {
+    const uint4 a = make_uint4(bswap32(h[0]), bswap32(h[1]), bswap32(h[2]), bswap32(h[3]));
+    const uint4 b = make_uint4(bswap32(h[4]), bswap32(h[5]), bswap32(h[6]), bswap32(h[7]));
+    for (int p = 0; p < pe.n_peers; ++p) {
+      uint4* o4 = reinterpret_cast<uint4*>(pe.digest[p] + row * 32);
+      o4[0] = a;
+      o4[1] = b;
+    }
+    if (pe.n_peers > 0) __threadfence_system();
+  }
 };
 
 __global__ void __launch_bounds__(SHA_THREADS) sha256_records_kernel(
     const uint32_t* __restrict__ words, const int64_t* __restrict__ rec_off, int64_t n,
     const uint8_t* __restrict__ op_bytes, const int64_t* __restrict__ op_off,
     const uint8_t* __restrict__ sym_bytes, const int64_t* __restrict__ sym_off,
-    const uint8_t* __restrict__ attr_digests, uint8_t* __restrict__ out) {
+    const uint8_t* __restrict__ attr_digests, uint8_t* __restrict__ out,
+    const dooly_digest_peers pe) {
   __shared__ uint32_t s_buf[SHA_THREADS * SHA_STRIDE];
   ShaStream st;
   for (int64_t base = (int64_t)blockIdx.x * SHA_THREADS; base < n;
@@ -213,7 +225,8 @@ __global__ void __launch_bounds__(SHA_THREADS) sha256_records_kernel(
       for (int k = 0; k < 8; ++k) st.put_be32(bswap32(d[k]));
     }
     }
-    st.finish(out + i * 32, valid);
+    st.finish(out + (pe.row0 + i) * 32, valid);
+    if (valid && pe.n_peers > 0) st.broadcast(pe, pe.row0 + i);
   }
 }
 
@@ -242,11 +255,13 @@ cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off,
                                   const uint8_t* op_bytes, const int64_t* op_off,
                                   const uint8_t* sym_bytes, const int64_t* sym_off,
                                   const uint8_t* attr_digests, uint8_t* out, cudaStream_t stream,
-                                  int n_sm, int64_t* launches) {
+                                  int n_sm, int64_t* launches, const dooly_digest_peers* peers) {
   if (n == 0) return cudaSuccess;
   *launches += 1;
+  dooly_digest_peers pe{};
+  if (peers) pe = *peers;
   sha256_records_kernel<<<(unsigned)sha_blocks(n, n_sm), SHA_THREADS, 0, stream>>>(
-      words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off, attr_digests, out);
+      words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off, attr_digests, out, pe);
   return cudaGetLastError();
 }
 

@@ -104,13 +104,19 @@ def fit_sharded(kind: int, x: torch.Tensor, y: torch.Tensor, off: np.ndarray, gr
 
 
 def dedup_sharded(recs_local, n_total: int, db_digests: Optional[torch.Tensor] = None,
-                  workspace=None, group=None):
-    """Hash the local records, all-gather digests, dedup globally, keep local slice."""
+                  workspace=None, group=None, peer_digests: Optional["PeerDigests"] = None):
+    """Hash the local records, all-gather digests, dedup globally, keep local slice.
+
+    With ``peer_digests`` the hash kernel itself stores every digest into all
+    ranks' gathered arrays (fused hash + all-gather) instead of an NCCL call."""
     from .profiler import DedupResult, dedup_digests, hash_records
 
     rank, size = world()
-    local = hash_records(recs_local)
-    full = all_gather_rows(local, n_total, group) if size > 1 else local
+    if peer_digests is not None:
+        full = peer_digests.hash(recs_local, shard_range(n_total, rank, size)[0])
+    else:
+        local = hash_records(recs_local)
+        full = all_gather_rows(local, n_total, group) if size > 1 else local
     res = dedup_digests(full, db_digests, workspace, sync=True)
     a, b = shard_range(n_total, rank, size)
     return DedupResult(res.digests[a:b], res.first[a:b], res.uid[a:b], res.is_new[a:b],
@@ -152,8 +158,6 @@ class PeerFitTable:
     (``available``); callers use ``fit_sharded``/NCCL otherwise."""
 
     def __init__(self, kind: int, n_total: int, device: torch.device, group=None):
-        from torch.multiprocessing.reductions import reduce_tensor
-
         from . import _lib
 
         self.kind, self.n_total, self.device = kind, n_total, device
@@ -166,37 +170,16 @@ class PeerFitTable:
         self.status = torch.zeros(n_total, dtype=torch.uint8, device=device)
         self.flag = torch.zeros(4, dtype=torch.int32, device=device)   # [0] arrivals
         self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)
-        torch.cuda.synchronize(device)
-        mine = [reduce_tensor(t) for t in (self.table, self.fit_err, self.status, self.flag)]
-        handles = [None] * size
-        if size > 1:
-            dist.all_gather_object(handles, mine, group=group)
-        self._peer_tensors = []          # keep the IPC mappings alive
+        self._peer_tensors = _share_with_peers(
+            [self.table, self.fit_err, self.status, self.flag], group)   # keeps mappings alive
         pe = _lib.GridPeers()
         pe.n_peers = size - 1
-        j = 0
-        for r in range(size):
-            if r == rank:
-                continue
-            ts = [fn(*args) for fn, args in handles[r]]
-            self._peer_tensors.append(ts)
+        for j, ts in enumerate(self._peer_tensors):
             pe.table[j], pe.fit_err[j], pe.status[j], pe.flag[j] = (t.data_ptr() for t in ts)
-            j += 1
         self._peers = pe
         self.calls = 0
-        if size > 1:
-            dist.barrier(group=group)
 
-    @staticmethod
-    def available(size: int) -> bool:
-        """Peer access between every pair of the first ``size`` visible GPUs (a
-        single GPU shared by several ranks maps its own memory and qualifies)."""
-        n = torch.cuda.device_count()
-        if n == 0:
-            return False
-        devs = sorted({r % n for r in range(size)})
-        return all(torch.cuda.can_device_access_peer(a, b)
-                   for a in devs for b in devs if a != b)
+    available = staticmethod(lambda size: peer_access_available(size))
 
     def fit_grid(self, x: torch.Tensor, y: torch.Tensor, row0: int):
         """Fit y's signatures as global rows [row0, row0 + len(y)) into every
@@ -228,3 +211,80 @@ class PeerFitTable:
         """Raise if a wait gave up (a peer never arrived); synchronises."""
         if int(self.timed_out.item()):
             raise RuntimeError("fused fit all-gather: a peer rank never signalled (timeout)")
+
+
+def peer_access_available(size: int) -> bool:
+    """Peer access between every pair of the GPUs ``size`` ranks use (a single
+    GPU shared by several ranks maps its own memory and qualifies)."""
+    n = torch.cuda.device_count()
+    if n == 0:
+        return False
+    devs = sorted({r % n for r in range(size)})
+    return all(torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs if a != b)
+
+
+def _share_with_peers(tensors, group=None) -> list:
+    """CUDA-IPC map this rank's ``tensors`` into every other rank (torch's
+    tensor-sharing reductions; handles exchanged once with all_gather_object).
+    Returns, for each other rank in rank order, its tensors mapped here."""
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    rank, size = world()
+    torch.cuda.synchronize(tensors[0].device)
+    mine = [reduce_tensor(t) for t in tensors]
+    handles = [None] * size
+    if size > 1:
+        dist.all_gather_object(handles, mine, group=group)
+    peers = [[fn(*args) for fn, args in handles[r]] for r in range(size) if r != rank]
+    if size > 1:
+        dist.barrier(group=group)
+    return peers
+
+
+class PeerDigests:
+    """Gathered digest array replicated on every rank and written in place by
+    every rank's hash kernel (dooly_sha256_records_bcast): the fused
+    hash + all-gather step of the multi-GPU dedup."""
+
+    def __init__(self, n_total: int, device: torch.device, group=None):
+        from . import _lib
+
+        rank, size = world()
+        if size - 1 > _lib.MAX_PEERS:
+            raise ValueError(f"at most {_lib.MAX_PEERS + 1} ranks per fused hash")
+        self.n_total, self.device, self.size = n_total, device, size
+        self.digests = torch.zeros((n_total, 32), dtype=torch.uint8, device=device)
+        self.flag = torch.zeros(4, dtype=torch.int32, device=device)
+        self.timed_out = torch.zeros(1, dtype=torch.int32, device=device)
+        self._peer_tensors = _share_with_peers([self.digests, self.flag], group)
+        pe = _lib.DigestPeers()
+        pe.n_peers = size - 1
+        for j, (d, f) in enumerate(self._peer_tensors):
+            pe.digest[j], pe.flag[j] = d.data_ptr(), f.data_ptr()
+        self._peers = pe
+        self.calls = 0
+
+    def hash(self, recs, row0: int) -> torch.Tensor:
+        """Hash this rank's records as global rows [row0, row0 + recs.n) into every
+        rank's array; returns the full (n_total, 32) digests once (on the stream)
+        all ranks have arrived."""
+        from . import _lib
+
+        if row0 < 0 or row0 + recs.n > self.n_total:
+            raise ValueError("records outside the gathered digest array")
+        self.calls += 1
+        self._peers.row0 = row0
+        ctx = _lib.ctx_for(self.device)
+        _lib.check(_lib.load_library().dooly_sha256_records_bcast(
+            ctx, recs.words.data_ptr(), recs.rec_off.data_ptr(), recs.n,
+            recs.op_bytes.data_ptr(), recs.op_off.data_ptr(), recs.op_off.numel() - 1,
+            recs.sym_bytes.data_ptr(), recs.sym_off.data_ptr(), recs.sym_off.numel() - 1,
+            recs.attr_digests.data_ptr(), recs.attr_digests.numel() // 32,
+            self.digests.data_ptr(), C.byref(self._peers), self.flag.data_ptr(),
+            (self.calls * self.size) & 0xFFFFFFFF, self.timed_out.data_ptr(),
+            _lib.stream_ptr(self.device)), ctx)
+        return self.digests
+
+    def check(self) -> None:
+        if int(self.timed_out.item()):
+            raise RuntimeError("fused hash all-gather: a peer rank never signalled (timeout)")

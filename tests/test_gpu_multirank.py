@@ -62,6 +62,15 @@ def _worker(rank: int, world: int, port: int, q) -> None:
         for name in ("first", "uid", "is_new", "in_db"):
             assert torch.equal(getattr(got, name), getattr(whole, name)[a:b]), name
         assert torch.equal(got.digests, whole.digests[a:b])
+        # fused hash + all-gather (digests stored into both ranks by the hash kernel)
+        pd = ddist.PeerDigests(n_total, dev)
+        for _ in range(2):
+            got = ddist.dedup_sharded(DeviceRecords.from_packed(sl, dev), n_total, peer_digests=pd)
+        torch.cuda.synchronize()
+        pd.check()
+        assert torch.equal(pd.digests, whole.digests)
+        for name in ("first", "uid", "is_new", "in_db"):
+            assert torch.equal(getattr(got, name), getattr(whole, name)[a:b]), name
         # ---- fit: contiguous signature ranges, regressor rows all-gathered
         for kind in (AFFINE, ATTN):
             x, y, off = synth_fit_data(kind, 301, 64, seed=kind, ragged=True)
@@ -151,5 +160,5 @@ def test_bench_two_ranks_torchrun():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
     assert d["fits"]["all_fitted"] and not d["unknown_signature_errors"]
     assert d["fits"]["allgather_path"].startswith("fused")
-    assert d["dedup"]["exchange"] and d["dedup"]["records_per_gpu"] == 100_000
+    assert d["dedup"]["exchange"].startswith("fused") and d["dedup"]["records_per_gpu"] == 100_000
     assert d["sim"]["all_ok"] and d["sim"]["requests"] == 20_000
