@@ -432,7 +432,12 @@ def run_ours(args):
     peer = None
     if dist_on and os.environ.get("DOOLY_FIT_ALLGATHER", "fused") == "fused" and \
             ddist.PeerFitTable.available(world):
-        peer = {k: ddist.PeerFitTable(k, world * n_sig[k], dev) for k in (AFFINE, ATTN)}
+        try:   # raises on every rank together if any rank cannot map its peers
+            peer = {k: ddist.PeerFitTable(k, world * n_sig[k], dev) for k in (AFFINE, ATTN)}
+        except RuntimeError as exc:
+            peer = None
+            if rank == 0:
+                print(f"fused all-gather unavailable ({exc}); using NCCL", file=sys.stderr)
 
     def do_fit(k):
         if peer is None:

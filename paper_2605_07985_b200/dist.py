@@ -235,9 +235,17 @@ def _share_with_peers(tensors, group=None) -> list:
     handles = [None] * size
     if size > 1:
         dist.all_gather_object(handles, mine, group=group)
-    peers = [[fn(*args) for fn, args in handles[r]] for r in range(size) if r != rank]
-    if size > 1:
-        dist.barrier(group=group)
+    err = None
+    try:
+        peers = [[fn(*args) for fn, args in handles[r]] for r in range(size) if r != rank]
+    except Exception as exc:  # e.g. IPC not permitted: every rank must learn it together
+        peers, err = None, exc
+    if size > 1:   # agree on success so no rank is left waiting in a later collective
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32,
+                          device=tensors[0].device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            raise RuntimeError(f"peer mapping failed on some rank: {err!r}")
     return peers
 
 
