@@ -15,7 +15,11 @@ import torch
 
 from .errors import DeviceError, raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libdooly_b200.so"
+import os as _os
+
+# DOOLY_LIB_PATH: load an alternative build (tuning experiments in tools/)
+LIB_PATH = Path(_os.environ.get("DOOLY_LIB_PATH") or
+                Path(__file__).resolve().parent / "_lib" / "libdooly_b200.so")
 
 KIND_AFFINE = 0
 KIND_ATTN = 1

@@ -33,7 +33,10 @@ template <int KIND>
 struct GridTraits;
 template <>
 struct GridTraits<DOOLY_KIND_AFFINE> {
-  static constexpr int P = 1, NC = 2, NEED = 4, R = 8, RS = 3;
+#ifndef DOOLY_AFFINE_RS
+#define DOOLY_AFFINE_RS 3
+#endif
+  static constexpr int P = 1, NC = 2, NEED = 4, R = 8, RS = DOOLY_AFFINE_RS;
 };
 template <>
 struct GridTraits<DOOLY_KIND_ATTN> {
@@ -639,6 +642,163 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
   }
 }
 
+// ---- warp-per-signature variant (no shared-memory stage, no CTA barriers).
+// One warp owns one signature at a time: pass 1 streams its y row from HBM
+// tagged L2::evict_last, the warp reduces b with shuffles, lanes 0..NC-1 form
+// c = W b and broadcast it, and pass 2 re-reads the row — an L2 hit, because
+// the launch keeps (warps in flight x 8 B x n_pts) well inside L2 — tagged
+// evict_first.  x (the shared grid) is read through L1, which this kernel
+// leaves entirely to it.  y crosses HBM once; there is no stage to fill or
+// drain, so every warp streams independently.
+__device__ __forceinline__ double4 g_ld_y(const double* p, bool keep) {
+  double4 v;
+  if (keep)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+  return v;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
+    const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
+    const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
+    uint8_t* __restrict__ status, const dooly_grid_peers pe) {
+  using T = GridTraits<KIND>;
+  constexpr int P = T::P, NC = T::NC;
+  // attention (FP64-bound) prefetches the next step's y/x ahead of its math;
+  // affine (HBM-bound, little math per point) measured faster without it
+  constexpr bool kPipe = KIND == DOOLY_KIND_ATTN;
+  __shared__ double sW[NC][NC];
+  __shared__ double sinv[P];
+  __shared__ uint32_t slo[P], shi[P];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int t = tid; t < NC * NC; t += blockDim.x) sW[t / NC][t % NC] = gf->W[t / NC][t % NC];
+  if (tid < P) {
+    sinv[tid] = gf->inv[tid];
+    slo[tid] = gf->lo[tid];
+    shi[tid] = gf->hi[tid];
+  }
+  const bool ok = gf->ok != 0;
+  __syncthreads();
+  double inv[P], nb[P];
+#pragma unroll
+  for (int k = 0; k < P; ++k) inv[k] = sinv[k], nb[k] = -4503599627370496.0 * sinv[k];
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int n = (int)n_pts;  // n_pts % 4 == 0, n_pts < 2^31 (launcher)
+  for (int64_t s = warp; s < n_sig; s += n_warps) {
+    if (!ok) {
+      if (lane == 0) write_unfitted_grid<KIND>(pe, table, s, fit_err, status);
+      continue;
+    }
+    const double* ys = y + s * n_pts;
+    // ---- pass 1: b = M^T y, 4 consecutive points per lane per step
+    double acc[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+    auto pass1_step = [&](const double4& yv, const uint4* xv) {
+      const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t xs[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+          xs[k] = j == 0 ? xv[k].x : j == 1 ? xv[k].y : j == 2 ? xv[k].z : xv[k].w;
+        double f[P];
+        grid_features<KIND>(xs, inv, nb, f);
+        if constexpr (KIND == DOOLY_KIND_AFFINE) {
+          acc[0] += yy[j];
+          acc[1] = fma(yy[j], f[0], acc[1]);
+        } else {
+          const double y1 = yy[j] * f[0], y2 = yy[j] * f[1], y3 = yy[j] * f[2];
+          acc[0] += yy[j];
+          acc[1] += y1;
+          acc[2] += y2;
+          acc[3] += y3;
+          acc[4] = fma(y1, f[0], acc[4]);
+          acc[5] = fma(y2, f[1], acc[5]);
+          acc[6] = fma(y3, f[2], acc[6]);
+          acc[7] = fma(y1, f[1], acc[7]);
+          acc[8] = fma(y1, f[2], acc[8]);
+          acc[9] = fma(y2, f[2], acc[9]);
+        }
+      }
+    };
+    double c[NC];
+    double err = 0.0;
+    auto pass2_step = [&](const double4& yv, const uint4* xv) {
+      const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t xs[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+          xs[k] = j == 0 ? xv[k].x : j == 1 ? xv[k].y : j == 2 ? xv[k].z : xv[k].w;
+        double f[P];
+        grid_features<KIND>(xs, inv, nb, f);
+        const double pr = fmax(grid_horner<KIND>(c, f), DOOLY_CLAMP_FLOOR);
+        err = fma(fabs(pr - yy[j]), g_rcp1(yy[j]), err);
+      }
+    };
+    // One pass over the row.  Attention (FP64-bound) issues the next step's
+    // y/x loads before this step's math; affine (HBM-bound, little math per
+    // point) measured faster with the plain loop (3.1 vs 3.4 ms / 0.5M sigs).
+    auto sweep = [&](bool keep, auto&& step) {
+      if constexpr (kPipe) {
+        int p = 4 * lane;
+        if (p >= n) return;  // rows shorter than 128 points leave upper lanes idle
+        double4 yv = g_ld_y(ys + p, keep);
+        uint4 xv[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) xv[k] = __ldg(reinterpret_cast<const uint4*>(x + k * n + p));
+        for (; p < n; p += 128) {
+          const double4 ycur = yv;
+          uint4 xcur[P];
+#pragma unroll
+          for (int k = 0; k < P; ++k) xcur[k] = xv[k];
+          if (p + 128 < n) {
+            yv = g_ld_y(ys + p + 128, keep);
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+              xv[k] = __ldg(reinterpret_cast<const uint4*>(x + k * n + p + 128));
+          }
+          step(ycur, xcur);
+        }
+      } else {
+        for (int p = 4 * lane; p < n; p += 128) {
+          const double4 yv = g_ld_y(ys + p, keep);
+          uint4 xv[P];
+#pragma unroll
+          for (int k = 0; k < P; ++k) xv[k] = __ldg(reinterpret_cast<const uint4*>(x + k * n + p));
+          step(yv, xv);
+        }
+      }
+    };
+    sweep(true, pass1_step);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k] = g_warp_sum(acc[k]);
+    // ---- c = W b: lane j < NC forms coefficient j, then broadcast
+    double cj = 0.0;
+    if (lane < NC) {
+#pragma unroll
+      for (int i = 0; i < NC; ++i) cj = fma(sW[lane][i], acc[i], cj);
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) c[k] = __shfl_sync(0xFFFFFFFFu, cj, k);
+    // ---- pass 2: training MAPE, the row re-read from L2
+    sweep(false, pass2_step);
+    err = g_warp_sum(err);
+    if (lane == 0)
+      emit_row<KIND>(pe, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
+                     err / (double)n_pts, DOOLY_FIT_OK);
+  }
+}
+
 template <int KIND>
 static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const double* y, int64_t n_sig,
                                     void* table, double* fit_err, uint8_t* status,
@@ -650,8 +810,24 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   if (e != cudaSuccess) return e;
   *launches += 1;
   if (n_sig == 0) return cudaSuccess;
+  const char* which = getenv("DOOLY_FIT_GRID_KERNEL");  // "warp" (default) | "stage" | "plain"
+  const bool want_warp = which == nullptr || which[0] == 'w';
+  if (want_warp && n_pts % 4 == 0 && n_pts < (1ll << 30) && (uintptr_t)y % 32 == 0 &&
+      (uintptr_t)x % 16 == 0) {
+    auto kern = fit_grid_warp_kernel<KIND>;
+    const int warps_per_sm = getenv("DOOLY_FIT_GRID_WARPS")
+                                        ? atoi(getenv("DOOLY_FIT_GRID_WARPS"))
+                                        : 16;
+    // warps in flight x row bytes must stay well inside L2 so pass 2 re-reads hit
+    int64_t blocks = (int64_t)n_sm * (warps_per_sm > 8 ? warps_per_sm / 8 : 1);
+    const int64_t need = (n_sig + 7) / 8;
+    if (blocks > need) blocks = need;
+    kern<<<(unsigned)blocks, 256, 0, stream>>>(x, n_pts, y, n_sig, gf, table, fit_err, status, pe);
+    *launches += 1;
+    return cudaGetLastError();
+  }
   const size_t stage = (size_t)GridTraits<KIND>::RS * n_pts * 8;
-  static const bool no_stage = getenv("DOOLY_FIT_GRID_NO_STAGE") != nullptr;
+  const bool no_stage = which != nullptr && which[0] == 'p';
   if (!no_stage && stage <= kGridStageMax && n_pts % 4 == 0 && (uintptr_t)y % 16 == 0) {
     auto kern = fit_grid_stage_kernel<KIND>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGridStageMax);

@@ -60,10 +60,14 @@ def _oracle(kind, x, y):
 
 
 @pytest.mark.parametrize("kind", [AFFINE, ATTN])
-@pytest.mark.parametrize("n_sig,n_pts", [(1, 512), (37, 512), (301, 512), (37, 510), (9, 4096)])
-def test_fit_grid_matches_oracle_and_csr(kind, n_sig, n_pts, dev):
-    """n_pts % 4 == 0 takes the shared-memory staged kernel, 510 the direct one."""
+@pytest.mark.parametrize("n_sig,n_pts", [(1, 512), (37, 512), (301, 512), (37, 510), (9, 4096), (7, 64), (5, 136)])
+@pytest.mark.parametrize("kernel", ["warp", "stage"])
+def test_fit_grid_matches_oracle_and_csr(kind, n_sig, n_pts, kernel, dev, monkeypatch):
+    """n_pts % 4 == 0 takes the warp-per-signature kernel (default) or the
+    shared-memory staged one (DOOLY_FIT_GRID_KERNEL=stage); 510 the direct one."""
     from paper_2605_07985_b200.sim import fit_tables
+
+    monkeypatch.setenv("DOOLY_FIT_GRID_KERNEL", kernel)
 
     rng = np.random.default_rng(17 + kind + n_sig)
     x = _grid(kind, n_pts, rng)[:, :n_pts]
