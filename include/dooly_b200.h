@@ -183,8 +183,9 @@ int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const 
  * y is row-major (n_sig, n_pts) f64.  Same rows, fit_err and statuses as
  * dooly_fit with pt_off[s] = s * n_pts and x repeated per signature, but the
  * Gram matrix, its factor, the scaling and the box are built once.
- * Workspace: dooly_fit_grid_workspace_size() bytes of device memory. */
-size_t dooly_fit_grid_workspace_size(void);
+ * Workspace: dooly_fit_grid_workspace_size(kind, n_pts) bytes of device memory
+ * (the shared factor plus the scaled feature planes of the grid). */
+size_t dooly_fit_grid_workspace_size(int kind, int64_t n_pts);
 int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
                    int64_t n_sig, void* table, double* fit_err, uint8_t* status, void* workspace,
                    size_t workspace_bytes, void* stream);

@@ -138,7 +138,7 @@ _SIGS = {
                             _P]),
     "dooly_predict": (C.c_int, [_P, C.c_int, _P, _I64, _P, _P, _I64, _P, _P, _P, _P]),
     "dooly_attn_pack_bytes": (C.c_size_t, [_I64]),
-    "dooly_fit_grid_workspace_size": (C.c_size_t, []),
+    "dooly_fit_grid_workspace_size": (C.c_size_t, [C.c_int, _I64]),
     "dooly_dedup": (C.c_int, [_P, _P, _P, _I64, _P, _P, _I64, _P, _P, _I64, _P, _I64, _P, _I64,
                               _P, _P, _P, _P, _P, _P, _P, C.c_size_t, _P]),
     "dooly_sim_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,

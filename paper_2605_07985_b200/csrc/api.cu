@@ -17,7 +17,7 @@ cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double*
                        uint8_t* status, void* ws, cudaStream_t stream, int n_sm,
                        int64_t* launches);
 size_t fit_workspace_size(int kind, int64_t n_sig);
-size_t fit_grid_workspace_size();
+size_t fit_grid_workspace_size(int kind, int64_t n_pts);
 cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
                             int64_t n_sig, void* table, double* fit_err, uint8_t* status,
                             const dooly_grid_peers* peers, void* ws, cudaStream_t stream,
@@ -189,7 +189,9 @@ int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const 
                     "fit");
 }
 
-size_t dooly_fit_grid_workspace_size(void) { return dooly::fit_grid_workspace_size(); }
+size_t dooly_fit_grid_workspace_size(int kind, int64_t n_pts) {
+  return dooly::fit_grid_workspace_size(kind, n_pts);
+}
 
 int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
                    int64_t n_sig, void* table, double* fit_err, uint8_t* status, void* workspace,
@@ -198,7 +200,7 @@ int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, c
   if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: unknown kind");
   if (n_sig < 0 || n_pts < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: negative size");
-  if (!workspace || workspace_bytes < dooly::fit_grid_workspace_size() ||
+  if (!workspace || workspace_bytes < dooly::fit_grid_workspace_size(kind, n_pts) ||
       (uintptr_t)workspace % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: workspace too small or misaligned");
   if ((n_pts > 0 && !x) || (n_sig > 0 && (!table || !fit_err || !status || (n_pts > 0 && !y))))
@@ -229,7 +231,7 @@ int dooly_fit_grid_bcast(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_
   if (kind != DOOLY_KIND_AFFINE && kind != DOOLY_KIND_ATTN)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: unknown kind");
   if (n_sig < 0 || n_pts < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: negative size");
-  if (!workspace || workspace_bytes < dooly::fit_grid_workspace_size() ||
+  if (!workspace || workspace_bytes < dooly::fit_grid_workspace_size(kind, n_pts) ||
       (uintptr_t)workspace % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: workspace too small or misaligned");
   if ((n_pts > 0 && !x) || (n_sig > 0 && (!table || !fit_err || !status || (n_pts > 0 && !y))))

@@ -54,6 +54,8 @@ struct GridFactor {
   int32_t pad_;
 };
 
+static size_t grid_factor_bytes() { return (sizeof(GridFactor) + 255) & ~(size_t)255; }
+
 __device__ __forceinline__ double g_u2d(uint32_t x) {
   return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
 }
@@ -139,7 +141,8 @@ __device__ __forceinline__ void grid_features(const uint32_t* xs, const double* 
 // One CTA: box, scaling, Gram of the shared design, Cholesky with drop.
 template <int KIND>
 __global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __restrict__ x,
-                                                            int64_t n_pts, GridFactor* gf) {
+                                                            int64_t n_pts, GridFactor* gf,
+                                                            double* __restrict__ fplanes) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC, NT = NC * (NC + 1) / 2;
   __shared__ uint32_t smn[kGW][3], smx[kGW][3];
@@ -186,6 +189,10 @@ __global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __re
   double inv[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) inv[k] = sinv[k];
+  for (int64_t p = tid; p < n_pts; p += kGT)
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+      fplanes[k * n_pts + p] = g_scale(x[k * n_pts + p], inv[k], -4503599627370496.0 * inv[k]);
   double acc[NT];
 #pragma unroll
   for (int i = 0; i < NT; ++i) acc[i] = 0.0;
@@ -663,9 +670,18 @@ __device__ __forceinline__ double4 g_ld_y(const double* p, bool keep) {
   return v;
 }
 
+// Feature planes: read-only, shared by every warp, kept in L1.
+__device__ __forceinline__ double4 g_ld_f(const double* p) {
+  double4 v;
+  asm("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p));
+  return v;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
-    const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
+    const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
     uint8_t* __restrict__ status, const dooly_grid_peers pe) {
   using T = GridTraits<KIND>;
@@ -701,16 +717,14 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     double acc[NC];
 #pragma unroll
     for (int k = 0; k < NC; ++k) acc[k] = 0.0;
-    auto pass1_step = [&](const double4& yv, const uint4* xv) {
+    auto pass1_step = [&](const double4& yv, const double4* fv) {
       const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        uint32_t xs[P];
+        double f[P];
 #pragma unroll
         for (int k = 0; k < P; ++k)
-          xs[k] = j == 0 ? xv[k].x : j == 1 ? xv[k].y : j == 2 ? xv[k].z : xv[k].w;
-        double f[P];
-        grid_features<KIND>(xs, inv, nb, f);
+          f[k] = j == 0 ? fv[k].x : j == 1 ? fv[k].y : j == 2 ? fv[k].z : fv[k].w;
         if constexpr (KIND == DOOLY_KIND_AFFINE) {
           acc[0] += yy[j];
           acc[1] = fma(yy[j], f[0], acc[1]);
@@ -731,51 +745,50 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     };
     double c[NC];
     double err = 0.0;
-    auto pass2_step = [&](const double4& yv, const uint4* xv) {
+    auto pass2_step = [&](const double4& yv, const double4* fv) {
       const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        uint32_t xs[P];
+        double f[P];
 #pragma unroll
         for (int k = 0; k < P; ++k)
-          xs[k] = j == 0 ? xv[k].x : j == 1 ? xv[k].y : j == 2 ? xv[k].z : xv[k].w;
-        double f[P];
-        grid_features<KIND>(xs, inv, nb, f);
+          f[k] = j == 0 ? fv[k].x : j == 1 ? fv[k].y : j == 2 ? fv[k].z : fv[k].w;
         const double pr = fmax(grid_horner<KIND>(c, f), DOOLY_CLAMP_FLOOR);
         err = fma(fabs(pr - yy[j]), g_rcp1(yy[j]), err);
       }
     };
-    // One pass over the row.  Attention (FP64-bound) issues the next step's
-    // y/x loads before this step's math; affine (HBM-bound, little math per
-    // point) measured faster with the plain loop (3.1 vs 3.4 ms / 0.5M sigs).
+    // One pass over the row: 4 consecutive points per lane per step, y from
+    // HBM/L2 and the scaled features f from the L1-resident planes.  Attention
+    // (FP64-bound) runs two steps per trip with both steps' loads issued first
+    // (ping-pong, no register copies); affine (HBM-bound, little math per
+    // point) measured faster with the plain loop.
+    auto ldf = [&](int p, double4* fv) {
+#pragma unroll
+      for (int k = 0; k < P; ++k) fv[k] = g_ld_f(fpl + k * n + p);
+    };
     auto sweep = [&](bool keep, auto&& step) {
       if constexpr (kPipe) {
         int p = 4 * lane;
-        if (p >= n) return;  // rows shorter than 128 points leave upper lanes idle
-        double4 yv = g_ld_y(ys + p, keep);
-        uint4 xv[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) xv[k] = __ldg(reinterpret_cast<const uint4*>(x + k * n + p));
-        for (; p < n; p += 128) {
-          const double4 ycur = yv;
-          uint4 xcur[P];
-#pragma unroll
-          for (int k = 0; k < P; ++k) xcur[k] = xv[k];
-          if (p + 128 < n) {
-            yv = g_ld_y(ys + p + 128, keep);
-#pragma unroll
-            for (int k = 0; k < P; ++k)
-              xv[k] = __ldg(reinterpret_cast<const uint4*>(x + k * n + p + 128));
-          }
-          step(ycur, xcur);
+        for (; p + 128 < n; p += 256) {
+          const double4 ya = g_ld_y(ys + p, keep), yb = g_ld_y(ys + p + 128, keep);
+          double4 fa[P], fb[P];
+          ldf(p, fa);
+          ldf(p + 128, fb);
+          step(ya, fa);
+          step(yb, fb);
+        }
+        if (p < n) {
+          const double4 ya = g_ld_y(ys + p, keep);
+          double4 fa[P];
+          ldf(p, fa);
+          step(ya, fa);
         }
       } else {
         for (int p = 4 * lane; p < n; p += 128) {
           const double4 yv = g_ld_y(ys + p, keep);
-          uint4 xv[P];
-#pragma unroll
-          for (int k = 0; k < P; ++k) xv[k] = __ldg(reinterpret_cast<const uint4*>(x + k * n + p));
-          step(yv, xv);
+          double4 fv[P];
+          ldf(p, fv);
+          step(yv, fv);
         }
       }
     };
@@ -805,7 +818,8 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
                                     const dooly_grid_peers& pe, void* ws, cudaStream_t stream,
                                     int n_sm, int64_t* launches) {
   GridFactor* gf = static_cast<GridFactor*>(ws);
-  fit_grid_prep_kernel<KIND><<<1, kGT, 0, stream>>>(x, n_pts, gf);
+  double* fpl = reinterpret_cast<double*>(static_cast<char*>(ws) + grid_factor_bytes());
+  fit_grid_prep_kernel<KIND><<<1, kGT, 0, stream>>>(x, n_pts, gf, fpl);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 1;
@@ -813,7 +827,7 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   const char* which = getenv("DOOLY_FIT_GRID_KERNEL");  // "warp" (default) | "stage" | "plain"
   const bool want_warp = which == nullptr || which[0] == 'w';
   if (want_warp && n_pts % 4 == 0 && n_pts < (1ll << 30) && (uintptr_t)y % 32 == 0 &&
-      (uintptr_t)x % 16 == 0) {
+      (uintptr_t)ws % 32 == 0) {
     auto kern = fit_grid_warp_kernel<KIND>;
     const int warps_per_sm = getenv("DOOLY_FIT_GRID_WARPS")
                                         ? atoi(getenv("DOOLY_FIT_GRID_WARPS"))
@@ -822,7 +836,8 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
     int64_t blocks = (int64_t)n_sm * (warps_per_sm > 8 ? warps_per_sm / 8 : 1);
     const int64_t need = (n_sig + 7) / 8;
     if (blocks > need) blocks = need;
-    kern<<<(unsigned)blocks, 256, 0, stream>>>(x, n_pts, y, n_sig, gf, table, fit_err, status, pe);
+    kern<<<(unsigned)blocks, 256, 0, stream>>>(fpl, n_pts, y, n_sig, gf, table, fit_err, status,
+                                               pe);
     *launches += 1;
     return cudaGetLastError();
   }
@@ -852,7 +867,12 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   return cudaGetLastError();
 }
 
-size_t fit_grid_workspace_size() { return (sizeof(GridFactor) + 255) & ~(size_t)255; }
+// Workspace: the GridFactor, then the scaled feature planes f_k(p) = RN(x_k(p) * inv_k)
+// (P x n_pts f64) that the warp kernel reads instead of converting x per point.
+size_t fit_grid_workspace_size(int kind, int64_t n_pts) {
+  const int P = kind == DOOLY_KIND_AFFINE ? 1 : 3;
+  return grid_factor_bytes() + (size_t)P * (size_t)(n_pts > 0 ? n_pts : 0) * 8;
+}
 
 cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
                             int64_t n_sig, void* table, double* fit_err, uint8_t* status,

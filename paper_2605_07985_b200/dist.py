@@ -196,7 +196,7 @@ class PeerFitTable:
         self.calls += 1
         self._peers.row0 = row0
         lib = _lib.load_library()
-        ws = _grid_workspace(self.device)
+        ws = _grid_workspace(self.device, self.kind, n_pts)
         ctx = _lib.ctx_for(self.device)
         _lib.check(lib.dooly_fit_grid_bcast(
             ctx, self.kind, x.data_ptr() if x.numel() else 0, n_pts,

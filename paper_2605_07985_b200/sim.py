@@ -196,7 +196,7 @@ def fit_grid(kind: int, x: torch.Tensor, y: torch.Tensor,
                         torch.empty(n_sig, dtype=torch.float64, device=dev),
                         torch.empty(n_sig, dtype=torch.uint8, device=dev))
     lib = _lib.load_library()
-    ws = _grid_workspace(dev)
+    ws = _grid_workspace(dev, kind, n_pts)
     ctx = _lib.ctx_for(dev)
     _lib.check(lib.dooly_fit_grid(
         ctx, kind, x.data_ptr() if x.numel() else 0, n_pts, y.data_ptr() if y.numel() else 0,
@@ -206,8 +206,8 @@ def fit_grid(kind: int, x: torch.Tensor, y: torch.Tensor,
     return out
 
 
-def _grid_workspace(dev: torch.device) -> torch.Tensor:
-    need = int(_lib.load_library().dooly_fit_grid_workspace_size())
+def _grid_workspace(dev: torch.device, kind: int, n_pts: int) -> torch.Tensor:
+    need = int(_lib.load_library().dooly_fit_grid_workspace_size(kind, n_pts))
     key = (str(dev), "grid")
     ws = _FIT_WS.get(key)
     if ws is None or ws.numel() < need:
