@@ -39,6 +39,8 @@ AFFINE, ATTN = 0, 1
 BYTES_PER_QUERY = {AFFINE: 4 + 4 + 8 + 0.25, ATTN: 4 + 12 + 8 + 0.25}   # sig + x + out + 2 flag bits
 BYTES_PER_POINT = {AFFINE: 4 + 8, ATTN: 12 + 8}                          # x u32 planes + y f64
 BYTES_PER_GRID_POINT = 8                     # shared grid: y f64 per point (x counted once per kind)
+FP64_PER_ATTN_POINT = 27
+FP64_PEAK_TINSTR = 64 * 148 * 1.965e9 / 1e12   # 18.6 T DFMA-class instr/s
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -506,8 +508,20 @@ def run_ours(args):
                      "frac": fit_bytes / (fit_dev_ms / 1e3) / 1e9 / hbm_peak,
                      "traffic": ncu_traffic("fit_grid", {k: n_sig[k] * n_pts[k] for k in (AFFINE, ATTN)}),
                      "alg_bytes_per_point": BYTES_PER_GRID_POINT,
-                     "note": "y crosses HBM once (8 B/point); the attention kind is FP64-bound "
-                             "(~32 FP64 instr/point); see DESIGN.md"},
+                     "note": "y crosses HBM once (8 B/point); the attention kind is FP64-bound, "
+                             "see fp64_attention and DESIGN.md"},
+        # attention kind against the FP64 pipe: 27 FP64 instructions per point and
+        # signature (pass 1: 3 mul + 4 add + 6 fma; pass 2: 9-fma Horner, clamp,
+        # subtract, 1-Newton reciprocal, fma), 64 per clock per SM nominal
+        "fp64_attention": {
+            "bound": "fp64", "instr_per_point": FP64_PER_ATTN_POINT,
+            "achieved": n_sig[ATTN] * n_pts[ATTN] * FP64_PER_ATTN_POINT
+            / (fit_ms[ATTN] / fit_steps / 1e3) / 1e12,
+            "peak": FP64_PEAK_TINSTR, "unit": "T FP64 instr/s",
+            "frac": n_sig[ATTN] * n_pts[ATTN] * FP64_PER_ATTN_POINT
+            / (fit_ms[ATTN] / fit_steps / 1e3) / 1e12 / FP64_PEAK_TINSTR,
+            "peak_source": "nominal 64 DFMA/clk/SM x 148 SMs x 1965 MHz (tools/fp64_probe.py "
+                           "measures DFMA at 34 TFLOP/s = 17 T instr/s)"},
         "all_fitted": status_ok,
     }
     # the general per-signature (CSR) kernel on the same points, x materialised per signature
