@@ -122,8 +122,12 @@ struct SlotArrays {  // per-warp views into dynamic shared memory
   uint32_t* left;    // prefill tokens still to schedule
   uint32_t* dec;     // output tokens produced
   uint32_t* kv;      // tokens in the KV cache before this iteration
+  uint32_t* out;     // output length (copied at admission: no HBM read per iteration)
+  uint32_t* ptot;    // prompt + output tokens (its KV reservation / kv_bytes_per_token)
   double* t_first;   // first-token time
+  double* arr;       // arrival time
 };
+constexpr int kSlotBytes = 40;  // 2 x f64 + 6 x u32 per running slot
 
 size_t sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards) {
   (void)cfg;
@@ -153,12 +157,15 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
   const int MB = cfg.max_batch;
   SlotArrays sl;
   {
-    unsigned char* p = dyn + (size_t)wid * MB * 24;
+    unsigned char* p = dyn + (size_t)wid * MB * kSlotBytes;
     sl.t_first = reinterpret_cast<double*>(p);
-    sl.rq = reinterpret_cast<uint32_t*>(p + (size_t)MB * 8);
+    sl.arr = sl.t_first + MB;
+    sl.rq = reinterpret_cast<uint32_t*>(p + (size_t)MB * 16);
     sl.left = sl.rq + MB;
     sl.dec = sl.left + MB;
     sl.kv = sl.dec + MB;
+    sl.out = sl.kv + MB;
+    sl.ptot = sl.out + MB;
   }
   const uint32_t W = cfg.window > 0 ? (uint32_t)cfg.window : 0u;
   const uint64_t kvb = (uint64_t)cfg.kv_bytes_per_token;
@@ -177,20 +184,41 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     int nrun = 0;
     uint64_t reserved = 0;
     int32_t status = DOOLY_OK;
-    double next_arr = n > 0 ? arr[0] : 0.0;
+    // Prefetch windows (registers, lane = offset): the arrival times from
+    // `arrive` on, and the waiting requests' (prompt, output, cached, arrival)
+    // from `wbase` on.  They are reloaded right after they are consumed and
+    // first read in the NEXT iteration, so the HBM/L2 latency overlaps an
+    // iteration's work instead of sitting on the critical path.
+    auto ld_arr = [&](int64_t i0) { return i0 + lane < n ? arr[i0 + lane] : 0.0; };
+    double win_arr = ld_arr(0);
+    int64_t wbase = 0;
+    uint32_t w_p = 0, w_o = 0, w_c = 0;
+    double w_a = 0.0;
+    auto ld_wait = [&](int64_t i0) {
+      wbase = i0;
+      const int64_t i = i0 + lane;
+      if (i < n) {
+        w_p = pr[i];
+        w_o = ou[i];
+        w_c = ca[i];
+        w_a = arr[i];
+      }
+    };
+    ld_wait(0);
 
     while (true) {
       // ---- 1. arrivals with arrival <= clock (sorted: a ballot prefix)
+      double next_arr = __shfl_sync(0xFFFFFFFFu, win_arr, 0);
       if (arrive < n && next_arr <= clock) {
         while (true) {
-          const int64_t idx = arrive + lane;
-          const bool in = idx < n && arr[idx] <= clock;
+          const bool in = arrive + lane < n && win_arr <= clock;
           const uint32_t b = __ballot_sync(0xFFFFFFFFu, in);
           const int cnt = __popc(b);  // prefix because arrivals are sorted
           arrive += cnt;
+          win_arr = ld_arr(arrive);
           if (cnt < 32) break;
         }
-        next_arr = arrive < n ? arr[arrive] : 0.0;
+        next_arr = arrive < n ? __shfl_sync(0xFFFFFFFFu, win_arr, 0) : 0.0;
       }
       if (nrun == 0 && admit == arrive) {
         if (arrive == n) break;
@@ -216,20 +244,15 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       uint32_t adm_pf = 0, adm_tok = 0, adm_kv = 0, adm_kvw = 0;
       int n_adm = 0;
       while (admit < arrive && nrun < MB && budget > 0) {
-        const int64_t idx = admit + lane;
-        uint32_t p_l = 0, o_l = 0, c_l = 0;
-        if (idx < arrive) {
-          p_l = pr[idx];
-          o_l = ou[idx];
-          c_l = ca[idx];
-        }
+        if (wbase != admit) ld_wait(admit);  // only after 32 admissions in one iteration
         int took = 0;  // admitted in this round (uniform after broadcast)
         bool blocked = false;
         for (int k = 0; k < 32; ++k) {
           if (admit + k >= arrive || nrun + took >= MB || budget <= 0) break;
-          const uint32_t p = __shfl_sync(0xFFFFFFFFu, p_l, k);
-          const uint32_t o = __shfl_sync(0xFFFFFFFFu, o_l, k);
-          const uint32_t c = __shfl_sync(0xFFFFFFFFu, c_l, k);
+          const uint32_t p = __shfl_sync(0xFFFFFFFFu, w_p, k);
+          const uint32_t o = __shfl_sync(0xFFFFFFFFu, w_o, k);
+          const uint32_t c = __shfl_sync(0xFFFFFFFFu, w_c, k);
+          const double a = __shfl_sync(0xFFFFFFFFu, w_a, k);
           const uint64_t need = (uint64_t)(p + o) * kvb;
           if (reserved + need > cap) {
             blocked = true;
@@ -245,7 +268,10 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
             sl.left[j] = work;   // updated after the iteration
             sl.dec[j] = take;    // scratch: tokens scheduled this iteration
             sl.kv[j] = c;
+            sl.out[j] = o;
+            sl.ptot[j] = p + o;
             sl.t_first[j] = 0.0;
+            sl.arr[j] = a;
           }
           adm_tok += take;
           if (work > 0) adm_pf += take;
@@ -262,6 +288,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
         status = DOOLY_ERR_INVALID_ARG;
         break;
       }
+      if (wbase != admit) ld_wait(admit);  // prefetch the next waiting requests
       __syncwarp();
       // ---- 3. iteration features
       uint32_t kvs = 0, kvw = 0;
@@ -315,7 +342,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       for (int j = lane; j < nrun; j += 32) {
         bool fin = false;
         const uint32_t r = sl.rq[j];
-        const uint32_t out_n = ou[r];
+        const uint32_t out_n = sl.out[j];
         if (j < n_dec) {  // decode: one token
           sl.kv[j] += 1;
           const uint32_t d = sl.dec[j] + 1;
@@ -333,14 +360,14 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
               if (l == take) {  // last chunk: emits the first output token
                 sl.dec[j] = 1;
                 sl.t_first[j] = clock;
-                ttft[base + r] = clock - arr[r];
+                ttft[base + r] = clock - sl.arr[j];
                 fin = out_n <= 1;
               }
             } else {  // fully cached request admitted this iteration: first decode step
               sl.kv[j] += 1;
               sl.dec[j] = 1;
               sl.t_first[j] = clock;
-              ttft[base + r] = clock - arr[r];
+              ttft[base + r] = clock - sl.arr[j];
               fin = out_n <= 1;
             }
           }
@@ -348,7 +375,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
         if (fin) {
           tpot[base + r] =
               out_n >= 2 ? __ddiv_rn(clock - sl.t_first[j], (double)(out_n - 1)) : nan64();
-          freed += (uint64_t)(pr[r] + out_n) * kvb;
+          freed += (uint64_t)sl.ptot[j] * kvb;
           sl.rq[j] = 0xFFFFFFFFu;  // tombstone
           fin_any = true;
         }
@@ -363,14 +390,17 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
         for (int j0 = 0; j0 < nrun; j0 += 32) {
           const int j = j0 + lane;
           const bool valid = j < nrun;
-          uint32_t rq = 0xFFFFFFFFu, lf = 0, dc = 0, kv = 0;
-          double tf = 0.0;
+          uint32_t rq = 0xFFFFFFFFu, lf = 0, dc = 0, kv = 0, on = 0, pt = 0;
+          double tf = 0.0, ar = 0.0;
           if (valid) {
             rq = sl.rq[j];
             lf = sl.left[j];
             dc = sl.dec[j];
             kv = sl.kv[j];
+            on = sl.out[j];
+            pt = sl.ptot[j];
             tf = sl.t_first[j];
+            ar = sl.arr[j];
           }
           const bool keep = rq != 0xFFFFFFFFu;
           const uint32_t km = __ballot_sync(0xFFFFFFFFu, keep);
@@ -381,7 +411,10 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
             sl.left[dst] = lf;
             sl.dec[dst] = dc;
             sl.kv[dst] = kv;
+            sl.out[dst] = on;
+            sl.ptot[dst] = pt;
             sl.t_first[dst] = tf;
+            sl.arr[dst] = ar;
           }
           w += __popc(km);
           __syncwarp();
@@ -412,7 +445,7 @@ cudaError_t launch_sim(const dooly_oplist* ops, const dooly_sched* cfg, const vo
   (void)ws_bytes;
   (void)n_sm;
   if (n_shards == 0) return cudaSuccess;
-  const size_t smem = (size_t)SIM_WARPS * cfg->max_batch * 24;
+  const size_t smem = (size_t)SIM_WARPS * cfg->max_batch * kSlotBytes;
   cudaError_t e = cudaFuncSetAttribute(sim_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
