@@ -199,26 +199,46 @@ def load_peaks():
 
 
 def link_ceiling(pinned, dev, h2d: int, d2h: int, step_s: float) -> dict:
-    """Measured pinned-copy bandwidth of this GPU's host link (one copy engine per
-    direction, full duplex) and the e2e step time it allows for these bytes."""
+    """Measured pinned-copy bandwidth of this GPU's host link, each direction alone
+    and both at once (full duplex shares the link: ~50 GB/s each way on the
+    gpurun B200s, tools/link_probe.py), and the e2e step time those allow: the
+    smaller direction's bytes move at the duplex rate alongside the same amount
+    of the larger direction, the rest of the larger at its solo rate."""
     import torch
 
     buf = pinned.view(torch.uint8)
-    d = torch.empty_like(buf, device=dev)
-    bw = {}
-    for name, fn in (("h2d", lambda: d.copy_(buf, non_blocking=True)),
-                     ("d2h", lambda: buf.copy_(d, non_blocking=True))):
-        fn()
+    n = buf.numel() // 2
+    a, b = buf[:n], buf[n:2 * n]
+    da = torch.empty_like(a, device=dev)
+    db = torch.empty_like(b, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def up():
+        with torch.cuda.stream(s1):
+            da.copy_(a, non_blocking=True)
+
+    def down():
+        with torch.cuda.stream(s2):
+            b.copy_(db, non_blocking=True)
+
+    def timed(fns, reps=3):
+        for f in fns:
+            f()
         torch.cuda.synchronize()
         t = time.perf_counter()
-        for _ in range(3):
-            fn()
+        for _ in range(reps):
+            for f in fns:
+                f()
         torch.cuda.synchronize()
-        bw[name] = 3 * buf.numel() / (time.perf_counter() - t)
-    del d
-    ideal = max(h2d / bw["h2d"], d2h / bw["d2h"])
-    return {"h2d_gb_s": bw["h2d"] / 1e9, "d2h_gb_s": bw["d2h"] / 1e9, "ideal_step_s": ideal,
-            "frac": ideal / step_s}
+        return (time.perf_counter() - t) / reps
+
+    bw_up, bw_down = n / timed([up]), n / timed([down])
+    bw_dup = n / timed([up, down])            # per direction, both active
+    del da, db
+    both = min(h2d, d2h)
+    ideal = both / bw_dup + (h2d - both) / bw_up + (d2h - both) / bw_down
+    return {"h2d_gb_s": bw_up / 1e9, "d2h_gb_s": bw_down / 1e9,
+            "duplex_gb_s_each_way": bw_dup / 1e9, "ideal_step_s": ideal, "frac": ideal / step_s}
 
 
 def gather_ceiling(nq: dict, k_ms: dict):
