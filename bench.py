@@ -40,6 +40,8 @@ BYTES_PER_QUERY = {AFFINE: 4 + 4 + 8 + 0.25, ATTN: 4 + 12 + 8 + 0.25}   # sig + 
 BYTES_PER_POINT = {AFFINE: 4 + 8, ATTN: 12 + 8}                          # x u32 planes + y f64
 BYTES_PER_GRID_POINT = 8                     # shared grid: y f64 per point (x counted once per kind)
 FP64_PER_ATTN_POINT = 27
+SHA_ALU_PER_BLOCK = 48 * 18 + 16 * 10          # SASS count, sha256_compress
+ALU_PEAK_TINSTR = 64 * 148 * 1.965e9 / 1e12       # ALU pipe lanes/clk/SM x SMs x clock
 FP64_PEAK_TINSTR = 64 * 148 * 1.965e9 / 1e12   # 18.6 T DFMA-class instr/s
 FALLBACK_HBM_GBS = 6650.0
 
@@ -715,7 +717,18 @@ def run_ours(args):
                      if pdig is not None else "NCCL all-gather of 32-B digests, global resolve"),
                  "sha_ms": sha_ms / d_steps,
                  "sha_blocks_per_s": recs.n * 2 / (sha_ms / d_steps / 1e3),
-                 "bound": "int32 ALU (SHA-256 rounds)"}
+                 "bound": "int32 ALU (SHA-256 rounds)",
+                 # rotates (SHF) and Ch/Maj/xor (LOP3) are ALU-pipe only: 18 per
+                 # scheduled round, 10 per round of the first 16 (the additions run
+                 # on the FMA pipe as IMAD); ALU pipe = 64 lanes/clk/SM
+                 "alu_roofline": {
+                     "instr_per_block": SHA_ALU_PER_BLOCK,
+                     "achieved": recs.n * 2 * SHA_ALU_PER_BLOCK / (sha_ms / d_steps / 1e3) / 1e12,
+                     "peak": ALU_PEAK_TINSTR, "unit": "T ALU instr/s",
+                     "frac": recs.n * 2 * SHA_ALU_PER_BLOCK / (sha_ms / d_steps / 1e3) / 1e12
+                     / ALU_PEAK_TINSTR,
+                     "note": "compression rounds only; canonical-message construction and "
+                             "lock-step padding of shorter messages are the remainder"}}
 
     # ---------------- sim sub-benchmark (C4)
     sim = None

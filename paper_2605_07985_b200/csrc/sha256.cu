@@ -27,6 +27,11 @@ __constant__ uint32_t kSha256K[64] = {
     0xc67178f2};
 
 __device__ __forceinline__ uint32_t rotr(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+__device__ __forceinline__ uint32_t fadd(uint32_t a, uint32_t b, uint32_t one) {
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(one), "r"(b));
+  return r;
+}
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 // One 64-byte block; w points at 16 big-endian words in shared memory.
@@ -37,15 +42,22 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 
 #define SHA_S1(x) (rotr(x, 6) ^ rotr(x, 11) ^ rotr(x, 25))
 #define SHA_s0(x) (rotr(x, 7) ^ rotr(x, 18) ^ ((x) >> 3))
 #define SHA_s1(x) (rotr(x, 17) ^ rotr(x, 19) ^ ((x) >> 10))
-#define SHA_RND(a, b, c, d, e, f, g, h, i)                                          \
-  {                                                                                 \
-    const uint32_t t1 = h + SHA_S1(e) + ((e & f) ^ (~e & g)) + kSha256K[r + i] + w[i]; \
-    const uint32_t t2 = SHA_S0(a) + ((a & b) ^ (a & c) ^ (b & c));                   \
-    d += t1;                                                                        \
-    h = t1 + t2;                                                                    \
+// Pipe balance: the rotates (SHF) and Ch/Maj/xor (LOP3) can only run on the
+// ALU pipe, which is what bounds SHA-256 (18 ALU instructions per round).  The
+// 10 additions per round go to the FMA pipe instead, as IMAD a * one + b with
+// `one` a kernel argument ptxas cannot fold back into IADD3.
+#define SHA_ADD(x, y) fadd((x), (y), one)
+#define SHA_RND(a, b, c, d, e, f, g, h, i)                                                   \
+  {                                                                                          \
+    const uint32_t t1 = SHA_ADD(SHA_ADD(SHA_ADD(h, SHA_S1(e)), (e & f) ^ (~e & g)),           \
+                                SHA_ADD(kSha256K[r + i], w[i]));                             \
+    const uint32_t t2 = SHA_ADD(SHA_S0(a), (a & b) ^ (a & c) ^ (b & c));                     \
+    d = SHA_ADD(d, t1);                                                                      \
+    h = SHA_ADD(t1, t2);                                                                     \
   }
-#define SHA_SCHED(i) \
-  w[i] += SHA_s0(w[((i) + 1) & 15]) + w[((i) + 9) & 15] + SHA_s1(w[((i) + 14) & 15])
+#define SHA_SCHED(i)                                                                           \
+  w[i] = SHA_ADD(SHA_ADD(SHA_ADD(w[i], SHA_s0(w[((i) + 1) & 15])), w[((i) + 9) & 15]),         \
+                 SHA_s1(w[((i) + 14) & 15]))
 #define SHA_16(sched)                                                              \
   sched(0); SHA_RND(a, b, c, d, e, f, g, k, 0);                                    \
   sched(1); SHA_RND(k, a, b, c, d, e, f, g, 1);                                    \
@@ -65,7 +77,8 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 
   sched(15); SHA_RND(b, c, d, e, f, g, k, a, 15);
 #define SHA_NOSCHED(i) (void)0
 
-__device__ __forceinline__ void sha256_compress(uint32_t hs[8], const uint32_t* w_in) {
+__device__ __forceinline__ void sha256_compress(uint32_t hs[8], const uint32_t* w_in,
+                                                uint32_t one) {
   uint32_t w[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) w[i] = w_in[i];
@@ -89,7 +102,7 @@ __device__ __forceinline__ void sha256_compress(uint32_t hs[8], const uint32_t* 
 
 // Out-of-line copy for the rare long-message drain inside the byte writer.
 __device__ __noinline__ void sha256_compress_blocks(uint32_t hs[8], const uint32_t* w, int nb) {
-  for (int b = 0; b < nb; ++b) sha256_compress(hs, w + 16 * b);
+  for (int b = 0; b < nb; ++b) sha256_compress(hs, w + 16 * b, 1u);
 }
 
 constexpr int SHA_THREADS = 128;
@@ -156,7 +169,7 @@ struct ShaStream {
   // FIPS 180-4 padding, then lock-step compression of the buffered blocks.
   // Must be called by all 32 lanes (valid == false lanes only take part in the
   // lock-step loop bound).
-  __device__ void finish(uint8_t* out, bool valid) {
+  __device__ void finish(uint8_t* out, bool valid, uint32_t one) {
     int nb = 0;
     if (valid) {
       const uint64_t bits = total * 8;
@@ -170,7 +183,7 @@ struct ShaStream {
     __syncwarp();
     const int nb_max = (int)__reduce_max_sync(0xFFFFFFFFu, (unsigned)nb);
     for (int b = 0; b < nb_max; ++b)
-      if (b < nb) sha256_compress(h, buf + 16 * b);
+      if (b < nb) sha256_compress(h, buf + 16 * b, one);
     if (!valid) return;
     uint4* o4 = reinterpret_cast<uint4*>(out);
     o4[0] = make_uint4(bswap32(h[0]), bswap32(h[1]), bswap32(h[2]), bswap32(h[3]));
@@ -194,7 +207,7 @@ __global__ void __launch_bounds__(SHA_THREADS) sha256_records_kernel(
     const uint8_t* __restrict__ op_bytes, const int64_t* __restrict__ op_off,
     const uint8_t* __restrict__ sym_bytes, const int64_t* __restrict__ sym_off,
     const uint8_t* __restrict__ attr_digests, uint8_t* __restrict__ out,
-    const dooly_digest_peers pe) {
+    const dooly_digest_peers pe, uint32_t one) {
   __shared__ uint32_t s_buf[SHA_THREADS * SHA_STRIDE];
   ShaStream st;
   for (int64_t base = (int64_t)blockIdx.x * SHA_THREADS; base < n;
@@ -225,14 +238,14 @@ __global__ void __launch_bounds__(SHA_THREADS) sha256_records_kernel(
       for (int k = 0; k < 8; ++k) st.put_be32(bswap32(d[k]));
     }
     }
-    st.finish(out + (pe.row0 + i) * 32, valid);
+    st.finish(out + (pe.row0 + i) * 32, valid, one);
     if (valid && pe.n_peers > 0) st.broadcast(pe, pe.row0 + i);
   }
 }
 
 __global__ void __launch_bounds__(SHA_THREADS) sha256_messages_kernel(
     const uint8_t* __restrict__ msgs, const int64_t* __restrict__ off, int64_t n,
-    uint8_t* __restrict__ out) {
+    uint8_t* __restrict__ out, uint32_t one) {
   __shared__ uint32_t s_buf[SHA_THREADS * SHA_STRIDE];
   ShaStream st;
   for (int64_t base = (int64_t)blockIdx.x * SHA_THREADS; base < n;
@@ -241,7 +254,7 @@ __global__ void __launch_bounds__(SHA_THREADS) sha256_messages_kernel(
     const bool valid = i < n;
     st.init(s_buf + threadIdx.x * SHA_STRIDE);
     if (valid) st.put_bytes(msgs + off[i], off[i + 1] - off[i]);
-    st.finish(out + i * 32, valid);
+    st.finish(out + i * 32, valid, one);
   }
 }
 
@@ -261,7 +274,7 @@ cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off,
   dooly_digest_peers pe{};
   if (peers) pe = *peers;
   sha256_records_kernel<<<(unsigned)sha_blocks(n, n_sm), SHA_THREADS, 0, stream>>>(
-      words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off, attr_digests, out, pe);
+      words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off, attr_digests, out, pe, 1u);
   return cudaGetLastError();
 }
 
@@ -269,7 +282,7 @@ cudaError_t launch_sha256_messages(const uint8_t* msgs, const int64_t* off, int6
                                    uint8_t* out, cudaStream_t stream, int n_sm) {
   if (n == 0) return cudaSuccess;
   sha256_messages_kernel<<<(unsigned)sha_blocks(n, n_sm), SHA_THREADS, 0, stream>>>(msgs, off, n,
-                                                                                     out);
+                                                                                     out, 1u);
   return cudaGetLastError();
 }
 
