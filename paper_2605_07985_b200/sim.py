@@ -56,10 +56,16 @@ class FitResult:
 _FIT_WS: dict = {}
 
 
+def _ws_key(device, tag) -> tuple:
+    """Scratch is cached per (device, stream, use): fits enqueued on different
+    streams may run concurrently and must not share a workspace."""
+    return (str(device), torch.cuda.current_stream(device).cuda_stream, tag)
+
+
 def _fit_workspace(kind: int, n_sig: int, device) -> torch.Tensor:
     """Cached device scratch for the attention fit's moment buffers."""
     need = int(_lib.load_library().dooly_fit_workspace_size(kind, n_sig))
-    key = (str(device), kind)
+    key = _ws_key(device, kind)
     buf = _FIT_WS.get(key)
     if buf is None or buf.numel() < need:
         buf = torch.empty(max(need, 256), dtype=torch.uint8, device=device)
@@ -208,7 +214,7 @@ def fit_grid(kind: int, x: torch.Tensor, y: torch.Tensor,
 
 def _grid_workspace(dev: torch.device, kind: int, n_pts: int) -> torch.Tensor:
     need = int(_lib.load_library().dooly_fit_grid_workspace_size(kind, n_pts))
-    key = (str(dev), "grid")
+    key = _ws_key(dev, "grid")
     ws = _FIT_WS.get(key)
     if ws is None or ws.numel() < need:
         ws = torch.empty(max(need, 256), dtype=torch.uint8, device=dev)
