@@ -258,9 +258,23 @@ def gather_ceiling(nq: dict, k_ms: dict):
     if 32 not in rate or 96 not in rate:
         return None
     ideal_ms = (nq[AFFINE] / rate[32] + nq[ATTN] / rate[96]) * 1e3
-    return {"rows_per_s": {"affine_32B": rate[32], "attention_96B": rate[96]},
-            "ideal_ms": ideal_ms, "frac": ideal_ms / (k_ms[AFFINE] + k_ms[ATTN]),
-            "source": "profiles/r1_gather_probe.jsonl (bare LDG.256 row gathers, 500k rows)"}
+    out = {"rows_per_s": {"affine_32B": rate[32], "attention_96B": rate[96]},
+           "ideal_ms": ideal_ms, "frac": ideal_ms / (k_ms[AFFINE] + k_ms[ATTN]),
+           "source": "profiles/r1_gather_probe.jsonl (bare LDG.256 row gathers, 500k rows)"}
+    # the predict kernel's own access pattern (streams + gathers + stores) with
+    # the evaluation replaced by a sum: the memory-system ceiling it runs against
+    mem = {}
+    for ln in p.read_text().splitlines():
+        r = json.loads(ln)
+        if r.get("probe") == "predict_mem" and r.get("rows") == 500_000:
+            mem[r["row_bytes"]] = max(mem.get(r["row_bytes"], 0.0), r["g_q_per_s"] * 1e9)
+    if 32 in mem and 96 in mem:
+        mem_ms = (nq[AFFINE] / mem[32] + nq[ATTN] / mem[96]) * 1e3
+        out["access_pattern_ceiling"] = {
+            "queries_per_s": {"affine": mem[32], "attention_96B": mem[96]},
+            "ideal_ms": mem_ms, "frac": mem_ms / (k_ms[AFFINE] + k_ms[ATTN]),
+            "source": "profiles/r1_gather_probe.jsonl predict_mem (tools/gather_probe.py predmem)"}
+    return out
 
 
 def ncu_traffic(kernel_key: str, units: dict):

@@ -5,6 +5,11 @@
 //   gather:     each lane hashes (query index) -> row, loads the row with
 //               LDG.256 (L2::evict_last, L1::no_allocate) exactly like
 //               predict_vec_kernel, and folds it into a checksum
+//   predict_mem: predict_vec_kernel's whole access pattern — 256-query tiles,
+//               8 queries per lane, sig and feature planes streamed with
+//               LDG.256 evict_first, SECTORS x LDG.256 row gathers per query,
+//               two STG.256 of results — with the evaluation replaced by a sum:
+//               the memory-system ceiling of the predict kernel itself
 //
 // Built by tools/gather_probe.py (nvcc -shared); not part of libdooly_b200.
 #include <cuda.h>
@@ -53,6 +58,69 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
     for (int j = 0; j < 8; ++j) acc += v[j];
   }
   if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+struct U8v {
+  uint32_t v[8];
+};
+__device__ __forceinline__ U8v ld_stream(const uint32_t* p) {
+  U8v r;
+  asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+        "=r"(r.v[6]), "=r"(r.v[7])
+      : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p),
+               "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+
+template <int SECTORS, int P>
+__global__ void __launch_bounds__(256) predict_mem_kernel(const uint8_t* __restrict__ table,
+                                                          const uint32_t* __restrict__ sig,
+                                                          const uint32_t* __restrict__ x,
+                                                          int64_t n_q, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_tiles = n_q >> 8;
+  for (int64_t tile = warp; tile < n_tiles; tile += n_warps) {
+    const int64_t q = (tile << 8) + lane * 8;
+    const U8v sv = ld_stream(sig + q);
+    U8v xv[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) xv[p] = ld_stream(x + p * n_q + q);
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint8_t* row = table + (uint64_t)sv.v[j] * (32 * SECTORS);
+      double s = (double)xv[P - 1].v[j];
+#pragma unroll
+      for (int k = 0; k < SECTORS; ++k) {
+        double a, b, c, d;
+        ld256(row + 32 * k, a, b, c, d);
+        s += a + b + c + d;
+      }
+      r[j] = s;
+    }
+    st_stream(out + q, r[0], r[1], r[2], r[3]);
+    st_stream(out + q + 4, r[4], r[5], r[6], r[7]);
+  }
+}
+
+extern "C" int probe_predict_mem(const void* table, const uint32_t* sig, const uint32_t* x,
+                                 int sectors, int64_t n_q, double* out, int blocks, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  auto t = static_cast<const uint8_t*>(table);
+  if (sectors == 1)
+    predict_mem_kernel<1, 1><<<blocks, 256, 0, s>>>(t, sig, x, n_q, out);
+  else if (sectors == 3)
+    predict_mem_kernel<3, 3><<<blocks, 256, 0, s>>>(t, sig, x, n_q, out);
+  else
+    return 1;
+  return (int)cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(256) l2_stream_kernel(const double4* __restrict__ buf,

@@ -60,6 +60,9 @@ def main() -> None:
     if "gather4" in only:
         gather4(lib, dev, n_sm, sink, st, timed)
         return
+    if "predmem" in only:
+        predict_mem(lib, dev, n_sm, timed)
+        return
     for mb in (16, 48):
         buf = torch.rand((mb << 20) // 8, dtype=torch.float64, device=dev)
         reps = 20
@@ -99,6 +102,29 @@ def main() -> None:
                                   "g_rows_per_s": n_q / ms / 1e6,
                                   "gb_per_s": n_q * rb / ms / 1e6}), flush=True)
         del table
+
+
+def predict_mem(lib, dev, n_sm, timed):
+    """predict_vec_kernel's access pattern with the evaluation removed, on the C5
+    bench shapes (0.5M rows, uniform random signatures), next to the product
+    kernel timed by tools/predict_sweep.py on the same sizes."""
+    lib.probe_predict_mem.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int64,
+                                      C.c_void_p, C.c_int, C.c_void_p]
+    st = torch.cuda.current_stream().cuda_stream
+    n_q, rows = 200_000_000, 500_000
+    for sectors, planes, occ in ((1, 1, 3), (3, 3, 2)):
+        table = torch.rand((rows * sectors * 32) // 8, dtype=torch.float64, device=dev)
+        sig = torch.randint(0, rows, (n_q,), dtype=torch.int32, device=dev)
+        x = torch.randint(0, 1 << 15, (planes, n_q), dtype=torch.int32, device=dev)
+        out = torch.empty(n_q, dtype=torch.float64, device=dev)
+        for per_sm in (occ, occ + 1, occ * 2):
+            ms = timed(lambda: lib.probe_predict_mem(table.data_ptr(), sig.data_ptr(), x.data_ptr(),
+                                                     sectors, n_q, out.data_ptr(), n_sm * per_sm,
+                                                     st))
+            print(json.dumps({"probe": "predict_mem", "row_bytes": 32 * sectors, "planes": planes,
+                              "rows": rows, "ctas_per_sm": per_sm, "ms": ms,
+                              "g_q_per_s": n_q / ms / 1e6}), flush=True)
+        del table, sig, x, out
 
 
 def gather4(lib, dev, n_sm, sink, st, timed):
