@@ -218,11 +218,10 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
           win_arr = ld_arr(arrive);
           if (cnt < 32) break;
         }
-        next_arr = arrive < n ? __shfl_sync(0xFFFFFFFFu, win_arr, 0) : 0.0;
       }
       if (nrun == 0 && admit == arrive) {
         if (arrive == n) break;
-        clock = next_arr;  // idle: jump to the next arrival (exact copy)
+        clock = __shfl_sync(0xFFFFFFFFu, win_arr, 0);  // idle: jump to the next arrival (exact copy)
         continue;
       }
       if (it >= cfg.max_iterations) {  // work remains but the cap is reached
