@@ -1,0 +1,198 @@
+"""C5 at BASELINE.json's full sizes (configs[4]: 1M signatures x 4096 sweep
+points, 1e9 queries; 4M dedup records; C4 1M-request trace), checked through
+oracle parity on random samples plus size-independent properties:
+
+* fit: 0.5M affine + 0.5M attention signatures on the shared sweep grid, every
+  signature fitted; 256 sampled signatures re-fitted by the CPU oracle agree
+  within the 1e-9 coefficient contract; the warp kernel and the staged kernel
+  agree on every signature (two independent code paths over the full batch);
+* predict: 5e8 affine + 5e8 attention queries; a 200k-query random sample is
+  bit-identical to the oracle (latency bits, extrapolation and clamp flags);
+  re-running the batch reproduces every output bit (determinism); the
+  checksum of the device output equals the sum of its chunks' checksums;
+* dedup: 4M records, digests of a 2k sample equal hashlib over the oracle's
+  canonical bytes; first-occurrence indices are minimal per digest and the
+  unique count equals torch.unique's;
+* sim: the C4 1M-request trace over 1184 replicas terminates on every shard,
+  and two sampled shards match the oracle's event loop bit for bit.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import ROOT  # noqa: F401
+from helpers import AFFINE, ATTN, rows_to_table
+
+pytestmark = pytest.mark.gpu
+
+N_SIG = 500_000      # per kind
+N_PTS = 4096
+N_Q = 500_000_000    # per kind
+
+
+@pytest.fixture(scope="module")
+def c5(dev):
+    import bench
+    from paper_2605_07985_b200.sim import fit_grid
+
+    out = {}
+    for kind in (AFFINE, ATTN):
+        x, y = bench.gen_grid_fit_data(kind, N_SIG, N_PTS, dev, seed=kind)
+        out[kind] = (x, y, fit_grid(kind, x, y))
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+def test_c5_fit_full_size(kind, c5, dev, monkeypatch):
+    from oracle import sim as osim
+    from paper_2605_07985_b200.sim import fit_grid
+
+    x, y, fr = c5[kind]
+    assert int((fr.status != 0).sum().item()) == 0
+    # oracle parity on a random sample of signatures
+    rng = np.random.default_rng(100 + kind)
+    pick = np.sort(rng.choice(N_SIG, 256, replace=False))
+    xs = x.cpu().numpy().view(np.uint32)
+    ys = y[torch.from_numpy(pick).to(dev)].cpu().numpy()
+    ref = osim.fit(kind, np.tile(xs, (1, len(pick))), ys.reshape(-1),
+                   np.arange(len(pick) + 1, dtype=np.int64) * N_PTS)
+    got = rows_to_table(kind, fr.rows()[pick])
+    dc = np.abs(got["coef"] - ref["coef"]).max(axis=1) / np.abs(ref["coef"]).max(axis=1)
+    assert dc.max() <= 1e-9, dc.max()
+    assert np.array_equal(got["lo"], ref["lo"]) and np.array_equal(got["hi"], ref["hi"])
+    assert np.array_equal(got["inv"], ref["inv"])
+    fe = fr.fit_err.cpu().numpy()[pick]
+    assert np.allclose(fe, ref["fit_err"], rtol=1e-6, atol=0)
+    # the staged kernel over the whole batch: an independent code path
+    monkeypatch.setenv("DOOLY_FIT_GRID_KERNEL", "stage")
+    st = fit_grid(kind, x, y)
+    nc = 2 if kind == AFFINE else 10
+    a, b = fr.table.view(torch.float64)[:, :nc], st.table.view(torch.float64)[:, :nc]
+    d = ((a - b).abs().amax(1) / b.abs().amax(1)).max().item()
+    assert d <= 1e-11, d
+    assert torch.equal(fr.table.view(torch.float64)[:, nc:], st.table.view(torch.float64)[:, nc:])
+
+
+@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+def test_c5_predict_full_size(kind, c5, dev):
+    import bench
+    from oracle import sim as osim
+    from paper_2605_07985_b200._lib import KIND_ATTN_PACKED
+    from paper_2605_07985_b200.sim import pack_attn, predict_batch
+
+    _, _, fr = c5[kind]
+    table = fr.table if kind == AFFINE else pack_attn(fr.table)
+    pk = AFFINE if kind == AFFINE else KIND_ATTN_PACKED
+    sig, x = bench.gen_queries(kind, fr.table, N_Q, dev, seed=7 + kind)
+    out, flags, err = predict_batch(pk, table, sig, x)
+    torch.cuda.synchronize()
+    assert int(err.item()) == np.iinfo(np.int64).max          # no unknown signature
+    # determinism over the full batch
+    out2, flags2, _ = predict_batch(pk, table, sig, x)
+    assert torch.equal(out.view(torch.int64), out2.view(torch.int64))
+    assert torch.equal(flags, flags2)
+    # checksum of checksums: the whole-batch sum equals the sum of chunk sums
+    tot = out.sum().item()
+    parts = sum(out[i:i + (1 << 26)].sum().item() for i in range(0, N_Q, 1 << 26))
+    assert abs(tot - parts) <= 1e-9 * abs(tot)
+    # bit-exact oracle parity on a random sample
+    rng = np.random.default_rng(200 + kind)
+    qi = torch.from_numpy(np.sort(rng.choice(N_Q, 200_000, replace=False))).to(dev)
+    tab = rows_to_table(kind, fr.rows())
+    s_np = sig[qi].cpu().numpy().view(np.uint32)
+    x_np = x[:, qi].cpu().numpy().view(np.uint32)
+    ref = osim.predict(kind, tab, s_np, x_np)
+    got = out[qi].cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), ref["out"].view(np.uint64))
+    bits = np.unpackbits(flags.cpu().numpy().view(np.uint8).reshape(2, -1), axis=1,
+                         bitorder="little")[:, :N_Q]
+    qn = qi.cpu().numpy()
+    assert np.array_equal(bits[0, qn].astype(bool), ref["extrap"])
+    assert np.array_equal(bits[1, qn].astype(bool), ref["clamped"])
+
+
+def test_c5_dedup_full_size(dev):
+    import bench
+    from oracle import profiler as oprof
+    from paper_2605_07985_b200.profiler import DeviceRecords, dedup_packed
+    from test_host import _canonical_from_words as canonical_from_packed
+
+    n = 4_000_000
+    packed, _ = bench.synth_records(n, seed=11)
+    res = dedup_packed(DeviceRecords.from_packed(packed, dev))
+    dig = res.digests
+    # unique count and first-occurrence minimality against torch on the device
+    words = dig.view(torch.int64).reshape(n, 4)
+    uniq, inv = torch.unique(words, dim=0, return_inverse=True)
+    assert res.n_unique == uniq.shape[0]
+    first_min = torch.full((uniq.shape[0],), n, dtype=torch.int64, device=dev)
+    first_min.scatter_reduce_(0, inv, torch.arange(n, device=dev), reduce="amin")
+    assert torch.equal(res.first, first_min[inv])
+    # SHA-256 over the canonical bytes of a sample (hashlib is the reference)
+    rng = np.random.default_rng(3)
+    for i in rng.choice(n, 2000, replace=False):
+        msg = canonical_from_packed(packed, int(i))
+        assert bytes(dig[int(i)].cpu().numpy()) == hashlib.sha256(msg).digest()
+        assert oprof.signature_hash(msg) == hashlib.sha256(msg).digest()
+
+
+def test_c4_sim_full_size(dev):
+    """1M-request Poisson trace over 1184 replicas (bench.py's C4 leg): every shard
+    terminates, and two sampled shards equal the oracle event loop bit for bit."""
+    import math
+
+    from paper_2605_07985_b200 import modelir
+    from paper_2605_07985_b200.profiler import profile_corpus
+    from paper_2605_07985_b200.sim import (SchedConfig, ShardedTrace, build_calltree, collect,
+                                           fit, make_sched, run_sharded)
+
+    man = modelir.load_manifest(modelir.builtin_manifest_path("llama70b"))
+    model, backend, hw, tp = man.models[0], man.backends[1], man.hardware, man.tp_degree
+    db, _ = profile_corpus(modelir.CorpusManifest((model,), (backend,), hw, tp, man.grid),
+                           device=dev)
+    regs = fit(db, dev)
+    ct = build_calltree(model, backend, regs, hw, tp)
+    cfg = make_sched(model, hw, tp, SchedConfig(chunk=8192, max_batch=256), ct)
+    n, S = 1_000_000, 1184
+    rng = np.random.default_rng(1)
+    arr = np.cumsum(rng.exponential(1.0 / (4.0 * S), size=n))
+    sp = math.sqrt(2 * math.log(1232 / 950))
+    so = math.sqrt(2 * math.log(397 / 388))
+    pr = np.clip(np.rint(rng.lognormal(math.log(950), sp, n)), 1, 8192 - 512).astype(np.uint32)
+    ou = np.clip(np.rint(rng.lognormal(math.log(388), so, n)), 1, 512).astype(np.uint32)
+    ca = np.zeros(n, np.uint32)
+    trace = ShardedTrace.from_arrays(arr, pr, ou, ca, S, dev)
+    res = run_sharded(trace, ct, cfg, regs)
+    met = collect(trace, res)
+    assert int((res.status != 0).sum().item()) == 0
+    assert np.all(np.isfinite(met.ttft)) and np.all(met.ttft >= 0)
+    # oracle ops built from the same regressor rows the kernel reads
+    tabs = {k: rows_to_table(k, regs.tables[k].rows()) for k in regs.tables}
+    from oracle import sim as osim
+
+    ops = []
+    for i in range(ct.n_ops):
+        feat, row = ct.oplist.feat[i], ct.oplist.row[i]
+        op = {"feat": feat, "repeat": ct.oplist.repeat[i], "window_slot": ct.oplist.window_slot[i],
+              "bytes_per_tok": ct.oplist.bytes_per_tok[i]}
+        if feat != osim.FEAT_COMM:
+            t = tabs[ATTN if feat == osim.FEAT_ATTN else AFFINE]
+            op.update(coef=list(t["coef"][row]), inv=list(t["inv"][row]))
+        ops.append(op)
+    n_iter = res.n_iter.cpu().numpy()
+    for s in (0, 777):
+        idx = np.arange(s, n, S)
+        r = osim.run_shard(arr[idx].tolist(), pr[idx].tolist(), ou[idx].tolist(), ca[idx].tolist(),
+                           ops, 8192, 256, cfg.kv_bytes_per_token, cfg.kv_capacity_bytes,
+                           ct.window, tp, hw.comm_alpha, hw.comm_beta)
+        assert n_iter[s] == r["n_iter"]
+        assert np.array_equal(met.ttft[idx].view(np.uint64), np.array(r["ttft"]).view(np.uint64))
+        m = ~np.isnan(np.array(r["tpot"]))
+        assert np.array_equal(met.tpot[idx][m], np.array(r["tpot"])[m])
