@@ -3,22 +3,30 @@
 // (one sweep grid per model/backend; the C5 scale sweep).
 //
 // With a shared design matrix M (n_pts x p) the normal-equation Gram M^T M,
-// its Cholesky-with-drop factor, the scaling (inv = 1/max x) and the training
-// box are the same for every signature, so they are computed ONCE
-// (fit_grid_prep_kernel, one CTA).  Per signature only X^T y remains:
-//   pass 1  b = M^T y          (p FMAs per point)
-//   solve   L L^T c = b        (shared factor, dropped columns stay 0)
-//   pass 2  training MAPE      (p FMAs + reciprocal per point)
+// its Cholesky-with-drop factor, the solve matrix W (c = W b), the scaling
+// (inv = 1/max x), the training box and the scaled feature planes
+// f_k(p) = RN(x_k(p) * inv_k) are the same for every signature, so they are
+// computed ONCE (fit_grid_prep_kernel, one CTA, into the workspace).  Per
+// signature only X^T y remains:
+//   pass 1  b = M^T y          (13 FP64 per point for the 10-column design)
+//   solve   c = W b            (lanes 0..p-1, one coefficient each)
+//   pass 2  training MAPE      (9-FMA regrouped polynomial + 1-Newton reciprocal)
 // versus ~95 FP64 instructions per point for the per-signature Gram path
-// (fit.cu).  Register blocking: a 256-thread CTA owns R signatures at a time,
-// every thread walks a strided subset of the points and recomputes that
-// point's monomials once for all R signatures (x is 4-12 B per point, shared
-// by all CTAs through L1/L2).  y rows are read with default caching so the
-// pass-2 re-read of the R rows a CTA just streamed hits L2.
+// (fit.cu).
+//
+// Three kernels share this contract:
+//   fit_grid_warp_kernel  (default) one warp per signature, no shared-memory
+//                         stage, no CTA barrier: y streamed from HBM with
+//                         L2::evict_last, 8 steps in flight per lane, re-read
+//                         from L2 in pass 2; f planes from L1.
+//   fit_grid_stage_kernel (DOOLY_FIT_GRID_KERNEL=stage) R signatures per CTA
+//                         staged in shared memory by 1-D TMA.
+//   fit_grid_kernel       (unaligned or n_pts % 4 != 0) the same with direct
+//                         global loads.
 //
 // Result contract: identical to dooly_fit with pt_off[s] = s * n_pts and x
 // repeated per signature — coefficients within 1e-9 normwise, fit_err within
-// 1e-9 relative (tests/test_gpu_fit_grid.py), same row layout and statuses.
+// the MAPE bound (tests/test_gpu_fit_grid.py), same row layout and statuses.
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -33,10 +41,7 @@ template <int KIND>
 struct GridTraits;
 template <>
 struct GridTraits<DOOLY_KIND_AFFINE> {
-#ifndef DOOLY_AFFINE_RS
-#define DOOLY_AFFINE_RS 3
-#endif
-  static constexpr int P = 1, NC = 2, NEED = 4, R = 8, RS = DOOLY_AFFINE_RS;
+  static constexpr int P = 1, NC = 2, NEED = 4, R = 8, RS = 3;
 };
 template <>
 struct GridTraits<DOOLY_KIND_ATTN> {
