@@ -586,3 +586,27 @@ def test_library_launch_counter(dev):
     x, y, off = synth_fit_data(AFFINE, 4, 16, seed=1)
     _fit_gpu(AFFINE, x, y, off, dev)
     assert _lib.launch_count(dev) == before + 1
+
+
+def test_sim_run_max_batch_1024(dev):
+    """The largest running batch the C-ABI accepts (1024 slots x 40 B of
+    per-warp shared memory) against the oracle event loop, bit for bit."""
+    from paper_2605_07985_b200 import _lib
+    from paper_2605_07985_b200.sim import CallTree, ShardedTrace, collect, run_sharded
+
+    ta, tt, ops, ol = _sim_setup(9, window=0, tp=1)
+    regs = _regs(ta, tt, dev)
+    arr, pr, ou, ca = _workload(4000, 9, rate=400.0)
+    sc = _lib.Sched()
+    sc.chunk, sc.max_batch, sc.window = 8192, 1024, 0
+    sc.kv_bytes_per_token, sc.kv_capacity_bytes, sc.max_iterations = 131072, 10**15, 10**7
+    trace = ShardedTrace.from_arrays(arr, pr, ou, ca, 2, dev)
+    res = run_sharded(trace, CallTree([], ol, 0), sc, regs)
+    met = collect(trace, res)
+    ref = osim.run_shards(arr.tolist(), pr.tolist(), ou.tolist(), ca.tolist(), 2, ops=ops,
+                          chunk=8192, max_batch=1024, kv_bytes_per_token=131072,
+                          kv_capacity=10**15, window=0, tp=1, alpha=5e-6, beta=5e-12)
+    assert res.n_iter.cpu().numpy().tolist() == ref["n_iter"]
+    assert np.array_equal(met.ttft.view(np.uint64), ref["ttft"].view(np.uint64))
+    m = ~np.isnan(ref["tpot"])
+    assert np.array_equal(met.tpot[m], ref["tpot"][m])
