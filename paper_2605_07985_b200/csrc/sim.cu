@@ -50,7 +50,11 @@ __device__ __forceinline__ void stage_ops(const dooly_oplist& ops, const void* a
 // in Python's operator order.
 __device__ __forceinline__ double comm_latency(int tp, double alpha, double beta, uint64_t bytes) {
   const double a = __ddiv_rn((double)(2 * (tp - 1)), (double)tp);
-  const double b = mul(__ddiv_rn((double)bytes, (double)tp), beta);
+  // bytes / tp for a power-of-two tp is an exact scaling: the multiply by 2^-k
+  // is bit-identical to the IEEE division
+  const double q = (tp & (tp - 1)) == 0 ? mul((double)bytes, __drcp_rn((double)tp))
+                                        : __ddiv_rn((double)bytes, (double)tp);
+  const double b = mul(q, beta);
   return mul(a, add(alpha, b));
 }
 
@@ -309,16 +313,26 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       const uint32_t prefill = take_p + adm_pf;
       const uint32_t batch = (uint32_t)n_dec + (take_p > 0 ? 1u : 0u) + (uint32_t)n_adm;
       // ---- 4. fused gather-evaluate-reduce over the call graph
+      // lanes evaluate their entries and the repeat products in parallel; the
+      // in-order sum then only chains the adds (shuffles issued 4 at a time)
       bool bad = false;
-      double v0 = 0.0, v1 = 0.0;
-      if (lane < ops.n_ops) v0 = entry_value(ops, &s_ops, lane, num_toks, prefill, batch, kvs, kvw, bad);
+      double w0 = 0.0, w1 = 0.0;
+      if (lane < ops.n_ops)
+        w0 = mul((double)ops.repeat[lane],
+                 entry_value(ops, &s_ops, lane, num_toks, prefill, batch, kvs, kvw, bad));
       if (lane + 32 < ops.n_ops)
-        v1 = entry_value(ops, &s_ops, lane + 32, num_toks, prefill, batch, kvs, kvw, bad);
+        w1 = mul((double)ops.repeat[lane + 32],
+                 entry_value(ops, &s_ops, lane + 32, num_toks, prefill, batch, kvs, kvw, bad));
       double lat = 0.0;
-      for (int e = 0; e < ops.n_ops; ++e) {
-        const double v = __shfl_sync(0xFFFFFFFFu, e < 32 ? v0 : v1, e & 31);
-        lat = add(lat, mul((double)ops.repeat[e], v));
+      int e = 0;
+      for (; e + 4 <= ops.n_ops; e += 4) {
+        double t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = __shfl_sync(0xFFFFFFFFu, e + u < 32 ? w0 : w1, (e + u) & 31);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) lat = add(lat, t[u]);
       }
+      for (; e < ops.n_ops; ++e) lat = add(lat, __shfl_sync(0xFFFFFFFFu, e < 32 ? w0 : w1, e & 31));
       if (__any_sync(0xFFFFFFFFu, bad)) {
         status = DOOLY_ERR_UNKNOWN_SIGNATURE;
         break;
