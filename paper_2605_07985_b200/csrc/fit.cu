@@ -859,7 +859,7 @@ __device__ __forceinline__ void warp_stream_points(const uint32_t* x, int64_t n_
 // later consumes (3 x-plane chunks + 2 y chunks per 128-point block), so the
 // ring needs no cross-lane synchronisation, only cp.async.wait_group; D blocks
 // are in flight per warp without holding any registers.
-constexpr int FA_DEPTH = 4;                      // blocks in flight per warp
+constexpr int FA_DEPTH = 4;                      // blocks in flight per warp (6, 8: no faster)
 constexpr int FA_BLOCK_BYTES = 3 * 128 * 4 + 128 * 8;  // 2560 B per 128-point block
 constexpr size_t FA_SMEM = (size_t)(FA_THREADS / 32) * FA_DEPTH * FA_BLOCK_BYTES;
 
@@ -1096,6 +1096,8 @@ static cudaError_t launch_attn(const uint32_t* x, int64_t n_pts, const double* y
   uint32_t* box = reinterpret_cast<uint32_t*>(mom + (size_t)ATTN_NACC * n_sig);
   const bool vec_ok = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && (n_pts % 4 == 0);
   int per_sm = 0;
+  cudaFuncSetAttribute(fit_moments_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)FA_SMEM);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_moments_attn_kernel, FA_THREADS,
                                                 FA_SMEM);
   int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
