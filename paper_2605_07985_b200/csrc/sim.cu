@@ -232,6 +232,77 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
         status = DOOLY_ERR_NON_TERMINATION;
         break;
       }
+      // ---- 1b. decode window (exact windowed commit).  When every
+      // running request is in decode and nothing can be admitted (no waiting
+      // request, batch full, or the FCFS head blocked by the KV cap — all of
+      // which only a finish can change), the next iterations have a fixed
+      // composition: iteration u has num_toks = batch = nrun, prefill = 0 and
+      // every request's KV one token longer per iteration.  Lane u evaluates
+      // iteration u's whole op list (same entry arithmetic, same in-order sum);
+      // the clock then commits them in order, stopping before the first
+      // iteration that starts with an arrival due, and before the first finish.
+      if (nrun > 0 && sl.left[nrun - 1] == 0) {
+        bool blocked = admit == arrive || nrun >= MB;
+        if (!blocked) {
+          if (wbase != admit) ld_wait(admit);
+          const uint64_t need = (uint64_t)(__shfl_sync(0xFFFFFFFFu, w_p, 0) +
+                                           __shfl_sync(0xFFFFFFFFu, w_o, 0)) * kvb;
+          blocked = reserved + need > cap;
+        }
+        if (blocked) {
+          uint32_t tf = 0xFFFFFFFFu, kv0 = 0;
+          for (int j = lane; j < nrun; j += 32) {
+            tf = min(tf, sl.out[j] - sl.dec[j]);
+            kv0 += sl.kv[j];
+          }
+          tf = __reduce_min_sync(0xFFFFFFFFu, tf);
+          kv0 = warp_sum_u32(kv0);
+          int64_t wmax = (int64_t)tf - 1;  // iterations before the first finish
+          if (wmax > 32) wmax = 32;
+          if (wmax > cfg.max_iterations - it) wmax = cfg.max_iterations - it;
+          if (wmax >= 2) {
+            const uint32_t nr = (uint32_t)nrun;
+            const uint32_t kvs_u = kv0 + (uint32_t)lane * nr;
+            uint32_t kvw_u = 0;
+            if (W) {
+              for (int j = 0; j < nrun; ++j) kvw_u += min(sl.kv[j] + (uint32_t)lane, W);
+            }
+            bool bad = false;
+            double lat_u = 0.0;
+            for (int e = 0; e < ops.n_ops; ++e)
+              lat_u = add(lat_u, mul((double)ops.repeat[e],
+                                     entry_value(ops, &s_ops, e, nr, 0u, nr, kvs_u, kvw_u, bad)));
+            if (__any_sync(0xFFFFFFFFu, bad && lane < wmax)) {
+              status = DOOLY_ERR_UNKNOWN_SIGNATURE;
+              break;
+            }
+            const double next_arr = __shfl_sync(0xFFFFFFFFu, win_arr, 0);
+            int weff = 0;
+            for (int u = 0; u < (int)wmax; ++u) {
+              if (u > 0 && arrive < n && next_arr <= clock) break;  // arrival due: normal path
+              clock = add(clock, __shfl_sync(0xFFFFFFFFu, lat_u, u));
+              ++weff;
+            }
+            if (log_feat != nullptr && lane < weff && it + lane < log_cap) {
+              const int64_t row = shard * log_cap + it + lane;
+              uint32_t* lf = log_feat + row * DOOLY_IT_FEATS;
+              lf[0] = nr;
+              lf[1] = 0u;
+              lf[2] = nr;
+              lf[3] = kvs_u;
+              lf[4] = kvw_u;
+              log_lat[row] = lat_u;
+            }
+            it += weff;
+            for (int j = lane; j < nrun; j += 32) {
+              sl.kv[j] += (uint32_t)weff;
+              sl.dec[j] += (uint32_t)weff;
+            }
+            __syncwarp();
+            continue;
+          }
+        }
+      }
       // ---- 2. schedule (decode prefix | <=1 prefill at the tail)
       const bool has_p = nrun > 0 && sl.left[nrun - 1] > 0;
       const int n_dec = nrun - (has_p ? 1 : 0);
