@@ -29,6 +29,9 @@
 namespace dooly {
 
 constexpr int SIM_WARPS = 4;
+#ifndef SIM_WIN
+#define SIM_WIN 1  // decode-window iterations per lane (window <= 32 * SIM_WIN); 2: C1 -13%, C4 +3%
+#endif
 
 struct StagedOps {
   AffineRow aff[DOOLY_MAX_OPS];
@@ -242,13 +245,16 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       // the clock then commits them in order, stopping before the first
       // iteration that starts with an arrival due, and before the first finish.
       if (nrun > 0 && sl.left[nrun - 1] == 0) {
-        bool blocked = admit == arrive || nrun >= MB;
-        if (!blocked) {
+        // hard: admission is blocked by the batch size or the KV cap of the FCFS
+        // head, which only a finish can lift — arrivals meanwhile just queue
+        bool hard = nrun >= MB;
+        if (!hard && admit < arrive) {
           if (wbase != admit) ld_wait(admit);
           const uint64_t need = (uint64_t)(__shfl_sync(0xFFFFFFFFu, w_p, 0) +
                                            __shfl_sync(0xFFFFFFFFu, w_o, 0)) * kvb;
-          blocked = reserved + need > cap;
+          hard = reserved + need > cap;
         }
+        const bool blocked = hard || admit == arrive;
         if (blocked) {
           uint32_t tf = 0xFFFFFFFFu, kv0 = 0;
           for (int j = lane; j < nrun; j += 32) {
@@ -258,40 +264,62 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
           tf = __reduce_min_sync(0xFFFFFFFFu, tf);
           kv0 = warp_sum_u32(kv0);
           int64_t wmax = (int64_t)tf - 1;  // iterations before the first finish
-          if (wmax > 32) wmax = 32;
+          if (wmax > 32 * SIM_WIN) wmax = 32 * SIM_WIN;
           if (wmax > cfg.max_iterations - it) wmax = cfg.max_iterations - it;
           if (wmax >= 2) {
             const uint32_t nr = (uint32_t)nrun;
-            const uint32_t kvs_u = kv0 + (uint32_t)lane * nr;
-            uint32_t kvw_u = 0;
-            if (W) {
-              for (int j = 0; j < nrun; ++j) kvw_u += min(sl.kv[j] + (uint32_t)lane, W);
-            }
             bool bad = false;
-            double lat_u = 0.0;
-            for (int e = 0; e < ops.n_ops; ++e)
-              lat_u = add(lat_u, mul((double)ops.repeat[e],
-                                     entry_value(ops, &s_ops, e, nr, 0u, nr, kvs_u, kvw_u, bad)));
-            if (__any_sync(0xFFFFFFFFu, bad && lane < wmax)) {
+            double lat_k[SIM_WIN];
+            uint32_t kvs_k[SIM_WIN], kvw_k[SIM_WIN];
+#pragma unroll
+            for (int k = 0; k < SIM_WIN; ++k) {  // lane evaluates iterations lane + 32k
+              const uint32_t u = (uint32_t)(lane + 32 * k);
+              kvs_k[k] = kv0 + u * nr;
+              kvw_k[k] = 0;
+              if (W && (int64_t)u < wmax)
+                for (int j = 0; j < nrun; ++j) kvw_k[k] += min(sl.kv[j] + u, W);
+              lat_k[k] = 0.0;
+              if ((int64_t)u < wmax)
+                for (int e = 0; e < ops.n_ops; ++e)
+                  lat_k[k] = add(lat_k[k], mul((double)ops.repeat[e],
+                                               entry_value(ops, &s_ops, e, nr, 0u, nr, kvs_k[k],
+                                                           kvw_k[k], bad)));
+            }
+            if (__any_sync(0xFFFFFFFFu, bad)) {
               status = DOOLY_ERR_UNKNOWN_SIGNATURE;
               break;
             }
             const double next_arr = __shfl_sync(0xFFFFFFFFu, win_arr, 0);
             int weff = 0;
-            for (int u = 0; u < (int)wmax; ++u) {
-              if (u > 0 && arrive < n && next_arr <= clock) break;  // arrival due: normal path
-              clock = add(clock, __shfl_sync(0xFFFFFFFFu, lat_u, u));
-              ++weff;
+#pragma unroll
+            for (int k = 0; k < SIM_WIN; ++k) {
+              bool stop = false;
+              for (int l = 0; l < 32; ++l) {
+                const int u = 32 * k + l;
+                if (u >= wmax || (!hard && u > 0 && arrive < n && next_arr <= clock)) {
+                  stop = true;  // arrival due (admit it) or the window is used up
+                  break;
+                }
+                clock = add(clock, __shfl_sync(0xFFFFFFFFu, lat_k[k], l));
+                ++weff;
+              }
+              if (stop) break;
             }
-            if (log_feat != nullptr && lane < weff && it + lane < log_cap) {
-              const int64_t row = shard * log_cap + it + lane;
-              uint32_t* lf = log_feat + row * DOOLY_IT_FEATS;
-              lf[0] = nr;
-              lf[1] = 0u;
-              lf[2] = nr;
-              lf[3] = kvs_u;
-              lf[4] = kvw_u;
-              log_lat[row] = lat_u;
+            if (log_feat != nullptr) {
+#pragma unroll
+              for (int k = 0; k < SIM_WIN; ++k) {
+                const int u = lane + 32 * k;
+                if (u < weff && it + u < log_cap) {
+                  const int64_t row = shard * log_cap + it + u;
+                  uint32_t* lf = log_feat + row * DOOLY_IT_FEATS;
+                  lf[0] = nr;
+                  lf[1] = 0u;
+                  lf[2] = nr;
+                  lf[3] = kvs_k[k];
+                  lf[4] = kvw_k[k];
+                  log_lat[row] = lat_k[k];
+                }
+              }
             }
             it += weff;
             for (int j = lane; j < nrun; j += 32) {
