@@ -833,7 +833,7 @@ def bench_sim(args, dev, dist_on, rank, world):
             "ttft_p99_s": float(np.nanpercentile(ttft, 99)),
             "config": f"llama-3-70b-like tp=4 flashattention-like on a100-like; Poisson "
                       f"{args.sim_rate} req/s per replica x {S} replicas; chunk 8192, max_batch 256",
-            "bound": "latency (sequential per-replica event loop; one warp per replica)"}
+            "bound": "latency (sequential per-replica event loop, one warp per replica; exact decode windows evaluate up to 32 event-free iterations in parallel)"}
 
 
 # ---------------------------------------------------------------- reference arm
