@@ -14,8 +14,11 @@
 // versus ~95 FP64 instructions per point for the per-signature Gram path
 // (fit.cu).
 //
-// Three kernels share this contract:
-//   fit_grid_warp_kernel  (default) one warp per signature, no shared-memory
+// Four kernels share this contract:
+//   fit_grid_db_kernel    (affine default) the warp kernel with the y loads of
+//                         the next YS steps in flight while the current YS
+//                         steps are evaluated (register double buffer).
+//   fit_grid_warp_kernel  (attention default) one warp per signature, no shared-memory
 //                         stage, no CTA barrier: y streamed from HBM with
 //                         L2::evict_last, 8 steps in flight per lane, re-read
 //                         from L2 in pass 2; f planes from L1.
@@ -28,6 +31,9 @@
 // repeated per signature — coefficients within 1e-9 normwise, fit_err within
 // the MAPE bound (tests/test_gpu_fit_grid.py), same row layout and statuses.
 #include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 
@@ -819,6 +825,138 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
   }
 }
 
+// Per-step arithmetic of the two passes (4 consecutive points per lane), the
+// same operations in the same order as fit_grid_warp_kernel's lambdas.
+template <int KIND>
+__device__ __forceinline__ void grid_p1_step(const double4& yv, const double4* fv, double* acc) {
+  constexpr int P = KIND == DOOLY_KIND_AFFINE ? 1 : 3;
+  const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double f[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) f[k] = j == 0 ? fv[k].x : j == 1 ? fv[k].y : j == 2 ? fv[k].z : fv[k].w;
+    if constexpr (KIND == DOOLY_KIND_AFFINE) {
+      acc[0] += yy[j];
+      acc[1] = fma(yy[j], f[0], acc[1]);
+    } else {
+      const double y1 = yy[j] * f[0], y2 = yy[j] * f[1], y3 = yy[j] * f[2];
+      acc[0] += yy[j];
+      acc[1] += y1;
+      acc[2] += y2;
+      acc[3] += y3;
+      acc[4] = fma(y1, f[0], acc[4]);
+      acc[5] = fma(y2, f[1], acc[5]);
+      acc[6] = fma(y3, f[2], acc[6]);
+      acc[7] = fma(y1, f[1], acc[7]);
+      acc[8] = fma(y1, f[2], acc[8]);
+      acc[9] = fma(y2, f[2], acc[9]);
+    }
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ void grid_p2_step(const double4& yv, const double4* fv, const double* c,
+                                             double& err) {
+  constexpr int P = KIND == DOOLY_KIND_AFFINE ? 1 : 3;
+  const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    double f[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) f[k] = j == 0 ? fv[k].x : j == 1 ? fv[k].y : j == 2 ? fv[k].z : fv[k].w;
+    const double pr = fmax(grid_horner<KIND>(c, f), DOOLY_CLAMP_FLOOR);
+    err = fma(fabs(pr - yy[j]), g_rcp1(yy[j]), err);
+  }
+}
+
+// Register double-buffered sweep (n % (128 * YS) == 0): the loads of batch
+// k + 1 (YS steps of y per lane) are in flight while batch k is evaluated, so
+// a lane always has between YS and 2 YS steps outstanding.
+template <int KIND, int YS, bool P1>
+__device__ __forceinline__ void grid_sweep_db(const double* __restrict__ fpl, int n, int lane,
+                                              const double* yr, const double* c, double* acc,
+                                              double& err) {
+  constexpr int P = KIND == DOOLY_KIND_AFFINE ? 1 : 3;
+  constexpr int S = 128 * YS;
+  double4 va[YS], vb[YS];
+  auto load = [&](double4* v, int p) {
+#pragma unroll
+    for (int t = 0; t < YS; ++t) v[t] = g_ld_y(yr + p + 128 * t, P1);
+  };
+  auto eval = [&](const double4* v, int p) {
+#pragma unroll
+    for (int t = 0; t < YS; ++t) {
+      double4 fv[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) fv[k] = g_ld_f(fpl + k * n + p + 128 * t);
+      if (P1)
+        grid_p1_step<KIND>(v[t], fv, acc);
+      else
+        grid_p2_step<KIND>(v[t], fv, c, err);
+    }
+  };
+  int p = 4 * lane;
+  load(va, p);
+  for (; p + S < n; p += 2 * S) {
+    load(vb, p + S);
+    eval(va, p);
+    if (p + 2 * S < n) load(va, p + 2 * S);
+    eval(vb, p + S);
+  }
+  if (p < n) eval(va, p);
+}
+
+template <int KIND, int YS>
+__global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
+    const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
+    const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
+    uint8_t* __restrict__ status, const dooly_grid_peers pe) {
+  using T = GridTraits<KIND>;
+  constexpr int P = T::P, NC = T::NC;
+  __shared__ double sW[NC][NC];
+  __shared__ double sinv[P];
+  __shared__ uint32_t slo[P], shi[P];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int t = tid; t < NC * NC; t += blockDim.x) sW[t / NC][t % NC] = gf->W[t / NC][t % NC];
+  if (tid < P) {
+    sinv[tid] = gf->inv[tid];
+    slo[tid] = gf->lo[tid];
+    shi[tid] = gf->hi[tid];
+  }
+  const bool ok = gf->ok != 0;
+  __syncthreads();
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int n = (int)n_pts;  // n_pts % (128 * YS) == 0 (launcher)
+  for (int64_t s = warp; s < n_sig; s += n_warps) {
+    if (!ok) {
+      if (lane == 0) write_unfitted_grid<KIND>(pe, table, s, fit_err, status);
+      continue;
+    }
+    const double* ys = y + s * n_pts;
+    double acc[NC], c[NC];
+    double err = 0.0;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k] = 0.0;
+    grid_sweep_db<KIND, YS, true>(fpl, n, lane, ys, c, acc, err);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) acc[k] = g_warp_sum(acc[k]);
+    double cj = 0.0;
+    if (lane < NC) {
+#pragma unroll
+      for (int i = 0; i < NC; ++i) cj = fma(sW[lane][i], acc[i], cj);
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) c[k] = __shfl_sync(0xFFFFFFFFu, cj, k);
+    grid_sweep_db<KIND, YS, false>(fpl, n, lane, ys, c, acc, err);
+    err = g_warp_sum(err);
+    if (lane == 0)
+      emit_row<KIND>(pe, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
+                     err / (double)n_pts, DOOLY_FIT_OK);
+  }
+}
+
 template <int KIND>
 static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const double* y, int64_t n_sig,
                                     void* table, double* fit_err, uint8_t* status,
@@ -831,25 +969,34 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   if (e != cudaSuccess) return e;
   *launches += 1;
   if (n_sig == 0) return cudaSuccess;
-  const char* which = getenv("DOOLY_FIT_GRID_KERNEL");  // "warp" (default) | "stage" | "plain"
-  const bool want_warp = which == nullptr || which[0] == 'w';
-  if (want_warp && n_pts % 4 == 0 && n_pts < (1ll << 30) && (uintptr_t)y % 32 == 0 &&
-      (uintptr_t)ws % 32 == 0) {
-    auto kern = fit_grid_warp_kernel<KIND>;
-    const int warps_per_sm = getenv("DOOLY_FIT_GRID_WARPS")
-                                        ? atoi(getenv("DOOLY_FIT_GRID_WARPS"))
-                                        : 16;
-    // warps in flight x row bytes must stay well inside L2 so pass 2 re-reads hit
-    int64_t blocks = (int64_t)n_sm * (warps_per_sm > 8 ? warps_per_sm / 8 : 1);
-    const int64_t need = (n_sig + 7) / 8;
-    if (blocks > need) blocks = need;
-    kern<<<(unsigned)blocks, 256, 0, stream>>>(fpl, n_pts, y, n_sig, gf, table, fit_err, status,
-                                               pe);
+  // "db" (default for affine) | "warp" (default for attention) | "stage" | "plain"
+  const char* which = getenv("DOOLY_FIT_GRID_KERNEL");
+  const bool aligned = n_pts < (1ll << 30) && (uintptr_t)y % 32 == 0 && (uintptr_t)ws % 32 == 0;
+  // warps in flight x row bytes must stay well inside L2 so pass 2 re-reads hit
+  const int warps_per_sm =
+      getenv("DOOLY_FIT_GRID_WARPS") ? atoi(getenv("DOOLY_FIT_GRID_WARPS")) : 16;
+  const int64_t warp_blocks =
+      std::min<int64_t>((int64_t)n_sm * (warps_per_sm > 8 ? warps_per_sm / 8 : 1), (n_sig + 7) / 8);
+  // Double-buffered warp kernel: measured 2.70 vs 2.78 ms (affine) and 5.39 vs
+  // 5.12 ms (attention) per 0.5M signatures x 4096 points against the warp
+  // kernel, so it is the affine default only.
+  const bool want_db = which != nullptr ? strcmp(which, "db") == 0 : KIND == DOOLY_KIND_AFFINE;
+  if (want_db && aligned && n_pts % 256 == 0) {
+    auto kern = n_pts % 512 == 0 ? fit_grid_db_kernel<KIND, 4> : fit_grid_db_kernel<KIND, 2>;
+    kern<<<(unsigned)warp_blocks, 256, 0, stream>>>(fpl, n_pts, y, n_sig, gf, table, fit_err,
+                                                    status, pe);
+    *launches += 1;
+    return cudaGetLastError();
+  }
+  const bool want_warp = which == nullptr || which[0] == 'w' || which[0] == 'd';
+  if (want_warp && n_pts % 4 == 0 && aligned) {
+    fit_grid_warp_kernel<KIND><<<(unsigned)warp_blocks, 256, 0, stream>>>(
+        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe);
     *launches += 1;
     return cudaGetLastError();
   }
   const size_t stage = (size_t)GridTraits<KIND>::RS * n_pts * 8;
-  const bool no_stage = which != nullptr && which[0] == 'p';
+  const bool no_stage = which != nullptr && strcmp(which, "plain") == 0;
   if (!no_stage && stage <= kGridStageMax && n_pts % 4 == 0 && (uintptr_t)y % 16 == 0) {
     auto kern = fit_grid_stage_kernel<KIND>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGridStageMax);

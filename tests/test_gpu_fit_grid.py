@@ -60,10 +60,11 @@ def _oracle(kind, x, y):
 
 
 @pytest.mark.parametrize("kind", [AFFINE, ATTN])
-@pytest.mark.parametrize("n_sig,n_pts", [(1, 512), (37, 512), (301, 512), (37, 510), (9, 4096), (7, 64), (5, 136)])
-@pytest.mark.parametrize("kernel", ["warp", "stage"])
+@pytest.mark.parametrize("n_sig,n_pts", [(1, 512), (37, 512), (301, 512), (37, 510), (9, 4096), (7, 64), (5, 136), (13, 768)])
+@pytest.mark.parametrize("kernel", ["warp", "stage", "db"])
 def test_fit_grid_matches_oracle_and_csr(kind, n_sig, n_pts, kernel, dev, monkeypatch):
-    """n_pts % 4 == 0 takes the warp-per-signature kernel (default) or the
+    """n_pts % 4 == 0 takes the warp-per-signature kernel, its register
+    double-buffered form (db: n_pts % 256 == 0, the affine default) or the
     shared-memory staged one (DOOLY_FIT_GRID_KERNEL=stage); 510 the direct one."""
     from paper_2605_07985_b200.sim import fit_tables
 
@@ -129,3 +130,19 @@ def test_fit_grid_rank_deficient_drops_columns(dev):
     pg = osim.eval_poly(ATTN, got["coef"][0], got["inv"][0], x.T)
     pr = osim.eval_poly(ATTN, ref["coef"][0], ref["inv"][0], x.T)
     assert np.max(np.abs(pg - pr) / pr) <= 1e-9
+
+
+@pytest.mark.parametrize("kind", [AFFINE, ATTN])
+def test_fit_grid_db_and_warp_bit_identical(kind, dev, monkeypatch):
+    """The double-buffered kernel runs the warp kernel's per-lane arithmetic in
+    the same order, so tables, fit_err and statuses are bit-identical."""
+    rng = np.random.default_rng(29 + kind)
+    x = _grid(kind, 4096, rng)[:, :4096]
+    y = _ys(kind, x, 2000, rng)
+    out = {}
+    for k in ("warp", "db"):
+        monkeypatch.setenv("DOOLY_FIT_GRID_KERNEL", k)
+        out[k] = _fit_grid_gpu(kind, x, y, dev)
+    a, b = out["warp"], out["db"]
+    assert torch.equal(a.table, b.table) and torch.equal(a.status, b.status)
+    assert torch.equal(a.fit_err.view(torch.int64), b.fit_err.view(torch.int64))

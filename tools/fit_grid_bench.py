@@ -28,9 +28,12 @@ def main() -> None:
     ap.add_argument("--points", type=int, default=4096)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--csr", action="store_true")
+    ap.add_argument("--kinds", default="0,1")
+    ap.add_argument("--vs-warp", action="store_true",
+                    help="check the table bit-identical to DOOLY_FIT_GRID_KERNEL=warp")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
-    for kind in (0, 1):
+    for kind in [int(k) for k in a.kinds.split(",")]:
         x, y = bench.gen_grid_fit_data(kind, a.sigs, a.points, dev, seed=kind)
         fr = fit_grid(kind, x, y)
         ms = []
@@ -45,6 +48,19 @@ def main() -> None:
                 "grid_fits_per_s": a.sigs / min(ms) * 1e3,
                 "y_gb_per_s": a.sigs * a.points * 8 / min(ms) / 1e6,
                 "all_ok": int((fr.status != 0).sum().item()) == 0}
+        if a.vs_warp:
+            env = os.environ.get("DOOLY_FIT_GRID_KERNEL")
+            os.environ["DOOLY_FIT_GRID_KERNEL"] = "warp"
+            fw = fit_grid(kind, x, y)
+            torch.cuda.synchronize()
+            if env is None:
+                del os.environ["DOOLY_FIT_GRID_KERNEL"]
+            else:
+                os.environ["DOOLY_FIT_GRID_KERNEL"] = env
+            line["bit_identical_vs_warp"] = bool(torch.equal(fw.table, fr.table) and torch.equal(
+                fw.fit_err.view(torch.int64), fr.fit_err.view(torch.int64)) and torch.equal(
+                fw.status, fr.status))
+            del fw
         if a.csr:
             xr = x.repeat(1, a.sigs)
             off = torch.arange(a.sigs + 1, dtype=torch.int64, device=dev) * a.points
