@@ -156,8 +156,26 @@ def _csr(items: Sequence, planes: int):
     return x, y, off
 
 
+GRID_GROUP_MIN = 8   # signatures sharing one sweep grid before fit() takes the grid path
+
+
+def _grid_groups(items: Sequence, planes: int):
+    """Partition signatures by their exact training points: {x bytes: [i, ...]}."""
+    groups: dict = {}
+    for i, (x, _) in enumerate(items):
+        xa = np.ascontiguousarray(np.asarray(x, dtype=np.uint32).reshape(planes, -1))
+        groups.setdefault(xa.tobytes(), []).append(i)
+    return groups
+
+
 def fit(db: LatencyDB, device=None, strict: bool = True) -> Regressors:
     """One least-squares regressor per measured signature.
+
+    Signatures swept over the same points (one sweep grid per model/backend,
+    SPEC.md:466-474) are fitted together by the shared-grid kernel
+    (``fit_grid``: the Gram and its factor once per group); the rest go through
+    the per-signature CSR kernel (``fit_tables``).  Both meet the same result
+    contract, so the grouping is invisible to callers.
 
     Raises InsufficientData(signature, have, need) for the first signature with
     fewer than max(4, p + 1) measurements (App. A.8) when ``strict``."""
@@ -170,12 +188,32 @@ def fit(db: LatencyDB, device=None, strict: bool = True) -> Regressors:
             for s, (_, y) in zip(sigs, items):
                 if y.shape[0] < NEED[kind]:
                     raise InsufficientData(s.digest.hex(), int(y.shape[0]), NEED[kind])
-        x, y, off = _csr(items, _lib.PLANES[kind])
-        fr = fit_tables(kind, torch.from_numpy(x.view(np.int32)).to(dev),
-                        torch.from_numpy(y).to(dev), torch.from_numpy(off).to(dev))
+        planes = _lib.PLANES[kind]
+        grids = [g for g in _grid_groups(items, planes).values() if len(g) >= GRID_GROUP_MIN]
+        in_grid = {i for g in grids for i in g}
+        rest = [i for i in range(len(items)) if i not in in_grid]
+        order = [i for g in grids for i in g] + rest
+        n = len(order)
+        fr = FitResult(kind, torch.empty((n, _lib.ROW_BYTES[kind]), dtype=torch.uint8, device=dev),
+                       torch.empty(n, dtype=torch.float64, device=dev),
+                       torch.empty(n, dtype=torch.uint8, device=dev))
+        r0 = 0
+        for g in grids:
+            xg = np.asarray(items[g[0]][0], dtype=np.uint32).reshape(planes, -1)
+            yg = np.stack([np.asarray(items[i][1], dtype=np.float64) for i in g])
+            r1 = r0 + len(g)
+            fit_grid(kind, torch.from_numpy(np.ascontiguousarray(xg).view(np.int32)).to(dev),
+                     torch.from_numpy(yg).to(dev),
+                     FitResult(kind, fr.table[r0:r1], fr.fit_err[r0:r1], fr.status[r0:r1]))
+            r0 = r1
+        if rest:
+            x, y, off = _csr([items[i] for i in rest], planes)
+            fit_tables(kind, torch.from_numpy(x.view(np.int32)).to(dev),
+                       torch.from_numpy(y).to(dev), torch.from_numpy(off).to(dev),
+                       FitResult(kind, fr.table[r0:], fr.fit_err[r0:], fr.status[r0:]))
         tables[kind] = fr
-        for row, s in enumerate(sigs):
-            index[s.digest] = (kind, row)
+        for row, i in enumerate(order):
+            index[sigs[i].digest] = (kind, row)
     torch.cuda.synchronize(dev)
     return Regressors(tables, index, dev)
 

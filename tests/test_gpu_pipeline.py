@@ -154,3 +154,28 @@ def test_tp4_calltree_comm_entries(dev):
     comm = oprof.comm_latency(4, 512 * model.hidden_dim * 2, man.hardware.comm_alpha,
                               man.hardware.comm_beta)
     assert lat > 2 * model.num_layers * comm
+
+
+def test_fit_db_grid_groups_match_csr(corpus, dev, monkeypatch):
+    """fit(db) fits signatures that share a sweep grid with the shared-grid
+    kernel; the result equals the per-signature CSR path within the fit
+    contract (coefficients 1e-9 normwise, same statuses and boxes)."""
+    from paper_2605_07985_b200 import _lib, sim
+
+    db, _ = _profile(corpus, dev)
+    n_grouped = 0
+    for kind in (0, 1):
+        items = [db.measurements[s.digest] for s in db.signatures
+                 if s.kind == kind and s.digest in db.measurements]
+        n_grouped += sum(len(g) for g in sim._grid_groups(items, _lib.PLANES[kind]).values()
+                         if len(g) >= sim.GRID_GROUP_MIN)
+    assert n_grouped > 0
+    regs_g = sim.fit(db, dev)
+    monkeypatch.setattr(sim, "GRID_GROUP_MIN", 1 << 30)
+    regs_c = sim.fit(db, dev)
+    for d in regs_c.index:
+        a, b = regs_g.regressor(d), regs_c.regressor(d)
+        ca, cb = np.array(a.coefficients), np.array(b.coefficients)
+        assert np.max(np.abs(ca - cb)) <= 2e-9 * np.max(np.abs(cb))
+        assert a.box == b.box and a.inv_scale == b.inv_scale
+        assert abs(a.fit_error - b.fit_error) <= 1e-9 * b.fit_error + 1e-12
