@@ -325,6 +325,174 @@ extern "C" int probe_tma_gather4(const void* table, uint32_t n_rows, int row_byt
   return 1;
 }
 
+
+// Cooperative gather: the 3 sectors of one 96-B row are loaded by 3 lanes of
+// ONE LDG.256 (lane 3j+k reads sector k of row j; 10 rows per instruction), so
+// a row costs the L1TEX wavefronts of the lines it touches (1-2) instead of 3.
+// STRIDE = 96 (packed rows, half straddle a line) or 128 (one line per row).
+template <int STRIDE>
+__global__ void __launch_bounds__(256) coop_gather_kernel(const uint8_t* __restrict__ table,
+                                                          uint32_t n_rows, int64_t n_q,
+                                                          unsigned long long* sink) {
+  const int lane = threadIdx.x & 31;
+  const int j = lane / 3, k = lane - 3 * (lane / 3);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0.0;
+  // one warp round = 8 instructions x 10 rows
+  for (int64_t q0 = warp * 80; q0 < n_q; q0 += n_warps * 80) {
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int64_t qq = q0 + t * 10 + (j < 10 ? j : 9);
+      const uint32_t r = mix((uint64_t)qq) % n_rows;
+      double a, b, c, d;
+      ld256(table + (uint64_t)r * STRIDE + 32 * (k < 3 ? k : 2), a, b, c, d);
+      v[t] = (j < 10 && qq < n_q) ? a + b + c + d : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc += v[t];
+  }
+  if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+extern "C" int probe_coop_gather(const void* table, uint32_t n_rows, int stride, int64_t n_q,
+                                 void* sink, int blocks, void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  auto t = static_cast<const uint8_t*>(table);
+  auto k = static_cast<unsigned long long*>(sink);
+  if (stride == 96)
+    coop_gather_kernel<96><<<blocks, 256, 0, s>>>(t, n_rows, n_q, k);
+  else if (stride == 128)
+    coop_gather_kernel<128><<<blocks, 256, 0, s>>>(t, n_rows, n_q, k);
+  else
+    return 1;
+  return (int)cudaGetLastError();
+}
+
+// Cooperative gather + shared-memory transpose (the predict data path): per
+// round of 32 rows, 3 LDG.256 per lane fetch sector (g % 3) of row (g / 3)
+// for g = 32 t + lane, the sectors are stored to a per-warp buffer (row stride
+// 112 B: conflict-free 16-B reads), and lane i then reads row i back (6 x
+// LDS.128) — memory-only, to measure what the transpose costs on top of the
+// cooperative gather.  The next round's loads are issued before this round's
+// stores.
+__global__ void __launch_bounds__(128) coop_smem_kernel(const uint8_t* __restrict__ table,
+                                                        uint32_t n_rows, int64_t n_q,
+                                                        unsigned long long* sink) {
+  __shared__ __align__(16) double srow[4][2][32 * 14];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0.0;
+  int row_of[3], k_of[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int g = 32 * t + lane;
+    row_of[t] = g / 3;
+    k_of[t] = g - 3 * (g / 3);
+  }
+  double4 a[3], b[3];
+  auto gather = [&](int64_t q0, double4* v) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const uint32_t r = mix((uint64_t)(q0 + row_of[t])) % n_rows;
+      ld256(table + (uint64_t)r * 96 + 32 * k_of[t], v[t].x, v[t].y, v[t].z, v[t].w);
+    }
+  };
+  int buf = 0;
+  int64_t q0 = warp * 32;
+  if (q0 < n_q) gather(q0, a);
+  for (; q0 < n_q; q0 += n_warps * 32) {
+    const int64_t qn = q0 + n_warps * 32;
+    if (qn < n_q) gather(qn, b);
+    double* sr = srow[w][buf];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      double* d = sr + row_of[t] * 14 + 4 * k_of[t];
+      *reinterpret_cast<double2*>(d) = make_double2(a[t].x, a[t].y);
+      *reinterpret_cast<double2*>(d + 2) = make_double2(a[t].z, a[t].w);
+    }
+    __syncwarp();
+    const double* mine = sr + lane * 14;
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const double2 v = *reinterpret_cast<const double2*>(mine + 2 * i);
+      s += v.x + v.y;
+    }
+    acc += s;
+    buf ^= 1;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) a[t] = b[t];
+  }
+  if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+extern "C" int probe_coop_smem(const void* table, uint32_t n_rows, int64_t n_q, void* sink,
+                               int blocks, void* stream) {
+  coop_smem_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint8_t*>(table), n_rows, n_q, static_cast<unsigned long long*>(sink));
+  return (int)cudaGetLastError();
+}
+
+// Cooperative gather + register transpose by shuffles: lane g of instruction t
+// holds sector (32 t + g) % 3 of row (32 t + g) / 3; for each sector k the
+// source lane L picks the one slot t with (L + 32 t) % 3 == k, so one SHFL per
+// 32-bit word delivers sector k of row i to lane i (24 SHFL per 32 rows).
+__global__ void __launch_bounds__(256) coop_shfl_kernel(const uint8_t* __restrict__ table,
+                                                        uint32_t n_rows, int64_t n_q,
+                                                        unsigned long long* sink) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double acc = 0.0;
+  int row_of[3], k_of[3], slot[3], src[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const int g = 32 * t + lane;
+    row_of[t] = g / 3;
+    k_of[t] = g - 3 * (g / 3);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    slot[k] = ((k - lane % 3 + 3) * 2) % 3;   // (L + 32 t) % 3 == k
+    src[k] = (3 * lane + k) & 31;             // holder of sector k of row `lane`
+  }
+  double4 a[3], b[3];
+  auto gather = [&](int64_t q0, double4* v) {
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const uint32_t r = mix((uint64_t)(q0 + row_of[t])) % n_rows;
+      ld256(table + (uint64_t)r * 96 + 32 * k_of[t], v[t].x, v[t].y, v[t].z, v[t].w);
+    }
+  };
+  int64_t q0 = warp * 32;
+  if (q0 < n_q) gather(q0, a);
+  for (; q0 < n_q; q0 += n_warps * 32) {
+    const int64_t qn = q0 + n_warps * 32;
+    if (qn < n_q) gather(qn, b);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double4 m = slot[k] == 0 ? a[0] : slot[k] == 1 ? a[1] : a[2];
+      s += __shfl_sync(0xFFFFFFFFu, m.x, src[k]) + __shfl_sync(0xFFFFFFFFu, m.y, src[k]) +
+           __shfl_sync(0xFFFFFFFFu, m.z, src[k]) + __shfl_sync(0xFFFFFFFFu, m.w, src[k]);
+    }
+    acc += s;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) a[t] = b[t];
+  }
+  if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+extern "C" int probe_coop_shfl(const void* table, uint32_t n_rows, int64_t n_q, void* sink,
+                               int blocks, void* stream) {
+  coop_shfl_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      static_cast<const uint8_t*>(table), n_rows, n_q, static_cast<unsigned long long*>(sink));
+  return (int)cudaGetLastError();
+}
+
 extern "C" int probe_gather(const void* table, uint32_t n_rows, int sectors, int64_t n_q,
                             void* sink, int blocks, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;

@@ -60,6 +60,43 @@ def main() -> None:
     if "gather4" in only:
         gather4(lib, dev, n_sm, sink, st, timed)
         return
+    if "coop" in only:
+        lib.probe_coop_gather.argtypes = lib.probe_gather.argtypes
+        n_q, rows = 500_000_000, 500_000
+        for stride in (96, 128):
+            table = torch.rand((rows * stride) // 8, dtype=torch.float64, device=dev)
+            for per_sm in (4, 8):
+                ms = timed(lambda: lib.probe_coop_gather(table.data_ptr(), rows, stride, n_q,
+                                                         sink.data_ptr(), n_sm * per_sm, st))
+                print(json.dumps({"probe": "coop_gather", "row_bytes": 96, "stride": stride,
+                                  "rows": rows, "ctas_per_sm": per_sm, "ms": ms,
+                                  "g_rows_per_s": n_q / ms / 1e6}), flush=True)
+            if stride == 96:
+                lib.probe_coop_smem.argtypes = [C.c_void_p, C.c_uint32, C.c_int64, C.c_void_p,
+                                                C.c_int, C.c_void_p]
+                for per_sm in (4, 6, 8):
+                    ms = timed(lambda: lib.probe_coop_smem(table.data_ptr(), rows, n_q,
+                                                           sink.data_ptr(), n_sm * per_sm, st))
+                    print(json.dumps({"probe": "coop_smem", "row_bytes": 96, "rows": rows,
+                                      "ctas_per_sm": per_sm, "ms": ms,
+                                      "g_rows_per_s": n_q / ms / 1e6}), flush=True)
+            if stride == 96:
+                lib.probe_coop_shfl.argtypes = lib.probe_coop_smem.argtypes
+                for per_sm in (4, 6, 8):
+                    ms = timed(lambda: lib.probe_coop_shfl(table.data_ptr(), rows, n_q,
+                                                           sink.data_ptr(), n_sm * per_sm, st))
+                    print(json.dumps({"probe": "coop_shfl", "row_bytes": 96, "rows": rows,
+                                      "ctas_per_sm": per_sm, "ms": ms,
+                                      "g_rows_per_s": n_q / ms / 1e6}), flush=True)
+            for sectors in (3,):
+                if stride != 96:
+                    continue
+                ms = timed(lambda: lib.probe_gather(table.data_ptr(), rows, sectors, n_q,
+                                                    sink.data_ptr(), n_sm * 8, st))
+                print(json.dumps({"probe": "gather", "row_bytes": 96, "rows": rows, "ms": ms,
+                                  "g_rows_per_s": n_q / ms / 1e6}), flush=True)
+            del table
+        return
     if "predmem" in only:
         predict_mem(lib, dev, n_sm, timed)
         return
