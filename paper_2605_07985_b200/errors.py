@@ -1,8 +1,8 @@
 """Error types raised at the hot-path boundary.
 
 Names, constructor signatures and meaning follow the reference hierarchy
-(`pkg/src/dooly/errors.py:4-85`); only the classes the dedup / fit / predict /
-simulate path can raise are defined here, plus the base class.  C-ABI status
+(`pkg/src/dooly/errors.py:4-85`); the taint / trace / opset classes serve the
+record producer (tracer.py, opset.py) that feeds dedup.  C-ABI status
 codes (include/dooly_b200.h) map onto these one-to-one in ``raise_for_status``.
 """
 
@@ -11,6 +11,34 @@ from __future__ import annotations
 
 class DoolyError(Exception):
     """Root of every error this package raises (errors.py:4)."""
+
+
+class MixValueConflict(DoolyError):
+    """One value would carry two labels inside a Mix taint (errors.py:8)."""
+
+
+class UnknownComponent(DoolyError):
+    """split() of a Mix by a value it does not contain (errors.py:12)."""
+
+
+class ShapeMismatch(DoolyError):
+    """A reshape whose element counts disagree (errors.py:28)."""
+
+
+class MalformedTrace(DoolyError):
+    """Trace events whose intervals do not nest (errors.py:32)."""
+
+
+class RetraceFailed(DoolyError):
+    """Two consecutive dummy batches both collided with model values (errors.py:36)."""
+
+
+class ContextUnavailable(DoolyError):
+    """Context emulation asked for a stateless entry (errors.py:40)."""
+
+
+class Unresolvable(DoolyError):
+    """No runnable ancestor covers a kernel, not even the root (errors.py:44)."""
 
 
 class ParseError(DoolyError):

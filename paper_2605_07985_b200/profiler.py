@@ -514,7 +514,7 @@ def profile_corpus(manifest, db: Optional[LatencyDB] = None, device=None,
     """cmd_profile without the CLI: dedup every (model, backend)
     runnable set in manifest order against the DB, sweep the new signatures.
     Returns (db, report) with per-config N/R counts."""
-    from .records import synthesize_entries
+    from .records import runnable_entries
 
     db = db if db is not None else LatencyDB()
     grid = grid or manifest.grid
@@ -522,7 +522,7 @@ def profile_corpus(manifest, db: Optional[LatencyDB] = None, device=None,
     for m in manifest.models:
         for b in manifest.backends:
             cid = db.add_configuration(manifest.hardware.name, m.name, b.name, manifest.tp_degree)
-            entries = synthesize_entries(m, b, manifest.tp_degree)
+            entries = runnable_entries(m, b, manifest.tp_degree)
             to_profile, skipped, digests = dedup_with_digests(entries, db, cid, device)
             for e, d in zip(to_profile, digests):
                 x, y = sweep(e, grid, m, manifest.hardware, b)
@@ -630,7 +630,7 @@ def profile_and_fit(manifest, db: Optional[LatencyDB] = None, device=None,
     (model_operations rows for all entries), then one sweep+fit launch per
     regression kind for all new signatures.  Measurements are never
     materialised; returns (db, Regressors, report)."""
-    from .records import synthesize_entries
+    from .records import runnable_entries
     from .sim import Regressors
 
     dev = _device(device)
@@ -640,7 +640,7 @@ def profile_and_fit(manifest, db: Optional[LatencyDB] = None, device=None,
     for m in manifest.models:
         for b in manifest.backends:
             cid = db.add_configuration(manifest.hardware.name, m.name, b.name, manifest.tp_degree)
-            entries = synthesize_entries(m, b, manifest.tp_degree)
+            entries = runnable_entries(m, b, manifest.tp_degree)
             to_profile, skipped, digs = dedup_with_digests(entries, db, cid, dev)
             items += [(e, m, b) for e in to_profile]
             digests += digs

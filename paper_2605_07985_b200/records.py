@@ -11,10 +11,12 @@ columnar layout the GPU dedup kernel consumes.
   D1/D2 SPEC.md:513-514 with the byte widths pinned in SURVEY App. A.1-A.3).
 * ``RecordPacker`` turns entries into the u32 record stream + string tables of
   include/dooly_b200.h (the canonical message is rebuilt on the GPU).
-* ``synthesize_entries`` is the builder's record producer standing in for the
-  absent tracer/opset: the runnable set of one
+* ``runnable_entries`` is the record producer: tracer.run_trace ->
+  opset.build_tree / prune / resolve.
+  ``synthesize_entries`` is the closed-form runnable set of one
   (model, backend, tp) in `run_trace` op order with layer
-  pruning (SPEC.md:364-367).
+  pruning; tests hold the traced sets equal to it entry for
+  entry, and ``producer="synth"`` selects it.
 """
 
 from __future__ import annotations
@@ -324,8 +326,22 @@ def synthesize_entries(cfg: ModelConfig, backend: BackendSpec, tp: int = 1) -> l
     return out
 
 
-def corpus_entries(manifest, tp: Optional[int] = None) -> list:
+def runnable_entries(cfg: ModelConfig, backend: BackendSpec, tp: int = 1,
+                     producer: str = "trace") -> list:
+    """The runnable set of one configuration: traced and resolved (default) or
+    the closed-form synthesizer."""
+    if producer == "synth":
+        return synthesize_entries(cfg, backend, tp)
+    if producer != "trace":
+        raise ValueError(f"unknown record producer {producer!r}")
+    from .opset import runnable_set
+
+    return runnable_set(cfg, backend, tp)
+
+
+def corpus_entries(manifest, tp: Optional[int] = None, producer: str = "trace") -> list:
     """All (model, backend) runnable sets in manifest order — models outer,
     backends inner (dedup order, App. A.4).  Returns [(model, backend, entries)]."""
     tp = manifest.tp_degree if tp is None else tp
-    return [(m, b, synthesize_entries(m, b, tp)) for m in manifest.models for b in manifest.backends]
+    return [(m, b, runnable_entries(m, b, tp, producer)) for m in manifest.models
+            for b in manifest.backends]

@@ -28,7 +28,7 @@ from .errors import (InsufficientData, LengthMismatch, NonTermination, UnknownSi
                      ValidationError, ZeroTruth)
 from .modelir import BackendSpec, HardwareSpec, ModelConfig, Request
 from .profiler import LatencyDB, _device, DeviceRecords, hash_records
-from .records import RunnableEntry, pack_entries, synthesize_entries
+from .records import RunnableEntry, pack_entries, runnable_entries
 
 NEED = {_lib.KIND_AFFINE: 4, _lib.KIND_ATTN: 11}          # max(4, p + 1), App. A.8
 FEATURE_NAMES = {_lib.KIND_AFFINE: ("num_toks",),
@@ -363,7 +363,7 @@ def build_calltree(model: ModelConfig, backend: BackendSpec, regs: Regressors,
     """Map a (model, backend, tp) runnable set onto regressor rows (digests are
     computed by the GPU hash kernel) and append the TP all-reduces: 2 per
     layer of num_toks * hidden * dtype bytes (App. A.16)."""
-    entries = synthesize_entries(model, backend, tp) if entries is None else list(entries)
+    entries = runnable_entries(model, backend, tp) if entries is None else list(entries)
     recs = DeviceRecords.from_packed(pack_entries(entries), regs.device)
     digs = hash_records(recs).cpu().numpy()
     ol = _lib.OpList()
