@@ -325,7 +325,7 @@ class ClockSampler:
                                              int(get_reasons(h))))
                     except pynvml.NVMLError:
                         pass
-                    time.sleep(0.005)
+                    time.sleep(0.002)
 
             self._thread = threading.Thread(target=loop, daemon=True)
             self._thread.start()
@@ -348,12 +348,22 @@ class ClockSampler:
         if self._thread is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         t0, t1 = self.window
-        inside = [s for s in self.samples if t0 is not None and t0 <= s[0] <= (t1 or t0)]
+        t1 = t1 or t0
+        inside = [s for s in self.samples if t0 is not None and t0 <= s[0] <= t1]
+        pad = 0.0
+        # a short timed region can fall between two NVML reads (a read takes
+        # ms on some drivers): widen the window until 3 samples, and say so
+        while len(inside) < 3 and pad < 0.05 and t0 is not None:
+            pad += 0.005
+            inside = [s for s in self.samples if t0 - pad <= s[0] <= t1 + pad]
         src = inside if inside else self.samples[-3:]
         reasons = sorted({name for _, _, r in src for bit, name in self.REASONS.items() if r & bit})
-        return {"sm_mhz": float(np.median([s[1] for s in src])) if src else None,
-                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
-                "source": "nvml, 5 ms sampling inside the timed region"}
+        out = {"sm_mhz": float(np.median([s[1] for s in src])) if src else None,
+               "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
+               "source": "nvml, 2 ms sampling inside the timed region"}
+        if pad:
+            out["window_pad_ms"] = round(pad * 1e3, 1)
+        return out
 
 
 def barrier_sync(dist_on: bool):
