@@ -128,36 +128,40 @@ def _slice_packed(packed, a: int, b: int):
                    repeat=packed.repeat[a:b].copy())
 
 
-def test_two_ranks_one_gpu_sharded_dedup_and_fit():
+@pytest.mark.parametrize("world", [2, 8])
+def test_ranks_one_gpu_sharded_dedup_and_fit(world):
+    """world 8 maps DOOLY_MAX_PEERS = 7 peers per rank (the 8-GPU box case)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(timeout=300)
-    results = dict(q.get(timeout=5) for _ in range(2))
-    assert results == {0: "ok", 1: "ok"}, results
+        p.join(timeout=600)
+    results = dict(q.get(timeout=5) for _ in range(world))
+    assert results == {r: "ok" for r in range(world)}, results
     assert all(p.exitcode == 0 for p in procs)
 
 
-def test_bench_two_ranks_torchrun():
+@pytest.mark.parametrize("world", [2, 8])
+def test_bench_ranks_torchrun(world):
     """bench.py's N > 1 path end to end (barriers, max-over-ranks timing, the
     fit-table and digest all-gathers, replica-sharded sim) at small sizes."""
     env = dict(os.environ, DOOLY_DIST_BACKEND="gloo")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"),
-           "--gpus", "2", "--steps", "3", "--warmup", "3", "--queries", "4000000",
+           "--gpus", str(world), "--steps", "3", "--warmup", "3", "--queries", "4000000",
            "--sigs", "20000", "--points", "512", "--records", "100000",
            "--e2e-queries", "2000000", "--sim-requests", "20000", "--sim-shards", "16",
            "--csr-fit", "0"]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["n_gpus"] == world and d["value"] > 0 and d["scaling"] == "weak"
     assert d["fits"]["all_fitted"] and not d["unknown_signature_errors"]
     assert d["fits"]["allgather_path"].startswith("fused")
     assert d["dedup"]["exchange"].startswith("fused") and d["dedup"]["records_per_gpu"] == 100_000
