@@ -391,13 +391,30 @@ def max_over_ranks(v: float, dist_on: bool) -> float:
 # --------------------------------------------------------------- CPU baselines
 
 
-def _oracle_predict_worker(args):
-    kind, table, sig, x = args
+_CPU_JOBS: list = []     # set before the fork: workers inherit tables and queries
+
+
+def _oracle_predict_worker(i):
     from oracle import sim as osim
 
     t0 = time.perf_counter()
-    osim.predict(kind, table, sig, x)
+    osim.predict(*_CPU_JOBS[i])
     return time.perf_counter() - t0
+
+
+def host_regressor_table(kind: int, n_sig: int, seed: int) -> dict:
+    """Random fitted-looking regressor table for the CPU arm (oracle/sim.py
+    layout): training boxes inside the C5 grids (affine num_toks <= 32768;
+    attention prefill_toks <= 32768, batch <= 256, kv_tokens <= 2^22),
+    inv = 1/hi as the fit computes it, small positive coefficients."""
+    rng = np.random.default_rng(seed)
+    caps = [32768] if kind == AFFINE else [32768, 256, 1 << 22]
+    hi = np.stack([rng.integers(c // 4, c + 1, n_sig) for c in caps], axis=1).astype(np.uint32)
+    lo = np.minimum(hi, np.stack([rng.integers(0, 4, n_sig) for _ in caps], axis=1)).astype(np.uint32)
+    inv = 1.0 / hi.astype(np.float64)
+    p = 2 if kind == AFFINE else 10
+    coef = rng.uniform(1e-7, 1e-4, (n_sig, p))
+    return {"coef": coef, "inv": inv, "lo": lo, "hi": hi}
 
 
 def cpu_predict_baseline(tables_host, queries_host, threads: int, budget_s: float = 12.0):
@@ -406,7 +423,8 @@ def cpu_predict_baseline(tables_host, queries_host, threads: int, budget_s: floa
 
     n_total = 0
     t_total = 0.0
-    chunk = 2_000_000
+    n_all = sum(queries_host[k][0].shape[0] for k in queries_host)
+    chunk = 2_000_000 if threads <= 1 else max(250_000, -(-n_all // (4 * threads)))
     jobs = []
     for kind in (AFFINE, ATTN):
         sig, x = queries_host[kind]
@@ -423,10 +441,14 @@ def cpu_predict_baseline(tables_host, queries_host, threads: int, budget_s: floa
     else:
         import multiprocessing as mp
 
+        # the jobs (tables of C5 size and the query chunks) reach the workers
+        # through fork, so only job indices cross the pipe inside the timing
+        _CPU_JOBS[:] = jobs
         ctx = mp.get_context("fork")
         with ctx.Pool(threads) as pool:
+            pool.map(_oracle_predict_worker, range(min(threads, len(jobs))))   # warm the pool
             t0 = time.perf_counter()
-            pool.map(_oracle_predict_worker, jobs)
+            pool.map(_oracle_predict_worker, range(len(jobs)), chunksize=1)
             t_total = time.perf_counter() - t0
         n_total = sum(j[2].shape[0] for j in jobs)
     return n_total / t_total, n_total
@@ -855,18 +877,15 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import sim as osim
     sys.path.insert(0, str(ROOT / "tests"))
-    from helpers import synth_fit_data, synth_queries
+    from helpers import synth_queries
 
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     tables, qh = {}, {}
-    n_sig = 20000
     for k in (AFFINE, ATTN):
-        x, y, off = synth_fit_data(k, n_sig, 64, seed=k)
-        f = osim.fit_uniform(k, x.reshape(x.shape[0], n_sig, 64).transpose(1, 0, 2),
-                             y.reshape(n_sig, 64))
-        tables[k] = {kk: f[kk] for kk in ("coef", "inv", "lo", "hi")}
+        # regressor tables of the C5 size (sigs / 2 rows per kind, as the GPU arm
+        # serves), boxes spanning the C5 sweep grids; queries inside the boxes
+        tables[k] = host_regressor_table(k, args.sigs // 2, seed=k)
         qh[k] = synth_queries(k, tables[k], args.ref_sample // 2, seed=k + 1)
     for _ in range(args.warmup):
         cpu_predict_baseline(tables, {k: (qh[k][0][:100000], qh[k][1][:, :100000])
@@ -883,8 +902,9 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": arm_config(args),
-            "config_sample": {"workload": "C5 predict batch (bounded CPU sample)",
-                       "queries_per_step": args.ref_sample},
+            "config_sample": {"workload": "C5 predict batch (bounded CPU sample): "
+                                          f"{args.sigs // 2} regressor rows per kind",
+                              "queries_per_step": args.ref_sample},
             "cpu_baseline": {"value": value, "unit": "predictions/s", "cores": threads,
                              "kind": "port",
                              "sample": f"{args.ref_sample} queries per step, oracle/sim.py "
