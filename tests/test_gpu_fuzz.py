@@ -1,0 +1,129 @@
+"""Seeded randomized parity sweeps on the GPU: many small configurations per
+kernel family, each against the CPU oracle at the same bar as the targeted
+tests (bit-exact for the serving loop and predictions, the fit contract for
+coefficients).  The serving-loop sweep varies exactly what its exact decode
+windows depend on (arrival rate, batch cap, chunk, KV cap, windows, cached
+prompts, tensor parallelism)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import AFFINE, ATTN, rows_to_table, synth_fit_data, synth_queries, table_to_rows
+from oracle import sim as osim
+from test_gpu_kernels import PACKED, _predict_gpu, _regs, _sim_setup, _unpack_bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_sim_run_random_configs(case, dev):
+    from paper_2605_07985_b200 import _lib
+    from paper_2605_07985_b200.sim import CallTree, ShardedTrace, collect, run_sharded
+
+    rng = np.random.default_rng(1000 + case)
+    window = int(rng.choice([0, 0, 512, 4096]))
+    tp = int(rng.choice([1, 1, 2, 4]))
+    shards = int(rng.integers(1, 7))
+    n = int(rng.integers(50, 900))
+    rate = float(rng.choice([0.5, 4.0, 40.0, 400.0]))
+    chunk = int(rng.choice([256, 2048, 8192]))
+    max_batch = int(rng.choice([1, 4, 32, 256]))
+    cap = int(rng.choice([10**15, 6 * 10**9, 2 * 10**9]))
+    ta, tt, ops, ol = _sim_setup(2000 + case, window=window, tp=tp)
+    regs = _regs(ta, tt, dev)
+    arr = np.cumsum(rng.exponential(1.0 / rate, size=n))
+    pr = rng.integers(1, 6000, size=n).astype(np.uint32)
+    ou = rng.integers(1, 400, size=n).astype(np.uint32)
+    ca = np.where(rng.random(n) < 0.15, pr, 0).astype(np.uint32)
+    sc = _lib.Sched()
+    sc.chunk, sc.max_batch, sc.window = chunk, max_batch, window
+    sc.kv_bytes_per_token, sc.kv_capacity_bytes, sc.max_iterations = 131072, cap, 10**7
+    trace = ShardedTrace.from_arrays(arr, pr, ou, ca, shards, dev)
+    res = run_sharded(trace, CallTree([], ol, window), sc, regs)
+    met = collect(trace, res)
+    ref = osim.run_shards(arr.tolist(), pr.tolist(), ou.tolist(), ca.tolist(), shards, ops=ops,
+                          chunk=chunk, max_batch=max_batch, kv_bytes_per_token=131072,
+                          kv_capacity=cap, window=window, tp=tp, alpha=5e-6, beta=5e-12)
+    assert res.n_iter.cpu().numpy().tolist() == ref["n_iter"]
+    assert np.array_equal(res.clock.cpu().numpy(), np.array(ref["clock"]))
+    assert np.array_equal(met.ttft.view(np.uint64), ref["ttft"].view(np.uint64))
+    m = ~np.isnan(ref["tpot"])
+    assert np.array_equal(np.isnan(met.tpot), ~m)
+    assert np.array_equal(met.tpot[m].view(np.uint64), ref["tpot"][m].view(np.uint64))
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_predict_random_tables(case, dev):
+    """Random table sizes, query counts and misalignments; fitted, unfitted
+    (lo > hi) and clamped rows; out-of-box and out-of-range queries."""
+    rng = np.random.default_rng(3000 + case)
+    kind = [AFFINE, ATTN, PACKED][case % 3]
+    packed = kind == PACKED
+    k = ATTN if packed else kind
+    n_sig = int(rng.integers(1, 3000))
+    x, y, off = synth_fit_data(k, n_sig, 48, seed=case)
+    f = osim.fit(k, x, y, off)
+    table = {key: f[key].copy() for key in ("coef", "inv", "lo", "hi")}
+    neg = rng.random(n_sig) < 0.05
+    table["coef"][neg, 0] = -abs(table["coef"][neg, 0]) - 1.0      # clamped predictions
+    n_q = int(rng.integers(1, 200_000))
+    offset = int(rng.choice([0, 0, 1, 3]))
+    sig, xq = synth_queries(k, table, n_q, seed=case + 7, outside=0.1)
+    sig[rng.random(n_q) < 0.002] = n_sig + 5                       # unknown signatures
+    if packed:
+        unfit = np.zeros(n_sig, bool)
+    else:
+        unfit = rng.random(n_sig) < 0.03                            # unfitted rows: lo > hi
+        table["lo"][unfit] = 0xFFFFFFFF
+        table["hi"][unfit] = 0
+        table["coef"][unfit] = np.nan
+        table["inv"][unfit] = np.nan
+    rows = table_to_rows(k, table)
+    out, flags, err = _predict_gpu(k, rows, sig, xq, dev, offset, packed)
+    ref = osim.predict(k, table, sig, xq)
+    bad = np.flatnonzero(ref["bad"])
+    assert err == (int(bad[0]) if bad.size else np.iinfo(np.int64).max)
+    ok = ~ref["bad"]
+    assert np.array_equal(out[ok].view(np.uint64), ref["out"][ok].view(np.uint64))
+    assert np.isnan(out[~ok]).all()
+    nw = (n_q + 31) // 32
+    assert np.array_equal(_unpack_bits(flags[0, :nw], n_q), ref["extrap"])
+    assert np.array_equal(_unpack_bits(flags[1, :nw], n_q), ref["clamped"])
+
+
+@pytest.mark.parametrize("case", range(20))
+def test_fit_random_csr(case, dev):
+    """Random signature counts and point counts per signature, including
+    signatures below the minimum (InsufficientData status), against the oracle."""
+    from paper_2605_07985_b200.sim import fit_tables
+
+    rng = np.random.default_rng(4000 + case)
+    kind = AFFINE if case % 2 == 0 else ATTN
+    n_sig = int(rng.integers(1, 400))
+    x, y, off = synth_fit_data(kind, n_sig, int(rng.integers(12, 300)), seed=case, ragged=True)
+    counts = np.diff(off)
+    need = 4 if kind == AFFINE else 11
+    short = rng.random(n_sig) < 0.1                                 # cut to 1..need-1 points
+    new_counts = np.where(short, np.minimum(counts, rng.integers(1, need, n_sig)), counts)
+    keep = np.concatenate([np.arange(off[s], off[s] + new_counts[s]) for s in range(n_sig)])
+    x, y = np.ascontiguousarray(x[:, keep]), y[keep]
+    off = np.concatenate([[0], np.cumsum(new_counts)]).astype(np.int64)
+    ref = osim.fit(kind, x, y, off)
+    fr = fit_tables(kind, torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).to(dev),
+                    torch.from_numpy(y).to(dev), torch.from_numpy(off).to(dev))
+    torch.cuda.synchronize()
+    got = rows_to_table(kind, fr.rows())
+    st = fr.status.cpu().numpy()
+    assert np.array_equal(st, ref["status"])
+    ok = st == 0
+    assert np.array_equal(got["lo"][ok], ref["lo"][ok]) and np.array_equal(got["hi"][ok], ref["hi"][ok])
+    assert np.array_equal(got["inv"][ok], ref["inv"][ok])
+    if ok.any():
+        c, r = got["coef"][ok], ref["coef"][ok]
+        d = np.abs(c - r).max(axis=1) / np.abs(r).max(axis=1)
+        assert d.max() <= 1e-9, d.max()
+        fe, fr_ = fr.fit_err.cpu().numpy()[ok], ref["fit_err"][ok]
+        assert np.all(np.abs(fe - fr_) <= 1e-9 * fr_ + 1e-12)
