@@ -271,3 +271,37 @@ def test_taint_matches_reference_golden():
         assert "error" not in c, (c, got)
         want = c["result"]
         assert (list(got) if isinstance(got, tuple) else got) == want, (c, got)
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_runnable_sets_random_architectures(seed):
+    """Random valid architectures (GQA/MHA, interleaved or listed sliding
+    windows, MoE, tensor parallelism): the traced and resolved runnable set
+    equals the closed-form one, and the kernel multiset is conserved."""
+    rng = random.Random(seed)
+    tp = rng.choice([1, 1, 2, 4])
+    kv = tp * rng.choice([1, 2, 4, 8])
+    q = kv * rng.choice([1, 2, 4, 8])
+    d = rng.choice([64, 128, 256])
+    n_layers = rng.randint(1, 24)
+    kinds = [rng.choice([None, None, 1024, 4096]) for _ in range(n_layers)]
+    moe = None
+    if rng.random() < 0.3:
+        e = rng.choice([4, 8, 16])
+        moe = modelir.MoESpec(e, rng.randint(1, 3), tp * rng.choice([512, 1792]))
+    cfg = modelir.ModelConfig(
+        name=f"rand{seed}", hidden_dim=q * d, num_layers=n_layers, num_q_heads=q,
+        num_kv_heads=kv, head_dim=d, intermediate_size=tp * rng.choice([1024, 3584, 7168]),
+        vocab_size=tp * rng.choice([8000, 32000, 64128]), dtype_bytes=rng.choice([1, 2]),
+        max_context=rng.choice([4096, 32768]), layer_attention=tuple(kinds), moe=moe)
+    cfg.validate()
+    backend = _man("corpus12").backends[seed % 3]
+    tr = tracer.run_trace(cfg, backend, tp=tp)
+    assert not tr.registry.collisions
+    tree = opset.build_tree(tr.events)
+    got = opset.resolve(opset.prune(tree))
+    want = synthesize_entries(cfg, backend, tp)
+    assert [canonical_bytes(e) for e in got] == [canonical_bytes(e) for e in want]
+    assert [(e.repeat_count, e.kernel_symbols, e.window) for e in got] == \
+        [(e.repeat_count, e.kernel_symbols, e.window) for e in want]
+    assert opset.covered_kernel_count(got) == tree.kernel_count()
