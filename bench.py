@@ -25,7 +25,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import time
 from pathlib import Path

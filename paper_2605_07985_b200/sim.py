@@ -28,7 +28,7 @@ from .errors import (InsufficientData, LengthMismatch, NonTermination, UnknownSi
                      ValidationError, ZeroTruth)
 from .modelir import BackendSpec, HardwareSpec, ModelConfig, Request
 from .profiler import LatencyDB, _device, DeviceRecords, hash_records
-from .records import RunnableEntry, pack_entries, runnable_entries
+from .records import pack_entries, runnable_entries
 
 NEED = {_lib.KIND_AFFINE: 4, _lib.KIND_ATTN: 11}          # max(4, p + 1), App. A.8
 FEATURE_NAMES = {_lib.KIND_AFFINE: ("num_toks",),

@@ -31,7 +31,7 @@ from typing import Iterable, Optional, Sequence
 
 import numpy as np
 
-from .errors import DuplicateKey, StoreUnavailable
+from .errors import StoreUnavailable
 
 STORE_VERSION = 1
 
