@@ -734,17 +734,26 @@ def run_ours(args):
         # fused into the hash kernel's epilogue over peer memory when available
         # (else an NCCL all-gather) — then a global first-occurrence resolve on
         # every rank (dist.dedup_sharded)
-        pdig = ddist.PeerDigests(n_total, dev) if peer is not None else None
+        # From 4 ranks on, the owner-routed form (all-to-all of digests to their
+        # owners and of the results back, dist.dedup_routed) keeps each rank's
+        # resolve at ~records_per_gpu keys instead of the whole list.
+        xchg = os.environ.get("DOOLY_DEDUP_EXCHANGE", "route" if world >= 4 else "gather")
+        routed = dist_on and xchg == "route"
+        pdig = ddist.PeerDigests(n_total, dev) if peer is not None and not routed else None
         for _ in range(d_steps):
             e0.record(stream)
-            if pdig is not None:
-                full = pdig.hash(recs, rank * recs.n)
+            if routed:
+                r = ddist.dedup_routed(recs, n_total, None, ws)
+                e1.record(stream)
             else:
-                hash_records(recs, dig)
-            e1.record(stream)
-            if pdig is None:
-                full = ddist.all_gather_rows(dig, n_total) if dist_on else dig
-            r = dedup_digests(full, None, ws, sync=False)
+                if pdig is not None:
+                    full = pdig.hash(recs, rank * recs.n)
+                else:
+                    hash_records(recs, dig)
+                e1.record(stream)
+                if pdig is None:
+                    full = ddist.all_gather_rows(dig, n_total) if dist_on else dig
+                r = dedup_digests(full, None, ws, sync=False)
             e2.record(stream)
             torch.cuda.synchronize()
             sha_ms += e0.elapsed_time(e1)
@@ -753,11 +762,19 @@ def run_ours(args):
         tot_ms = max_over_ranks(tot_ms / d_steps, dist_on)
         if pdig is not None:
             pdig.check()
-        n_unique = int(dedup_digests(full, None, ws).n_unique)
+        n_unique = int(r.n_unique) if routed else int(dedup_digests(full, None, ws).n_unique)
+        if routed:   # e0 -> e1 spans the whole routed dedup; time the hash alone once
+            e0.record(stream)
+            hash_records(recs, dig)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            sha_ms = e0.elapsed_time(e1) * d_steps
         msg_len = 8 + 4 + 6 + 4 + 3 * 12 + 4 + 2 * (4 + 16)  # approx canonical length
         dedup = {"value": world * recs.n / (tot_ms / 1e3), "unit": "records/s",
                  "records_per_gpu": recs.n, "unique": n_unique, "ms_per_step": tot_ms,
                  "exchange": None if not dist_on else (
+                     "owner-routed: all-to-all of (digest, index) to the owners, resolve "
+                     "there, all-to-all of the results back" if routed else
                      "fused: digests stored into every rank by the hash kernel, global resolve"
                      if pdig is not None else "NCCL all-gather of 32-B digests, global resolve"),
                  "sha_ms": sha_ms / d_steps,

@@ -123,6 +123,89 @@ def dedup_sharded(recs_local, n_total: int, db_digests: Optional[torch.Tensor] =
                        res.in_db[a:b], res.n_unique)
 
 
+def owner_of(digests: torch.Tensor, size: int) -> torch.Tensor:
+    """Owning rank of each 32-byte digest: the last 8 bytes modulo the world
+    size (the dedup hash table probes the first bytes, so an owner's keys
+    still spread over its whole table)."""
+    tail = digests[:, 24:32].contiguous().view(torch.int64).reshape(-1)
+    return torch.remainder(tail & 0x7FFFFFFFFFFFFFFF, size)
+
+
+def _all_to_all(t: torch.Tensor, send: list, recv: list, group=None) -> torch.Tensor:
+    """all_to_all_single on dim 0 with per-rank split sizes (NCCL on the
+    device; gloo through host memory)."""
+    out_shape = (sum(recv),) + tuple(t.shape[1:])
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty(out_shape, dtype=t.dtype, device=t.device)
+        dist.all_to_all_single(out, t.contiguous(), recv, send, group=group)
+        return out
+    h = t.contiguous().cpu()
+    out = torch.empty(out_shape, dtype=t.dtype)
+    dist.all_to_all_single(out, h, recv, send, group=group)
+    return out.to(t.device)
+
+
+def dedup_routed(recs_local, n_total: int, db_digests: Optional[torch.Tensor] = None,
+                 workspace=None, group=None):
+    """Multi-GPU dedup with owner routing: each digest goes to the
+    rank that owns it, so every rank resolves ~n_total / world keys instead of
+    all of them (the all-gather form resolves the whole list on every rank).
+
+      1. hash the local records (K1a);
+      2. all-to-all of (digest, global index) to the owners; a rank's bucket
+         keeps its records' order and ranks send in rank order, so what an
+         owner receives is in global order;
+      3. the owner resolves its keys (K1b) — every copy of a digest is there,
+         so first occurrence, DB membership and is_new are exact;
+      4. uid = rank of the first occurrence among ALL first occurrences: the
+         owners' sorted first-occurrence indices are all-gathered and each
+         owner counts the smaller ones (searchsorted);
+      5. all-to-all of (first, uid, flags) back to the records' home ranks.
+    Bit-identical to the single-rank dedup of the whole list."""
+    from .profiler import DedupResult, dedup_digests, hash_records
+
+    rank, size = world()
+    dev = recs_local.words.device
+    a, _ = shard_range(n_total, rank, size)
+    dig = hash_records(recs_local)
+    n_loc = dig.shape[0]
+    own = owner_of(dig, size) if n_loc else torch.empty(0, dtype=torch.int64, device=dev)
+    order = torch.sort(own, stable=True).indices
+    send = torch.bincount(own, minlength=size)
+    recv = _all_to_all(send, [1] * size, [1] * size, group)
+    send_l, recv_l = send.tolist(), recv.tolist()
+    gidx = torch.arange(a, a + n_loc, dtype=torch.int64, device=dev)
+    payload = torch.cat([dig[order].view(torch.int64), gidx[order, None]], dim=1)   # (n, 5) i64
+    got = _all_to_all(payload, send_l, recv_l, group)
+    r_dig = got[:, :4].contiguous().view(torch.uint8).reshape(-1, 32)
+    r_gidx = got[:, 4].contiguous()
+    if db_digests is not None and db_digests.shape[0]:
+        db_digests = db_digests[owner_of(db_digests, size) == rank]
+    res = dedup_digests(r_dig, db_digests, workspace, sync=False)
+    m = r_dig.shape[0]
+    # first occurrences of this owner, in global order (r_gidx is increasing)
+    firsts = r_gidx[res.first == torch.arange(m, device=dev)] if m else r_gidx[:0]
+    counts = torch.tensor([firsts.numel()], dtype=torch.int64, device=dev)
+    all_counts = _gather_cat(counts, size, group)
+    per = int(all_counts.max().item())
+    pad = torch.full((per,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
+    pad[: firsts.numel()] = firsts
+    all_firsts = _gather_cat(pad, size, group)
+    all_firsts = torch.sort(all_firsts).values[: int(all_counts.sum().item())]
+    rank_of_first = torch.searchsorted(all_firsts, firsts)
+    first_g = r_gidx[res.first] if m else r_gidx[:0]
+    uid_g = rank_of_first[res.uid.long()] if m else r_gidx[:0]
+    flags = res.is_new.long() | (res.in_db.long() << 1)
+    back = torch.stack([first_g, uid_g, flags], dim=1) if m else \
+        torch.empty((0, 3), dtype=torch.int64, device=dev)
+    ret = _all_to_all(back, recv_l, send_l, group)
+    out = torch.empty_like(ret)
+    out[order] = ret
+    return DedupResult(dig, out[:, 0].contiguous(), out[:, 1].to(torch.int32),
+                       (out[:, 2] & 1).to(torch.uint8), ((out[:, 2] >> 1) & 1).to(torch.uint8),
+                       int(all_counts.sum().item()))
+
+
 def gather_requests(values: torch.Tensor, group=None) -> torch.Tensor:
     """All-gather equally sized per-rank vectors (e.g. padded TTFT blocks)."""
     rank, size = world()

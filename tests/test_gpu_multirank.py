@@ -62,6 +62,18 @@ def _worker(rank: int, world: int, port: int, q) -> None:
         for name in ("first", "uid", "is_new", "in_db"):
             assert torch.equal(getattr(got, name), getattr(whole, name)[a:b]), name
         assert torch.equal(got.digests, whole.digests[a:b])
+        # owner-routed dedup (all-to-all to the digest owners and back)
+        got = ddist.dedup_routed(DeviceRecords.from_packed(sl, dev), n_total)
+        assert got.n_unique == whole.n_unique
+        for name in ("first", "uid", "is_new", "in_db"):
+            assert torch.equal(getattr(got, name), getattr(whole, name)[a:b]), name
+        assert torch.equal(got.digests, whole.digests[a:b])
+        db = whole.digests[::97].clone()                      # some keys already in the DB
+        whole_db = dedup_packed(DeviceRecords.from_packed(packed, dev), db)
+        got = ddist.dedup_routed(DeviceRecords.from_packed(sl, dev), n_total, db)
+        assert got.n_unique == whole_db.n_unique
+        for name in ("first", "uid", "is_new", "in_db"):
+            assert torch.equal(getattr(got, name), getattr(whole_db, name)[a:b]), name
         # fused hash + all-gather (digests stored into both ranks by the hash kernel)
         pd = ddist.PeerDigests(n_total, dev)
         for _ in range(2):
@@ -164,5 +176,6 @@ def test_bench_ranks_torchrun(world):
     assert d["n_gpus"] == world and d["value"] > 0 and d["scaling"] == "weak"
     assert d["fits"]["all_fitted"] and not d["unknown_signature_errors"]
     assert d["fits"]["allgather_path"].startswith("fused")
-    assert d["dedup"]["exchange"].startswith("fused") and d["dedup"]["records_per_gpu"] == 100_000
+    assert d["dedup"]["exchange"].startswith("fused" if world < 4 else "owner-routed")
+    assert d["dedup"]["records_per_gpu"] == 100_000 and d["dedup"]["unique"] > 0
     assert d["sim"]["all_ok"] and d["sim"]["requests"] == 20_000
