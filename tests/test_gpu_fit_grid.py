@@ -135,7 +135,9 @@ def test_fit_grid_rank_deficient_drops_columns(dev):
 @pytest.mark.parametrize("kind", [AFFINE, ATTN])
 def test_fit_grid_db_and_warp_bit_identical(kind, dev, monkeypatch):
     """The double-buffered kernel runs the warp kernel's per-lane arithmetic in
-    the same order, so tables, fit_err and statuses are bit-identical."""
+    the same order (the warp kernel's grouped attention passes switched off),
+    so tables, fit_err and statuses are bit-identical."""
+    monkeypatch.setenv("DOOLY_FIT_GRID_FACTOR", "0")
     rng = np.random.default_rng(29 + kind)
     x = _grid(kind, 4096, rng)[:, :4096]
     y = _ys(kind, x, 2000, rng)
@@ -146,3 +148,29 @@ def test_fit_grid_db_and_warp_bit_identical(kind, dev, monkeypatch):
     a, b = out["warp"], out["db"]
     assert torch.equal(a.table, b.table) and torch.equal(a.status, b.status)
     assert torch.equal(a.fit_err.view(torch.int64), b.fit_err.view(torch.int64))
+
+
+def test_fit_grid_grouped_attention_passes(dev, monkeypatch):
+    """Sweep grids with the kv axis innermost take the grouped attention passes
+    (prefill_toks and batch factored out of each aligned 4-point group); a
+    shuffled grid falls back to the per-point passes.  Both meet the oracle
+    contract and agree with each other."""
+    rng = np.random.default_rng(41)
+    x = _grid(ATTN, 4096, rng)[:, :4096]
+    y = _ys(ATTN, x, 300, rng)
+    ref, _, _ = _oracle(ATTN, x, y)
+    grouped = _fit_grid_gpu(ATTN, x, y, dev)
+    monkeypatch.setenv("DOOLY_FIT_GRID_FACTOR", "0")
+    plain = _fit_grid_gpu(ATTN, x, y, dev)
+    monkeypatch.delenv("DOOLY_FIT_GRID_FACTOR")
+    perm = rng.permutation(x.shape[1])
+    shuffled = _fit_grid_gpu(ATTN, np.ascontiguousarray(x[:, perm]), np.ascontiguousarray(y[:, perm]),
+                             dev)
+    for fr in (grouped, plain, shuffled):
+        got = rows_to_table(ATTN, fr.rows())
+        dc = np.abs(got["coef"] - ref["coef"]).max(axis=1) / np.abs(ref["coef"]).max(axis=1)
+        assert dc.max() <= COEF_TOL, dc.max()
+        fe = fr.fit_err.cpu().numpy()
+        assert np.max(np.abs(fe - ref["fit_err"]) / ref["fit_err"]) <= 1e-8
+    a, b = (rows_to_table(ATTN, f.rows())["coef"] for f in (grouped, plain))
+    assert np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)) <= 1e-12

@@ -31,6 +31,8 @@ def main() -> None:
     ap.add_argument("--kinds", default="0,1")
     ap.add_argument("--vs-warp", action="store_true",
                     help="check the table bit-identical to DOOLY_FIT_GRID_KERNEL=warp")
+    ap.add_argument("--vs-unfactored", action="store_true",
+                    help="max coefficient difference against DOOLY_FIT_GRID_FACTOR=0")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     for kind in [int(k) for k in a.kinds.split(",")]:
@@ -61,6 +63,18 @@ def main() -> None:
                 fw.fit_err.view(torch.int64), fr.fit_err.view(torch.int64)) and torch.equal(
                 fw.status, fr.status))
             del fw
+        if a.vs_unfactored:
+            os.environ["DOOLY_FIT_GRID_FACTOR"] = "0"
+            fu = fit_grid(kind, x, y)
+            torch.cuda.synchronize()
+            del os.environ["DOOLY_FIT_GRID_FACTOR"]
+            nc = 2 if kind == 0 else 10
+            ga, gu = fr.table.view(torch.float64), fu.table.view(torch.float64)
+            d = (ga[:, :nc] - gu[:, :nc]).abs().amax(1) / gu[:, :nc].abs().amax(1)
+            line["max_coef_rel_diff_vs_unfactored"] = float(d.max().item())
+            line["fit_err_max_rel_diff"] = float(((fr.fit_err - fu.fit_err).abs() /
+                                                  fu.fit_err.abs()).max().item())
+            del fu
         if a.csr:
             xr = x.repeat(1, a.sigs)
             off = torch.arange(a.sigs + 1, dtype=torch.int64, device=dev) * a.points
