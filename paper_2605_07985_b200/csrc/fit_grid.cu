@@ -674,6 +674,50 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
   }
 }
 
+// Grouped attention steps (the 4 points of a lane share f1 = u1 and f2 = u2,
+// prep's grp4): pass 1 as kv sums times the group's f1/f2 monomials (7.25 FP64
+// per point instead of 13), pass 2 with the f1/f2 terms folded per group into
+// p = A + f3 (B + c6 f3) (8.75 instead of 14).
+__device__ __forceinline__ void grid_g1_step(const double4& yv, const double4& f3, double u1,
+                                             double u2, double* acc) {
+  const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
+  const double ff[4] = {f3.x, f3.y, f3.z, f3.w};
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double y3 = yy[j] * ff[j];
+    s0 += yy[j];
+    s1 += y3;
+    s2 = fma(y3, ff[j], s2);
+  }
+  const double u11 = u1 * u1, u22 = u2 * u2, u12 = u1 * u2;
+  acc[0] += s0;
+  acc[1] = fma(u1, s0, acc[1]);
+  acc[2] = fma(u2, s0, acc[2]);
+  acc[3] += s1;
+  acc[4] = fma(u11, s0, acc[4]);
+  acc[5] = fma(u22, s0, acc[5]);
+  acc[6] += s2;
+  acc[7] = fma(u12, s0, acc[7]);
+  acc[8] = fma(u1, s1, acc[8]);
+  acc[9] = fma(u2, s1, acc[9]);
+}
+
+__device__ __forceinline__ void grid_g2_step(const double4& yv, const double4& f3, double u1,
+                                             double u2, const double* c, double& err) {
+  const double t1 = fma(c[7], u2, fma(c[4], u1, c[1]));
+  const double t2 = fma(c[5], u2, c[2]);
+  const double A = fma(u1, t1, fma(u2, t2, c[0]));
+  const double B = fma(c[9], u2, fma(c[8], u1, c[3]));
+  const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
+  const double ff[4] = {f3.x, f3.y, f3.z, f3.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double pr = fmax(fma(ff[j], fma(c[6], ff[j], B), A), DOOLY_CLAMP_FLOOR);
+    err = fma(fabs(pr - yy[j]), g_rcp1(yy[j]), err);
+  }
+}
+
 // ---- warp-per-signature variant (no shared-memory stage, no CTA barriers).
 // One warp owns one signature at a time: pass 1 streams its y row from HBM
 // tagged L2::evict_last, the warp reduces b with shuffles, lanes 0..NC-1 form
@@ -828,29 +872,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
       // feature plane read per step instead of three.  Pass 2 likewise folds
       // the f1/f2 terms per group: 8.75 FP64 per point instead of 14.
       auto fstep = [&](const double4& yv, int pp) {
-        const double4 f3 = g_ld_f(fpl + 2 * n + pp);
-        const double u1 = __ldg(fpl + pp), u2 = __ldg(fpl + n + pp);
-        const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
-        const double ff[4] = {f3.x, f3.y, f3.z, f3.w};
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double y3 = yy[j] * ff[j];
-          s0 += yy[j];
-          s1 += y3;
-          s2 = fma(y3, ff[j], s2);
-        }
-        const double u11 = u1 * u1, u22 = u2 * u2, u12 = u1 * u2;
-        acc[0] += s0;
-        acc[1] = fma(u1, s0, acc[1]);
-        acc[2] = fma(u2, s0, acc[2]);
-        acc[3] += s1;
-        acc[4] = fma(u11, s0, acc[4]);
-        acc[5] = fma(u22, s0, acc[5]);
-        acc[6] += s2;
-        acc[7] = fma(u12, s0, acc[7]);
-        acc[8] = fma(u1, s1, acc[8]);
-        acc[9] = fma(u2, s1, acc[9]);
+        grid_g1_step(yv, g_ld_f(fpl + 2 * n + pp), __ldg(fpl + pp), __ldg(fpl + n + pp), acc);
       };
       int p = 4 * lane;
       constexpr int YS = 8;
@@ -879,19 +901,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     if (factored) {
       // per group: p = A + f3 (B + c6 f3) with A, B the group's f1/f2 terms
       auto fstep2 = [&](const double4& yv, int pp) {
-        const double4 f3 = g_ld_f(fpl + 2 * n + pp);
-        const double u1 = __ldg(fpl + pp), u2 = __ldg(fpl + n + pp);
-        const double t1 = fma(c[7], u2, fma(c[4], u1, c[1]));
-        const double t2 = fma(c[5], u2, c[2]);
-        const double A = fma(u1, t1, fma(u2, t2, c[0]));
-        const double B = fma(c[9], u2, fma(c[8], u1, c[3]));
-        const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
-        const double ff[4] = {f3.x, f3.y, f3.z, f3.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double pr = fmax(fma(ff[j], fma(c[6], ff[j], B), A), DOOLY_CLAMP_FLOOR);
-          err = fma(fabs(pr - yy[j]), g_rcp1(yy[j]), err);
-        }
+        grid_g2_step(yv, g_ld_f(fpl + 2 * n + pp), __ldg(fpl + pp), __ldg(fpl + n + pp), c, err);
       };
       int p = 4 * lane;
       constexpr int YS = 8;
@@ -961,7 +971,7 @@ __device__ __forceinline__ void grid_p2_step(const double4& yv, const double4* f
 // Register double-buffered sweep (n % (128 * YS) == 0): the loads of batch
 // k + 1 (YS steps of y per lane) are in flight while batch k is evaluated, so
 // a lane always has between YS and 2 YS steps outstanding.
-template <int KIND, int YS, bool P1>
+template <int KIND, int YS, bool P1, bool GROUPED = false>
 __device__ __forceinline__ void grid_sweep_db(const double* __restrict__ fpl, int n, int lane,
                                               const double* yr, const double* c, double* acc,
                                               double& err) {
@@ -975,13 +985,23 @@ __device__ __forceinline__ void grid_sweep_db(const double* __restrict__ fpl, in
   auto eval = [&](const double4* v, int p) {
 #pragma unroll
     for (int t = 0; t < YS; ++t) {
-      double4 fv[P];
+      const int q = p + 128 * t;
+      if constexpr (GROUPED) {
+        const double4 f3 = g_ld_f(fpl + 2 * n + q);
+        const double u1 = __ldg(fpl + q), u2 = __ldg(fpl + n + q);
+        if (P1)
+          grid_g1_step(v[t], f3, u1, u2, acc);
+        else
+          grid_g2_step(v[t], f3, u1, u2, c, err);
+      } else {
+        double4 fv[P];
 #pragma unroll
-      for (int k = 0; k < P; ++k) fv[k] = g_ld_f(fpl + k * n + p + 128 * t);
-      if (P1)
-        grid_p1_step<KIND>(v[t], fv, acc);
-      else
-        grid_p2_step<KIND>(v[t], fv, c, err);
+        for (int k = 0; k < P; ++k) fv[k] = g_ld_f(fpl + k * n + q);
+        if (P1)
+          grid_p1_step<KIND>(v[t], fv, acc);
+        else
+          grid_p2_step<KIND>(v[t], fv, c, err);
+      }
     }
   };
   int p = 4 * lane;
@@ -999,7 +1019,7 @@ template <int KIND, int YS>
 __global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
     const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
-    uint8_t* __restrict__ status, const dooly_grid_peers pe) {
+    uint8_t* __restrict__ status, const dooly_grid_peers pe, int allow_factor) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC;
   __shared__ double sW[NC][NC];
@@ -1027,7 +1047,10 @@ __global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
     double err = 0.0;
 #pragma unroll
     for (int k = 0; k < NC; ++k) acc[k] = 0.0;
-    grid_sweep_db<KIND, YS, true>(fpl, n, lane, ys, c, acc, err);
+    if (KIND == DOOLY_KIND_ATTN && allow_factor && gf->grp4 != 0)
+      grid_sweep_db<KIND, YS, true, KIND == DOOLY_KIND_ATTN>(fpl, n, lane, ys, c, acc, err);
+    else
+      grid_sweep_db<KIND, YS, true>(fpl, n, lane, ys, c, acc, err);
 #pragma unroll
     for (int k = 0; k < NC; ++k) acc[k] = g_warp_sum(acc[k]);
     double cj = 0.0;
@@ -1037,7 +1060,10 @@ __global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
     }
 #pragma unroll
     for (int k = 0; k < NC; ++k) c[k] = __shfl_sync(0xFFFFFFFFu, cj, k);
-    grid_sweep_db<KIND, YS, false>(fpl, n, lane, ys, c, acc, err);
+    if (KIND == DOOLY_KIND_ATTN && allow_factor && gf->grp4 != 0)
+      grid_sweep_db<KIND, YS, false, KIND == DOOLY_KIND_ATTN>(fpl, n, lane, ys, c, acc, err);
+    else
+      grid_sweep_db<KIND, YS, false>(fpl, n, lane, ys, c, acc, err);
     err = g_warp_sum(err);
     if (lane == 0)
       emit_row<KIND>(pe, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
@@ -1059,6 +1085,8 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   if (n_sig == 0) return cudaSuccess;
   // "db" (default for affine) | "warp" (default for attention) | "stage" | "plain"
   const char* which = getenv("DOOLY_FIT_GRID_KERNEL");
+  const char* fac = getenv("DOOLY_FIT_GRID_FACTOR");   // "0": per-point attention passes
+  const int allow_factor = fac == nullptr || fac[0] != '0';
   const bool aligned = n_pts < (1ll << 30) && (uintptr_t)y % 32 == 0 && (uintptr_t)ws % 32 == 0;
   // warps in flight x row bytes must stay well inside L2 so pass 2 re-reads hit
   const int warps_per_sm =
@@ -1072,15 +1100,14 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   if (want_db && aligned && n_pts % 256 == 0) {
     auto kern = n_pts % 512 == 0 ? fit_grid_db_kernel<KIND, 4> : fit_grid_db_kernel<KIND, 2>;
     kern<<<(unsigned)warp_blocks, 256, 0, stream>>>(fpl, n_pts, y, n_sig, gf, table, fit_err,
-                                                    status, pe);
+                                                    status, pe, allow_factor);
     *launches += 1;
     return cudaGetLastError();
   }
   const bool want_warp = which == nullptr || which[0] == 'w' || which[0] == 'd';
   if (want_warp && n_pts % 4 == 0 && aligned) {
-    const char* fac = getenv("DOOLY_FIT_GRID_FACTOR");   // "0" disables the factored pass 1
     fit_grid_warp_kernel<KIND><<<(unsigned)warp_blocks, 256, 0, stream>>>(
-        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, fac == nullptr || fac[0] != '0');
+        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, allow_factor);
     *launches += 1;
     return cudaGetLastError();
   }

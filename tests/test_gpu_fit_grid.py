@@ -133,11 +133,12 @@ def test_fit_grid_rank_deficient_drops_columns(dev):
 
 
 @pytest.mark.parametrize("kind", [AFFINE, ATTN])
-def test_fit_grid_db_and_warp_bit_identical(kind, dev, monkeypatch):
+@pytest.mark.parametrize("factor", ["0", "1"])
+def test_fit_grid_db_and_warp_bit_identical(kind, factor, dev, monkeypatch):
     """The double-buffered kernel runs the warp kernel's per-lane arithmetic in
-    the same order (the warp kernel's grouped attention passes switched off),
-    so tables, fit_err and statuses are bit-identical."""
-    monkeypatch.setenv("DOOLY_FIT_GRID_FACTOR", "0")
+    the same order (per-point or grouped attention passes alike), so tables,
+    fit_err and statuses are bit-identical."""
+    monkeypatch.setenv("DOOLY_FIT_GRID_FACTOR", factor)
     rng = np.random.default_rng(29 + kind)
     x = _grid(kind, 4096, rng)[:, :4096]
     y = _ys(kind, x, 2000, rng)
