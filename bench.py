@@ -38,7 +38,8 @@ AFFINE, ATTN = 0, 1
 BYTES_PER_QUERY = {AFFINE: 4 + 4 + 8 + 0.25, ATTN: 4 + 12 + 8 + 0.25}   # sig + x + out + 2 flag bits
 BYTES_PER_POINT = {AFFINE: 4 + 8, ATTN: 12 + 8}                          # x u32 planes + y f64
 BYTES_PER_GRID_POINT = 8                     # shared grid: y f64 per point (x counted once per kind)
-FP64_PER_ATTN_POINT = 27
+FP64_PER_ATTN_POINT = 27          # per-point passes (13 pass 1 + 14 pass 2)
+FP64_PER_ATTN_POINT_GROUPED = 16  # grouped passes: 7.25 + 8.75 (4-point groups share f1, f2)
 SHA_ALU_PER_BLOCK = 48 * 18 + 16 * 10          # SASS count, sha256_compress
 ALU_PEAK_TINSTR = 64 * 148 * 1.965e9 / 1e12       # ALU pipe lanes/clk/SM x SMs x clock
 FP64_PEAK_TINSTR = 64 * 148 * 1.965e9 / 1e12   # 18.6 T DFMA-class instr/s
@@ -558,6 +559,10 @@ def run_ours(args):
             peer[k].check()
             status_ok &= int((peer[k].status != 0).sum().item()) == 0
     fit_bytes = sum(n_sig[k] * n_pts[k] * BYTES_PER_GRID_POINT for k in (AFFINE, ATTN))
+    xa = fit_in[ATTN][0][:2].reshape(2, -1, 4) if n_pts[ATTN] % 4 == 0 else None
+    grouped = xa is not None and bool((xa == xa[:, :, :1]).all().item()) and \
+        os.environ.get("DOOLY_FIT_GRID_FACTOR", "1") != "0"
+    fp64_attn = FP64_PER_ATTN_POINT_GROUPED if grouped else FP64_PER_ATTN_POINT
     fit_dev_ms = sum(fit_ms.values()) / fit_steps
     fits = {
         "value": world * args.sigs / (fit_total_ms / 1e3), "unit": "fits/s",
@@ -577,15 +582,17 @@ def run_ours(args):
                      "alg_bytes_per_point": BYTES_PER_GRID_POINT,
                      "note": "y crosses HBM once (8 B/point); the attention kind is FP64-bound, "
                              "see fp64_attention and DESIGN.md"},
-        # attention kind against the FP64 pipe: 27 FP64 instructions per point and
-        # signature (pass 1: 3 mul + 4 add + 6 fma; pass 2: 9-fma Horner, clamp,
-        # subtract, 1-Newton reciprocal, fma), 64 per clock per SM nominal
+        # FP64 instructions per attention point: per-point passes 27 (pass 1:
+        # 3 mul + 4 add + 6 fma; pass 2: 9-fma Horner, clamp, subtract, 1-Newton
+        # reciprocal, fma), grouped passes 16; 64 per clock per SM nominal
         "fp64_attention": {
-            "bound": "fp64", "instr_per_point": FP64_PER_ATTN_POINT,
-            "achieved": n_sig[ATTN] * n_pts[ATTN] * FP64_PER_ATTN_POINT
+            "bound": "fp64", "instr_per_point": fp64_attn,
+            "passes": "grouped (aligned 4-point groups share prefill_toks and batch)"
+            if fp64_attn == FP64_PER_ATTN_POINT_GROUPED else "per-point",
+            "achieved": n_sig[ATTN] * n_pts[ATTN] * fp64_attn
             / (fit_ms[ATTN] / fit_steps / 1e3) / 1e12,
             "peak": FP64_PEAK_TINSTR, "unit": "T FP64 instr/s",
-            "frac": n_sig[ATTN] * n_pts[ATTN] * FP64_PER_ATTN_POINT
+            "frac": n_sig[ATTN] * n_pts[ATTN] * fp64_attn
             / (fit_ms[ATTN] / fit_steps / 1e3) / 1e12 / FP64_PEAK_TINSTR,
             "peak_source": "nominal 64 DFMA/clk/SM x 148 SMs x 1965 MHz (tools/fp64_probe.py "
                            "measures DFMA at 34 TFLOP/s = 17 T instr/s)"},

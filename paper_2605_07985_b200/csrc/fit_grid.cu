@@ -204,6 +204,13 @@ __global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __re
 #pragma unroll
     for (int k = 0; k < P; ++k)
       fplanes[k * n_pts + p] = g_scale(x[k * n_pts + p], inv[k], -4503599627370496.0 * inv[k]);
+  if (KIND == DOOLY_KIND_ATTN && n_pts % 4 == 0) {   // 16-B aligned only then
+    // group plane for the grouped passes: (f1, f2) of each aligned 4-point group
+    double2* gpl = reinterpret_cast<double2*>(fplanes + 3 * n_pts);
+    for (int64_t g = tid; g < n_pts / 4; g += kGT)
+      gpl[g] = make_double2(g_scale(x[4 * g], inv[0], -4503599627370496.0 * inv[0]),
+                            g_scale(x[n_pts + 4 * g], inv[1], -4503599627370496.0 * inv[1]));
+  }
   double acc[NT];
 #pragma unroll
   for (int i = 0; i < NT; ++i) acc[i] = 0.0;
@@ -872,7 +879,8 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
       // feature plane read per step instead of three.  Pass 2 likewise folds
       // the f1/f2 terms per group: 8.75 FP64 per point instead of 14.
       auto fstep = [&](const double4& yv, int pp) {
-        grid_g1_step(yv, g_ld_f(fpl + 2 * n + pp), __ldg(fpl + pp), __ldg(fpl + n + pp), acc);
+        const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
+        grid_g1_step(yv, g_ld_f(fpl + 2 * n + pp), u.x, u.y, acc);
       };
       int p = 4 * lane;
       constexpr int YS = 8;
@@ -901,7 +909,8 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     if (factored) {
       // per group: p = A + f3 (B + c6 f3) with A, B the group's f1/f2 terms
       auto fstep2 = [&](const double4& yv, int pp) {
-        grid_g2_step(yv, g_ld_f(fpl + 2 * n + pp), __ldg(fpl + pp), __ldg(fpl + n + pp), c, err);
+        const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
+        grid_g2_step(yv, g_ld_f(fpl + 2 * n + pp), u.x, u.y, c, err);
       };
       int p = 4 * lane;
       constexpr int YS = 8;
@@ -988,7 +997,8 @@ __device__ __forceinline__ void grid_sweep_db(const double* __restrict__ fpl, in
       const int q = p + 128 * t;
       if constexpr (GROUPED) {
         const double4 f3 = g_ld_f(fpl + 2 * n + q);
-        const double u1 = __ldg(fpl + q), u2 = __ldg(fpl + n + q);
+        const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (q >> 2));
+        const double u1 = u.x, u2 = u.y;
         if (P1)
           grid_g1_step(v[t], f3, u1, u2, acc);
         else
@@ -1138,10 +1148,13 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
 }
 
 // Workspace: the GridFactor, then the scaled feature planes f_k(p) = RN(x_k(p) * inv_k)
-// (P x n_pts f64) that the warp kernel reads instead of converting x per point.
+// (P x n_pts f64) that the warp kernel reads instead of converting x per point,
+// then (attention) the (f1, f2) plane of the aligned 4-point groups.
 size_t fit_grid_workspace_size(int kind, int64_t n_pts) {
   const int P = kind == DOOLY_KIND_AFFINE ? 1 : 3;
-  return grid_factor_bytes() + (size_t)P * (size_t)(n_pts > 0 ? n_pts : 0) * 8;
+  const size_t n = (size_t)(n_pts > 0 ? n_pts : 0);
+  // attention: + the (f1, f2) group plane of the grouped passes
+  return grid_factor_bytes() + (size_t)P * n * 8 + (kind == DOOLY_KIND_AFFINE ? 0 : (n / 4) * 16);
 }
 
 cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,

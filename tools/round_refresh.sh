@@ -6,7 +6,10 @@ timeout 900 python bench.py --impl reference > gpurun_out/rr_ref.json 2> gpurun_
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv -k regex:'predict_vec|predict_scalar|fit_|sha256|dedup_|sim_run|iter_eval|attn_pack|profile_fit|peer_' \
     --log-file gpurun_out/rr_launches.csv python bench.py --steps 2 --warmup 1 \
     > gpurun_out/rr_launches_bench.log 2>&1
-# full capture of the affine grid-fit kernel (DRAM bytes per point)
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:fit_grid_db -c 1 \
-    -o gpurun_out/rr_fgdb -f python tools/fit_grid_bench.py --sigs 200000 --kinds 0 --reps 1 \
-    > gpurun_out/rr_fgdb.log 2>&1
+# full captures: the attention grid fit (grouped passes) and the CSR moments kernel
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:fit_grid_warp -c 1 \
+    -o gpurun_out/rr_fgw -f python tools/fit_grid_bench.py --sigs 200000 --kinds 1 --reps 1 \
+    > gpurun_out/rr_fgw.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:fit_moments_attn -c 1 \
+    -o gpurun_out/rr_mom -f python tools/fit_grid_bench.py --sigs 60000 --kinds 1 --reps 1 --csr \
+    > gpurun_out/rr_mom.log 2>&1
