@@ -509,16 +509,22 @@ def run_ours(args):
             if rank == 0:
                 print(f"fused all-gather unavailable ({exc}); using NCCL", file=sys.stderr)
 
+    # the serving form of the attention table (96-B rows) is part of the fit
+    # output: written by the fit epilogue itself on one rank (fit_grid_packed),
+    # by dooly_attn_pack after the fused all-gather otherwise
+    packed96 = torch.empty((n_sig[ATTN] + 1, 96), dtype=torch.uint8, device=dev) \
+        if peer is None else None
+
     def do_fit(k):
         if peer is None:
-            return fit_grid(k, fit_in[k][0], fit_in[k][1], fit_out.get(k))
+            return fit_grid(k, fit_in[k][0], fit_in[k][1], fit_out.get(k),
+                            packed=packed96 if k == ATTN else None)
         r0 = rank * n_sig[k]
         pt = peer[k].fit_grid(fit_in[k][0], fit_in[k][1], r0)
         sl = slice(r0, r0 + n_sig[k])
         return FitResult(k, pt.table[sl], pt.fit_err[sl], pt.status[sl])
 
     fit_out = {}
-    packed96 = None
     for _ in range(max(1, args.warmup)):
         for k in (AFFINE, ATTN):
             fit_out[k] = do_fit(k)
@@ -538,7 +544,7 @@ def run_ours(args):
         for k in (AFFINE, ATTN):
             ev[k][0].record(stream)
             fit_out[k] = do_fit(k)
-            if k == ATTN:   # serving form of the attention table (96-B rows), part of the fit output
+            if k == ATTN and peer is not None:   # serving form (96-B rows) of this rank's rows
                 packed96 = pack_attn(fit_out[k].table, packed96, check=False)
             ev[k][1].record(stream)
         ag0.record(stream)

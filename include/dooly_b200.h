@@ -186,6 +186,16 @@ int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const 
  * Workspace: dooly_fit_grid_workspace_size(kind, n_pts) bytes of device memory
  * (the shared factor plus the scaled feature planes of the grid). */
 size_t dooly_fit_grid_workspace_size(int kind, int64_t n_pts);
+
+/* dooly_fit_grid for attention signatures that also writes the packed 96-byte
+ * serving form of the table from the fit epilogue: `packed` receives the
+ * dooly_attn_pack_header row followed by one dooly_attn_row96 per signature,
+ * byte-identical to dooly_attn_pack(table) (every fitted row carries the
+ * shared grid's box, so the field widths are known before the fit).
+ * Replaces fit(db) + the serving-table build. */
+int dooly_fit_grid_packed(dooly_ctx* ctx, const uint32_t* x, int64_t n_pts, const double* y,
+                          int64_t n_sig, void* table, double* fit_err, uint8_t* status,
+                          void* packed, void* workspace, size_t workspace_bytes, void* stream);
 int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const double* y,
                    int64_t n_sig, void* table, double* fit_err, uint8_t* status, void* workspace,
                    size_t workspace_bytes, void* stream);

@@ -144,6 +144,8 @@ _SIGS = {
     "dooly_sim_eval": (C.c_int, [_P, C.POINTER(OpList), _P, _I64, _P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P,
                                  _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "dooly_fit_grid": (C.c_int, [_P, C.c_int, _P, _I64, _P, _I64, _P, _P, _P, _P, C.c_size_t, _P]),
+    "dooly_fit_grid_packed": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _P, _P, _P, C.c_size_t,
+                                        _P]),
     "dooly_fit_grid_bcast": (C.c_int, [_P, C.c_int, _P, _I64, _P, _I64, _P, _P, _P,
                                        C.POINTER(GridPeers), _P, C.c_uint32, _P, _P, C.c_size_t,
                                        _P]),

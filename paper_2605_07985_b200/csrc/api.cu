@@ -21,7 +21,7 @@ size_t fit_grid_workspace_size(int kind, int64_t n_pts);
 cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
                             int64_t n_sig, void* table, double* fit_err, uint8_t* status,
                             const dooly_grid_peers* peers, void* ws, cudaStream_t stream,
-                            int n_sm, int64_t* launches);
+                            int n_sm, int64_t* launches, void* packed = nullptr);
 cudaError_t launch_attn_pack(const void* table, int64_t n_sig, void* packed, cudaStream_t stream,
                              int n_sm, int64_t* launches);
 cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off, int64_t n,
@@ -213,6 +213,29 @@ int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, c
                                            nullptr, workspace, (cudaStream_t)stream, ctx->n_sm,
                                            &ctx->launches),
                     "fit_grid");
+}
+
+int dooly_fit_grid_packed(dooly_ctx* ctx, const uint32_t* x, int64_t n_pts, const double* y,
+                          int64_t n_sig, void* table, double* fit_err, uint8_t* status,
+                          void* packed, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  const int kind = DOOLY_KIND_ATTN;
+  if (n_sig < 0 || n_pts < 0)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_packed: negative size");
+  if (!workspace || workspace_bytes < dooly::fit_grid_workspace_size(kind, n_pts) ||
+      (uintptr_t)workspace % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_packed: workspace too small or misaligned");
+  if (!packed || (n_pts > 0 && !x) ||
+      (n_sig > 0 && (!table || !fit_err || !status || (n_pts > 0 && !y))))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_packed: null pointer");
+  if ((uintptr_t)table % 16 || (uintptr_t)packed % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_packed: table and packed must be 16-byte aligned");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_fit_grid(kind, x, n_pts, y, n_sig, table, fit_err, status,
+                                           nullptr, workspace, (cudaStream_t)stream, ctx->n_sm,
+                                           &ctx->launches, packed),
+                    "fit_grid_packed");
 }
 
 int dooly_fit_grid_bcast(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts,

@@ -63,6 +63,17 @@ struct GridFactor {
   uint32_t lo[3], hi[3];
   int32_t ok;        // n_pts >= need
   int32_t grp4;      // attention: x0 and x1 constant on every aligned group of 4 points
+  // packed 96-B serving form (attention): bit-field layout of the box, as
+  // dooly_attn_pack derives it (widths from the largest fitted hi)
+  uint32_t pk_s1, pk_s2;  // bit offsets of the second and third box fields
+  int32_t pk_ok;          // the three widths fit in 64 bits
+  int32_t pk_pad_;
+};
+
+// Epilogue destinations: the peer tables of the fused all-gather and,
+// optionally, the packed 96-B attention rows (dooly_fit_grid_packed).
+struct GridOut : dooly_grid_peers {
+  uint8_t* packed;   // header row + one row per signature, or null
 };
 
 static size_t grid_factor_bytes() { return (sizeof(GridFactor) + 255) & ~(size_t)255; }
@@ -153,7 +164,8 @@ __device__ __forceinline__ void grid_features(const uint32_t* xs, const double* 
 template <int KIND>
 __global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __restrict__ x,
                                                             int64_t n_pts, GridFactor* gf,
-                                                            double* __restrict__ fplanes) {
+                                                            double* __restrict__ fplanes,
+                                                            uint8_t* packed, int64_t n_rows) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC, NT = NC * (NC + 1) / 2;
   __shared__ uint32_t smn[kGW][3], smx[kGW][3];
@@ -290,6 +302,30 @@ __global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __re
       for (int j = 0; j < NC; ++j) gf->W[j][e] = c[j];
     }
     gf->ok = n_pts >= T::NEED ? 1 : 0;
+    if constexpr (KIND == DOOLY_KIND_ATTN) {
+      // packed-form field widths from the largest fitted hi (every fitted row
+      // carries the grid's box), as dooly_attn_pack's scan would find them
+      uint32_t w[3], mh[3];
+      for (int k = 0; k < 3; ++k) {
+        mh[k] = gf->ok ? gf->hi[k] : 0u;
+        w[k] = max(1, 32 - __clz((int)mh[k]));
+      }
+      gf->pk_s1 = w[0];
+      gf->pk_s2 = w[0] + w[1];
+      gf->pk_ok = (w[0] + w[1] + w[2] <= 64) ? 1 : 0;
+      if (packed != nullptr) {
+        dooly_attn_pack_header h;
+        memset(&h, 0, sizeof(h));
+        h.magic = DOOLY_PACK_MAGIC;
+        h.ok = gf->pk_ok ? 1u : 0u;   // inv = 1/hi by construction: no bad_inv rows
+        for (int k = 0; k < 3; ++k) {
+          h.width[k] = w[k];
+          h.max_hi[k] = mh[k];
+        }
+        h.n_sig = n_rows;
+        *reinterpret_cast<dooly_attn_pack_header*>(packed) = h;
+      }
+    }
   }
 }
 
@@ -330,13 +366,33 @@ __device__ __forceinline__ void put_row(void* table, int64_t row, const RowBuf<K
 }
 
 template <int KIND>
-__device__ __forceinline__ void emit_row(const dooly_grid_peers& pe, void* table, double* fit_err,
-                                         uint8_t* status, int64_t s, const RowBuf<KIND>& r,
-                                         double err, uint8_t st) {
+__device__ __forceinline__ void emit_row(const GridOut& pe, const GridFactor* gf, void* table,
+                                         double* fit_err, uint8_t* status, int64_t s,
+                                         const RowBuf<KIND>& r, double err, uint8_t st) {
   const int64_t g = pe.row0 + s;
   put_row<KIND>(table, g, r);
   fit_err[g] = err;
   status[g] = st;
+  if constexpr (KIND == DOOLY_KIND_ATTN) {
+    if (pe.packed != nullptr) {
+      // the 96-B serving row, exactly as dooly_attn_pack writes it: c[10],
+      // then the box bit-packed with the table's field widths
+      const uint64_t w6 = (uint64_t)__double_as_longlong(r.v[6].y);
+      const uint64_t w7a = (uint64_t)__double_as_longlong(r.v[7].x);
+      const uint64_t w7b = (uint64_t)__double_as_longlong(r.v[7].y);
+      const uint32_t lo0 = (uint32_t)w6, lo1 = (uint32_t)(w6 >> 32), lo2 = (uint32_t)w7a;
+      const uint32_t hi0 = (uint32_t)(w7a >> 32), hi1 = (uint32_t)w7b, hi2 = (uint32_t)(w7b >> 32);
+      uint64_t lb = ~0ull, hb = 0ull;
+      if (lo0 <= hi0 && gf->pk_ok) {
+        lb = (uint64_t)lo0 | ((uint64_t)lo1 << gf->pk_s1) | ((uint64_t)lo2 << gf->pk_s2);
+        hb = (uint64_t)hi0 | ((uint64_t)hi1 << gf->pk_s1) | ((uint64_t)hi2 << gf->pk_s2);
+      }
+      double2* o = reinterpret_cast<double2*>(pe.packed + 96 * (1 + g));
+#pragma unroll
+      for (int i = 0; i < 5; ++i) o[i] = r.v[i];
+      o[5] = make_double2(__longlong_as_double((long long)lb), __longlong_as_double((long long)hb));
+    }
+  }
   for (int p = 0; p < pe.n_peers; ++p) {
     put_row<KIND>(pe.table[p], g, r);
     pe.fit_err[p][g] = err;
@@ -346,8 +402,8 @@ __device__ __forceinline__ void emit_row(const dooly_grid_peers& pe, void* table
 }
 
 template <int KIND>
-__device__ void write_unfitted_grid(const dooly_grid_peers& pe, void* table, int64_t s,
-                                    double* fit_err, uint8_t* status) {
+__device__ void write_unfitted_grid(const GridOut& pe, const GridFactor* gf, void* table,
+                                    int64_t s, double* fit_err, uint8_t* status) {
   double c[10], inv[3];
   uint32_t lo[3], hi[3];
   for (int i = 0; i < 10; ++i) c[i] = nan64();
@@ -356,7 +412,7 @@ __device__ void write_unfitted_grid(const dooly_grid_peers& pe, void* table, int
     lo[k] = 0xFFFFFFFFu;
     hi[k] = 0;
   }
-  emit_row<KIND>(pe, table, fit_err, status, s, make_row<KIND>(c, inv, lo, hi), nan64(),
+  emit_row<KIND>(pe, gf, table, fit_err, status, s, make_row<KIND>(c, inv, lo, hi), nan64(),
                  DOOLY_FIT_INSUFFICIENT);
 }
 
@@ -364,7 +420,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kGT, 2) fit_grid_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
-    uint8_t* __restrict__ status, const dooly_grid_peers pe) {
+    uint8_t* __restrict__ status, const GridOut pe) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC, R = T::R;
   __shared__ double sL[NC][NC], srd[NC], sinv[P];
@@ -390,7 +446,7 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_kernel(
     const int64_t s0 = g * R;
     const int nr = (int)min((int64_t)R, n_sig - s0);
     if (!ok) {
-      if (tid < nr) write_unfitted_grid<KIND>(pe, table, s0 + tid, fit_err, status);
+      if (tid < nr) write_unfitted_grid<KIND>(pe, gf, table, s0 + tid, fit_err, status);
       continue;
     }
     const double* yg = y + s0 * n_pts;
@@ -479,7 +535,7 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_kernel(
       double e = 0.0;
 #pragma unroll
       for (int w = 0; w < kGW; ++w) e += serr[w][tid];
-      emit_row<KIND>(pe, table, fit_err, status, s0 + tid,
+      emit_row<KIND>(pe, gf, table, fit_err, status, s0 + tid,
                      make_row<KIND>(scoef[tid], sinv, slo, shi), e / (double)n_pts,
                      DOOLY_FIT_OK);
     }
@@ -515,7 +571,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
-    uint8_t* __restrict__ status, const dooly_grid_peers pe) {
+    uint8_t* __restrict__ status, const GridOut pe) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC, R = T::RS;
   extern __shared__ __align__(128) unsigned char gdyn[];
@@ -560,7 +616,7 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
   if (!ok) {
     for (int64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
       const int nr = (int)min((int64_t)R, n_sig - g * R);
-      if (tid < nr) write_unfitted_grid<KIND>(pe, table, g * R + tid, fit_err, status);
+      if (tid < nr) write_unfitted_grid<KIND>(pe, gf, table, g * R + tid, fit_err, status);
     }
     return;
   }
@@ -673,7 +729,7 @@ __global__ void __launch_bounds__(kGT, 2) fit_grid_stage_kernel(
       double e = 0.0;
 #pragma unroll
       for (int w = 0; w < kGW; ++w) e += serr[w][tid];
-      emit_row<KIND>(pe, table, fit_err, status, s0 + tid,
+      emit_row<KIND>(pe, gf, table, fit_err, status, s0 + tid,
                      make_row<KIND>(scoef[tid], sinv, slo, shi), e / (double)n_pts,
                      DOOLY_FIT_OK);
     }
@@ -759,7 +815,7 @@ template <int KIND>
 __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
-    uint8_t* __restrict__ status, const dooly_grid_peers pe, int allow_factor) {
+    uint8_t* __restrict__ status, const GridOut pe, int allow_factor) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC;
 
@@ -784,7 +840,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
   const int n = (int)n_pts;  // n_pts % 4 == 0, n_pts < 2^31 (launcher)
   for (int64_t s = warp; s < n_sig; s += n_warps) {
     if (!ok) {
-      if (lane == 0) write_unfitted_grid<KIND>(pe, table, s, fit_err, status);
+      if (lane == 0) write_unfitted_grid<KIND>(pe, gf, table, s, fit_err, status);
       continue;
     }
     const double* ys = y + s * n_pts;
@@ -927,7 +983,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     }
     err = g_warp_sum(err);
     if (lane == 0)
-      emit_row<KIND>(pe, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
+      emit_row<KIND>(pe, gf, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
                      err / (double)n_pts, DOOLY_FIT_OK);
   }
 }
@@ -1029,7 +1085,7 @@ template <int KIND, int YS>
 __global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
     const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
-    uint8_t* __restrict__ status, const dooly_grid_peers pe, int allow_factor) {
+    uint8_t* __restrict__ status, const GridOut pe, int allow_factor) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC;
   __shared__ double sW[NC][NC];
@@ -1049,7 +1105,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
   const int n = (int)n_pts;  // n_pts % (128 * YS) == 0 (launcher)
   for (int64_t s = warp; s < n_sig; s += n_warps) {
     if (!ok) {
-      if (lane == 0) write_unfitted_grid<KIND>(pe, table, s, fit_err, status);
+      if (lane == 0) write_unfitted_grid<KIND>(pe, gf, table, s, fit_err, status);
       continue;
     }
     const double* ys = y + s * n_pts;
@@ -1076,7 +1132,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
       grid_sweep_db<KIND, YS, false>(fpl, n, lane, ys, c, acc, err);
     err = g_warp_sum(err);
     if (lane == 0)
-      emit_row<KIND>(pe, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
+      emit_row<KIND>(pe, gf, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
                      err / (double)n_pts, DOOLY_FIT_OK);
   }
 }
@@ -1084,11 +1140,11 @@ __global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
 template <int KIND>
 static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const double* y, int64_t n_sig,
                                     void* table, double* fit_err, uint8_t* status,
-                                    const dooly_grid_peers& pe, void* ws, cudaStream_t stream,
+                                    const GridOut& pe, void* ws, cudaStream_t stream,
                                     int n_sm, int64_t* launches) {
   GridFactor* gf = static_cast<GridFactor*>(ws);
   double* fpl = reinterpret_cast<double*>(static_cast<char*>(ws) + grid_factor_bytes());
-  fit_grid_prep_kernel<KIND><<<1, kGT, 0, stream>>>(x, n_pts, gf, fpl);
+  fit_grid_prep_kernel<KIND><<<1, kGT, 0, stream>>>(x, n_pts, gf, fpl, pe.packed, pe.row0 + n_sig);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   *launches += 1;
@@ -1160,9 +1216,10 @@ size_t fit_grid_workspace_size(int kind, int64_t n_pts) {
 cudaError_t launch_fit_grid(int kind, const uint32_t* x, int64_t n_pts, const double* y,
                             int64_t n_sig, void* table, double* fit_err, uint8_t* status,
                             const dooly_grid_peers* peers, void* ws, cudaStream_t stream,
-                            int n_sm, int64_t* launches) {
-  dooly_grid_peers pe{};
-  if (peers) pe = *peers;
+                            int n_sm, int64_t* launches, void* packed) {
+  GridOut pe{};
+  if (peers) static_cast<dooly_grid_peers&>(pe) = *peers;
+  pe.packed = static_cast<uint8_t*>(packed);
   if (kind == DOOLY_KIND_AFFINE)
     return launch_grid_kind<DOOLY_KIND_AFFINE>(x, n_pts, y, n_sig, table, fit_err, status, pe, ws,
                                                stream, n_sm, launches);

@@ -222,11 +222,15 @@ def fit(db: LatencyDB, device=None, strict: bool = True) -> Regressors:
 
 
 def fit_grid(kind: int, x: torch.Tensor, y: torch.Tensor,
-             out: Optional[FitResult] = None) -> FitResult:
+             out: Optional[FitResult] = None, packed: Optional[torch.Tensor] = None) -> FitResult:
     """Shared-grid batch fit (dooly_fit_grid): every signature was swept over the
     same points.  x: (P, n_pts) int32/uint32 device tensor, y: (n_sig, n_pts) f64.
     Same result contract as ``fit_tables`` with x repeated per signature; the
-    Gram matrix and its factor are built once for the whole batch."""
+    Gram matrix and its factor are built once for the whole batch.
+
+    ``packed`` (attention only; (n_sig + 1, 96) u8): the fit epilogue also
+    writes the 96-B serving table, byte-identical to ``pack_attn(table)``
+    (dooly_fit_grid_packed)."""
     dev = y.device
     if y.dim() != 2:
         raise ValueError("y must be (n_sig, n_pts)")
@@ -242,6 +246,17 @@ def fit_grid(kind: int, x: torch.Tensor, y: torch.Tensor,
     lib = _lib.load_library()
     ws = _grid_workspace(dev, kind, n_pts)
     ctx = _lib.ctx_for(dev)
+    if packed is not None:
+        if kind != _lib.KIND_ATTN or packed.shape != (n_sig + 1, 96) or \
+                packed.dtype != torch.uint8 or not packed.is_contiguous():
+            raise ValueError("packed must be a contiguous (n_sig + 1, 96) uint8 tensor "
+                             "(attention kind)")
+        _lib.check(lib.dooly_fit_grid_packed(
+            ctx, x.data_ptr() if x.numel() else 0, n_pts, y.data_ptr() if y.numel() else 0,
+            n_sig, out.table.data_ptr() if n_sig else 0, out.fit_err.data_ptr() if n_sig else 0,
+            out.status.data_ptr() if n_sig else 0, packed.data_ptr(), ws.data_ptr(), ws.numel(),
+            _lib.stream_ptr(dev)), ctx)
+        return out
     _lib.check(lib.dooly_fit_grid(
         ctx, kind, x.data_ptr() if x.numel() else 0, n_pts, y.data_ptr() if y.numel() else 0,
         n_sig, out.table.data_ptr() if n_sig else 0, out.fit_err.data_ptr() if n_sig else 0,

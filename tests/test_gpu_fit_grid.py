@@ -175,3 +175,26 @@ def test_fit_grid_grouped_attention_passes(dev, monkeypatch):
         assert np.max(np.abs(fe - ref["fit_err"]) / ref["fit_err"]) <= 1e-8
     a, b = (rows_to_table(ATTN, f.rows())["coef"] for f in (grouped, plain))
     assert np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)) <= 1e-12
+
+
+@pytest.mark.parametrize("n_sig,n_pts,kernel", [(300, 4096, "warp"), (37, 512, "db"), (5, 64, "stage"),
+                                                (9, 125, "warp"), (4, 8, "warp")])
+def test_fit_grid_packed_equals_attn_pack(n_sig, n_pts, kernel, dev, monkeypatch):
+    """dooly_fit_grid_packed's epilogue writes the 96-B serving table
+    byte-identical to dooly_attn_pack of the fitted table (header included),
+    for every grid kernel and for unfitted tables (too few points)."""
+    from paper_2605_07985_b200.sim import fit_grid, pack_attn
+
+    monkeypatch.setenv("DOOLY_FIT_GRID_KERNEL", kernel)
+    rng = np.random.default_rng(n_sig + n_pts)
+    x = _grid(ATTN, n_pts, rng)[:, :n_pts]
+    y = _ys(ATTN, x, n_sig, rng)
+    xt = torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).to(dev)
+    yt = torch.from_numpy(y).to(dev)
+    packed = torch.full((n_sig + 1, 96), 0xAB, dtype=torch.uint8, device=dev)
+    fr = fit_grid(ATTN, xt, yt, packed=packed)
+    ref = pack_attn(fr.table)
+    torch.cuda.synchronize()
+    assert torch.equal(packed, ref)
+    plain = fit_grid(ATTN, xt, yt)
+    assert torch.equal(plain.table, fr.table) and torch.equal(plain.status, fr.status)
