@@ -39,7 +39,13 @@ def test_library_rejects_bad_arguments_without_gpu():
 
     lib = _lib.load_library()
     assert lib.dooly_predict(None, 0, None, 0, None, None, 0, None, None, None, None) == 1
+    assert lib.dooly_fit_grid_packed(None, None, 0, None, 0, None, None, None, None, None, 0,
+                                     None) == 1
     assert lib.dooly_dedup_workspace_size(1000, 10) >= 2048 * 4
+    # attention grid workspace: factor + 3 feature planes + the (f1, f2) group plane
+    a = lib.dooly_fit_grid_workspace_size(1, 4096)
+    assert a == lib.dooly_fit_grid_workspace_size(1, 0) + 3 * 4096 * 8 + 4096 // 4 * 16
+    assert lib.dooly_fit_grid_workspace_size(0, 4096) == lib.dooly_fit_grid_workspace_size(0, 0) + 4096 * 8
 
 
 def test_struct_layouts_match_header():
