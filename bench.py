@@ -402,6 +402,31 @@ def _oracle_predict_worker(i):
     return time.perf_counter() - t0
 
 
+def cpu_per_item_baseline(tables_host, queries_host, n_items: int) -> dict:
+    """SPEC.md:566's predict(regs, signature_hash, features) one query at a time
+    in plain Python (oracle/sim.py predict_one, one thread) on a bounded sample."""
+    from oracle import sim as osim
+
+    done, t_total = 0, 0.0
+    for kind in (AFFINE, ATTN):
+        tab = tables_host[kind]
+        sig, x = queries_host[kind]
+        m = min(n_items // 2, sig.shape[0])
+        need = sorted({int(v) for v in sig[:m]})
+        rows = {i: (tab["coef"][i].tolist(), tab["inv"][i].tolist(), tab["lo"][i].tolist(),
+                    tab["hi"][i].tolist()) for i in need}
+        sl = [int(v) for v in sig[:m]]
+        xl = x[:, :m].T.tolist()
+        t0 = time.perf_counter()
+        for q in range(m):
+            osim.predict_one(kind, rows, sl[q], xl[q])
+        t_total += time.perf_counter() - t0
+        done += m
+    return {"value": done / t_total, "unit": "predictions/s", "cores": 1, "kind": "port",
+            "sample": f"{done} queries of the same C5 batch, oracle/sim.py predict_one "
+                      "(plain Python per query, 1 thread)"}
+
+
 def host_regressor_table(kind: int, n_sig: int, seed: int) -> dict:
     """Random fitted-looking regressor table for the CPU arm (oracle/sim.py
     layout): training boxes inside the C5 grids (affine num_toks <= 32768;
@@ -724,7 +749,8 @@ def run_ours(args):
         rate, n_done = cpu_predict_baseline(tables_host, qh, threads=1)
         cpu = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port",
                "sample": f"{n_done} queries (half affine, half attention) of the same C5 batch, "
-                         "oracle/sim.py predict (numpy, 1 thread)"}
+                         "oracle/sim.py predict (numpy, 1 thread)",
+               "per_item": cpu_per_item_baseline(tables_host, qh, args.cpu_sample_items)}
 
     # ---------------- dedup sub-benchmark
     dedup = None
@@ -956,6 +982,8 @@ def main(argv=None):
     ap.add_argument("--records", type=int, default=4_000_000)
     ap.add_argument("--e2e-queries", type=int, default=200_000_000)
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
+    ap.add_argument("--cpu-sample-items", type=int, default=400_000,
+                    help="queries of the per-item (plain Python) CPU line")
     ap.add_argument("--ref-sample", type=int, default=40_000_000)
     ap.add_argument("--sim-requests", type=int, default=1_000_000)
     ap.add_argument("--sim-shards", type=int, default=1184)

@@ -166,6 +166,34 @@ def predict(kind: int, table: dict, sig: np.ndarray, x: np.ndarray) -> dict:
     return {"out": out, "extrap": extrap, "clamped": cl & known, "bad": ~known}
 
 
+def predict_one(kind: int, rows: dict, s: int, xs) -> tuple:
+    """SPEC.md:566-574 for ONE query in plain Python floats (the per-item form
+    of ``predict``; same operation order, so bit-identical):
+    ``rows`` maps a signature index to (coef list, inv list, lo list, hi list).
+    Returns (latency, extrapolated, clamped); an unknown or unfitted signature
+    gives (nan, False, False)."""
+    row = rows.get(s)
+    if row is None or row[2][0] > row[3][0]:
+        return math.nan, False, False
+    c, inv, lo, hi = row
+    if kind == AFFINE:
+        p = c[0] + c[1] * (float(xs[0]) * inv[0])
+    else:
+        f1, f2, f3 = float(xs[0]) * inv[0], float(xs[1]) * inv[1], float(xs[2]) * inv[2]
+        p = c[0]
+        p = p + c[1] * f1
+        p = p + c[2] * f2
+        p = p + c[3] * f3
+        p = p + c[4] * (f1 * f1)
+        p = p + c[5] * (f2 * f2)
+        p = p + c[6] * (f3 * f3)
+        p = p + c[7] * (f1 * f2)
+        p = p + c[8] * (f1 * f3)
+        p = p + c[9] * (f2 * f3)
+    ext = any(v < a or v > b for v, a, b in zip(xs, lo, hi))
+    return (FLOOR, ext, True) if p < FLOOR else (p, ext, False)
+
+
 # -------------------------------------------------------------- iter_latency
 
 

@@ -228,3 +228,26 @@ def test_mape_kat():
     assert osim.mape([3.0], [3.0]) == 0.0
     with pytest.raises(ZeroDivisionError):
         osim.mape([1], [0])
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_predict_one_equals_batch_predict(kind):
+    """The per-item oracle predict (plain Python floats) is bit-identical to
+    the vectorised one, flags included."""
+    import numpy as np
+
+    from helpers import synth_fit_data, synth_queries
+    from oracle import sim as osim
+
+    x, y, off = synth_fit_data(kind, 64, 32, seed=kind)
+    f = osim.fit(kind, x, y, off)
+    table = {k: f[k] for k in ("coef", "inv", "lo", "hi")}
+    table["coef"][3, 0] = -1.0                                   # a clamped signature
+    sig, xq = synth_queries(kind, table, 3000, seed=5, outside=0.1)
+    ref = osim.predict(kind, table, sig, xq)
+    rows = {i: (list(table["coef"][i]), list(table["inv"][i]), list(table["lo"][i]),
+                list(table["hi"][i])) for i in range(64)}
+    for q in range(sig.shape[0]):
+        p, e, c = osim.predict_one(kind, rows, int(sig[q]), [int(v) for v in xq[:, q]])
+        assert np.float64(p).view(np.uint64) == ref["out"][q].view(np.uint64)
+        assert e == bool(ref["extrap"][q]) and c == bool(ref["clamped"][q])
