@@ -9,11 +9,20 @@ Headline step (config C5 of BASELINE.json, per GPU — weak scaling):
     the signature's training box; inputs resident in HBM (~20 GB per step,
     >> 126 MB L2, so no L2 flush is needed).
 Also measured in the same run and reported as extra keys:
-    fits   — the C5 fit of those 1M signatures x 4096 points (+ NCCL all-gather
-             of the regressor rows when N > 1);
-    dedup  — SHA-256 + first-occurrence dedup of 4M packed records (~1M unique);
-    sim    — config C4: Llama-3-70B-like (tp=4) serving replicas, device event
-             loop over a Poisson trace sharded into S fixed replicas.
+    fits     — the C5 fit of those 1M signatures x 4096 points on the shared
+               sweep grid, the attention serving table (96-B rows) written by
+               the fit epilogue; at N > 1 the regressor rows reach every rank
+               through the fused peer-memory all-gather (NCCL otherwise);
+    fits_csr — the same points through the per-signature (CSR) fit;
+    dedup    — SHA-256 + first-occurrence dedup of 4M packed records (~1M
+               unique); at N > 1 fused digest all-gather (2 ranks) or
+               owner-routed all-to-all (4+ ranks);
+    sim      — config C4: Llama-3-70B-like (tp=4) serving replicas, device event
+               loop over a Poisson trace sharded into S fixed replicas;
+    e2e      — the predict batch through the public host API (pinned host
+               buffers, copies inside the timed region);
+    cpu_baseline — the CPU oracle on a bounded sample of the same batch: numpy
+               batch predict (1 thread) and per-item plain Python predict_one.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 torchrun launches one rank per GPU (RANK/LOCAL_RANK/WORLD_SIZE from env).
