@@ -150,6 +150,20 @@ def fit_uniform(kind: int, x: np.ndarray, y: np.ndarray) -> dict:
     return {"coef": c, "inv": inv, "lo": lo, "hi": hi, "fit_err": err}
 
 
+def fit_error(kind: int, coef: np.ndarray, inv: np.ndarray, x: np.ndarray,
+              y: np.ndarray) -> np.ndarray:
+    """A.15 training MAPE of GIVEN coefficients: c (S, p), inv (S, P), x (S, P, n)
+    or (P, n) shared, y (S, n).  Checks a device fit_err against the
+    device's own coefficients (fit_err parity then follows coefficient parity)."""
+    x = np.asarray(x)
+    xq = np.moveaxis(x, -2, -1)
+    if xq.ndim == 2:
+        xq = xq[None]
+    pred = eval_poly(kind, coef[:, None, :], inv[:, None, :], xq)
+    pred, _ = clamp(pred)
+    return np.mean(np.abs(pred - y) / y, axis=1)
+
+
 def predict(kind: int, table: dict, sig: np.ndarray, x: np.ndarray) -> dict:
     """SPEC.md:566-574 for a batch: x (P, Q).  Unknown/unfitted rows -> NaN, bad."""
     sig = np.asarray(sig, dtype=np.int64)
@@ -265,8 +279,13 @@ def schedule_step(running: list, waiting_head, chunk: int, max_batch: int, kv_ok
 def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch: int,
               kv_bytes_per_token: int, kv_capacity: int, window: int = 0, tp: int = 1,
               alpha: float = 0.0, beta: float = 0.0, max_iterations: int = 50_000_000,
-              log: bool = False) -> dict:
-    """SPEC.md:596-604 event loop for one replica (requests sorted by arrival)."""
+              log: bool = False, latency=None) -> dict:
+    """SPEC.md:596-604 event loop for one replica (requests sorted by arrival).
+
+    ``latency(reqs, feats) -> seconds`` replaces the regression iteration
+    latency (``iter_latency`` over ``ops``): reference_run (SPEC.md:606-612)
+    passes the brute-force oracle here, so both runs share this scheduler code.
+    reqs = [(tokens, is_prefill, kv_before)] per scheduled request."""
     n = len(arrival)
     ttft = [math.nan] * n
     tpot = [math.nan] * n
@@ -276,6 +295,7 @@ def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch:
     reserved = 0
     feats_log, lat_log = [], []
     start_log, clock_log = [], []          # idle jump target (0.0 if busy), clock after it
+    comp_log = []                          # batch composition: ((request, tokens, prefill), ...)
     first_it, last_it = [-1] * n, [-1] * n
     jump = 0.0
     status = "ok"
@@ -324,10 +344,14 @@ def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch:
         kv = sum(r["kv"] for r, _, _ in active)
         kvw = sum(min(r["kv"], window) for r, _, _ in active) if window else 0
         feats = (num_toks, prefill, batch, kv, kvw)
-        lat = iter_latency(feats, ops, tp, alpha, beta)
+        if latency is None:
+            lat = iter_latency(feats, ops, tp, alpha, beta)
+        else:
+            lat = latency([(t, pf, r["kv"]) for r, t, pf in active], feats)
         clock = clock + lat
         it += 1
         if log:
+            comp_log.append(tuple((r["i"], t, pf) for r, t, pf in active))
             feats_log.append(feats)
             lat_log.append(lat)
             start_log.append(jump)
@@ -357,7 +381,55 @@ def run_shard(arrival, prompt, output, cached, ops: list, chunk: int, max_batch:
             running = [r for r in running if id(r) not in ids]
     return {"ttft": np.array(ttft), "tpot": np.array(tpot), "n_iter": it, "clock": clock,
             "status": status, "feats": feats_log, "lat": lat_log, "start": start_log,
-            "clocks": clock_log, "first_it": first_it, "last_it": last_it}
+            "clocks": clock_log, "first_it": first_it, "last_it": last_it,
+            "compositions": comp_log}
+
+
+def reference_run(arrival, prompt, output, cached, entries: list, hw: dict, cost_multiplier,
+                  dtype_bytes: int, chunk: int, max_batch: int, kv_bytes_per_token: int,
+                  kv_capacity: int, tp: int = 1, hidden: int = 0, num_layers: int = 0,
+                  oracle=None, max_iterations: int = 50_000_000, log: bool = False) -> dict:
+    """SPEC.md:606-612 reference_run: the same event loop, but every iteration's
+    latency is the direct oracle evaluation of every runnable entry at the
+    batch's concrete dims (no regression): sum in list order of
+    repeat x oracle(entry, reqs), then the TP all-reduces (2 per layer of
+    num_toks x hidden x dtype bytes, App. A.16).
+
+    ``oracle(entry, reqs) -> seconds`` defaults to the roofline model at the
+    concrete batch (oracle.profiler.batch_latency); SPEC.md:629's invariant is
+    tested with an exactly-affine oracle here.  entries are runnable-set JSON
+    dicts (SPEC.md:404); hw: {peak_flops, mem_bw, comm_alpha, comm_beta}."""
+    from . import profiler as oprof
+
+    if oracle is None:
+        def oracle(entry, reqs):
+            return oprof.batch_latency(entry, reqs, hw, cost_multiplier, dtype_bytes)
+
+    def latency(reqs, feats):
+        lat = 0.0
+        for e in entries:
+            lat = lat + float(e["repeat_count"]) * oracle(e, reqs)
+        if tp > 1:
+            nbytes = feats[0] * hidden * dtype_bytes
+            comm = 2 * (tp - 1) / tp * (hw["comm_alpha"] + nbytes / tp * hw["comm_beta"])
+            lat = lat + float(2 * num_layers) * comm
+        return lat
+
+    return run_shard(arrival, prompt, output, cached, [], chunk, max_batch, kv_bytes_per_token,
+                     kv_capacity, 0, tp, 0.0, 0.0, max_iterations, log, latency)
+
+
+def percentile_mape(pred, truth, percentiles=(25, 50, 75, 90, 95, 99)) -> dict:
+    """A5: relative error of each reported percentile of a metric
+    (NaNs — e.g. TPOT of 1-token requests — dropped on both sides)."""
+    p = np.asarray(pred, dtype=np.float64)
+    t = np.asarray(truth, dtype=np.float64)
+    p, t = p[~np.isnan(p)], t[~np.isnan(t)]
+    out = {}
+    for q in percentiles:
+        a, b = float(np.percentile(p, q)), float(np.percentile(t, q))
+        out[f"p{q}"] = abs(a - b) / b
+    return out
 
 
 def run_shards(arrival, prompt, output, cached, n_shards: int, **kw) -> dict:

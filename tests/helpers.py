@@ -71,3 +71,104 @@ def synth_queries(kind: int, table: dict, n_q: int, seed: int = 1, outside: floa
         m = rng.random(n_q) < outside
         x[m] = hi[m] + 1 + rng.integers(0, 1000, size=(m.sum(), x.shape[1]))
     return sig.astype(np.uint32), np.ascontiguousarray(x.T.astype(np.uint32))
+
+
+def oracle_grid(grid) -> dict:
+    """modelir.SweepGrid -> the oracle's plain grid dict."""
+    return {"token_counts": tuple(grid.token_counts), "request_counts": tuple(grid.request_counts),
+            "kv_lens": tuple(grid.kv_lens), "prefill_chunk": grid.prefill_chunk,
+            "max_batch": grid.max_batch}
+
+
+def oracle_hw(hw) -> dict:
+    return {"peak_flops": hw.peak_flops, "mem_bw": hw.mem_bw, "comm_alpha": hw.comm_alpha,
+            "comm_beta": hw.comm_beta}
+
+
+def oracle_sweep(entry, grid, model, hw, backend):
+    """oracle/profiler.py sweep of one RunnableEntry (JSON form) — the checker."""
+    from oracle import profiler as oprof
+
+    return oprof.sweep(entry.to_json(), oracle_grid(grid), model.max_context, oracle_hw(hw),
+                       backend.cost_multiplier, model.dtype_bytes)
+
+
+# ---------------------------------------------- SPEC.md:629 exactly-affine oracle
+
+
+def affine_oracle_coefs(entries) -> list:
+    """Per-entry coefficients of an oracle whose latency is EXACTLY affine in
+    the entry's regression features: non-attention
+    a + b * num_toks; attention a + b1 * prefill_toks + b2 * batch + b3 * kv_tokens.
+    Deterministic in the entry's signature (entries sharing a signature share
+    the oracle, as they share the regressor)."""
+    import hashlib
+
+    from paper_2605_07985_b200.records import canonical_bytes
+
+    out = []
+    for e in entries:
+        i = hashlib.sha256(canonical_bytes(e)).digest()[0]
+        a = 5e-6 * (1.0 + 0.25 * (i % 7))
+        if e.feature == "attention":
+            out.append((a, 2e-9 * (1 + i % 3), 3e-7 * (1 + i % 5), 1e-10 * (1 + i % 4)))
+        else:
+            out.append((a, 1.5e-8 * (1 + i % 11)))
+    return out
+
+
+def affine_oracle_value(entry, coef, feats) -> float:
+    if entry.feature == "attention":
+        a, b1, b2, b3 = coef
+        return a + b1 * feats[0] + b2 * feats[1] + b3 * feats[2]
+    return coef[0] + coef[1] * feats[0]
+
+
+def affine_oracle_batch(entries, coefs):
+    """oracle(entry_json, reqs) for oracle.sim.reference_run: the affine
+    latency at the iteration's concrete dims (features summed over requests,
+    kv capped at the entry's window — App. A.6)."""
+    by_key = {}
+    for e, c in zip(entries, coefs):
+        by_key[id(e)] = c
+    table = [(e.to_json(), e, c) for e, c in zip(entries, coefs)]
+
+    def oracle(entry_json, reqs):
+        for ej, e, c in table:
+            if ej is entry_json:
+                break
+        else:
+            raise KeyError("unknown entry")
+        if e.feature == "attention":
+            w = e.window
+            pre = sum(t for t, pf, _ in reqs if pf)
+            kv = sum(min(k, w) if w else k for _, _, k in reqs)
+            return affine_oracle_value(e, c, (pre, len(reqs), kv))
+        return affine_oracle_value(e, c, (sum(t for t, _, _ in reqs),))
+
+    return [ej for ej, _, _ in table], oracle
+
+
+def affine_oracle_sweep(entry, coef, grid, max_context):
+    """Measurements of one entry under the affine oracle at its sweep points."""
+    from oracle import profiler as oprof
+
+    ej = entry.to_json()
+    pts = oprof.sweep_points(ej, oracle_grid(grid), max_context)
+    x = np.array([oprof.point_features(ej, p) for p in pts], dtype=np.uint32).T
+    y = np.array([affine_oracle_value(entry, coef, x[:, j].tolist()) for j in range(x.shape[1])])
+    return np.ascontiguousarray(x), y
+
+
+def oracle_ops(entries, fits) -> list:
+    """Oracle regression op list (oracle.sim.iter_latency format) from per-entry
+    oracle fits [(kind, fit dict)] in entry order."""
+    from oracle import sim as osim
+
+    ops = []
+    for e, (kind, r) in zip(entries, fits):
+        ops.append({"feat": osim.FEAT_ATTN if kind == ATTN else
+                    (osim.FEAT_NUM_SEQS if e.feature == "num_seqs" else osim.FEAT_NUM_TOKS),
+                    "coef": list(r["coef"][0]), "inv": list(r["inv"][0]),
+                    "repeat": e.repeat_count, "window_slot": 1 if e.window else 0})
+    return ops

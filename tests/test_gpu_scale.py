@@ -3,18 +3,18 @@ points, 1e9 queries; 4M dedup records; C4 1M-request trace), checked through
 oracle parity on random samples plus size-independent properties:
 
 * fit: 0.5M affine + 0.5M attention signatures on the shared sweep grid, every
-  signature fitted; 256 sampled signatures re-fitted by the CPU oracle agree
-  within the 1e-9 coefficient contract; the warp kernel and the staged kernel
+  signature fitted; 10k sampled signatures per kind re-fitted by the CPU
+  oracle agree within the 1e-9 coefficient contract (fit_err within 1e-9); the warp kernel and the staged kernel
   agree on every signature (two independent code paths over the full batch);
-* predict: 5e8 affine + 5e8 attention queries; a 200k-query random sample is
-  bit-identical to the oracle (latency bits, extrapolation and clamp flags);
+* predict: 5e8 affine + 5e8 attention queries; a contiguous 10M-query block per
+  kind is bit-identical to the oracle (latency bits, extrapolation and clamp flags);
   re-running the batch reproduces every output bit (determinism); the
   checksum of the device output equals the sum of its chunks' checksums;
 * dedup: 4M records, digests of a 2k sample equal hashlib over the oracle's
   canonical bytes; first-occurrence indices are minimal per digest and the
   unique count equals torch.unique's;
-* sim: the C4 1M-request trace over 1184 replicas terminates on every shard,
-  and two sampled shards match the oracle's event loop bit for bit.
+* sim: the C4 1M-request trace over S = 64 replicas terminates on every shard,
+  and a sampled shard matches the oracle's event loop bit for bit.
 """
 
 from __future__ import annotations
@@ -34,6 +34,8 @@ pytestmark = pytest.mark.gpu
 N_SIG = 500_000      # per kind
 N_PTS = 4096
 N_Q = 500_000_000    # per kind
+N_ORACLE_SIGS = 10_000   # full oracle fit comparison per kind
+N_ORACLE_Q = 10_000_000  # bit-exact oracle predictions per kind
 
 
 @pytest.fixture(scope="module")
@@ -56,20 +58,32 @@ def test_c5_fit_full_size(kind, c5, dev, monkeypatch):
 
     x, y, fr = c5[kind]
     assert int((fr.status != 0).sum().item()) == 0
-    # oracle parity on a random sample of signatures
+    # full oracle fit of >= 10k signatures (SURVEY §8(d) parity scale), in
+    # vectorised chunks of the oracle's fit_uniform
     rng = np.random.default_rng(100 + kind)
-    pick = np.sort(rng.choice(N_SIG, 256, replace=False))
+    pick = np.sort(rng.choice(N_SIG, N_ORACLE_SIGS, replace=False))
     xs = x.cpu().numpy().view(np.uint32)
     ys = y[torch.from_numpy(pick).to(dev)].cpu().numpy()
-    ref = osim.fit(kind, np.tile(xs, (1, len(pick))), ys.reshape(-1),
-                   np.arange(len(pick) + 1, dtype=np.int64) * N_PTS)
     got = rows_to_table(kind, fr.rows()[pick])
-    dc = np.abs(got["coef"] - ref["coef"]).max(axis=1) / np.abs(ref["coef"]).max(axis=1)
-    assert dc.max() <= 1e-9, dc.max()
-    assert np.array_equal(got["lo"], ref["lo"]) and np.array_equal(got["hi"], ref["hi"])
-    assert np.array_equal(got["inv"], ref["inv"])
     fe = fr.fit_err.cpu().numpy()[pick]
-    assert np.allclose(fe, ref["fit_err"], rtol=1e-6, atol=0)
+    for a in range(0, len(pick), 500):
+        b = min(a + 500, len(pick))
+        ref = osim.fit_uniform(kind, np.broadcast_to(xs, (b - a,) + xs.shape), ys[a:b])
+        dc = (np.abs(got["coef"][a:b] - ref["coef"]).max(axis=1)
+              / np.abs(ref["coef"]).max(axis=1))
+        assert dc.max() <= 1e-9, dc.max()
+        for k in ("lo", "hi", "inv"):
+            assert np.array_equal(got[k][a:b], ref[k]), k
+        # fit_err: the oracle MAPE of the device's own coefficients (the MAPE
+        # pass is regrouped on the device, so equal to rounding), and within
+        # the coefficient-tolerance bound of the oracle's own fit_err
+        own = osim.fit_error(kind, got["coef"][a:b], got["inv"][a:b], xs, ys[a:b])
+        d_own = np.max(np.abs(fe[a:b] - own) / own)
+        assert d_own <= 1e-12, d_own
+        d_ref = np.max(np.abs(fe[a:b] - ref["fit_err"]) / ref["fit_err"])
+        assert d_ref <= 1e-6, d_ref
+        print(f"fit kind {kind}: coef rel {dc.max():.2e}, fit_err vs own-coef MAPE "
+              f"{d_own:.2e}, vs oracle fit {d_ref:.2e}")
     # the staged kernel over the whole batch: an independent code path
     monkeypatch.setenv("DOOLY_FIT_GRID_KERNEL", "stage")
     st = fit_grid(kind, x, y)
@@ -102,20 +116,25 @@ def test_c5_predict_full_size(kind, c5, dev):
     tot = out.sum().item()
     parts = sum(out[i:i + (1 << 26)].sum().item() for i in range(0, N_Q, 1 << 26))
     assert abs(tot - parts) <= 1e-9 * abs(tot)
-    # bit-exact oracle parity on a random sample
+    # bit-exact oracle parity on >= 10M queries per kind:
+    # a contiguous 10M block (every code path of a tile) checked in chunks
     rng = np.random.default_rng(200 + kind)
-    qi = torch.from_numpy(np.sort(rng.choice(N_Q, 200_000, replace=False))).to(dev)
+    q0 = int(rng.integers(0, N_Q - N_ORACLE_Q)) // 256 * 256
     tab = rows_to_table(kind, fr.rows())
-    s_np = sig[qi].cpu().numpy().view(np.uint32)
-    x_np = x[:, qi].cpu().numpy().view(np.uint32)
-    ref = osim.predict(kind, tab, s_np, x_np)
-    got = out[qi].cpu().numpy()
-    assert np.array_equal(got.view(np.uint64), ref["out"].view(np.uint64))
-    bits = np.unpackbits(flags.cpu().numpy().view(np.uint8).reshape(2, -1), axis=1,
-                         bitorder="little")[:, :N_Q]
-    qn = qi.cpu().numpy()
-    assert np.array_equal(bits[0, qn].astype(bool), ref["extrap"])
-    assert np.array_equal(bits[1, qn].astype(bool), ref["clamped"])
+    words = (N_Q + 31) // 32
+    fl = flags.cpu().numpy()
+    for a in range(q0, q0 + N_ORACLE_Q, 1 << 21):
+        b = min(a + (1 << 21), q0 + N_ORACLE_Q)
+        s_np = sig[a:b].cpu().numpy().view(np.uint32)
+        x_np = x[:, a:b].cpu().numpy().view(np.uint32)
+        ref = osim.predict(kind, tab, s_np, x_np)
+        got = out[a:b].cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), ref["out"].view(np.uint64))
+        bits = np.unpackbits(fl[:, a // 32:(b + 31) // 32].view(np.uint8), axis=1,
+                             bitorder="little")[:, :b - a]
+        assert np.array_equal(bits[0].astype(bool), ref["extrap"])
+        assert np.array_equal(bits[1].astype(bool), ref["clamped"])
+    assert words == fl.shape[1]
 
 
 def test_c5_dedup_full_size(dev):
@@ -144,8 +163,10 @@ def test_c5_dedup_full_size(dev):
 
 
 def test_c4_sim_full_size(dev):
-    """1M-request Poisson trace over 1184 replicas (bench.py's C4 leg): every shard
-    terminates, and two sampled shards equal the oracle event loop bit for bit."""
+    """C4 as BASELINE.md §3 / SURVEY §8(d) define it: 1M-request Poisson trace
+    over S = 64 fixed replicas (request i -> shard i mod 64): every shard
+    terminates, and a sampled shard (15,625 requests) equals the oracle event
+    loop bit for bit."""
     import math
 
     from paper_2605_07985_b200 import modelir
@@ -160,7 +181,7 @@ def test_c4_sim_full_size(dev):
     regs = fit(db, dev)
     ct = build_calltree(model, backend, regs, hw, tp)
     cfg = make_sched(model, hw, tp, SchedConfig(chunk=8192, max_batch=256), ct)
-    n, S = 1_000_000, 1184
+    n, S = 1_000_000, 64
     rng = np.random.default_rng(1)
     arr = np.cumsum(rng.exponential(1.0 / (4.0 * S), size=n))
     sp = math.sqrt(2 * math.log(1232 / 950))
@@ -187,7 +208,7 @@ def test_c4_sim_full_size(dev):
             op.update(coef=list(t["coef"][row]), inv=list(t["inv"][row]))
         ops.append(op)
     n_iter = res.n_iter.cpu().numpy()
-    for s in (0, 777):
+    for s in (37,):
         idx = np.arange(s, n, S)
         r = osim.run_shard(arr[idx].tolist(), pr[idx].tolist(), ou[idx].tolist(), ca[idx].tolist(),
                            ops, 8192, 256, cfg.kv_bytes_per_token, cfg.kv_capacity_bytes,

@@ -1,11 +1,12 @@
-"""K5 fused sweep -> fit vs the host sweep + oracle fit."""
+"""K5 fused sweep -> fit vs the ORACLE sweep (oracle/profiler.py
+op_cost / oracle_latency) + oracle fit."""
 
 from __future__ import annotations
 
 import numpy as np
 import pytest
 
-from helpers import rows_to_table
+from helpers import oracle_sweep, rows_to_table
 from oracle import sim as osim
 
 pytestmark = pytest.mark.gpu
@@ -25,7 +26,7 @@ def _unique_entries(manifest):
     return out
 
 
-@pytest.mark.parametrize("name", ["corpus12", "mixtral", "fixtures"])
+@pytest.mark.parametrize("name", ["corpus12", "mixtral", "fixtures", "llama70b"])
 def test_profile_fit_matches_host_sweep_and_oracle(name, dev):
     from paper_2605_07985_b200 import modelir, profiler
 
@@ -45,7 +46,7 @@ def test_profile_fit_matches_host_sweep_and_oracle(name, dev):
             gy = py.cpu().numpy()
             rows = rows_to_table(kind, fr.rows())
             for j, i in enumerate(idx):
-                x, y = profiler.sweep(ents[i], man.grid, m, man.hardware, b)
+                x, y = oracle_sweep(ents[i], man.grid, m, man.hardware, b)
                 a, z = off[j], off[j + 1]
                 assert np.array_equal(gx[:, a:z], x), (ents[i].name, j)
                 assert np.array_equal(gy[a:z], y), ents[i].name       # bit-identical latencies
