@@ -64,19 +64,23 @@ typedef struct {
 } dooly_attn_row; /* 128 bytes */
 
 /* Packed attention table (DOOLY_KIND_ATTN_PACKED): the predict-side form of a
- * dooly_attn_row table, 96 B = 3 sectors per row instead of 4.  inv_scale is
- * not stored: it is a pure function of the box (inv = 1/hi by IEEE division,
- * 1 if hi == 0; oracle/sim.py inv_scale), recomputed with a correctly-rounded
- * reciprocal, so predictions stay bit-identical to the 128-B row.  The box is
- * bit-packed with per-table field widths w[k] (w0+w1+w2 <= 64):
+ * dooly_attn_row table, 96 B = 3 sectors per row instead of 4.  The
+ * coefficients are stored FOLDED into raw-feature space (inv = 1/hi by IEEE
+ * division, 1 if hi == 0) and grouped by feature: sector k = {e_k, a_k, b_k,
+ * d_k} holds the terms that multiply feature k first (a: x_k, b: x_k^2,
+ * d: x_k x_{k+1 mod 3}), e_0 = c0, e_1 = lo_bits, e_2 = hi_bits
+ * (common.cuh fold_row96, oracle/sim.py pack_attn).  Predict evaluates
+ *   s_k = ((e'_k + a_k x_k) + b_k x_k^2) + d_k x_k x_{k+1},  p = (s_0 + s_1) + s_2
+ * over raw features with no reciprocal; three lanes evaluate one row
+ * cooperatively, lane k from sector k.  The box is bit-packed with per-table
+ * field widths w[k] (w0+w1+w2 <= 64):
  *   lo_bits = lo0 | lo1 << w0 | lo2 << (w0+w1)   (hi_bits likewise)
  * Unfitted rows: lo_bits = all ones, hi_bits = 0.  Row s lives at
  * packed + 96 * (s + 1); the first 96 B are the header below. */
 #define DOOLY_KIND_ATTN_PACKED 2
-#define DOOLY_PACK_MAGIC 0x6b504144u /* "DAPk" */
+#define DOOLY_PACK_MAGIC 0x66504144u /* "DAPf": folded coefficients */
 typedef struct {
-  double c[10];
-  uint64_t lo_bits, hi_bits;
+  double w[12]; /* sector k = words 4k..4k+3 = {e_k, a_k, b_k, d_k} */
 } dooly_attn_row96; /* 96 bytes */
 
 typedef struct {

@@ -180,6 +180,54 @@ def predict(kind: int, table: dict, sig: np.ndarray, x: np.ndarray) -> dict:
     return {"out": out, "extrap": extrap, "clamped": cl & known, "bad": ~known}
 
 
+def pack_attn(table: dict) -> dict:
+    """The folded 96-B serving table of an attention table (include/dooly_b200.h
+    dooly_attn_row96; csrc/common.cuh fold_row96): coefficients carried into
+    raw-feature space with the row's inv_scale, grouped by feature — sector k
+    = (e_k, a_k, b_k, d_k): a_k = c_{1+k} i_k, b_k = (c_{4+k} i_k) i_k,
+    d_0 = (c7 i_0) i_1, d_1 = (c9 i_1) i_2, d_2 = (c8 i_0) i_2, e_0 = c0 —
+    in this exact rounding order.  Returns {"w": (S, 3, 4) with e_1 = e_2 = 0,
+    "lo", "hi"}."""
+    c = np.asarray(table["coef"], dtype=np.float64)
+    inv = np.asarray(table["inv"], dtype=np.float64)
+    i0, i1, i2 = inv[:, 0], inv[:, 1], inv[:, 2]
+    w = np.zeros((c.shape[0], 3, 4))
+    w[:, 0] = np.stack([c[:, 0], c[:, 1] * i0, (c[:, 4] * i0) * i0, (c[:, 7] * i0) * i1], axis=1)
+    w[:, 1] = np.stack([np.zeros_like(i1), c[:, 2] * i1, (c[:, 5] * i1) * i1, (c[:, 9] * i1) * i2],
+                       axis=1)
+    w[:, 2] = np.stack([np.zeros_like(i2), c[:, 3] * i2, (c[:, 6] * i2) * i2, (c[:, 8] * i0) * i2],
+                       axis=1)
+    return {"w": w, "lo": table["lo"], "hi": table["hi"]}
+
+
+def eval_folded(w: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """The serving row's per-feature 3-way tree over raw features
+    (common.cuh eval_row96): s_k = ((e_k + a_k x_k) + b_k (x_k x_k)) +
+    d_k (x_k x_{k+1 mod 3}); p = (s_0 + s_1) + s_2.  w (..., 3, 4), x (..., 3)."""
+    xf = np.asarray(x, dtype=np.float64)
+    s = []
+    for k in range(3):
+        xk, xn = xf[..., k], xf[..., (k + 1) % 3]
+        e, a, b, d = w[..., k, 0], w[..., k, 1], w[..., k, 2], w[..., k, 3]
+        s.append(((e + a * xk) + b * (xk * xk)) + d * (xk * xn))
+    return (s[0] + s[1]) + s[2]
+
+
+def predict_packed(packed: dict, sig: np.ndarray, x: np.ndarray) -> dict:
+    """SPEC.md:566-574 served from the folded table (DOOLY_KIND_ATTN_PACKED)."""
+    sig = np.asarray(sig, dtype=np.int64)
+    n_sig = packed["w"].shape[0]
+    known = (sig >= 0) & (sig < n_sig)
+    s = np.where(known, sig, 0)
+    lo, hi = packed["lo"][s], packed["hi"][s]
+    known &= lo[:, 0] <= hi[:, 0]
+    xq = np.asarray(x).T
+    out, cl = clamp(eval_folded(packed["w"][s], xq))
+    out = np.where(known, out, np.nan)
+    extrap = np.any((xq < lo) | (xq > hi), axis=1) & known
+    return {"out": out, "extrap": extrap, "clamped": cl & known, "bad": ~known}
+
+
 def predict_one(kind: int, rows: dict, s: int, xs) -> tuple:
     """SPEC.md:566-574 for ONE query in plain Python floats (the per-item form
     of ``predict``; same operation order, so bit-identical):

@@ -24,7 +24,7 @@ LIB_PATH = Path(_os.environ.get("DOOLY_LIB_PATH") or
 KIND_AFFINE = 0
 KIND_ATTN = 1
 KIND_ATTN_PACKED = 2   # predict-only 96-B rows (dooly_attn_pack), see include/dooly_b200.h
-PACK_MAGIC = 0x6B504144
+PACK_MAGIC = 0x66504144   # "DAPf": folded coefficients (include/dooly_b200.h)
 FEAT_NUM_TOKS, FEAT_NUM_SEQS, FEAT_ATTN, FEAT_COMM = 0, 1, 2, 3
 MAX_OPS = 64
 IT_FEATS = 5

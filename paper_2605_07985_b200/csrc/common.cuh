@@ -115,6 +115,50 @@ __device__ __forceinline__ double eval_attn(const AttnRow& r, uint32_t x0, uint3
   return p;
 }
 
+// ---- packed serving rows (DOOLY_KIND_ATTN_PACKED; parity contract) --------
+// The 96-B serving row carries the coefficients FOLDED into raw-feature
+// space (inv = RN(1/hi), 1 if hi == 0), grouped by feature: sector k holds
+// everything that multiplies feature k first,
+//   a_k = c_{1+k} * inv_k,  b_k = (c_{4+k} * inv_k) * inv_k,
+//   d_0 = (c7 * inv_0) * inv_1,  d_1 = (c9 * inv_1) * inv_2,  d_2 = (c8 * inv_0) * inv_2,
+// as words {e_k, a_k, b_k, d_k} with e_0 = c0, e_1 = lo_bits, e_2 = hi_bits.
+// The value is the per-feature 3-way tree over raw features
+//   s_k = ((e'_k + a_k x_k) + b_k (x_k x_k)) + d_k (x_k x_{k+1 mod 3}),
+//   e'_0 = c0, e'_1 = e'_2 = 0,        p = (s_0 + s_1) + s_2,
+// so lane k of a 3-lane group evaluates s_k from its own 32-B sector and its
+// own two feature planes (predict.cu).  oracle/sim.py pack_attn /
+// eval_folded perform the identical operations.
+__device__ __forceinline__ void fold_row96(const double* c, const double* inv, uint64_t lo_bits,
+                                           uint64_t hi_bits, double* w) {
+  w[0] = c[0];
+  w[1] = mul(c[1], inv[0]);
+  w[2] = mul(mul(c[4], inv[0]), inv[0]);
+  w[3] = mul(mul(c[7], inv[0]), inv[1]);
+  w[4] = __longlong_as_double((long long)lo_bits);
+  w[5] = mul(c[2], inv[1]);
+  w[6] = mul(mul(c[5], inv[1]), inv[1]);
+  w[7] = mul(mul(c[9], inv[1]), inv[2]);
+  w[8] = __longlong_as_double((long long)hi_bits);
+  w[9] = mul(c[3], inv[2]);
+  w[10] = mul(mul(c[6], inv[2]), inv[2]);
+  w[11] = mul(mul(c[8], inv[0]), inv[2]);
+}
+
+// s_k of the tree (e = e'_k, x = x_k, y = x_{k+1})
+__device__ __forceinline__ double sector_sum(double e, double a, double b, double d, double x,
+                                             double y) {
+  return add(add(add(e, mul(a, x)), mul(b, mul(x, x))), mul(d, mul(x, y)));
+}
+
+__device__ __forceinline__ double eval_row96(const double* w, uint32_t x0, uint32_t x1,
+                                             uint32_t x2) {
+  const double a = (double)x0, b = (double)x1, c = (double)x2;
+  const double s0 = sector_sum(w[0], w[1], w[2], w[3], a, b);
+  const double s1 = sector_sum(0.0, w[5], w[6], w[7], b, c);
+  const double s2 = sector_sum(0.0, w[9], w[10], w[11], c, a);
+  return add(add(s0, s1), s2);
+}
+
 __device__ __forceinline__ bool affine_valid(const AffineRow& r) { return r.lo <= r.hi; }
 __device__ __forceinline__ bool attn_valid(const AttnRow& r) { return r.lo[0] <= r.hi[0]; }
 

@@ -375,8 +375,8 @@ __device__ __forceinline__ void emit_row(const GridOut& pe, const GridFactor* gf
   status[g] = st;
   if constexpr (KIND == DOOLY_KIND_ATTN) {
     if (pe.packed != nullptr) {
-      // the 96-B serving row, exactly as dooly_attn_pack writes it: c[10],
-      // then the box bit-packed with the table's field widths
+      // the 96-B serving row, exactly as dooly_attn_pack writes it: the
+      // folded coefficients, then the box bit-packed with the table's field widths
       const uint64_t w6 = (uint64_t)__double_as_longlong(r.v[6].y);
       const uint64_t w7a = (uint64_t)__double_as_longlong(r.v[7].x);
       const uint64_t w7b = (uint64_t)__double_as_longlong(r.v[7].y);
@@ -387,10 +387,16 @@ __device__ __forceinline__ void emit_row(const GridOut& pe, const GridFactor* gf
         lb = (uint64_t)lo0 | ((uint64_t)lo1 << gf->pk_s1) | ((uint64_t)lo2 << gf->pk_s2);
         hb = (uint64_t)hi0 | ((uint64_t)hi1 << gf->pk_s1) | ((uint64_t)hi2 << gf->pk_s2);
       }
+      double c[10], inv[3] = {r.v[5].x, r.v[5].y, r.v[6].x}, w[12];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        c[2 * i] = r.v[i].x;
+        c[2 * i + 1] = r.v[i].y;
+      }
+      fold_row96(c, inv, lb, hb, w);
       double2* o = reinterpret_cast<double2*>(pe.packed + 96 * (1 + g));
 #pragma unroll
-      for (int i = 0; i < 5; ++i) o[i] = r.v[i];
-      o[5] = make_double2(__longlong_as_double((long long)lb), __longlong_as_double((long long)hb));
+      for (int i = 0; i < 6; ++i) o[i] = make_double2(w[2 * i], w[2 * i + 1]);
     }
   }
   for (int p = 0; p < pe.n_peers; ++p) {

@@ -17,6 +17,9 @@
 //     each 256-query tile) — no atomics, no byte stores;
 //   * grid = resident CTAs x 148 SMs, grid-stride over 256-query tiles.
 // The evaluation itself (common.cuh) is the bit-exact parity contract.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 
 namespace dooly {
@@ -116,23 +119,30 @@ __device__ __forceinline__ AttnRow gather_attn(const dooly_attn_row* t, uint32_t
   return r;
 }
 
-__device__ __forceinline__ AttnRow gather_attn96(const dooly_attn_row96* t, uint32_t s,
-                                                const PackInfo& pk) {
+struct Row96 {  // folded serving row (include/dooly_b200.h dooly_attn_row96)
+  double w[12];
+  uint32_t lo[3], hi[3];
+};
+
+__device__ __forceinline__ void unpack_box(uint64_t lb, uint64_t hb, const PackInfo& pk,
+                                           uint32_t* lo, uint32_t* hi) {
+  lo[0] = (uint32_t)(lb & pk.m0);
+  lo[1] = (uint32_t)((lb >> pk.s1) & pk.m1);
+  lo[2] = (uint32_t)((lb >> pk.s2) & pk.m2);
+  hi[0] = (uint32_t)(hb & pk.m0);
+  hi[1] = (uint32_t)((hb >> pk.s1) & pk.m1);
+  hi[2] = (uint32_t)((hb >> pk.s2) & pk.m2);
+}
+
+__device__ __forceinline__ Row96 gather_attn96(const dooly_attn_row96* t, uint32_t s,
+                                               const PackInfo& pk) {
   const double* p = reinterpret_cast<const double*>(t + s);
-  AttnRow r;
-  double wl, wh;
-  ld_row_256(p, r.c[0], r.c[1], r.c[2], r.c[3]);
-  ld_row_256(p + 4, r.c[4], r.c[5], r.c[6], r.c[7]);
-  ld_row_256(p + 8, r.c[8], r.c[9], wl, wh);
-  const uint64_t lb = (uint64_t)__double_as_longlong(wl), hb = (uint64_t)__double_as_longlong(wh);
-  r.lo[0] = (uint32_t)(lb & pk.m0);
-  r.lo[1] = (uint32_t)((lb >> pk.s1) & pk.m1);
-  r.lo[2] = (uint32_t)((lb >> pk.s2) & pk.m2);
-  r.hi[0] = (uint32_t)(hb & pk.m0);
-  r.hi[1] = (uint32_t)((hb >> pk.s1) & pk.m1);
-  r.hi[2] = (uint32_t)((hb >> pk.s2) & pk.m2);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) r.inv[k] = inv_of(r.hi[k]);
+  Row96 r;
+  ld_row_256(p, r.w[0], r.w[1], r.w[2], r.w[3]);
+  ld_row_256(p + 4, r.w[4], r.w[5], r.w[6], r.w[7]);
+  ld_row_256(p + 8, r.w[8], r.w[9], r.w[10], r.w[11]);
+  unpack_box((uint64_t)__double_as_longlong(r.w[4]), (uint64_t)__double_as_longlong(r.w[8]), pk,
+             r.lo, r.hi);
   return r;
 }
 
@@ -146,15 +156,14 @@ __device__ __forceinline__ double eval_query(const void* table, int64_t n_sig, u
     return nan64();
   }
   if constexpr (KIND == DOOLY_KIND_ATTN_PACKED) {
-    const AttnRow r =
-        gather_attn96(static_cast<const dooly_attn_row96*>(table) + 1, s, pk);
-    if (!attn_valid(r)) {
+    const Row96 r = gather_attn96(static_cast<const dooly_attn_row96*>(table) + 1, s, pk);
+    if (!(r.lo[0] <= r.hi[0])) {
       bad = true;
       return nan64();
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) extrap |= xs[k] < r.lo[k] || xs[k] > r.hi[k];
-    return clamp_floor(eval_attn(r, xs[0], xs[1], xs[2]), clamped);
+    return clamp_floor(eval_row96(r.w, xs[0], xs[1], xs[2]), clamped);
   } else if constexpr (KIND == DOOLY_KIND_AFFINE) {
     const AffineRow r = gather_affine(static_cast<const dooly_affine_row*>(table), s);
     if (!affine_valid(r)) {
@@ -255,6 +264,136 @@ __global__ void __launch_bounds__(256) predict_vec_kernel(
     atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)bad_min);
 }
 
+// Cooperative packed-attention path (DOOLY_KIND_ATTN_PACKED; opt-in, see
+// predict_attn_mode).
+//
+// The row gather is L1TEX-wavefront-bound: a warp-wide LDG.256 costs one
+// wavefront per distinct 128-B line, so one lane fetching its own 96-B row
+// with three LDG.256 costs ~3 wavefronts per query (predict_vec_kernel).
+// Here THREE lanes share a row: lane k of a group loads sector k, so one
+// LDG.256 covers the whole rows of 10 queries (1.5 lines each on average).
+// The serving row groups its folded coefficients by feature (common.cuh
+// fold_row96), so lane k evaluates the partial sum s_k from its own sector
+// and its own two feature planes (loaded in lane-rotated plane order: no
+// selects), lane 2 adds the two partials it receives by shuffle, clamps and
+// stores.  The box check is split the same way: lane 1 holds lo_bits and
+// tests x < lo, lane 2 holds hi_bits and tests x > hi (one ballot combines
+// them; one shuffle brings lo_0 for the fitted-row test).  Tiles are 160
+// queries: 10 groups x 16 consecutive queries; lanes 30 and 31 idle.
+constexpr int kCoopGroups = 10;
+constexpr int kCoopPerGroup = 16;
+constexpr int kCoopTile = kCoopGroups * kCoopPerGroup;  // 160 queries = 5 flag words
+
+template <int MINB, int B>
+__global__ void __launch_bounds__(256, MINB) predict_attn_coop_kernel(
+    const void* __restrict__ table, int64_t n_sig, const uint32_t* __restrict__ sig,
+    const uint32_t* __restrict__ x, int64_t n_q, double* __restrict__ out,
+    uint32_t* __restrict__ flags, int64_t* __restrict__ err_first) {
+  PackInfo pk = read_pack_header(table, n_sig);
+  if (!pk.ok) n_sig = 0;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / 3, k = lane - 3 * g;
+  const bool act = g < kCoopGroups;
+  const bool k0 = k == 0, k1 = k == 1, k2 = k == 2;
+  const int kn = k2 ? 0 : k + 1, kt = k0 ? 2 : k - 1;  // planes of x_{k+1}, x_{k+2}
+  // this lane's box fields (own / next / third feature) and the x < lo vs
+  // x > hi orientation (lane 1 compares complements: x < lo <=> ~x > ~lo)
+  auto shf = [&](int i) { return i == 0 ? 0u : i == 1 ? pk.s1 : pk.s2; };
+  auto msk = [&](int i) { return i == 0 ? pk.m0 : i == 1 ? pk.m1 : pk.m2; };
+  const uint32_t sh_o = shf(k), sh_n = shf(kn), sh_t = shf(kt);
+  const uint64_t m_o = msk(k), m_n = msk(kn), m_t = msk(kt);
+  const uint32_t flip = k1 ? 0xFFFFFFFFu : 0u;
+  const double* rows =
+      reinterpret_cast<const double*>(static_cast<const dooly_attn_row96*>(table) + 1) + 4 * k;
+  const uint32_t* xo = x + (int64_t)k * n_q;
+  const uint32_t* xn = x + (int64_t)kn * n_q;
+  const uint32_t* xt = x + (int64_t)kt * n_q;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_tiles = (n_q + kCoopTile - 1) / kCoopTile;
+  const int64_t n_words = (n_q + 31) >> 5;
+  const uint32_t nsig32 = n_sig > 0xFFFFFFFFll ? 0xFFFFFFFFu : (uint32_t)n_sig;
+  const uint32_t all_u32 = n_sig > 0xFFFFFFFFll ? 1u : 0u;
+  int64_t bad_min = INT64_MAX;
+
+  for (int64_t tile = warp; tile < n_tiles; tile += n_warps) {
+    const int64_t qg = tile * kCoopTile + g * kCoopPerGroup;
+    uint32_t ebits = 0, cbits = 0;
+#pragma unroll
+    for (int h = 0; h < kCoopPerGroup / 8; ++h) {
+      const int64_t qh = qg + 8 * h;
+      const bool live = act && qh < n_q;  // n_q % 8 == 0: a half is all in or all out
+      // branch-free: dead halves re-read query 0 and unknown signatures read
+      // the header row; both are masked by `valid` (no divergence, so the
+      // shuffles below need no reconvergence)
+      const int64_t qs = live ? qh : 0;
+      const U8 sv = ld_stream_256(sig + qs);
+      const U8 vo = ld_stream_256(xo + qs);
+      const U8 vn = ld_stream_256(xn + qs);
+      const U8 vt = ld_stream_256(xt + qs);
+      double res[8];
+      uint32_t badbits = 0;
+#pragma unroll
+      for (int j0 = 0; j0 < 8; j0 += B) {
+        double a[B][4];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const uint32_t sj = sv.v[j0 + j];
+          // unknown rows read the header row (index -1), masked by `valid`
+          const int64_t rj = ((sj < nsig32) | all_u32) ? (int64_t)sj : -1;
+          ld_row_256(rows + 12 * rj, a[j][0], a[j][1], a[j][2], a[j][3]);
+        }
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+          const int q = j0 + j;
+          const double part = sector_sum(k0 ? a[j][0] : 0.0, a[j][1], a[j][2], a[j][3],
+                                         (double)vo.v[q], (double)vn.v[q]);
+          const double s0 = __shfl_up_sync(0xFFFFFFFFu, part, 2);
+          const double s1 = __shfl_up_sync(0xFFFFFFFFu, part, 1);
+          // box: lanes 1 / 2 test their bound on all three features
+          const uint64_t wb = (uint64_t)__double_as_longlong(a[j][0]);
+          const uint32_t f0 = (uint32_t)(wb & pk.m0);
+          // (bitwise, not short-circuit: no branches around the shuffles)
+          const uint32_t out_any =
+              (uint32_t)((vo.v[q] ^ flip) > ((uint32_t)((wb >> sh_o) & m_o) ^ flip)) |
+              (uint32_t)((vn.v[q] ^ flip) > ((uint32_t)((wb >> sh_n) & m_n) ^ flip)) |
+              (uint32_t)((vt.v[q] ^ flip) > ((uint32_t)((wb >> sh_t) & m_t) ^ flip));
+          const uint32_t below = __ballot_sync(0xFFFFFFFFu, out_any != 0u);
+          const uint32_t lo0 = __shfl_up_sync(0xFFFFFFFFu, f0, 1);
+          // lane 2 finishes (other lanes' results are unused)
+          const uint32_t valid = (uint32_t)live & ((uint32_t)(sv.v[q] < nsig32) | all_u32) &
+                                 (uint32_t)(lo0 <= f0);
+          const double sum = add(add(s0, s1), part);
+          const uint32_t cl = (uint32_t)(sum < DOOLY_CLAMP_FLOOR);
+          const double p = cl ? DOOLY_CLAMP_FLOOR : sum;
+          const uint32_t e = valid & (out_any | ((below >> (lane - 1)) & 1u));
+          res[q] = valid ? p : nan64();
+          ebits |= e << (8 * h + q);
+          cbits |= (valid & cl) << (8 * h + q);
+          badbits |= (valid ^ 1u) << q;
+        }
+      }
+      if (k2 && live && badbits != 0u) bad_min = min(bad_min, qh + (__ffs(badbits) - 1));
+      if (k2 && live) {
+        st_stream_256(out + qh, res[0], res[1], res[2], res[3]);
+        st_stream_256(out + qh + 4, res[4], res[5], res[6], res[7]);
+      }
+    }
+    if (flags != nullptr) {
+      // group g holds the 16 bits of its queries; word w = groups 2w, 2w+1
+      const uint32_t pe = __shfl_down_sync(0xFFFFFFFFu, ebits, 3);
+      const uint32_t pc = __shfl_down_sync(0xFFFFFFFFu, cbits, 3);
+      const int64_t word = tile * (kCoopTile / 32) + (g >> 1);
+      if (k2 && act && (g & 1) == 0 && word < n_words) {
+        flags[word] = (ebits & 0xFFFFu) | (pe << 16);
+        flags[n_words + word] = (cbits & 0xFFFFu) | (pc << 16);
+      }
+    }
+  }
+  if (err_first != nullptr && bad_min != INT64_MAX)
+    atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)bad_min);
+}
+
 // Scalar path (misaligned inputs): one query per thread, flags via ballot.
 template <int KIND>
 __global__ void __launch_bounds__(256) predict_scalar_kernel(
@@ -288,6 +427,21 @@ __global__ void __launch_bounds__(256) predict_scalar_kernel(
   }
 }
 
+// DOOLY_PREDICT_ATTN selects the packed-attention kernel: default one lane per
+// row (predict_vec_kernel, 81 G q/s at C5); "coop" / "coop8" / "coop1" the
+// cooperative 3-lanes-per-row kernel (4 or 8 rows in flight per group, 2 or 1
+// CTAs/SM).  The cooperative form halves the gather wavefronts but issues ~10
+// warp-instructions per query against ~2 (every per-query step is replicated
+// over the group's three lanes) and measured 59 G q/s — profiles/r2_predict.md.
+static int predict_attn_mode() {
+  const char* v = getenv("DOOLY_PREDICT_ATTN");
+  return v == nullptr              ? 1
+         : strcmp(v, "coop") == 0  ? 0
+         : strcmp(v, "coop8") == 0 ? 2
+         : strcmp(v, "coop1") == 0 ? 3
+                                   : 1;
+}
+
 template <int KIND>
 cudaError_t launch_predict_kind(const void* table, int64_t n_sig, const uint32_t* sig,
                                 const uint32_t* x, int64_t n_q, double* out, uint32_t* flags,
@@ -297,7 +451,18 @@ cudaError_t launch_predict_kind(const void* table, int64_t n_sig, const uint32_t
                        ((uintptr_t)out % 32 == 0) && ((uintptr_t)table % 32 == 0) &&
                        (Planes<KIND>::P == 1 || n_q % 8 == 0);
   int per_sm = 0;
-  if (aligned) {
+  const int mode = predict_attn_mode();
+  if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && mode != 1) {
+    auto kern = mode == 2 ? predict_attn_coop_kernel<2, 8>
+              : mode == 3 ? predict_attn_coop_kernel<1, 8>
+                          : predict_attn_coop_kernel<2, 4>;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+    const int64_t tiles = (n_q + kCoopTile - 1) / kCoopTile;
+    int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+    const int64_t need = (tiles + 7) / 8;
+    if (blocks > need) blocks = need;
+    kern<<<(unsigned)blocks, 256, 0, stream>>>(table, n_sig, sig, x, n_q, out, flags, err_first);
+  } else if (aligned) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_vec_kernel<KIND>, 256, 0);
     const int64_t tiles = (n_q + 255) / 256;
     int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 4);
@@ -399,10 +564,11 @@ __global__ void __launch_bounds__(256) attn_pack_write_kernel(const dooly_attn_r
       lb = (uint64_t)r.lo[0] | ((uint64_t)r.lo[1] << s1) | ((uint64_t)r.lo[2] << s2);
       hb = (uint64_t)r.hi[0] | ((uint64_t)r.hi[1] << s1) | ((uint64_t)r.hi[2] << s2);
     }
+    double w[12];
+    fold_row96(r.c, r.inv, lb, hb, w);
     double2* o = reinterpret_cast<double2*>(out + s);
 #pragma unroll
-    for (int i = 0; i < 5; ++i) o[i] = make_double2(r.c[2 * i], r.c[2 * i + 1]);
-    o[5] = make_double2(__longlong_as_double((long long)lb), __longlong_as_double((long long)hb));
+    for (int i = 0; i < 6; ++i) o[i] = make_double2(w[2 * i], w[2 * i + 1]);
   }
 }
 

@@ -282,9 +282,13 @@ PACK_HEADER = np.dtype([("magic", "<u4"), ("ok", "<u4"), ("width", "<u4", 3), ("
 
 def pack_attn(table: torch.Tensor, out: Optional[torch.Tensor] = None,
               check: bool = True) -> torch.Tensor:
-    """Attention table (n_sig, 128) u8 -> packed predict table (n_sig + 1, 96) u8
-    (``KIND_ATTN_PACKED``: 3 sectors per row, inv_scale recomputed as 1/hi, box
-    bit-packed; include/dooly_b200.h).  Bit-identical predictions.  ``check``
+    """Attention table (n_sig, 128) u8 -> packed serving table (n_sig + 1, 96) u8
+    (``KIND_ATTN_PACKED``: 3 sectors per row, coefficients folded into
+    raw-feature space with the row's inv_scale = 1/hi, box bit-packed;
+    include/dooly_b200.h).  Served by the cooperative 3-lanes-per-row kernel
+    with the folded 3-way evaluation tree (oracle/sim.py predict_packed is its
+    bit-exact CPU form; it differs from the 128-B row's evaluation by rounding
+    only, <= 1e-12 relative in the tests).  ``check``
     syncs and raises ValueError when the table is not representable (box widths
     over 64 bits, or an inv_scale that is not 1/hi); unchecked, a bad header
     makes predict flag every query unknown."""

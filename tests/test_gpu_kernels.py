@@ -138,12 +138,47 @@ def test_predict_bit_exact(kind, n_q, offset, dev):
     rows = table_to_rows(kind, table)
     sig, xq = synth_queries(kind, table, n_q, seed=n_q, outside=0.05)
     out, flags, err = _predict_gpu(kind, rows, sig, xq, dev, offset, packed)
-    ref = osim.predict(kind, table, sig, xq)
+    ref = (osim.predict_packed(osim.pack_attn(table), sig, xq) if packed
+           else osim.predict(kind, table, sig, xq))
+    if packed:
+        # the folded serving form vs the scaled evaluation: rounding only
+        # (well inside the north_star's 1e-9 relative on latencies)
+        sc = osim.predict(kind, table, sig, xq)
+        live = ~sc["clamped"]
+        assert np.max(np.abs(ref["out"][live] - sc["out"][live]) / sc["out"][live]) <= 1e-12
+        assert np.array_equal(ref["extrap"], sc["extrap"])
     assert err == np.iinfo(np.int64).max
     assert np.array_equal(out.view(np.uint64), ref["out"].view(np.uint64))   # bit-exact
     nw = (n_q + 31) // 32
     assert np.array_equal(_unpack_bits(flags[0, :nw], n_q), ref["extrap"])
     assert np.array_equal(_unpack_bits(flags[1, :nw], n_q), ref["clamped"])
+
+
+@pytest.mark.parametrize("mode", ["coop", "coop8", "coop1"])
+@pytest.mark.parametrize("n_q", [8, 160 * 7, 160 * 1000 + 88])
+def test_predict_packed_cooperative_kernel(mode, n_q, dev, monkeypatch):
+    """The opt-in cooperative packed-attention kernel (3 lanes per row) is
+    bit-identical to the oracle, flags and unknown/unfitted rows included."""
+    monkeypatch.setenv("DOOLY_PREDICT_ATTN", mode)
+    x, y, off = synth_fit_data(ATTN, 257, 64, seed=21)
+    ref_fit = osim.fit(ATTN, x, y, np.array([0, 3, *off[2:]], dtype=np.int64))  # row 0 unfitted
+    table = {k: ref_fit[k] for k in ("coef", "inv", "lo", "hi")}
+    table["coef"][7, 0] = -1.0
+    table["lo"][0], table["hi"][0] = table["lo"][1], table["hi"][1]             # box, but unfitted
+    rows = table_to_rows(ATTN, table)
+    rows["lo"][0] = 0xFFFFFFFF
+    rows["hi"][0] = 0
+    sig, xq = synth_queries(ATTN, table, n_q, seed=n_q, outside=0.05)
+    sig[::97] = 300                                                             # unknown
+    out, flags, err = _predict_gpu(ATTN, rows, sig, xq, dev, 0, True)
+    tab = dict(table)
+    tab["lo"], tab["hi"] = rows["lo"].copy(), rows["hi"].copy()
+    ref = osim.predict_packed(osim.pack_attn(tab), sig, xq)
+    assert np.array_equal(out.view(np.uint64), ref["out"].view(np.uint64))
+    nw = (n_q + 31) // 32
+    assert np.array_equal(_unpack_bits(flags[0, :nw], n_q), ref["extrap"])
+    assert np.array_equal(_unpack_bits(flags[1, :nw], n_q), ref["clamped"])
+    assert err == int(np.argmax(ref["bad"]))
 
 
 @pytest.mark.parametrize("kind", [AFFINE, ATTN, PACKED])
@@ -203,7 +238,7 @@ def test_attn_pack_header_and_refusals(dev):
     t = lambda tb: torch.from_numpy(table_to_rows(ATTN, tb).view(np.uint8).reshape(64, -1).copy()).to(dev)
     pk = pack_attn(t(table))
     h = pk[0].cpu().numpy().view(PACK_HEADER)[0]
-    assert int(h["ok"]) == 1 and int(h["n_sig"]) == 64 and int(h["magic"]) == 0x6B504144
+    assert int(h["ok"]) == 1 and int(h["n_sig"]) == 64 and int(h["magic"]) == 0x66504144
     assert list(h["max_hi"]) == list(table["hi"].max(axis=0))
     assert list(h["width"]) == [int(v).bit_length() for v in table["hi"].max(axis=0)]
     bad = {k: v.copy() for k, v in table.items()}

@@ -121,13 +121,15 @@ def test_c5_predict_full_size(kind, c5, dev):
     rng = np.random.default_rng(200 + kind)
     q0 = int(rng.integers(0, N_Q - N_ORACLE_Q)) // 256 * 256
     tab = rows_to_table(kind, fr.rows())
+    packed_tab = osim.pack_attn(tab) if kind == ATTN else None
     words = (N_Q + 31) // 32
     fl = flags.cpu().numpy()
     for a in range(q0, q0 + N_ORACLE_Q, 1 << 21):
         b = min(a + (1 << 21), q0 + N_ORACLE_Q)
         s_np = sig[a:b].cpu().numpy().view(np.uint32)
         x_np = x[:, a:b].cpu().numpy().view(np.uint32)
-        ref = osim.predict(kind, tab, s_np, x_np)
+        ref = (osim.predict(kind, tab, s_np, x_np) if kind == AFFINE
+               else osim.predict_packed(packed_tab, s_np, x_np))
         got = out[a:b].cpu().numpy()
         assert np.array_equal(got.view(np.uint64), ref["out"].view(np.uint64))
         bits = np.unpackbits(fl[:, a // 32:(b + 31) // 32].view(np.uint8), axis=1,

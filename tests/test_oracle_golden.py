@@ -251,3 +251,21 @@ def test_predict_one_equals_batch_predict(kind):
         p, e, c = osim.predict_one(kind, rows, int(sig[q]), [int(v) for v in xq[:, q]])
         assert np.float64(p).view(np.uint64) == ref["out"][q].view(np.uint64)
         assert e == bool(ref["extrap"][q]) and c == bool(ref["clamped"][q])
+
+
+def test_packed_serving_form_matches_scaled_evaluation():
+    """The folded 96-B serving form (pack_attn / predict_packed, the contract of
+    DOOLY_KIND_ATTN_PACKED) differs from the scaled 10-column evaluation by
+    rounding only: <= 1e-12 relative, identical flags and unknown rows."""
+    from helpers import synth_queries
+
+    x, y, off = synth_fit_data(ATTN, 300, 48, seed=77)
+    f = osim.fit(ATTN, x, y, off)
+    table = {k: f[k] for k in ("coef", "inv", "lo", "hi")}
+    sig, xq = synth_queries(ATTN, table, 200_000, seed=3, outside=0.05)
+    a = osim.predict(ATTN, table, sig, xq)
+    b = osim.predict_packed(osim.pack_attn(table), sig, xq)
+    live = ~a["clamped"] & ~a["bad"]
+    assert np.max(np.abs(a["out"][live] - b["out"][live]) / a["out"][live]) <= 1e-12
+    for k in ("extrap", "bad"):
+        assert np.array_equal(a[k], b[k])
