@@ -13,16 +13,24 @@ Also measured in the same run and reported as extra keys:
                sweep grid, the attention serving table (96-B rows) written by
                the fit epilogue; at N > 1 the regressor rows reach every rank
                through the fused peer-memory all-gather (NCCL otherwise);
+               roofline per kind (affine HBM, attention FP64 + HBM);
     fits_csr — the same points through the per-signature (CSR) fit;
     dedup    — SHA-256 + first-occurrence dedup of 4M packed records (~1M
                unique); at N > 1 fused digest all-gather (2 ranks) or
                owner-routed all-to-all (4+ ranks);
-    sim      — config C4: Llama-3-70B-like (tp=4) serving replicas, device event
-               loop over a Poisson trace sharded into S fixed replicas;
+    sim      — config C4 as BASELINE.md defines it: Llama-3-70B-like (tp=4),
+               1M-request Poisson trace over S = 64 fixed replicas, device event
+               loop; sim.sim_eval (dooly_sim_eval over the run's own logged
+               iterations: 28 B/iteration HBM and FP64 fractions); s1184 the
+               same trace over 1184 replicas;
     e2e      — the predict batch through the public host API (pinned host
-               buffers, copies inside the timed region);
-    cpu_baseline — the CPU oracle on a bounded sample of the same batch: numpy
-               batch predict (1 thread) and per-item plain Python predict_one.
+               buffers, latencies and flag bit-planes back, copies inside the
+               timed region);
+    cpu_baseline — the CPU oracle on the box's host cores for EVERY metric
+               (predictions here; fits / dedup / sim inside their keys): the
+               per-item oracle on one thread and the numpy oracle over all
+               cores, 1 warm-up + median of 5 on bounded samples, with the
+               host's core count, affinity and BLAS threads.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 torchrun launches one rank per GPU (RANK/LOCAL_RANK/WORLD_SIZE from env).
@@ -299,6 +307,30 @@ def ncu_traffic(kernel_key: str, units: dict):
         return None
 
 
+def l1tex_roofline(nq: dict, k_ms: dict, sm_mhz):
+    """The binding resource of random-row predict: L1TEX data-pipe wavefronts
+    (one per distinct line per warp-wide access, shuffles and shared accesses
+    included; peak 1 per clock per SM — ncu l1tex__data_pipe_lsu_wavefronts
+    against sm__cycles_elapsed).  Wavefronts per query come from the committed
+    ncu measurement (profiles/ncu_summary.json "predict"), the time and clock
+    from this run."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists() or not sm_mhz:
+        return None
+    try:
+        per = json.loads(p.read_text())["predict"]["l1tex_wavefronts_per_unit"]
+    except (ValueError, KeyError):
+        return None
+    wf = sum(float(per[str(k)]) * nq[k] for k in (AFFINE, ATTN))
+    t = (k_ms[AFFINE] + k_ms[ATTN]) / 1e3
+    peak = 148 * sm_mhz * 1e6
+    return {"bound": "l1tex data-pipe wavefronts", "achieved": wf / t / 1e9, "peak": peak / 1e9,
+            "unit": "G wavefronts/s", "frac": wf / t / peak,
+            "wavefronts_per_query": {str(k): float(per[str(k)]) for k in (AFFINE, ATTN)},
+            "source": "profiles/ncu_summary.json predict.l1tex_wavefronts_per_unit (ncu), "
+                      "peak 1/clk/SM x 148 SMs x this run's median SM clock"}
+
+
 class ClockSampler:
     """SM clocks + throttle reasons sampled every ~5 ms through NVML in a
     background thread, restricted to the timed region (mark_start/mark_end)."""
@@ -398,49 +430,276 @@ def max_over_ranks(v: float, dist_on: bool) -> float:
 
 
 # --------------------------------------------------------------- CPU baselines
+#
+# SURVEY §8(d) "CPU path timing": the CPU oracle (oracle/, the restatement of
+# the reference's specified algorithm) on the GPU box's host cores, for every
+# metric the bench reports — predictions, fits, dedup records, sim requests —
+# as two lines each: the per-item oracle (one Python thread, the "reference CPU
+# path") and the vectorised numpy oracle over all host cores (fork pool).
+# Method: 1 warm-up run, then the median of 5 timed runs (time.perf_counter),
+# each run a bounded sample of the same workload (stated per line).
 
 
-_CPU_JOBS: list = []     # set before the fork: workers inherit tables and queries
+_CPU_JOBS: list = []     # set before the fork: workers inherit the job inputs
 
 
-def _oracle_predict_worker(i):
+def host_info() -> dict:
+    """Core count, affinity and BLAS threading of this host."""
+    info = {"os_cpu_count": os.cpu_count(),
+            "affinity_cores": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+            else os.cpu_count(),
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "method": "1 warm-up run, median of 5 timed runs (time.perf_counter)"}
+    try:
+        from threadpoolctl import threadpool_info
+
+        info["blas"] = [{"api": i.get("internal_api"), "threads": i.get("num_threads")}
+                        for i in threadpool_info()]
+    except Exception as exc:  # noqa: BLE001 — report, never guess
+        info["blas"] = f"unavailable ({exc})"
+    return info
+
+
+def one_thread():
+    """BLAS pinned to one thread (per-item lines, and each fork-pool worker so
+    the all-core lines do not oversubscribe the host)."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        return threadpool_limits(1)
+    except Exception:  # noqa: BLE001
+        import contextlib
+
+        return contextlib.nullcontext()
+
+
+def median_rate(fn, units: float, reps: int = 5) -> tuple:
+    """1 warm-up call, then the median of ``reps`` timed calls -> (units/s, median s)."""
+    fn()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    med = float(np.median(ts))
+    return units / med, med
+
+
+def _cpu_all_cores(worker, jobs: list, threads: int, units: float, post=None) -> tuple:
+    """Median-of-5 rate of ``worker`` over ``jobs`` on a fork pool of ``threads``
+    processes (inputs inherited through fork; only job indices cross the pipe
+    inside the timing)."""
+    import multiprocessing as mp
+
+    _CPU_JOBS[:] = jobs
+    ctx = mp.get_context("fork")
+    with ctx.Pool(threads) as pool:
+        def run():
+            out = pool.map(worker, range(len(jobs)), chunksize=1)
+            if post is not None:
+                post(out)
+        return median_rate(run, units)
+
+
+def _w_predict(i):
     from oracle import sim as osim
 
-    t0 = time.perf_counter()
-    osim.predict(*_CPU_JOBS[i])
-    return time.perf_counter() - t0
+    with one_thread():
+        osim.predict(*_CPU_JOBS[i])
+    return 0
 
 
-def cpu_per_item_baseline(tables_host, queries_host, n_items: int) -> dict:
-    """SPEC.md:566's predict(regs, signature_hash, features) one query at a time
-    in plain Python (oracle/sim.py predict_one, one thread) on a bounded sample."""
+def _w_fit(i):
     from oracle import sim as osim
 
-    done, t_total = 0, 0.0
+    kind, x, y = _CPU_JOBS[i]
+    with one_thread():
+        osim.fit_uniform(kind, np.broadcast_to(x, (y.shape[0],) + x.shape), y)
+    return 0
+
+
+def _w_hash(i):
+    from oracle import profiler as oprof
+
+    return [oprof.signature_hash(oprof.canonicalize(e)) for e in _CPU_JOBS[i]]
+
+
+def _w_sim(i):
+    from oracle import sim as osim
+
+    args, kw = _CPU_JOBS[i]
+    osim.run_shard(*args, **kw)
+    return 0
+
+
+def cpu_predictions(tables_host, queries_host, threads: int, n_item: int, n_numpy: int,
+                    n_all: int) -> dict:
+    """Predictions/s of the oracle on the C5 batch's own tables
+    and queries: per-item predict_one (1 thread), numpy predict (1 thread),
+    numpy predict over all cores."""
+    from oracle import sim as osim
+
+    out = {}
+    # per item (plain Python per query)
+    prep = []
     for kind in (AFFINE, ATTN):
         tab = tables_host[kind]
         sig, x = queries_host[kind]
-        m = min(n_items // 2, sig.shape[0])
+        m = min(n_item // 2, sig.shape[0])
         need = sorted({int(v) for v in sig[:m]})
         rows = {i: (tab["coef"][i].tolist(), tab["inv"][i].tolist(), tab["lo"][i].tolist(),
                     tab["hi"][i].tolist()) for i in need}
-        sl = [int(v) for v in sig[:m]]
-        xl = x[:, :m].T.tolist()
-        t0 = time.perf_counter()
-        for q in range(m):
-            osim.predict_one(kind, rows, sl[q], xl[q])
-        t_total += time.perf_counter() - t0
-        done += m
-    return {"value": done / t_total, "unit": "predictions/s", "cores": 1, "kind": "port",
-            "sample": f"{done} queries of the same C5 batch, oracle/sim.py predict_one "
-                      "(plain Python per query, 1 thread)"}
+        prep.append((kind, rows, [int(v) for v in sig[:m]], x[:, :m].T.tolist()))
+
+    def per_item():
+        for kind, rows, sl, xl in prep:
+            for q in range(len(sl)):
+                osim.predict_one(kind, rows, sl[q], xl[q])
+
+    n1 = sum(len(p[2]) for p in prep)
+    with one_thread():
+        rate, med = median_rate(per_item, n1)
+    out["per_item"] = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port",
+                       "sample": f"{n1} queries of the C5 batch, oracle/sim.py predict_one "
+                                 "(plain Python per query)", "median_s": med}
+    # numpy batch, one thread
+    jobs1 = [(k, tables_host[k], queries_host[k][0][:n_numpy // 2],
+              queries_host[k][1][:, :n_numpy // 2]) for k in (AFFINE, ATTN)]
+    n2 = sum(j[2].shape[0] for j in jobs1)
+    with one_thread():
+        rate, med = median_rate(lambda: [osim.predict(*j) for j in jobs1], n2)
+    out["numpy_1thread"] = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port",
+                            "sample": f"{n2} queries of the C5 batch, oracle/sim.py predict "
+                                      "(numpy)", "median_s": med}
+    # numpy over all cores
+    chunk = max(250_000, -(-n_all // (4 * threads)))
+    jobs = []
+    for kind in (AFFINE, ATTN):
+        sig, x = queries_host[kind]
+        m = min(n_all // 2, sig.shape[0])
+        for q0 in range(0, m, chunk):
+            q1 = min(m, q0 + chunk)
+            jobs.append((kind, tables_host[kind], sig[q0:q1], x[:, q0:q1]))
+    n3 = sum(j[2].shape[0] for j in jobs)
+    rate, med = _cpu_all_cores(_w_predict, jobs, threads, n3)
+    out["all_cores"] = {"value": rate, "unit": "predictions/s", "cores": threads, "kind": "port",
+                        "sample": f"{n3} queries of the C5 batch, oracle/sim.py predict (numpy) "
+                                  f"over {threads} processes", "median_s": med}
+    return out
+
+
+def cpu_fits(grid_x: dict, y_sample: dict, threads: int, n_item: int) -> dict:
+    """Fits/s of the oracle (App. A.7) on C5 signatures of the
+    shared sweep grids: per-signature oracle.fit (1 thread) and vectorised
+    fit_uniform over all cores."""
+    from oracle import sim as osim
+
+    out = {}
+    per = {k: max(1, n_item // 2) for k in (AFFINE, ATTN)}
+
+    def per_item():
+        for k in (AFFINE, ATTN):
+            x, y = grid_x[k], y_sample[k][:per[k]]
+            n = x.shape[1]
+            osim.fit(k, np.tile(x, (1, y.shape[0])), y.reshape(-1),
+                     np.arange(y.shape[0] + 1, dtype=np.int64) * n)
+
+    n1 = sum(min(per[k], y_sample[k].shape[0]) for k in (AFFINE, ATTN))
+    with one_thread():
+        rate, med = median_rate(per_item, n1)
+    out["per_item"] = {"value": rate, "unit": "fits/s", "cores": 1, "kind": "port",
+                       "sample": f"{n1} C5 signatures (half affine, half attention) x "
+                                 f"{grid_x[AFFINE].shape[1]} points, oracle/sim.py fit "
+                                 "(one least-squares solve per signature)", "median_s": med}
+    jobs = []
+    for k in (AFFINE, ATTN):
+        y = y_sample[k]
+        for s0 in range(0, y.shape[0], 64):
+            jobs.append((k, grid_x[k], y[s0:s0 + 64]))
+    n2 = sum(y_sample[k].shape[0] for k in (AFFINE, ATTN))
+    rate, med = _cpu_all_cores(_w_fit, jobs, threads, n2)
+    out["all_cores"] = {"value": rate, "unit": "fits/s", "cores": threads, "kind": "port",
+                        "sample": f"{n2} C5 signatures, oracle/sim.py fit_uniform (numpy, 64 "
+                                  f"signatures per job) over {threads} processes",
+                        "median_s": med}
+    return out
+
+
+def packed_as_entries(packed, n: int) -> list:
+    """The first n packed C5 records as runnable-set JSON entries:
+    every model-config dim at its packed position, the kernel symbols, operator
+    granularity — the oracle canonicalises these to the GPU's exact bytes."""
+    w = packed.words
+    sym = [bytes(packed.sym_bytes[packed.sym_off[i]:packed.sym_off[i + 1]]).decode()
+           for i in range(len(packed.sym_off) - 1)]
+    out = []
+    for i in range(n):
+        o = int(packed.rec_off[i])
+        op, nd, ns = int(w[o]), int(w[o + 1]) & 0xFFFF, int(w[o + 1]) >> 16
+        dims = {int(w[o + 4 + 3 * k]): int(w[o + 5 + 3 * k]) | (int(w[o + 6 + 3 * k]) << 32)
+                for k in range(nd)}
+        flat = [[dims[pp], "MC"] if pp in dims else [7, "NT"] for pp in range(max(dims) + 1)]
+        out.append({"granularity": "operator", "name": packed.op_names[op],
+                    "arg_template": [flat], "scalars": [], "attrs": {},
+                    "kernel_symbols": [sym[int(w[o + 4 + 3 * nd + k])] for k in range(ns)],
+                    "repeat_count": int(w[o + 3])})
+    return out
+
+
+def cpu_dedup(entries: list, threads: int, n_item: int) -> dict:
+    """Records/s of the oracle dedup path: canonicalize ->
+    SHA-256 (hashlib) -> first-occurrence dedup (dict), per item on one thread,
+    and with the hashing spread over all cores (the dedup merge in the parent)."""
+    from oracle import profiler as oprof
+
+    out = {}
+    sample = entries[:n_item]
+    rate, med = median_rate(lambda: oprof.dedup_digests(
+        [oprof.signature_hash(oprof.canonicalize(e)) for e in sample]), len(sample))
+    out["per_item"] = {"value": rate, "unit": "records/s", "cores": 1, "kind": "port",
+                       "sample": f"{len(sample)} C5 records, oracle/profiler.py canonicalize + "
+                                 "signature_hash (hashlib) + dedup_digests (dict)",
+                       "median_s": med}
+    step = max(1, -(-len(entries) // (4 * threads)))
+    jobs = [entries[i:i + step] for i in range(0, len(entries), step)]
+    rate, med = _cpu_all_cores(
+        _w_hash, jobs, threads, len(entries),
+        post=lambda parts: oprof.dedup_digests([d for part in parts for d in part]))
+    out["all_cores"] = {"value": rate, "unit": "records/s", "cores": threads, "kind": "port",
+                        "sample": f"{len(entries)} C5 records, canonicalize + hashlib over "
+                                  f"{threads} processes, dict dedup of all digests in the parent",
+                        "median_s": med}
+    return out
+
+
+def cpu_sim(shards: list, kw: dict, threads: int) -> dict:
+    """Requests/s of the oracle serving loop (regression
+    iteration latency, oracle/sim.py run_shard) on C4 replica samples: one
+    shard sample on one thread, and one sample per process over all cores."""
+    from oracle import sim as osim
+
+    out = {}
+    a0 = shards[0]
+    rate, med = median_rate(lambda: osim.run_shard(*a0, **kw), len(a0[0]))
+    out["per_item"] = {"value": rate, "unit": "requests/s", "cores": 1, "kind": "port",
+                       "sample": f"first {len(a0[0])} requests of one C4 replica, oracle/sim.py "
+                                 "run_shard (Python event loop, the GPU's regressor rows)",
+                       "median_s": med}
+    jobs = [(a, kw) for a in shards[:threads]]
+    n = sum(len(a[0]) for a, _ in jobs)
+    rate, med = _cpu_all_cores(_w_sim, jobs, threads, n)
+    out["all_cores"] = {"value": rate, "unit": "requests/s", "cores": threads, "kind": "port",
+                        "sample": f"first {len(a0[0])} requests of each of {len(jobs)} C4 "
+                                  f"replicas, one replica per process", "median_s": med}
+    return out
 
 
 def host_regressor_table(kind: int, n_sig: int, seed: int) -> dict:
-    """Random fitted-looking regressor table for the CPU arm (oracle/sim.py
+    """Random fitted-looking regressor table for the reference arm (oracle/sim.py
     layout): training boxes inside the C5 grids (affine num_toks <= 32768;
     attention prefill_toks <= 32768, batch <= 256, kv_tokens <= 2^22),
-    inv = 1/hi as the fit computes it, small positive coefficients."""
+    inv = 1/hi as the fit computes it, small positive coefficients.  The
+    oracle's predict cost does not depend on the coefficient values."""
     rng = np.random.default_rng(seed)
     caps = [32768] if kind == AFFINE else [32768, 256, 1 << 22]
     hi = np.stack([rng.integers(c // 4, c + 1, n_sig) for c in caps], axis=1).astype(np.uint32)
@@ -449,43 +708,6 @@ def host_regressor_table(kind: int, n_sig: int, seed: int) -> dict:
     p = 2 if kind == AFFINE else 10
     coef = rng.uniform(1e-7, 1e-4, (n_sig, p))
     return {"coef": coef, "inv": inv, "lo": lo, "hi": hi}
-
-
-def cpu_predict_baseline(tables_host, queries_host, threads: int, budget_s: float = 12.0):
-    """Oracle predict (numpy) on a bounded sample; returns (queries/s, sample desc)."""
-    from oracle import sim as osim
-
-    n_total = 0
-    t_total = 0.0
-    n_all = sum(queries_host[k][0].shape[0] for k in queries_host)
-    chunk = 2_000_000 if threads <= 1 else max(250_000, -(-n_all // (4 * threads)))
-    jobs = []
-    for kind in (AFFINE, ATTN):
-        sig, x = queries_host[kind]
-        for q0 in range(0, sig.shape[0], chunk):
-            jobs.append((kind, tables_host[kind], sig[q0:q0 + chunk], x[:, q0:q0 + chunk]))
-    if threads <= 1:
-        t0 = time.perf_counter()
-        for j in jobs:
-            osim.predict(*j)
-            n_total += j[2].shape[0]
-            if time.perf_counter() - t0 > budget_s:
-                break
-        t_total = time.perf_counter() - t0
-    else:
-        import multiprocessing as mp
-
-        # the jobs (tables of C5 size and the query chunks) reach the workers
-        # through fork, so only job indices cross the pipe inside the timing
-        _CPU_JOBS[:] = jobs
-        ctx = mp.get_context("fork")
-        with ctx.Pool(threads) as pool:
-            pool.map(_oracle_predict_worker, range(min(threads, len(jobs))))   # warm the pool
-            t0 = time.perf_counter()
-            pool.map(_oracle_predict_worker, range(len(jobs)), chunksize=1)
-            t_total = time.perf_counter() - t0
-        n_total = sum(j[2].shape[0] for j in jobs)
-    return n_total / t_total, n_total
 
 
 # ------------------------------------------------------------------- main arm
@@ -611,6 +833,17 @@ def run_ours(args):
                     "attention: 16x16x16 (prefill_toks, batch, kv_tokens)); sim.fit_grid",
         "kernel_ms": {"affine": fit_ms[AFFINE] / fit_steps, "attention": fit_ms[ATTN] / fit_steps,
                       "allgather": ag_ms / fit_steps},
+        "roofline_by_kind": {
+            "affine": {"bound": "hbm", "achieved": n_sig[AFFINE] * n_pts[AFFINE] * BYTES_PER_GRID_POINT
+                       / (fit_ms[AFFINE] / fit_steps / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                       "frac": n_sig[AFFINE] * n_pts[AFFINE] * BYTES_PER_GRID_POINT
+                       / (fit_ms[AFFINE] / fit_steps / 1e3) / 1e9 / hbm_peak},
+            "attention": {"bound": "fp64 (see fp64_attention); hbm alongside",
+                          "hbm_achieved": n_sig[ATTN] * n_pts[ATTN] * BYTES_PER_GRID_POINT
+                          / (fit_ms[ATTN] / fit_steps / 1e3) / 1e9, "hbm_peak": hbm_peak,
+                          "unit": "GB/s",
+                          "hbm_frac": n_sig[ATTN] * n_pts[ATTN] * BYTES_PER_GRID_POINT
+                          / (fit_ms[ATTN] / fit_steps / 1e3) / 1e9 / hbm_peak}},
         "launches_per_step": fit_launches,
         "allgather_path": None if not dist_on else (
             "fused: peer-memory row stores in the fit epilogue + device arrival counter"
@@ -665,6 +898,12 @@ def run_ours(args):
                     "alg_bytes_per_point": BYTES_PER_POINT,
                     "max_coef_rel_diff_vs_grid": worst,
                     "path": "sim.fit_tables (dooly_fit): per-signature points, Gram per signature"}
+    cpu_on = rank == 0 and world == 1 and args.cpu_sample > 0
+    cpu_fit_in = None
+    if cpu_on:
+        m = max(2, args.cpu_fit_sigs // 2)
+        cpu_fit_in = ({k: fit_in[k][0].cpu().numpy().view(np.uint32) for k in (AFFINE, ATTN)},
+                      {k: fit_in[k][1][:m].cpu().numpy() for k in (AFFINE, ATTN)})
     del fit_in
     pack_attn(fit_out[ATTN].table, packed96, check=True)   # raises if not representable
     rows128 = {k: fit_out[k].table for k in (AFFINE, ATTN)}
@@ -720,7 +959,8 @@ def run_ours(args):
         host_q = {}
         for k in (AFFINE, ATTN):
             host_q[k] = (qs[k][0][: n_e[k]].cpu().pin_memory(), qs[k][1][:, : n_e[k]].cpu().pin_memory(),
-                         torch.empty(n_e[k], dtype=torch.float64).pin_memory())
+                         torch.empty(n_e[k], dtype=torch.float64).pin_memory(),
+                         torch.empty((2, (n_e[k] + 31) // 32), dtype=torch.int32).pin_memory())
         batches = [(pkind[k], tables[k], *host_q[k]) for k in (AFFINE, ATTN)]
         for _ in range(2):
             predict_host_many(batches)
@@ -732,18 +972,20 @@ def run_ours(args):
         barrier_sync(dist_on)
         e_s = max_over_ranks((time.perf_counter() - t0) / e_steps, dist_on)
         h2d = sum(host_q[k][0].numel() * 4 + host_q[k][1].numel() * 4 for k in (AFFINE, ATTN))
-        d2h = sum(host_q[k][2].numel() * 8 for k in (AFFINE, ATTN))
+        d2h = sum(host_q[k][2].numel() * 8 + host_q[k][3].numel() * 4 for k in (AFFINE, ATTN))
         e2e = {"value": world * args.e2e_queries / e_s, "unit": "predictions/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "queries_per_step_per_gpu": args.e2e_queries,
-               "path": "sim.predict_host_many: pinned host -> device -> kernel -> host, both kinds' "
-                       "chunks interleaved over 3 streams",
+               "path": "sim.predict_host_many: pinned host -> device -> kernel -> host (latencies "
+                       "and the extrapolation/clamp flag bit-planes), both kinds' chunks "
+                       "interleaved over 3 streams",
                "link_ceiling": link_ceiling(host_q[AFFINE][2], dev, h2d, d2h, e_s)}
         del host_q
 
-    # ---------------- CPU baseline (rank 0, N=1 only)
+    # ---------------- CPU baselines (rank 0, N=1 only)
     cpu = None
-    if rank == 0 and world == 1 and args.cpu_sample > 0:
+    cpu_threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    if cpu_on:
         tables_host = {}
         qh = {}
         sys.path.insert(0, str(ROOT / "tests"))
@@ -755,11 +997,13 @@ def run_ours(args):
             m = args.cpu_sample // 2
             qh[k] = (qs[k][0][:m].cpu().numpy().view(np.uint32),
                      qs[k][1][:, :m].cpu().numpy().view(np.uint32))
-        rate, n_done = cpu_predict_baseline(tables_host, qh, threads=1)
-        cpu = {"value": rate, "unit": "predictions/s", "cores": 1, "kind": "port",
-               "sample": f"{n_done} queries (half affine, half attention) of the same C5 batch, "
-                         "oracle/sim.py predict (numpy, 1 thread)",
-               "per_item": cpu_per_item_baseline(tables_host, qh, args.cpu_sample_items)}
+        lines = cpu_predictions(tables_host, qh, cpu_threads, args.cpu_sample_items,
+                                args.cpu_sample // 5, args.cpu_sample)
+        cpu = dict(lines["numpy_1thread"], per_item=lines["per_item"], all_cores=lines["all_cores"],
+                   host=host_info())
+        fits["cpu_baseline"] = dict(cpu_fits(*cpu_fit_in, cpu_threads, args.cpu_fit_items),
+                                    host=host_info())
+        del tables_host, qh
 
     # ---------------- dedup sub-benchmark
     dedup = None
@@ -840,10 +1084,20 @@ def run_ours(args):
                      "note": "compression rounds only; canonical-message construction and "
                              "lock-step padding of shorter messages are the remainder"}}
 
+        if cpu_on:
+            ents = packed_as_entries(packed, args.cpu_dedup_records)
+            from oracle import profiler as oprof
+
+            for i in range(0, len(ents), max(1, len(ents) // 50)):   # the CPU path hashes the same bytes
+                want = bytes(r.digests[i].cpu().numpy())
+                assert oprof.signature_hash(oprof.canonicalize(ents[i])) == want
+            dedup["cpu_baseline"] = dict(cpu_dedup(ents, cpu_threads, args.cpu_dedup_items),
+                                         host=host_info())
+
     # ---------------- sim sub-benchmark (C4)
     sim = None
     if args.sim_requests > 0:
-        sim = bench_sim(args, dev, dist_on, rank, world)
+        sim = bench_sim(args, dev, dist_on, rank, world, cpu_threads if cpu_on else 0)
 
     if rank == 0:
         line = {
@@ -860,7 +1114,8 @@ def run_ours(args):
                          if peak_kind == "measured" else "fallback 6.65 TB/s",
                          "kernel_ms": {"affine": k_ms[AFFINE], "attention": k_ms[ATTN]},
                          "alg_bytes_per_query": BYTES_PER_QUERY,
-                         "gather_ceiling": gather_ceiling(nq, k_ms)},
+                         "gather_ceiling": gather_ceiling(nq, k_ms),
+                         "l1tex": l1tex_roofline(nq, k_ms, clocks.get("sm_mhz"))},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "fits": fits, "fits_csr": fits_csr, "dedup": dedup, "sim": sim, "unknown_signature_errors": bad,
         }
@@ -870,15 +1125,35 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def bench_sim(args, dev, dist_on, rank, world):
-    """C4: Llama-3-70B-like tp=4 replicas; regressors from the C4 manifest's sweep."""
+def c4_trace(n: int, S: int, rate_per_replica: float):
+    """C4 trace: Poisson arrivals at rate_per_replica x S,
+    Table-3 length distributions (lognormal with the medians/means of
+    PAPER.md:621-623), seed 1."""
+    rng = np.random.default_rng(1)
+    arr = np.cumsum(rng.exponential(1.0 / (rate_per_replica * S), size=n))
+    sig_p = math.sqrt(2 * math.log(1232 / 950))
+    sig_o = math.sqrt(2 * math.log(397 / 388))
+    pr = np.clip(np.rint(rng.lognormal(math.log(950), sig_p, n)), 1, 8192 - 512).astype(np.uint32)
+    ou = np.clip(np.rint(rng.lognormal(math.log(388), sig_o, n)), 1, 512).astype(np.uint32)
+    return arr, pr, ou, np.zeros(n, np.uint32)
+
+
+def bench_sim(args, dev, dist_on, rank, world, cpu_threads: int = 0):
+    """C4: Llama-3-70B-like tp=4 serving replicas; regressors from the C4
+    manifest's sweep.  The headline sim line is C4 as defined (S = 64 fixed
+    replicas, request i -> replica i mod S, replicas round-robin over ranks);
+    ``s1184`` reruns the trace over 1184 replicas (8 per SM) as a throughput
+    extra; ``sim_eval`` times dooly_sim_eval (K4a iteration evaluation + the
+    per-replica clock scan + per-request TTFT/TPOT) over the C4 run's own
+    logged iterations."""
     import torch
 
+    from paper_2605_07985_b200 import _lib
     from paper_2605_07985_b200 import dist as ddist
     from paper_2605_07985_b200 import modelir
     from paper_2605_07985_b200.profiler import profile_corpus
     from paper_2605_07985_b200.sim import (SchedConfig, ShardedTrace, build_calltree, fit,
-                                           make_sched, run_sharded)
+                                           make_sched, run_sharded, sim_eval)
 
     man = modelir.load_manifest(modelir.builtin_manifest_path("llama70b"))
     model, backend, hw = man.models[0], man.backends[1], man.hardware
@@ -888,48 +1163,132 @@ def bench_sim(args, dev, dist_on, rank, world):
     ct = build_calltree(model, backend, regs, hw, man.tp_degree)
     sched = SchedConfig(chunk=8192, max_batch=256)
     cfg = make_sched(model, hw, man.tp_degree, sched, ct)
-    # trace: Poisson, Table-3 lengths, shards S fixed; this rank simulates shards s = rank mod world
     n = args.sim_requests
-    rng = np.random.default_rng(1)
-    rate = args.sim_rate * args.sim_shards
-    arr = np.cumsum(rng.exponential(1.0 / rate, size=n))
-    sig_p = math.sqrt(2 * math.log(1232 / 950))
-    sig_o = math.sqrt(2 * math.log(397 / 388))
-    pr = np.clip(np.rint(rng.lognormal(math.log(950), sig_p, n)), 1, 8192 - 512).astype(np.uint32)
-    ou = np.clip(np.rint(rng.lognormal(math.log(388), sig_o, n)), 1, 512).astype(np.uint32)
-    ca = np.zeros(n, np.uint32)
+    conf = (f"llama-3-70b-like tp=4 flashattention-like on a100-like; Poisson "
+            f"{args.sim_rate} req/s per replica; chunk 8192, max_batch 256")
+
+    def run_c4(S, log_cap=0):
+        arr, pr, ou, ca = c4_trace(n, S, args.sim_rate)
+        mine = np.arange(S)[np.arange(S) % world == rank]
+        sel = np.concatenate([np.arange(s, n, S) for s in mine])
+        sel.sort()
+        trace = ShardedTrace.from_arrays(arr[sel], pr[sel], ou[sel], ca[sel], len(mine), dev)
+        res = run_sharded(trace, ct, cfg, regs)      # warm-up
+        barrier_sync(dist_on)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = run_sharded(trace, ct, cfg, regs, out=res)
+        e1.record()
+        barrier_sync(dist_on)
+        ms = max_over_ranks(e0.elapsed_time(e1), dist_on)
+        if log_cap:   # untimed rerun with the per-iteration log (sim_eval's inputs)
+            res = run_sharded(trace, ct, cfg, regs, log_cap=log_cap)
+        ok = int((res.status != 0).sum().item()) == 0
+        ttft = res.ttft.cpu()
+        if dist_on:   # global percentiles: every rank's TTFTs, NaN-padded to a common length
+            m = int(max_over_ranks(float(ttft.numel()), dist_on))
+            pad = torch.full((m,), float("nan"), dtype=torch.float64)
+            pad[: ttft.numel()] = ttft
+            ttft = ddist.gather_requests(pad.to(dev)).reshape(-1).cpu()
+            ok = max_over_ranks(0.0 if ok else 1.0, dist_on) == 0.0
+        ttft = ttft.numpy()
+        n_it = int(res.n_iter.sum().item())
+        line = {"value": n / (ms / 1e3), "unit": "requests/s", "ms": ms, "requests": n,
+                "shards": S, "iterations_rank0": n_it, "iterations_per_s": n_it / (ms / 1e3),
+                "max_iterations_per_replica": int(res.n_iter.max().item()), "all_ok": ok,
+                "ttft_p50_s": float(np.nanpercentile(ttft, 50)),
+                "ttft_p99_s": float(np.nanpercentile(ttft, 99)), "config": conf + f" x {S} replicas"}
+        return line, trace, res, (arr, pr, ou, ca)
+
     S = args.sim_shards
-    mine = np.arange(S)[np.arange(S) % world == rank]
-    sel = np.concatenate([np.arange(s, n, S) for s in mine])
-    sel.sort()
-    trace = ShardedTrace.from_arrays(arr[sel], pr[sel], ou[sel], ca[sel], len(mine), dev)
-    for _ in range(1):
-        res = run_sharded(trace, ct, cfg, regs)
-    barrier_sync(dist_on)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    res = run_sharded(trace, ct, cfg, regs, out=res)
-    e1.record()
-    barrier_sync(dist_on)
-    ms = max_over_ranks(e0.elapsed_time(e1), dist_on)
-    n_it = int(res.n_iter.sum().item())
-    ok = int((res.status != 0).sum().item()) == 0
-    ttft = res.ttft.cpu()
-    if dist_on:   # global percentiles: every rank's TTFTs, NaN-padded to a common length
-        m = int(max_over_ranks(float(ttft.numel()), dist_on))
-        pad = torch.full((m,), float("nan"), dtype=torch.float64)
-        pad[: ttft.numel()] = ttft
-        ttft = ddist.gather_requests(pad.to(dev)).reshape(-1).cpu()
-        ok = max_over_ranks(0.0 if ok else 1.0, dist_on) == 0.0
-    ttft = ttft.numpy()
-    return {"value": n / (ms / 1e3), "unit": "requests/s", "ms": ms, "requests": n,
-            "shards": S, "iterations_rank0": n_it,
-            "iterations_per_s": n_it / (ms / 1e3), "all_ok": ok,
-            "ttft_p50_s": float(np.nanpercentile(ttft, 50)),
-            "ttft_p99_s": float(np.nanpercentile(ttft, 99)),
-            "config": f"llama-3-70b-like tp=4 flashattention-like on a100-like; Poisson "
-                      f"{args.sim_rate} req/s per replica x {S} replicas; chunk 8192, max_batch 256",
-            "bound": "latency (sequential per-replica event loop, one warp per replica; exact decode windows evaluate up to 32 event-free iterations in parallel)"}
+    sim, trace, res, c4 = run_c4(S, log_cap=args.sim_log_cap)
+    sim["bound"] = ("latency: each replica's event loop is sequential (SPEC.md:638); one warp "
+                    "per replica, exact decode windows evaluate up to 32 event-free iterations "
+                    "in parallel; S = 64 replicas occupy 64 warps of the GPU")
+    # ---- dooly_sim_eval over the C4 run's logged iterations (28 B per iteration
+    # + 36 B per request); every logged iteration of every replica
+    if args.sim_log_cap > 0:
+        n_it = res.n_iter.cpu().numpy()
+        if int(n_it.max()) <= args.sim_log_cap:
+            S_mine = trace.n_shards
+            feats = torch.cat([res.log_feat[s, :int(n_it[s])] for s in range(S_mine)]).t().contiguous()
+            off = torch.from_numpy(np.concatenate([[0], np.cumsum(n_it)]).astype(np.int64)).to(dev)
+            it_start = torch.zeros(feats.shape[1], dtype=torch.float64, device=dev)
+            # request -> a (first, last) iteration pair inside its replica (timing input)
+            g = torch.Generator(device=dev)
+            g.manual_seed(5)
+            req_shard = torch.repeat_interleave(torch.arange(S_mine, device=dev),
+                                                trace.shard_off[1:] - trace.shard_off[:-1])
+            lo = off[:-1][req_shard]
+            span = (off[1:] - off[:-1])[req_shard]
+            f_it = (lo + (torch.rand(req_shard.numel(), generator=g, device=dev, dtype=torch.float64)
+                          * span).long()).int()
+            l_it = torch.minimum(f_it.long() + 380, off[1:][req_shard] - 1).int()
+            def once():
+                return sim_eval(ct, regs, feats, trace.arrival, f_it, l_it, trace.output,
+                                it_start=it_start, it_off=off)
+            once()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            l0 = _lib.launch_count(dev)
+            e0.record()
+            once()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            N_it, N_req = feats.shape[1], trace.arrival.numel()
+            nbytes = N_it * 28 + N_req * 36
+            feat_of = [ct.oplist.feat[i] for i in range(ct.n_ops)]
+            # FP64 instructions per iteration of the call graph's evaluation:
+            # affine entry 5 (scale, multiply, add, clamp, repeat product) + 1
+            # add; attention entry 27 (3 scalings, 6 monomials, 9 products, 9
+            # adds) + repeat product + add; comm entry 6
+            fp64_per_it = sum(6 if f in (_lib.FEAT_NUM_TOKS, _lib.FEAT_NUM_SEQS) else
+                              29 if f == _lib.FEAT_ATTN else 6 for f in feat_of)
+            sim["sim_eval"] = {
+                "iterations": N_it, "requests": N_req, "ms": ms,
+                "iterations_per_s": N_it / (ms / 1e3), "launches": _lib.launch_count(dev) - l0,
+                "roofline": {"hbm_achieved_gbs": nbytes / (ms / 1e3) / 1e9,
+                             "hbm_frac": nbytes / (ms / 1e3) / 1e9 / load_peaks()[0],
+                             "fp64_achieved_tinstr": N_it * fp64_per_it / (ms / 1e3) / 1e12,
+                             "fp64_frac": N_it * fp64_per_it / (ms / 1e3) / 1e12 / FP64_PEAK_TINSTR,
+                             "alg_bytes": "28 B/iteration (5 u32 features in, f64 out) + 36 B/request",
+                             "fp64_instr_per_iteration": fp64_per_it},
+                "inputs": "the S = 64 C4 run's logged per-iteration features (every iteration of "
+                          "every replica); it_start zero (no idle jumps), per-request first/last "
+                          "iterations drawn inside the request's replica",
+                "bound": "the per-replica clock scan is sequential f64 (App. A.11): 64 replicas "
+                         "= 64 warps; the iteration evaluation itself is parallel"}
+            del feats, it_start
+    if args.sim_wide_shards > 0:
+        wide, _, _, _ = run_c4(args.sim_wide_shards)
+        sim["s1184" if args.sim_wide_shards == 1184 else f"s{args.sim_wide_shards}"] = wide
+    # ---- CPU oracle serving loop on replica samples (rank 0, N = 1)
+    if cpu_threads and rank == 0 and world == 1:
+        sys.path.insert(0, str(ROOT / "tests"))
+        from helpers import AFFINE as HA, ATTN as HT, rows_to_table
+
+        tabs = {k: rows_to_table(k, regs.tables[k].rows()) for k in regs.tables}
+        ops = []
+        for i in range(ct.n_ops):
+            feat, row = ct.oplist.feat[i], ct.oplist.row[i]
+            op = {"feat": feat, "repeat": ct.oplist.repeat[i],
+                  "window_slot": ct.oplist.window_slot[i], "bytes_per_tok": ct.oplist.bytes_per_tok[i]}
+            if feat != _lib.FEAT_COMM:
+                t = tabs[HT if feat == _lib.FEAT_ATTN else HA]
+                op.update(coef=list(t["coef"][row]), inv=list(t["inv"][row]))
+            ops.append(op)
+        arr, pr, ou, ca = c4
+        m = args.cpu_sim_requests
+        shards = []
+        for s_ in range(min(S, cpu_threads)):
+            idx = np.arange(s_, n, S)[:m]
+            shards.append((arr[idx].tolist(), pr[idx].tolist(), ou[idx].tolist(), ca[idx].tolist()))
+        kw = dict(ops=ops, chunk=8192, max_batch=256, kv_bytes_per_token=cfg.kv_bytes_per_token,
+                  kv_capacity=cfg.kv_capacity_bytes, window=ct.window, tp=man.tp_degree,
+                  alpha=hw.comm_alpha, beta=hw.comm_beta)
+        sim["cpu_baseline"] = dict(cpu_sim(shards, kw, cpu_threads), host=host_info())
+    return sim
 
 
 # ---------------------------------------------------------------- reference arm
@@ -951,15 +1310,26 @@ def run_reference(args):
         # serves), boxes spanning the C5 sweep grids; queries inside the boxes
         tables[k] = host_regressor_table(k, args.sigs // 2, seed=k)
         qh[k] = synth_queries(k, tables[k], args.ref_sample // 2, seed=k + 1)
-    for _ in range(args.warmup):
-        cpu_predict_baseline(tables, {k: (qh[k][0][:100000], qh[k][1][:, :100000])
-                                      for k in qh}, threads=1)
+    import multiprocessing as mp
+
+    chunk = max(250_000, -(-args.ref_sample // (4 * threads)))
+    jobs = []
+    for kind in (AFFINE, ATTN):
+        sig, x = qh[kind]
+        for q0 in range(0, sig.shape[0], chunk):
+            jobs.append((kind, tables[kind], sig[q0:q0 + chunk], x[:, q0:q0 + chunk]))
+    _CPU_JOBS[:] = jobs
+    n_done = sum(j[2].shape[0] for j in jobs)
     times = []
-    for _ in range(args.steps):
-        rate, n_done = cpu_predict_baseline(tables, qh, threads=threads)
-        times.append(n_done / rate)
-    ms = 1e3 * float(np.mean(times))
-    value = args.ref_sample / (ms / 1e3)
+    with mp.get_context("fork").Pool(threads) as pool:
+        for _ in range(max(1, args.warmup)):
+            pool.map(_w_predict, range(len(jobs)), chunksize=1)
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            pool.map(_w_predict, range(len(jobs)), chunksize=1)
+            times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.median(times))
+    value = n_done / (ms / 1e3)
     line = {"impl": "reference",
             "metric": "latency predictions/s (C5 predict batch; fits/s, dedup, sim alongside)",
             "value": value, "unit": "predictions/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -971,8 +1341,10 @@ def run_reference(args):
                               "queries_per_step": args.ref_sample},
             "cpu_baseline": {"value": value, "unit": "predictions/s", "cores": threads,
                              "kind": "port",
-                             "sample": f"{args.ref_sample} queries per step, oracle/sim.py "
-                                       f"predict over {threads} processes"},
+                             "sample": f"{n_done} queries per step, oracle/sim.py "
+                                       f"predict over {threads} processes (median of "
+                                       f"{args.steps} steps after {max(1, args.warmup)} warm-up)",
+                             "host": host_info()},
             "e2e": {"value": value, "unit": "predictions/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -991,12 +1363,21 @@ def main(argv=None):
     ap.add_argument("--records", type=int, default=4_000_000)
     ap.add_argument("--e2e-queries", type=int, default=200_000_000)
     ap.add_argument("--cpu-sample", type=int, default=20_000_000)
-    ap.add_argument("--cpu-sample-items", type=int, default=400_000,
+    ap.add_argument("--cpu-sample-items", type=int, default=200_000,
                     help="queries of the per-item (plain Python) CPU line")
     ap.add_argument("--ref-sample", type=int, default=40_000_000)
     ap.add_argument("--sim-requests", type=int, default=1_000_000)
-    ap.add_argument("--sim-shards", type=int, default=1184)
+    ap.add_argument("--sim-shards", type=int, default=64, help="C4: S fixed replicas")
+    ap.add_argument("--sim-wide-shards", type=int, default=1184,
+                    help="extra sim line over this many replicas (0: skip)")
     ap.add_argument("--sim-rate", type=float, default=4.0)
+    ap.add_argument("--sim-log-cap", type=int, default=400_000,
+                    help="per-replica iteration log for the sim_eval timing (0: skip)")
+    ap.add_argument("--cpu-fit-sigs", type=int, default=2048)
+    ap.add_argument("--cpu-fit-items", type=int, default=64)
+    ap.add_argument("--cpu-dedup-records", type=int, default=400_000)
+    ap.add_argument("--cpu-dedup-items", type=int, default=50_000)
+    ap.add_argument("--cpu-sim-requests", type=int, default=1000)
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the bench contract requires --warmup >= 3", file=sys.stderr)

@@ -224,7 +224,7 @@ class LatencyDB:
     model_operations: list = field(default_factory=list)   # (config_id, digest, repeat)
     measurements: dict = field(default_factory=dict)       # digest -> (x (p, n) u32, y f64)
     workloads: dict = field(default_factory=dict)          # digest -> [workload dict | None] per point
-    sources: dict = field(default_factory=dict)            # digest -> "oracle" | "imported"
+    sources: dict = field(default_factory=dict)            # digest -> ["oracle" | "imported"] per point
     comm_measurements: dict = field(default_factory=dict)  # (topology, tp, bytes) -> latency_s
     _index: dict = field(default_factory=dict)
 
@@ -274,6 +274,7 @@ class LatencyDB:
         if np.any(~(y > 0)):
             raise OraclePanic(f"{digest.hex()[:12]}: latency_s must be > 0 (SPEC.md:427)")
         wl = list(workloads) if workloads is not None else [None] * y.shape[0]
+        src = [source] * y.shape[0]
         if digest in self.measurements:
             ox, oy = self.measurements[digest]
             old = {tuple(ox[:, i]): oy[i] for i in range(oy.shape[0])}
@@ -288,9 +289,19 @@ class LatencyDB:
             x = np.concatenate([ox, x[:, keep]], axis=1)
             y = np.concatenate([oy, y[keep]])
             wl = self.workloads.get(digest, [None] * oy.shape[0]) + [wl[i] for i in keep]
+            src = self.point_sources(digest) + [source] * len(keep)
         self.measurements[digest] = (x, y)
         self.workloads[digest] = wl
-        self.sources.setdefault(digest, source)
+        self.sources[digest] = src
+
+    def point_sources(self, digest: bytes) -> list:
+        """Source of every measurement point of a signature (SPEC D4: oracle or
+        imported, tracked per point)."""
+        n = self.measurements[digest][1].shape[0] if digest in self.measurements else 0
+        src = self.sources.get(digest)
+        if src is None:
+            return ["oracle"] * n
+        return [src] * n if isinstance(src, str) else list(src)
 
     def insert_comm(self, topology: str, tp_degree: int, nbytes: int, latency_s: float) -> None:
         """comm sub-schema keyed by hardware topology (Appendix E)."""
@@ -308,20 +319,29 @@ class LatencyDB:
 
     def save(self, path) -> None:
         """Persist: ``.npz`` snapshot, or the single-file SQLite store (D5) for any
-        other suffix (``store.save``)."""
+        other suffix (``store.save``).  The snapshot holds plain arrays only (the
+        metadata as one UTF-8 JSON array) and loads with allow_pickle=False; it
+        keeps every table (components, per-point workloads and sources, comm)."""
         if not str(path).endswith(".npz"):
             from .store import save
 
             save(self, path)
             return
-        sig = np.array([[s.digest.hex(), s.op_name, s.granularity, str(s.kind), s.feature]
-                        for s in self.signatures], dtype=object)
-        meas = {f"x_{d.hex()}": v[0] for d, v in self.measurements.items()}
-        meas.update({f"y_{d.hex()}": v[1] for d, v in self.measurements.items()})
-        np.savez(path, signatures=sig,
-                 configurations=np.array(self.configurations, dtype=object),
-                 model_operations=np.array([(c, d.hex(), r) for c, d, r in self.model_operations],
-                                           dtype=object), **meas)
+        import json
+
+        meta = {"configurations": [list(c) for c in self.configurations],
+                "signatures": [[r.digest.hex(), r.op_name, r.granularity, int(r.kind), r.feature,
+                                r.components] for r in self.signatures],
+                "model_operations": [[int(c), d.hex(), int(r)] for c, d, r in self.model_operations],
+                "workloads": {d.hex(): w for d, w in self.workloads.items()},
+                "sources": {d.hex(): self.point_sources(d) for d in self.measurements},
+                "comm": [[t, int(tp), int(b), float(v)]
+                         for (t, tp, b), v in self.comm_measurements.items()]}
+        arrays = {"meta": np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8)}
+        for d, (x, y) in self.measurements.items():
+            arrays[f"x_{d.hex()}"] = np.ascontiguousarray(x, dtype=np.uint32)
+            arrays[f"y_{d.hex()}"] = np.ascontiguousarray(y, dtype=np.float64)
+        np.savez(path, **arrays)
 
     @staticmethod
     def load(path) -> "LatencyDB":
@@ -329,22 +349,28 @@ class LatencyDB:
             from .store import load
 
             return load(path)
+        import json
+
         try:
-            z = np.load(path, allow_pickle=True)
-        except OSError as exc:
-            raise StoreUnavailable(str(exc)) from exc
+            z = np.load(path, allow_pickle=False)
+            meta = json.loads(bytes(z["meta"]).decode())
+        except (OSError, KeyError, ValueError) as exc:
+            raise StoreUnavailable(f"{path}: {exc}") from exc
         db = LatencyDB()
-        db.configurations = [tuple(c) for c in z["configurations"].tolist()]
-        for h, name, gran, kind, feat in z["signatures"].tolist():
+        db.configurations = [tuple(c) for c in meta["configurations"]]
+        for h, name, gran, kind, feat, comp in meta["signatures"]:
             d = bytes.fromhex(h)
             db._index[d] = len(db.signatures)
-            db.signatures.append(SignatureRow(d, name, gran, int(kind), feat))
+            db.signatures.append(SignatureRow(d, name, gran, int(kind), feat, comp))
         db.model_operations = [(int(c), bytes.fromhex(h), int(r))
-                               for c, h, r in z["model_operations"].tolist()]
+                               for c, h, r in meta["model_operations"]]
         for key in z.files:
             if key.startswith("x_"):
                 d = bytes.fromhex(key[2:])
                 db.measurements[d] = (z[key], z["y_" + key[2:]])
+        db.workloads = {bytes.fromhex(h): w for h, w in meta["workloads"].items()}
+        db.sources = {bytes.fromhex(h): s for h, s in meta["sources"].items()}
+        db.comm_measurements = {(t, tp, b): v for t, tp, b, v in meta["comm"]}
         return db
 
 
@@ -626,31 +652,87 @@ def profile_fit(items: Sequence, hw: HardwareSpec, grid: SweepGrid, device=None,
 
 def profile_and_fit(manifest, db: Optional[LatencyDB] = None, device=None,
                     grid: Optional[SweepGrid] = None):
-    """cmd_profile + fit with the fused K5 path: GPU dedup of every runnable set
-    (model_operations rows for all entries), then one sweep+fit launch per
-    regression kind for all new signatures.  Measurements are never
-    materialised; returns (db, Regressors, report)."""
+    """cmd_profile + fit with the fused K5 path.
+
+    One GPU dedup of every runnable set of the manifest in global order
+    (App. A.4) against the DB's keys, then one sweep+fit launch per regression
+    kind for the new signatures.  The DB changes only after the sweep+fit
+    succeeded (an OraclePanic leaves it untouched): the new signatures, their
+    swept measurements (emitted by the same kernel, so ``sim.fit(db)`` and
+    ``store.save`` see them) and the model_operations rows of every entry.
+    The returned Regressors cover every signature the manifest references:
+    the new ones from the fused fit, those already in the DB fitted from their
+    stored measurements (InsufficientData if they have none).
+    Returns (db, Regressors, report)."""
+    from .errors import InsufficientData
     from .records import runnable_entries
-    from .sim import Regressors
+    from .sim import NEED, FitResult, Regressors, fit as fit_db
 
     dev = _device(device)
     db = db if db is not None else LatencyDB()
     grid = grid or manifest.grid
-    items, digests, report = [], [], []
+    configs, entries = [], []
     for m in manifest.models:
         for b in manifest.backends:
-            cid = db.add_configuration(manifest.hardware.name, m.name, b.name, manifest.tp_degree)
-            entries = runnable_entries(m, b, manifest.tp_degree)
-            to_profile, skipped, digs = dedup_with_digests(entries, db, cid, dev)
-            items += [(e, m, b) for e in to_profile]
-            digests += digs
-            report.append({"model": m.name, "backend": b.name, "entries": len(entries),
-                           "profiled": len(to_profile), "skipped": len(skipped)})
-    res = profile_fit(items, manifest.hardware, grid, dev)
+            ents = runnable_entries(m, b, manifest.tp_degree)
+            configs.append((m, b, len(entries), len(entries) + len(ents)))
+            entries += ents
+    if not entries:
+        return db, Regressors({}, {}, dev), []
+    res = dedup_packed(DeviceRecords.from_packed(pack_entries(entries), dev), db.digest_tensor(dev))
+    is_new = res.is_new.cpu().numpy().astype(bool)
+    digs = [bytes(r) for r in res.digests.cpu().numpy()]
+    items, new_digests, report = [], [], []
+    for m, b, lo, hi in configs:
+        for i in range(lo, hi):
+            if is_new[i]:
+                items.append((entries[i], m, b))
+                new_digests.append(digs[i])
+        n_new = int(is_new[lo:hi].sum())
+        report.append({"model": m.name, "backend": b.name, "entries": hi - lo,
+                       "profiled": n_new, "skipped": hi - lo - n_new})
+    fitted = profile_fit(items, manifest.hardware, grid, dev, emit_points=True)  # may raise
+    torch.cuda.synchronize(dev)
+    # ---- commit to the DB (nothing above touched it)
+    for (e, _, _), d in zip(items, new_digests):
+        db.add_signature(d, e)
     tables, index = {}, {}
-    for kind, (fr, idx, _) in res.items():
+    for kind, (fr, idx, (px, py, poff)) in fitted.items():
         tables[kind] = fr
+        x, y, off = px.cpu().numpy().view(np.uint32), py.cpu().numpy(), poff.cpu().numpy()
         for row, i in enumerate(idx):
-            index[digests[i]] = (kind, row)
+            e, m, _ = items[i]
+            a, z = int(off[row]), int(off[row + 1])
+            db.insert_measurements(new_digests[i], x[:, a:z], y[a:z],
+                                   sweep_points(e, grid, m.max_context))
+            index[new_digests[i]] = (kind, row)
+    for (m, b, lo, hi) in configs:
+        cid = db.add_configuration(manifest.hardware.name, m.name, b.name, manifest.tp_degree)
+        for i in range(lo, hi):
+            db.add_model_operation(cid, digs[i], entries[i].repeat_count)
+    # ---- signatures the manifest shares with what the DB already held
+    old = [d for d in dict.fromkeys(digs) if d not in index]
+    if old:
+        sub = LatencyDB()
+        for d in old:
+            row = db.signature(d)
+            if d not in db.measurements:
+                raise InsufficientData(d.hex(), 0, NEED[row.kind])
+            sub._index[d] = len(sub.signatures)
+            sub.signatures.append(row)
+            sub.measurements[d] = db.measurements[d]
+        prev = fit_db(sub, dev)
+        for kind, fr in prev.tables.items():
+            base = tables[kind].table.shape[0] if kind in tables else 0
+            if kind in tables:
+                t = tables[kind]
+                tables[kind] = FitResult(kind, torch.cat([t.table, fr.table]),
+                                         torch.cat([t.fit_err, fr.fit_err]),
+                                         torch.cat([t.status, fr.status]))
+            else:
+                tables[kind] = fr
+            for d, (k, r) in prev.index.items():
+                if k == kind:
+                    index[d] = (kind, base + r)
     torch.cuda.synchronize(dev)
     return db, Regressors(tables, index, dev), report

@@ -133,7 +133,8 @@ class Regressors:
         if digest not in self.index:
             raise UnknownSignature(digest.hex())
         kind, row = self.index[digest]
-        r = self.tables[kind].rows()[row]
+        # one row crosses the link, not the table
+        r = self.tables[kind].table[row].cpu().numpy().view(ROW_DTYPE[kind])[0]
         return Regressor(digest, FEATURE_NAMES[kind], tuple(np.atleast_1d(r["c"]).tolist()),
                          tuple(np.atleast_1d(r["inv"]).tolist()),
                          tuple(zip(np.atleast_1d(r["lo"]).tolist(), np.atleast_1d(r["hi"]).tolist())),
@@ -216,6 +217,21 @@ def fit(db: LatencyDB, device=None, strict: bool = True) -> Regressors:
             index[sigs[i].digest] = (kind, row)
     torch.cuda.synchronize(dev)
     return Regressors(tables, index, dev)
+
+
+def fit_cached(db: LatencyDB, db_path, device=None, strict: bool = True) -> Regressors:
+    """cmd_simulate's lazy fit ("fit runs lazily and caches
+    regressors alongside the db"): reuse the regressor file beside ``db_path``
+    when every measured signature's fingerprint still matches its
+    measurements, else fit on the GPU and rewrite the file."""
+    from .store import load_regressors, save_regressors
+
+    regs = load_regressors(db_path, db, device)
+    if regs is not None:
+        return regs
+    regs = fit(db, device, strict)
+    save_regressors(db_path, regs, db)
+    return regs
 
 
 # -------------------------------------------------------------------- predict
@@ -670,32 +686,40 @@ def mape(pred: Sequence[float], truth: Sequence[float]) -> float:
 
 
 def predict_host(kind: int, table: torch.Tensor, sig: torch.Tensor, x: torch.Tensor,
-                 out: torch.Tensor, chunk: int = 1 << 23, n_streams: int = 3) -> torch.Tensor:
+                 out: torch.Tensor, flags: Optional[torch.Tensor] = None, chunk: int = 1 << 23,
+                 n_streams: int = 3) -> torch.Tensor:
     """Host-buffer entry point of K3: pinned host sig (n,) i32 and x (P, n) i32 in,
-    pinned host f64 latencies out (see ``predict_host_many``); returns ``out``."""
-    predict_host_many([(kind, table, sig, x, out)], chunk, n_streams)
+    pinned host f64 latencies out and, when ``flags`` is given, the SPEC.md:569
+    flag bit-planes (2, ceil(n/32)) i32 (extrapolated, clamped; bit q % 32 of
+    word q // 32) — see ``predict_host_many``; returns ``out``."""
+    predict_host_many([(kind, table, sig, x, out, flags)], chunk, n_streams)
     return out
 
 
 def predict_host_many(batches: Sequence, chunk: int = 1 << 23, n_streams: int = 3) -> None:
-    """Several host-buffer query batches ``(kind, table, sig, x, out)`` (pinned host
-    tensors; tables on the device) through one copy/compute pipeline.  Chunks
-    of all batches are interleaved over ``n_streams`` CUDA streams, so the H2D
-    copy engine, the kernels and the D2H copy engine overlap.  Mixing kinds
-    also balances the link: attention queries are H2D-heavy (16 B in, 8 B
-    out), affine ones symmetric (8 B in, 8 B out).  Synchronises; raises
-    UnknownSignature if any query hit an unfitted row."""
+    """Several host-buffer query batches ``(kind, table, sig, x, out[, flags])``
+    (pinned host tensors; tables on the device; ``flags`` None or a pinned
+    (2, ceil(n/32)) i32 tensor receiving the extrapolation / clamp bit-planes)
+    through one copy/compute pipeline.  Chunks of all batches are interleaved
+    over ``n_streams`` CUDA streams, so the H2D copy engine, the kernels and the
+    D2H copy engine overlap.  Mixing kinds also balances the link: attention
+    queries are H2D-heavy (16 B in, 8 B out), affine ones symmetric (8 B in,
+    8 B out).  Synchronises; raises UnknownSignature if any query hit an
+    unfitted row."""
     if not batches:
         return
+    batches = [tuple(b) + (None,) * (6 - len(b)) for b in batches]
     dev = batches[0][1].device
     cur = torch.cuda.current_stream(dev)
     streams = [torch.cuda.Stream(dev) for _ in range(max(1, n_streams))]
     pmax = max(b[3].shape[0] for b in batches)
     c = min(chunk, max(max(b[2].numel() for b in batches), 1))
+    c = -(-c // 32) * 32                       # chunk starts stay on flag-word boundaries
+    cw = c // 32
     bufs = [(torch.empty(c, dtype=torch.int32, device=dev),
              torch.empty((pmax, c), dtype=torch.int32, device=dev),
              torch.empty(c, dtype=torch.float64, device=dev),
-             torch.empty((2, (c + 31) // 32), dtype=torch.int32, device=dev),
+             torch.empty(2 * cw, dtype=torch.int32, device=dev),
              torch.full((1,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev))
             for _ in streams]
     for s in streams:
@@ -709,9 +733,10 @@ def predict_host_many(batches: Sequence, chunk: int = 1 << 23, n_streams: int = 
                 work.append((i, cursors[i], min(n, cursors[i] + c)))
                 cursors[i] += c
     for j, (i, q0, q1) in enumerate(work):
-        kind, table, sig, x, out = batches[i]
+        kind, table, sig, x, out, hflags = batches[i]
         P = x.shape[0]
         m = q1 - q0
+        w = (m + 31) // 32
         s = streams[j % len(streams)]
         d_sig, d_x, d_out, d_flags, d_err = bufs[j % len(streams)]
         with torch.cuda.stream(s):
@@ -719,9 +744,13 @@ def predict_host_many(batches: Sequence, chunk: int = 1 << 23, n_streams: int = 
             xs = d_x[:P, :m] if m == c else torch.empty((P, m), dtype=torch.int32, device=dev)
             for p in range(P):
                 xs[p].copy_(x[p, q0:q1], non_blocking=True)
-            predict_batch(kind, table, d_sig[:m], xs, d_out[:m], d_flags if m == c else None,
-                          d_err, want_flags=m == c)
+            fl = d_flags[:2 * w].view(2, w) if hflags is not None else None
+            predict_batch(kind, table, d_sig[:m], xs, d_out[:m], fl, d_err,
+                          want_flags=hflags is not None)
             out[q0:q1].copy_(d_out[:m], non_blocking=True)
+            if hflags is not None:
+                for p in range(2):
+                    hflags[p, q0 // 32:q0 // 32 + w].copy_(fl[p], non_blocking=True)
     for s in streams:
         s.synchronize()
     if any(int(b[4].item()) != torch.iinfo(torch.int64).max for b in bufs):

@@ -106,10 +106,10 @@ def save(db, path) -> None:
             rows = []
             for d, (x, y) in db.measurements.items():
                 wl = db.workloads.get(d) or [None] * y.shape[0]
-                src = db.sources.get(d, "oracle")
+                src = db.point_sources(d)
                 for i in range(y.shape[0]):
                     rows.append((d, *_features(x, i), None if wl[i] is None else json.dumps(wl[i]),
-                                 float(y[i]), src, i))
+                                 float(y[i]), src[i], i))
             con.executemany("INSERT INTO measurements VALUES (?, ?, ?, ?, ?, ?, ?, ?)", rows)
             con.executemany("INSERT INTO comm_measurements VALUES (?, ?, ?, ?)",
                             [(*k, v) for k, v in db.comm_measurements.items()])
@@ -152,7 +152,7 @@ def load(path):
             x = np.array([r[:P] for r in rows], dtype=np.uint32).T.reshape(P, -1)
             db.measurements[d] = (np.ascontiguousarray(x), np.array([r[4] for r in rows]))
             db.workloads[d] = [None if r[3] is None else json.loads(r[3]) for r in rows]
-            db.sources[d] = rows[0][5]
+            db.sources[d] = [r[5] for r in rows]
         db.comm_measurements = {(t, int(tp), int(b)): float(v) for t, tp, b, v in con.execute(
             "SELECT topology, tp_degree, bytes, latency_s FROM comm_measurements")}
         return db
@@ -168,11 +168,11 @@ def export_jsonl(db, path) -> int:
     with open(path, "w") as f:
         for d, (x, y) in db.measurements.items():
             wl = db.workloads.get(d) or [None] * y.shape[0]
-            src = db.sources.get(d, "oracle")
+            src = db.point_sources(d)
             for i in range(y.shape[0]):
                 rec = {"sig": d.hex(), "workload": wl[i],
                        "features": [int(v) for v in x[:, i]],
-                       "latency_s": float(y[i]), "source": src}
+                       "latency_s": float(y[i]), "source": src[i]}
                 f.write(json.dumps(rec, sort_keys=True) + "\n")
                 n += 1
     return n
@@ -239,3 +239,98 @@ def query(db, digest: bytes, features: Optional[Sequence[int]] = None,
             continue
         out.append((f, float(y[i])))
     return out
+
+
+# ------------------------------------------------- regressors beside the DB
+
+
+REG_DDL = (
+    "CREATE TABLE meta(key TEXT PRIMARY KEY, value TEXT NOT NULL);",
+    "CREATE TABLE regressors(\n"
+    "  signature_hash BLOB PRIMARY KEY CHECK(length(signature_hash) = 32),\n"
+    "  kind INTEGER NOT NULL, ord INTEGER NOT NULL, row BLOB NOT NULL,\n"
+    "  fit_error REAL, status INTEGER NOT NULL, fingerprint BLOB NOT NULL);",
+)
+
+
+def regressor_path(db_path) -> str:
+    """The regressor cache that lives beside a DB file."""
+    return str(db_path) + ".regressors"
+
+
+def measurement_fingerprint(x: np.ndarray, y: np.ndarray) -> bytes:
+    """SHA-256 of a signature's training points: a cached regressor is valid
+    only for exactly the measurements it was fitted on."""
+    import hashlib
+
+    h = hashlib.sha256(np.ascontiguousarray(x, dtype=np.uint32).tobytes())
+    h.update(np.ascontiguousarray(y, dtype=np.float64).tobytes())
+    return h.digest()
+
+
+def save_regressors(db_path, regs, db) -> None:
+    """Write every fitted row (the exact device bytes), its fit_error, status and
+    the fingerprint of the measurements it came from, atomically."""
+    path = regressor_path(db_path)
+    tmp = path + ".tmp"
+    if os.path.exists(tmp):
+        os.remove(tmp)
+    host = {k: (fr.table.cpu().numpy(), fr.fit_err.cpu().numpy(), fr.status.cpu().numpy())
+            for k, fr in regs.tables.items()}
+    rows = []
+    for d, (kind, row) in regs.index.items():
+        t, fe, st = host[kind]
+        x, y = db.measurements[d]
+        rows.append((d, int(kind), int(row), t[row].tobytes(), float(fe[row]), int(st[row]),
+                     measurement_fingerprint(x, y)))
+    con = _connect(tmp, create=True)
+    with con:
+        for stmt in REG_DDL:
+            con.execute(stmt)
+        con.execute("INSERT INTO meta VALUES ('store_version', ?)", (str(STORE_VERSION),))
+        con.executemany("INSERT INTO regressors VALUES (?, ?, ?, ?, ?, ?, ?)", rows)
+    con.close()
+    os.replace(tmp, path)
+
+
+def load_regressors(db_path, db, device=None):
+    """The cached Regressors for ``db``, or None when the cache is missing,
+    lacks a measured signature, or any fingerprint is stale."""
+    import torch
+
+    from . import _lib
+    from .profiler import _device
+    from .sim import FitResult, Regressors
+
+    path = regressor_path(db_path)
+    if not os.path.exists(path):
+        return None
+    con = _connect(path, create=False)
+    try:
+        rows = con.execute("SELECT signature_hash, kind, ord, row, fit_error, status, fingerprint "
+                           "FROM regressors ORDER BY kind, ord").fetchall()
+    except sqlite3.Error:
+        return None
+    finally:
+        con.close()
+    have = {bytes(r[0]): r for r in rows}
+    if set(have) != set(db.measurements):
+        return None
+    for d, (x, y) in db.measurements.items():
+        if bytes(have[d][6]) != measurement_fingerprint(x, y):
+            return None
+    dev = _device(device)
+    tables, index = {}, {}
+    for kind in sorted({int(r[1]) for r in rows}):
+        ks = [r for r in rows if int(r[1]) == kind]
+        if [int(r[2]) for r in ks] != list(range(len(ks))):
+            return None
+        tab = np.frombuffer(b"".join(bytes(r[3]) for r in ks), dtype=np.uint8)
+        tab = tab.reshape(len(ks), _lib.ROW_BYTES[kind])
+        fe = np.array([np.nan if r[4] is None else r[4] for r in ks], dtype=np.float64)
+        st = np.array([r[5] for r in ks], dtype=np.uint8)
+        tables[kind] = FitResult(kind, torch.from_numpy(tab.copy()).to(dev),
+                                 torch.from_numpy(fe).to(dev), torch.from_numpy(st).to(dev))
+        for r in ks:
+            index[bytes(r[0])] = (kind, int(r[2]))
+    return Regressors(tables, index, dev)

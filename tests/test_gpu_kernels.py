@@ -215,16 +215,20 @@ def test_predict_host_pipeline_matches_device(dev):
             t, k = pack_attn(t), PACKED
         n = 100_003 + 8 * kind
         sig, xq = synth_queries(kind, table, n, seed=5 + kind, outside=0.02)
-        dev_out, _, _ = predict_batch(k, t, _i32(sig).to(dev), _i32(xq).to(dev))
+        dev_out, dev_flags, _ = predict_batch(k, t, _i32(sig).to(dev), _i32(xq).to(dev))
         hs, hx = _i32(sig).pin_memory(), _i32(xq).pin_memory()
         ho = torch.empty(n, dtype=torch.float64).pin_memory()
-        predict_host(k, t, hs, hx, ho, chunk=4096 * 3, n_streams=2)
+        hf = torch.zeros((2, (n + 31) // 32), dtype=torch.int32).pin_memory()
+        predict_host(k, t, hs, hx, ho, hf, chunk=4096 * 3, n_streams=2)
         assert torch.equal(ho, dev_out.cpu())
-        outs.append(dev_out.cpu())
-        batches.append((k, t, hs, hx, torch.empty(n, dtype=torch.float64).pin_memory()))
+        assert torch.equal(hf, dev_flags.cpu())            # SPEC.md:569 flags reach the host
+        assert int(hf[0].count_nonzero()) > 0              # some extrapolated queries
+        outs.append((dev_out.cpu(), dev_flags.cpu()))
+        batches.append((k, t, hs, hx, torch.empty(n, dtype=torch.float64).pin_memory(),
+                        torch.zeros((2, (n + 31) // 32), dtype=torch.int32).pin_memory()))
     predict_host_many(batches, chunk=8192, n_streams=3)
-    for (_, _, _, _, o), want in zip(batches, outs):
-        assert torch.equal(o, want)
+    for (_, _, _, _, o, f), (want, want_f) in zip(batches, outs):
+        assert torch.equal(o, want) and torch.equal(f, want_f)
 
 
 def test_attn_pack_header_and_refusals(dev):

@@ -76,3 +76,87 @@ def test_profile_and_fit_equals_db_fit(corpus, dev):
         cb = np.array(regs_b.regressor(d).coefficients)
         assert np.max(np.abs(ca - cb)) <= 1e-9 * np.max(np.abs(cb))
         assert regs_a.regressor(d).box == regs_b.regressor(d).box
+
+
+def test_profile_and_fit_with_prepopulated_db(corpus, dev):
+    """a second profile_and_fit over a manifest sharing signatures
+    with the DB returns regressors for EVERY referenced signature, writes the
+    swept measurements of the new ones (so sim.fit(db) covers them), and
+    records model_operations for all entries."""
+    from paper_2605_07985_b200 import modelir
+    from paper_2605_07985_b200.profiler import profile_and_fit
+    from paper_2605_07985_b200.records import runnable_entries, canonical_bytes
+    from paper_2605_07985_b200.sim import fit
+
+    first = modelir.CorpusManifest(corpus.models[:2], corpus.backends, corpus.hardware, 1,
+                                   corpus.grid)
+    db, regs1, _ = profile_and_fit(first, device=dev)
+    n_sig1 = len(db.signatures)
+    db, regs2, rep = profile_and_fit(corpus, db=db, device=dev)
+    assert sum(r["profiled"] for r in rep) == len(db.signatures) - n_sig1
+    assert set(db.measurements) == {s.digest for s in db.signatures}
+    referenced = {d for _, d, _ in db.model_operations}
+    assert referenced <= set(regs2.index)
+    assert len(db.model_operations) == sum(len(runnable_entries(m, b, 1))
+                                           for m in first.models + corpus.models
+                                           for b in corpus.backends)
+    ref = fit(db, dev)
+    for d in referenced:
+        a = np.array(regs2.regressor(d).coefficients)
+        b = np.array(ref.regressor(d).coefficients)
+        assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(b))
+        assert regs2.regressor(d).box == ref.regressor(d).box
+
+
+def test_profile_and_fit_failure_leaves_db_untouched(fixtures_manifest, dev, monkeypatch):
+    from paper_2605_07985_b200 import records
+    from paper_2605_07985_b200.errors import OraclePanic
+    from paper_2605_07985_b200.profiler import LatencyDB, profile_and_fit
+
+    real = records.runnable_entries
+
+    def with_unknown_op(m, b, tp=1, producer="trace"):
+        ents = real(m, b, tp, producer)
+        e = ents[-1]
+        return ents + [records.RunnableEntry("operator", "mystery_op", e.arg_template,
+                                             kernel_symbols=("k",))]
+
+    monkeypatch.setattr(records, "runnable_entries", with_unknown_op)
+    db = LatencyDB()
+    with pytest.raises(OraclePanic):
+        profile_and_fit(fixtures_manifest, db=db, device=dev)
+    assert db.signatures == [] and db.measurements == {} and db.model_operations == []
+
+
+def test_fit_cached_beside_the_db(fixtures_manifest, dev, tmp_path, monkeypatch):
+    """fit runs lazily and caches regressors alongside the db —
+    reloaded without refitting while the measurements are unchanged, refitted
+    when they change."""
+    import paper_2605_07985_b200.sim as sim
+    from paper_2605_07985_b200 import store
+    from paper_2605_07985_b200.profiler import profile_corpus
+
+    db, _ = profile_corpus(fixtures_manifest, device=dev)
+    path = tmp_path / "lat.db"
+    db.save(path)
+    regs = sim.fit_cached(db, path, dev)
+    assert (tmp_path / "lat.db.regressors").exists()
+    calls = []
+    monkeypatch.setattr(sim, "fit", lambda *a, **k: calls.append(1) or None)
+    again = sim.fit_cached(LatencyDB_load(path), path, dev)
+    assert calls == []                                           # served from the cache
+    for d in regs.index:
+        assert regs.regressor(d) == again.regressor(d)
+    monkeypatch.undo()
+    d = db.signatures[0].digest
+    x, y = db.measurements[d]
+    db.measurements[d] = (x, y * 1.5)                            # stale now
+    assert store.load_regressors(path, db, dev) is None
+    fresh = sim.fit_cached(db, path, dev)
+    assert fresh.regressor(d).coefficients != regs.regressor(d).coefficients
+
+
+def LatencyDB_load(path):
+    from paper_2605_07985_b200.profiler import LatencyDB
+
+    return LatencyDB.load(path)
