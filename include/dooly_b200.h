@@ -40,6 +40,7 @@ extern "C" {
 #define DOOLY_ERR_DUPLICATE_KEY 4      /* errors.py:52 DuplicateKey */
 #define DOOLY_ERR_NON_TERMINATION 5    /* errors.py:84 NonTermination */
 #define DOOLY_ERR_CUDA 6
+#define DOOLY_ERR_NCCL 7               /* dooly_comm_* (NCCL inside the library) */
 
 /* peer ranks a fused compute + all-gather call can write (8-GPU box) */
 #define DOOLY_MAX_PEERS 7
@@ -152,6 +153,11 @@ int dooly_sha256_records_bcast(dooly_ctx* ctx, const uint32_t* words, const int6
                                uint8_t* out_digest, const dooly_digest_peers* peers,
                                uint32_t* flag, uint32_t target, int32_t* timed_out, void* stream);
 
+/* Let this context's device access `peer_device`'s memory (the fused *_bcast
+ * calls store into peer buffers mapped through CUDA IPC): cudaDeviceEnablePeerAccess
+ * from the context's device, already-enabled tolerated. */
+int dooly_enable_peer_access(dooly_ctx* ctx, int peer_device);
+
 /* Plain SHA-256 of n byte messages (msgs + off[i]..off[i+1]) — signature_hash(bytes). */
 int dooly_sha256_messages(dooly_ctx* ctx, const uint8_t* msgs, const int64_t* off, int64_t n,
                           uint8_t* out_digest, void* stream);
@@ -230,6 +236,69 @@ int dooly_fit_grid_bcast(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_
                          uint8_t* status, const dooly_grid_peers* peers, uint32_t* flag,
                          uint32_t target, int32_t* timed_out, void* workspace,
                          size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------- owner-routed dedup (K1c)
+ * The multi-GPU dedup of SURVEY §8(e) with digests routed to their owner
+ * rank (owner = last 8 digest bytes as int64 & INT64_MAX, mod world; world <=
+ * DOOLY_MAX_PEERS + 1), every step a device kernel:
+ *   dooly_route_plan   stable counting sort of n local digests by owner:
+ *                      out_perm[j] = local index of routed row j, out_counts
+ *                      [world] rows per owner, out_digests / out_gidx the rows
+ *                      (global index gidx0 + i) in bucket order — the send
+ *                      buffers of the all-to-all (dooly_alltoallv);
+ *   (owner)            dooly_dedup_digests on the received digests (+ its
+ *                      share of the DB keys, planned the same way), then
+ *   dooly_dedup_firsts its first occurrences' global indices in order
+ *                      (same workspace, right after the dedup);
+ *   dooly_route_reply  per received row (global first, global uid, is_new |
+ *                      in_db << 1) as 3 int64; uid = number of first
+ *                      occurrences over all owners with a smaller global index
+ *                      (all_firsts: world sorted lists of `per` entries padded
+ *                      with INT64_MAX, the all-gather of every owner's firsts);
+ *   dooly_route_finish the replies (all-to-all back, bucket order) scattered
+ *                      through out_perm into first / uid / is_new / in_db.
+ * Equal to dooly_dedup_digests over the whole global list, bit for bit. */
+size_t dooly_route_workspace_size(int64_t n, int world);
+int dooly_route_plan(dooly_ctx* ctx, const uint8_t* digests, int64_t n, int world, int64_t gidx0,
+                     int64_t* out_perm, int64_t* out_counts, uint8_t* out_digests,
+                     int64_t* out_gidx, void* workspace, size_t workspace_bytes, void* stream);
+int dooly_dedup_firsts(dooly_ctx* ctx, int64_t n, int64_t n_db, const int64_t* gidx,
+                       int64_t* out_firsts, void* workspace, size_t workspace_bytes,
+                       void* stream);
+int dooly_route_reply(dooly_ctx* ctx, const int64_t* gidx, const int64_t* first,
+                      const uint8_t* is_new, const uint8_t* in_db, int64_t m,
+                      const int64_t* all_firsts, int64_t per, int world, int64_t* out_rows,
+                      void* stream);
+int dooly_route_finish(dooly_ctx* ctx, const int64_t* rows, const int64_t* perm, int64_t n,
+                       int64_t* out_first, uint32_t* out_uid, uint8_t* out_is_new,
+                       uint8_t* out_in_db, void* stream);
+
+/* ------------------------------------------------------------ communicator
+ * NCCL inside the library: the NCCL forms of the multi-GPU
+ * exchanges beside the fused peer-memory ones.  Replaces the reference's
+ * nothing — the reference is single-process Python; these are the
+ * exports §8(b) names.  Failures return DOOLY_ERR_NCCL, message via
+ * dooly_comm_last_error (NULL comm: the calling thread's last failure).
+ *   one process per GPU: rank 0 gets the id (dooly_comm_unique_id), the caller
+ *     ships the DOOLY_COMM_ID_BYTES to every rank, each rank calls
+ *     dooly_comm_init_rank(device, id, nranks, rank);
+ *   one process, ndev GPUs: dooly_comm_create (ncclCommInitAll).
+ * dooly_allgather is in place: bufs[i] (local device i) holds nranks blocks of
+ * bytes_per_rank, its own at (rank0 + i) x bytes_per_rank.  dooly_alltoallv
+ * (one local device) sends block p of `send` to rank p and receives block p of
+ * `recv` from it; counts are HOST arrays of nranks element counts. */
+#define DOOLY_COMM_ID_BYTES 128
+typedef struct dooly_comm dooly_comm;
+int dooly_comm_unique_id(uint8_t* out_id);
+int dooly_comm_init_rank(int device, const uint8_t* id, int nranks, int rank, dooly_comm** out);
+int dooly_comm_create(int ndev, const int* devs, dooly_comm** out);
+void dooly_comm_destroy(dooly_comm* comm);
+const char* dooly_comm_last_error(const dooly_comm* comm);
+int dooly_comm_size(const dooly_comm* comm, int* nranks, int* rank0, int* n_local);
+int dooly_allgather(dooly_comm* comm, void* const* bufs, size_t bytes_per_rank,
+                    void* const* streams);
+int dooly_alltoallv(dooly_comm* comm, const void* send, const int64_t* send_counts, void* recv,
+                    const int64_t* recv_counts, size_t elem_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K3 predict
  * Replaces predict.  sig[i] indexes the table; x is

@@ -158,8 +158,24 @@ _SIGS = {
     "dooly_sim_run": (C.c_int, [_P, C.POINTER(OpList), C.POINTER(Sched), _P, _I64, _P, _I64,
                                 _P, _P, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _I64, _P,
                                 C.c_size_t, _P]),
+    "dooly_enable_peer_access": (C.c_int, [_P, C.c_int]),
+    "dooly_route_workspace_size": (C.c_size_t, [_I64, C.c_int]),
+    "dooly_route_plan": (C.c_int, [_P, _P, _I64, C.c_int, _I64, _P, _P, _P, _P, _P, C.c_size_t,
+                                   _P]),
+    "dooly_dedup_firsts": (C.c_int, [_P, _I64, _I64, _P, _P, _P, C.c_size_t, _P]),
+    "dooly_route_reply": (C.c_int, [_P, _P, _P, _P, _P, _I64, _P, _I64, C.c_int, _P, _P]),
+    "dooly_route_finish": (C.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _P]),
+    "dooly_comm_unique_id": (C.c_int, [_P]),
+    "dooly_comm_init_rank": (C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "dooly_comm_create": (C.c_int, [C.c_int, _P, C.POINTER(C.c_void_p)]),
+    "dooly_comm_destroy": (None, [_P]),
+    "dooly_comm_last_error": (C.c_char_p, [_P]),
+    "dooly_comm_size": (C.c_int, [_P, _P, _P, _P]),
+    "dooly_allgather": (C.c_int, [_P, _P, C.c_size_t, _P]),
+    "dooly_alltoallv": (C.c_int, [_P, _P, _P, _P, _P, C.c_size_t, _P]),
 }
 EXPORTS = tuple(_SIGS)
+COMM_ID_BYTES = 128
 
 _lock = threading.Lock()
 _lib = None
@@ -208,6 +224,12 @@ def ctx_for(device: torch.device) -> C.c_void_p:
 def check(rc: int, ctx) -> None:
     if rc:
         msg = load_library().dooly_last_error(ctx)
+        raise_for_status(rc, msg.decode() if msg else f"status {rc}")
+
+
+def check_comm(rc: int, comm) -> None:
+    if rc:
+        msg = load_library().dooly_comm_last_error(comm)
         raise_for_status(rc, msg.decode() if msg else f"status {rc}")
 
 

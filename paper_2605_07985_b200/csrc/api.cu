@@ -32,7 +32,22 @@ cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off,
                                   const dooly_digest_peers* peers = nullptr);
 cudaError_t launch_peer_sync(int n_peers, uint32_t* const* peer_flags, uint32_t* flag,
                              uint32_t target, int32_t* timed_out, cudaStream_t stream,
-                             int64_t* launches);
+                             int64_t* launches, int slot);
+cudaError_t enable_peer_access(int device, int peer);
+cudaError_t launch_dedup_firsts(int64_t n, int64_t n_db, const int64_t* gidx, int64_t* out_firsts,
+                                void* ws, cudaStream_t stream, int n_sm, int64_t* launches);
+size_t route_workspace_size(int64_t n, int world);
+cudaError_t launch_route_plan(const uint8_t* dig, int64_t n, int world, int64_t gidx0,
+                              int64_t* perm, int64_t* counts, uint8_t* out_dig, int64_t* out_gidx,
+                              void* ws, cudaStream_t stream, int64_t* launches);
+cudaError_t launch_route_reply(const int64_t* gidx, const int64_t* first, const uint8_t* is_new,
+                               const uint8_t* in_db, int64_t m, const int64_t* all_firsts,
+                               int64_t per, int world, int64_t* rows, cudaStream_t stream,
+                               int n_sm, int64_t* launches);
+cudaError_t launch_route_finish(const int64_t* rows, const int64_t* perm, int64_t n,
+                                int64_t* out_first, uint32_t* out_uid, uint8_t* out_is_new,
+                                uint8_t* out_in_db, cudaStream_t stream, int n_sm,
+                                int64_t* launches);
 cudaError_t launch_sha256_messages(const uint8_t* msgs, const int64_t* off, int64_t n,
                                    uint8_t* out, cudaStream_t stream, int n_sm);
 size_t dedup_workspace_size(int64_t n, int64_t n_db);
@@ -262,12 +277,14 @@ int dooly_fit_grid_bcast(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_
   if ((uintptr_t)table % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: table must be 16-byte aligned");
   DeviceGuard g(ctx->device);
-  cudaError_t e = dooly::launch_fit_grid(kind, x, n_pts, y, n_sig, table, fit_err, status, peers,
-                                         workspace, (cudaStream_t)stream, ctx->n_sm,
-                                         &ctx->launches);
+  cudaError_t e = dooly::launch_peer_sync(peers->n_peers, peers->flag, flag, target, timed_out,
+                                          (cudaStream_t)stream, &ctx->launches, 1);
+  if (e == cudaSuccess)
+    e = dooly::launch_fit_grid(kind, x, n_pts, y, n_sig, table, fit_err, status, peers,
+                               workspace, (cudaStream_t)stream, ctx->n_sm, &ctx->launches);
   if (e == cudaSuccess)
     e = dooly::launch_peer_sync(peers->n_peers, peers->flag, flag, target, timed_out,
-                                (cudaStream_t)stream, &ctx->launches);
+                                (cudaStream_t)stream, &ctx->launches, 0);
   return check_cuda(ctx, e, "fit_grid_bcast");
 }
 
@@ -316,14 +333,23 @@ int dooly_sha256_records_bcast(dooly_ctx* ctx, const uint32_t* words, const int6
   if ((uintptr_t)out_digest % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records_bcast: digests must be 16-B aligned");
   DeviceGuard g(ctx->device);
-  cudaError_t e = dooly::launch_sha256_records(words, rec_off, n, op_bytes, op_off, sym_bytes,
-                                               sym_off, attr_digests, out_digest,
-                                               (cudaStream_t)stream, ctx->n_sm, &ctx->launches,
-                                               peers);
+  cudaError_t e = dooly::launch_peer_sync(peers->n_peers, peers->flag, flag, target, timed_out,
+                                          (cudaStream_t)stream, &ctx->launches, 1);
+  if (e == cudaSuccess)
+    e = dooly::launch_sha256_records(words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off,
+                                     attr_digests, out_digest, (cudaStream_t)stream, ctx->n_sm,
+                                     &ctx->launches, peers);
   if (e == cudaSuccess)
     e = dooly::launch_peer_sync(peers->n_peers, peers->flag, flag, target, timed_out,
-                                (cudaStream_t)stream, &ctx->launches);
+                                (cudaStream_t)stream, &ctx->launches, 0);
   return check_cuda(ctx, e, "sha256_records_bcast");
+}
+
+int dooly_enable_peer_access(dooly_ctx* ctx, int peer_device) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (peer_device < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "enable_peer_access: bad device");
+  return check_cuda(ctx, dooly::enable_peer_access(ctx->device, peer_device),
+                    "enable_peer_access");
 }
 
 int dooly_sha256_messages(dooly_ctx* ctx, const uint8_t* msgs, const int64_t* off, int64_t n,
@@ -351,8 +377,8 @@ int dooly_dedup_digests(dooly_ctx* ctx, const uint8_t* digests, int64_t n,
                         void* stream) {
   if (!ctx) return DOOLY_ERR_INVALID_ARG;
   if (n < 0 || n_db < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: negative size");
-  if (n + n_db >= (int64_t)0x7FFFFFFF)
-    return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: more than 2^31-1 digests per call");
+  if (n + n_db >= (int64_t)0xFFFFFFFF)   // slots hold u32 indices; 0xFFFFFFFF marks empty
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: more than 2^32-2 digests per call");
   if (!out_n_unique || (n > 0 && (!digests || !out_first || !out_uid || !out_is_new)) ||
       (n_db > 0 && !db_digests))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: null pointer");
@@ -365,6 +391,79 @@ int dooly_dedup_digests(dooly_ctx* ctx, const uint8_t* digests, int64_t n,
                                         workspace_bytes, (cudaStream_t)stream, ctx->n_sm,
                                         &ctx->launches),
                     "dedup");
+}
+
+size_t dooly_route_workspace_size(int64_t n, int world) {
+  return dooly::route_workspace_size(n, world);
+}
+
+int dooly_route_plan(dooly_ctx* ctx, const uint8_t* digests, int64_t n, int world, int64_t gidx0,
+                     int64_t* out_perm, int64_t* out_counts, uint8_t* out_digests,
+                     int64_t* out_gidx, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n < 0 || world < 1 || world > DOOLY_MAX_PEERS + 1 || gidx0 < 0)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_plan: bad size or world");
+  if (!out_counts || (n > 0 && (!digests || !out_perm || !out_digests || !out_gidx)))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_plan: null pointer");
+  if ((uintptr_t)digests % 16 || (uintptr_t)out_digests % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_plan: digests must be 16-byte aligned");
+  if (!workspace || workspace_bytes < dooly::route_workspace_size(n, world) ||
+      (uintptr_t)workspace % 16)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_plan: workspace too small or misaligned");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_route_plan(digests, n, world, gidx0, out_perm, out_counts,
+                                             out_digests, out_gidx, workspace,
+                                             (cudaStream_t)stream, &ctx->launches),
+                    "route_plan");
+}
+
+int dooly_dedup_firsts(dooly_ctx* ctx, int64_t n, int64_t n_db, const int64_t* gidx,
+                       int64_t* out_firsts, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n < 0 || n_db < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup_firsts: negative size");
+  if (n > 0 && (!gidx || !out_firsts || !workspace))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup_firsts: null pointer");
+  if (workspace_bytes < dooly::dedup_workspace_size(n, n_db))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup_firsts: workspace too small");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_dedup_firsts(n, n_db, gidx, out_firsts, workspace,
+                                               (cudaStream_t)stream, ctx->n_sm, &ctx->launches),
+                    "dedup_firsts");
+}
+
+int dooly_route_reply(dooly_ctx* ctx, const int64_t* gidx, const int64_t* first,
+                      const uint8_t* is_new, const uint8_t* in_db, int64_t m,
+                      const int64_t* all_firsts, int64_t per, int world, int64_t* out_rows,
+                      void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (m < 0 || per < 0 || world < 1 || world > DOOLY_MAX_PEERS + 1)
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_reply: bad size or world");
+  if (m > 0 && (!gidx || !first || !is_new || !out_rows || (per > 0 && !all_firsts)))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_reply: null pointer");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_route_reply(gidx, first, is_new, in_db, m, all_firsts, per,
+                                              world, out_rows, (cudaStream_t)stream, ctx->n_sm,
+                                              &ctx->launches),
+                    "route_reply");
+}
+
+int dooly_route_finish(dooly_ctx* ctx, const int64_t* rows, const int64_t* perm, int64_t n,
+                       int64_t* out_first, uint32_t* out_uid, uint8_t* out_is_new,
+                       uint8_t* out_in_db, void* stream) {
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  if (n < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_finish: negative size");
+  if (n > 0 && (!rows || !perm || !out_first || !out_uid || !out_is_new))
+    return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_finish: null pointer");
+  DeviceGuard g(ctx->device);
+  return check_cuda(ctx,
+                    dooly::launch_route_finish(rows, perm, n, out_first, out_uid, out_is_new,
+                                               out_in_db, (cudaStream_t)stream, ctx->n_sm,
+                                               &ctx->launches),
+                    "route_finish");
 }
 
 static int check_oplist(dooly_ctx* ctx, const dooly_oplist* ops, int64_t n_aff, int64_t n_attn,

@@ -43,7 +43,7 @@ static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 static size_t cub_scan_bytes(int64_t n) {
   size_t bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                (int)(n > 0 ? n : 1));
+                                (int64_t)(n > 0 ? n : 1));
   return bytes;
 }
 
@@ -171,12 +171,34 @@ cudaError_t launch_dedup(const uint8_t* digests, int64_t n, const uint8_t* db, i
   dedup_resolve_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
       n, w.slots, w.mark, w.slot_of, out_first, out_is_new, out_in_db, w.first_flag);
   size_t tmp = w.cub_bytes;
-  if ((e = cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.first_flag, w.rank, (int)n, stream)) !=
-      cudaSuccess)
+  if ((e = cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.first_flag, w.rank, (int64_t)n,
+                                         stream)) != cudaSuccess)
     return e;
   dedup_uid_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
       n, out_first, w.rank, w.first_flag, out_uid, out_n_unique);
   *launches += 4;  // insert, resolve, cub scan, uid
+  return cudaGetLastError();
+}
+
+// Owner-routed dedup (route.cu): after launch_dedup on an owner's received
+// digests, the owner's first occurrences in order — out_firsts[rank[i]] =
+// gidx[i] for every first occurrence i — read from the same workspace's
+// first-occurrence flags and their exclusive scan.
+__global__ void __launch_bounds__(DEDUP_THREADS) dedup_firsts_kernel(
+    int64_t n, const uint32_t* __restrict__ first_flag, const uint32_t* __restrict__ rank,
+    const int64_t* __restrict__ gidx, int64_t* __restrict__ out_firsts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    if (first_flag[i]) out_firsts[rank[i]] = gidx[i];
+}
+
+cudaError_t launch_dedup_firsts(int64_t n, int64_t n_db, const int64_t* gidx, int64_t* out_firsts,
+                                void* ws, cudaStream_t stream, int n_sm, int64_t* launches) {
+  if (n == 0) return cudaSuccess;
+  DedupWs w = carve(ws, n, n_db);
+  dedup_firsts_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(n, w.first_flag, w.rank,
+                                                                       gidx, out_firsts);
+  *launches += 1;
   return cudaGetLastError();
 }
 

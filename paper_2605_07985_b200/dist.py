@@ -16,6 +16,13 @@ the plumbing.
   predict queries split contiguously; no collective (each rank holds the table).
   sim     S fixed replica shards, shard s on rank s mod world ("replicas only",
           no data-path collective); per-request TTFT/TPOT gathered at the end.
+
+Data-path collectives on GPUs go through the NCCL communicator INSIDE
+libdooly_b200 (``LibComm``: dooly_comm_init_rank / dooly_allgather /
+dooly_alltoallv); torch.distributed is the bootstrap only (it ships the
+128-byte NCCL id) and the gloo host path of the CPU tests and of several
+ranks sharing one GPU.  DOOLY_COMM=torch switches the GPU path to
+torch.distributed's own NCCL collectives (side-by-side checks).
 """
 
 from __future__ import annotations
@@ -131,11 +138,89 @@ def owner_of(digests: torch.Tensor, size: int) -> torch.Tensor:
     return torch.remainder(tail & 0x7FFFFFFFFFFFFFFF, size)
 
 
+class LibComm:
+    """The NCCL communicator inside libdooly_b200 for this process's GPU
+    (include/dooly_b200.h dooly_comm_*).  Collective: every rank of the group
+    constructs it together (rank 0's NCCL id reaches the others through
+    torch.distributed, the bootstrap)."""
+
+    def __init__(self, device: torch.device, group=None):
+        from . import _lib
+
+        rank, size = world()
+        lib = _lib.load_library()
+        idb = (C.c_uint8 * _lib.COMM_ID_BYTES)()
+        if rank == 0:
+            _lib.check_comm(lib.dooly_comm_unique_id(idb), None)
+        box = [bytes(idb)]
+        if size > 1:
+            dist.broadcast_object_list(box, src=0, group=group)
+        idb = (C.c_uint8 * _lib.COMM_ID_BYTES).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        _lib.check_comm(lib.dooly_comm_init_rank(device.index, idb, size, rank, C.byref(h)), None)
+        self.handle, self.rank, self.size, self.device = h, rank, size, device
+
+    def allgather(self, t: torch.Tensor) -> torch.Tensor:
+        """Equal-shape per-rank blocks concatenated on dim 0 (dooly_allgather, in place)."""
+        from . import _lib
+
+        t = t.contiguous()
+        out = torch.empty((t.shape[0] * self.size,) + tuple(t.shape[1:]), dtype=t.dtype,
+                          device=t.device)
+        nb = t.numel() * t.element_size()
+        out.view(-1)[self.rank * t.numel():(self.rank + 1) * t.numel()].copy_(t.view(-1))
+        bufs = (C.c_void_p * 1)(out.data_ptr())
+        streams = (C.c_void_p * 1)(_lib.stream_ptr(self.device))
+        _lib.check_comm(_lib.load_library().dooly_allgather(self.handle, bufs, nb, streams),
+                        self.handle)
+        return out
+
+    def alltoallv(self, t: torch.Tensor, send: list, recv: list) -> torch.Tensor:
+        """Rows of ``t`` split by ``send`` counts to the ranks; ``recv`` rows back."""
+        from . import _lib
+
+        t = t.contiguous()
+        row = int(np.prod(t.shape[1:], dtype=np.int64)) * t.element_size()
+        out = torch.empty((sum(recv),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        sc = (C.c_int64 * self.size)(*send)
+        rc = (C.c_int64 * self.size)(*recv)
+        _lib.check_comm(_lib.load_library().dooly_alltoallv(
+            self.handle, t.data_ptr() if t.numel() else 0, sc,
+            out.data_ptr() if out.numel() else 0, rc, max(row, 1),
+            _lib.stream_ptr(self.device)), self.handle)
+        return out
+
+    def close(self) -> None:
+        from . import _lib
+
+        if self.handle:
+            _lib.load_library().dooly_comm_destroy(self.handle)
+            self.handle = None
+
+
+_COMMS: dict = {}
+
+
+def lib_comm(device: torch.device, group=None):
+    """This process's LibComm for ``group`` (created on first use, collectively),
+    or None when the data path uses torch.distributed (gloo, or DOOLY_COMM=torch)."""
+    if dist.get_backend(group) != "nccl" or os.environ.get("DOOLY_COMM", "lib") == "torch":
+        return None
+    key = (device.index, id(group))
+    if key not in _COMMS:
+        _COMMS[key] = LibComm(device, group)
+    return _COMMS[key]
+
+
 def _all_to_all(t: torch.Tensor, send: list, recv: list, group=None) -> torch.Tensor:
-    """all_to_all_single on dim 0 with per-rank split sizes (NCCL on the
-    device; gloo through host memory)."""
+    """all-to-all on dim 0 with per-rank split sizes: libdooly's NCCL
+    (dooly_alltoallv) on GPUs, torch's NCCL under DOOLY_COMM=torch, gloo
+    through host memory."""
     out_shape = (sum(recv),) + tuple(t.shape[1:])
     if dist.get_backend(group) == "nccl":
+        comm = lib_comm(t.device, group)
+        if comm is not None:
+            return comm.alltoallv(t, send, recv)
         out = torch.empty(out_shape, dtype=t.dtype, device=t.device)
         dist.all_to_all_single(out, t.contiguous(), recv, send, group=group)
         return out
@@ -150,60 +235,95 @@ def dedup_routed(recs_local, n_total: int, db_digests: Optional[torch.Tensor] = 
     """Multi-GPU dedup with owner routing: each digest goes to the
     rank that owns it, so every rank resolves ~n_total / world keys instead of
     all of them (the all-gather form resolves the whole list on every rank).
+    Every data step is a libdooly kernel (route.cu); the exchanges are the
+    communicator's all-to-alls / all-gathers:
 
       1. hash the local records (K1a);
-      2. all-to-all of (digest, global index) to the owners; a rank's bucket
-         keeps its records' order and ranks send in rank order, so what an
-         owner receives is in global order;
-      3. the owner resolves its keys (K1b) — every copy of a digest is there,
-         so first occurrence, DB membership and is_new are exact;
-      4. uid = rank of the first occurrence among ALL first occurrences: the
-         owners' sorted first-occurrence indices are all-gathered and each
-         owner counts the smaller ones (searchsorted);
-      5. all-to-all of (first, uid, flags) back to the records' home ranks.
+      2. dooly_route_plan: stable bucket of (digest, global index) by owner;
+         all-to-all to the owners — a rank's bucket keeps its records' order
+         and ranks send in rank order, so what an owner receives is in
+         global order;
+      3. the owner resolves its keys (K1b, with its planned share of the DB
+         keys) — every copy of a digest is there, so first occurrence, DB
+         membership and is_new are exact — and lists its first occurrences'
+         global indices (dooly_dedup_firsts);
+      4. the owners' sorted first lists are all-gathered; dooly_route_reply
+         gives each received record its global first index, its global uid
+         (first occurrences over all owners with a smaller global index) and
+         flags;
+      5. all-to-all of the replies back; dooly_route_finish scatters them
+         through the plan's permutation.
     Bit-identical to the single-rank dedup of the whole list."""
-    from .profiler import DedupResult, dedup_digests, hash_records
+    from . import _lib
+    from .profiler import DedupResult, DedupWorkspace, hash_records
 
     rank, size = world()
     dev = recs_local.words.device
+    lib = _lib.load_library()
+    ctx = _lib.ctx_for(dev)
+    st = _lib.stream_ptr(dev)
     a, _ = shard_range(n_total, rank, size)
+
+    def plan(dig, gidx0):
+        n = dig.shape[0]
+        perm = torch.empty(n, dtype=torch.int64, device=dev)
+        counts = torch.empty(size, dtype=torch.int64, device=dev)
+        sdig = torch.empty((n, 32), dtype=torch.uint8, device=dev)
+        sgidx = torch.empty(n, dtype=torch.int64, device=dev)
+        ws = torch.empty(int(lib.dooly_route_workspace_size(n, size)), dtype=torch.uint8,
+                         device=dev)
+        _lib.check(lib.dooly_route_plan(ctx, _lib.ptr(dig) if n else 0, n, size, gidx0,
+                                        _lib.ptr(perm), counts.data_ptr(), _lib.ptr(sdig),
+                                        _lib.ptr(sgidx), ws.data_ptr(), ws.numel(), st), ctx)
+        return perm, counts, sdig, sgidx
+
     dig = hash_records(recs_local)
-    n_loc = dig.shape[0]
-    own = owner_of(dig, size) if n_loc else torch.empty(0, dtype=torch.int64, device=dev)
-    order = torch.sort(own, stable=True).indices
-    send = torch.bincount(own, minlength=size)
-    recv = _all_to_all(send, [1] * size, [1] * size, group)
-    send_l, recv_l = send.tolist(), recv.tolist()
-    gidx = torch.arange(a, a + n_loc, dtype=torch.int64, device=dev)
-    payload = torch.cat([dig[order].view(torch.int64), gidx[order, None]], dim=1)   # (n, 5) i64
-    got = _all_to_all(payload, send_l, recv_l, group)
-    r_dig = got[:, :4].contiguous().view(torch.uint8).reshape(-1, 32)
-    r_gidx = got[:, 4].contiguous()
+    n = dig.shape[0]
+    perm, counts, sdig, sgidx = plan(dig, a)
+    send = counts.cpu().tolist()                         # host counts for the exchange
+    recv = _all_to_all(counts, [1] * size, [1] * size, group).cpu().tolist()
+    r_dig = _all_to_all(sdig, send, recv, group)
+    r_gidx = _all_to_all(sgidx, send, recv, group)
+    db_own = None
     if db_digests is not None and db_digests.shape[0]:
-        db_digests = db_digests[owner_of(db_digests, size) == rank]
-    res = dedup_digests(r_dig, db_digests, workspace, sync=False)
+        _, dcounts, ddig, _ = plan(db_digests.contiguous(), 0)
+        dc = dcounts.cpu().tolist()
+        o = sum(dc[:rank])
+        db_own = ddig[o:o + dc[rank]]
+    n_db = 0 if db_own is None else db_own.shape[0]
     m = r_dig.shape[0]
-    # first occurrences of this owner, in global order (r_gidx is increasing)
-    firsts = r_gidx[res.first == torch.arange(m, device=dev)] if m else r_gidx[:0]
-    counts = torch.tensor([firsts.numel()], dtype=torch.int64, device=dev)
-    all_counts = _gather_cat(counts, size, group)
-    per = int(all_counts.max().item())
+    ws = (workspace or DedupWorkspace(dev)).get(m, n_db)
+    first = torch.empty(m, dtype=torch.int64, device=dev)
+    uid = torch.empty(m, dtype=torch.int32, device=dev)
+    is_new = torch.empty(m, dtype=torch.uint8, device=dev)
+    in_db = torch.empty(m, dtype=torch.uint8, device=dev)
+    n_unique = torch.zeros(1, dtype=torch.int64, device=dev)
+    _lib.check(lib.dooly_dedup_digests(
+        ctx, _lib.ptr(r_dig) if m else 0, m, _lib.ptr(db_own) if n_db else 0, n_db,
+        _lib.ptr(first), _lib.ptr(uid), _lib.ptr(is_new), _lib.ptr(in_db), n_unique.data_ptr(),
+        ws.data_ptr(), ws.numel(), st), ctx)
+    n_first = int(n_unique.item())
+    firsts = torch.empty(max(n_first, 1), dtype=torch.int64, device=dev)
+    _lib.check(lib.dooly_dedup_firsts(ctx, m, n_db, _lib.ptr(r_gidx) if m else 0,
+                                      firsts.data_ptr(), ws.data_ptr(), ws.numel(), st), ctx)
+    all_counts = _gather_cat(n_unique, size, group)
+    per = max(1, int(all_counts.max().item()))
     pad = torch.full((per,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=dev)
-    pad[: firsts.numel()] = firsts
+    pad[:n_first] = firsts[:n_first]
     all_firsts = _gather_cat(pad, size, group)
-    all_firsts = torch.sort(all_firsts).values[: int(all_counts.sum().item())]
-    rank_of_first = torch.searchsorted(all_firsts, firsts)
-    first_g = r_gidx[res.first] if m else r_gidx[:0]
-    uid_g = rank_of_first[res.uid.long()] if m else r_gidx[:0]
-    flags = res.is_new.long() | (res.in_db.long() << 1)
-    back = torch.stack([first_g, uid_g, flags], dim=1) if m else \
-        torch.empty((0, 3), dtype=torch.int64, device=dev)
-    ret = _all_to_all(back, recv_l, send_l, group)
-    out = torch.empty_like(ret)
-    out[order] = ret
-    return DedupResult(dig, out[:, 0].contiguous(), out[:, 1].to(torch.int32),
-                       (out[:, 2] & 1).to(torch.uint8), ((out[:, 2] >> 1) & 1).to(torch.uint8),
-                       int(all_counts.sum().item()))
+    rows = torch.empty((m, 3), dtype=torch.int64, device=dev)
+    _lib.check(lib.dooly_route_reply(ctx, _lib.ptr(r_gidx) if m else 0, _lib.ptr(first),
+                                     _lib.ptr(is_new), _lib.ptr(in_db), m, all_firsts.data_ptr(),
+                                     per, size, _lib.ptr(rows), st), ctx)
+    back = _all_to_all(rows, recv, send, group)
+    out_first = torch.empty(n, dtype=torch.int64, device=dev)
+    out_uid = torch.empty(n, dtype=torch.int32, device=dev)
+    out_new = torch.empty(n, dtype=torch.uint8, device=dev)
+    out_db = torch.empty(n, dtype=torch.uint8, device=dev)
+    _lib.check(lib.dooly_route_finish(ctx, _lib.ptr(back) if n else 0, _lib.ptr(perm), n,
+                                      _lib.ptr(out_first), _lib.ptr(out_uid), _lib.ptr(out_new),
+                                      _lib.ptr(out_db), st), ctx)
+    return DedupResult(dig, out_first, out_uid, out_new, out_db, int(all_counts.sum().item()))
 
 
 def gather_requests(values: torch.Tensor, group=None) -> torch.Tensor:
@@ -215,8 +335,12 @@ def gather_requests(values: torch.Tensor, group=None) -> torch.Tensor:
 
 
 def _gather_cat(t: torch.Tensor, size: int, group=None) -> torch.Tensor:
-    """all_gather of equal-shape tensors concatenated on dim 0 (one NCCL call)."""
+    """all_gather of equal-shape tensors concatenated on dim 0 (one NCCL call:
+    libdooly's dooly_allgather, or torch's under DOOLY_COMM=torch)."""
     if dist.get_backend(group) == "nccl":
+        comm = lib_comm(t.device, group)
+        if comm is not None:
+            return comm.allgather(t)
         out = torch.empty((t.shape[0] * size,) + tuple(t.shape[1:]), dtype=t.dtype,
                           device=t.device)
         dist.all_gather_into_tensor(out, t, group=group)
@@ -312,15 +436,25 @@ def _share_with_peers(tensors, group=None) -> list:
     Returns, for each other rank in rank order, its tensors mapped here."""
     from torch.multiprocessing.reductions import reduce_tensor
 
+    from . import _lib
+
     rank, size = world()
-    torch.cuda.synchronize(tensors[0].device)
-    mine = [reduce_tensor(t) for t in tensors]
+    dev = tensors[0].device
+    torch.cuda.synchronize(dev)
+    mine = (dev.index, [reduce_tensor(t) for t in tensors])
     handles = [None] * size
     if size > 1:
         dist.all_gather_object(handles, mine, group=group)
     err = None
     try:
-        peers = [[fn(*args) for fn, args in handles[r]] for r in range(size) if r != rank]
+        # the fused epilogues run on THIS device and store into the peers'
+        # buffers: enable access from here to every peer device (torch opens
+        # the IPC handles under the exporting device, which does not)
+        ctx = _lib.ctx_for(dev)
+        for r in range(size):
+            if r != rank and handles[r][0] != dev.index:
+                _lib.check(_lib.load_library().dooly_enable_peer_access(ctx, handles[r][0]), ctx)
+        peers = [[fn(*args) for fn, args in handles[r][1]] for r in range(size) if r != rank]
     except Exception as exc:  # e.g. IPC not permitted: every rank must learn it together
         peers, err = None, exc
     if size > 1:   # agree on success so no rank is left waiting in a later collective

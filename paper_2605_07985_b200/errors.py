@@ -97,6 +97,10 @@ class DeviceError(DoolyError):
     """A CUDA call inside libdooly_b200 failed (status DOOLY_ERR_CUDA)."""
 
 
+class CommError(DoolyError):
+    """An NCCL call inside libdooly_b200 failed (status DOOLY_ERR_NCCL)."""
+
+
 # C-ABI status codes (include/dooly_b200.h) -> exception class.
 STATUS_OK = 0
 STATUS_INVALID_ARG = 1
@@ -105,6 +109,7 @@ STATUS_UNKNOWN_SIGNATURE = 3
 STATUS_DUPLICATE_KEY = 4
 STATUS_NON_TERMINATION = 5
 STATUS_CUDA = 6
+STATUS_NCCL = 7
 
 _STATUS_CLASS = {
     STATUS_INVALID_ARG: ValueError,
@@ -112,6 +117,7 @@ _STATUS_CLASS = {
     STATUS_DUPLICATE_KEY: DuplicateKey,
     STATUS_NON_TERMINATION: NonTermination,
     STATUS_CUDA: DeviceError,
+    STATUS_NCCL: CommError,
 }
 
 
