@@ -6,6 +6,8 @@
 
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 
 namespace dooly {
@@ -100,9 +102,14 @@ int check_cuda(dooly_ctx* ctx, cudaError_t e, const char* where) {
 }
 
 // Guard: every call runs on the ctx's device.
+// Device guard of every launching entry point, also an NVTX range named after
+// the entry point (SURVEY §5 tracing: host-side ranges nsys / ncu --nvtx can
+// filter on; no-ops without a tool attached).
 struct DeviceGuard {
   int prev = -1;
-  explicit DeviceGuard(int dev) {
+  explicit DeviceGuard(int dev, const char* range = nullptr) {
+    if (range) nvtxRangePushA(range);
+    pushed = range != nullptr;
     cudaGetDevice(&prev);
     if (prev != dev) cudaSetDevice(dev);
   }
@@ -110,7 +117,9 @@ struct DeviceGuard {
     int cur = -1;
     cudaGetDevice(&cur);
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    if (pushed) nvtxRangePop();
   }
+  bool pushed = false;
 };
 
 }  // namespace
@@ -151,7 +160,7 @@ int dooly_predict(dooly_ctx* ctx, int kind, const void* table, int64_t n_sig,
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: null pointer");
   if ((uintptr_t)table % 32 != 0)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "predict: table must be 32-byte aligned");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   if (n_q > 0) ctx->launches += 1;
   return check_cuda(ctx,
                     dooly::launch_predict(kind, table, n_sig, sig, x, n_q, out, flag_bits,
@@ -173,7 +182,7 @@ int dooly_attn_pack(dooly_ctx* ctx, const void* table, int64_t n_sig, void* pack
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "attn_pack: packed must be 32-B, table 16-B aligned");
   if (n_sig > 0xFFFFFFFFll)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "attn_pack: more than 2^32 rows");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_attn_pack(table, n_sig, packed, (cudaStream_t)stream,
                                             ctx->n_sm, &ctx->launches),
@@ -196,7 +205,7 @@ int dooly_fit(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, const 
   if (workspace != nullptr &&
       (workspace_bytes < dooly::fit_workspace_size(kind, n_sig) || (uintptr_t)workspace % 256))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit: workspace too small or misaligned");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_fit(kind, x, n_pts, y, pt_off, n_sig, table, fit_err, status,
                                       workspace, (cudaStream_t)stream, ctx->n_sm,
@@ -222,7 +231,7 @@ int dooly_fit_grid(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_pts, c
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: null pointer");
   if ((uintptr_t)table % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid: table must be 16-byte aligned");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_fit_grid(kind, x, n_pts, y, n_sig, table, fit_err, status,
                                            nullptr, workspace, (cudaStream_t)stream, ctx->n_sm,
@@ -245,7 +254,7 @@ int dooly_fit_grid_packed(dooly_ctx* ctx, const uint32_t* x, int64_t n_pts, cons
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_packed: null pointer");
   if ((uintptr_t)table % 16 || (uintptr_t)packed % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_packed: table and packed must be 16-byte aligned");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_fit_grid(kind, x, n_pts, y, n_sig, table, fit_err, status,
                                            nullptr, workspace, (cudaStream_t)stream, ctx->n_sm,
@@ -276,7 +285,7 @@ int dooly_fit_grid_bcast(dooly_ctx* ctx, int kind, const uint32_t* x, int64_t n_
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: null pointer");
   if ((uintptr_t)table % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "fit_grid_bcast: table must be 16-byte aligned");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   cudaError_t e = dooly::launch_peer_sync(peers->n_peers, peers->flag, flag, target, timed_out,
                                           (cudaStream_t)stream, &ctx->launches, 1);
   if (e == cudaSuccess)
@@ -300,7 +309,7 @@ int dooly_sha256_records(dooly_ctx* ctx, const uint32_t* words, const int64_t* r
   if (n < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records: negative size");
   if (n > 0 && (!words || !rec_off || !op_bytes || !op_off || !out_digest))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records: null pointer");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_sha256_records(words, rec_off, n, op_bytes, op_off, sym_bytes,
                                                  sym_off, attr_digests, out_digest,
@@ -332,7 +341,7 @@ int dooly_sha256_records_bcast(dooly_ctx* ctx, const uint32_t* words, const int6
                   "sha256_records_bcast: null or misaligned peer buffer");
   if ((uintptr_t)out_digest % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_records_bcast: digests must be 16-B aligned");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   cudaError_t e = dooly::launch_peer_sync(peers->n_peers, peers->flag, flag, target, timed_out,
                                           (cudaStream_t)stream, &ctx->launches, 1);
   if (e == cudaSuccess)
@@ -358,7 +367,7 @@ int dooly_sha256_messages(dooly_ctx* ctx, const uint8_t* msgs, const int64_t* of
   if (n < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_messages: negative size");
   if (n > 0 && (!off || !out_digest))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "sha256_messages: null pointer");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   if (n > 0) ctx->launches += 1;
   return check_cuda(ctx,
                     dooly::launch_sha256_messages(msgs, off, n, out_digest,
@@ -384,7 +393,7 @@ int dooly_dedup_digests(dooly_ctx* ctx, const uint8_t* digests, int64_t n,
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: null pointer");
   if (workspace_bytes < dooly::dedup_workspace_size(n, n_db))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: workspace too small");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_dedup(digests, n, db_digests, n_db, out_first, out_uid,
                                         out_is_new, out_in_db, out_n_unique, workspace,
@@ -410,7 +419,7 @@ int dooly_route_plan(dooly_ctx* ctx, const uint8_t* digests, int64_t n, int worl
   if (!workspace || workspace_bytes < dooly::route_workspace_size(n, world) ||
       (uintptr_t)workspace % 16)
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_plan: workspace too small or misaligned");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_route_plan(digests, n, world, gidx0, out_perm, out_counts,
                                              out_digests, out_gidx, workspace,
@@ -427,7 +436,7 @@ int dooly_dedup_firsts(dooly_ctx* ctx, int64_t n, int64_t n_db, const int64_t* g
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup_firsts: null pointer");
   if (workspace_bytes < dooly::dedup_workspace_size(n, n_db))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup_firsts: workspace too small");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_dedup_firsts(n, n_db, gidx, out_firsts, workspace,
                                                (cudaStream_t)stream, ctx->n_sm, &ctx->launches),
@@ -443,7 +452,7 @@ int dooly_route_reply(dooly_ctx* ctx, const int64_t* gidx, const int64_t* first,
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_reply: bad size or world");
   if (m > 0 && (!gidx || !first || !is_new || !out_rows || (per > 0 && !all_firsts)))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_reply: null pointer");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_route_reply(gidx, first, is_new, in_db, m, all_firsts, per,
                                               world, out_rows, (cudaStream_t)stream, ctx->n_sm,
@@ -458,7 +467,7 @@ int dooly_route_finish(dooly_ctx* ctx, const int64_t* rows, const int64_t* perm,
   if (n < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_finish: negative size");
   if (n > 0 && (!rows || !perm || !out_first || !out_uid || !out_is_new))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "route_finish: null pointer");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_route_finish(rows, perm, n, out_first, out_uid, out_is_new,
                                                out_in_db, (cudaStream_t)stream, ctx->n_sm,
@@ -499,7 +508,7 @@ int dooly_iter_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_
   if (n_it < 0) return fail(ctx, DOOLY_ERR_INVALID_ARG, "iter_eval: negative size");
   if (n_it > 0 && (!it_feat || !it_lat))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "iter_eval: null pointer");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   if (n_it > 0) ctx->launches += 1;
   return check_cuda(ctx,
                     dooly::launch_iter_eval(ops, affine_table, n_affine, attn_table, n_attn,
@@ -525,7 +534,7 @@ int dooly_sim_eval(dooly_ctx* ctx, const dooly_oplist* ops, const void* affine_t
   int rc = dooly_iter_eval(ctx, ops, affine_table, n_affine, attn_table, n_attn, it_feat, n_it,
                            it_lat, err_first, stream);
   if (rc) return rc;
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   return check_cuda(ctx,
                     dooly::launch_sim_eval(it_lat, it_start, it_off, n_shards, n_it, clock,
                                            arrival, first_it, last_it, out_tok, n_req, ttft,
@@ -565,7 +574,7 @@ int dooly_profile_fit(dooly_ctx* ctx, int kind, const dooly_sweep_desc* descs, i
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "profile_fit: null pointer");
   if ((out_x != nullptr) != (out_y != nullptr) || (out_x != nullptr && out_off == nullptr))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "profile_fit: out_x/out_y/out_off go together");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   if (n_sig > 0) ctx->launches += 1;
   return check_cuda(ctx,
                     dooly::launch_profile_fit(kind, descs, n_sig, grid, table, fit_err, status,
@@ -599,7 +608,7 @@ int dooly_sim_run(dooly_ctx* ctx, const dooly_oplist* ops, const dooly_sched* cf
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "sim: null pointer");
   if (workspace_bytes < dooly::sim_workspace_size(cfg, 0, n_shards))
     return fail(ctx, DOOLY_ERR_INVALID_ARG, "sim: workspace too small");
-  DeviceGuard g(ctx->device);
+  DeviceGuard g(ctx->device, __func__);
   if (n_shards > 0) ctx->launches += 1;
   return check_cuda(
       ctx,
