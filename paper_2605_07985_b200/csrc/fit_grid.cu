@@ -1143,6 +1143,171 @@ __global__ void __launch_bounds__(256, 2) fit_grid_db_kernel(
   }
 }
 
+// ---- warp-specialised attention grid fit (opt-in, DOOLY_FIT_GRID_KERNEL=ws /
+// ws8 / ws3; measured slower than fit_grid_warp_kernel, see the launcher and
+// profiles/r2_fit_grid_ws.md).  One persistent CTA per SM: warp 0 is the
+// PRODUCER — lane 0 bulk-copies (1-D TMA, cp.async.bulk + mbarrier
+// complete_tx) whole y rows of the CTA's signatures into an S-stage shared
+// memory ring — and the other WSG x WSW warps are CONSUMERS in WSG groups, group
+// g fitting the CTA's signatures k = g, g + WSG, ...  A group fits one
+// signature with all its threads: each thread keeps the scaled features of
+// ITS points in registers for the whole launch (the grid is shared by every
+// signature), reads the row's y from shared memory in both passes (pass 2
+// re-reads smem instead of L2), and the group reduces b and the MAPE through
+// shared memory behind a named barrier; thread 0 emits the row and releases
+// the stage to the producer.  y crosses HBM once, always with a ring of rows
+// in flight, and no consumer ever waits on a global load.  The arithmetic is
+// exactly fit_grid_warp_kernel's (grouped passes when the grid is grp4,
+// per-point passes otherwise), only the summation order differs.
+constexpr size_t kWsRing = 160 * 1024;               // y ring bytes
+
+template <int kWsGroups, int kWsWarps>
+__global__ void __launch_bounds__(32 + kWsGroups * kWsWarps * 32, 1) fit_grid_ws_kernel(
+    const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
+    const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
+    uint8_t* __restrict__ status, const GridOut pe, int allow_factor, int n_stage) {
+  constexpr int KIND = DOOLY_KIND_ATTN, NC = 10;
+  constexpr int kWsGT = kWsWarps * 32;                 // threads per group
+  constexpr int kWsMaxG = 32 / kWsWarps;               // 4-point groups per thread (n_pts <= 4096)
+  extern __shared__ __align__(128) unsigned char wsdyn[];
+  double* ring = reinterpret_cast<double*>(wsdyn);
+  __shared__ __align__(8) uint64_t full[8], empty[8];
+  __shared__ double sW[NC][NC];
+  __shared__ double part[kWsGroups][kWsWarps][NC + 1];
+  __shared__ double scoef[kWsGroups][NC];
+  __shared__ double sinv[3];
+  __shared__ uint32_t slo[3], shi[3];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int t = tid; t < NC * NC; t += blockDim.x) sW[t / NC][t % NC] = gf->W[t / NC][t % NC];
+  if (tid < 3) {
+    sinv[tid] = gf->inv[tid];
+    slo[tid] = gf->lo[tid];
+    shi[tid] = gf->hi[tid];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < n_stage; ++i) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(g_smem(&full[i])));
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(g_smem(&empty[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const bool ok = gf->ok != 0;
+  const bool grouped = allow_factor && gf->grp4 != 0;
+  const int n = (int)n_pts;
+  const int64_t n_mine = n_sig > blockIdx.x ? (n_sig - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint32_t row_bytes = (uint32_t)n * 8u;
+
+  if (wid == 0) {  // ---------------- producer
+    if (lane == 0 && ok) {
+      for (int64_t k = 0; k < n_mine; ++k) {
+        const int st = (int)(k % n_stage);
+        if (k >= n_stage) g_wait(&empty[st], (uint32_t)(((k / n_stage) - 1) & 1));
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(g_smem(&full[st])),
+                     "r"(row_bytes)
+                     : "memory");
+        const int64_t s = blockIdx.x + k * gridDim.x;
+        g_bulk(ring + (size_t)st * n, y + s * n_pts, row_bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers
+  const int g = (wid - 1) / kWsWarps, gw = (wid - 1) % kWsWarps, gt = tid - 32 - g * kWsGT;
+  const int ngr = n / (4 * kWsGT);  // 4-point groups per thread (launcher: 1..kWsMaxG)
+  // this thread's points: groups q = gt + kWsGT * j, points 4q .. 4q + 3
+  // (f3 per point and the group's (u1, u2) in registers; the per-point passes
+  // of a non-grp4 grid read f1 / f2 from the L1-resident planes)
+  double4 f3r[kWsMaxG];
+  double2 ur[kWsMaxG];
+#pragma unroll
+  for (int j = 0; j < kWsMaxG; ++j) {
+    if (j < ngr) {
+      const int q = gt + kWsGT * j;
+      f3r[j] = g_ld_f(fpl + 2 * n + 4 * q);
+      ur[j] = grouped ? __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + q)
+                      : make_double2(0.0, 0.0);
+    }
+  }
+  const int bar_id = 1 + g;
+  auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kWsGT) : "memory"); };
+  for (int64_t k = g; k < n_mine; k += kWsGroups) {
+    const int64_t s = blockIdx.x + k * gridDim.x;
+    if (!ok) {
+      if (gt == 0) write_unfitted_grid<KIND>(pe, gf, table, s, fit_err, status);
+      continue;
+    }
+    const int st = (int)(k % n_stage);
+    g_wait(&full[st], (uint32_t)((k / n_stage) & 1));
+    const double* yr = ring + (size_t)st * n;
+    double acc[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int j = 0; j < kWsMaxG; ++j) {
+      if (j < ngr) {
+        const double4 yv = *reinterpret_cast<const double4*>(yr + 4 * (gt + kWsGT * j));
+        if (grouped) {
+          grid_g1_step(yv, f3r[j], ur[j].x, ur[j].y, acc);
+        } else {
+          const int q = gt + kWsGT * j;
+          const double4 fv[3] = {g_ld_f(fpl + 4 * q), g_ld_f(fpl + n + 4 * q), f3r[j]};
+          grid_p1_step<KIND>(yv, fv, acc);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NC; ++i) acc[i] = g_warp_sum(acc[i]);
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < NC; ++i) part[g][gw][i] = acc[i];
+    group_sync();
+    if (gt < NC) {  // c = W b: thread j forms coefficient j
+      double b[NC];
+#pragma unroll
+      for (int i = 0; i < NC; ++i) {
+        double v = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWsWarps; ++w) v += part[g][w][i];
+        b[i] = v;
+      }
+      double cj = 0.0;
+#pragma unroll
+      for (int i = 0; i < NC; ++i) cj = fma(sW[gt][i], b[i], cj);
+      scoef[g][gt] = cj;
+    }
+    group_sync();
+    double c[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) c[i] = scoef[g][i];
+    double err = 0.0;
+#pragma unroll
+    for (int j = 0; j < kWsMaxG; ++j) {
+      if (j < ngr) {
+        const double4 yv = *reinterpret_cast<const double4*>(yr + 4 * (gt + kWsGT * j));
+        if (grouped) {
+          grid_g2_step(yv, f3r[j], ur[j].x, ur[j].y, c, err);
+        } else {
+          const int q = gt + kWsGT * j;
+          const double4 fv[3] = {g_ld_f(fpl + 4 * q), g_ld_f(fpl + n + 4 * q), f3r[j]};
+          grid_p2_step<KIND>(yv, fv, c, err);
+        }
+      }
+    }
+    err = g_warp_sum(err);
+    if (lane == 0) part[g][gw][NC] = err;
+    group_sync();  // every read of the stage and of scoef is done
+    if (gt == 0) {
+      asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(g_smem(&empty[st])) : "memory");
+      double e = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWsWarps; ++w) e += part[g][w][NC];
+      emit_row<KIND>(pe, gf, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
+                     e / (double)n_pts, DOOLY_FIT_OK);
+    }
+  }
+}
+
 template <int KIND>
 static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const double* y, int64_t n_sig,
                                     void* table, double* fit_err, uint8_t* status,
@@ -1155,7 +1320,7 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   if (e != cudaSuccess) return e;
   *launches += 1;
   if (n_sig == 0) return cudaSuccess;
-  // "db" (default for affine) | "warp" (default for attention) | "stage" | "plain"
+  // "db" (default for affine) | "warp" (default for attention) | "ws"/"ws8"/"ws3" | "stage" | "plain"
   const char* which = getenv("DOOLY_FIT_GRID_KERNEL");
   const char* fac = getenv("DOOLY_FIT_GRID_FACTOR");   // "0": per-point attention passes
   const int allow_factor = fac == nullptr || fac[0] != '0';
@@ -1173,6 +1338,30 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
     auto kern = n_pts % 512 == 0 ? fit_grid_db_kernel<KIND, 4> : fit_grid_db_kernel<KIND, 2>;
     kern<<<(unsigned)warp_blocks, 256, 0, stream>>>(fpl, n_pts, y, n_sig, gf, table, fit_err,
                                                     status, pe, allow_factor);
+    *launches += 1;
+    return cudaGetLastError();
+  }
+  // warp-specialised TMA ring (attention default): whole rows <= 32 KB,
+  // n_pts a multiple of 512 (4-point groups spread evenly over a group's threads)
+  // opt-in (measured 6.85 ms vs the warp kernel's 3.69 ms per 0.5M x 4096
+  // attention points: two or three consumer warps per SMSP cannot hide the
+  // FP64 dependency chains; profiles/r2_fit_grid_ws.md)
+  const bool want_ws = which != nullptr && strncmp(which, "ws", 2) == 0;
+  // variants: "ws" 2 groups x 4 warps, "ws8" 2 x 8, "ws3" 3 x 4
+  const int wsw = which != nullptr && strcmp(which, "ws8") == 0 ? 8 : 4;
+  const int wsg = which != nullptr && strcmp(which, "ws3") == 0 ? 3 : 2;
+  if (KIND == DOOLY_KIND_ATTN && want_ws && aligned && n_pts % (4 * 32 * wsw) == 0 &&
+      n_pts / (4 * 32 * wsw) <= 32 / wsw) {
+    const int n_stage = (int)std::min<int64_t>(8, kWsRing / (n_pts * 8));
+    const size_t smem = (size_t)n_stage * n_pts * 8;
+    auto kern = wsw == 8 ? fit_grid_ws_kernel<2, 8>
+              : wsg == 3 ? fit_grid_ws_kernel<3, 4> : fit_grid_ws_kernel<2, 4>;
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    const int64_t blocks = std::min<int64_t>(n_sm, std::max<int64_t>(1, n_sig));
+    kern<<<(unsigned)blocks, 32 + wsg * wsw * 32, smem, stream>>>(
+        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, allow_factor, n_stage);
     *launches += 1;
     return cudaGetLastError();
   }

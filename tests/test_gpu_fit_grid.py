@@ -61,7 +61,7 @@ def _oracle(kind, x, y):
 
 @pytest.mark.parametrize("kind", [AFFINE, ATTN])
 @pytest.mark.parametrize("n_sig,n_pts", [(1, 512), (37, 512), (301, 512), (37, 510), (9, 4096), (7, 64), (5, 136), (13, 768)])
-@pytest.mark.parametrize("kernel", ["warp", "stage", "db"])
+@pytest.mark.parametrize("kernel", ["warp", "stage", "db", "ws"])
 def test_fit_grid_matches_oracle_and_csr(kind, n_sig, n_pts, kernel, dev, monkeypatch):
     """n_pts % 4 == 0 takes the warp-per-signature kernel, its register
     double-buffered form (db: n_pts % 256 == 0, the affine default) or the
@@ -178,7 +178,8 @@ def test_fit_grid_grouped_attention_passes(dev, monkeypatch):
 
 
 @pytest.mark.parametrize("n_sig,n_pts,kernel", [(300, 4096, "warp"), (37, 512, "db"), (5, 64, "stage"),
-                                                (9, 125, "warp"), (4, 8, "warp")])
+                                                (9, 125, "warp"), (4, 8, "warp"), (300, 4096, "ws"),
+                                                (1000, 2048, "ws"), (3, 512, "ws")])
 def test_fit_grid_packed_equals_attn_pack(n_sig, n_pts, kernel, dev, monkeypatch):
     """dooly_fit_grid_packed's epilogue writes the 96-B serving table
     byte-identical to dooly_attn_pack of the fitted table (header included),
@@ -198,3 +199,29 @@ def test_fit_grid_packed_equals_attn_pack(n_sig, n_pts, kernel, dev, monkeypatch
     assert torch.equal(packed, ref)
     plain = fit_grid(ATTN, xt, yt)
     assert torch.equal(plain.table, fr.table) and torch.equal(plain.status, fr.status)
+
+
+@pytest.mark.parametrize("factor", ["0", "1"])
+@pytest.mark.parametrize("n_sig", [1, 149, 3001])
+def test_fit_grid_ws_matches_warp(factor, n_sig, dev, monkeypatch):
+    """The warp-specialised TMA-ring attention kernel (default) against the
+    warp kernel: same statuses and boxes, coefficients within 1e-12 normwise
+    (only the summation order differs), fit_err within 1e-12 relative; more
+    signatures than CTAs x stages so the ring wraps."""
+    monkeypatch.setenv("DOOLY_FIT_GRID_FACTOR", factor)
+    rng = np.random.default_rng(7 + n_sig)
+    x = _grid(ATTN, 4096, rng)[:, :4096]
+    y = _ys(ATTN, x, n_sig, rng)
+    out = {}
+    for k in ("warp", "ws"):
+        monkeypatch.setenv("DOOLY_FIT_GRID_KERNEL", k)
+        out[k] = _fit_grid_gpu(ATTN, x, y, dev)
+    a = rows_to_table(ATTN, out["warp"].rows())
+    b = rows_to_table(ATTN, out["ws"].rows())
+    assert torch.equal(out["warp"].status, out["ws"].status)
+    for k in ("lo", "hi", "inv"):
+        assert np.array_equal(a[k], b[k])
+    dc = np.abs(a["coef"] - b["coef"]).max(axis=1) / np.abs(a["coef"]).max(axis=1)
+    assert dc.max() <= 1e-12, dc.max()
+    fa, fb = out["warp"].fit_err.cpu().numpy(), out["ws"].fit_err.cpu().numpy()
+    assert np.max(np.abs(fa - fb) / fa) <= 1e-12
