@@ -115,15 +115,47 @@ def _a5(manifest, model_name, rate, dev, seed=1):
     regs = fit(db, dev)
     sched = SchedConfig(chunk=8192, max_batch=256)
     reqs = _requests(200, rate, seed)
-    met, feats, lat, _ = _gpu_run(reqs, model, backend, manifest.hardware, regs, sched, 200000)
+    met, feats, lat, ct = _gpu_run(reqs, model, backend, manifest.hardware, regs, sched, 200000)
     ref = _reference(reqs, runnable_entries(model, backend, 1), model, backend,
                      manifest.hardware, sched)
+    # the GPU run IS the oracle's regression pipeline: the oracle event loop over
+    # the same regressor rows reproduces it bit for bit, so whatever separates
+    # it from reference_run is the regression family's error, not the kernels'
+    _assert_gpu_equals_oracle_run(reqs, model, manifest.hardware, regs, sched, met, feats, ct)
     err = {"ttft": osim.percentile_mape(met.ttft, ref["ttft"]),
            "tpot": osim.percentile_mape(met.tpot, ref["tpot"]),
            "same_compositions": feats == [tuple(f) for f in ref["feats"]],
            "iterations": (len(feats), ref["n_iter"])}
     print(f"A5 {model_name} rate {rate}: {err}")
     return err
+
+
+def _assert_gpu_equals_oracle_run(reqs, model, hw, regs, sched, met, feats, ct):
+    from helpers import rows_to_table
+    from paper_2605_07985_b200.sim import kv_capacity
+
+    tabs = {k: rows_to_table(k, regs.tables[k].rows()) for k in regs.tables}
+    ops = []
+    for i in range(ct.n_ops):
+        feat, row = ct.oplist.feat[i], ct.oplist.row[i]
+        op = {"feat": feat, "repeat": ct.oplist.repeat[i], "window_slot": ct.oplist.window_slot[i],
+              "bytes_per_tok": ct.oplist.bytes_per_tok[i]}
+        if feat != osim.FEAT_COMM:
+            t = tabs[ATTN if feat == osim.FEAT_ATTN else 0]
+            op.update(coef=list(t["coef"][row]), inv=list(t["inv"][row]))
+        ops.append(op)
+    r = osim.run_shard([q.arrival_s for q in reqs], [q.prompt_tokens for q in reqs],
+                       [q.output_tokens for q in reqs], [q.cached_tokens for q in reqs], ops,
+                       sched.chunk, sched.max_batch, model.kv_bytes_per_token(),
+                       kv_capacity(model, hw, 1, sched), ct.window, 1, log=True)
+    assert feats == [tuple(f) for f in r["feats"]]
+    assert np.array_equal(met.ttft.view(np.uint64), np.asarray(r["ttft"]).view(np.uint64))
+    ok = ~np.isnan(r["tpot"])
+    assert np.array_equal(met.tpot[ok], np.asarray(r["tpot"])[ok])
+
+
+class A5NotMet(Exception):
+    """A5's tolerances not met (the only failure the strict xfails accept)."""
 
 
 def _a5_holds(err) -> bool:
@@ -147,15 +179,19 @@ def test_a5_c1_busy_percentiles(corpus, dev):
     assert max(err["ttft"].values()) <= 0.05 and max(err["tpot"].values()) <= 0.08, err
 
 
-@pytest.mark.xfail(strict=True, reason="SPEC D2 regression family (affine / quadratic) cannot "
+@pytest.mark.xfail(strict=True, raises=A5NotMet, reason="SPEC D2 regression family (affine / quadratic) cannot "
                    "represent the roofline oracle's hinge: measured TPOT error ~30% at C1's own "
                    "0.5 req/s (memory-bound decode below the ridge); DESIGN.md §7")
 def test_a5_c1_light_load(corpus, dev):
-    assert _a5_holds(_a5(corpus, "llama-3-8b-like", 0.5, dev))
+    err = _a5(corpus, "llama-3-8b-like", 0.5, dev)
+    if not _a5_holds(err):
+        raise A5NotMet(str(err))
 
 
-@pytest.mark.xfail(strict=True, reason="SPEC D2 regression family on the MoE fixture: affine "
+@pytest.mark.xfail(strict=True, raises=A5NotMet, reason="SPEC D2 regression family on the MoE fixture: affine "
                    "fits of tiny ops go below the 1e-7 clamp at decode batch sizes (TPOT error "
                    ">10x); DESIGN.md §7")
 def test_a5_moe_fixture(fixtures_manifest, dev):
-    assert _a5_holds(_a5(fixtures_manifest, "moe-small", 1000.0, dev))
+    err = _a5(fixtures_manifest, "moe-small", 1000.0, dev)
+    if not _a5_holds(err):
+        raise A5NotMet(str(err))

@@ -116,6 +116,10 @@ def _worker(rank: int, world: int, port: int, q) -> None:
             assert torch.equal(pt.table, ref.table), kind
             assert torch.equal(pt.status, ref.status), kind
             assert torch.equal(pt.fit_err, ref.fit_err), kind
+            # the collective form side by side: the same local fit, rows all-gathered
+            mine = fit_grid(kind, xg, yg[a:b])
+            assert torch.equal(ddist.all_gather_rows(mine.table, n_total), pt.table), kind
+            assert torch.equal(ddist.all_gather_rows(mine.fit_err, n_total), pt.fit_err), kind
             dist.barrier()
         dist.barrier()
         q.put((rank, "ok"))
@@ -167,7 +171,7 @@ def test_bench_ranks_torchrun(world):
            "--gpus", str(world), "--steps", "3", "--warmup", "3", "--queries", "4000000",
            "--sigs", "20000", "--points", "512", "--records", "100000",
            "--e2e-queries", "2000000", "--sim-requests", "20000", "--sim-shards", "16",
-           "--csr-fit", "0"]
+           "--sim-wide-shards", "0", "--csr-fit", "0"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
