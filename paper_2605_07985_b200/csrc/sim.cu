@@ -580,29 +580,61 @@ cudaError_t launch_sim(const dooly_oplist* ops, const dooly_sched* cfg, const vo
 // thread per request reads its first/last-token clocks.
 namespace dooly {
 
-__global__ void __launch_bounds__(128) sim_clock_kernel(const double* __restrict__ it_lat,
-                                                        const double* __restrict__ it_start,
-                                                        const int64_t* __restrict__ it_off,
-                                                        int64_t n_shards, int64_t n_it,
-                                                        double* __restrict__ clock) {
-  const int lane = threadIdx.x & 31;
+// One warp per shard.  The recurrence is inherently sequential (the same f64
+// operation order as the event loop), so lane 0 runs it over a 256-iteration
+// chunk staged in shared memory by the whole warp (coalesced loads of it_lat /
+// it_start, the next chunk's loads issued before the scan), then the warp
+// writes the chunk's clocks back coalesced.
+constexpr int kClockChunk = 256;
+constexpr int kClockWarps = 4;
+
+__global__ void __launch_bounds__(32 * kClockWarps) sim_clock_kernel(
+    const double* __restrict__ it_lat, const double* __restrict__ it_start,
+    const int64_t* __restrict__ it_off, int64_t n_shards, int64_t n_it,
+    double* __restrict__ clock) {
+  __shared__ double sl[kClockWarps][kClockChunk], ss[kClockWarps][kClockChunk];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (w >= n_shards) return;
   const int64_t b = it_off ? it_off[w] : 0, e = it_off ? it_off[w + 1] : n_it;
-  double c = 0.0;
-  for (int64_t i0 = b; i0 < e; i0 += 32) {
-    const int64_t i = i0 + lane;
-    const double l = i < e ? it_lat[i] : 0.0;
-    const double s = (i < e && it_start) ? it_start[i] : 0.0;
-    double mine = 0.0;
-    const int m = (int)min((int64_t)32, e - i0);
-    for (int j = 0; j < m; ++j) {
-      const double lj = __shfl_sync(0xFFFFFFFFu, l, j);
-      const double sj = __shfl_sync(0xFFFFFFFFu, s, j);
-      c = __dadd_rn(c < sj ? sj : c, lj);
-      if (lane == j) mine = c;
+  double* L = sl[wid];
+  double* S = ss[wid];
+  constexpr int PER = kClockChunk / 32;
+  double nl[PER], ns[PER];
+  auto fetch = [&](int64_t i0) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int64_t i = i0 + k * 32 + lane;
+      nl[k] = i < e ? it_lat[i] : 0.0;
+      ns[k] = (i < e && it_start) ? it_start[i] : 0.0;
     }
-    if (i < e) clock[i] = mine;
+  };
+  double c = 0.0;
+  fetch(b);
+  for (int64_t i0 = b; i0 < e; i0 += kClockChunk) {
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      L[k * 32 + lane] = nl[k];
+      S[k * 32 + lane] = ns[k];
+    }
+    __syncwarp();
+    if (i0 + kClockChunk < e) fetch(i0 + kClockChunk);   // next chunk in flight during the scan
+    const int m = (int)min((int64_t)kClockChunk, e - i0);
+    if (lane == 0) {
+#pragma unroll 8
+      for (int j = 0; j < m; ++j) {
+        const double sj = S[j];
+        c = __dadd_rn(c < sj ? sj : c, L[j]);
+        L[j] = c;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int64_t i = i0 + k * 32 + lane;
+      if (i < e) clock[i] = L[k * 32 + lane];
+    }
+    __syncwarp();
   }
 }
 
@@ -637,9 +669,9 @@ cudaError_t launch_sim_eval(const double* it_lat, const double* it_start, const 
                             int64_t* err_first, cudaStream_t stream, int n_sm,
                             int64_t* launches) {
   if (n_it > 0 && n_shards > 0) {
-    const int64_t blocks = (n_shards * 32 + 127) / 128;
-    sim_clock_kernel<<<(unsigned)blocks, 128, 0, stream>>>(it_lat, it_start, it_off, n_shards,
-                                                           n_it, clock);
+    const int64_t blocks = (n_shards + kClockWarps - 1) / kClockWarps;
+    sim_clock_kernel<<<(unsigned)blocks, 32 * kClockWarps, 0, stream>>>(it_lat, it_start, it_off,
+                                                                        n_shards, n_it, clock);
     *launches += 1;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
