@@ -965,17 +965,21 @@ def run_ours(args):
         for _ in range(2):
             predict_host_many(batches)
         barrier_sync(dist_on)
-        e_steps = max(1, min(args.steps, 3))
-        t0 = time.perf_counter()
+        e_steps = max(3, min(args.steps, 5))
+        e_times = []
         for _ in range(e_steps):
-            predict_host_many(batches)
+            t0 = time.perf_counter()
+            predict_host_many(batches)          # synchronises (host buffers are the output)
+            e_times.append(time.perf_counter() - t0)
         barrier_sync(dist_on)
-        e_s = max_over_ranks((time.perf_counter() - t0) / e_steps, dist_on)
+        # median step: the host link is shared with the rest of the box
+        e_s = max_over_ranks(float(np.median(e_times)), dist_on)
         h2d = sum(host_q[k][0].numel() * 4 + host_q[k][1].numel() * 4 for k in (AFFINE, ATTN))
         d2h = sum(host_q[k][2].numel() * 8 + host_q[k][3].numel() * 4 for k in (AFFINE, ATTN))
         e2e = {"value": world * args.e2e_queries / e_s, "unit": "predictions/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "queries_per_step_per_gpu": args.e2e_queries,
+               "steps": e_steps, "step_s": e_times, "method": "median of the timed steps",
                "path": "sim.predict_host_many: pinned host -> device -> kernel -> host (latencies "
                        "and the extrapolation/clamp flag bit-planes), both kinds' chunks "
                        "interleaved over 3 streams",

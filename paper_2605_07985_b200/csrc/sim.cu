@@ -621,10 +621,13 @@ __global__ void __launch_bounds__(32 * kClockWarps) sim_clock_kernel(
     if (i0 + kClockChunk < e) fetch(i0 + kClockChunk);   // next chunk in flight during the scan
     const int m = (int)min((int64_t)kClockChunk, e - i0);
     if (lane == 0) {
+      // busy iterations (it_start == 0: the common case) chain only the add;
+      // the max with an idle jump target is taken on the rare nonzero start
 #pragma unroll 8
       for (int j = 0; j < m; ++j) {
         const double sj = S[j];
-        c = __dadd_rn(c < sj ? sj : c, L[j]);
+        if (__double_as_longlong(sj) != 0ll && c < sj) c = sj;
+        c = __dadd_rn(c, L[j]);
         L[j] = c;
       }
     }
