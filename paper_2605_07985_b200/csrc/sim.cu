@@ -33,50 +33,68 @@ constexpr int SIM_WARPS = 4;
 #define SIM_WIN 1  // decode-window iterations per lane (window <= 32 * SIM_WIN); 2: C1 -13%, C4 +3%
 #endif
 
+// The op list staged in shared memory: regressor rows, and the per-entry
+// fields (feature, repeat, window slot, comm bytes per token) so that lanes
+// evaluating DIFFERENT entries read shared memory instead of issuing
+// lane-divergent loads from the kernel-parameter bank (which serialise per
+// distinct address); the comm constants 2(tp-1)/tp and 1/tp are formed once.
 struct StagedOps {
   AffineRow aff[DOOLY_MAX_OPS];
   AttnRow attn[DOOLY_MAX_OPS];
+  int32_t feat[DOOLY_MAX_OPS];
+  int32_t wslot[DOOLY_MAX_OPS];
+  double rep[DOOLY_MAX_OPS];
+  uint64_t bpt[DOOLY_MAX_OPS];
+  double comm_a;    // RN(2(tp-1) / tp)
+  double comm_rtp;  // RN(1 / tp) when tp is a power of two (exact scaling), else 0
 };
 
 __device__ __forceinline__ void stage_ops(const dooly_oplist& ops, const void* aff_t,
                                           const void* attn_t, StagedOps* s, int tid, int nthr) {
   for (int e = tid; e < ops.n_ops; e += nthr) {
     const int f = ops.feat[e];
+    s->feat[e] = f;
+    s->wslot[e] = ops.window_slot[e];
+    s->rep[e] = (double)ops.repeat[e];
+    s->bpt[e] = (uint64_t)ops.bytes_per_tok[e];
     if (f == DOOLY_FEAT_ATTN)
       s->attn[e] = load_attn(static_cast<const dooly_attn_row*>(attn_t), ops.row[e]);
     else if (f != DOOLY_FEAT_COMM)
       s->aff[e] = load_affine(static_cast<const dooly_affine_row*>(aff_t), ops.row[e]);
   }
+  if (tid == 0) {
+    const int tp = ops.tp > 0 ? ops.tp : 1;
+    s->comm_a = __ddiv_rn((double)(2 * (tp - 1)), (double)tp);
+    s->comm_rtp = (tp & (tp - 1)) == 0 ? __drcp_rn((double)tp) : 0.0;
+  }
 }
 
 // comm_latency: 2(tp-1)/tp * (alpha + bytes/tp * beta), evaluated
-// in Python's operator order.
-__device__ __forceinline__ double comm_latency(int tp, double alpha, double beta, uint64_t bytes) {
-  const double a = __ddiv_rn((double)(2 * (tp - 1)), (double)tp);
-  // bytes / tp for a power-of-two tp is an exact scaling: the multiply by 2^-k
-  // is bit-identical to the IEEE division
-  const double q = (tp & (tp - 1)) == 0 ? mul((double)bytes, __drcp_rn((double)tp))
-                                        : __ddiv_rn((double)bytes, (double)tp);
+// in Python's operator order (a = RN(2(tp-1)/tp) and, for a power-of-two tp,
+// bytes/tp as the exact scaling by RN(1/tp) — both staged once).
+__device__ __forceinline__ double comm_latency(const StagedOps* s, int tp, double alpha,
+                                               double beta, uint64_t bytes) {
+  const double q = s->comm_rtp != 0.0 ? mul((double)bytes, s->comm_rtp)
+                                      : __ddiv_rn((double)bytes, (double)tp);
   const double b = mul(q, beta);
-  return mul(a, add(alpha, b));
+  return mul(s->comm_a, add(alpha, b));
 }
 
 // One entry's clamped contribution before the repeat multiply; invalid rows -> NaN.
 __device__ __forceinline__ double entry_value(const dooly_oplist& ops, const StagedOps* s, int e,
                                               uint32_t num_toks, uint32_t prefill, uint32_t batch,
                                               uint32_t kv_full, uint32_t kv_win, bool& bad) {
-  const int f = ops.feat[e];
+  const int f = s->feat[e];
   bool cl;
   if (f == DOOLY_FEAT_COMM)
-    return comm_latency(ops.tp, ops.comm_alpha, ops.comm_beta,
-                        (uint64_t)num_toks * (uint64_t)ops.bytes_per_tok[e]);
+    return comm_latency(s, ops.tp, ops.comm_alpha, ops.comm_beta, (uint64_t)num_toks * s->bpt[e]);
   if (f == DOOLY_FEAT_ATTN) {
     const AttnRow& r = s->attn[e];
     if (!attn_valid(r)) {
       bad = true;
       return nan64();
     }
-    return clamp_floor(eval_attn(r, prefill, batch, ops.window_slot[e] ? kv_win : kv_full), cl);
+    return clamp_floor(eval_attn(r, prefill, batch, s->wslot[e] ? kv_win : kv_full), cl);
   }
   const AffineRow& r = s->aff[e];
   if (!affine_valid(r)) {
@@ -101,7 +119,7 @@ __global__ void __launch_bounds__(256) iter_eval_kernel(
     bool bad = false;
     for (int e = 0; e < ops.n_ops; ++e) {
       const double v = entry_value(ops, &s, e, nt, pf, bt, kv, kw, bad);
-      lat = add(lat, mul((double)ops.repeat[e], v));
+      lat = add(lat, mul(s.rep[e], v));
     }
     out[i] = lat;
     if (bad && err_first) atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)i);
@@ -281,7 +299,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
               lat_k[k] = 0.0;
               if ((int64_t)u < wmax)
                 for (int e = 0; e < ops.n_ops; ++e)
-                  lat_k[k] = add(lat_k[k], mul((double)ops.repeat[e],
+                  lat_k[k] = add(lat_k[k], mul(s_ops.rep[e],
                                                entry_value(ops, &s_ops, e, nr, 0u, nr, kvs_k[k],
                                                            kvw_k[k], bad)));
             }
@@ -417,10 +435,10 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       bool bad = false;
       double w0 = 0.0, w1 = 0.0;
       if (lane < ops.n_ops)
-        w0 = mul((double)ops.repeat[lane],
+        w0 = mul(s_ops.rep[lane],
                  entry_value(ops, &s_ops, lane, num_toks, prefill, batch, kvs, kvw, bad));
       if (lane + 32 < ops.n_ops)
-        w1 = mul((double)ops.repeat[lane + 32],
+        w1 = mul(s_ops.rep[lane + 32],
                  entry_value(ops, &s_ops, lane + 32, num_toks, prefill, batch, kvs, kvw, bad));
       double lat = 0.0;
       int e = 0;
