@@ -427,8 +427,126 @@ __global__ void __launch_bounds__(256) predict_scalar_kernel(
   }
 }
 
+// ---- staged packed-attention path (DOOLY_KIND_ATTN_PACKED; opt-in, measured
+// slower than the one-lane kernel — profiles/r2_predict.md session 2).
+//
+// ncu on the one-lane-per-row kernel: the busiest unit is the L1 -> L2 request
+// interface (l1tex__m_l1tex2xbar_req_cycles_active ~87%), and a lane's
+// LDG.256 of one row sector is one request, so a 96-B row costs 3 requests.
+// Here the warp fills its rows COOPERATIVELY with cp.async (LDGSTS, L2 ->
+// shared memory without a register round trip): lane l copies 16-B chunk
+// (l mod 6) of row (l / 6) in one instruction, so the 6 chunks of a row are
+// adjacent lanes of the same instruction and coalesce into the 1-2 requests
+// of the lines the row touches (~1.5 per row instead of 3).  Then every lane
+// evaluates its own queries from shared memory with the one-lane arithmetic
+// (eval_row96), so nothing is split across lanes.  Rows sit at a 112-B
+// stride (7 x 16 B): LDS.128 by 8 consecutive lanes hits 8 distinct bank
+// quads.  Steps of kStQ = 64 queries per warp (2 per lane); sig is staged in
+// shared memory for the fill's row lookups.
+constexpr int kStQ = 32;                  // queries per warp step (one per lane)
+constexpr int kStStride = 112;            // bytes per staged row
+constexpr int kStWarps = 4;
+constexpr int kStPer = kStQ * 6 / 32;     // 16-B chunks per lane per step (6)
+
+__global__ void __launch_bounds__(kStWarps * 32, 5) predict_attn_staged_kernel(
+    const void* __restrict__ table, int64_t n_sig, const uint32_t* __restrict__ sig,
+    const uint32_t* __restrict__ x, int64_t n_q, double* __restrict__ out,
+    uint32_t* __restrict__ flags, int64_t* __restrict__ err_first) {
+  // two row buffers per warp: step k+1's fill is in flight while step k evaluates
+  __shared__ __align__(16) unsigned char rows_s[kStWarps][2][kStQ * kStStride];
+  __shared__ uint32_t sig_s[kStWarps][2][kStQ];
+  PackInfo pk = read_pack_header(table, n_sig);
+  if (!pk.ok) n_sig = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned char* rows_g = static_cast<const unsigned char*>(table) + 96;
+  // this lane's chunks: c = lane + 32 i -> row c / 6, byte offset 16 (c % 6)
+  int ch_row[kStPer];
+  uint32_t ch_off[kStPer], ch_dst[kStPer];
+#pragma unroll
+  for (int i = 0; i < kStPer; ++i) {
+    const int c = lane + 32 * i;
+    ch_row[i] = c / 6;
+    ch_off[i] = 16u * (uint32_t)(c % 6);
+    ch_dst[i] = (uint32_t)(ch_row[i] * kStStride) + ch_off[i];
+  }
+  const uint32_t rs_base0 = (uint32_t)__cvta_generic_to_shared(rows_s[wid][0]);
+  const uint32_t rs_base1 = (uint32_t)__cvta_generic_to_shared(rows_s[wid][1]);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_steps = (n_q + kStQ - 1) / kStQ;
+  const int64_t n_words = (n_q + 31) >> 5;
+  int64_t bad_min = INT64_MAX;
+
+  uint32_t sv_n = 0, xv_n[3] = {0u, 0u, 0u};
+  // stage step `st` (buffer b): sig + features into registers / smem, issue the fill
+  auto stage = [&](int64_t st, int b) {
+    const int64_t q = st * kStQ + lane;
+    const bool in = q < n_q;
+    sv_n = in ? __ldg(sig + q) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int p = 0; p < 3; ++p) xv_n[p] = in ? __ldg(x + p * n_q + q) : 0u;
+    sig_s[wid][b][lane] = sv_n;
+    __syncwarp();
+    const uint32_t base = b ? rs_base1 : rs_base0;
+#pragma unroll
+    for (int i = 0; i < kStPer; ++i) {
+      const uint32_t s = sig_s[wid][b][ch_row[i]];
+      if (s < (uint64_t)n_sig) {
+        const unsigned char* src = rows_g + (int64_t)s * 96 + ch_off[i];
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + ch_dst[i]),
+                     "l"(src)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  int64_t st = warp;
+  if (st < n_steps) stage(st, 0);
+  for (int b = 0; st < n_steps; st += n_warps, b ^= 1) {
+    const uint32_t sv = sv_n, x0 = xv_n[0], x1 = xv_n[1], x2 = xv_n[2];
+    const bool more = st + n_warps < n_steps;
+    if (more) {
+      stage(st + n_warps, b ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    const int64_t q = st * kStQ + lane;
+    const double2* rp = reinterpret_cast<const double2*>(rows_s[wid][b] + lane * kStStride);
+    double w[12];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const double2 v = rp[k];
+      w[2 * k] = v.x;
+      w[2 * k + 1] = v.y;
+    }
+    uint32_t lo[3], hi[3];
+    unpack_box((uint64_t)__double_as_longlong(w[4]), (uint64_t)__double_as_longlong(w[8]), pk, lo,
+               hi);
+    const bool live = q < n_q;
+    const bool valid = live && sv < (uint64_t)n_sig && lo[0] <= hi[0];
+    bool cl = false;
+    const double p = clamp_floor(eval_row96(w, x0, x1, x2), cl);
+    const bool e = valid && (x0 < lo[0] || x0 > hi[0] || x1 < lo[1] || x1 > hi[1] ||
+                             x2 < lo[2] || x2 > hi[2]);
+    if (live) out[q] = valid ? p : nan64();
+    if (live && !valid && q < bad_min) bad_min = q;
+    const uint32_t be = __ballot_sync(0xFFFFFFFFu, e), bc = __ballot_sync(0xFFFFFFFFu, valid && cl);
+    if (flags != nullptr && lane == 0 && st < n_words) {
+      flags[st] = be;
+      flags[n_words + st] = bc;
+    }
+    __syncwarp();   // buffer b is refilled two steps later
+  }
+  if (err_first != nullptr && bad_min != INT64_MAX)
+    atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)bad_min);
+}
+
 // DOOLY_PREDICT_ATTN selects the packed-attention kernel: default one lane per
-// row (predict_vec_kernel, 81 G q/s at C5); "coop" / "coop8" / "coop1" the
+// row (predict_vec_kernel, 81 G q/s at C5); "staged" the cp.async-filled
+// shared-memory variant (73 G q/s); "coop" / "coop8" / "coop1" the
 // cooperative 3-lanes-per-row kernel (4 or 8 rows in flight per group, 2 or 1
 // CTAs/SM).  The cooperative form halves the gather wavefronts but issues ~10
 // warp-instructions per query against ~2 (every per-query step is replicated
@@ -439,6 +557,7 @@ static int predict_attn_mode() {
          : strcmp(v, "coop") == 0  ? 0
          : strcmp(v, "coop8") == 0 ? 2
          : strcmp(v, "coop1") == 0 ? 3
+         : strcmp(v, "staged") == 0 ? 4
                                    : 1;
 }
 
@@ -452,7 +571,16 @@ cudaError_t launch_predict_kind(const void* table, int64_t n_sig, const uint32_t
                        (Planes<KIND>::P == 1 || n_q % 8 == 0);
   int per_sm = 0;
   const int mode = predict_attn_mode();
-  if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && mode != 1) {
+  if (KIND == DOOLY_KIND_ATTN_PACKED && mode == 4 && (uintptr_t)table % 16 == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_attn_staged_kernel,
+                                                  kStWarps * 32, 0);
+    const int64_t steps = (n_q + kStQ - 1) / kStQ;
+    int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+    const int64_t need = (steps + kStWarps - 1) / kStWarps;
+    if (blocks > need) blocks = need;
+    predict_attn_staged_kernel<<<(unsigned)blocks, kStWarps * 32, 0, stream>>>(
+        table, n_sig, sig, x, n_q, out, flags, err_first);
+  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && mode != 1 && mode != 4) {
     auto kern = mode == 2 ? predict_attn_coop_kernel<2, 8>
               : mode == 3 ? predict_attn_coop_kernel<1, 8>
                           : predict_attn_coop_kernel<2, 4>;
