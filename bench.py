@@ -331,6 +331,30 @@ def l1tex_roofline(nq: dict, k_ms: dict, sm_mhz):
                       "peak 1/clk/SM x 148 SMs x this run's median SM clock"}
 
 
+def xbar_roofline(nq: dict, k_ms: dict, sm_mhz):
+    """The unit that binds random-row predict on B200: the L1TEX -> crossbar
+    request interface (one L2 request per distinct row sector per warp
+    access; ncu l1tex__m_l1tex2xbar_req_cycles_active, peak 1 cycle per clock
+    per SM).  Busy cycles per query from the committed ncu measurement
+    (profiles/ncu_summary.json "predict"), time and clock from this run."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists() or not sm_mhz:
+        return None
+    try:
+        per = json.loads(p.read_text())["predict"]["xbar_req_cycles_per_unit"]
+    except (ValueError, KeyError):
+        return None
+    cyc = sum(float(per[str(k)]) * nq[k] for k in (AFFINE, ATTN))
+    t = (k_ms[AFFINE] + k_ms[ATTN]) / 1e3
+    peak = 148 * sm_mhz * 1e6
+    return {"bound": "L1TEX->XBAR request interface (L2 requests of the row gathers)",
+            "achieved": cyc / t / 1e9, "peak": peak / 1e9, "unit": "G busy-cycles/s",
+            "frac": cyc / t / peak,
+            "busy_cycles_per_query": {str(k): float(per[str(k)]) for k in (AFFINE, ATTN)},
+            "source": "profiles/ncu_summary.json predict.xbar_req_cycles_per_unit (ncu), "
+                      "peak 1/clk/SM x 148 SMs x this run's median SM clock"}
+
+
 class ClockSampler:
     """SM clocks + throttle reasons sampled every ~5 ms through NVML in a
     background thread, restricted to the timed region (mark_start/mark_end)."""
@@ -1119,7 +1143,8 @@ def run_ours(args):
                          "kernel_ms": {"affine": k_ms[AFFINE], "attention": k_ms[ATTN]},
                          "alg_bytes_per_query": BYTES_PER_QUERY,
                          "gather_ceiling": gather_ceiling(nq, k_ms),
-                         "l1tex": l1tex_roofline(nq, k_ms, clocks.get("sm_mhz"))},
+                         "l1tex": l1tex_roofline(nq, k_ms, clocks.get("sm_mhz")),
+                         "xbar": xbar_roofline(nq, k_ms, clocks.get("sm_mhz"))},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "fits": fits, "fits_csr": fits_csr, "dedup": dedup, "sim": sim, "unknown_signature_errors": bad,
         }
