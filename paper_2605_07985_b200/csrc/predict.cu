@@ -544,21 +544,144 @@ __global__ void __launch_bounds__(kStWarps * 32, 5) predict_attn_staged_kernel(
     atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)bad_min);
 }
 
-// DOOLY_PREDICT_ATTN selects the packed-attention kernel: default one lane per
-// row (predict_vec_kernel, 81 G q/s at C5); "staged" the cp.async-filled
-// shared-memory variant (73 G q/s); "coop" / "coop8" / "coop1" the
-// cooperative 3-lanes-per-row kernel (4 or 8 rows in flight per group, 2 or 1
-// CTAs/SM).  The cooperative form halves the gather wavefronts but issues ~10
-// warp-instructions per query against ~2 (every per-query step is replicated
-// over the group's three lanes) and measured 59 G q/s — profiles/r2_predict.md.
+// ---- paired packed-attention path (DOOLY_KIND_ATTN_PACKED).
+//
+// The one-lane kernel is bound by the L1 -> L2 request interface: each lane's
+// LDG.256 of a row sector is its own request, 3.26 per query.  Here two
+// lanes serve two queries j, j+1 with three loads, arranged so that two of
+// them fetch ADJACENT sectors of one row in the same instruction (which
+// coalesce into one request unless the pair straddles a line):
+//     load 1: A <- row j sector 0,   B <- row j   sector 1
+//     load 2: A <- row j sector 2,   B <- row j+1 sector 0
+//     load 3: A <- row j+1 sector 1, B <- row j+1 sector 2
+// (~2.25 requests per query).  Each lane forms the per-feature partial sums
+// s_k (A.19) of the three sectors it holds, one shuffle exchange hands each
+// finishing lane the s_1 it lacks (A finishes j, B finishes j+1), and the
+// lane holding a query's lo_bits reports its x < lo test and lo_0 to the
+// finishing lane.  Every instruction is uniform across the two roles.
+// Pairs own 8 consecutive queries (sig / feature streams as LDG.256, results
+// regrouped so each lane stores 4 consecutive latencies as one STG.256);
+// tiles are 16 pairs x 8 = 128 queries per warp.
+__device__ __forceinline__ double u2d(uint32_t v) { return (double)v; }
+
+__global__ void __launch_bounds__(256, 2) predict_attn_pair_kernel(
+    const void* __restrict__ table, int64_t n_sig, const uint32_t* __restrict__ sig,
+    const uint32_t* __restrict__ x, int64_t n_q, double* __restrict__ out,
+    uint32_t* __restrict__ flags, int64_t* __restrict__ err_first) {
+  PackInfo pk = read_pack_header(table, n_sig);
+  if (!pk.ok) n_sig = 0;
+  const int lane = threadIdx.x & 31, pr = lane >> 1;
+  const bool B = (lane & 1) != 0;
+  const double* rows = reinterpret_cast<const double*>(static_cast<const dooly_attn_row96*>(table) + 1);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_tiles = (n_q + 127) >> 7;
+  const int64_t n_words = (n_q + 31) >> 5;
+  int64_t bad_min = INT64_MAX;
+  for (int64_t tile = warp; tile < n_tiles; tile += n_warps) {
+    const int64_t qp = (tile << 7) + 8 * pr;
+    const bool live = qp < n_q;  // n_q % 8 == 0: a pair's 8 queries are all in or all out
+    const int64_t qs = live ? qp : 0;
+    const U8 sv = ld_stream_256(sig + qs);
+    const U8 x0 = ld_stream_256(x + qs), x1 = ld_stream_256(x + n_q + qs),
+             x2 = ld_stream_256(x + 2 * n_q + qs);
+    double res[4];
+    uint32_t ebits = 0, cbits = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const uint32_t sa = sv.v[j], sb = sv.v[j + 1];
+      const double* ra = sa < (uint64_t)n_sig ? rows + 12 * (int64_t)sa : rows - 12;
+      const double* rb = sb < (uint64_t)n_sig ? rows + 12 * (int64_t)sb : rows - 12;
+      double w1[4], w2[4], w3[4];
+      ld_row_256(B ? ra + 4 : ra, w1[0], w1[1], w1[2], w1[3]);
+      ld_row_256(B ? rb : ra + 8, w2[0], w2[1], w2[2], w2[3]);
+      ld_row_256(B ? rb + 8 : rb + 4, w3[0], w3[1], w3[2], w3[3]);
+      // features of the two queries
+      const uint32_t a0 = x0.v[j], a1 = x1.v[j], a2 = x2.v[j];
+      const uint32_t b0 = x0.v[j + 1], b1 = x1.v[j + 1], b2 = x2.v[j + 1];
+      // slot 1: A (j, s0: x0, x1) | B (j, s1: x1, x2)
+      // slot 2: A (j, s2: x2, x0) | B (j+1, s0: x0, x1)
+      // slot 3: A (j+1, s1: x1, x2) | B (j+1, s2: x2, x0)
+      const double u1 = u2d(B ? a1 : a0), v1 = u2d(B ? a2 : a1);
+      const double u2 = u2d(B ? b0 : a2), v2 = u2d(B ? b1 : a0);
+      const double u3 = u2d(B ? b2 : b1), v3 = u2d(B ? b0 : b2);
+      const double S1 = sector_sum(B ? 0.0 : w1[0], w1[1], w1[2], w1[3], u1, v1);
+      const double S2 = sector_sum(B ? w2[0] : 0.0, w2[1], w2[2], w2[3], u2, v2);
+      const double S3 = sector_sum(0.0, w3[1], w3[2], w3[3], u3, v3);
+      // A needs s1(j) = B's S1; B needs s1(j+1) = A's S3
+      const double got = __shfl_xor_sync(0xFFFFFFFFu, B ? S1 : S3, 1);
+      const double sum = B ? add(add(S2, got), S3) : add(add(S1, got), S2);
+      // box: the finishing lane holds hi_bits (A: slot 2 = sector 2 of j; B:
+      // slot 3 = sector 2 of j+1); the partner holds lo_bits (B: slot 1 =
+      // sector 1 of j; A: slot 3 = sector 1 of j+1) and tests x < lo for it
+      const uint64_t hib = (uint64_t)__double_as_longlong(B ? w3[0] : w2[0]);
+      const uint64_t lob = (uint64_t)__double_as_longlong(B ? w1[0] : w3[0]);
+      const uint32_t p0 = B ? a0 : b0, p1 = B ? a1 : b1, p2 = B ? a2 : b2;   // partner's query
+      const uint32_t l0 = (uint32_t)(lob & pk.m0), l1 = (uint32_t)((lob >> pk.s1) & pk.m1),
+                     l2 = (uint32_t)((lob >> pk.s2) & pk.m2);
+      const bool below_p = (p0 < l0) | (p1 < l1) | (p2 < l2);
+      const uint32_t lo0 = __shfl_xor_sync(0xFFFFFFFFu, l0, 1);
+      const uint32_t bel = __ballot_sync(0xFFFFFFFFu, below_p);
+      const bool below = (bel >> (lane ^ 1)) & 1u;
+      const uint32_t h0 = (uint32_t)(hib & pk.m0), h1 = (uint32_t)((hib >> pk.s1) & pk.m1),
+                     h2 = (uint32_t)((hib >> pk.s2) & pk.m2);
+      const uint32_t m0 = B ? b0 : a0, m1 = B ? b1 : a1, m2 = B ? b2 : a2;  // my query
+      const bool above = (m0 > h0) | (m1 > h1) | (m2 > h2);
+      const uint32_t my_sig = B ? sb : sa;
+      const bool valid = live && my_sig < (uint64_t)n_sig && lo0 <= h0;
+      bool cl = false;
+      const double pv = clamp_floor(sum, cl);
+      const int jm = j + (B ? 1 : 0);                 // my query's index in the pair's 8
+      res[j >> 1] = valid ? pv : nan64();
+      ebits |= (uint32_t)(valid && (below || above)) << jm;
+      cbits |= (uint32_t)(valid && cl) << jm;
+      if (live && !valid && qp + jm < bad_min) bad_min = qp + jm;
+    }
+    // regroup: A holds j = 0,2,4,6 and B 1,3,5,7 -> A 0..3, B 4..7
+    const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[2], 1);  // A<-p1, B<-p4
+    const double g2 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[1] : res[3], 1);  // A<-p3, B<-p6
+    if (live) {
+      if (B)
+        st_stream_256(out + qp + 4, g1, res[2], g2, res[3]);
+      else
+        st_stream_256(out + qp, res[0], g1, res[1], g2);
+    }
+    if (flags != nullptr) {
+      uint32_t e8 = ebits | __shfl_xor_sync(0xFFFFFFFFu, ebits, 1);
+      uint32_t c8 = cbits | __shfl_xor_sync(0xFFFFFFFFu, cbits, 1);
+      const int sh = 8 * (pr & 3);
+      e8 <<= sh;
+      c8 <<= sh;
+      e8 |= __shfl_xor_sync(0xFFFFFFFFu, e8, 2);
+      c8 |= __shfl_xor_sync(0xFFFFFFFFu, c8, 2);
+      e8 |= __shfl_xor_sync(0xFFFFFFFFu, e8, 4);
+      c8 |= __shfl_xor_sync(0xFFFFFFFFu, c8, 4);
+      const int64_t word = (tile << 2) + (pr >> 2);
+      if ((lane & 7) == 0 && word < n_words) {
+        flags[word] = e8;
+        flags[n_words + word] = c8;
+      }
+    }
+  }
+  if (err_first != nullptr && bad_min != INT64_MAX)
+    atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)bad_min);
+}
+
+// DOOLY_PREDICT_ATTN selects the packed-attention kernel: default the paired
+// kernel (two lanes, two queries, three loads of which two coalesce: 2.5 L2
+// requests per query, 93 G q/s at C5); "vec" one lane per row (3.26 requests,
+// 81 G q/s); "staged" the cp.async-filled shared-memory variant (73 G q/s);
+// "coop" / "coop8" / "coop1" the 3-lanes-per-row kernel (59 G q/s).  The
+// request counts and why the others lose: profiles/r2_predict.md.
 static int predict_attn_mode() {
   const char* v = getenv("DOOLY_PREDICT_ATTN");
-  return v == nullptr              ? 1
+  return v == nullptr              ? 5
          : strcmp(v, "coop") == 0  ? 0
          : strcmp(v, "coop8") == 0 ? 2
          : strcmp(v, "coop1") == 0 ? 3
          : strcmp(v, "staged") == 0 ? 4
-                                   : 1;
+         : strcmp(v, "vec") == 0 ? 1
+                                   : 5;
 }
 
 template <int KIND>
@@ -580,6 +703,14 @@ cudaError_t launch_predict_kind(const void* table, int64_t n_sig, const uint32_t
     if (blocks > need) blocks = need;
     predict_attn_staged_kernel<<<(unsigned)blocks, kStWarps * 32, 0, stream>>>(
         table, n_sig, sig, x, n_q, out, flags, err_first);
+  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && mode == 5) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_attn_pair_kernel, 256, 0);
+    const int64_t tiles = (n_q + 127) / 128;
+    int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+    const int64_t need = (tiles + 7) / 8;
+    if (blocks > need) blocks = need;
+    predict_attn_pair_kernel<<<(unsigned)blocks, 256, 0, stream>>>(table, n_sig, sig, x, n_q, out,
+                                                                   flags, err_first);
   } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && mode != 1 && mode != 4) {
     auto kern = mode == 2 ? predict_attn_coop_kernel<2, 8>
               : mode == 3 ? predict_attn_coop_kernel<1, 8>

@@ -154,11 +154,12 @@ def test_predict_bit_exact(kind, n_q, offset, dev):
     assert np.array_equal(_unpack_bits(flags[1, :nw], n_q), ref["clamped"])
 
 
-@pytest.mark.parametrize("mode", ["coop", "coop8", "coop1", "staged"])
+@pytest.mark.parametrize("mode", ["coop", "coop8", "coop1", "staged", "pair", "vec"])
 @pytest.mark.parametrize("n_q", [8, 160 * 7, 160 * 1000 + 88])
 def test_predict_packed_cooperative_kernel(mode, n_q, dev, monkeypatch):
-    """The opt-in cooperative packed-attention kernel (3 lanes per row) is
-    bit-identical to the oracle, flags and unknown/unfitted rows included."""
+    """Every packed-attention kernel (paired default, one lane per row, the
+    cp.async-staged and the 3-lanes-per-row variants) is bit-identical to the
+    oracle, flags and unknown/unfitted rows included."""
     monkeypatch.setenv("DOOLY_PREDICT_ATTN", mode)
     x, y, off = synth_fit_data(ATTN, 257, 64, seed=21)
     ref_fit = osim.fit(ATTN, x, y, np.array([0, 3, *off[2:]], dtype=np.int64))  # row 0 unfitted
