@@ -564,10 +564,30 @@ __global__ void __launch_bounds__(kStWarps * 32, 5) predict_attn_staged_kernel(
 // tiles are 16 pairs x 8 = 128 queries per warp.
 __device__ __forceinline__ double u2d(uint32_t v) { return (double)v; }
 
-__global__ void __launch_bounds__(256, 2) predict_attn_pair_kernel(
+struct U4q {
+  uint32_t v[4];
+};
+__device__ __forceinline__ U4q ld_stream_128(const uint32_t* p) {
+  U4q r;
+  asm("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3])
+      : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream_128(double* p, double a, double b) {
+  asm volatile("st.global.L1::no_allocate.v2.f64 [%0], {%1,%2};" ::"l"(p),
+               "d"(a), "d"(b)
+               : "memory");
+}
+
+// QPP = queries per pair (8: 128-query tiles, LDG.256 streams; 4: 64-query
+// tiles, LDG.128 streams, fewer live registers -> more resident warps)
+template <int QPP, int MINB>
+__global__ void __launch_bounds__(256, MINB) predict_attn_pair_kernel(
     const void* __restrict__ table, int64_t n_sig, const uint32_t* __restrict__ sig,
     const uint32_t* __restrict__ x, int64_t n_q, double* __restrict__ out,
     uint32_t* __restrict__ flags, int64_t* __restrict__ err_first) {
+  constexpr int TQ = 16 * QPP;  // queries per warp tile
   PackInfo pk = read_pack_header(table, n_sig);
   if (!pk.ok) n_sig = 0;
   const int lane = threadIdx.x & 31, pr = lane >> 1;
@@ -575,30 +595,38 @@ __global__ void __launch_bounds__(256, 2) predict_attn_pair_kernel(
   const double* rows = reinterpret_cast<const double*>(static_cast<const dooly_attn_row96*>(table) + 1);
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n_tiles = (n_q + 127) >> 7;
+  const int64_t n_tiles = (n_q + TQ - 1) / TQ;
   const int64_t n_words = (n_q + 31) >> 5;
   int64_t bad_min = INT64_MAX;
   for (int64_t tile = warp; tile < n_tiles; tile += n_warps) {
-    const int64_t qp = (tile << 7) + 8 * pr;
-    const bool live = qp < n_q;  // n_q % 8 == 0: a pair's 8 queries are all in or all out
+    const int64_t qp = tile * TQ + QPP * pr;
+    const bool live = qp < n_q;  // n_q % 8 == 0: a pair's queries are all in or all out
     const int64_t qs = live ? qp : 0;
-    const U8 sv = ld_stream_256(sig + qs);
-    const U8 x0 = ld_stream_256(x + qs), x1 = ld_stream_256(x + n_q + qs),
-             x2 = ld_stream_256(x + 2 * n_q + qs);
-    double res[4];
+    uint32_t sv[QPP], x0[QPP], x1[QPP], x2[QPP];
+    if constexpr (QPP == 8) {
+      const U8 a = ld_stream_256(sig + qs), b = ld_stream_256(x + qs),
+               c = ld_stream_256(x + n_q + qs), d = ld_stream_256(x + 2 * n_q + qs);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sv[j] = a.v[j], x0[j] = b.v[j], x1[j] = c.v[j], x2[j] = d.v[j];
+    } else {
+      const U4q a = ld_stream_128(sig + qs), b = ld_stream_128(x + qs),
+                c = ld_stream_128(x + n_q + qs), d = ld_stream_128(x + 2 * n_q + qs);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sv[j] = a.v[j], x0[j] = b.v[j], x1[j] = c.v[j], x2[j] = d.v[j];
+    }
+    double res[QPP / 2];
     uint32_t ebits = 0, cbits = 0;
 #pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      const uint32_t sa = sv.v[j], sb = sv.v[j + 1];
+    for (int j = 0; j < QPP; j += 2) {
+      const uint32_t sa = sv[j], sb = sv[j + 1];
       const double* ra = sa < (uint64_t)n_sig ? rows + 12 * (int64_t)sa : rows - 12;
       const double* rb = sb < (uint64_t)n_sig ? rows + 12 * (int64_t)sb : rows - 12;
       double w1[4], w2[4], w3[4];
       ld_row_256(B ? ra + 4 : ra, w1[0], w1[1], w1[2], w1[3]);
       ld_row_256(B ? rb : ra + 8, w2[0], w2[1], w2[2], w2[3]);
       ld_row_256(B ? rb + 8 : rb + 4, w3[0], w3[1], w3[2], w3[3]);
-      // features of the two queries
-      const uint32_t a0 = x0.v[j], a1 = x1.v[j], a2 = x2.v[j];
-      const uint32_t b0 = x0.v[j + 1], b1 = x1.v[j + 1], b2 = x2.v[j + 1];
+      const uint32_t a0 = x0[j], a1 = x1[j], a2 = x2[j];
+      const uint32_t b0 = x0[j + 1], b1 = x1[j + 1], b2 = x2[j + 1];
       // slot 1: A (j, s0: x0, x1) | B (j, s1: x1, x2)
       // slot 2: A (j, s2: x2, x0) | B (j+1, s0: x0, x1)
       // slot 3: A (j+1, s1: x1, x2) | B (j+1, s2: x2, x0)
@@ -631,33 +659,46 @@ __global__ void __launch_bounds__(256, 2) predict_attn_pair_kernel(
       const bool valid = live && my_sig < (uint64_t)n_sig && lo0 <= h0;
       bool cl = false;
       const double pv = clamp_floor(sum, cl);
-      const int jm = j + (B ? 1 : 0);                 // my query's index in the pair's 8
+      const int jm = j + (B ? 1 : 0);                 // my query's index in the pair's QPP
       res[j >> 1] = valid ? pv : nan64();
       ebits |= (uint32_t)(valid && (below || above)) << jm;
       cbits |= (uint32_t)(valid && cl) << jm;
       if (live && !valid && qp + jm < bad_min) bad_min = qp + jm;
     }
-    // regroup: A holds j = 0,2,4,6 and B 1,3,5,7 -> A 0..3, B 4..7
-    const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[2], 1);  // A<-p1, B<-p4
-    const double g2 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[1] : res[3], 1);  // A<-p3, B<-p6
-    if (live) {
-      if (B)
-        st_stream_256(out + qp + 4, g1, res[2], g2, res[3]);
-      else
-        st_stream_256(out + qp, res[0], g1, res[1], g2);
+    // regroup: A holds the even queries, B the odd ones -> A the first half, B the second
+    if constexpr (QPP == 8) {
+      const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[2], 1);  // A<-p1, B<-p4
+      const double g2 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[1] : res[3], 1);  // A<-p3, B<-p6
+      if (live) {
+        if (B)
+          st_stream_256(out + qp + 4, g1, res[2], g2, res[3]);
+        else
+          st_stream_256(out + qp, res[0], g1, res[1], g2);
+      }
+    } else {
+      const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[1], 1);  // A<-p1, B<-p2
+      if (live) {
+        if (B)
+          st_stream_128(out + qp + 2, g1, res[1]);
+        else
+          st_stream_128(out + qp, res[0], g1);
+      }
     }
     if (flags != nullptr) {
+      // a pair's QPP bits; 32 / QPP pairs per flag word
       uint32_t e8 = ebits | __shfl_xor_sync(0xFFFFFFFFu, ebits, 1);
       uint32_t c8 = cbits | __shfl_xor_sync(0xFFFFFFFFu, cbits, 1);
-      const int sh = 8 * (pr & 3);
+      constexpr int PPW = 32 / QPP;                   // pairs per word
+      const int sh = QPP * (pr % PPW);
       e8 <<= sh;
       c8 <<= sh;
-      e8 |= __shfl_xor_sync(0xFFFFFFFFu, e8, 2);
-      c8 |= __shfl_xor_sync(0xFFFFFFFFu, c8, 2);
-      e8 |= __shfl_xor_sync(0xFFFFFFFFu, e8, 4);
-      c8 |= __shfl_xor_sync(0xFFFFFFFFu, c8, 4);
-      const int64_t word = (tile << 2) + (pr >> 2);
-      if ((lane & 7) == 0 && word < n_words) {
+#pragma unroll
+      for (int o = 2; o < 2 * PPW; o <<= 1) {
+        e8 |= __shfl_xor_sync(0xFFFFFFFFu, e8, o);
+        c8 |= __shfl_xor_sync(0xFFFFFFFFu, c8, o);
+      }
+      const int64_t word = tile * (TQ / 32) + pr / PPW;
+      if ((lane & (2 * PPW - 1)) == 0 && word < n_words) {
         flags[word] = e8;
         flags[n_words + word] = c8;
       }
@@ -681,6 +722,8 @@ static int predict_attn_mode() {
          : strcmp(v, "coop1") == 0 ? 3
          : strcmp(v, "staged") == 0 ? 4
          : strcmp(v, "vec") == 0 ? 1
+         : strcmp(v, "pair4") == 0 ? 6
+         : strcmp(v, "pair4b") == 0 ? 7
                                    : 5;
 }
 
@@ -703,14 +746,16 @@ cudaError_t launch_predict_kind(const void* table, int64_t n_sig, const uint32_t
     if (blocks > need) blocks = need;
     predict_attn_staged_kernel<<<(unsigned)blocks, kStWarps * 32, 0, stream>>>(
         table, n_sig, sig, x, n_q, out, flags, err_first);
-  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && mode == 5) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, predict_attn_pair_kernel, 256, 0);
-    const int64_t tiles = (n_q + 127) / 128;
+  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && (mode == 5 || mode == 6 || mode == 7)) {
+    auto kern = mode == 6 ? predict_attn_pair_kernel<4, 3>
+              : mode == 7 ? predict_attn_pair_kernel<4, 2> : predict_attn_pair_kernel<8, 2>;
+    const int tq = mode == 5 ? 128 : 64;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
+    const int64_t tiles = (n_q + tq - 1) / tq;
     int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
     const int64_t need = (tiles + 7) / 8;
     if (blocks > need) blocks = need;
-    predict_attn_pair_kernel<<<(unsigned)blocks, 256, 0, stream>>>(table, n_sig, sig, x, n_q, out,
-                                                                   flags, err_first);
+    kern<<<(unsigned)blocks, 256, 0, stream>>>(table, n_sig, sig, x, n_q, out, flags, err_first);
   } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && mode != 1 && mode != 4) {
     auto kern = mode == 2 ? predict_attn_coop_kernel<2, 8>
               : mode == 3 ? predict_attn_coop_kernel<1, 8>
