@@ -67,7 +67,7 @@ struct GridFactor {
   // dooly_attn_pack derives it (widths from the largest fitted hi)
   uint32_t pk_s1, pk_s2;  // bit offsets of the second and third box fields
   int32_t pk_ok;          // the three widths fit in 64 bits
-  int32_t pk_pad_;
+  int32_t f3p128;         // attention: x2 periodic with a period dividing 128 points
 };
 
 // Epilogue destinations: the peer tables of the fused all-gather and,
@@ -270,8 +270,19 @@ __global__ void __launch_bounds__(kGT) fit_grid_prep_kernel(const uint32_t* __re
     }
   }
   grp4 = __syncthreads_and(grp4);
+  // ... and when the kv axis repeats with a period dividing 128 points (the C5
+  // 16-value kv axis does), a warp-kernel lane sees the same four f3 values at
+  // every step (its points are 4 lane + 128 t): it keeps them in registers
+  int f3p = 0;
+  if constexpr (KIND == DOOLY_KIND_ATTN) {
+    f3p = n_pts % 128 == 0 ? 1 : 0;
+    const uint32_t* x2 = x + 2 * n_pts;
+    for (int64_t q = 128 + tid; f3p && q < n_pts; q += kGT) f3p = x2[q] == x2[q & 127] ? 1 : 0;
+  }
+  f3p = __syncthreads_and(f3p);
   if (tid == 0) {
     gf->grp4 = grp4;
+    gf->f3p128 = f3p;
     double diag[NC];
     for (int j = 0; j < NC; ++j) diag[j] = G[j][j];
     for (int j = 0; j < NC; ++j) {
@@ -837,6 +848,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
   }
   const bool ok = gf->ok != 0;
   const bool factored = KIND == DOOLY_KIND_ATTN && allow_factor && gf->grp4 != 0;
+  const bool f3reg = factored && gf->f3p128 != 0;
   __syncthreads();
   double inv[P], nb[P];
 #pragma unroll
@@ -844,6 +856,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int n = (int)n_pts;  // n_pts % 4 == 0, n_pts < 2^31 (launcher)
+  const double4 f3l = f3reg ? g_ld_f(fpl + 2 * n + 4 * lane) : make_double4(0.0, 0.0, 0.0, 0.0);
   for (int64_t s = warp; s < n_sig; s += n_warps) {
     if (!ok) {
       if (lane == 0) write_unfitted_grid<KIND>(pe, gf, table, s, fit_err, status);
@@ -942,7 +955,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
       // the f1/f2 terms per group: 8.75 FP64 per point instead of 14.
       auto fstep = [&](const double4& yv, int pp) {
         const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
-        grid_g1_step(yv, g_ld_f(fpl + 2 * n + pp), u.x, u.y, acc);
+        grid_g1_step(yv, f3reg ? f3l : g_ld_f(fpl + 2 * n + pp), u.x, u.y, acc);
       };
       int p = 4 * lane;
       constexpr int YS = 8;
@@ -972,7 +985,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
       // per group: p = A + f3 (B + c6 f3) with A, B the group's f1/f2 terms
       auto fstep2 = [&](const double4& yv, int pp) {
         const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
-        grid_g2_step(yv, g_ld_f(fpl + 2 * n + pp), u.x, u.y, c, err);
+        grid_g2_step(yv, f3reg ? f3l : g_ld_f(fpl + 2 * n + pp), u.x, u.y, c, err);
       };
       int p = 4 * lane;
       constexpr int YS = 8;
