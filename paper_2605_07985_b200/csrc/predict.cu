@@ -724,6 +724,7 @@ static int predict_attn_mode() {
          : strcmp(v, "vec") == 0 ? 1
          : strcmp(v, "pair4") == 0 ? 6
          : strcmp(v, "pair4b") == 0 ? 7
+         : strcmp(v, "pair3") == 0 ? 8
                                    : 5;
 }
 
@@ -746,10 +747,11 @@ cudaError_t launch_predict_kind(const void* table, int64_t n_sig, const uint32_t
     if (blocks > need) blocks = need;
     predict_attn_staged_kernel<<<(unsigned)blocks, kStWarps * 32, 0, stream>>>(
         table, n_sig, sig, x, n_q, out, flags, err_first);
-  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && (mode == 5 || mode == 6 || mode == 7)) {
+  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && (mode >= 5 && mode <= 8)) {
     auto kern = mode == 6 ? predict_attn_pair_kernel<4, 3>
-              : mode == 7 ? predict_attn_pair_kernel<4, 2> : predict_attn_pair_kernel<8, 2>;
-    const int tq = mode == 5 ? 128 : 64;
+              : mode == 7 ? predict_attn_pair_kernel<4, 2>
+              : mode == 8 ? predict_attn_pair_kernel<8, 3> : predict_attn_pair_kernel<8, 2>;
+    const int tq = (mode == 5 || mode == 8) ? 128 : 64;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
     const int64_t tiles = (n_q + tq - 1) / tq;
     int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);

@@ -154,7 +154,8 @@ def test_predict_bit_exact(kind, n_q, offset, dev):
     assert np.array_equal(_unpack_bits(flags[1, :nw], n_q), ref["clamped"])
 
 
-@pytest.mark.parametrize("mode", ["coop", "coop8", "coop1", "staged", "pair", "pair4", "pair4b", "vec"])
+@pytest.mark.parametrize("mode", ["coop", "coop8", "coop1", "staged", "pair", "pair4", "pair4b", "pair3",
+                                  "vec"])
 @pytest.mark.parametrize("n_q", [8, 160 * 7, 160 * 1000 + 88])
 def test_predict_packed_cooperative_kernel(mode, n_q, dev, monkeypatch):
     """Every packed-attention kernel (paired default, one lane per row, the
