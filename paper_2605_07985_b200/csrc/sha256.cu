@@ -106,6 +106,9 @@ __device__ __noinline__ void sha256_compress_blocks(uint32_t hs[8], const uint32
 }
 
 constexpr int SHA_THREADS = 128;
+#ifndef SHA_MINB
+#define SHA_MINB 6  // 6 CTAs/SM (67 registers): 0.924 vs 0.93-0.99 ms for 4M records; 7-8 slower
+#endif
 constexpr int SHA_BUF_BLOCKS = 3;  // 192 B: C1-C5 canonical messages fit (longer ones drain)
 constexpr int SHA_STRIDE = SHA_BUF_BLOCKS * 16 + 1;   // odd word stride: conflict-free reads
 
@@ -202,7 +205,7 @@ struct ShaStream {
   }
 };
 
-__global__ void __launch_bounds__(SHA_THREADS) sha256_records_kernel(
+__global__ void __launch_bounds__(SHA_THREADS, SHA_MINB) sha256_records_kernel(
     const uint32_t* __restrict__ words, const int64_t* __restrict__ rec_off, int64_t n,
     const uint8_t* __restrict__ op_bytes, const int64_t* __restrict__ op_off,
     const uint8_t* __restrict__ sym_bytes, const int64_t* __restrict__ sym_off,
