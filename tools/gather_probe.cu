@@ -513,3 +513,134 @@ extern "C" int probe_l2_stream(const void* buf, int64_t bytes, int reps, void* s
       static_cast<const double4*>(buf), bytes / 32, reps, static_cast<unsigned long long*>(sink));
   return (int)cudaGetLastError();
 }
+
+// Hybrid: do TMA tile::gather4 and LDG.256 row gathers use different request
+// paths into L2?  TW warps per CTA gather rows [0, n_tma) with gather4 (as
+// tma_gather4_kernel), LW warps gather rows [n_tma, n_q) with 3 x LDG.256 (as
+// gather_kernel<3>); total rows/s vs either path alone.
+template <int TW, int LW, int D>
+__global__ void __launch_bounds__(32 * (TW + LW)) hybrid_gather_kernel(
+    const __grid_constant__ CUtensorMap tmap, const uint8_t* __restrict__ table, uint32_t n_rows,
+    int64_t n_tma, int64_t n_q, unsigned long long* sink) {
+  constexpr int ROW = 96;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc = 0.0;
+  if (warp >= TW) {
+    const int64_t tid = (blockIdx.x * (int64_t)LW + (warp - TW)) * 32 + lane;
+    const int64_t stride = (int64_t)gridDim.x * LW * 32;
+    for (int64_t q = n_tma + tid; q < n_q; q += stride * 8) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t qq = q + j * stride;
+        const uint32_t r = mix((uint64_t)qq) % n_rows;
+        const uint8_t* p = table + (uint64_t)r * ROW;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          double a, b, c, d;
+          ld256(p + 32 * k, a, b, c, d);
+          s += a + b + c + d;
+        }
+        v[j] = qq < n_q ? s : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc += v[j];
+    }
+    if (acc == 1.2345) atomicAdd(sink, 1ull);
+    return;
+  }
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem) + warp * D;
+  uint8_t* slots = smem + 128 * ((8 * D * TW + 127) / 128) + (size_t)warp * D * 32 * ROW;
+  if (lane == 0)
+    for (int b = 0; b < D; ++b)
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bars + b)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const int64_t gwarp = blockIdx.x * (int64_t)TW + warp;
+  const int64_t n_gwarps = (int64_t)gridDim.x * TW;
+  const int64_t n_rounds = n_tma / 32;
+  auto issue = [&](int64_t round, int b) {
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(bars + b);
+    const int64_t q = round * 32 + lane;
+    const int32_t r = (int32_t)(mix((uint64_t)q) % n_rows);
+    const int32_t r0 = __shfl_sync(0xFFFFFFFFu, r, (lane * 4) & 31);
+    const int32_t r1 = __shfl_sync(0xFFFFFFFFu, r, (lane * 4 + 1) & 31);
+    const int32_t r2 = __shfl_sync(0xFFFFFFFFu, r, (lane * 4 + 2) & 31);
+    const int32_t r3 = __shfl_sync(0xFFFFFFFFu, r, (lane * 4 + 3) & 31);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar), "r"(32 * ROW) : "memory");
+    __syncwarp();
+    if (lane < 8) {
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(slots + (size_t)b * 32 * ROW + lane * 4 * ROW);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+          : "memory");
+    }
+  };
+  int64_t round = gwarp;
+  for (int b = 0; b < D && round + (int64_t)b * n_gwarps < n_rounds; ++b) issue(round + (int64_t)b * n_gwarps, b);
+  uint32_t phase = 0;
+  for (int b = 0; round < n_rounds; round += n_gwarps) {
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(bars + b);
+    uint32_t done = 0;
+    for (int spin = 0; !done; ++spin) {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(bar), "r"((phase >> b) & 1u) : "memory");
+      if (spin > 2000000) {
+        atomicAdd(sink + 1, 1ull);
+        return;
+      }
+    }
+    phase ^= 1u << b;
+    const double2* row = reinterpret_cast<const double2*>(slots + (size_t)b * 32 * ROW + lane * ROW);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < ROW / 16; ++k) {
+      const double2 v = row[k];
+      s += v.x + v.y;
+    }
+    acc += s;
+    __syncwarp();
+    const int64_t nxt = round + (int64_t)D * n_gwarps;
+    if (nxt < n_rounds) issue(nxt, b);
+    b = (b + 1) % D;
+  }
+  if (acc == 1.2345) atomicAdd(sink, 1ull);
+}
+
+extern "C" int probe_hybrid_gather(const void* table, uint32_t n_rows, int cfg, int64_t n_tma,
+                                   int64_t n_q, void* sink, int blocks, void* stream) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+    return 100;
+  CUtensorMap tmap;
+  cuuint64_t dims[2] = {24, n_rows};
+  cuuint64_t strides[1] = {96};
+  cuuint32_t box[2] = {24, 1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = ((EncodeTiled)fn)(&tmap, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(table), dims,
+                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return 200 + (int)cr;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto t = static_cast<const uint8_t*>(table);
+  auto k = static_cast<unsigned long long*>(sink);
+#define PROBE_HY(C, TW, LW, DD)                                                              \
+  if (cfg == C) {                                                                            \
+    const size_t smem = 128 * ((8 * DD * TW + 127) / 128) + (size_t)TW * DD * 32 * 96;      \
+    cudaFuncSetAttribute(hybrid_gather_kernel<TW, LW, DD>,                                   \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    hybrid_gather_kernel<TW, LW, DD><<<blocks, 32 * (TW + LW), smem, s>>>(tmap, t, n_rows, n_tma, \
+                                                                          n_q, k);           \
+    return (int)cudaGetLastError();                                                          \
+  }
+  PROBE_HY(0, 4, 4, 2) PROBE_HY(1, 4, 8, 2) PROBE_HY(2, 2, 6, 2) PROBE_HY(3, 4, 4, 4)
+#undef PROBE_HY
+  return 1;
+}

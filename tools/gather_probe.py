@@ -97,6 +97,9 @@ def main() -> None:
                                   "g_rows_per_s": n_q / ms / 1e6}), flush=True)
             del table
         return
+    if "hybrid" in only:
+        hybrid(lib, dev, n_sm, sink, st, timed)
+        return
     if "predmem" in only:
         predict_mem(lib, dev, n_sm, timed)
         return
@@ -188,6 +191,33 @@ def gather4(lib, dev, n_sm, sink, st, timed):
                                   "g_rows_per_s": n_q / ms / 1e6, "timeouts": int(sink[1].item()),
                                   "gb_per_s": n_q * rb / ms / 1e6}), flush=True)
         del table
+
+
+def hybrid(lib, dev, n_sm, sink, st, timed):
+    """TMA gather4 warps and LDG.256 warps in the same CTAs on disjoint query
+    ranges: if the two paths used separate request interfaces, the total would
+    exceed either alone (96-B rows, 0.5M-row table)."""
+    lib.probe_hybrid_gather.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_int64, C.c_int64,
+                                        C.c_void_p, C.c_int, C.c_void_p]
+    n_q, rows = 500_000_000, 500_000
+    table = torch.rand((rows * 96) // 8, dtype=torch.float64, device=dev)
+    for cfg, per_sm in ((0, 2), (0, 3), (1, 2), (2, 2), (2, 3), (3, 2)):
+        for frac in (0.0, 0.3, 0.45, 0.6, 1.0):
+            n_tma = int(n_q * frac) // 32 * 32
+            rc = lib.probe_hybrid_gather(table.data_ptr(), rows, cfg, min(n_tma, 1 << 20),
+                                         min(n_q, 1 << 21), sink.data_ptr(), n_sm * per_sm, st)
+            torch.cuda.synchronize()
+            if rc != 0 or int(sink[1].item()):
+                print(json.dumps({"probe": "hybrid", "cfg": cfg, "rc": rc,
+                                  "timeouts": int(sink[1].item())}), flush=True)
+                sink.zero_()
+                continue
+            ms = timed(lambda: lib.probe_hybrid_gather(table.data_ptr(), rows, cfg, n_tma, n_q,
+                                                       sink.data_ptr(), n_sm * per_sm, st))
+            print(json.dumps({"probe": "hybrid", "cfg": cfg, "ctas_per_sm": per_sm,
+                              "tma_frac": frac, "ms": ms, "g_rows_per_s": n_q / ms / 1e6,
+                              "timeouts": int(sink[1].item())}), flush=True)
+    del table
 
 
 if __name__ == "__main__":
