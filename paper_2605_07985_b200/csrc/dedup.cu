@@ -11,6 +11,9 @@
 // the immutable digest arrays, never against slot contents.
 // uids (rank among first occurrences, in index order) come from one
 // exclusive scan of the first-occurrence flags.
+#include <cstdlib>
+#include <cstring>
+
 #include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
@@ -115,6 +118,52 @@ __global__ void __launch_bounds__(DEDUP_THREADS) dedup_insert_kernel(
   }
 }
 
+// Warp-cooperative form (SURVEY §8 north_star): 8-lane groups, one 256-bit key
+// per group, lane k holding word k.  The group's key load is one coalesced
+// 32-B sector (4 keys per warp instruction); the group leader claims the slot
+// with atomicCAS and broadcasts the occupant; on a collision every lane loads
+// word k of the occupant's digest and the group compares all 256 bits with one
+// __all_sync.  Same slot protocol as dedup_insert_kernel, so the resulting
+// table (and every output) is identical.  Selected with DOOLY_DEDUP_INSERT=group.
+__global__ void __launch_bounds__(DEDUP_THREADS) dedup_insert_group_kernel(
+    const uint8_t* __restrict__ keys, int64_t m, uint32_t base, const uint8_t* __restrict__ batch,
+    int64_t n, const uint8_t* __restrict__ db, uint32_t* slots, uint8_t* mark,
+    uint32_t* slot_of, uint64_t mask) {
+  const int lane = threadIdx.x & 31, k = lane & 7, g0 = lane & ~7;
+  const unsigned gmask = 0xFFu << g0;
+  const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  const uint32_t* kw = reinterpret_cast<const uint32_t*>(keys);
+  const uint32_t* bw = reinterpret_cast<const uint32_t*>(batch);
+  const uint32_t* dw = reinterpret_cast<const uint32_t*>(db);
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; i < m; i += stride) {
+    const uint32_t w = __ldg(kw + i * 8 + k);
+    const uint32_t me = base + (uint32_t)i;
+    uint64_t slot = __shfl_sync(gmask, w, g0) & mask;
+    while (true) {
+      uint32_t cur = 0;
+      if (k == 0) cur = atomicCAS(slots + slot, kEmpty, me);
+      cur = __shfl_sync(gmask, cur, g0);
+      if (cur == kEmpty) break;
+      const uint32_t o = cur < (uint32_t)n ? __ldg(bw + (int64_t)cur * 8 + k)
+                                           : __ldg(dw + (int64_t)(cur - (uint32_t)n) * 8 + k);
+      if (__all_sync(gmask, o == w)) {
+        if (k == 0 && me < cur) atomicMin(slots + slot, me);
+        break;
+      }
+      slot = (slot + 1) & mask;
+    }
+    if (k == 0) {
+      if (slot_of != nullptr) slot_of[i] = (uint32_t)slot;
+      else mark[slot] = 1;  // DB pass
+    }
+  }
+}
+
+static bool dedup_group_insert() {
+  const char* v = getenv("DOOLY_DEDUP_INSERT");
+  return v != nullptr && strcmp(v, "group") == 0;
+}
+
 __global__ void __launch_bounds__(DEDUP_THREADS) dedup_resolve_kernel(
     int64_t n, const uint32_t* __restrict__ slots, const uint8_t* __restrict__ mark,
     const uint32_t* __restrict__ slot_of, int64_t* __restrict__ out_first,
@@ -161,13 +210,16 @@ cudaError_t launch_dedup(const uint8_t* digests, int64_t n, const uint8_t* db, i
   if ((e = cudaMemsetAsync(w.slots, 0xFF, w.cap * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(w.mark, 0, w.cap, stream)) != cudaSuccess) return e;
   const uint64_t mask = w.cap - 1;
+  const bool grp = dedup_group_insert();
+  auto insert = grp ? dedup_insert_group_kernel : dedup_insert_kernel;
+  auto grid = [&](int64_t m) { return grid_for(grp ? 8 * m : m, n_sm); };
   if (n_db > 0) {
-    dedup_insert_kernel<<<grid_for(n_db, n_sm), DEDUP_THREADS, 0, stream>>>(
-        db, n_db, (uint32_t)n, digests, n, db, w.slots, w.mark, nullptr, mask);
+    insert<<<grid(n_db), DEDUP_THREADS, 0, stream>>>(db, n_db, (uint32_t)n, digests, n, db,
+                                                     w.slots, w.mark, nullptr, mask);
     *launches += 1;
   }
-  dedup_insert_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
-      digests, n, 0u, digests, n, db, w.slots, w.mark, w.slot_of, mask);
+  insert<<<grid(n), DEDUP_THREADS, 0, stream>>>(digests, n, 0u, digests, n, db, w.slots, w.mark,
+                                                w.slot_of, mask);
   dedup_resolve_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
       n, w.slots, w.mark, w.slot_of, out_first, out_is_new, out_in_db, w.first_flag);
   size_t tmp = w.cub_bytes;

@@ -314,9 +314,14 @@ def _dedup_gpu(digs: np.ndarray, db: np.ndarray, dev):
             "in_db": r.in_db.cpu().numpy().astype(bool).tolist(), "n_unique": r.n_unique}
 
 
+@pytest.mark.parametrize("insert", ["thread", "group"])
 @pytest.mark.parametrize("n,n_distinct,n_db", [(1, 1, 0), (1000, 100, 0), (50000, 20000, 5000),
                                                (200000, 150000, 0)])
-def test_dedup_bit_exact(n, n_distinct, n_db, dev):
+def test_dedup_bit_exact(n, n_distinct, n_db, insert, dev, monkeypatch):
+    """Both insert kernels (one thread per key; 8-lane groups per 256-bit key,
+    DOOLY_DEDUP_INSERT=group) against the oracle."""
+    if insert == "group":
+        monkeypatch.setenv("DOOLY_DEDUP_INSERT", "group")
     rng = np.random.default_rng(n)
     pool = rng.integers(0, 256, size=(n_distinct, 32), dtype=np.uint8)
     # collisions on the probe word (first 4 bytes) but different digests

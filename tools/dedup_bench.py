@@ -45,6 +45,18 @@ def main() -> None:
 
     sha_ms = timed(lambda: hash_records(recs))
     dd_ms = timed(lambda: dedup_packed(recs, workspace=ws))
+    from paper_2605_07985_b200.profiler import dedup_digests
+    dig = res.digests
+    ins = {}
+    for mode in ("thread", "group"):
+        if mode == "group":
+            os.environ["DOOLY_DEDUP_INSERT"] = "group"
+        else:
+            os.environ.pop("DOOLY_DEDUP_INSERT", None)
+        r = dedup_digests(dig, workspace=ws)
+        ins[mode] = {"ms": timed(lambda: dedup_digests(dig, workspace=ws)),
+                     "same": bool(torch.equal(r.first, res.first) and torch.equal(r.uid, res.uid))}
+    os.environ.pop("DOOLY_DEDUP_INSERT", None)
     # the same digests from the default kernel variant (DOOLY_SHA_VARIANT unset)
     var = os.environ.pop("DOOLY_SHA_VARIANT", None)
     base = hash_records(recs).clone()
@@ -53,7 +65,7 @@ def main() -> None:
     same = bool(torch.equal(ref, base))
     print(json.dumps({"records": a.records, "sha_ms": sha_ms, "dedup_ms": dd_ms,
                       "records_per_s": a.records / dd_ms * 1e3, "unique": int(res.n_unique),
-                      "digests_unchanged": same}))
+                      "digests_unchanged": same, "dedup_digests_by_insert": ins}))
 
 
 if __name__ == "__main__":
