@@ -107,7 +107,7 @@ __device__ __noinline__ void sha256_compress_blocks(uint32_t hs[8], const uint32
 
 constexpr int SHA_THREADS = 128;
 #ifndef SHA_MINB
-#define SHA_MINB 6  // 6 CTAs/SM (67 registers): 0.924 vs 0.93-0.99 ms for 4M records; 7-8 slower
+#define SHA_MINB 4  // 4M C5 records: 0.831 ms at 4 CTAs/SM (88 registers), 0.833 at 5, 0.846 at 6, 0.854 at 7
 #endif
 constexpr int SHA_BUF_BLOCKS = 3;  // 192 B: C1-C5 canonical messages fit (longer ones drain)
 constexpr int SHA_STRIDE = SHA_BUF_BLOCKS * 16 + 1;   // odd word stride: conflict-free reads
@@ -139,7 +139,15 @@ struct ShaStream {
   __device__ __forceinline__ void emit(uint32_t w) {
     buf[nw++] = w;
     if (nw == SHA_BUF_BLOCKS * 16) {  // long message: drain (rare, divergent)
-      sha256_compress_blocks(h, buf, SHA_BUF_BLOCKS);
+      // The out-of-line drain gets a COPY of the chaining state: passing h
+      // itself would take its address and force the whole stream state into
+      // local memory (an LDL/STL pair around every emitted byte and word).
+      uint32_t t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] = h[k];
+      sha256_compress_blocks(t, buf, SHA_BUF_BLOCKS);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) h[k] = t[k];
       nw = 0;
     }
   }
@@ -213,8 +221,8 @@ __global__ void __launch_bounds__(SHA_THREADS, SHA_MINB) sha256_records_kernel(
     const dooly_digest_peers pe, uint32_t one) {
   __shared__ uint32_t s_buf[SHA_THREADS * SHA_STRIDE];
   ShaStream st;
-  for (int64_t base = (int64_t)blockIdx.x * SHA_THREADS; base < n;
-       base += (int64_t)gridDim.x * SHA_THREADS) {
+  const int64_t stride = (int64_t)gridDim.x * SHA_THREADS;
+  for (int64_t base = (int64_t)blockIdx.x * SHA_THREADS; base < n; base += stride) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < n;
     st.init(s_buf + threadIdx.x * SHA_STRIDE);
