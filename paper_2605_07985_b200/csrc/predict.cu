@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace dooly {
@@ -582,6 +584,124 @@ __device__ __forceinline__ void st_stream_128(double* p, double a, double b) {
 
 // QPP = queries per pair (8: 128-query tiles, LDG.256 streams; 4: 64-query
 // tiles, LDG.128 streams, fewer live registers -> more resident warps)
+// One 16 x QPP-query tile of the paired path (shared by the paired kernel and
+// the pair warps of the hybrid kernel).
+template <int QPP>
+__device__ __forceinline__ void pair_tile(int64_t tile, const double* __restrict__ rows,
+                                          int64_t n_sig, const PackInfo& pk,
+                                          const uint32_t* __restrict__ sig,
+                                          const uint32_t* __restrict__ x, int64_t n_q,
+                                          double* __restrict__ out, uint32_t* __restrict__ flags,
+                                          int64_t n_words, int64_t& bad_min, int lane) {
+  constexpr int TQ = 16 * QPP;  // queries per warp tile
+  const int pr = lane >> 1;
+  const bool B = (lane & 1) != 0;
+  const int64_t qp = tile * TQ + QPP * pr;
+  const bool live = qp < n_q;  // n_q % 8 == 0: a pair's queries are all in or all out
+  const int64_t qs = live ? qp : 0;
+  uint32_t sv[QPP], x0[QPP], x1[QPP], x2[QPP];
+  if constexpr (QPP == 8) {
+    const U8 a = ld_stream_256(sig + qs), b = ld_stream_256(x + qs),
+             c = ld_stream_256(x + n_q + qs), d = ld_stream_256(x + 2 * n_q + qs);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sv[j] = a.v[j], x0[j] = b.v[j], x1[j] = c.v[j], x2[j] = d.v[j];
+  } else {
+    const U4q a = ld_stream_128(sig + qs), b = ld_stream_128(x + qs),
+              c = ld_stream_128(x + n_q + qs), d = ld_stream_128(x + 2 * n_q + qs);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sv[j] = a.v[j], x0[j] = b.v[j], x1[j] = c.v[j], x2[j] = d.v[j];
+  }
+  double res[QPP / 2];
+  uint32_t ebits = 0, cbits = 0;
+#pragma unroll
+  for (int j = 0; j < QPP; j += 2) {
+    const uint32_t sa = sv[j], sb = sv[j + 1];
+    const double* ra = sa < (uint64_t)n_sig ? rows + 12 * (int64_t)sa : rows - 12;
+    const double* rb = sb < (uint64_t)n_sig ? rows + 12 * (int64_t)sb : rows - 12;
+    double w1[4], w2[4], w3[4];
+    ld_row_256(B ? ra + 4 : ra, w1[0], w1[1], w1[2], w1[3]);
+    ld_row_256(B ? rb : ra + 8, w2[0], w2[1], w2[2], w2[3]);
+    ld_row_256(B ? rb + 8 : rb + 4, w3[0], w3[1], w3[2], w3[3]);
+    const uint32_t a0 = x0[j], a1 = x1[j], a2 = x2[j];
+    const uint32_t b0 = x0[j + 1], b1 = x1[j + 1], b2 = x2[j + 1];
+    // slot 1: A (j, s0: x0, x1) | B (j, s1: x1, x2)
+    // slot 2: A (j, s2: x2, x0) | B (j+1, s0: x0, x1)
+    // slot 3: A (j+1, s1: x1, x2) | B (j+1, s2: x2, x0)
+    const double u1 = u2d(B ? a1 : a0), v1 = u2d(B ? a2 : a1);
+    const double u2 = u2d(B ? b0 : a2), v2 = u2d(B ? b1 : a0);
+    const double u3 = u2d(B ? b2 : b1), v3 = u2d(B ? b0 : b2);
+    const double S1 = sector_sum(B ? 0.0 : w1[0], w1[1], w1[2], w1[3], u1, v1);
+    const double S2 = sector_sum(B ? w2[0] : 0.0, w2[1], w2[2], w2[3], u2, v2);
+    const double S3 = sector_sum(0.0, w3[1], w3[2], w3[3], u3, v3);
+    // A needs s1(j) = B's S1; B needs s1(j+1) = A's S3
+    const double got = __shfl_xor_sync(0xFFFFFFFFu, B ? S1 : S3, 1);
+    const double sum = B ? add(add(S2, got), S3) : add(add(S1, got), S2);
+    // box: the finishing lane holds hi_bits (A: slot 2 = sector 2 of j; B:
+    // slot 3 = sector 2 of j+1); the partner holds lo_bits (B: slot 1 =
+    // sector 1 of j; A: slot 3 = sector 1 of j+1) and tests x < lo for it
+    const uint64_t hib = (uint64_t)__double_as_longlong(B ? w3[0] : w2[0]);
+    const uint64_t lob = (uint64_t)__double_as_longlong(B ? w1[0] : w3[0]);
+    const uint32_t p0 = B ? a0 : b0, p1 = B ? a1 : b1, p2 = B ? a2 : b2;   // partner's query
+    const uint32_t l0 = (uint32_t)(lob & pk.m0), l1 = (uint32_t)((lob >> pk.s1) & pk.m1),
+                   l2 = (uint32_t)((lob >> pk.s2) & pk.m2);
+    const bool below_p = (p0 < l0) | (p1 < l1) | (p2 < l2);
+    const uint32_t lo0 = __shfl_xor_sync(0xFFFFFFFFu, l0, 1);
+    const uint32_t bel = __ballot_sync(0xFFFFFFFFu, below_p);
+    const bool below = (bel >> (lane ^ 1)) & 1u;
+    const uint32_t h0 = (uint32_t)(hib & pk.m0), h1 = (uint32_t)((hib >> pk.s1) & pk.m1),
+                   h2 = (uint32_t)((hib >> pk.s2) & pk.m2);
+    const uint32_t m0 = B ? b0 : a0, m1 = B ? b1 : a1, m2 = B ? b2 : a2;  // my query
+    const bool above = (m0 > h0) | (m1 > h1) | (m2 > h2);
+    const uint32_t my_sig = B ? sb : sa;
+    const bool valid = live && my_sig < (uint64_t)n_sig && lo0 <= h0;
+    bool cl = false;
+    const double pv = clamp_floor(sum, cl);
+    const int jm = j + (B ? 1 : 0);                 // my query's index in the pair's QPP
+    res[j >> 1] = valid ? pv : nan64();
+    ebits |= (uint32_t)(valid && (below || above)) << jm;
+    cbits |= (uint32_t)(valid && cl) << jm;
+    if (live && !valid && qp + jm < bad_min) bad_min = qp + jm;
+  }
+  // regroup: A holds the even queries, B the odd ones -> A the first half, B the second
+  if constexpr (QPP == 8) {
+    const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[2], 1);  // A<-p1, B<-p4
+    const double g2 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[1] : res[3], 1);  // A<-p3, B<-p6
+    if (live) {
+      if (B)
+        st_stream_256(out + qp + 4, g1, res[2], g2, res[3]);
+      else
+        st_stream_256(out + qp, res[0], g1, res[1], g2);
+    }
+  } else {
+    const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[1], 1);  // A<-p1, B<-p2
+    if (live) {
+      if (B)
+        st_stream_128(out + qp + 2, g1, res[1]);
+      else
+        st_stream_128(out + qp, res[0], g1);
+    }
+  }
+  if (flags != nullptr) {
+    // a pair's QPP bits; 32 / QPP pairs per flag word
+    uint32_t e8 = ebits | __shfl_xor_sync(0xFFFFFFFFu, ebits, 1);
+    uint32_t c8 = cbits | __shfl_xor_sync(0xFFFFFFFFu, cbits, 1);
+    constexpr int PPW = 32 / QPP;                   // pairs per word
+    const int sh = QPP * (pr % PPW);
+    e8 <<= sh;
+    c8 <<= sh;
+#pragma unroll
+    for (int o = 2; o < 2 * PPW; o <<= 1) {
+      e8 |= __shfl_xor_sync(0xFFFFFFFFu, e8, o);
+      c8 |= __shfl_xor_sync(0xFFFFFFFFu, c8, o);
+    }
+    const int64_t word = tile * (TQ / 32) + pr / PPW;
+    if ((lane & (2 * PPW - 1)) == 0 && word < n_words) {
+      flags[word] = e8;
+      flags[n_words + word] = c8;
+    }
+  }
+}
+
 template <int QPP, int MINB>
 __global__ void __launch_bounds__(256, MINB) predict_attn_pair_kernel(
     const void* __restrict__ table, int64_t n_sig, const uint32_t* __restrict__ sig,
@@ -590,122 +710,198 @@ __global__ void __launch_bounds__(256, MINB) predict_attn_pair_kernel(
   constexpr int TQ = 16 * QPP;  // queries per warp tile
   PackInfo pk = read_pack_header(table, n_sig);
   if (!pk.ok) n_sig = 0;
-  const int lane = threadIdx.x & 31, pr = lane >> 1;
-  const bool B = (lane & 1) != 0;
+  const int lane = threadIdx.x & 31;
   const double* rows = reinterpret_cast<const double*>(static_cast<const dooly_attn_row96*>(table) + 1);
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_tiles = (n_q + TQ - 1) / TQ;
   const int64_t n_words = (n_q + 31) >> 5;
   int64_t bad_min = INT64_MAX;
-  for (int64_t tile = warp; tile < n_tiles; tile += n_warps) {
-    const int64_t qp = tile * TQ + QPP * pr;
-    const bool live = qp < n_q;  // n_q % 8 == 0: a pair's queries are all in or all out
-    const int64_t qs = live ? qp : 0;
-    uint32_t sv[QPP], x0[QPP], x1[QPP], x2[QPP];
-    if constexpr (QPP == 8) {
-      const U8 a = ld_stream_256(sig + qs), b = ld_stream_256(x + qs),
-               c = ld_stream_256(x + n_q + qs), d = ld_stream_256(x + 2 * n_q + qs);
+  for (int64_t tile = warp; tile < n_tiles; tile += n_warps)
+    pair_tile<QPP>(tile, rows, n_sig, pk, sig, x, n_q, out, flags, n_words, bad_min, lane);
+  if (err_first != nullptr && bad_min != INT64_MAX)
+    atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)bad_min);
+}
+
+// ---- hybrid packed-attention path (DOOLY_PREDICT_ATTN=hybrid).
+//
+// profiles/r2_predict.md session 5: TMA tile::gather4 row fetches and LDG.256
+// row gathers do not share one request interface completely — warps of both
+// kinds side by side gather ~14% more random 96-B rows per second than either
+// alone.  Here NPW warps per CTA run the paired path over the first part of the
+// query range and NTW warps serve the rest in 32-query rounds: lane l's row
+// arrives in shared memory by `cp.async.bulk.tensor.2d ... tile::gather4`
+// (lanes 0-7 each fetch the rows of lanes 4i..4i+3; one mbarrier per stage
+// counts the 3 KB), HY_D stages in flight per warp, sig/features loaded into
+// registers one round before the gather is issued.  The lane then evaluates
+// its own query with the one-lane arithmetic (eval_row96), so every query's
+// value and flags are those of the other paths bit for bit.
+constexpr int HY_D = 3;                   // gather stages per TMA warp
+constexpr int HY_STAGE = 32 * 96;         // bytes per stage (32 rows)
+
+__device__ __forceinline__ void hy_wait(uint32_t bar, uint32_t parity) {
+  // bounded: a byte-count mismatch must fail loudly, not hang the GPU
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1u << 26)) __trap();
+  }
+}
+
+template <int NPW, int NTW>
+__global__ void __launch_bounds__(32 * (NPW + NTW), 2) predict_attn_hybrid_kernel(
+    const __grid_constant__ CUtensorMap tmap, const void* __restrict__ table, int64_t n_sig,
+    const uint32_t* __restrict__ sig, const uint32_t* __restrict__ x, int64_t n_q,
+    double* __restrict__ out, uint32_t* __restrict__ flags, int64_t* __restrict__ err_first,
+    int64_t pair_q0) {
+  extern __shared__ __align__(128) unsigned char hy_smem[];
+  PackInfo pk = read_pack_header(table, n_sig);
+  if (!pk.ok) n_sig = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t n_words = (n_q + 31) >> 5;
+  int64_t bad_min = INT64_MAX;
+  if (wid < NPW) {
+    // paired path over tiles [pair_q0 / 128, n_tiles)
+    const double* rows =
+        reinterpret_cast<const double*>(static_cast<const dooly_attn_row96*>(table) + 1);
+    const int64_t n_tiles = (n_q + 127) / 128;
+    const int64_t nw = (int64_t)gridDim.x * NPW;
+    for (int64_t tile = pair_q0 / 128 + blockIdx.x * (int64_t)NPW + wid; tile < n_tiles; tile += nw)
+      pair_tile<8>(tile, rows, n_sig, pk, sig, x, n_q, out, flags, n_words, bad_min, lane);
+  } else {
+    const int tw = wid - NPW;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(hy_smem) + 8u * HY_D * tw;
+    const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(hy_smem) + 128u * ((8 * HY_D * NTW + 127) / 128) +
+                           (uint32_t)(HY_STAGE * HY_D * tw);
+    const unsigned char* slot_p = hy_smem + 128 * ((8 * HY_D * NTW + 127) / 128) + HY_STAGE * HY_D * tw;
+    if (lane == 0)
+      for (int b = 0; b < HY_D; ++b)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u * b));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    const int64_t n_rounds = pair_q0 / 32;          // the TMA range: queries [0, pair_q0)
+    const int64_t nw = (int64_t)gridDim.x * NTW;
+    const int64_t r0 = blockIdx.x * (int64_t)NTW + tw;
+    // Software pipeline per warp (rounds rd, rd + nw, ... of this warp): the
+    // sig of a round is loaded 4 rounds before its gather is issued, its
+    // features when the gather is issued, and it is evaluated 2 rounds later.
+    struct Q {
+      uint32_t s, a, b, c;
+    };
+    auto ld_sig = [&](int64_t rd) {
+      return rd < n_rounds ? __ldg(sig + rd * 32 + lane) : 0xFFFFFFFFu;
+    };
+    auto ld_x = [&](int64_t rd, uint32_t sv) {
+      Q v{sv, 0u, 0u, 0u};
+      if (rd < n_rounds) {
+        const int64_t q = rd * 32 + lane;
+        v.a = __ldg(x + q);
+        v.b = __ldg(x + n_q + q);
+        v.c = __ldg(x + 2 * n_q + q);
+      }
+      return v;
+    };
+    auto issue = [&](int64_t rd, uint32_t s, int b) {
+      if (rd >= n_rounds) return;
+      const int32_t row = s < (uint64_t)n_sig ? (int32_t)s + 1 : 0;   // row 0: the header
+      const int i0 = (lane & 7) * 4;
+      const int32_t g0 = __shfl_sync(0xFFFFFFFFu, row, i0), g1 = __shfl_sync(0xFFFFFFFFu, row, i0 + 1),
+                    g2 = __shfl_sync(0xFFFFFFFFu, row, i0 + 2), g3 = __shfl_sync(0xFFFFFFFFu, row, i0 + 3);
+      const uint32_t bar = bar0 + 8u * b;
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(HY_STAGE)
+                     : "memory");
+      __syncwarp();
+      if (lane < 8)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(slot0 + (uint32_t)(HY_STAGE * b + lane * 4 * 96)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(g0), "r"(g1), "r"(g2), "r"(g3),
+            "r"(bar)
+            : "memory");
+    };
+    // prologue: rounds r0, r0 + nw gathered; sigs of r0 + 2 nw .. r0 + 5 nw loaded
+    Q qc = ld_x(r0, ld_sig(r0));
+    issue(r0, qc.s, 0);
+    Q q1 = ld_x(r0 + nw, ld_sig(r0 + nw));
+    issue(r0 + nw, q1.s, 1);
+    uint32_t s2 = ld_sig(r0 + 2 * nw), s3 = ld_sig(r0 + 3 * nw), s4 = ld_sig(r0 + 4 * nw),
+             s5 = ld_sig(r0 + 5 * nw);
+    uint32_t phase = 0;
+    int b = 0;
+    for (int64_t rd = r0; rd < n_rounds; rd += nw) {
+      // gather round rd + 2 nw into the stage freed by round rd - nw
+      const int b2 = b == 0 ? 2 : b - 1;
+      issue(rd + 2 * nw, s2, b2);
+      const Q q2 = ld_x(rd + 2 * nw, s2);
+      s2 = s3;
+      s3 = s4;
+      s4 = s5;
+      s5 = ld_sig(rd + 6 * nw);
+      hy_wait(bar0 + 8u * b, (phase >> b) & 1u);
+      phase ^= 1u << b;
+      const double2* rp = reinterpret_cast<const double2*>(slot_p + HY_STAGE * b + lane * 96);
+      double w[12];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sv[j] = a.v[j], x0[j] = b.v[j], x1[j] = c.v[j], x2[j] = d.v[j];
-    } else {
-      const U4q a = ld_stream_128(sig + qs), b = ld_stream_128(x + qs),
-                c = ld_stream_128(x + n_q + qs), d = ld_stream_128(x + 2 * n_q + qs);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sv[j] = a.v[j], x0[j] = b.v[j], x1[j] = c.v[j], x2[j] = d.v[j];
-    }
-    double res[QPP / 2];
-    uint32_t ebits = 0, cbits = 0;
-#pragma unroll
-    for (int j = 0; j < QPP; j += 2) {
-      const uint32_t sa = sv[j], sb = sv[j + 1];
-      const double* ra = sa < (uint64_t)n_sig ? rows + 12 * (int64_t)sa : rows - 12;
-      const double* rb = sb < (uint64_t)n_sig ? rows + 12 * (int64_t)sb : rows - 12;
-      double w1[4], w2[4], w3[4];
-      ld_row_256(B ? ra + 4 : ra, w1[0], w1[1], w1[2], w1[3]);
-      ld_row_256(B ? rb : ra + 8, w2[0], w2[1], w2[2], w2[3]);
-      ld_row_256(B ? rb + 8 : rb + 4, w3[0], w3[1], w3[2], w3[3]);
-      const uint32_t a0 = x0[j], a1 = x1[j], a2 = x2[j];
-      const uint32_t b0 = x0[j + 1], b1 = x1[j + 1], b2 = x2[j + 1];
-      // slot 1: A (j, s0: x0, x1) | B (j, s1: x1, x2)
-      // slot 2: A (j, s2: x2, x0) | B (j+1, s0: x0, x1)
-      // slot 3: A (j+1, s1: x1, x2) | B (j+1, s2: x2, x0)
-      const double u1 = u2d(B ? a1 : a0), v1 = u2d(B ? a2 : a1);
-      const double u2 = u2d(B ? b0 : a2), v2 = u2d(B ? b1 : a0);
-      const double u3 = u2d(B ? b2 : b1), v3 = u2d(B ? b0 : b2);
-      const double S1 = sector_sum(B ? 0.0 : w1[0], w1[1], w1[2], w1[3], u1, v1);
-      const double S2 = sector_sum(B ? w2[0] : 0.0, w2[1], w2[2], w2[3], u2, v2);
-      const double S3 = sector_sum(0.0, w3[1], w3[2], w3[3], u3, v3);
-      // A needs s1(j) = B's S1; B needs s1(j+1) = A's S3
-      const double got = __shfl_xor_sync(0xFFFFFFFFu, B ? S1 : S3, 1);
-      const double sum = B ? add(add(S2, got), S3) : add(add(S1, got), S2);
-      // box: the finishing lane holds hi_bits (A: slot 2 = sector 2 of j; B:
-      // slot 3 = sector 2 of j+1); the partner holds lo_bits (B: slot 1 =
-      // sector 1 of j; A: slot 3 = sector 1 of j+1) and tests x < lo for it
-      const uint64_t hib = (uint64_t)__double_as_longlong(B ? w3[0] : w2[0]);
-      const uint64_t lob = (uint64_t)__double_as_longlong(B ? w1[0] : w3[0]);
-      const uint32_t p0 = B ? a0 : b0, p1 = B ? a1 : b1, p2 = B ? a2 : b2;   // partner's query
-      const uint32_t l0 = (uint32_t)(lob & pk.m0), l1 = (uint32_t)((lob >> pk.s1) & pk.m1),
-                     l2 = (uint32_t)((lob >> pk.s2) & pk.m2);
-      const bool below_p = (p0 < l0) | (p1 < l1) | (p2 < l2);
-      const uint32_t lo0 = __shfl_xor_sync(0xFFFFFFFFu, l0, 1);
-      const uint32_t bel = __ballot_sync(0xFFFFFFFFu, below_p);
-      const bool below = (bel >> (lane ^ 1)) & 1u;
-      const uint32_t h0 = (uint32_t)(hib & pk.m0), h1 = (uint32_t)((hib >> pk.s1) & pk.m1),
-                     h2 = (uint32_t)((hib >> pk.s2) & pk.m2);
-      const uint32_t m0 = B ? b0 : a0, m1 = B ? b1 : a1, m2 = B ? b2 : a2;  // my query
-      const bool above = (m0 > h0) | (m1 > h1) | (m2 > h2);
-      const uint32_t my_sig = B ? sb : sa;
-      const bool valid = live && my_sig < (uint64_t)n_sig && lo0 <= h0;
+      for (int k = 0; k < 6; ++k) {
+        const double2 v = rp[k];
+        w[2 * k] = v.x;
+        w[2 * k + 1] = v.y;
+      }
+      uint32_t lo[3], hi[3];
+      unpack_box((uint64_t)__double_as_longlong(w[4]), (uint64_t)__double_as_longlong(w[8]), pk, lo,
+                 hi);
+      const int64_t q = rd * 32 + lane;
+      const bool valid = qc.s < (uint64_t)n_sig && lo[0] <= hi[0];
       bool cl = false;
-      const double pv = clamp_floor(sum, cl);
-      const int jm = j + (B ? 1 : 0);                 // my query's index in the pair's QPP
-      res[j >> 1] = valid ? pv : nan64();
-      ebits |= (uint32_t)(valid && (below || above)) << jm;
-      cbits |= (uint32_t)(valid && cl) << jm;
-      if (live && !valid && qp + jm < bad_min) bad_min = qp + jm;
-    }
-    // regroup: A holds the even queries, B the odd ones -> A the first half, B the second
-    if constexpr (QPP == 8) {
-      const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[2], 1);  // A<-p1, B<-p4
-      const double g2 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[1] : res[3], 1);  // A<-p3, B<-p6
-      if (live) {
-        if (B)
-          st_stream_256(out + qp + 4, g1, res[2], g2, res[3]);
-        else
-          st_stream_256(out + qp, res[0], g1, res[1], g2);
+      const double pv = clamp_floor(eval_row96(w, qc.a, qc.b, qc.c), cl);
+      const bool e = valid && (qc.a < lo[0] || qc.a > hi[0] || qc.b < lo[1] || qc.b > hi[1] ||
+                               qc.c < lo[2] || qc.c > hi[2]);
+      out[q] = valid ? pv : nan64();
+      if (!valid && q < bad_min) bad_min = q;
+      const uint32_t be = __ballot_sync(0xFFFFFFFFu, e), bc = __ballot_sync(0xFFFFFFFFu, valid && cl);
+      if (flags != nullptr && lane == 0) {
+        flags[rd] = be;
+        flags[n_words + rd] = bc;
       }
-    } else {
-      const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[1], 1);  // A<-p1, B<-p2
-      if (live) {
-        if (B)
-          st_stream_128(out + qp + 2, g1, res[1]);
-        else
-          st_stream_128(out + qp, res[0], g1);
-      }
-    }
-    if (flags != nullptr) {
-      // a pair's QPP bits; 32 / QPP pairs per flag word
-      uint32_t e8 = ebits | __shfl_xor_sync(0xFFFFFFFFu, ebits, 1);
-      uint32_t c8 = cbits | __shfl_xor_sync(0xFFFFFFFFu, cbits, 1);
-      constexpr int PPW = 32 / QPP;                   // pairs per word
-      const int sh = QPP * (pr % PPW);
-      e8 <<= sh;
-      c8 <<= sh;
-#pragma unroll
-      for (int o = 2; o < 2 * PPW; o <<= 1) {
-        e8 |= __shfl_xor_sync(0xFFFFFFFFu, e8, o);
-        c8 |= __shfl_xor_sync(0xFFFFFFFFu, c8, o);
-      }
-      const int64_t word = tile * (TQ / 32) + pr / PPW;
-      if ((lane & (2 * PPW - 1)) == 0 && word < n_words) {
-        flags[word] = e8;
-        flags[n_words + word] = c8;
-      }
+      __syncwarp();   // stage b is re-filled by the next iteration's issue
+      qc = q1;
+      q1 = q2;
+      b = b == 2 ? 0 : b + 1;
     }
   }
   if (err_first != nullptr && bad_min != INT64_MAX)
     atomicMin(reinterpret_cast<unsigned long long*>(err_first), (unsigned long long)bad_min);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D tensor map over the packed table's rows (header = row 0): 24 u32 words x
+// (n_sig + 1) rows, 96-B row stride, box = one row.
+static bool row96_tensor_map(CUtensorMap* m, const void* table, int64_t n_sig) {
+  static EncodeTiledFn encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess)
+      fn = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(fn);
+  }();
+  if (encode == nullptr || n_sig + 1 > (int64_t)INT32_MAX) return false;
+  const cuuint64_t dims[2] = {24, (cuuint64_t)(n_sig + 1)};
+  const cuuint64_t strides[1] = {96};
+  const cuuint32_t box[2] = {24, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(table), dims, strides, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // DOOLY_PREDICT_ATTN selects the packed-attention kernel: default the paired
@@ -725,6 +921,7 @@ static int predict_attn_mode() {
          : strcmp(v, "pair4") == 0 ? 6
          : strcmp(v, "pair4b") == 0 ? 7
          : strcmp(v, "pair3") == 0 ? 8
+         : strcmp(v, "hybrid") == 0 ? 9
                                    : 5;
 }
 
@@ -747,6 +944,24 @@ cudaError_t launch_predict_kind(const void* table, int64_t n_sig, const uint32_t
     if (blocks > need) blocks = need;
     predict_attn_staged_kernel<<<(unsigned)blocks, kStWarps * 32, 0, stream>>>(
         table, n_sig, sig, x, n_q, out, flags, err_first);
+  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && mode == 9 && n_q >= 128) {
+    // TMA share of the queries (DOOLY_PREDICT_TMA_FRAC, default 0.3), whole 128-query tiles
+    const char* fv = getenv("DOOLY_PREDICT_TMA_FRAC");
+    const double frac = fv ? atof(fv) : 0.3;
+    const int64_t n_tiles = (n_q + 127) / 128;
+    int64_t tma_tiles = (int64_t)(frac * (double)n_tiles);
+    if (tma_tiles < 0) tma_tiles = 0;
+    if (tma_tiles > n_tiles - 1) tma_tiles = n_tiles - 1;
+    CUtensorMap tm;
+    if (!row96_tensor_map(&tm, table, n_sig)) return cudaErrorInvalidValue;
+    constexpr int NPW = 8, NTW = 4;
+    const size_t smem = 128 * ((8 * HY_D * NTW + 127) / 128) + (size_t)HY_STAGE * HY_D * NTW;
+    auto kern = predict_attn_hybrid_kernel<NPW, NTW>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * (NPW + NTW), smem);
+    const int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+    kern<<<(unsigned)blocks, 32 * (NPW + NTW), smem, stream>>>(tm, table, n_sig, sig, x, n_q, out,
+                                                               flags, err_first, tma_tiles * 128);
   } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && (mode >= 5 && mode <= 8)) {
     auto kern = mode == 6 ? predict_attn_pair_kernel<4, 3>
               : mode == 7 ? predict_attn_pair_kernel<4, 2>

@@ -155,13 +155,17 @@ def test_predict_bit_exact(kind, n_q, offset, dev):
 
 
 @pytest.mark.parametrize("mode", ["coop", "coop8", "coop1", "staged", "pair", "pair4", "pair4b", "pair3",
-                                  "vec"])
+                                  "vec", "hybrid", "hybrid:0.9", "hybrid:0"])
 @pytest.mark.parametrize("n_q", [8, 160 * 7, 160 * 1000 + 88])
 def test_predict_packed_cooperative_kernel(mode, n_q, dev, monkeypatch):
     """Every packed-attention kernel (paired default, one lane per row, the
-    cp.async-staged and the 3-lanes-per-row variants) is bit-identical to the
+    cp.async-staged, the 3-lanes-per-row and the TMA gather4 + paired hybrid
+    variants, the latter at several TMA shares) is bit-identical to the
     oracle, flags and unknown/unfitted rows included."""
+    mode, _, frac = mode.partition(":")
     monkeypatch.setenv("DOOLY_PREDICT_ATTN", mode)
+    if frac:
+        monkeypatch.setenv("DOOLY_PREDICT_TMA_FRAC", frac)
     x, y, off = synth_fit_data(ATTN, 257, 64, seed=21)
     ref_fit = osim.fit(ATTN, x, y, np.array([0, 3, *off[2:]], dtype=np.int64))  # row 0 unfitted
     table = {k: ref_fit[k] for k in ("coef", "inv", "lo", "hi")}

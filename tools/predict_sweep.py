@@ -59,7 +59,7 @@ def main() -> None:
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--layouts", default="affine,attn,attn96")
     ap.add_argument("--vs-ldg", action="store_true",
-                    help="attn96: compare out/flags bit for bit with DOOLY_PREDICT_TMA unset")
+                    help="attn96: compare out/flags bit for bit with DOOLY_PREDICT_ATTN unset (the default kernel)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     base = {"affine": _lib.KIND_AFFINE, "attn": _lib.KIND_ATTN, "attn96": _lib.KIND_ATTN}
@@ -88,16 +88,18 @@ def main() -> None:
         med = ms[len(ms) // 2]
         ok = int(err.item()) == torch.iinfo(torch.int64).max
         line = {"layout": name, "sigs": a.sigs, "queries": a.queries, "ms": med,
+                "mode": os.environ.get("DOOLY_PREDICT_ATTN", "default"),
+                "tma_frac": os.environ.get("DOOLY_PREDICT_TMA_FRAC"),
                 "gq_per_s": a.queries / med / 1e6, "all_known": ok,
                 "checksum": float(out.sum().item())}
         if a.vs_ldg and name == "attn96":
-            env = os.environ.pop("DOOLY_PREDICT_TMA", None)
+            env = os.environ.pop("DOOLY_PREDICT_ATTN", None)
             out2, flags2 = torch.empty_like(out), torch.empty_like(flags)
             err2 = torch.full_like(err, torch.iinfo(torch.int64).max)
             predict_batch(kind, table, sig, x, out2, flags2, err2)
             torch.cuda.synchronize()
             if env is not None:
-                os.environ["DOOLY_PREDICT_TMA"] = env
+                os.environ["DOOLY_PREDICT_ATTN"] = env
             line["bit_identical_vs_ldg"] = bool(torch.equal(out.view(torch.int64),
                                                             out2.view(torch.int64))
                                                 and torch.equal(flags, flags2)
