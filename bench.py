@@ -808,6 +808,27 @@ def run_ours(args):
     for _ in range(max(1, args.warmup)):
         for k in (AFFINE, ATTN):
             fit_out[k] = do_fit(k)
+    fused_note = None
+    if peer is not None:
+        # the fused path's first use on this box: every rank's rows must have
+        # landed in every rank's table (no handshake timed out, no all-zero
+        # row); all ranks agree, and fall back to the NCCL all-gather together
+        ok = 1
+        for k in (AFFINE, ATTN):
+            ok &= int(peer[k].timed_out.item()) == 0
+            ok &= bool(peer[k].table.view(peer[k].n_total, -1).any(dim=1).all().item())
+        flag = torch.tensor([ok], dtype=torch.int32,
+                            device=dev if torch.distributed.get_backend() == "nccl" else "cpu")
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            fused_note = "fused all-gather failed its first-use check on this box; NCCL used"
+            if rank == 0:
+                print(fused_note, file=sys.stderr)
+            peer = None
+            packed96 = torch.empty((n_sig[ATTN] + 1, 96), dtype=torch.uint8, device=dev)
+            fit_out.clear()
+            for k in (AFFINE, ATTN):
+                fit_out[k] = do_fit(k)
     barrier_sync(dist_on)
     stream = torch.cuda.current_stream()
     ev = {k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -871,7 +892,8 @@ def run_ours(args):
         "launches_per_step": fit_launches,
         "allgather_path": None if not dist_on else (
             "fused: peer-memory row stores in the fit epilogue + device arrival counter"
-            if peer is not None else "NCCL all_gather of the regressor rows"),
+            if peer is not None else "NCCL all_gather of the regressor rows"
+            + (f" ({fused_note})" if fused_note else "")),
         "roofline": {"bound": "hbm", "achieved": fit_bytes / (fit_dev_ms / 1e3) / 1e9,
                      "peak": hbm_peak, "unit": "GB/s",
                      "frac": fit_bytes / (fit_dev_ms / 1e3) / 1e9 / hbm_peak,
