@@ -584,6 +584,10 @@ __device__ __forceinline__ void st_stream_128(double* p, double a, double b) {
 
 // QPP = queries per pair (8: 128-query tiles, LDG.256 streams; 4: 64-query
 // tiles, LDG.128 streams, fewer live registers -> more resident warps)
+#ifndef PAIR_STRIDE_D
+#define PAIR_STRIDE_D 12  // doubles per packed row slot (experiment: 16 = 128-B slots)
+#endif
+
 // One 16 x QPP-query tile of the paired path (shared by the paired kernel and
 // the pair warps of the hybrid kernel).
 template <int QPP>
@@ -616,8 +620,8 @@ __device__ __forceinline__ void pair_tile(int64_t tile, const double* __restrict
 #pragma unroll
   for (int j = 0; j < QPP; j += 2) {
     const uint32_t sa = sv[j], sb = sv[j + 1];
-    const double* ra = sa < (uint64_t)n_sig ? rows + 12 * (int64_t)sa : rows - 12;
-    const double* rb = sb < (uint64_t)n_sig ? rows + 12 * (int64_t)sb : rows - 12;
+    const double* ra = sa < (uint64_t)n_sig ? rows + PAIR_STRIDE_D * (int64_t)sa : rows - PAIR_STRIDE_D;
+    const double* rb = sb < (uint64_t)n_sig ? rows + PAIR_STRIDE_D * (int64_t)sb : rows - PAIR_STRIDE_D;
     double w1[4], w2[4], w3[4];
     ld_row_256(B ? ra + 4 : ra, w1[0], w1[1], w1[2], w1[3]);
     ld_row_256(B ? rb : ra + 8, w2[0], w2[1], w2[2], w2[3]);
@@ -711,7 +715,7 @@ __global__ void __launch_bounds__(256, MINB) predict_attn_pair_kernel(
   PackInfo pk = read_pack_header(table, n_sig);
   if (!pk.ok) n_sig = 0;
   const int lane = threadIdx.x & 31;
-  const double* rows = reinterpret_cast<const double*>(static_cast<const dooly_attn_row96*>(table) + 1);
+  const double* rows = reinterpret_cast<const double*>(table) + PAIR_STRIDE_D;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n_tiles = (n_q + TQ - 1) / TQ;
