@@ -966,11 +966,12 @@ cudaError_t launch_predict_kind(const void* table, int64_t n_sig, const uint32_t
     const int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
     kern<<<(unsigned)blocks, 32 * (NPW + NTW), smem, stream>>>(tm, table, n_sig, sig, x, n_q, out,
                                                                flags, err_first, tma_tiles * 128);
-  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && (mode >= 5 && mode <= 8)) {
+  } else if (KIND == DOOLY_KIND_ATTN_PACKED && aligned && (mode >= 5 && mode <= 9)) {
+    // (mode 9 below 128 queries: the paired kernel alone)
     auto kern = mode == 6 ? predict_attn_pair_kernel<4, 3>
               : mode == 7 ? predict_attn_pair_kernel<4, 2>
               : mode == 8 ? predict_attn_pair_kernel<8, 3> : predict_attn_pair_kernel<8, 2>;
-    const int tq = (mode == 5 || mode == 8) ? 128 : 64;
+    const int tq = (mode == 6 || mode == 7) ? 64 : 128;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0);
     const int64_t tiles = (n_q + tq - 1) / tq;
     int64_t blocks = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
