@@ -370,6 +370,28 @@ def test_corpus_census_and_rerun(corpus, dev):
     assert to_profile == [] and len(skipped) == 42
 
 
+def test_a3_overall_reuse_on_gpu(corpus, dev):
+    """A3 through the GPU dedup, config by config into one DB over
+    the whole corpus (every record kind): N = 486, R = 439, 47 unique = N - R,
+    reuse >= 50%, >= 95% of the uniques seen within the first four models."""
+    from paper_2605_07985_b200.profiler import LatencyDB, dedup
+    from paper_2605_07985_b200.records import corpus_entries
+
+    db = LatencyDB()
+    n = r = 0
+    per_model, cur = [], None
+    for m, _, ents in corpus_entries(corpus):
+        to_profile, skipped = dedup(ents, db, device=dev)
+        n += len(ents)
+        r += len(skipped)
+        if m.name != cur:
+            cur = m.name
+            per_model.append(0)
+        per_model[-1] = len(db.signatures)
+    assert (n, r, len(db.signatures)) == (486, 439, 47)
+    assert r / n >= 0.5 and per_model[3] >= 0.95 * per_model[-1]
+
+
 def test_dedup_packed_large_uniform(dev):
     """C5-style bulk records (vectorised packer) vs oracle digests + dedup."""
     from paper_2605_07985_b200.profiler import DeviceRecords, dedup_packed

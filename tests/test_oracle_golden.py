@@ -96,6 +96,30 @@ def test_census_saturates_within_four_models(corpus):
     assert counts[3] >= 0.95 * counts[-1]
 
 
+def test_a3_overall_reuse_and_saturation(corpus):
+    """A3 over every record of the 12-model x 3-backend corpus, not
+    only attention: unique signatures = N - R, count-reuse ratio >= 50%, and the
+    cumulative unique count reaches >= 95% of its final value within the first
+    four models (manifest order)."""
+    from paper_2605_07985_b200.records import corpus_entries
+
+    seen, n, r, per_model, cur = set(), 0, 0, [], None
+    for m, _, es in corpus_entries(corpus):
+        for e in es:
+            h = oprof.signature_hash(oprof.canonicalize(e.to_json()))
+            n += 1
+            r += h in seen
+            seen.add(h)
+        if m.name != cur:
+            cur = m.name
+            per_model.append(0)
+        per_model[-1] = len(seen)
+    assert len(seen) == n - r
+    assert r / n >= 0.5
+    assert per_model[3] >= 0.95 * per_model[-1]
+    assert (n, r, len(seen)) == (486, 439, 47)
+
+
 def test_dedup_rerun_and_empty_db():
     ents = [{"name": "linear", "granularity": "operator", "arg_template": [[[8, "NT"], [64, "MC"]]],
              "kernel_symbols": ["g"], "attrs": {}}] * 3
