@@ -953,20 +953,29 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
       // (13 FP64 per group) — 7.25 FP64 per point instead of 13, and one
       // feature plane read per step instead of three.  Pass 2 likewise folds
       // the f1/f2 terms per group: 8.75 FP64 per point instead of 14.
-      auto fstep = [&](const double4& yv, int pp) {
-        const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
-        grid_g1_step(yv, f3reg ? f3l : g_ld_f(fpl + 2 * n + pp), u.x, u.y, acc);
+      // f3 source as a compile-time choice: the lane's register quad (f3reg)
+      // or an L1 load — a runtime select would copy the quad into the load's
+      // destination registers before every predicated load (8 moves a step)
+      auto pass1 = [&](auto f3of) {
+        auto fstep = [&](const double4& yv, int pp) {
+          const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
+          grid_g1_step(yv, f3of(pp), u.x, u.y, acc);
+        };
+        int p = 4 * lane;
+        constexpr int YS = 8;
+        for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
+          double4 yv[YS];
+#pragma unroll
+          for (int t = 0; t < YS; ++t) yv[t] = g_ld_y(ys + p + 128 * t, true);
+#pragma unroll
+          for (int t = 0; t < YS; ++t) fstep(yv[t], p + 128 * t);
+        }
+        for (; p < n; p += 128) fstep(g_ld_y(ys + p, true), p);
       };
-      int p = 4 * lane;
-      constexpr int YS = 8;
-      for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
-        double4 yv[YS];
-#pragma unroll
-        for (int t = 0; t < YS; ++t) yv[t] = g_ld_y(ys + p + 128 * t, true);
-#pragma unroll
-        for (int t = 0; t < YS; ++t) fstep(yv[t], p + 128 * t);
-      }
-      for (; p < n; p += 128) fstep(g_ld_y(ys + p, true), p);
+      if (f3reg)
+        pass1([&](int) { return f3l; });
+      else
+        pass1([&](int pp) { return g_ld_f(fpl + 2 * n + pp); });
     } else {
       sweep(true, pass1_step);
     }
@@ -983,20 +992,26 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     // ---- pass 2: training MAPE, the row re-read from L2
     if (factored) {
       // per group: p = A + f3 (B + c6 f3) with A, B the group's f1/f2 terms
-      auto fstep2 = [&](const double4& yv, int pp) {
-        const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
-        grid_g2_step(yv, f3reg ? f3l : g_ld_f(fpl + 2 * n + pp), u.x, u.y, c, err);
+      auto pass2 = [&](auto f3of) {
+        auto fstep2 = [&](const double4& yv, int pp) {
+          const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
+          grid_g2_step(yv, f3of(pp), u.x, u.y, c, err);
+        };
+        int p = 4 * lane;
+        constexpr int YS = 8;
+        for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
+          double4 yv[YS];
+#pragma unroll
+          for (int t = 0; t < YS; ++t) yv[t] = g_ld_y(ys + p + 128 * t, false);
+#pragma unroll
+          for (int t = 0; t < YS; ++t) fstep2(yv[t], p + 128 * t);
+        }
+        for (; p < n; p += 128) fstep2(g_ld_y(ys + p, false), p);
       };
-      int p = 4 * lane;
-      constexpr int YS = 8;
-      for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
-        double4 yv[YS];
-#pragma unroll
-        for (int t = 0; t < YS; ++t) yv[t] = g_ld_y(ys + p + 128 * t, false);
-#pragma unroll
-        for (int t = 0; t < YS; ++t) fstep2(yv[t], p + 128 * t);
-      }
-      for (; p < n; p += 128) fstep2(g_ld_y(ys + p, false), p);
+      if (f3reg)
+        pass2([&](int) { return f3l; });
+      else
+        pass2([&](int pp) { return g_ld_f(fpl + 2 * n + pp); });
     } else {
       sweep(false, pass2_step);
     }
