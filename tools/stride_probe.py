@@ -2,10 +2,11 @@
 (experiment: a 128-B slot keeps a row's three sectors in one line, so the
 paired loads' two same-row sectors always coalesce).  Run once with the
 default library (96-B slots) and once with a PAIR_STRIDE_D=16 build
-(DOOLY_LIB_PATH=tools/_build/libdooly_stride128.so --slot 128); the
+(DOOLY_LIB_PATH=tools/_build/libdooly_stride128.so --slot 128; a PAIR_SPLIT build
+with --slot split); the
 checksums must agree.
 
-    python tools/stride_probe.py --slot 96|128 [--sigs 500000] [--queries 500000000]
+    python tools/stride_probe.py --slot 96|128|split [--sigs 500000] [--queries 500000000]
 """
 
 from __future__ import annotations
@@ -28,7 +29,7 @@ from predict_sweep import gen_queries, synth_table  # noqa: E402
 
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("--slot", type=int, default=96)
+    ap.add_argument("--slot", default="96", choices=["96", "128", "split"])
     ap.add_argument("--sigs", type=int, default=500_000)
     ap.add_argument("--queries", type=int, default=500_000_000)
     ap.add_argument("--reps", type=int, default=5)
@@ -38,9 +39,16 @@ def main() -> None:
     sig, x = gen_queries(_lib.KIND_ATTN, table, a.queries, dev, 1)
     t96 = pack_attn(table)
     del table
-    if a.slot == 128:
+    if a.slot == "128":
         t = torch.zeros((a.sigs + 1, 128), dtype=torch.uint8, device=dev)
         t[:, :96] = t96
+    elif a.slot == "split":
+        # header padded to 128 B, then sectors 0-1 of every row (64-B slots), then sector 2
+        n = a.sigs
+        t = torch.zeros(128 + 96 * n, dtype=torch.uint8, device=dev)
+        t[:96] = t96[0]
+        t[128:128 + 64 * n] = t96[1:, :64].reshape(-1)
+        t[128 + 64 * n:] = t96[1:, 64:].reshape(-1)
     else:
         t = t96
     lib = _lib.load_library()
