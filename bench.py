@@ -57,6 +57,7 @@ BYTES_PER_POINT = {AFFINE: 4 + 8, ATTN: 12 + 8}                          # x u32
 BYTES_PER_GRID_POINT = 8                     # shared grid: y f64 per point (x counted once per kind)
 FP64_PER_ATTN_POINT = 27          # per-point passes (13 pass 1 + 14 pass 2)
 FP64_PER_ATTN_POINT_GROUPED = 16  # grouped passes: 7.25 + 8.75 (4-point groups share f1, f2)
+FP64_PER_ATTN_POINT_PERIODIC = 14  # + kv period dividing 128 points: per-position pass 1, 5.25 + 8.75
 SHA_ALU_PER_BLOCK = 48 * 18 + 16 * 10          # SASS count, sha256_compress
 ALU_PEAK_TINSTR = 64 * 148 * 1.965e9 / 1e12       # ALU pipe lanes/clk/SM x SMs x clock
 FP64_PEAK_TINSTR = 64 * 148 * 1.965e9 / 1e12   # 18.6 T DFMA-class instr/s
@@ -869,7 +870,12 @@ def run_ours(args):
     xa = fit_in[ATTN][0][:2].reshape(2, -1, 4) if n_pts[ATTN] % 4 == 0 else None
     grouped = xa is not None and bool((xa == xa[:, :, :1]).all().item()) and \
         os.environ.get("DOOLY_FIT_GRID_FACTOR", "1") != "0"
-    fp64_attn = FP64_PER_ATTN_POINT_GROUPED if grouped else FP64_PER_ATTN_POINT
+    x2 = fit_in[ATTN][0][2]
+    periodic = grouped and n_pts[ATTN] % 128 == 0 and \
+        bool((x2.reshape(-1, 128) == x2[:128]).all().item()) and \
+        os.environ.get("DOOLY_FIT_GRID_FACTOR", "2") not in ("0", "1")
+    fp64_attn = FP64_PER_ATTN_POINT_PERIODIC if periodic else \
+        FP64_PER_ATTN_POINT_GROUPED if grouped else FP64_PER_ATTN_POINT
     fit_dev_ms = sum(fit_ms.values()) / fit_steps
     fits = {
         "value": world * args.sigs / (fit_total_ms / 1e3), "unit": "fits/s",
@@ -903,10 +909,14 @@ def run_ours(args):
                              "see fp64_attention and DESIGN.md"},
         # FP64 instructions per attention point: per-point passes 27 (pass 1:
         # 3 mul + 4 add + 6 fma; pass 2: 9-fma Horner, clamp, subtract, 1-Newton
-        # reciprocal, fma), grouped passes 16; 64 per clock per SM nominal
+        # reciprocal, fma), grouped passes 16, grouped with the per-position
+        # pass 1 (grid_r1_step) 14; 64 per clock per SM nominal
         "fp64_attention": {
             "bound": "fp64", "instr_per_point": fp64_attn,
-            "passes": "grouped (aligned 4-point groups share prefill_toks and batch)"
+            "passes": "grouped, per-position pass 1 (aligned 4-point groups share "
+            "prefill_toks and batch; the kv axis repeats every 128 points)"
+            if fp64_attn == FP64_PER_ATTN_POINT_PERIODIC else
+            "grouped (aligned 4-point groups share prefill_toks and batch)"
             if fp64_attn == FP64_PER_ATTN_POINT_GROUPED else "per-point",
             "achieved": n_sig[ATTN] * n_pts[ATTN] * fp64_attn
             / (fit_ms[ATTN] / fit_steps / 1e3) / 1e12,

@@ -783,6 +783,49 @@ __device__ __forceinline__ void grid_g1_step(const double4& yv, const double4& f
   acc[9] = fma(u2, s1, acc[9]);
 }
 
+// Pass 1 when a lane also sees the same four f3 values at every step (f3p128):
+// f3 leaves the per-point work entirely.  Per lane position j the step sums
+// T_j = sum y, U1_j = sum u1 y, U2_j = sum u2 y (3 FP64 per point), and the
+// three moments quadratic in (u1, u2) take the group sum S0 (3 + 3 + 3 per
+// group): 5.25 FP64 per point instead of 7.25.  grid_r1_fold forms the ten
+// moments from them with the lane's f3 quad once per signature.
+struct GridR1 {
+  double T[4], U1[4], U2[4], Q[3];
+};
+
+__device__ __forceinline__ void grid_r1_step(const double4& yv, double u1, double u2, GridR1& r) {
+  const double yy[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    r.T[j] += yy[j];
+    r.U1[j] = fma(u1, yy[j], r.U1[j]);
+    r.U2[j] = fma(u2, yy[j], r.U2[j]);
+  }
+  const double s0 = (yy[0] + yy[1]) + (yy[2] + yy[3]);
+  r.Q[0] = fma(u1 * u1, s0, r.Q[0]);
+  r.Q[1] = fma(u2 * u2, s0, r.Q[1]);
+  r.Q[2] = fma(u1 * u2, s0, r.Q[2]);
+}
+
+__device__ __forceinline__ void grid_r1_fold(const GridR1& r, const double4& f3, double* acc) {
+  const double ff[4] = {f3.x, f3.y, f3.z, f3.w};
+  acc[0] = (r.T[0] + r.T[1]) + (r.T[2] + r.T[3]);
+  acc[1] = (r.U1[0] + r.U1[1]) + (r.U1[2] + r.U1[3]);
+  acc[2] = (r.U2[0] + r.U2[1]) + (r.U2[2] + r.U2[3]);
+  acc[4] = r.Q[0];
+  acc[5] = r.Q[1];
+  acc[7] = r.Q[2];
+  acc[3] = acc[6] = acc[8] = acc[9] = 0.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double t3 = r.T[j] * ff[j];
+    acc[3] += t3;
+    acc[6] = fma(t3, ff[j], acc[6]);
+    acc[8] = fma(r.U1[j], ff[j], acc[8]);
+    acc[9] = fma(r.U2[j], ff[j], acc[9]);
+  }
+}
+
 __device__ __forceinline__ void grid_g2_step(const double4& yv, const double4& f3, double u1,
                                              double u2, const double* c, double& err) {
   const double t1 = fma(c[7], u2, fma(c[4], u1, c[1]));
@@ -828,6 +871,150 @@ __device__ __forceinline__ double4 g_ld_f(const double* p) {
   return v;
 }
 
+// ---- per-warp bulk-copy ring (attention, f3-periodic grouped grids).
+// ncu of the warp kernel: y latency binds it (long_scoreboard 2.75 of 7.1
+// cycles per issue, DRAM 62%, FP64 pipe 54%) because the y loads in flight
+// live in registers (8 steps x 8 registers per lane) and the register file
+// caps residency at 16 warps/SM.  Here every warp streams its OWN signatures
+// through a private NS-stage shared-memory ring filled by 1-D TMA
+// (cp.async.bulk, mbarrier complete_tx): lane 0 keeps NS chunks of CHB bytes
+// in flight without a register, the lanes read each chunk with two
+// conflict-free LDS.128 per step (the halves of a lane's 32 B swapped on
+// lanes with bit 2 set, and the lane's f3 quad permuted to match), and the
+// ring runs on across the pass and signature boundaries, so the next
+// signature's pass 1 streams in while this one is solved and emitted.  No CTA
+// barrier, no cross-warp traffic: the arithmetic is the warp kernel's
+// (grid_r1_step / grid_g2_step).  Pass 2's chunks come from L2 (pass 1
+// copies with an evict_last policy, pass 2 with evict_first).
+constexpr int kRingPts = 512;  // n_pts must be a multiple (every ring variant's chunk divides it)
+
+template <int NS, int CHB, int MINB>
+__global__ void __launch_bounds__(256, MINB) fit_grid_ring_kernel(
+    const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
+    const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
+    uint8_t* __restrict__ status, const GridOut pe) {
+  constexpr int KIND = DOOLY_KIND_ATTN, NC = 10, STEPS = CHB / 1024;
+  static_assert(CHB % 1024 == 0 && (kRingPts * 8) % CHB == 0, "chunk = whole 128-point steps");
+  extern __shared__ __align__(128) unsigned char rdyn[];
+  __shared__ double sW[NC][NC];
+  __shared__ double sinv[3];
+  __shared__ uint32_t slo[3], shi[3];
+  __shared__ __align__(8) uint64_t rbar[8][NS];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int n = (int)n_pts;
+  if (!(gf->ok && gf->grp4 && gf->f3p128 && n % kRingPts == 0)) return;  // warp kernel's case
+  for (int t = tid; t < NC * NC; t += blockDim.x) sW[t / NC][t % NC] = gf->W[t / NC][t % NC];
+  if (tid < 3) {
+    sinv[tid] = gf->inv[tid];
+    slo[tid] = gf->lo[tid];
+    shi[tid] = gf->hi[tid];
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NS; ++i)
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(g_smem(&rbar[wid][i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  unsigned char* ring = rdyn + (size_t)wid * NS * CHB;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + tid) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nch = n * 8 / CHB;  // chunks per pass
+  const int64_t per_sig = 2 * (int64_t)nch;
+  const int64_t my_sigs = warp < n_sig ? (n_sig - 1 - warp) / n_warps + 1 : 0;
+  const int64_t total = my_sigs * per_sig;
+  uint64_t pol_keep = 0, pol_first = 0;
+  if (lane == 0) {
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+  }
+  // lane 0's issue cursor (incremental: no 64-bit division per chunk):
+  // signature is_s, chunk is_w of its 2 nch, stage is_st; left = chunks to issue
+  int64_t is_s = warp, left = total;
+  int is_w = 0, is_st = 0;
+  auto issue = [&]() {
+    const bool p1 = is_w < nch;
+    const double* src = y + is_s * (int64_t)n + (int64_t)(p1 ? is_w : is_w - nch) * (CHB / 8);
+    uint64_t* bar = &rbar[wid][is_st];
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(g_smem(bar)), "r"(CHB)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(g_smem(ring + is_st * CHB)),
+        "l"(src), "r"(CHB), "r"(g_smem(bar)), "l"(p1 ? pol_keep : pol_first)
+        : "memory");
+    if (++is_w == 2 * nch) {
+      is_w = 0;
+      is_s += n_warps;
+    }
+    is_st = is_st + 1 == NS ? 0 : is_st + 1;
+    --left;
+  };
+  if (lane == 0)
+    for (int i = 0; i < NS && left > 0; ++i) issue();
+  const int h = (lane >> 2) & 1;  // bank swizzle of the two 16-B halves
+  const double4 f3 = g_ld_f(fpl + 2 * n + 4 * lane);
+  const double4 f3q = h ? make_double4(f3.z, f3.w, f3.x, f3.y) : f3;
+  const double2* gpl = reinterpret_cast<const double2*>(fpl + 3 * n);
+  // consume cursor: stage c_st, its phase parity c_ph
+  int c_st = 0;
+  uint32_t c_ph = 0;
+  // chunk w of the current pass: wait for it, evaluate its STEPS steps,
+  // release the stage to the chunk NS ahead
+  auto consume = [&](int w, auto&& step) {
+    g_wait(&rbar[wid][c_st], c_ph);
+    const unsigned char* base = ring + c_st * CHB + 32 * lane;
+#pragma unroll
+    for (int t = 0; t < STEPS; ++t) {
+      const double2 a = *reinterpret_cast<const double2*>(base + 1024 * t + 16 * h);
+      const double2 b = *reinterpret_cast<const double2*>(base + 1024 * t + 16 * (1 - h));
+      const double2 u = __ldg(gpl + ((w * (CHB / 8) + 128 * t + 4 * lane) >> 2));
+      step(make_double4(a.x, a.y, b.x, b.y), u);
+    }
+    __syncwarp();  // every lane's reads of the stage precede the refill
+    if (lane == 0 && left > 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue();
+    }
+    if (++c_st == NS) {
+      c_st = 0;
+      c_ph ^= 1u;
+    }
+  };
+  for (int64_t si = 0; si < my_sigs; ++si) {
+    const int64_t s = warp + si * n_warps;
+    GridR1 r1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r1.T[j] = r1.U1[j] = r1.U2[j] = 0.0;
+    r1.Q[0] = r1.Q[1] = r1.Q[2] = 0.0;
+    for (int w = 0; w < nch; ++w)
+      consume(w, [&](const double4& yv, const double2& u) { grid_r1_step(yv, u.x, u.y, r1); });
+    double c[NC];
+    {
+      double acc[NC];
+      grid_r1_fold(r1, f3q, acc);
+#pragma unroll
+      for (int i = 0; i < NC; ++i) acc[i] = g_warp_sum(acc[i]);
+      double cj = 0.0;
+      if (lane < NC) {
+#pragma unroll
+        for (int i = 0; i < NC; ++i) cj = fma(sW[lane][i], acc[i], cj);
+      }
+#pragma unroll
+      for (int i = 0; i < NC; ++i) c[i] = __shfl_sync(0xFFFFFFFFu, cj, i);
+    }
+    double err = 0.0;
+    for (int w = 0; w < nch; ++w)
+      consume(w, [&](const double4& yv, const double2& u) {
+        grid_g2_step(yv, f3q, u.x, u.y, c, err);
+      });
+    err = g_warp_sum(err);
+    if (lane == 0)
+      emit_row<KIND>(pe, gf, table, fit_err, status, s, make_row<KIND>(c, sinv, slo, shi),
+                     err / (double)n, DOOLY_FIT_OK);
+  }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
@@ -835,6 +1022,10 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     uint8_t* __restrict__ status, const GridOut pe, int allow_factor) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC;
+  // allow_factor & 4: fit_grid_ring_kernel took the f3-periodic grouped grid
+  if (KIND == DOOLY_KIND_ATTN && (allow_factor & 4) && gf->ok && gf->grp4 && gf->f3p128 &&
+      n_pts % kRingPts == 0)
+    return;
 
   __shared__ double sW[NC][NC];
   __shared__ double sinv[P];
@@ -972,10 +1163,32 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
         }
         for (; p < n; p += 128) fstep(g_ld_y(ys + p, true), p);
       };
-      if (f3reg)
+      if (f3reg && (allow_factor & 3) >= 2) {
+        // f3 fixed per lane position: per-position sums, f3 folded in once
+        GridR1 r1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r1.T[j] = r1.U1[j] = r1.U2[j] = 0.0;
+        r1.Q[0] = r1.Q[1] = r1.Q[2] = 0.0;
+        auto rstep = [&](const double4& yv, int pp) {
+          const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
+          grid_r1_step(yv, u.x, u.y, r1);
+        };
+        int p = 4 * lane;
+        constexpr int YS = 8;
+        for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
+          double4 yv[YS];
+#pragma unroll
+          for (int t = 0; t < YS; ++t) yv[t] = g_ld_y(ys + p + 128 * t, true);
+#pragma unroll
+          for (int t = 0; t < YS; ++t) rstep(yv[t], p + 128 * t);
+        }
+        for (; p < n; p += 128) rstep(g_ld_y(ys + p, true), p);
+        grid_r1_fold(r1, f3l, acc);
+      } else if (f3reg) {
         pass1([&](int) { return f3l; });
-      else
+      } else {
         pass1([&](int pp) { return g_ld_f(fpl + 2 * n + pp); });
+      }
     } else {
       sweep(true, pass1_step);
     }
@@ -1350,8 +1563,10 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   if (n_sig == 0) return cudaSuccess;
   // "db" (default for affine) | "warp" (default for attention) | "ws"/"ws8"/"ws3" | "stage" | "plain"
   const char* which = getenv("DOOLY_FIT_GRID_KERNEL");
-  const char* fac = getenv("DOOLY_FIT_GRID_FACTOR");   // "0": per-point attention passes
-  const int allow_factor = fac == nullptr || fac[0] != '0';
+  // "0": per-point attention passes; "1": grouped passes without the
+  // per-position pass 1 (grid_r1_step) on f3-periodic grids
+  const char* fac = getenv("DOOLY_FIT_GRID_FACTOR");
+  const int allow_factor = fac == nullptr ? 2 : fac[0] == '0' ? 0 : fac[0] == '1' ? 1 : 2;
   const bool aligned = n_pts < (1ll << 30) && (uintptr_t)y % 32 == 0 && (uintptr_t)ws % 32 == 0;
   // warps in flight x row bytes must stay well inside L2 so pass 2 re-reads hit
   const int warps_per_sm =
@@ -1393,10 +1608,34 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
     *launches += 1;
     return cudaGetLastError();
   }
-  const bool want_warp = which == nullptr || which[0] == 'w' || which[0] == 'd';
+  // per-warp bulk-copy ring for f3-periodic grouped grids (the grid's
+  // properties are known on the device only: the ring kernel returns at once
+  // on other grids and the warp kernel, launched after it, skips the ring's case)
+  const bool want_ring = which != nullptr && strncmp(which, "ring", 4) == 0;
+  int ring_flag = 0;
+  if (KIND == DOOLY_KIND_ATTN && want_ring && allow_factor == 2 && aligned &&
+      n_pts % kRingPts == 0) {
+    // "ring": 3 x 4 KB stages, 2 CTAs/SM; "ring6": 6 x 2 KB; "ring2": 2 x 4 KB, 3 CTAs/SM
+    const int v = strcmp(which, "ring6") == 0 ? 1 : strcmp(which, "ring2") == 0 ? 2 : 0;
+    auto kern = v == 1 ? fit_grid_ring_kernel<6, 2048, 2>
+              : v == 2 ? fit_grid_ring_kernel<2, 4096, 3> : fit_grid_ring_kernel<3, 4096, 2>;
+    const int per_sm = v == 2 ? 3 : 2;
+    const size_t smem = (size_t)8 * (v == 1 ? 6 * 2048 : v == 2 ? 2 * 4096 : 3 * 4096);
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    const int64_t blocks = std::min<int64_t>((int64_t)n_sm * per_sm, (n_sig + 7) / 8);
+    kern<<<(unsigned)blocks, 256, smem, stream>>>(fpl, n_pts, y, n_sig, gf, table, fit_err,
+                                                  status, pe);
+    *launches += 1;
+    e2 = cudaGetLastError();
+    if (e2 != cudaSuccess) return e2;
+    ring_flag = 4;
+  }
+  const bool want_warp = which == nullptr || which[0] == 'w' || which[0] == 'd' || want_ring;
   if (want_warp && n_pts % 4 == 0 && aligned) {
     fit_grid_warp_kernel<KIND><<<(unsigned)warp_blocks, 256, 0, stream>>>(
-        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, allow_factor);
+        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, allow_factor | ring_flag);
     *launches += 1;
     return cudaGetLastError();
   }

@@ -617,66 +617,6 @@ __device__ __forceinline__ void pair_tile(int64_t tile, const double* __restrict
   }
   double res[QPP / 2];
   uint32_t ebits = 0, cbits = 0;
-#ifdef PAIR_SPLIT
-  // experiment: rows split into a 64-B-aligned table of sectors 0-1 and a
-  // 32-B table of sector 2 (header padded to 128 B), so each lane pair's
-  // same-row load never straddles a line: 2 row requests per query
-  const double* r64 = rows + 4;                        // table + 128 B
-  const double* r32 = r64 + 8 * n_sig;
-  const double* hdr = rows - PAIR_STRIDE_D;            // the header: a safe dummy row
-#pragma unroll
-  for (int j = 0; j < QPP; j += 2) {
-    const uint32_t sa = sv[j], sb = sv[j + 1];
-    const bool va = sa < (uint64_t)n_sig, vb = sb < (uint64_t)n_sig;
-    const double* a64 = va ? r64 + 8 * (int64_t)sa : hdr;
-    const double* b64 = vb ? r64 + 8 * (int64_t)sb : hdr;
-    const double* a32 = va ? r32 + 4 * (int64_t)sa : hdr;
-    const double* b32 = vb ? r32 + 4 * (int64_t)sb : hdr;
-    double w1[4], w2[4], w3[4];
-    ld_row_256(B ? a64 + 4 : a64, w1[0], w1[1], w1[2], w1[3]);   // A s0(j)   | B s1(j)
-    ld_row_256(B ? b64 + 4 : b64, w2[0], w2[1], w2[2], w2[3]);   // A s0(j+1) | B s1(j+1)
-    ld_row_256(B ? b32 : a32, w3[0], w3[1], w3[2], w3[3]);       // A s2(j)   | B s2(j+1)
-    const uint32_t a0 = x0[j], a1 = x1[j], a2 = x2[j];
-    const uint32_t b0 = x0[j + 1], b1 = x1[j + 1], b2 = x2[j + 1];
-    const double u1 = u2d(B ? a1 : a0), v1 = u2d(B ? a2 : a1);
-    const double u2 = u2d(B ? b1 : b0), v2 = u2d(B ? b2 : b1);
-    const double u3 = u2d(B ? b2 : a2), v3 = u2d(B ? b0 : a0);
-    const double S1 = sector_sum(B ? 0.0 : w1[0], w1[1], w1[2], w1[3], u1, v1);
-    const double S2 = sector_sum(B ? 0.0 : w2[0], w2[1], w2[2], w2[3], u2, v2);
-    const double S3 = sector_sum(0.0, w3[1], w3[2], w3[3], u3, v3);
-    // A needs s1(j) = B's S1; B needs s0(j+1) = A's S2
-    const double got = __shfl_xor_sync(0xFFFFFFFFu, B ? S1 : S2, 1);
-    const double sum = B ? add(add(got, S2), S3) : add(add(S1, got), S3);
-    // box: each lane's S3 sector holds its own query's hi_bits; B holds both
-    // queries' lo_bits (w1[0] for j, w2[0] for j+1) and reports j's to A
-    const uint64_t hib = (uint64_t)__double_as_longlong(w3[0]);
-    const uint64_t lja = (uint64_t)__double_as_longlong(w1[0]);
-    const uint64_t ljb = (uint64_t)__double_as_longlong(w2[0]);
-    const uint32_t la0 = (uint32_t)(lja & pk.m0), la1 = (uint32_t)((lja >> pk.s1) & pk.m1),
-                   la2 = (uint32_t)((lja >> pk.s2) & pk.m2);
-    const uint32_t lb0 = (uint32_t)(ljb & pk.m0), lb1 = (uint32_t)((ljb >> pk.s1) & pk.m1),
-                   lb2 = (uint32_t)((ljb >> pk.s2) & pk.m2);
-    const bool below_a = (a0 < la0) | (a1 < la1) | (a2 < la2);
-    const bool below_b = (b0 < lb0) | (b1 < lb1) | (b2 < lb2);
-    const uint32_t lo0a = __shfl_xor_sync(0xFFFFFFFFu, la0, 1);
-    const uint32_t bel = __ballot_sync(0xFFFFFFFFu, below_a);
-    const bool below = B ? below_b : ((bel >> (lane ^ 1)) & 1u) != 0;
-    const uint32_t lo0 = B ? lb0 : lo0a;
-    const uint32_t h0 = (uint32_t)(hib & pk.m0), h1 = (uint32_t)((hib >> pk.s1) & pk.m1),
-                   h2 = (uint32_t)((hib >> pk.s2) & pk.m2);
-    const uint32_t m0 = B ? b0 : a0, m1 = B ? b1 : a1, m2 = B ? b2 : a2;  // my query
-    const bool above = (m0 > h0) | (m1 > h1) | (m2 > h2);
-    const uint32_t my_sig = B ? sb : sa;
-    const bool valid = live && my_sig < (uint64_t)n_sig && lo0 <= h0;
-    bool cl = false;
-    const double pv = clamp_floor(sum, cl);
-    const int jm = j + (B ? 1 : 0);
-    res[j >> 1] = valid ? pv : nan64();
-    ebits |= (uint32_t)(valid && (below || above)) << jm;
-    cbits |= (uint32_t)(valid && cl) << jm;
-    if (live && !valid && qp + jm < bad_min) bad_min = qp + jm;
-  }
-#else
 #pragma unroll
   for (int j = 0; j < QPP; j += 2) {
     const uint32_t sa = sv[j], sb = sv[j + 1];
@@ -726,7 +666,6 @@ __device__ __forceinline__ void pair_tile(int64_t tile, const double* __restrict
     cbits |= (uint32_t)(valid && cl) << jm;
     if (live && !valid && qp + jm < bad_min) bad_min = qp + jm;
   }
-#endif
   // regroup: A holds the even queries, B the odd ones -> A the first half, B the second
   if constexpr (QPP == 8) {
     const double g1 = __shfl_xor_sync(0xFFFFFFFFu, B ? res[0] : res[2], 1);  // A<-p1, B<-p4

@@ -61,7 +61,7 @@ def _oracle(kind, x, y):
 
 @pytest.mark.parametrize("kind", [AFFINE, ATTN])
 @pytest.mark.parametrize("n_sig,n_pts", [(1, 512), (37, 512), (301, 512), (37, 510), (9, 4096), (7, 64), (5, 136), (13, 768)])
-@pytest.mark.parametrize("kernel", ["warp", "stage", "db", "ws"])
+@pytest.mark.parametrize("kernel", ["warp", "stage", "db", "ws", "ring", "ring6", "ring2"])
 def test_fit_grid_matches_oracle_and_csr(kind, n_sig, n_pts, kernel, dev, monkeypatch):
     """n_pts % 4 == 0 takes the warp-per-signature kernel, its register
     double-buffered form (db: n_pts % 256 == 0, the affine default) or the
@@ -225,3 +225,43 @@ def test_fit_grid_ws_matches_warp(factor, n_sig, dev, monkeypatch):
     assert dc.max() <= 1e-12, dc.max()
     fa, fb = out["warp"].fit_err.cpu().numpy(), out["ws"].fit_err.cpu().numpy()
     assert np.max(np.abs(fa - fb) / fa) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", ["ring", "ring6", "ring2"])
+@pytest.mark.parametrize("n_sig", [1, 149, 3001])
+def test_fit_grid_ring_matches_warp(variant, n_sig, dev, monkeypatch):
+    """The per-warp bulk-copy ring kernel (f3-periodic grouped grids) against
+    the warp kernel: same statuses, boxes and inv; coefficients within 1e-12
+    normwise and fit_err within 1e-10 relative (the order of the per-lane MAPE
+    sums differs; the contract is 1e-9); more signatures than warps x stages so every ring wraps across
+    signature boundaries, and the packed serving rows written by its epilogue
+    byte-identical to dooly_attn_pack of its own table."""
+    from paper_2605_07985_b200.sim import fit_grid, pack_attn
+
+    rng = np.random.default_rng(11 + n_sig)
+    # the C5 shape: 16 x 16 x 16 (prefill_toks, batch, kv_tokens), kv innermost
+    t = 2 ** np.arange(16)
+    bt = np.arange(1, 17) * 8
+    kv = np.linspace(0, 1 << 22, 16).astype(np.int64)
+    x = np.stack(np.meshgrid(t, bt, kv, indexing="ij")).reshape(3, -1).astype(np.uint32)
+    y = _ys(ATTN, x, n_sig, rng)
+    out = {}
+    for k in ("warp", variant):
+        monkeypatch.setenv("DOOLY_FIT_GRID_KERNEL", k)
+        out[k] = _fit_grid_gpu(ATTN, x, y, dev)
+    a = rows_to_table(ATTN, out["warp"].rows())
+    b = rows_to_table(ATTN, out[variant].rows())
+    assert torch.equal(out["warp"].status, out[variant].status)
+    assert int((out[variant].status != 0).sum().item()) == 0
+    for k in ("lo", "hi", "inv"):
+        assert np.array_equal(a[k], b[k])
+    dc = np.abs(a["coef"] - b["coef"]).max(axis=1) / np.abs(a["coef"]).max(axis=1)
+    assert dc.max() <= 1e-12, dc.max()
+    fa, fb = out["warp"].fit_err.cpu().numpy(), out[variant].fit_err.cpu().numpy()
+    assert np.max(np.abs(fa - fb) / fa) <= 1e-10
+    xt = torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).to(dev)
+    yt = torch.from_numpy(y).to(dev)
+    packed = torch.full((n_sig + 1, 96), 0xAB, dtype=torch.uint8, device=dev)
+    fr = fit_grid(ATTN, xt, yt, packed=packed)
+    torch.cuda.synchronize()
+    assert torch.equal(packed, pack_attn(fr.table))
