@@ -1019,9 +1019,13 @@ template <int KIND>
 __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
-    uint8_t* __restrict__ status, const GridOut pe, int allow_factor) {
+    uint8_t* __restrict__ status, const GridOut pe, int allow_factor, int su_groups) {
   using T = GridTraits<KIND>;
   constexpr int P = T::P, NC = T::NC;
+  // the (f1, f2) group plane staged in shared memory (su_groups > 0): the
+  // grouped passes read it with LDS instead of an L1 LDG per step, which ptxas
+  // schedules next to its use instead of hoisting it beside the y loads
+  extern __shared__ double2 gsu[];
   // allow_factor & 4: fit_grid_ring_kernel took the f3-periodic grouped grid
   if (KIND == DOOLY_KIND_ATTN && (allow_factor & 4) && gf->ok && gf->grp4 && gf->f3p128 &&
       n_pts % kRingPts == 0)
@@ -1038,9 +1042,15 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     shi[tid] = gf->hi[tid];
   }
   const bool ok = gf->ok != 0;
-  const bool factored = KIND == DOOLY_KIND_ATTN && allow_factor && gf->grp4 != 0;
+  const bool factored = KIND == DOOLY_KIND_ATTN && (allow_factor & 3) && gf->grp4 != 0;
   const bool f3reg = factored && gf->f3p128 != 0;
   __syncthreads();
+  const bool su = factored && su_groups > 0;
+  if (su) {
+    const double2* g2 = reinterpret_cast<const double2*>(fpl + 3 * n_pts);
+    for (int g = tid; g < su_groups; g += blockDim.x) gsu[g] = g2[g];
+    __syncthreads();
+  }
   double inv[P], nb[P];
 #pragma unroll
   for (int k = 0; k < P; ++k) inv[k] = sinv[k], nb[k] = -4503599627370496.0 * sinv[k];
@@ -1165,25 +1175,33 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
       };
       if (f3reg && (allow_factor & 3) >= 2) {
         // f3 fixed per lane position: per-position sums, f3 folded in once
-        GridR1 r1;
+        auto run_r1 = [&](auto uof) {
+          GridR1 r1;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) r1.T[j] = r1.U1[j] = r1.U2[j] = 0.0;
-        r1.Q[0] = r1.Q[1] = r1.Q[2] = 0.0;
-        auto rstep = [&](const double4& yv, int pp) {
-          const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
-          grid_r1_step(yv, u.x, u.y, r1);
+          for (int j = 0; j < 4; ++j) r1.T[j] = r1.U1[j] = r1.U2[j] = 0.0;
+          r1.Q[0] = r1.Q[1] = r1.Q[2] = 0.0;
+          auto rstep = [&](const double4& yv, int pp) {
+            const double2 u = uof(pp);
+            grid_r1_step(yv, u.x, u.y, r1);
+          };
+          int p = 4 * lane;
+          constexpr int YS = 8;
+          for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
+            double4 yv[YS];
+#pragma unroll
+            for (int t = 0; t < YS; ++t) yv[t] = g_ld_y(ys + p + 128 * t, true);
+#pragma unroll
+            for (int t = 0; t < YS; ++t) rstep(yv[t], p + 128 * t);
+          }
+          for (; p < n; p += 128) rstep(g_ld_y(ys + p, true), p);
+          grid_r1_fold(r1, f3l, acc);
         };
-        int p = 4 * lane;
-        constexpr int YS = 8;
-        for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
-          double4 yv[YS];
-#pragma unroll
-          for (int t = 0; t < YS; ++t) yv[t] = g_ld_y(ys + p + 128 * t, true);
-#pragma unroll
-          for (int t = 0; t < YS; ++t) rstep(yv[t], p + 128 * t);
-        }
-        for (; p < n; p += 128) rstep(g_ld_y(ys + p, true), p);
-        grid_r1_fold(r1, f3l, acc);
+        if (su)
+          run_r1([&](int pp) { return gsu[pp >> 2]; });
+        else
+          run_r1([&](int pp) {
+            return __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
+          });
       } else if (f3reg) {
         pass1([&](int) { return f3l; });
       } else {
@@ -1205,9 +1223,9 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     // ---- pass 2: training MAPE, the row re-read from L2
     if (factored) {
       // per group: p = A + f3 (B + c6 f3) with A, B the group's f1/f2 terms
-      auto pass2 = [&](auto f3of) {
+      auto pass2 = [&](auto f3of, auto uof) {
         auto fstep2 = [&](const double4& yv, int pp) {
-          const double2 u = __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
+          const double2 u = uof(pp);
           grid_g2_step(yv, f3of(pp), u.x, u.y, c, err);
         };
         int p = 4 * lane;
@@ -1221,10 +1239,15 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
         }
         for (; p < n; p += 128) fstep2(g_ld_y(ys + p, false), p);
       };
-      if (f3reg)
-        pass2([&](int) { return f3l; });
+      auto ug = [&](int pp) {
+        return __ldg(reinterpret_cast<const double2*>(fpl + 3 * n) + (pp >> 2));
+      };
+      if (f3reg && su)
+        pass2([&](int) { return f3l; }, [&](int pp) { return gsu[pp >> 2]; });
+      else if (f3reg)
+        pass2([&](int) { return f3l; }, ug);
       else
-        pass2([&](int pp) { return g_ld_f(fpl + 2 * n + pp); });
+        pass2([&](int pp) { return g_ld_f(fpl + 2 * n + pp); }, ug);
     } else {
       sweep(false, pass2_step);
     }
@@ -1580,7 +1603,7 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   if (want_db && aligned && n_pts % 256 == 0) {
     auto kern = n_pts % 512 == 0 ? fit_grid_db_kernel<KIND, 4> : fit_grid_db_kernel<KIND, 2>;
     kern<<<(unsigned)warp_blocks, 256, 0, stream>>>(fpl, n_pts, y, n_sig, gf, table, fit_err,
-                                                    status, pe, allow_factor);
+                                                    status, pe, allow_factor & 3);
     *launches += 1;
     return cudaGetLastError();
   }
@@ -1604,7 +1627,7 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
     if (e2 != cudaSuccess) return e2;
     const int64_t blocks = std::min<int64_t>(n_sm, std::max<int64_t>(1, n_sig));
     kern<<<(unsigned)blocks, 32 + wsg * wsw * 32, smem, stream>>>(
-        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, allow_factor, n_stage);
+        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, allow_factor & 3, n_stage);
     *launches += 1;
     return cudaGetLastError();
   }
@@ -1613,7 +1636,7 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   // on other grids and the warp kernel, launched after it, skips the ring's case)
   const bool want_ring = which != nullptr && strncmp(which, "ring", 4) == 0;
   int ring_flag = 0;
-  if (KIND == DOOLY_KIND_ATTN && want_ring && allow_factor == 2 && aligned &&
+  if (KIND == DOOLY_KIND_ATTN && want_ring && (allow_factor & 3) == 2 && aligned &&
       n_pts % kRingPts == 0) {
     // "ring": 3 x 4 KB stages, 2 CTAs/SM; "ring6": 6 x 2 KB; "ring2": 2 x 4 KB, 3 CTAs/SM
     const int v = strcmp(which, "ring6") == 0 ? 1 : strcmp(which, "ring2") == 0 ? 2 : 0;
@@ -1634,8 +1657,11 @@ static cudaError_t launch_grid_kind(const uint32_t* x, int64_t n_pts, const doub
   }
   const bool want_warp = which == nullptr || which[0] == 'w' || which[0] == 'd' || want_ring;
   if (want_warp && n_pts % 4 == 0 && aligned) {
-    fit_grid_warp_kernel<KIND><<<(unsigned)warp_blocks, 256, 0, stream>>>(
-        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, allow_factor | ring_flag);
+    // attention: the group plane in shared memory when it is small (C5: 16 KB)
+    const int su_groups = KIND == DOOLY_KIND_ATTN && getenv("DOOLY_FIT_GRID_SU0") == nullptr &&
+                                  n_pts <= 8192 ? (int)(n_pts / 4) : 0;
+    fit_grid_warp_kernel<KIND><<<(unsigned)warp_blocks, 256, (size_t)su_groups * 16, stream>>>(
+        fpl, n_pts, y, n_sig, gf, table, fit_err, status, pe, allow_factor | ring_flag, su_groups);
     *launches += 1;
     return cudaGetLastError();
   }
