@@ -32,6 +32,7 @@ constexpr int SIM_WARPS = 4;
 #ifndef SIM_WIN
 #define SIM_WIN 1  // decode-window iterations per lane (window <= 32 * SIM_WIN); 2: C1 -13%, C4 +3%
 #endif
+static_assert(SIM_WIN <= 2, "s_sum holds 64 iteration latencies per warp");
 
 // The op list staged in shared memory: regressor rows, and the per-entry
 // fields (feature, repeat, window slot, comm bytes per token) so that lanes
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     uint32_t* __restrict__ log_feat, double* __restrict__ log_lat, int64_t log_cap) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ StagedOps s_ops;
+  __shared__ __align__(16) double s_sum[SIM_WARPS][64];  // per-entry products of an iteration
   stage_ops(ops, aff_t, attn_t, &s_ops, threadIdx.x, blockDim.x);
   __syncthreads();
 
@@ -308,20 +310,17 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
               break;
             }
             const double next_arr = __shfl_sync(0xFFFFFFFFu, win_arr, 0);
-            int weff = 0;
+            // iteration latencies in order through shared memory (broadcast loads)
+            double* sw = s_sum[wid];
 #pragma unroll
-            for (int k = 0; k < SIM_WIN; ++k) {
-              bool stop = false;
-              for (int l = 0; l < 32; ++l) {
-                const int u = 32 * k + l;
-                if (u >= wmax || (!hard && u > 0 && arrive < n && next_arr <= clock)) {
-                  stop = true;  // arrival due (admit it) or the window is used up
-                  break;
-                }
-                clock = add(clock, __shfl_sync(0xFFFFFFFFu, lat_k[k], l));
-                ++weff;
-              }
-              if (stop) break;
+            for (int k = 0; k < SIM_WIN; ++k) sw[32 * k + lane] = lat_k[k];
+            __syncwarp();
+            int weff = 0;
+            for (int u = 0; u < 32 * SIM_WIN; ++u) {
+              if (u >= wmax || (!hard && u > 0 && arrive < n && next_arr <= clock))
+                break;  // arrival due (admit it) or the window is used up
+              clock = add(clock, sw[u]);
+              ++weff;
             }
             if (log_feat != nullptr) {
 #pragma unroll
@@ -440,16 +439,23 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       if (lane + 32 < ops.n_ops)
         w1 = mul(s_ops.rep[lane + 32],
                  entry_value(ops, &s_ops, lane + 32, num_toks, prefill, batch, kvs, kvw, bad));
+      // the products go through shared memory: every lane then reads them in
+      // op-list order two at a time (broadcast LDS.128), so the in-order sum
+      // costs one load per two adds instead of two 32-bit shuffles and a select
+      // per entry
+      double* sw = s_sum[wid];
+      sw[lane] = w0;
+      sw[lane + 32] = w1;
+      __syncwarp();
       double lat = 0.0;
       int e = 0;
-      for (; e + 4 <= ops.n_ops; e += 4) {
-        double t[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) t[u] = __shfl_sync(0xFFFFFFFFu, e + u < 32 ? w0 : w1, (e + u) & 31);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) lat = add(lat, t[u]);
+#pragma unroll 4
+      for (; e + 2 <= ops.n_ops; e += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(sw + e);
+        lat = add(lat, v.x);
+        lat = add(lat, v.y);
       }
-      for (; e < ops.n_ops; ++e) lat = add(lat, __shfl_sync(0xFFFFFFFFu, e < 32 ? w0 : w1, e & 31));
+      if (e < ops.n_ops) lat = add(lat, sw[e]);
       if (__any_sync(0xFFFFFFFFu, bad)) {
         status = DOOLY_ERR_UNKNOWN_SIGNATURE;
         break;
