@@ -31,7 +31,13 @@ cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off,
                                   const uint8_t* sym_bytes, const int64_t* sym_off,
                                   const uint8_t* attr_digests, uint8_t* out, cudaStream_t stream,
                                   int n_sm, int64_t* launches,
-                                  const dooly_digest_peers* peers = nullptr);
+                                  const dooly_digest_peers* peers = nullptr,
+                                  const RecGroup* group = nullptr);
+RecGroup rec_group_carve(void* ws, int64_t n, int64_t n_db);
+cudaError_t launch_rec_group(const uint32_t* words, const int64_t* rec_off, int64_t n, void* ws,
+                             int64_t n_db, cudaStream_t stream, int n_sm, int64_t* launches);
+cudaError_t launch_digest_copy(const uint32_t* rep, int64_t n, uint8_t* digests,
+                               cudaStream_t stream, int n_sm, int64_t* launches);
 cudaError_t launch_peer_sync(int n_peers, uint32_t* const* peer_flags, uint32_t* flag,
                              uint32_t target, int32_t* timed_out, cudaStream_t stream,
                              int64_t* launches, int slot);
@@ -550,8 +556,33 @@ int dooly_dedup(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off, i
                 int64_t n_db, uint8_t* out_digest, int64_t* out_first, uint32_t* out_uid,
                 uint8_t* out_is_new, uint8_t* out_in_db, int64_t* out_n_unique,
                 void* workspace, size_t workspace_bytes, void* stream) {
-  int rc = dooly_sha256_records(ctx, words, rec_off, n, op_bytes, op_off, n_ops, sym_bytes,
-                                sym_off, n_sym, attr_digests, n_attr, out_digest, stream);
+  if (!ctx) return DOOLY_ERR_INVALID_ARG;
+  // Record grouping (dedup.cu): SHA-256 once per distinct packed content, the
+  // other records copy their representative's digest.  DOOLY_DEDUP_GROUP=0
+  // hashes every record.  Argument errors fall through to the checked calls.
+  const char* gv = getenv("DOOLY_DEDUP_GROUP");
+  const bool group = (gv == nullptr || gv[0] != '0') && n > 0 && n_db >= 0 &&
+                     n + n_db < (int64_t)0xFFFFFFFF && words && rec_off && op_bytes && op_off &&
+                     out_digest && workspace &&
+                     workspace_bytes >= dooly::dedup_workspace_size(n, n_db);
+  int rc;
+  if (group) {
+    DeviceGuard g(ctx->device, __func__);
+    const cudaStream_t st = (cudaStream_t)stream;
+    const dooly::RecGroup rg = dooly::rec_group_carve(workspace, n, n_db);
+    cudaError_t e = dooly::launch_rec_group(words, rec_off, n, workspace, n_db, st, ctx->n_sm,
+                                            &ctx->launches);
+    if (e == cudaSuccess)
+      e = dooly::launch_sha256_records(words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off,
+                                       attr_digests, out_digest, st, ctx->n_sm, &ctx->launches,
+                                       nullptr, &rg);
+    if (e == cudaSuccess)
+      e = dooly::launch_digest_copy(rg.rep, n, out_digest, st, ctx->n_sm, &ctx->launches);
+    rc = check_cuda(ctx, e, "dedup: record grouping + sha256");
+  } else {
+    rc = dooly_sha256_records(ctx, words, rec_off, n, op_bytes, op_off, n_ops, sym_bytes,
+                              sym_off, n_sym, attr_digests, n_attr, out_digest, stream);
+  }
   if (rc) return rc;
   return dooly_dedup_digests(ctx, out_digest, n, db_digests, n_db, out_first, out_uid,
                              out_is_new, out_in_db, out_n_unique, workspace, workspace_bytes,

@@ -169,4 +169,12 @@ __device__ __forceinline__ double clamp_floor(double p, bool& clamped) {
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
 
+// Record grouping ahead of SHA-256 (dedup.cu): per record its representative
+// (a record with identical packed content), the representatives' list and count.
+struct RecGroup {
+  uint32_t* rep;
+  uint32_t* list;
+  uint32_t* count;
+};
+
 }  // namespace dooly

@@ -244,6 +244,134 @@ __global__ void __launch_bounds__(DEDUP_THREADS) dedup_firsts_kernel(
     if (first_flag[i]) out_firsts[rank[i]] = gidx[i];
 }
 
+// ---- record grouping ahead of SHA-256 (dooly_dedup): records whose packed
+// content is identical apart from the repeat count (w3, not part of the
+// canonical message, include/dooly_b200.h) have identical canonical bytes and
+// therefore identical digests, so SHA-256 runs once per distinct content and
+// the other records copy the representative's digest.  Exactness never rests
+// on the 64-bit content hash: a slot stores a record index (claimed by CAS)
+// and equality is decided by comparing the two records word by word.  Equal
+// packed content is sufficient, not necessary, for equal digests; the digest
+// dedup that follows still decides first occurrences over all records.
+// The workspace is the digest dedup's own (slots, slot_of, rank, mark),
+// consumed here before dooly_dedup_digests re-initialises it.
+__device__ __forceinline__ uint64_t grp_mix(uint64_t h, uint32_t w) {
+  return (h ^ w) * 0x100000001b3ull;
+}
+__device__ __forceinline__ uint64_t grp_fmix(uint64_t h) {
+  h ^= h >> 33;
+  h *= 0xff51afd7ed558ccdull;
+  h ^= h >> 33;
+  h *= 0xc4ceb9fe1a85ec53ull;
+  return h ^ (h >> 33);
+}
+
+// Record length in words from its header: 4 + 3 n_dims + n_sym.
+__device__ __forceinline__ uint32_t grp_len(const uint32_t* r) {
+  const uint32_t w1 = __ldg(r + 1);
+  return 4u + 3u * (w1 & 0xFFFFu) + (w1 >> 16);
+}
+
+// One thread per record.  Every load of a probe is independent of the
+// others (no early exit inside the word loops), so a record costs a few
+// memory round trips: its offset, its words, its slot, then either the CAS or
+// the representative's offset and words.
+__global__ void __launch_bounds__(DEDUP_THREADS) rec_group_kernel(
+    const uint32_t* __restrict__ words, const int64_t* __restrict__ rec_off, int64_t n,
+    uint32_t* slots, uint64_t mask, uint32_t* __restrict__ rep, uint32_t* __restrict__ list,
+    uint32_t* count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the list append below is warp-aggregated)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
+       base += stride) {
+    const int64_t i = base + lane;
+    bool is_rep = false;
+    if (i < n) {
+      const uint32_t* r = words + rec_off[i];
+      const uint32_t len = grp_len(r);
+      uint64_t h = 0xcbf29ce484222325ull ^ len;
+#pragma unroll 4
+      for (uint32_t k = 0; k < len; ++k) {
+        const uint32_t w = __ldg(r + k);
+        h = k != 3 ? grp_mix(h, w) : h;
+      }
+      h = grp_fmix(h);
+      uint64_t slot = h & mask;
+      while (true) {
+        uint32_t v = *reinterpret_cast<volatile uint32_t*>(slots + slot);
+        if (v == kEmpty) {
+          v = atomicCAS(slots + slot, kEmpty, (uint32_t)i);
+          if (v == kEmpty) {
+            rep[i] = (uint32_t)i;
+            is_rep = true;
+            break;
+          }
+        }
+        // full comparison against the slot's representative v (repeat word excluded)
+        const uint32_t* rv = words + rec_off[v];
+        uint32_t diff = grp_len(rv) ^ len;
+        if (diff == 0) {
+#pragma unroll 4
+          for (uint32_t k = 0; k < len; ++k)
+            diff |= k != 3 ? (__ldg(rv + k) ^ __ldg(r + k)) : 0u;
+        }
+        if (diff == 0) {
+          rep[i] = v;
+          break;
+        }
+        slot = (slot + 1) & mask;
+      }
+    }
+    const uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rep);
+    uint32_t at = 0;
+    if (lane == 0 && b != 0u) at = atomicAdd(count, (uint32_t)__popc(b));
+    at = __shfl_sync(0xFFFFFFFFu, at, 0);
+    if (is_rep) list[at + __popc(b & ((1u << lane) - 1u))] = (uint32_t)i;
+  }
+}
+
+__global__ void __launch_bounds__(DEDUP_THREADS) digest_copy_kernel(
+    const uint32_t* __restrict__ rep, int64_t n, uint8_t* digests) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t r = rep[i];
+    if (r != (uint32_t)i) {
+      const uint4* src = reinterpret_cast<const uint4*>(digests + (int64_t)r * 32);
+      uint4* dst = reinterpret_cast<uint4*>(digests + i * 32);
+      dst[0] = src[0];
+      dst[1] = src[1];
+    }
+  }
+}
+
+RecGroup rec_group_carve(void* ws, int64_t n, int64_t n_db) {
+  DedupWs w = carve(ws, n, n_db);
+  return RecGroup{w.slot_of, w.rank, reinterpret_cast<uint32_t*>(w.mark)};
+}
+
+cudaError_t launch_rec_group(const uint32_t* words, const int64_t* rec_off, int64_t n, void* ws,
+                             int64_t n_db, cudaStream_t stream, int n_sm, int64_t* launches) {
+  if (n == 0) return cudaSuccess;
+  DedupWs w = carve(ws, n, n_db);
+  const RecGroup g = rec_group_carve(ws, n, n_db);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(w.slots, 0xFF, w.cap * 4, stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(g.count, 0, sizeof(uint32_t), stream)) != cudaSuccess) return e;
+  rec_group_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
+      words, rec_off, n, w.slots, w.cap - 1, g.rep, g.list, g.count);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_digest_copy(const uint32_t* rep, int64_t n, uint8_t* digests,
+                               cudaStream_t stream, int n_sm, int64_t* launches) {
+  if (n == 0) return cudaSuccess;
+  digest_copy_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(rep, n, digests);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dedup_firsts(int64_t n, int64_t n_db, const int64_t* gidx, int64_t* out_firsts,
                                 void* ws, cudaStream_t stream, int n_sm, int64_t* launches) {
   if (n == 0) return cudaSuccess;

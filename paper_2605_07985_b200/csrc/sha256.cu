@@ -213,18 +213,24 @@ struct ShaStream {
   }
 };
 
+// LIST: hash only the records list[0 .. *count) (the representatives of the
+// record grouping in dooly_dedup); each digest still lands at its record's row.
+template <bool LIST>
 __global__ void __launch_bounds__(SHA_THREADS, SHA_MINB) sha256_records_kernel(
     const uint32_t* __restrict__ words, const int64_t* __restrict__ rec_off, int64_t n,
     const uint8_t* __restrict__ op_bytes, const int64_t* __restrict__ op_off,
     const uint8_t* __restrict__ sym_bytes, const int64_t* __restrict__ sym_off,
     const uint8_t* __restrict__ attr_digests, uint8_t* __restrict__ out,
-    const dooly_digest_peers pe, uint32_t one) {
+    const dooly_digest_peers pe, uint32_t one, const uint32_t* __restrict__ list,
+    const uint32_t* __restrict__ count) {
   __shared__ uint32_t s_buf[SHA_THREADS * SHA_STRIDE];
   ShaStream st;
   const int64_t stride = (int64_t)gridDim.x * SHA_THREADS;
-  for (int64_t base = (int64_t)blockIdx.x * SHA_THREADS; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    const bool valid = i < n;
+  const int64_t n_eff = LIST ? (int64_t)*count : n;
+  for (int64_t base = (int64_t)blockIdx.x * SHA_THREADS; base < n_eff; base += stride) {
+    const int64_t t = base + threadIdx.x;
+    const bool valid = t < n_eff;
+    const int64_t i = LIST ? (valid ? (int64_t)list[t] : 0) : t;
     st.init(s_buf + threadIdx.x * SHA_STRIDE);
     if (valid) {
     const uint32_t* r = words + rec_off[i];
@@ -279,13 +285,20 @@ cudaError_t launch_sha256_records(const uint32_t* words, const int64_t* rec_off,
                                   const uint8_t* op_bytes, const int64_t* op_off,
                                   const uint8_t* sym_bytes, const int64_t* sym_off,
                                   const uint8_t* attr_digests, uint8_t* out, cudaStream_t stream,
-                                  int n_sm, int64_t* launches, const dooly_digest_peers* peers) {
+                                  int n_sm, int64_t* launches, const dooly_digest_peers* peers,
+                                  const RecGroup* group) {
   if (n == 0) return cudaSuccess;
   *launches += 1;
   dooly_digest_peers pe{};
   if (peers) pe = *peers;
-  sha256_records_kernel<<<(unsigned)sha_blocks(n, n_sm), SHA_THREADS, 0, stream>>>(
-      words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off, attr_digests, out, pe, 1u);
+  if (group != nullptr)
+    sha256_records_kernel<true><<<(unsigned)sha_blocks(n, n_sm), SHA_THREADS, 0, stream>>>(
+        words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off, attr_digests, out, pe, 1u,
+        group->list, group->count);
+  else
+    sha256_records_kernel<false><<<(unsigned)sha_blocks(n, n_sm), SHA_THREADS, 0, stream>>>(
+        words, rec_off, n, op_bytes, op_off, sym_bytes, sym_off, attr_digests, out, pe, 1u,
+        nullptr, nullptr);
   return cudaGetLastError();
 }
 

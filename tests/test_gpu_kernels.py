@@ -635,6 +635,42 @@ def test_dedup_single_call_matches_two_calls(corpus, dev):
     assert one_db.n_unique == two.n_unique == one.n_unique
 
 
+@pytest.mark.parametrize("source", ["corpus", "synth"])
+@pytest.mark.parametrize("with_db", [False, True])
+def test_dedup_record_grouping_matches_ungrouped(source, with_db, corpus, dev, monkeypatch):
+    """dooly_dedup hashes each distinct packed content once (records that
+    differ only in the repeat count share a digest) and copies the digest to
+    the rest: every output equals the path that hashes every record
+    (DOOLY_DEDUP_GROUP=0), and the digests equal the standalone
+    dooly_sha256_records of every record."""
+    from paper_2605_07985_b200.profiler import DeviceRecords, dedup_packed, hash_records
+    from paper_2605_07985_b200.records import pack_entries, synthesize_entries
+    from bench import synth_records
+
+    rng = np.random.default_rng(5)
+    if source == "corpus":
+        ents = [e for m in corpus.models for b in corpus.backends for e in synthesize_entries(m, b)]
+        ents = [ents[i] for i in rng.permutation(len(ents))] * 3
+        packed = pack_entries(ents)
+        # vary the repeat count (w3, not hashed) of every record
+        packed.words[packed.rec_off[:packed.n] + 3] = rng.integers(1, 1 << 20, packed.n)
+    else:
+        packed, _ = synth_records(300_000, seed=9)
+    recs = DeviceRecords.from_packed(packed, dev)
+    db = hash_records(recs)[rng.choice(recs.n, 5, replace=False)].clone() if with_db else None
+    monkeypatch.delenv("DOOLY_DEDUP_GROUP", raising=False)
+    g = dedup_packed(recs, db)
+    monkeypatch.setenv("DOOLY_DEDUP_GROUP", "0")
+    u = dedup_packed(recs, db)
+    assert torch.equal(g.digests, u.digests)
+    assert torch.equal(g.digests, hash_records(recs))
+    for a, b in ((g.first, u.first), (g.uid, u.uid), (g.is_new, u.is_new), (g.in_db, u.in_db)):
+        assert torch.equal(a, b)
+    assert g.n_unique == u.n_unique
+    if source == "corpus":
+        assert g.n_unique < recs.n // 3
+
+
 def test_sim_non_termination(dev):
     from paper_2605_07985_b200 import _lib
     from paper_2605_07985_b200.errors import NonTermination
