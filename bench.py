@@ -1097,6 +1097,12 @@ def run_ours(args):
             if routed:
                 r = ddist.dedup_routed(recs, n_total, None, ws)
                 e1.record(stream)
+            elif not dist_on:
+                # one process: the public batch call (dooly_dedup: record grouping,
+                # SHA-256 of the representatives, digest copy, resolve)
+                r = dedup_packed(recs, workspace=ws, sync=False)
+                full = r.digests
+                e1.record(stream)
             else:
                 if pdig is not None:
                     full = pdig.hash(recs, rank * recs.n)
@@ -1104,7 +1110,7 @@ def run_ours(args):
                     hash_records(recs, dig)
                 e1.record(stream)
                 if pdig is None:
-                    full = ddist.all_gather_rows(dig, n_total) if dist_on else dig
+                    full = ddist.all_gather_rows(dig, n_total)
                 r = dedup_digests(full, None, ws, sync=False)
             e2.record(stream)
             torch.cuda.synchronize()
@@ -1115,7 +1121,7 @@ def run_ours(args):
         if pdig is not None:
             pdig.check()
         n_unique = int(r.n_unique) if routed else int(dedup_digests(full, None, ws).n_unique)
-        if routed:   # e0 -> e1 spans the whole routed dedup; time the hash alone once
+        if routed or not dist_on:   # e0 -> e1 spans the whole dedup; time the hash alone once
             e0.record(stream)
             hash_records(recs, dig)
             e1.record(stream)
