@@ -29,10 +29,6 @@
 namespace dooly {
 
 constexpr int SIM_WARPS = 4;
-#ifndef SIM_WIN
-#define SIM_WIN 1  // decode-window iterations per lane (window <= 32 * SIM_WIN); 2: C1 -13%, C4 +3%
-#endif
-static_assert(SIM_WIN <= 2, "s_sum holds 64 iteration latencies per warp");
 
 // The op list staged in shared memory: regressor rows, and the per-entry
 // fields (feature, repeat, window slot, comm bytes per token) so that lanes
@@ -152,8 +148,10 @@ struct SlotArrays {  // per-warp views into dynamic shared memory
   uint32_t* ptot;    // prompt + output tokens (its KV reservation / kv_bytes_per_token)
   double* t_first;   // first-token time
   double* arr;       // arrival time
+  uint32_t* wb;      // window scratch: KV tokens at window iteration u >= 1 are wb + u
+  uint32_t* wr;      // window scratch: iterations the slot runs from the window's start
 };
-constexpr int kSlotBytes = 40;  // 2 x f64 + 6 x u32 per running slot
+constexpr int kSlotBytes = 48;  // 2 x f64 + 8 x u32 per running slot
 
 size_t sim_workspace_size(const dooly_sched* cfg, int64_t n_req, int64_t n_shards) {
   (void)cfg;
@@ -176,7 +174,8 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     uint32_t* __restrict__ log_feat, double* __restrict__ log_lat, int64_t log_cap) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ StagedOps s_ops;
-  __shared__ __align__(16) double s_sum[SIM_WARPS][64];  // per-entry products of an iteration
+  __shared__ __align__(16) double s_sum[SIM_WARPS][64];  // per-entry products / window latencies
+  __shared__ uint32_t s_hc[SIM_WARPS][32], s_hk[SIM_WARPS][32];  // window finish histograms
   stage_ops(ops, aff_t, attn_t, &s_ops, threadIdx.x, blockDim.x);
   __syncthreads();
 
@@ -193,6 +192,8 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     sl.kv = sl.dec + MB;
     sl.out = sl.kv + MB;
     sl.ptot = sl.out + MB;
+    sl.wb = sl.ptot + MB;
+    sl.wr = sl.wb + MB;
   }
   const uint32_t W = cfg.window > 0 ? (uint32_t)cfg.window : 0u;
   const uint64_t kvb = (uint64_t)cfg.kv_bytes_per_token;
@@ -255,99 +256,6 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
         status = DOOLY_ERR_NON_TERMINATION;
         break;
       }
-      // ---- 1b. decode window (exact windowed commit).  When every
-      // running request is in decode and nothing can be admitted (no waiting
-      // request, batch full, or the FCFS head blocked by the KV cap — all of
-      // which only a finish can change), the next iterations have a fixed
-      // composition: iteration u has num_toks = batch = nrun, prefill = 0 and
-      // every request's KV one token longer per iteration.  Lane u evaluates
-      // iteration u's whole op list (same entry arithmetic, same in-order sum);
-      // the clock then commits them in order, stopping before the first
-      // iteration that starts with an arrival due, and before the first finish.
-      if (nrun > 0 && sl.left[nrun - 1] == 0) {
-        // hard: admission is blocked by the batch size or the KV cap of the FCFS
-        // head, which only a finish can lift — arrivals meanwhile just queue
-        bool hard = nrun >= MB;
-        if (!hard && admit < arrive) {
-          if (wbase != admit) ld_wait(admit);
-          const uint64_t need = (uint64_t)(__shfl_sync(0xFFFFFFFFu, w_p, 0) +
-                                           __shfl_sync(0xFFFFFFFFu, w_o, 0)) * kvb;
-          hard = reserved + need > cap;
-        }
-        const bool blocked = hard || admit == arrive;
-        if (blocked) {
-          uint32_t tf = 0xFFFFFFFFu, kv0 = 0;
-          for (int j = lane; j < nrun; j += 32) {
-            tf = min(tf, sl.out[j] - sl.dec[j]);
-            kv0 += sl.kv[j];
-          }
-          tf = __reduce_min_sync(0xFFFFFFFFu, tf);
-          kv0 = warp_sum_u32(kv0);
-          int64_t wmax = (int64_t)tf - 1;  // iterations before the first finish
-          if (wmax > 32 * SIM_WIN) wmax = 32 * SIM_WIN;
-          if (wmax > cfg.max_iterations - it) wmax = cfg.max_iterations - it;
-          if (wmax >= 2) {
-            const uint32_t nr = (uint32_t)nrun;
-            bool bad = false;
-            double lat_k[SIM_WIN];
-            uint32_t kvs_k[SIM_WIN], kvw_k[SIM_WIN];
-#pragma unroll
-            for (int k = 0; k < SIM_WIN; ++k) {  // lane evaluates iterations lane + 32k
-              const uint32_t u = (uint32_t)(lane + 32 * k);
-              kvs_k[k] = kv0 + u * nr;
-              kvw_k[k] = 0;
-              if (W && (int64_t)u < wmax)
-                for (int j = 0; j < nrun; ++j) kvw_k[k] += min(sl.kv[j] + u, W);
-              lat_k[k] = 0.0;
-              if ((int64_t)u < wmax)
-                for (int e = 0; e < ops.n_ops; ++e)
-                  lat_k[k] = add(lat_k[k], mul(s_ops.rep[e],
-                                               entry_value(ops, &s_ops, e, nr, 0u, nr, kvs_k[k],
-                                                           kvw_k[k], bad)));
-            }
-            if (__any_sync(0xFFFFFFFFu, bad)) {
-              status = DOOLY_ERR_UNKNOWN_SIGNATURE;
-              break;
-            }
-            const double next_arr = __shfl_sync(0xFFFFFFFFu, win_arr, 0);
-            // iteration latencies in order through shared memory (broadcast loads)
-            double* sw = s_sum[wid];
-#pragma unroll
-            for (int k = 0; k < SIM_WIN; ++k) sw[32 * k + lane] = lat_k[k];
-            __syncwarp();
-            int weff = 0;
-            for (int u = 0; u < 32 * SIM_WIN; ++u) {
-              if (u >= wmax || (!hard && u > 0 && arrive < n && next_arr <= clock))
-                break;  // arrival due (admit it) or the window is used up
-              clock = add(clock, sw[u]);
-              ++weff;
-            }
-            if (log_feat != nullptr) {
-#pragma unroll
-              for (int k = 0; k < SIM_WIN; ++k) {
-                const int u = lane + 32 * k;
-                if (u < weff && it + u < log_cap) {
-                  const int64_t row = shard * log_cap + it + u;
-                  uint32_t* lf = log_feat + row * DOOLY_IT_FEATS;
-                  lf[0] = nr;
-                  lf[1] = 0u;
-                  lf[2] = nr;
-                  lf[3] = kvs_k[k];
-                  lf[4] = kvw_k[k];
-                  log_lat[row] = lat_k[k];
-                }
-              }
-            }
-            it += weff;
-            for (int j = lane; j < nrun; j += 32) {
-              sl.kv[j] += (uint32_t)weff;
-              sl.dec[j] += (uint32_t)weff;
-            }
-            __syncwarp();
-            continue;
-          }
-        }
-      }
       // ---- 2. schedule (decode prefix | <=1 prefill at the tail)
       const bool has_p = nrun > 0 && sl.left[nrun - 1] > 0;
       const int n_dec = nrun - (has_p ? 1 : 0);
@@ -362,10 +270,11 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       const int nrun0 = nrun;
       uint32_t adm_pf = 0, adm_tok = 0, adm_kv = 0, adm_kvw = 0;
       int n_adm = 0;
+      bool blocked = false;       // the FCFS head does not fit the KV capacity
+      bool adm_partial = false;   // an admitted prompt keeps prefilling after this iteration
       while (admit < arrive && nrun < MB && budget > 0) {
         if (wbase != admit) ld_wait(admit);  // only after 32 admissions in one iteration
         int took = 0;  // admitted in this round (uniform after broadcast)
-        bool blocked = false;
         for (int k = 0; k < 32; ++k) {
           if (admit + k >= arrive || nrun + took >= MB || budget <= 0) break;
           const uint32_t p = __shfl_sync(0xFFFFFFFFu, w_p, k);
@@ -394,6 +303,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
           }
           adm_tok += take;
           if (work > 0) adm_pf += take;
+          if (take < work) adm_partial = true;
           adm_kv += c;
           adm_kvw += W ? min(c, W) : 0u;
           ++took;
@@ -428,7 +338,168 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       const uint32_t num_toks = (uint32_t)n_dec + take_p + adm_tok;
       const uint32_t prefill = take_p + adm_pf;
       const uint32_t batch = (uint32_t)n_dec + (take_p > 0 ? 1u : 0u) + (uint32_t)n_adm;
-      // ---- 4. fused gather-evaluate-reduce over the call graph
+      // ---- 4. window of exactly predictable iterations.  If every
+      // request still running after this iteration is decoding (the tail
+      // prefill and every admitted prompt complete now) and no admission can
+      // happen before an arrival (no request waits) or before a finish (the
+      // FCFS head is blocked by the batch or KV cap), the following iterations
+      // have a known composition: slot j runs wr_j iterations from this one,
+      // decoding with wb_j + u KV tokens at iteration u >= 1, and leaves after
+      // its last token.  Lane u evaluates iteration u's whole op list (the same
+      // entry arithmetic and in-order sum as the serial path); the clock then
+      // commits them in order, stopping before the first iteration that starts
+      // with an arrival due (no stop while the head is blocked: arrivals only
+      // queue).  Finishes inside the window are stamped with the clock of their
+      // last iteration, exactly as the event loop would.
+      bool fin_any = false;
+      uint64_t freed = 0;
+      const bool waiting = admit < arrive;
+      const bool hard = waiting && (nrun >= MB || blocked);
+      const bool p_done = !has_p || take_p == sl.left[nrun0 - 1];
+      int64_t wmax = 1;
+      uint32_t wB = 0;
+      if (p_done && !adm_partial && (!waiting || hard)) {
+        uint32_t rmax = 0, rmin = 0xFFFFFFFFu;
+        if (W == 0) {
+          s_hc[wid][lane] = 0u;
+          s_hk[wid][lane] = 0u;
+          __syncwarp();
+        }
+        for (int j = lane; j < nrun; j += 32) {
+          uint32_t b, r;
+          const uint32_t o = sl.out[j];
+          if (j < n_dec) {  // decoding: out - dec tokens to go
+            b = sl.kv[j];
+            r = o - sl.dec[j];
+          } else if (j < nrun0) {  // the tail prefill, completing in this iteration
+            b = sl.kv[j] + take_p - 1u;
+            r = o > 1u ? o : 1u;
+          } else {  // admitted now: prefill completes now (or fully cached: first decode)
+            const uint32_t c = sl.kv[j];
+            b = sl.left[j] > 0u ? c + sl.dec[j] - 1u : c;
+            r = o > 1u ? o : 1u;
+          }
+          sl.wb[j] = b;
+          sl.wr[j] = r;
+          rmax = max(rmax, r);
+          rmin = min(rmin, r);
+          wB += b;
+          if (W == 0 && r < 32u) {
+            atomicAdd(&s_hc[wid][r], 1u);
+            atomicAdd(&s_hk[wid][r], b);
+          }
+        }
+        rmax = __reduce_max_sync(0xFFFFFFFFu, rmax);
+        rmin = __reduce_min_sync(0xFFFFFFFFu, rmin);
+        wB = warp_sum_u32(wB);
+        wmax = hard ? rmin : rmax;
+        if (wmax > 32) wmax = 32;
+        if (wmax > cfg.max_iterations - it) wmax = cfg.max_iterations - it;
+        __syncwarp();
+      }
+      if (wmax >= 2) {
+        // features of iteration u (lane u); iteration 0 is the one scheduled above
+        uint32_t nt = num_toks, pf = prefill, bt = batch, ks = kvs, kw = kvw;
+        const uint32_t u = (uint32_t)lane;
+        uint32_t F = 0, K = 0;  // finished-before-u counts and KV sums (bins r <= u)
+        if (W == 0) {
+          F = s_hc[wid][lane];
+          K = s_hk[wid][lane];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t f2 = __shfl_up_sync(0xFFFFFFFFu, F, o);
+            const uint32_t k2 = __shfl_up_sync(0xFFFFFFFFu, K, o);
+            if (lane >= o) {
+              F += f2;
+              K += k2;
+            }
+          }
+        }
+        if (u > 0) {
+          uint32_t nr = 0;
+          ks = 0;
+          kw = 0;
+          if (W == 0) {
+            nr = (uint32_t)nrun - F;
+            ks = (wB - K) + u * nr;
+          } else {
+            for (int j = 0; j < nrun; ++j) {
+              const uint32_t b = sl.wb[j] + u;
+              if (sl.wr[j] > u) {
+                ++nr;
+                ks += b;
+                kw += min(b, W);
+              }
+            }
+          }
+          nt = bt = nr;
+          pf = 0;
+        }
+        bool bad = false;
+        double lat = 0.0;
+        if ((int64_t)u < wmax)
+          for (int e = 0; e < ops.n_ops; ++e)
+            lat = add(lat, mul(s_ops.rep[e], entry_value(ops, &s_ops, e, nt, pf, bt, ks, kw, bad)));
+        if (__any_sync(0xFFFFFFFFu, bad)) {
+          status = DOOLY_ERR_UNKNOWN_SIGNATURE;
+          break;
+        }
+        double* sw = s_sum[wid];
+        sw[lane] = lat;
+        __syncwarp();
+        const double next_arr = __shfl_sync(0xFFFFFFFFu, win_arr, 0);
+        int weff = 0;
+        double myclk = 0.0;
+        for (int v = 0; v < (int)wmax; ++v) {
+          if (!hard && v > 0 && arrive < n && next_arr <= clock) break;  // admit it first
+          clock = add(clock, sw[v]);
+          if (v == lane) myclk = clock;
+          ++weff;
+        }
+        __syncwarp();
+        if (log_feat != nullptr && lane < weff && it + lane < log_cap) {
+          const int64_t row = shard * log_cap + it + lane;
+          uint32_t* lf = log_feat + row * DOOLY_IT_FEATS;
+          lf[0] = nt;
+          lf[1] = pf;
+          lf[2] = bt;
+          lf[3] = ks;
+          lf[4] = kw;
+          log_lat[row] = lat;
+        }
+        it += weff;
+        const double clk0 = __shfl_sync(0xFFFFFFFFu, myclk, 0);
+        for (int j0 = 0; j0 < nrun; j0 += 32) {
+          const int j = j0 + lane;
+          const bool valid = j < nrun;
+          const uint32_t r = valid ? sl.wr[j] : 1u;
+          const uint32_t p = r < (uint32_t)weff ? r : (uint32_t)weff;  // iterations it ran
+          const double clk_last = __shfl_sync(0xFFFFFFFFu, myclk, (int)p - 1);
+          if (valid) {
+            const bool newf = j >= n_dec;  // first token in iteration 0
+            const uint32_t rq = sl.rq[j];
+            const uint32_t out_n = sl.out[j];
+            sl.kv[j] = sl.wb[j] + p;
+            sl.dec[j] = (newf ? 0u : sl.dec[j]) + p;
+            sl.left[j] = 0u;
+            double tf = 0.0;
+            if (newf) {
+              tf = clk0;
+              sl.t_first[j] = clk0;
+              ttft[base + rq] = clk0 - sl.arr[j];
+            } else {
+              tf = sl.t_first[j];
+            }
+            if (r <= (uint32_t)weff) {
+              tpot[base + rq] = out_n >= 2 ? __ddiv_rn(clk_last - tf, (double)(out_n - 1)) : nan64();
+              freed += (uint64_t)sl.ptot[j] * kvb;
+              sl.rq[j] = 0xFFFFFFFFu;  // tombstone
+              fin_any = true;
+            }
+          }
+        }
+      } else {
+      // ---- 4s. one iteration: fused gather-evaluate-reduce over the call graph
       // lanes evaluate their entries and the repeat products in parallel; the
       // in-order sum then only chains the adds (shuffles issued 4 at a time)
       bool bad = false;
@@ -473,8 +544,6 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       }
       ++it;
       // ---- 5. advance request state, stamp tokens, release finished reservations
-      bool fin_any = false;
-      uint64_t freed = 0;
       for (int j = lane; j < nrun; j += 32) {
         bool fin = false;
         const uint32_t r = sl.rq[j];
@@ -515,6 +584,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
           sl.rq[j] = 0xFFFFFFFFu;  // tombstone
           fin_any = true;
         }
+      }
       }
       if (__any_sync(0xFFFFFFFFu, fin_any)) {
 #pragma unroll
