@@ -24,11 +24,16 @@
 // iteration the running list is [decode-phase ... | at most one prefill-phase
 // request], because prefill budget is granted in running order and admission
 // stops as soon as the budget is exhausted.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace dooly {
 
-constexpr int SIM_WARPS = 4;
+#ifndef SIM_WARPS_N
+#define SIM_WARPS_N 4  // replicas (warps) per CTA
+#endif
+constexpr int SIM_WARPS = SIM_WARPS_N;
 
 // The op list staged in shared memory: regressor rows, and the per-entry
 // fields (feature, repeat, window slot, comm bytes per token) so that lanes
@@ -44,6 +49,10 @@ struct StagedOps {
   uint64_t bpt[DOOLY_MAX_OPS];
   double comm_a;    // RN(2(tp-1) / tp)
   double comm_rtp;  // RN(1 / tp) when tp is a power of two (exact scaling), else 0
+  // entries grouped by kind (op-list order within a kind) for the window's
+  // straight-line evaluation: [0, n_aff) affine, then attention, then comm
+  uint8_t kidx[DOOLY_MAX_OPS];
+  int n_aff, n_att;
 };
 
 __device__ __forceinline__ void stage_ops(const dooly_oplist& ops, const void* aff_t,
@@ -60,6 +69,16 @@ __device__ __forceinline__ void stage_ops(const dooly_oplist& ops, const void* a
       s->aff[e] = load_affine(static_cast<const dooly_affine_row*>(aff_t), ops.row[e]);
   }
   if (tid == 0) {
+    int k = 0;
+    for (int pass = 0; pass < 3; ++pass) {
+      for (int e = 0; e < ops.n_ops; ++e) {
+        const int f = ops.feat[e];
+        const int cls = f == DOOLY_FEAT_ATTN ? 1 : f == DOOLY_FEAT_COMM ? 2 : 0;
+        if (cls == pass) s->kidx[k++] = (uint8_t)e;
+      }
+      if (pass == 0) s->n_aff = k;
+      if (pass == 1) s->n_att = k - s->n_aff;
+    }
     const int tp = ops.tp > 0 ? ops.tp : 1;
     s->comm_a = __ddiv_rn((double)(2 * (tp - 1)), (double)tp);
     s->comm_rtp = (tp & (tp - 1)) == 0 ? __drcp_rn((double)tp) : 0.0;
@@ -164,6 +183,50 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
   return __reduce_add_sync(0xFFFFFFFFu, v);
 }
 
+// One iteration's latency by a single lane, entries evaluated grouped by kind
+// with no data-dependent branch inside a group (4 affine or 2 attention
+// entries per straight-line step, so their FP64 chains overlap), each repeat
+// product parked in the lane's column of pv (entry-major, 32 doubles per
+// entry), then the sum in op-list order.  Every entry value and product is
+// the same IEEE operation sequence as entry_value / the serial path.
+__device__ __forceinline__ double window_latency(const dooly_oplist& ops, const StagedOps* s,
+                                                 double* pv, int lane, uint32_t nt, uint32_t pf,
+                                                 uint32_t bt, uint32_t ks, uint32_t kw,
+                                                 bool& bad) {
+  const int na = s->n_aff, nat = s->n_att, n = ops.n_ops;
+  for (int i = 0; i < na; i += 4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = s->kidx[min(i + k, na - 1)];  // the tail repeats the last entry
+      const AffineRow& r = s->aff[e];
+      bad |= !affine_valid(r);
+      bool cl;
+      const double v = clamp_floor(eval_affine(r, s->feat[e] == DOOLY_FEAT_NUM_SEQS ? bt : nt), cl);
+      pv[e * 32 + lane] = mul(s->rep[e], v);
+    }
+  }
+  for (int i = 0; i < nat; i += 2) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int e = s->kidx[na + min(i + k, nat - 1)];
+      const AttnRow& r = s->attn[e];
+      bad |= !attn_valid(r);
+      bool cl;
+      const double v = clamp_floor(eval_attn(r, pf, bt, s->wslot[e] ? kw : ks), cl);
+      pv[e * 32 + lane] = mul(s->rep[e], v);
+    }
+  }
+  for (int i = na + nat; i < n; ++i) {
+    const int e = s->kidx[i];
+    pv[e * 32 + lane] =
+        mul(s->rep[e], comm_latency(s, ops.tp, ops.comm_alpha, ops.comm_beta, (uint64_t)nt * s->bpt[e]));
+  }
+  double lat = 0.0;
+#pragma unroll 4
+  for (int e = 0; e < n; ++e) lat = add(lat, pv[e * 32 + lane]);
+  return lat;
+}
+
 __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     const dooly_oplist ops, const dooly_sched cfg, const void* __restrict__ aff_t,
     const void* __restrict__ attn_t, const double* __restrict__ arrival,
@@ -171,7 +234,7 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     const uint32_t* __restrict__ cached, const int64_t* __restrict__ shard_off, int64_t n_shards,
     double* __restrict__ ttft, double* __restrict__ tpot, int64_t* __restrict__ n_iter_out,
     double* __restrict__ clock_out, int32_t* __restrict__ status_out,
-    uint32_t* __restrict__ log_feat, double* __restrict__ log_lat, int64_t log_cap) {
+    uint32_t* __restrict__ log_feat, double* __restrict__ log_lat, int64_t log_cap, int use_pv) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ StagedOps s_ops;
   __shared__ __align__(16) double s_sum[SIM_WARPS][64];  // per-entry products / window latencies
@@ -195,6 +258,9 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     sl.wb = sl.ptot + MB;
     sl.wr = sl.wb + MB;
   }
+  // window products (entry-major, one column per lane) after the slot arrays, if launched with room
+  double* pv_base = use_pv ? reinterpret_cast<double*>(dyn + (size_t)SIM_WARPS * MB * kSlotBytes)
+                           : nullptr;
   const uint32_t W = cfg.window > 0 ? (uint32_t)cfg.window : 0u;
   const uint64_t kvb = (uint64_t)cfg.kv_bytes_per_token;
   const uint64_t cap = (uint64_t)cfg.kv_capacity_bytes;
@@ -437,9 +503,14 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
         }
         bool bad = false;
         double lat = 0.0;
-        if ((int64_t)u < wmax)
+        if (pv_base != nullptr) {
+          lat = window_latency(ops, &s_ops, pv_base + (size_t)wid * ops.n_ops * 32, lane, nt, pf,
+                               bt, ks, kw, bad);
+          bad = bad && (int64_t)u < wmax;
+        } else if ((int64_t)u < wmax) {
           for (int e = 0; e < ops.n_ops; ++e)
             lat = add(lat, mul(s_ops.rep[e], entry_value(ops, &s_ops, e, nt, pf, bt, ks, kw, bad)));
+        }
         if (__any_sync(0xFFFFFFFFu, bad)) {
           status = DOOLY_ERR_UNKNOWN_SIGNATURE;
           break;
@@ -651,14 +722,26 @@ cudaError_t launch_sim(const dooly_oplist* ops, const dooly_sched* cfg, const vo
   (void)ws_bytes;
   (void)n_sm;
   if (n_shards == 0) return cudaSuccess;
-  const size_t smem = (size_t)SIM_WARPS * cfg->max_batch * kSlotBytes;
-  cudaError_t e = cudaFuncSetAttribute(sim_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  size_t smem = (size_t)SIM_WARPS * cfg->max_batch * kSlotBytes;
+  // the window's product columns (n_ops x 32 doubles per warp) when they fit beside the slots
+  const size_t pv = (size_t)SIM_WARPS * ops->n_ops * 32 * sizeof(double);
+  int dev = 0, optin = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, sim_run_kernel);
+  if (e != cudaSuccess) return e;
+  const int use_pv = getenv("DOOLY_SIM_PV0") == nullptr &&
+                     smem + pv + fa.sharedSizeBytes <= (size_t)optin;
+  if (use_pv) smem += pv;
+  e = cudaFuncSetAttribute(sim_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (n_shards + SIM_WARPS - 1) / SIM_WARPS;
   sim_run_kernel<<<(unsigned)blocks, SIM_WARPS * 32, smem, stream>>>(
       *ops, *cfg, aff, attn, arrival, prompt, output, cached, shard_off, n_shards, ttft, tpot,
-      n_iter, final_clock, shard_status, it_log_feat, it_log_lat, it_log_cap);
+      n_iter, final_clock, shard_status, it_log_feat, it_log_lat, it_log_cap, use_pv);
   return cudaGetLastError();
 }
 

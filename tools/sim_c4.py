@@ -52,7 +52,7 @@ def main() -> None:
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
     n_it = res.n_iter.cpu()
-    print(json.dumps({"shards": a.shards, "requests": a.requests, "ms": min(ms),
+    print(json.dumps({"shards": a.shards, "requests": a.requests, "ms": min(ms), "n_ops": ct.n_ops,
                       "iterations": int(n_it.sum()), "max_iterations": int(n_it.max()),
                       "us_per_iteration_longest": min(ms) * 1e3 / int(n_it.max()),
                       "ttft_checksum": float(torch.nan_to_num(res.ttft).sum())}))
