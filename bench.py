@@ -741,9 +741,10 @@ def host_regressor_table(kind: int, n_sig: int, seed: int) -> dict:
 def arm_config(args) -> dict:
     """The workload both arms report (the reference arm times a bounded sample of it)."""
     return {"workload": f"C5 scale sweep: {args.sigs:.3g} signatures x {args.points} points "
-                        f"fitted on the shared sweep grid, then {args.queries:.3g} queries "
-                        "per GPU per step (half affine, half attention)",
-            "queries_per_gpu": args.queries, "signatures_per_gpu": args.sigs,
+                        f"fitted on the shared sweep grid (split across the GPUs, one all-gather "
+                        f"of the rows), then {args.queries:.3g} queries per GPU per step over the "
+                        "full table (half affine, half attention)",
+            "queries_per_gpu": args.queries, "signatures": args.sigs,
             "points_per_signature": args.points,
             "l2": "inputs >> L2 (126 MB); no flush"}
 
@@ -768,7 +769,11 @@ def run_ours(args):
     seed = 1000 * rank
 
     # ---------------- fit inputs (C5: one shared sweep grid per kind) and the fit sub-benchmark
-    n_sig = {AFFINE: args.sigs // 2, ATTN: args.sigs - args.sigs // 2}
+    # C5: args.sigs signatures in total; each rank fits a contiguous 1/world of
+    # each kind (strong scaling of the fit), one all-gather gives every rank the
+    # full table, and every rank serves its own queries over that full table
+    n_sig_total = {AFFINE: args.sigs // 2, ATTN: args.sigs - args.sigs // 2}
+    n_sig = {k: -(-n_sig_total[k] // world) for k in (AFFINE, ATTN)}
     fit_in = {k: gen_grid_fit_data(k, n_sig[k], args.points, dev, seed + k) for k in (AFFINE, ATTN)}
     n_pts = {k: fit_in[k][0].shape[1] for k in (AFFINE, ATTN)}
     torch.cuda.synchronize()
@@ -793,13 +798,12 @@ def run_ours(args):
     # the serving form of the attention table (96-B rows) is part of the fit
     # output: written by the fit epilogue itself on one rank (fit_grid_packed),
     # by dooly_attn_pack after the fused all-gather otherwise
-    packed96 = torch.empty((n_sig[ATTN] + 1, 96), dtype=torch.uint8, device=dev) \
-        if peer is None else None
+    packed96 = torch.empty((world * n_sig[ATTN] + 1, 96), dtype=torch.uint8, device=dev)
 
     def do_fit(k):
         if peer is None:
             return fit_grid(k, fit_in[k][0], fit_in[k][1], fit_out.get(k),
-                            packed=packed96 if k == ATTN else None)
+                            packed=packed96 if k == ATTN and not dist_on else None)
         r0 = rank * n_sig[k]
         pt = peer[k].fit_grid(fit_in[k][0], fit_in[k][1], r0)
         sl = slice(r0, r0 + n_sig[k])
@@ -826,7 +830,6 @@ def run_ours(args):
             if rank == 0:
                 print(fused_note, file=sys.stderr)
             peer = None
-            packed96 = torch.empty((n_sig[ATTN] + 1, 96), dtype=torch.uint8, device=dev)
             fit_out.clear()
             for k in (AFFINE, ATTN):
                 fit_out[k] = do_fit(k)
@@ -842,16 +845,24 @@ def run_ours(args):
     t_end = torch.cuda.Event(enable_timing=True)
     fit_launches0 = _lib.launch_count(dev)
     t_start.record(stream)
+    full = {k: fit_out[k].table for k in (AFFINE, ATTN)}   # one rank: the local rows are the table
     for _ in range(fit_steps):
         for k in (AFFINE, ATTN):
             ev[k][0].record(stream)
             fit_out[k] = do_fit(k)
-            if k == ATTN and peer is not None:   # serving form (96-B rows) of this rank's rows
-                packed96 = pack_attn(fit_out[k].table, packed96, check=False)
             ev[k][1].record(stream)
         ag0.record(stream)
-        if dist_on and peer is None:   # the one exchange step: every rank gets every rank's rows
-            full = {k: ddist.gather_requests(fit_out[k].table) for k in (AFFINE, ATTN)}
+        if dist_on:   # the one exchange step: every rank gets every rank's rows
+            if peer is None:
+                full = {k: ddist.gather_requests(fit_out[k].table).reshape(
+                    -1, fit_out[k].table.shape[-1]) for k in (AFFINE, ATTN)}
+            else:     # already stored into every rank's full table by the fit epilogues
+                full = {k: peer[k].table for k in (AFFINE, ATTN)}
+            # serving form (96-B rows) of the full attention table (one rank:
+            # written by the fit epilogue itself)
+            packed96 = pack_attn(full[ATTN], packed96, check=False)
+        else:
+            full = {k: fit_out[k].table for k in (AFFINE, ATTN)}
         ag1.record(stream)
         torch.cuda.synchronize()
         for k in (AFFINE, ATTN):
@@ -878,8 +889,10 @@ def run_ours(args):
         FP64_PER_ATTN_POINT_GROUPED if grouped else FP64_PER_ATTN_POINT
     fit_dev_ms = sum(fit_ms.values()) / fit_steps
     fits = {
-        "value": world * args.sigs / (fit_total_ms / 1e3), "unit": "fits/s",
-        "ms_per_step": fit_total_ms, "signatures_per_gpu": args.sigs, "points": n_pts,
+        "value": world * sum(n_sig.values()) / (fit_total_ms / 1e3), "unit": "fits/s",
+        "ms_per_step": fit_total_ms, "signatures": world * sum(n_sig.values()),
+        "signatures_per_gpu": sum(n_sig.values()), "points": n_pts,
+        "scaling": "strong: C5's signature set is split across the ranks",
         "workload": "C5 shared sweep grid per kind (affine: 4096 token counts in [1, 32768]; "
                     "attention: 16x16x16 (prefill_toks, batch, kv_tokens)); sim.fit_grid",
         "kernel_ms": {"affine": fit_ms[AFFINE] / fit_steps, "attention": fit_ms[ATTN] / fit_steps,
@@ -948,7 +961,7 @@ def run_ours(args):
             del xr, fc
         torch.cuda.empty_cache()
         csr_bytes = sum(n_sig[k] * n_pts[k] * BYTES_PER_POINT[k] for k in (AFFINE, ATTN))
-        fits_csr = {"value": args.sigs / (sum(csr_ms.values()) / 1e3), "unit": "fits/s",
+        fits_csr = {"value": sum(n_sig.values()) / (sum(csr_ms.values()) / 1e3), "unit": "fits/s",
                     "kernel_ms": {"affine": csr_ms[AFFINE], "attention": csr_ms[ATTN]},
                     "achieved_gbs": csr_bytes / (sum(csr_ms.values()) / 1e3) / 1e9,
                     "alg_bytes_per_point": BYTES_PER_POINT,
@@ -961,9 +974,9 @@ def run_ours(args):
         cpu_fit_in = ({k: fit_in[k][0].cpu().numpy().view(np.uint32) for k in (AFFINE, ATTN)},
                       {k: fit_in[k][1][:m].cpu().numpy() for k in (AFFINE, ATTN)})
     del fit_in
-    pack_attn(fit_out[ATTN].table, packed96, check=True)   # raises if not representable
-    rows128 = {k: fit_out[k].table for k in (AFFINE, ATTN)}
-    tables = {AFFINE: fit_out[AFFINE].table, ATTN: packed96}
+    pack_attn(full[ATTN], packed96, check=True)   # raises if not representable
+    rows128 = dict(full)   # every rank queries the full table
+    tables = {AFFINE: full[AFFINE], ATTN: packed96}
     pkind = {AFFINE: AFFINE, ATTN: KIND_ATTN_PACKED}
     torch.cuda.empty_cache()
 

@@ -160,11 +160,13 @@ def test_ranks_one_gpu_sharded_dedup_and_fit(world):
     assert all(p.exitcode == 0 for p in procs)
 
 
-@pytest.mark.parametrize("world", [2, 8])
-def test_bench_ranks_torchrun(world):
+@pytest.mark.parametrize("world,allgather", [(2, "fused"), (8, "fused"), (2, "collective")])
+def test_bench_ranks_torchrun(world, allgather):
     """bench.py's N > 1 path end to end (barriers, max-over-ranks timing, the
-    fit-table and digest all-gathers, replica-sharded sim) at small sizes."""
-    env = dict(os.environ, DOOLY_DIST_BACKEND="gloo")
+    fit-table and digest all-gathers, replica-sharded sim) at small sizes: the
+    C5 signature set split across the ranks, every rank's queries served from
+    the full gathered table."""
+    env = dict(os.environ, DOOLY_DIST_BACKEND="gloo", DOOLY_FIT_ALLGATHER=allgather)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"),
@@ -179,7 +181,9 @@ def test_bench_ranks_torchrun(world):
     d = json.loads(lines[0])
     assert d["n_gpus"] == world and d["value"] > 0 and d["scaling"] == "weak"
     assert d["fits"]["all_fitted"] and not d["unknown_signature_errors"]
-    assert d["fits"]["allgather_path"].startswith("fused")
-    assert d["dedup"]["exchange"].startswith("fused" if world < 4 else "owner-routed")
+    assert d["fits"]["allgather_path"].startswith("fused" if allgather == "fused" else "NCCL")
+    assert d["fits"]["signatures"] == 20_000 and d["fits"]["signatures_per_gpu"] == 20_000 // world
+    assert d["dedup"]["exchange"].startswith(
+        "owner-routed" if world >= 4 else "fused" if allgather == "fused" else "NCCL")
     assert d["dedup"]["records_per_gpu"] == 100_000 and d["dedup"]["unique"] > 0
     assert d["sim"]["all_ok"] and d["sim"]["requests"] == 20_000
