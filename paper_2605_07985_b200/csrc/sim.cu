@@ -789,23 +789,44 @@ __global__ void __launch_bounds__(32 * kClockWarps) sim_clock_kernel(
   double c = 0.0;
   fetch(b);
   for (int64_t i0 = b; i0 < e; i0 += kClockChunk) {
+    bool jump = false;  // an idle jump target anywhere in this chunk
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       L[k * 32 + lane] = nl[k];
       S[k * 32 + lane] = ns[k];
+      jump |= __double_as_longlong(ns[k]) != 0ll;
     }
+    jump = __any_sync(0xFFFFFFFFu, jump);
     __syncwarp();
     if (i0 + kClockChunk < e) fetch(i0 + kClockChunk);   // next chunk in flight during the scan
     const int m = (int)min((int64_t)kClockChunk, e - i0);
     if (lane == 0) {
-      // busy iterations (it_start == 0: the common case) chain only the add;
-      // the max with an idle jump target is taken on the rare nonzero start
+      if (!jump) {
+        // busy chunk (it_start == 0 throughout, the common case): only the adds chain
+        int j = 0;
+        for (; j + 8 <= m; j += 8) {
+          double v[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[t] = L[j + t];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            c = __dadd_rn(c, v[t]);
+            L[j + t] = c;
+          }
+        }
+        for (; j < m; ++j) {
+          c = __dadd_rn(c, L[j]);
+          L[j] = c;
+        }
+      } else {
+        // the max with an idle jump target on a nonzero start
 #pragma unroll 8
-      for (int j = 0; j < m; ++j) {
-        const double sj = S[j];
-        if (__double_as_longlong(sj) != 0ll && c < sj) c = sj;
-        c = __dadd_rn(c, L[j]);
-        L[j] = c;
+        for (int j = 0; j < m; ++j) {
+          const double sj = S[j];
+          if (__double_as_longlong(sj) != 0ll && c < sj) c = sj;
+          c = __dadd_rn(c, L[j]);
+          L[j] = c;
+        }
       }
     }
     __syncwarp();
