@@ -1015,8 +1015,14 @@ __global__ void __launch_bounds__(256, MINB) fit_grid_ring_kernel(
   }
 }
 
+#ifndef FG_WARP_MINB
+#define FG_WARP_MINB 2  // CTAs per SM the warp kernel's registers are sized for
+#endif
+#ifndef FG_WARP_YS
+#define FG_WARP_YS 8    // y steps (4 points per lane each) issued ahead of their math
+#endif
 template <int KIND>
-__global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
+__global__ void __launch_bounds__(256, FG_WARP_MINB) fit_grid_warp_kernel(
     const double* __restrict__ fpl, int64_t n_pts, const double* __restrict__ y, int64_t n_sig,
     const GridFactor* __restrict__ gf, void* __restrict__ table, double* __restrict__ fit_err,
     uint8_t* __restrict__ status, const GridOut pe, int allow_factor, int su_groups) {
@@ -1120,7 +1126,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
     };
     auto sweep = [&](bool keep, auto&& step) {
       int p = 4 * lane;
-      constexpr int YS = 8;
+      constexpr int YS = FG_WARP_YS;
       for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
         double4 yv[YS];
 #pragma unroll
@@ -1163,7 +1169,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
           grid_g1_step(yv, f3of(pp), u.x, u.y, acc);
         };
         int p = 4 * lane;
-        constexpr int YS = 8;
+        constexpr int YS = FG_WARP_YS;
         for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
           double4 yv[YS];
 #pragma unroll
@@ -1185,7 +1191,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
             grid_r1_step(yv, u.x, u.y, r1);
           };
           int p = 4 * lane;
-          constexpr int YS = 8;
+          constexpr int YS = FG_WARP_YS;
           for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
             double4 yv[YS];
 #pragma unroll
@@ -1229,7 +1235,7 @@ __global__ void __launch_bounds__(256, 2) fit_grid_warp_kernel(
           grid_g2_step(yv, f3of(pp), u.x, u.y, c, err);
         };
         int p = 4 * lane;
-        constexpr int YS = 8;
+        constexpr int YS = FG_WARP_YS;
         for (; p + 128 * (YS - 1) < n; p += 128 * YS) {
           double4 yv[YS];
 #pragma unroll
