@@ -55,6 +55,67 @@ def test_sim_run_random_configs(case, dev):
     assert np.array_equal(met.tpot[m].view(np.uint64), ref["tpot"][m].view(np.uint64))
 
 
+@pytest.mark.parametrize("case", range(120))
+def test_sim_run_window_edges(case, dev):
+    """The serving loop's windows at their edges, every shard's per-iteration
+    features and latencies against the oracle event loop: short outputs (many
+    finishes inside a window, requests finishing in their admitting iteration),
+    fully cached prompts (first decode step at admission), prompts longer than
+    the chunk (partial prefills end the window at iteration 0), batch and KV
+    caps that block the FCFS head (windows run across arrivals until the first
+    finish), bursts and idle gaps."""
+    from paper_2605_07985_b200 import _lib
+    from paper_2605_07985_b200.sim import CallTree, ShardedTrace, collect, run_sharded
+
+    rng = np.random.default_rng(5000 + case)
+    window = int(rng.choice([0, 0, 0, 64]))
+    tp = int(rng.choice([1, 2]))
+    shards = int(rng.integers(8, 33))
+    n = int(rng.integers(200, 1200))
+    chunk = int(rng.choice([64, 512, 8192]))
+    max_batch = int(rng.choice([2, 8, 48, 64]))
+    max_batch = min(max_batch, chunk)
+    cap = int(rng.choice([10**15, 3 * 10**8, 8 * 10**8]))
+    ta, tt, ops, ol = _sim_setup(6000 + case, window=window, tp=tp)
+    regs = _regs(ta, tt, dev)
+    gaps = rng.exponential(1.0 / float(rng.choice([2.0, 50.0, 2000.0])), size=n)
+    gaps[rng.random(n) < 0.05] *= 200.0        # idle gaps
+    gaps[rng.random(n) < 0.2] = 0.0            # bursts (equal arrival times)
+    arr = np.cumsum(gaps)
+    pr = rng.integers(1, 3 * chunk if rng.random() < 0.5 else 600, size=n).astype(np.uint32)
+    pr = np.minimum(pr, 2000).astype(np.uint32)
+    ou = np.where(rng.random(n) < 0.3, rng.integers(1, 4, size=n),
+                  rng.integers(1, 60, size=n)).astype(np.uint32)
+    ca = np.where(rng.random(n) < 0.2, pr, np.where(rng.random(n) < 0.2, pr // 2, 0)).astype(np.uint32)
+    kvb = 131072
+    cap = max(cap, int((int(pr.max()) + int(ou.max())) * kvb))   # every request fits alone
+    sc = _lib.Sched()
+    sc.chunk, sc.max_batch, sc.window = chunk, max_batch, window
+    sc.kv_bytes_per_token, sc.kv_capacity_bytes, sc.max_iterations = kvb, cap, 10**7
+    trace = ShardedTrace.from_arrays(arr, pr, ou, ca, shards, dev)
+    log_cap = 6000
+    res = run_sharded(trace, CallTree([], ol, window), sc, regs, log_cap=log_cap)
+    met = collect(trace, res)
+    n_iter = res.n_iter.cpu().numpy().tolist()
+    lf = res.log_feat.cpu().numpy().view(np.uint32)
+    ll = res.log_lat.cpu().numpy()
+    for s in range(shards):
+        r = osim.run_shard(arr[s::shards].tolist(), pr[s::shards].tolist(), ou[s::shards].tolist(),
+                           ca[s::shards].tolist(), ops, chunk, max_batch, kvb, cap, window, tp,
+                           5e-6, 5e-12, log=True)
+        assert n_iter[s] == r["n_iter"], s
+        k = min(r["n_iter"], log_cap)
+        assert [tuple(int(v) for v in row) for row in lf[s, :k]] == \
+            [tuple(f) for f in r["feats"][:k]], s
+        assert np.array_equal(ll[s, :k], np.array(r["lat"][:k])), s
+        idx = np.arange(s, n, shards)
+        assert np.array_equal(met.ttft[idx].view(np.uint64), np.asarray(r["ttft"]).view(np.uint64)), s
+        rt = np.asarray(r["tpot"])
+        assert np.array_equal(np.isnan(met.tpot[idx]), np.isnan(rt)), s
+        m = ~np.isnan(rt)
+        assert np.array_equal(met.tpot[idx][m].view(np.uint64), rt[m].view(np.uint64)), s
+
+
 @pytest.mark.parametrize("case", range(24))
 def test_predict_random_tables(case, dev):
     """Random table sizes, query counts and misalignments; fitted, unfitted
