@@ -258,9 +258,34 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     sl.wb = sl.ptot + MB;
     sl.wr = sl.wb + MB;
   }
-  // window products (entry-major, one column per lane) after the slot arrays, if launched with room
-  double* pv_base = use_pv ? reinterpret_cast<double*>(dyn + (size_t)SIM_WARPS * MB * kSlotBytes)
-                           : nullptr;
+  // after the slot arrays, if launched with room (use_pv):
+  //  2: the decode-product table P[x][e] = repeat_e x value_e(num_toks = batch = x) of every
+  //     affine and comm entry for x in [0, MB], shared by the CTA's warps — a window
+  //     iteration u >= 1 is pure decode with num_toks = batch = nr(u) <= MB, so its
+  //     non-attention products are table reads (the same IEEE operations, done once);
+  //  1: per-lane product columns for window_latency.
+  double* pv_base = use_pv == 1 ? reinterpret_cast<double*>(dyn + (size_t)SIM_WARPS * MB * kSlotBytes)
+                                : nullptr;
+  double* ptab = use_pv == 2 ? reinterpret_cast<double*>(dyn + (size_t)SIM_WARPS * MB * kSlotBytes)
+                             : nullptr;
+  if (ptab != nullptr) {
+    const int no = ops.n_ops;
+    for (int idx = threadIdx.x; idx < (MB + 1) * no; idx += blockDim.x) {
+      const int e = idx % no;
+      const uint32_t x = (uint32_t)(idx / no);
+      const int f = s_ops.feat[e];
+      double v = 0.0;
+      if (f == DOOLY_FEAT_COMM) {
+        v = mul(s_ops.rep[e], comm_latency(&s_ops, ops.tp, ops.comm_alpha, ops.comm_beta,
+                                           (uint64_t)x * s_ops.bpt[e]));
+      } else if (f != DOOLY_FEAT_ATTN) {
+        bool cl;
+        v = mul(s_ops.rep[e], clamp_floor(eval_affine(s_ops.aff[e], x), cl));
+      }
+      ptab[idx] = v;
+    }
+    __syncthreads();
+  }
   const uint32_t W = cfg.window > 0 ? (uint32_t)cfg.window : 0u;
   const uint64_t kvb = (uint64_t)cfg.kv_bytes_per_token;
   const uint64_t cap = (uint64_t)cfg.kv_capacity_bytes;
@@ -503,7 +528,45 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
         }
         bool bad = false;
         double lat = 0.0;
-        if (pv_base != nullptr) {
+        if (ptab != nullptr) {
+          // iteration 0 (any composition) by entries across lanes, as the serial path
+          double w0 = 0.0, w1 = 0.0;
+          if (lane < ops.n_ops)
+            w0 = mul(s_ops.rep[lane], entry_value(ops, &s_ops, lane, num_toks, prefill, batch, kvs,
+                                                  kvw, bad));
+          if (lane + 32 < ops.n_ops)
+            w1 = mul(s_ops.rep[lane + 32], entry_value(ops, &s_ops, lane + 32, num_toks, prefill,
+                                                       batch, kvs, kvw, bad));
+          double* sw0 = s_sum[wid];
+          sw0[lane] = w0;
+          sw0[lane + 32] = w1;
+          __syncwarp();
+          if (lane == 0) {
+            int e = 0;
+#pragma unroll 4
+            for (; e + 2 <= ops.n_ops; e += 2) {
+              const double2 v = *reinterpret_cast<const double2*>(sw0 + e);
+              lat = add(lat, v.x);
+              lat = add(lat, v.y);
+            }
+            if (e < ops.n_ops) lat = add(lat, sw0[e]);
+          } else {
+            // decode iteration u: table products, attention entries evaluated
+            const double* prow = ptab + (size_t)min(nt, (uint32_t)MB) * ops.n_ops;
+            for (int e = 0; e < ops.n_ops; ++e) {
+              double v;
+              if (s_ops.feat[e] == DOOLY_FEAT_ATTN) {
+                bool cl;
+                v = mul(s_ops.rep[e],
+                        clamp_floor(eval_attn(s_ops.attn[e], 0u, bt, s_ops.wslot[e] ? kw : ks), cl));
+              } else {
+                v = prow[e];
+              }
+              lat = add(lat, v);
+            }
+          }
+          __syncwarp();
+        } else if (pv_base != nullptr) {
           lat = window_latency(ops, &s_ops, pv_base + (size_t)wid * ops.n_ops * 32, lane, nt, pf,
                                bt, ks, kw, bad);
           bad = bad && (int64_t)u < wmax;
@@ -733,9 +796,18 @@ cudaError_t launch_sim(const dooly_oplist* ops, const dooly_sched* cfg, const vo
   cudaFuncAttributes fa;
   e = cudaFuncGetAttributes(&fa, sim_run_kernel);
   if (e != cudaSuccess) return e;
-  const int use_pv = getenv("DOOLY_SIM_PV0") == nullptr &&
-                     smem + pv + fa.sharedSizeBytes <= (size_t)optin;
-  if (use_pv) smem += pv;
+  // the decode-product table (one per CTA) when it fits, else the product columns
+  const size_t pt = (size_t)(cfg->max_batch + 1) * ops->n_ops * sizeof(double);
+  const char* pvenv = getenv("DOOLY_SIM_PV");
+  const int want = pvenv != nullptr ? atoi(pvenv) : 2;
+  int use_pv = 0;
+  if (want >= 2 && smem + pt + fa.sharedSizeBytes <= (size_t)optin) {
+    use_pv = 2;
+    smem += pt;
+  } else if (want >= 1 && smem + pv + fa.sharedSizeBytes <= (size_t)optin) {
+    use_pv = 1;
+    smem += pv;
+  }
   e = cudaFuncSetAttribute(sim_run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t blocks = (n_shards + SIM_WARPS - 1) / SIM_WARPS;
