@@ -329,7 +329,13 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
     };
     ld_wait(0);
 
+#ifdef SIM_PASS_COUNT
+    int64_t passes = 0;  // diagnostic build: loop passes instead of iterations in n_iter_out
+#endif
     while (true) {
+#ifdef SIM_PASS_COUNT
+      ++passes;
+#endif
       // ---- 1. arrivals with arrival <= clock (sorted: a ballot prefix)
       double next_arr = __shfl_sync(0xFFFFFFFFu, win_arr, 0);
       if (arrive < n && next_arr <= clock) {
@@ -772,7 +778,11 @@ __global__ void __launch_bounds__(SIM_WARPS * 32) sim_run_kernel(
       __syncwarp();
     }
     if (lane == 0) {
+#ifdef SIM_PASS_COUNT
+      n_iter_out[shard] = passes;
+#else
       n_iter_out[shard] = it;
+#endif
       clock_out[shard] = clock;
       status_out[shard] = status;
     }
