@@ -11,7 +11,12 @@
 //   parallelism is across shards, and inside a shard across the running batch
 //   (lanes own running slots) and across op-list entries (lanes own entries).
 //   The scheduler state lives in shared memory; the per-iteration loop touches
-//   HBM only to read newly admitted requests and to write TTFT/TPOT.
+//   HBM only to read newly admitted requests and to write TTFT/TPOT.  One loop
+//   pass per admission: the scheduled iteration is window iteration 0, and
+//   when the rest of the window's composition is fixed (everything decoding,
+//   no admission possible before an arrival or a finish) lanes 1..31 evaluate
+//   the following iterations in parallel, finishes included; the clock then
+//   commits them in order (profiles/r2_sim_window.md).
 //
 // Parity: per-entry predictions use the same no-FMA evaluation as predict
 //   (common.cuh); the per-iteration sum runs in op-list order on lane 0 with

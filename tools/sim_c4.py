@@ -1,6 +1,7 @@
 """Run the C4 serving simulation once (Llama-3-70B-like tp=4,
 1M-request Poisson trace, S fixed replicas) — for ncu captures of
-sim_run_kernel and for SIM_WIN / layout experiments.
+sim_run_kernel and for layout / build-knob experiments (SIM_WARPS_N, SIM_UNROLL,
+DOOLY_SIM_PV).
 
     python tools/sim_c4.py [--shards 64] [--requests 1000000] [--reps 3]
 """
