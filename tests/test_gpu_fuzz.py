@@ -116,6 +116,16 @@ def test_sim_run_window_edges(case, dev):
         assert np.array_equal(met.tpot[idx][m].view(np.uint64), rt[m].view(np.uint64)), s
 
 
+@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("case", range(6))
+def test_sim_run_window_eval_modes(mode, case, dev, monkeypatch):
+    """The window's evaluation fallbacks (DOOLY_SIM_PV=1: per-lane product
+    columns, 0: the plain per-lane loop — used when the decode-product table
+    does not fit in shared memory) give the same bit-exact runs."""
+    monkeypatch.setenv("DOOLY_SIM_PV", mode)
+    test_sim_run_window_edges(case, dev)
+
+
 @pytest.mark.parametrize("case", range(24))
 def test_predict_random_tables(case, dev):
     """Random table sizes, query counts and misalignments; fitted, unfitted
