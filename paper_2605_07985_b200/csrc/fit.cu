@@ -37,6 +37,7 @@
 // vector peak and lower precisions cannot meet the 1e-9 contract).
 #include "attn_moments.cuh"
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -768,6 +769,145 @@ static cudaError_t launch_kind(const uint32_t* x, int64_t n_pts, const double* y
 }
 
 // ====================================================================
+// Affine CSR path, one WARP per signature (the default for affine).  Pass 1
+// streams the signature's x (u32) and y (f64) from HBM, 4 consecutive points
+// per lane per step with 16-B / 32-B vector loads (4 steps in flight),
+// tagged L2::evict_last; the raw sums (x, x^2, y, xy; two accumulator sets)
+// and the box reduce with shuffles; every lane solves the 2x2 scaled normal
+// equations with the same Cholesky-with-drop arithmetic as reduce_and_solve;
+// pass 2 re-streams the points — normally L2 hits — for the training MAPE.
+// No shared memory and no CTA barrier: every warp streams independently,
+// where the staged CTA kernel stops a whole CTA at each signature's solve.
+// x planes (16 B per lane step): L2 eviction hints need 256-bit accesses, so
+// x goes through the default policy (16 KB per 4096-point signature).
+__device__ __forceinline__ uint4 ld_keep_u4(const void* p, bool) { return ld_stream_u4(p); }
+__device__ __forceinline__ double4 ld_keep_d4(const double* p, bool keep) {
+  double4 v;
+  if (keep)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
+// Visit points [beg, beg + n) of a signature once: the misaligned head and the
+// tail point by point, the aligned body 4 points per lane with FA_YS steps of
+// loads issued ahead of their use.
+constexpr int FA_YS = 4;
+template <typename F4, typename F1>
+__device__ __forceinline__ void warp_stream_affine(const uint32_t* x, const double* y, int64_t beg,
+                                                   int64_t n, bool vec, bool keep, F4&& f4,
+                                                   F1&& f1) {
+  const int lane = threadIdx.x & 31;
+  int64_t h = vec ? (4 - (beg & 3)) & 3 : 0;  // head points before the 32-B aligned body
+  if (h > n) h = n;
+  if (lane < h) f1(__ldg(x + beg + lane), __ldg(y + beg + lane));
+  int64_t i = h;
+  if (vec) {
+    const int64_t body = h + (n - h) / 128 * 128;
+    for (; i + 128 * FA_YS <= body; i += 128 * FA_YS) {
+      uint4 xv[FA_YS];
+      double4 yv[FA_YS];
+#pragma unroll
+      for (int t = 0; t < FA_YS; ++t) {
+        const int64_t q = beg + i + 128 * t + 4 * lane;
+        xv[t] = ld_keep_u4(x + q, keep);
+        yv[t] = ld_keep_d4(y + q, keep);
+      }
+#pragma unroll
+      for (int t = 0; t < FA_YS; ++t) f4(xv[t], yv[t]);
+    }
+    for (; i < body; i += 128) {
+      const int64_t q = beg + i + 4 * lane;
+      f4(ld_keep_u4(x + q, keep), ld_keep_d4(y + q, keep));
+    }
+  }
+  for (int64_t k = i + lane; k < n; k += 32) f1(__ldg(x + beg + k), __ldg(y + beg + k));
+}
+
+__global__ void __launch_bounds__(256, 2) fit_affine_warp_kernel(
+    const uint32_t* __restrict__ x, const double* __restrict__ y, const int64_t* __restrict__ off,
+    int64_t n_sig, dooly_affine_row* __restrict__ table, double* __restrict__ fit_err,
+    uint8_t* __restrict__ status, bool vec_ok) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < n_sig; s += n_warps) {
+    const int64_t beg = __ldg(off + s), n = __ldg(off + s + 1) - beg;
+    if (n < FitTraits<DOOLY_KIND_AFFINE>::NEED) {
+      if (lane == 0) write_unfitted<DOOLY_KIND_AFFINE>(table, s, fit_err, status);
+      continue;
+    }
+    // ---- pass 1: raw sums (x, x^2, y, xy) in two sets, and the box
+    double a[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+    uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+    auto acc1 = [&](uint32_t xi, double yi, int set) {
+      const double v = u2d(xi);
+      mn = min(mn, xi);
+      mx = max(mx, xi);
+      FitTraits<DOOLY_KIND_AFFINE>::accumulate(&v, yi, a[set]);
+    };
+    warp_stream_affine(
+        x, y, beg, n, vec_ok, true,
+        [&](const uint4& xv, const double4& yv) {
+          acc1(xv.x, yv.x, 0);
+          acc1(xv.y, yv.y, 1);
+          acc1(xv.z, yv.z, 0);
+          acc1(xv.w, yv.w, 1);
+        },
+        [&](uint32_t xi, double yi) { acc1(xi, yi, 0); });
+    double sx = warp_sum(a[0][0] + a[1][0]), sxx = warp_sum(a[0][1] + a[1][1]);
+    double sy = warp_sum(a[0][2] + a[1][2]), sxy = warp_sum(a[0][3] + a[1][3]);
+    mn = __reduce_min_sync(0xFFFFFFFFu, mn);
+    mx = __reduce_max_sync(0xFFFFFFFFu, mx);
+    // ---- 2x2 scaled normal equations, Cholesky with drop (reduce_and_solve's
+    // arithmetic for NCOL = 2), solved redundantly by every lane
+    const double inv = mx > 0 ? 1.0 / (double)mx : 1.0;  // IEEE division (oracle parity)
+    const double g00 = (double)n, g01 = sx * inv, g11 = sxx * (1.0 * inv * inv);
+    const double b0 = sy * 1.0, b1 = sxy * inv;
+    const bool k0 = g00 > DROP_TOL * g00;
+    const double d0 = k0 ? sqrt(g00) : 0.0, rd0 = k0 ? rcp64(d0) : 0.0;
+    const double l10 = g01 * rd0;
+    const double p11 = fma(-l10, l10, g11);
+    const bool k1 = p11 > DROP_TOL * g11;
+    const double d1 = k1 ? sqrt(p11) : 0.0, rd1 = k1 ? rcp64(d1) : 0.0;
+    const double z0 = b0 * rd0;
+    const double z1 = fma(-l10, z0, b1) * rd1;
+    double c[2];
+    c[1] = z1 * rd1;
+    c[0] = fma(-l10, c[1], z0) * rd0;
+    // ---- pass 2: training MAPE (the points re-read, normally from L2)
+    double e0 = 0.0, e1 = 0.0;
+    auto term = [&](uint32_t xi, double yi) {
+      const uint32_t xv[1] = {xi};
+      return mape_term<DOOLY_KIND_AFFINE>(xv, yi, c, &inv);
+    };
+    warp_stream_affine(
+        x, y, beg, n, vec_ok, false,
+        [&](const uint4& xv, const double4& yv) {
+          e0 += term(xv.x, yv.x);
+          e1 += term(xv.y, yv.y);
+          e0 += term(xv.z, yv.z);
+          e1 += term(xv.w, yv.w);
+        },
+        [&](uint32_t xi, double yi) { e0 += term(xi, yi); });
+    const double e = warp_sum(e0 + e1);
+    if (lane == 0) {
+      dooly_affine_row* row = table + s;
+      row->c0 = c[0];
+      row->c1 = c[1];
+      row->inv_scale = inv;
+      row->lo = mn;
+      row->hi = mx;
+      fit_err[s] = e / (double)n;
+      status[s] = DOOLY_FIT_OK;
+    }
+  }
+}
+
+// ====================================================================
 // Attention (10-column) path: three kernels.
 //
 // ncu showed the fused stage kernel spending ~a third of its warp time in the
@@ -1145,6 +1285,16 @@ cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double*
   if (n_sig == 0) return cudaSuccess;
   if (kind == DOOLY_KIND_AFFINE) {
     *launches += 1;
+    const char* which = getenv("DOOLY_FIT_CSR_AFFINE");  // "stage": the staged CTA kernel
+    if (which == nullptr || strcmp(which, "stage") != 0) {
+      const bool vec_ok = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 32 == 0);
+      int64_t blocks = (int64_t)n_sm * 2;
+      const int64_t need = (n_sig + 7) / 8;
+      if (blocks > need) blocks = need;
+      fit_affine_warp_kernel<<<(unsigned)blocks, 256, 0, stream>>>(
+          x, y, off, n_sig, static_cast<dooly_affine_row*>(table), fit_err, status, vec_ok);
+      return cudaGetLastError();
+    }
     return launch_kind<DOOLY_KIND_AFFINE>(x, n_pts, y, off, n_sig, table, fit_err, status,
                                           stream, n_sm);
   }

@@ -200,3 +200,35 @@ def test_fit_random_csr(case, dev):
         assert d.max() <= 1e-9, d.max()
         fe, fr_ = fr.fit_err.cpu().numpy()[ok], ref["fit_err"][ok]
         assert np.all(np.abs(fe - fr_) <= 1e-9 * fr_ + 1e-12)
+
+
+@pytest.mark.parametrize("shift", [0, 1, 3])
+def test_fit_csr_affine_warp_large_ragged(shift, dev, monkeypatch):
+    """The warp-per-signature affine CSR kernel on ragged signatures of 1k-6k
+    points at every head misalignment (offsets shifted by `shift` points, so
+    the 4-point vector body starts after a 1-3 point head), against the oracle
+    and against the staged CTA kernel (DOOLY_FIT_CSR_AFFINE=stage)."""
+    from paper_2605_07985_b200.sim import fit_tables
+
+    x, y, off = synth_fit_data(AFFINE, 60, 6000, seed=90 + shift, ragged=True)
+    pad = np.full((1, shift), 7, np.uint32)
+    x = np.ascontiguousarray(np.concatenate([pad, x], axis=1))
+    y = np.concatenate([np.full(shift, 1e-5), y])
+    off = np.concatenate([[0], off + shift]).astype(np.int64)     # signature 0: the padding
+    xt = torch.from_numpy(x.view(np.int32)).to(dev)
+    yt, ot = torch.from_numpy(y).to(dev), torch.from_numpy(off).to(dev)
+    ref = osim.fit(AFFINE, x, y, off)
+    fr = fit_tables(AFFINE, xt, yt, ot)
+    monkeypatch.setenv("DOOLY_FIT_CSR_AFFINE", "stage")
+    fs = fit_tables(AFFINE, xt, yt, ot)
+    torch.cuda.synchronize()
+    for res in (fr, fs):
+        got = rows_to_table(AFFINE, res.rows())
+        st = res.status.cpu().numpy()
+        assert np.array_equal(st, ref["status"])
+        ok = st == 0
+        assert np.array_equal(got["lo"][ok], ref["lo"][ok]) and np.array_equal(got["hi"][ok], ref["hi"][ok])
+        d = np.abs(got["coef"][ok] - ref["coef"][ok]).max(axis=1) / np.abs(ref["coef"][ok]).max(axis=1)
+        assert d.max() <= 1e-9, d.max()
+        fe, fr_ = res.fit_err.cpu().numpy()[ok], ref["fit_err"][ok]
+        assert np.all(np.abs(fe - fr_) <= 1e-9 * fr_ + 1e-12)
