@@ -1072,6 +1072,53 @@ __device__ __forceinline__ void warp_stream_points_async(unsigned char* ring, co
   }
 }
 
+// Pass 1 of one attention signature by one warp: the 44 raw sums and the box,
+// warp-reduced (every lane returns every sum).
+__device__ __forceinline__ void attn_pass1(unsigned char* ring, const uint32_t* x, int64_t n_pts,
+                                           const double* y, int64_t beg, int64_t n, bool vec,
+                                           int grouped, double* acc, uint32_t* mn, uint32_t* mx) {
+#pragma unroll
+  for (int i = 0; i < ATTN_NACC; ++i) acc[i] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    mn[k] = 0xFFFFFFFFu;
+    mx[k] = 0u;
+  }
+  warp_stream_points_async(
+      ring, x, n_pts, y, beg, n, vec,
+      [&](const AttnPoints4& p) {
+        // 4 consecutive points sharing prefill_toks and batch (a sweep grid
+        // with kv innermost): grouped moments, ~25 FP64 per point instead of 63
+        const bool same = grouped && p.x[1][0] == p.x[0][0] && p.x[2][0] == p.x[0][0] &&
+                          p.x[3][0] == p.x[0][0] && p.x[1][1] == p.x[0][1] &&
+                          p.x[2][1] == p.x[0][1] && p.x[3][1] == p.x[0][1];
+        if (same) {
+          double c4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            c4[u] = u2d(p.x[u][2]);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+              mn[k] = min(mn[k], p.x[u][k]);
+              mx[k] = max(mx[k], p.x[u][k]);
+            }
+          }
+          attn_accumulate_group(u2d(p.x[0][0]), u2d(p.x[0][1]), c4, p.y, acc);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) attn_point(p.x[u], p.y[u], acc, mn, mx);
+        }
+      },
+      [&](const uint32_t* xv, double yv) { attn_point(xv, yv, acc, mn, mx); });
+#pragma unroll
+  for (int i = 0; i < ATTN_NACC; ++i) acc[i] = warp_sum(acc[i]);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    mn[k] = __reduce_min_sync(0xFFFFFFFFu, mn[k]);
+    mx[k] = __reduce_max_sync(0xFFFFFFFFu, mx[k]);
+  }
+}
+
 __global__ void __launch_bounds__(FA_THREADS) fit_moments_attn_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y,
     const int64_t* __restrict__ off, int64_t n_sig, double* __restrict__ mom,
@@ -1085,42 +1132,8 @@ __global__ void __launch_bounds__(FA_THREADS) fit_moments_attn_kernel(
     const int64_t beg = __ldg(off + s), n = __ldg(off + s + 1) - beg;
     if (n < FitTraits<DOOLY_KIND_ATTN>::NEED) continue;  // the solve kernel marks it
     double acc[ATTN_NACC];
-#pragma unroll
-    for (int i = 0; i < ATTN_NACC; ++i) acc[i] = 0.0;
-    uint32_t mn[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, mx[3] = {0u, 0u, 0u};
-    warp_stream_points_async(
-        ring, x, n_pts, y, beg, n, vec_ok && (beg % 4 == 0),
-        [&](const AttnPoints4& p) {
-          // 4 consecutive points sharing prefill_toks and batch (a sweep grid
-          // with kv innermost): grouped moments, ~25 FP64 per point instead of 63
-          const bool same = grouped && p.x[1][0] == p.x[0][0] && p.x[2][0] == p.x[0][0] &&
-                            p.x[3][0] == p.x[0][0] && p.x[1][1] == p.x[0][1] &&
-                            p.x[2][1] == p.x[0][1] && p.x[3][1] == p.x[0][1];
-          if (same) {
-            double c4[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              c4[u] = u2d(p.x[u][2]);
-#pragma unroll
-              for (int k = 0; k < 3; ++k) {
-                mn[k] = min(mn[k], p.x[u][k]);
-                mx[k] = max(mx[k], p.x[u][k]);
-              }
-            }
-            attn_accumulate_group(u2d(p.x[0][0]), u2d(p.x[0][1]), c4, p.y, acc);
-          } else {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) attn_point(p.x[u], p.y[u], acc, mn, mx);
-          }
-        },
-        [&](const uint32_t* xv, double yv) { attn_point(xv, yv, acc, mn, mx); });
-#pragma unroll
-    for (int i = 0; i < ATTN_NACC; ++i) acc[i] = warp_sum(acc[i]);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      mn[k] = __reduce_min_sync(0xFFFFFFFFu, mn[k]);
-      mx[k] = __reduce_max_sync(0xFFFFFFFFu, mx[k]);
-    }
+    uint32_t mn[3], mx[3];
+    attn_pass1(ring, x, n_pts, y, beg, n, vec_ok && (beg % 4 == 0), grouped, acc, mn, mx);
     // moment-major stores, spread over lanes (every lane holds every sum)
 #pragma unroll
     for (int i = 0; i < ATTN_NACC; ++i)
@@ -1132,11 +1145,80 @@ __global__ void __launch_bounds__(FA_THREADS) fit_moments_attn_kernel(
   }
 }
 
+// The 10-column solve of one signature from its 44 raw sums (34 moments of
+// degree 1..4 + 10 X^T y sums, in accumulator order) and its box: scaled
+// moments, Gram, Cholesky with drop, substitution.  Writes c[10] and inv[3].
+__device__ __forceinline__ void attn_solve_row(int64_t n, const double* raw, const uint32_t* hi,
+                                               double* c, double* inv) {
+  constexpr int NC = 10;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) inv[k] = hi[k] > 0 ? 1.0 / (double)hi[k] : 1.0;  // IEEE division (oracle parity)
+  // scaled moments: raw sum * prod inv^e; the scales follow the same
+  // degree-<=4 monomial recurrence as the moments themselves
+  double sc[35], msc[35];
+  attn_monomials(inv[0], inv[1], inv[2], sc);
+  msc[0] = (double)n;
+#pragma unroll
+  for (int m = 1; m < 35; ++m) msc[m] = raw[m - 1] * sc[m];
+  double L[NC][NC];  // lower triangle used
+  attn_gram(msc, L);
+  double b[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) b[i] = raw[34 + i] * sc[attn_colmon(i)];
+  // Cholesky with drop (same rule as the oracle): L overwrites G
+  double rd[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const double gjj = L[j][j];
+    double d2 = gjj;
+#pragma unroll
+    for (int k = 0; k < j; ++k) d2 = fma(-L[j][k], L[j][k], d2);
+    const bool keep = d2 > DROP_TOL * gjj;
+    const double d = keep ? sqrt(d2) : 0.0;
+    rd[j] = keep ? rcp64(d) : 0.0;
+    L[j][j] = d;
+#pragma unroll
+    for (int i = j + 1; i < NC; ++i) {
+      double t = L[i][j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t = fma(-L[i][k], L[j][k], t);
+      L[i][j] = t * rd[j];
+    }
+  }
+  double z[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    double t = b[j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) t = fma(-L[j][k], z[k], t);
+    z[j] = t * rd[j];
+  }
+#pragma unroll
+  for (int j = NC - 1; j >= 0; --j) {
+    double t = z[j];
+#pragma unroll
+    for (int k = j + 1; k < NC; ++k) t = fma(-L[k][j], c[k], t);
+    c[j] = t * rd[j];
+  }
+}
+
+__device__ __forceinline__ void write_attn_row(dooly_attn_row* row, const double* c,
+                                               const double* inv, const uint32_t* lo,
+                                               const uint32_t* hi) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) row->c[i] = c[i];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    row->inv_scale[k] = inv[k];
+    row->lo[k] = lo[k];
+    row->hi[k] = hi[k];
+  }
+}
+
 __global__ void __launch_bounds__(128) fit_solve_attn_kernel(
     const int64_t* __restrict__ off, int64_t n_sig, const double* __restrict__ mom,
     const uint32_t* __restrict__ box, dooly_attn_row* __restrict__ table,
     double* __restrict__ fit_err, uint8_t* __restrict__ status) {
-  constexpr int NC = 10;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_sig;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = __ldg(off + s + 1) - __ldg(off + s);
@@ -1145,71 +1227,42 @@ __global__ void __launch_bounds__(128) fit_solve_attn_kernel(
       continue;
     }
     uint32_t lo[3], hi[3];
-    double inv[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       lo[k] = __ldg(box + (int64_t)k * n_sig + s);
       hi[k] = __ldg(box + (int64_t)(3 + k) * n_sig + s);
-      inv[k] = hi[k] > 0 ? 1.0 / (double)hi[k] : 1.0;  // IEEE division (oracle parity)
     }
-    // scaled moments: raw sum * prod inv^e; the scales follow the same
-    // degree-<=4 monomial recurrence as the moments themselves
-    double sc[35], msc[35];
-    attn_monomials(inv[0], inv[1], inv[2], sc);
-    msc[0] = (double)n;
+    double raw[ATTN_NACC];
 #pragma unroll
-    for (int m = 1; m < 35; ++m) msc[m] = __ldg(mom + (int64_t)(m - 1) * n_sig + s) * sc[m];
-    double L[NC][NC];  // lower triangle used
-    attn_gram(msc, L);
-    double b[NC];
-#pragma unroll
-    for (int i = 0; i < NC; ++i) b[i] = __ldg(mom + (int64_t)(34 + i) * n_sig + s) * sc[attn_colmon(i)];
-    // Cholesky with drop (same rule as the oracle): L overwrites G
-    double rd[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      const double gjj = L[j][j];
-      double d2 = gjj;
-#pragma unroll
-      for (int k = 0; k < j; ++k) d2 = fma(-L[j][k], L[j][k], d2);
-      const bool keep = d2 > DROP_TOL * gjj;
-      const double d = keep ? sqrt(d2) : 0.0;
-      rd[j] = keep ? rcp64(d) : 0.0;
-      L[j][j] = d;
-#pragma unroll
-      for (int i = j + 1; i < NC; ++i) {
-        double t = L[i][j];
-#pragma unroll
-        for (int k = 0; k < j; ++k) t = fma(-L[i][k], L[j][k], t);
-        L[i][j] = t * rd[j];
-      }
-    }
-    double z[NC], c[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      double t = b[j];
-#pragma unroll
-      for (int k = 0; k < j; ++k) t = fma(-L[j][k], z[k], t);
-      z[j] = t * rd[j];
-    }
-#pragma unroll
-    for (int j = NC - 1; j >= 0; --j) {
-      double t = z[j];
-#pragma unroll
-      for (int k = j + 1; k < NC; ++k) t = fma(-L[k][j], c[k], t);
-      c[j] = t * rd[j];
-    }
-    dooly_attn_row* row = table + s;
-#pragma unroll
-    for (int i = 0; i < NC; ++i) row->c[i] = c[i];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      row->inv_scale[k] = inv[k];
-      row->lo[k] = lo[k];
-      row->hi[k] = hi[k];
-    }
+    for (int i = 0; i < ATTN_NACC; ++i) raw[i] = __ldg(mom + (int64_t)i * n_sig + s);
+    double c[10], inv[3];
+    attn_solve_row(n, raw, hi, c, inv);
+    write_attn_row(table + s, c, inv, lo, hi);
     status[s] = DOOLY_FIT_OK;
   }
+}
+
+// Training MAPE of one attention signature by one warp (warp-summed).
+__device__ __forceinline__ double attn_pass2(const uint32_t* x, int64_t n_pts, const double* y,
+                                             int64_t beg, int64_t n, bool vec, const AttnRow& r) {
+  double e0 = 0.0, e1 = 0.0;
+  auto term = [&](const uint32_t* xv, double yv) {
+    double v[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[k] = u2d(xv[k]);
+    const double p = fmax(eval_fma<DOOLY_KIND_ATTN>(r.c, r.inv, v), DOOLY_CLAMP_FLOOR);
+    return fabs(p - yv) * rcp64(yv);
+  };
+  warp_stream_points(
+      x, n_pts, y, beg, n, vec,
+      [&](const AttnPoints4& p) {
+        e0 += term(p.x[0], p.y[0]);
+        e1 += term(p.x[1], p.y[1]);
+        e0 += term(p.x[2], p.y[2]);
+        e1 += term(p.x[3], p.y[3]);
+      },
+      [&](const uint32_t* xv, double yv) { e0 += term(xv, yv); });
+  return warp_sum(e0 + e1);
 }
 
 __global__ void __launch_bounds__(FA_THREADS) fit_mape_attn_kernel(
@@ -1223,24 +1276,49 @@ __global__ void __launch_bounds__(FA_THREADS) fit_mape_attn_kernel(
     const int64_t beg = __ldg(off + s), n = __ldg(off + s + 1) - beg;
     if (n < FitTraits<DOOLY_KIND_ATTN>::NEED) continue;
     const AttnRow r = load_attn(table, (uint32_t)s);
-    double e0 = 0.0, e1 = 0.0;
-    auto term = [&](const uint32_t* xv, double yv) {
-      double v[3];
+    const double e = attn_pass2(x, n_pts, y, beg, n, vec_ok && (beg % 4 == 0), r);
+    if (lane == 0) fit_err[s] = e / (double)n;
+  }
+}
+
+// Fused attention CSR fit (opt-in, DOOLY_FIT_CSR_ATTN=fused; measured slower
+// than the split kernels, see launch_fit): one warp per signature runs pass 1,
+// the solve (every lane, the same arithmetic as fit_solve_attn_kernel) and
+// pass 2, whose re-read of the signature's points mostly hits L2 — 2 CTAs of 4
+// warps per SM keep (warps in flight x 20 B x points) within L2.
+__global__ void __launch_bounds__(FA_THREADS, 2) fit_fused_attn_kernel(
+    const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y,
+    const int64_t* __restrict__ off, int64_t n_sig, dooly_attn_row* __restrict__ table,
+    double* __restrict__ fit_err, uint8_t* __restrict__ status, bool vec_ok, int grouped) {
+  extern __shared__ __align__(16) unsigned char fa_dyn[];
+  unsigned char* ring = fa_dyn + (size_t)(threadIdx.x >> 5) * FA_DEPTH * FA_BLOCK_BYTES;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < n_sig; s += n_warps) {
+    const int64_t beg = __ldg(off + s), n = __ldg(off + s + 1) - beg;
+    if (n < FitTraits<DOOLY_KIND_ATTN>::NEED) {
+      if (lane == 0) write_unfitted<DOOLY_KIND_ATTN>(table, s, fit_err, status);
+      continue;
+    }
+    const bool vec = vec_ok && (beg % 4 == 0);
+    AttnRow r;
+    {
+      double acc[ATTN_NACC];
+      uint32_t mn[3], mx[3];
+      attn_pass1(ring, x, n_pts, y, beg, n, vec, grouped, acc, mn, mx);
+      attn_solve_row(n, acc, mx, r.c, r.inv);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) v[k] = u2d(xv[k]);
-      const double p = fmax(eval_fma<DOOLY_KIND_ATTN>(r.c, r.inv, v), DOOLY_CLAMP_FLOOR);
-      return fabs(p - yv) * rcp64(yv);
-    };
-    warp_stream_points(
-        x, n_pts, y, beg, n, vec_ok && (beg % 4 == 0),
-        [&](const AttnPoints4& p) {
-          e0 += term(p.x[0], p.y[0]);
-          e1 += term(p.x[1], p.y[1]);
-          e0 += term(p.x[2], p.y[2]);
-          e1 += term(p.x[3], p.y[3]);
-        },
-        [&](const uint32_t* xv, double yv) { e0 += term(xv, yv); });
-    const double e = warp_sum(e0 + e1);
+      for (int k = 0; k < 3; ++k) {
+        r.lo[k] = mn[k];
+        r.hi[k] = mx[k];
+      }
+    }
+    if (lane == 0) {
+      write_attn_row(table + s, r.c, r.inv, r.lo, r.hi);
+      status[s] = DOOLY_FIT_OK;
+    }
+    const double e = attn_pass2(x, n_pts, y, beg, n, vec, r);
     if (lane == 0) fit_err[s] = e / (double)n;
   }
 }
@@ -1297,6 +1375,26 @@ cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double*
     }
     return launch_kind<DOOLY_KIND_AFFINE>(x, n_pts, y, off, n_sig, table, fit_err, status,
                                           stream, n_sm);
+  }
+  // "fused": one warp per signature for pass 1, solve and pass 2 (opt-in:
+  // 5.54 vs 5.24 ms per 200k x 4096 points — the points cross HBM once, 19.9
+  // instead of 32.8 GB, but at 224 registers 8 warps per SM leave it latency-
+  // bound where the split kernels run near HBM speed)
+  const char* which = getenv("DOOLY_FIT_CSR_ATTN");
+  if (which != nullptr && strcmp(which, "fused") == 0) {
+    *launches += 1;
+    const bool vec_ok = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && (n_pts % 4 == 0);
+    cudaError_t e = cudaFuncSetAttribute(fit_fused_attn_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FA_SMEM);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = (int64_t)n_sm * 2;
+    const int64_t need = (n_sig + FA_THREADS / 32 - 1) / (FA_THREADS / 32);
+    if (blocks > need) blocks = need;
+    const char* grp = getenv("DOOLY_FIT_GROUPED");   // "0": per-point moments only
+    fit_fused_attn_kernel<<<(unsigned)blocks, FA_THREADS, FA_SMEM, stream>>>(
+        x, n_pts, y, off, n_sig, static_cast<dooly_attn_row*>(table), fit_err, status, vec_ok,
+        grp == nullptr || grp[0] != '0');
+    return cudaGetLastError();
   }
   if (ws == nullptr) {  // no workspace: fused single-kernel path
     *launches += 1;

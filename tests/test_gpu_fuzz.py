@@ -232,3 +232,37 @@ def test_fit_csr_affine_warp_large_ragged(shift, dev, monkeypatch):
         assert d.max() <= 1e-9, d.max()
         fe, fr_ = res.fit_err.cpu().numpy()[ok], ref["fit_err"][ok]
         assert np.all(np.abs(fe - fr_) <= 1e-9 * fr_ + 1e-12)
+
+
+@pytest.mark.parametrize("shift", [0, 2])
+def test_fit_csr_attn_fused_matches_split(shift, dev, monkeypatch):
+    """The opt-in fused attention CSR kernel (pass 1, solve and pass 2 in one
+    warp per signature) against the default moments / solve / MAPE kernels and the oracle, on
+    ragged signatures of 100-5000 points at two head alignments (the vector
+    path and the point-by-point path)."""
+    from paper_2605_07985_b200.sim import fit_tables
+
+    x, y, off = synth_fit_data(ATTN, 80, 5000, seed=70 + shift, ragged=True)
+    pad = np.full((3, shift), 5, np.uint32)
+    x = np.ascontiguousarray(np.concatenate([pad, x], axis=1))
+    y = np.concatenate([np.full(shift, 1e-5), y])
+    off = np.concatenate([[0], off + shift]).astype(np.int64)
+    xt = torch.from_numpy(x.view(np.int32)).to(dev)
+    yt, ot = torch.from_numpy(y).to(dev), torch.from_numpy(off).to(dev)
+    split = fit_tables(ATTN, xt, yt, ot)
+    monkeypatch.setenv("DOOLY_FIT_CSR_ATTN", "fused")
+    fused = fit_tables(ATTN, xt, yt, ot)
+    torch.cuda.synchronize()
+    assert torch.equal(fused.status, split.status)
+    ok = (split.status == 0).cpu().numpy()
+    a = fused.table.view(torch.float64).cpu().numpy()[ok, :10]
+    b = split.table.view(torch.float64).cpu().numpy()[ok, :10]
+    assert np.max(np.abs(a - b).max(axis=1) / np.abs(b).max(axis=1)) <= 1e-14
+    assert torch.equal(fused.table[:, 80:], split.table[:, 80:])        # scaling + box
+    fe, fs = fused.fit_err.cpu().numpy()[ok], split.fit_err.cpu().numpy()[ok]
+    assert np.all(np.abs(fe - fs) <= 1e-12 * fs)
+    ref = osim.fit(ATTN, x, y, off)
+    assert np.array_equal(fused.status.cpu().numpy(), ref["status"])
+    got = rows_to_table(ATTN, fused.rows())
+    d = np.abs(got["coef"][ok] - ref["coef"][ok]).max(axis=1) / np.abs(ref["coef"][ok]).max(axis=1)
+    assert d.max() <= 1e-9, d.max()
