@@ -1244,7 +1244,8 @@ __global__ void __launch_bounds__(128) fit_solve_attn_kernel(
 
 // Training MAPE of one attention signature by one warp (warp-summed).
 __device__ __forceinline__ double attn_pass2(const uint32_t* x, int64_t n_pts, const double* y,
-                                             int64_t beg, int64_t n, bool vec, const AttnRow& r) {
+                                             int64_t beg, int64_t n, bool vec, const AttnRow& r,
+                                             unsigned char* ring = nullptr) {
   double e0 = 0.0, e1 = 0.0;
   auto term = [&](const uint32_t* xv, double yv) {
     double v[3];
@@ -1253,15 +1254,17 @@ __device__ __forceinline__ double attn_pass2(const uint32_t* x, int64_t n_pts, c
     const double p = fmax(eval_fma<DOOLY_KIND_ATTN>(r.c, r.inv, v), DOOLY_CLAMP_FLOOR);
     return fabs(p - yv) * rcp64(yv);
   };
-  warp_stream_points(
-      x, n_pts, y, beg, n, vec,
-      [&](const AttnPoints4& p) {
-        e0 += term(p.x[0], p.y[0]);
-        e1 += term(p.x[1], p.y[1]);
-        e0 += term(p.x[2], p.y[2]);
-        e1 += term(p.x[3], p.y[3]);
-      },
-      [&](const uint32_t* xv, double yv) { e0 += term(xv, yv); });
+  auto f4 = [&](const AttnPoints4& p) {
+    e0 += term(p.x[0], p.y[0]);
+    e1 += term(p.x[1], p.y[1]);
+    e0 += term(p.x[2], p.y[2]);
+    e1 += term(p.x[3], p.y[3]);
+  };
+  auto f1 = [&](const uint32_t* xv, double yv) { e0 += term(xv, yv); };
+  if (ring != nullptr)   // blocks in flight through the warp's cp.async ring
+    warp_stream_points_async(ring, x, n_pts, y, beg, n, vec, f4, f1);
+  else
+    warp_stream_points(x, n_pts, y, beg, n, vec, f4, f1);
   return warp_sum(e0 + e1);
 }
 
@@ -1318,7 +1321,7 @@ __global__ void __launch_bounds__(FA_THREADS, 2) fit_fused_attn_kernel(
       write_attn_row(table + s, r.c, r.inv, r.lo, r.hi);
       status[s] = DOOLY_FIT_OK;
     }
-    const double e = attn_pass2(x, n_pts, y, beg, n, vec, r);
+    const double e = attn_pass2(x, n_pts, y, beg, n, vec, r, ring);
     if (lane == 0) fit_err[s] = e / (double)n;
   }
 }
@@ -1377,9 +1380,9 @@ cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double*
                                           stream, n_sm);
   }
   // "fused": one warp per signature for pass 1, solve and pass 2 (opt-in:
-  // 5.54 vs 5.24 ms per 200k x 4096 points — the points cross HBM once, 19.9
-  // instead of 32.8 GB, but at 224 registers 8 warps per SM leave it latency-
-  // bound where the split kernels run near HBM speed)
+  // 13.21 vs 13.34 ms per 0.5M x 4096 points — the points cross HBM once, but
+  // at 234 registers 8 warps per SM leave it latency-bound where the split
+  // kernels run near HBM speed)
   const char* which = getenv("DOOLY_FIT_CSR_ATTN");
   if (which != nullptr && strcmp(which, "fused") == 0) {
     *launches += 1;
