@@ -133,9 +133,48 @@ def test_c3_mixtral_moe_dedup_fit(dev):
                 for c in man.grid.kv_lens if t >= r and c + -(-t // r) <= 32768)
     valid += sum(1 for r in man.grid.request_counts for c in man.grid.kv_lens if c + 1 <= 32768)
     assert x.shape[1] == valid and valid > 100
-    ref = _oracle_fit_db(db)[att.digest][1]
+    ref_all = _oracle_fit_db(db)
+    ref = ref_all[att.digest][1]
     c = np.array(regs.regressor(att.digest).coefficients)
     assert np.max(np.abs(c - ref["coef"][0])) <= 1e-9 * np.max(np.abs(ref["coef"][0]))
+    # every MoE-model signature (router, top-k, fused experts, ...) against the oracle fit
+    worst = 0.0
+    for d, (kind, r) in ref_all.items():
+        cc = np.array(regs.regressor(d).coefficients)
+        worst = max(worst, np.max(np.abs(cc - r["coef"][0])) / np.max(np.abs(r["coef"][0])))
+    assert worst <= 1e-9, worst
+    # a serving run of the MoE model on the device event loop == the oracle event
+    # loop over the same regressor rows, bit for bit
+    from paper_2605_07985_b200.sim import SchedConfig, build_calltree, make_sched, run
+
+    model, backend = man.models[0], man.backends[0]
+    spec = modelir.WorkloadSpec(mode="stream", rate=20.0, num_requests=300,
+                                prompt_len=modelir.LengthDist(950, 1232),
+                                output_len=modelir.LengthDist(388, 397), max_len=8192)
+    reqs = modelir.sample_workload(spec, seed=3)
+    # the MoE weights (94 GB) exceed one 80-GB a100-like device: a stated KV budget
+    sched = SchedConfig(chunk=8192, max_batch=256, max_kv_memory=20 * 10**9)
+    m = run(reqs, model, backend, man.hardware, regs, sched)
+    ct = build_calltree(model, backend, regs, man.hardware, 1)
+    cfg = make_sched(model, man.hardware, 1, sched, ct)
+    tabs = {k: rows_to_table(k, regs.tables[k].rows()) for k in regs.tables}
+    ops = []
+    for i in range(ct.n_ops):
+        feat, row = ct.oplist.feat[i], ct.oplist.row[i]
+        op = {"feat": feat, "repeat": ct.oplist.repeat[i], "window_slot": ct.oplist.window_slot[i],
+              "bytes_per_tok": ct.oplist.bytes_per_tok[i]}
+        if feat != osim.FEAT_COMM:
+            t = tabs[1 if feat == osim.FEAT_ATTN else 0]
+            op.update(coef=list(t["coef"][row]), inv=list(t["inv"][row]))
+        ops.append(op)
+    r = osim.run_shard([q.arrival_s for q in reqs], [q.prompt_tokens for q in reqs],
+                       [q.output_tokens for q in reqs], [q.cached_tokens for q in reqs], ops,
+                       8192, 256, cfg.kv_bytes_per_token, cfg.kv_capacity_bytes, ct.window)
+    assert m.n_iterations[0] == r["n_iter"]
+    assert np.array_equal(m.ttft.view(np.uint64), np.asarray(r["ttft"]).view(np.uint64))
+    mask = ~np.isnan(r["tpot"])
+    assert np.array_equal(np.isnan(m.tpot), ~mask)
+    assert np.array_equal(m.tpot[mask].view(np.uint64), np.asarray(r["tpot"])[mask].view(np.uint64))
 
 
 def test_tp4_calltree_comm_entries(dev):
