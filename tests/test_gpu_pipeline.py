@@ -144,37 +144,10 @@ def test_c3_mixtral_moe_dedup_fit(dev):
         worst = max(worst, np.max(np.abs(cc - r["coef"][0])) / np.max(np.abs(r["coef"][0])))
     assert worst <= 1e-9, worst
     # a serving run of the MoE model on the device event loop == the oracle event
-    # loop over the same regressor rows, bit for bit
-    from paper_2605_07985_b200.sim import SchedConfig, build_calltree, make_sched, run
-
-    model, backend = man.models[0], man.backends[0]
-    spec = modelir.WorkloadSpec(mode="stream", rate=20.0, num_requests=300,
-                                prompt_len=modelir.LengthDist(950, 1232),
-                                output_len=modelir.LengthDist(388, 397), max_len=8192)
-    reqs = modelir.sample_workload(spec, seed=3)
-    # the MoE weights (94 GB) exceed one 80-GB a100-like device: a stated KV budget
-    sched = SchedConfig(chunk=8192, max_batch=256, max_kv_memory=20 * 10**9)
-    m = run(reqs, model, backend, man.hardware, regs, sched)
-    ct = build_calltree(model, backend, regs, man.hardware, 1)
-    cfg = make_sched(model, man.hardware, 1, sched, ct)
-    tabs = {k: rows_to_table(k, regs.tables[k].rows()) for k in regs.tables}
-    ops = []
-    for i in range(ct.n_ops):
-        feat, row = ct.oplist.feat[i], ct.oplist.row[i]
-        op = {"feat": feat, "repeat": ct.oplist.repeat[i], "window_slot": ct.oplist.window_slot[i],
-              "bytes_per_tok": ct.oplist.bytes_per_tok[i]}
-        if feat != osim.FEAT_COMM:
-            t = tabs[1 if feat == osim.FEAT_ATTN else 0]
-            op.update(coef=list(t["coef"][row]), inv=list(t["inv"][row]))
-        ops.append(op)
-    r = osim.run_shard([q.arrival_s for q in reqs], [q.prompt_tokens for q in reqs],
-                       [q.output_tokens for q in reqs], [q.cached_tokens for q in reqs], ops,
-                       8192, 256, cfg.kv_bytes_per_token, cfg.kv_capacity_bytes, ct.window)
-    assert m.n_iterations[0] == r["n_iter"]
-    assert np.array_equal(m.ttft.view(np.uint64), np.asarray(r["ttft"]).view(np.uint64))
-    mask = ~np.isnan(r["tpot"])
-    assert np.array_equal(np.isnan(m.tpot), ~mask)
-    assert np.array_equal(m.tpot[mask].view(np.uint64), np.asarray(r["tpot"])[mask].view(np.uint64))
+    # loop over the same regressor rows, bit for bit (the MoE weights, 94 GB,
+    # exceed one 80-GB a100-like device: a stated KV budget)
+    _assert_run_equals_oracle(man, man.models[0], man.backends[0], regs, rate=20.0, seed=3,
+                              max_kv_memory=20 * 10**9)
 
 
 def test_tp4_calltree_comm_entries(dev):
@@ -218,3 +191,58 @@ def test_fit_db_grid_groups_match_csr(corpus, dev, monkeypatch):
         assert np.max(np.abs(ca - cb)) <= 2e-9 * np.max(np.abs(cb))
         assert a.box == b.box and a.inv_scale == b.inv_scale
         assert abs(a.fit_error - b.fit_error) <= 1e-9 * b.fit_error + 1e-12
+
+
+def _assert_run_equals_oracle(man, model, backend, regs, rate: float, seed: int,
+                              max_kv_memory=None, n: int = 300):
+    """The device event loop (sim.run) over a seeded Poisson stream equals the
+    oracle event loop over the same regressor rows, bit for bit."""
+    from paper_2605_07985_b200 import modelir
+    from paper_2605_07985_b200.sim import SchedConfig, build_calltree, make_sched, run
+
+    spec = modelir.WorkloadSpec(mode="stream", rate=rate, num_requests=n,
+                                prompt_len=modelir.LengthDist(950, 1232),
+                                output_len=modelir.LengthDist(388, 397), max_len=8192)
+    reqs = modelir.sample_workload(spec, seed=seed)
+    sched = SchedConfig(chunk=8192, max_batch=256, max_kv_memory=max_kv_memory)
+    m = run(reqs, model, backend, man.hardware, regs, sched)
+    ct = build_calltree(model, backend, regs, man.hardware, 1)
+    cfg = make_sched(model, man.hardware, 1, sched, ct)
+    tabs = {k: rows_to_table(k, regs.tables[k].rows()) for k in regs.tables}
+    ops = []
+    for i in range(ct.n_ops):
+        feat, row = ct.oplist.feat[i], ct.oplist.row[i]
+        op = {"feat": feat, "repeat": ct.oplist.repeat[i], "window_slot": ct.oplist.window_slot[i],
+              "bytes_per_tok": ct.oplist.bytes_per_tok[i]}
+        if feat != osim.FEAT_COMM:
+            t = tabs[1 if feat == osim.FEAT_ATTN else 0]
+            op.update(coef=list(t["coef"][row]), inv=list(t["inv"][row]))
+        ops.append(op)
+    r = osim.run_shard([q.arrival_s for q in reqs], [q.prompt_tokens for q in reqs],
+                       [q.output_tokens for q in reqs], [q.cached_tokens for q in reqs], ops,
+                       8192, 256, cfg.kv_bytes_per_token, cfg.kv_capacity_bytes, ct.window)
+    assert m.n_iterations[0] == r["n_iter"]
+    assert np.array_equal(m.ttft.view(np.uint64), np.asarray(r["ttft"]).view(np.uint64))
+    mask = ~np.isnan(r["tpot"])
+    assert np.array_equal(np.isnan(m.tpot), ~mask)
+    assert np.array_equal(m.tpot[mask].view(np.uint64), np.asarray(r["tpot"])[mask].view(np.uint64))
+    return ct
+
+
+def test_c2_zoo_serving_runs(corpus, dev):
+    """C2: serving runs of four zoo configurations (dense GQA / MHA, sliding-window
+    models, every backend) on the device event loop, each bit-identical to the
+    oracle event loop over the same regressor rows."""
+    from paper_2605_07985_b200 import modelir
+    from paper_2605_07985_b200.sim import fit
+
+    picks = [(0, 0), (1, 2), (3, 1), (11, 0)]   # windowed x2, MHA, GQA 28/4
+    windows = 0
+    for mi, bi in picks:
+        model, backend = corpus.models[mi], corpus.backends[bi]
+        man = modelir.CorpusManifest((model,), (backend,), corpus.hardware, 1, corpus.grid)
+        db, _ = _profile(man, dev)
+        regs = fit(db, dev)
+        ct = _assert_run_equals_oracle(man, model, backend, regs, rate=8.0, seed=mi + 1)
+        windows += ct.window > 0
+    assert windows == 2
