@@ -1001,7 +1001,10 @@ __device__ __forceinline__ void warp_stream_points(const uint32_t* x, int64_t n_
 // later consumes (3 x-plane chunks + 2 y chunks per 128-point block), so the
 // ring needs no cross-lane synchronisation, only cp.async.wait_group; D blocks
 // are in flight per warp without holding any registers.
-constexpr int FA_DEPTH = 4;                      // blocks in flight per warp (6, 8: no faster)
+#ifndef FA_DEPTH_N
+#define FA_DEPTH_N 8
+#endif
+constexpr int FA_DEPTH = FA_DEPTH_N;  // blocks in flight per warp (8: fused 13.24 -> 12.93 ms, split 13.30 -> 13.15)
 constexpr int FA_BLOCK_BYTES = 3 * 128 * 4 + 128 * 8;  // 2560 B per 128-point block
 constexpr size_t FA_SMEM = (size_t)(FA_THREADS / 32) * FA_DEPTH * FA_BLOCK_BYTES;
 
@@ -1284,8 +1287,8 @@ __global__ void __launch_bounds__(FA_THREADS) fit_mape_attn_kernel(
   }
 }
 
-// Fused attention CSR fit (opt-in, DOOLY_FIT_CSR_ATTN=fused; measured slower
-// than the split kernels, see launch_fit): one warp per signature runs pass 1,
+// Fused attention CSR fit (the default; DOOLY_FIT_CSR_ATTN=split selects the
+// three kernels, see launch_fit): one warp per signature runs pass 1,
 // the solve (every lane, the same arithmetic as fit_solve_attn_kernel) and
 // pass 2, whose re-read of the signature's points mostly hits L2 — 2 CTAs of 4
 // warps per SM keep (warps in flight x 20 B x points) within L2.
@@ -1379,12 +1382,12 @@ cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double*
     return launch_kind<DOOLY_KIND_AFFINE>(x, n_pts, y, off, n_sig, table, fit_err, status,
                                           stream, n_sm);
   }
-  // "fused": one warp per signature for pass 1, solve and pass 2 (opt-in:
-  // 13.21 vs 13.34 ms per 0.5M x 4096 points — the points cross HBM once, but
-  // at 234 registers 8 warps per SM leave it latency-bound where the split
-  // kernels run near HBM speed)
+  // default: one warp per signature for pass 1, solve and pass 2 (the points
+  // cross HBM once; 12.93 vs 13.15 ms per 0.5M x 4096 points for the split
+  // kernels, DOOLY_FIT_CSR_ATTN=split — at 234 registers and 8 warps per SM
+  // the fused kernel is latency-bound, the split ones run near HBM speed)
   const char* which = getenv("DOOLY_FIT_CSR_ATTN");
-  if (which != nullptr && strcmp(which, "fused") == 0) {
+  if (which == nullptr || strcmp(which, "split") != 0) {
     *launches += 1;
     const bool vec_ok = ((uintptr_t)x % 16 == 0) && ((uintptr_t)y % 16 == 0) && (n_pts % 4 == 0);
     cudaError_t e = cudaFuncSetAttribute(fit_fused_attn_kernel,

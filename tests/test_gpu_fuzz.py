@@ -236,8 +236,8 @@ def test_fit_csr_affine_warp_large_ragged(shift, dev, monkeypatch):
 
 @pytest.mark.parametrize("shift", [0, 2])
 def test_fit_csr_attn_fused_matches_split(shift, dev, monkeypatch):
-    """The opt-in fused attention CSR kernel (pass 1, solve and pass 2 in one
-    warp per signature) against the default moments / solve / MAPE kernels and the oracle, on
+    """The fused attention CSR kernel (the default: pass 1, solve and pass 2 in
+    one warp per signature) against the moments / solve / MAPE kernels and the oracle, on
     ragged signatures of 100-5000 points at two head alignments (the vector
     path and the point-by-point path)."""
     from paper_2605_07985_b200.sim import fit_tables
@@ -249,9 +249,9 @@ def test_fit_csr_attn_fused_matches_split(shift, dev, monkeypatch):
     off = np.concatenate([[0], off + shift]).astype(np.int64)
     xt = torch.from_numpy(x.view(np.int32)).to(dev)
     yt, ot = torch.from_numpy(y).to(dev), torch.from_numpy(off).to(dev)
-    split = fit_tables(ATTN, xt, yt, ot)
-    monkeypatch.setenv("DOOLY_FIT_CSR_ATTN", "fused")
     fused = fit_tables(ATTN, xt, yt, ot)
+    monkeypatch.setenv("DOOLY_FIT_CSR_ATTN", "split")
+    split = fit_tables(ATTN, xt, yt, ot)
     torch.cuda.synchronize()
     assert torch.equal(fused.status, split.status)
     ok = (split.status == 0).cpu().numpy()
