@@ -62,7 +62,8 @@ size_t dedup_workspace_size(int64_t n, int64_t n_db);
 cudaError_t launch_dedup(const uint8_t* digests, int64_t n, const uint8_t* db, int64_t n_db,
                          int64_t* out_first, uint32_t* out_uid, uint8_t* out_is_new,
                          uint8_t* out_in_db, int64_t* out_n_unique, void* ws, size_t ws_bytes,
-                         cudaStream_t stream, int n_sm, int64_t* launches);
+                         cudaStream_t stream, int n_sm, int64_t* launches,
+                         const uint32_t* grp = nullptr);
 cudaError_t launch_iter_eval(const dooly_oplist* ops, const void* aff, int64_t n_aff,
                              const void* attn, int64_t n_attn, const uint32_t* it_feat,
                              int64_t n_it, double* it_lat, int64_t* err_first,
@@ -579,6 +580,17 @@ int dooly_dedup(dooly_ctx* ctx, const uint32_t* words, const int64_t* rec_off, i
     if (e == cudaSuccess)
       e = dooly::launch_digest_copy(rg.rep, n, out_digest, st, ctx->n_sm, &ctx->launches);
     rc = check_cuda(ctx, e, "dedup: record grouping + sha256");
+    if (rc) return rc;
+    // records sharing a group share the digest: only the group minima insert
+    // (rg.rep = each record's group minimum), the others resolve through it
+    if (!out_n_unique || !out_first || !out_uid || !out_is_new || (n_db > 0 && !db_digests))
+      return fail(ctx, DOOLY_ERR_INVALID_ARG, "dedup: null pointer");
+    return check_cuda(ctx,
+                      dooly::launch_dedup(out_digest, n, db_digests, n_db, out_first, out_uid,
+                                          out_is_new, out_in_db, out_n_unique, workspace,
+                                          workspace_bytes, st, ctx->n_sm, &ctx->launches,
+                                          rg.rep),
+                      "dedup");
   } else {
     rc = dooly_sha256_records(ctx, words, rec_off, n, op_bytes, op_off, n_ops, sym_bytes,
                               sym_off, n_sym, attr_digests, n_attr, out_digest, stream);

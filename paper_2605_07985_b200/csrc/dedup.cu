@@ -95,9 +95,12 @@ __device__ __forceinline__ bool digest_eq(const uint8_t* p, const uint32_t d[8])
 __global__ void __launch_bounds__(DEDUP_THREADS) dedup_insert_kernel(
     const uint8_t* __restrict__ keys, int64_t m, uint32_t base, const uint8_t* __restrict__ batch,
     int64_t n, const uint8_t* __restrict__ db, uint32_t* slots, uint8_t* mark,
-    uint32_t* slot_of, uint64_t mask) {
+    uint32_t* slot_of, uint64_t mask, const uint32_t* __restrict__ grp) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
+    // grouped records (grp = each record's group minimum): only the minima
+    // insert; the others share their minimum's digest and slot
+    if (grp != nullptr && __ldg(grp + i) != (uint32_t)i) continue;
     uint32_t d[8];
     load_digest(keys + i * 32, d);
     const uint32_t me = base + (uint32_t)i;
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(DEDUP_THREADS) dedup_insert_kernel(
 __global__ void __launch_bounds__(DEDUP_THREADS) dedup_insert_group_kernel(
     const uint8_t* __restrict__ keys, int64_t m, uint32_t base, const uint8_t* __restrict__ batch,
     int64_t n, const uint8_t* __restrict__ db, uint32_t* slots, uint8_t* mark,
-    uint32_t* slot_of, uint64_t mask) {
+    uint32_t* slot_of, uint64_t mask, const uint32_t* __restrict__ grp) {
   const int lane = threadIdx.x & 31, k = lane & 7, g0 = lane & ~7;
   const unsigned gmask = 0xFFu << g0;
   const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 3;
@@ -136,6 +139,7 @@ __global__ void __launch_bounds__(DEDUP_THREADS) dedup_insert_group_kernel(
   const uint32_t* bw = reinterpret_cast<const uint32_t*>(batch);
   const uint32_t* dw = reinterpret_cast<const uint32_t*>(db);
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 3; i < m; i += stride) {
+    if (grp != nullptr && __ldg(grp + i) != (uint32_t)i) continue;   // group-uniform
     const uint32_t w = __ldg(kw + i * 8 + k);
     const uint32_t me = base + (uint32_t)i;
     uint64_t slot = __shfl_sync(gmask, w, g0) & mask;
@@ -167,10 +171,11 @@ static bool dedup_group_insert() {
 __global__ void __launch_bounds__(DEDUP_THREADS) dedup_resolve_kernel(
     int64_t n, const uint32_t* __restrict__ slots, const uint8_t* __restrict__ mark,
     const uint32_t* __restrict__ slot_of, int64_t* __restrict__ out_first,
-    uint8_t* __restrict__ out_is_new, uint8_t* __restrict__ out_in_db, uint32_t* first_flag) {
+    uint8_t* __restrict__ out_is_new, uint8_t* __restrict__ out_in_db, uint32_t* first_flag,
+    const uint32_t* __restrict__ grp) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t s = slot_of[i];
+    const uint32_t s = slot_of[grp != nullptr ? __ldg(grp + i) : (uint32_t)i];
     const uint32_t f = slots[s];
     const uint8_t in_db = mark[s];
     const bool first = f == (uint32_t)i;
@@ -202,7 +207,8 @@ static unsigned grid_for(int64_t m, int n_sm) {
 cudaError_t launch_dedup(const uint8_t* digests, int64_t n, const uint8_t* db, int64_t n_db,
                          int64_t* out_first, uint32_t* out_uid, uint8_t* out_is_new,
                          uint8_t* out_in_db, int64_t* out_n_unique, void* ws, size_t ws_bytes,
-                         cudaStream_t stream, int n_sm, int64_t* launches) {
+                         cudaStream_t stream, int n_sm, int64_t* launches,
+                         const uint32_t* grp) {
   (void)ws_bytes;
   cudaError_t e;
   if (n == 0) return cudaMemsetAsync(out_n_unique, 0, sizeof(int64_t), stream);
@@ -210,18 +216,18 @@ cudaError_t launch_dedup(const uint8_t* digests, int64_t n, const uint8_t* db, i
   if ((e = cudaMemsetAsync(w.slots, 0xFF, w.cap * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(w.mark, 0, w.cap, stream)) != cudaSuccess) return e;
   const uint64_t mask = w.cap - 1;
-  const bool grp = dedup_group_insert();
-  auto insert = grp ? dedup_insert_group_kernel : dedup_insert_kernel;
-  auto grid = [&](int64_t m) { return grid_for(grp ? 8 * m : m, n_sm); };
+  const bool lanes8 = dedup_group_insert();
+  auto insert = lanes8 ? dedup_insert_group_kernel : dedup_insert_kernel;
+  auto grid = [&](int64_t m) { return grid_for(lanes8 ? 8 * m : m, n_sm); };
   if (n_db > 0) {
     insert<<<grid(n_db), DEDUP_THREADS, 0, stream>>>(db, n_db, (uint32_t)n, digests, n, db,
-                                                     w.slots, w.mark, nullptr, mask);
+                                                     w.slots, w.mark, nullptr, mask, nullptr);
     *launches += 1;
   }
   insert<<<grid(n), DEDUP_THREADS, 0, stream>>>(digests, n, 0u, digests, n, db, w.slots, w.mark,
-                                                w.slot_of, mask);
+                                                w.slot_of, mask, grp);
   dedup_resolve_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
-      n, w.slots, w.mark, w.slot_of, out_first, out_is_new, out_in_db, w.first_flag);
+      n, w.slots, w.mark, w.slot_of, out_first, out_is_new, out_in_db, w.first_flag, grp);
   size_t tmp = w.cub_bytes;
   if ((e = cub::DeviceScan::ExclusiveSum(w.cub_tmp, tmp, w.first_flag, w.rank, (int64_t)n,
                                          stream)) != cudaSuccess)
@@ -278,16 +284,10 @@ __device__ __forceinline__ uint32_t grp_len(const uint32_t* r) {
 // the representative's offset and words.
 __global__ void __launch_bounds__(DEDUP_THREADS) rec_group_kernel(
     const uint32_t* __restrict__ words, const int64_t* __restrict__ rec_off, int64_t n,
-    uint32_t* slots, uint64_t mask, uint32_t* __restrict__ rep, uint32_t* __restrict__ list,
-    uint32_t* count) {
-  const int lane = threadIdx.x & 31;
+    uint32_t* slots, uint64_t mask, uint32_t* __restrict__ rep) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  // warp-uniform trip count (the list append below is warp-aggregated)
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
-       base += stride) {
-    const int64_t i = base + lane;
-    bool is_rep = false;
-    if (i < n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    {
       const uint32_t* r = words + rec_off[i];
       const uint32_t len = grp_len(r);
       uint64_t h = 0xcbf29ce484222325ull ^ len;
@@ -303,8 +303,7 @@ __global__ void __launch_bounds__(DEDUP_THREADS) rec_group_kernel(
         if (v == kEmpty) {
           v = atomicCAS(slots + slot, kEmpty, (uint32_t)i);
           if (v == kEmpty) {
-            rep[i] = (uint32_t)i;
-            is_rep = true;
+            rep[i] = (uint32_t)slot;   // the group's slot; rec_group_min_kernel resolves it
             break;
           }
         }
@@ -316,12 +315,33 @@ __global__ void __launch_bounds__(DEDUP_THREADS) rec_group_kernel(
           for (uint32_t k = 0; k < len; ++k)
             diff |= k != 3 ? (__ldg(rv + k) ^ __ldg(r + k)) : 0u;
         }
-        if (diff == 0) {
-          rep[i] = v;
+        if (diff == 0) {   // same content: the slot keeps the group's smallest index
+          if ((uint32_t)i < v) atomicMin(slots + slot, (uint32_t)i);
+          rep[i] = (uint32_t)slot;
           break;
         }
         slot = (slot + 1) & mask;
       }
+    }
+  }
+}
+
+// Each record's representative is its group's smallest index (the slot's
+// final value); the representatives are listed for SHA-256.
+__global__ void __launch_bounds__(DEDUP_THREADS) rec_group_min_kernel(
+    const uint32_t* __restrict__ slots, int64_t n, uint32_t* __restrict__ rep,
+    uint32_t* __restrict__ list, uint32_t* count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the list append is warp-aggregated)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n;
+       base += stride) {
+    const int64_t i = base + lane;
+    bool is_rep = false;
+    if (i < n) {
+      const uint32_t m = slots[rep[i]];
+      rep[i] = m;
+      is_rep = m == (uint32_t)i;
     }
     const uint32_t b = __ballot_sync(0xFFFFFFFFu, is_rep);
     uint32_t at = 0;
@@ -345,9 +365,12 @@ __global__ void __launch_bounds__(DEDUP_THREADS) digest_copy_kernel(
   }
 }
 
+// rep lives in the scan's rank array (read by the digest copy and by the
+// grouped insert / resolve, all before the scan), the list in slot_of (read by
+// SHA-256 before the insert writes it), the count in the DB-mark bytes.
 RecGroup rec_group_carve(void* ws, int64_t n, int64_t n_db) {
   DedupWs w = carve(ws, n, n_db);
-  return RecGroup{w.slot_of, w.rank, reinterpret_cast<uint32_t*>(w.mark)};
+  return RecGroup{w.rank, w.slot_of, reinterpret_cast<uint32_t*>(w.mark)};
 }
 
 cudaError_t launch_rec_group(const uint32_t* words, const int64_t* rec_off, int64_t n, void* ws,
@@ -358,9 +381,11 @@ cudaError_t launch_rec_group(const uint32_t* words, const int64_t* rec_off, int6
   cudaError_t e;
   if ((e = cudaMemsetAsync(w.slots, 0xFF, w.cap * 4, stream)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(g.count, 0, sizeof(uint32_t), stream)) != cudaSuccess) return e;
-  rec_group_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(
-      words, rec_off, n, w.slots, w.cap - 1, g.rep, g.list, g.count);
-  *launches += 1;
+  rec_group_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(words, rec_off, n, w.slots,
+                                                                   w.cap - 1, g.rep);
+  rec_group_min_kernel<<<grid_for(n, n_sm), DEDUP_THREADS, 0, stream>>>(w.slots, n, g.rep, g.list,
+                                                                       g.count);
+  *launches += 2;
   return cudaGetLastError();
 }
 

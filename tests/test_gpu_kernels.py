@@ -637,12 +637,17 @@ def test_dedup_single_call_matches_two_calls(corpus, dev):
 
 @pytest.mark.parametrize("source", ["corpus", "synth"])
 @pytest.mark.parametrize("with_db", [False, True])
-def test_dedup_record_grouping_matches_ungrouped(source, with_db, corpus, dev, monkeypatch):
+@pytest.mark.parametrize("insert", ["thread", "group"])
+def test_dedup_record_grouping_matches_ungrouped(source, with_db, insert, corpus, dev,
+                                                 monkeypatch):
     """dooly_dedup hashes each distinct packed content once (records that
-    differ only in the repeat count share a digest) and copies the digest to
-    the rest: every output equals the path that hashes every record
-    (DOOLY_DEDUP_GROUP=0), and the digests equal the standalone
-    dooly_sha256_records of every record."""
+    differ only in the repeat count share a digest), copies the digest to the
+    rest, and inserts only each group's smallest index into the digest table
+    (the others resolve through it): every output equals the path that hashes
+    and inserts every record (DOOLY_DEDUP_GROUP=0), with either insert kernel,
+    and the digests equal the standalone dooly_sha256_records of every record."""
+    if insert == "group":
+        monkeypatch.setenv("DOOLY_DEDUP_INSERT", "group")
     from paper_2605_07985_b200.profiler import DeviceRecords, dedup_packed, hash_records
     from paper_2605_07985_b200.records import pack_entries, synthesize_entries
     from bench import synth_records
