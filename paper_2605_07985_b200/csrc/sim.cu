@@ -886,44 +886,56 @@ __global__ void __launch_bounds__(32 * kClockWarps) sim_clock_kernel(
   for (int64_t i0 = b; i0 < e; i0 += kClockChunk) {
     bool jump = false;  // an idle jump target anywhere in this chunk
 #pragma unroll
+    for (int k = 0; k < PER; ++k) jump |= __double_as_longlong(ns[k]) != 0ll;
+    jump = __any_sync(0xFFFFFFFFu, jump);
+    const int m = (int)min((int64_t)kClockChunk, e - i0);
+    if (!jump) {
+      // busy chunk (it_start == 0 throughout, the common case): iteration
+      // k*32 + l sits in lane l's cur[k]; every lane runs the same add chain
+      // over shuffled values (no shared memory, the shuffles are independent
+      // of the chain) and lane l keeps the clocks of its own iterations.
+      // Past the end of the shard the values are 0.0: adding them leaves the
+      // clock as is, and they are not stored.
+      double cur[PER], out[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        cur[k] = nl[k];
+        out[k] = 0.0;
+      }
+      if (i0 + kClockChunk < e) fetch(i0 + kClockChunk);   // next chunk in flight
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+          c = __dadd_rn(c, __shfl_sync(0xFFFFFFFFu, cur[k], l));
+          out[k] = lane == l ? c : out[k];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int64_t i = i0 + k * 32 + lane;
+        if (i < e) clock[i] = out[k];
+      }
+      continue;
+    }
+#pragma unroll
     for (int k = 0; k < PER; ++k) {
       L[k * 32 + lane] = nl[k];
       S[k * 32 + lane] = ns[k];
-      jump |= __double_as_longlong(ns[k]) != 0ll;
     }
-    jump = __any_sync(0xFFFFFFFFu, jump);
     __syncwarp();
     if (i0 + kClockChunk < e) fetch(i0 + kClockChunk);   // next chunk in flight during the scan
-    const int m = (int)min((int64_t)kClockChunk, e - i0);
     if (lane == 0) {
-      if (!jump) {
-        // busy chunk (it_start == 0 throughout, the common case): only the adds chain
-        int j = 0;
-        for (; j + 8 <= m; j += 8) {
-          double v[8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) v[t] = L[j + t];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            c = __dadd_rn(c, v[t]);
-            L[j + t] = c;
-          }
-        }
-        for (; j < m; ++j) {
-          c = __dadd_rn(c, L[j]);
-          L[j] = c;
-        }
-      } else {
-        // the max with an idle jump target on a nonzero start
+      // the max with an idle jump target on a nonzero start
 #pragma unroll 8
-        for (int j = 0; j < m; ++j) {
-          const double sj = S[j];
-          if (__double_as_longlong(sj) != 0ll && c < sj) c = sj;
-          c = __dadd_rn(c, L[j]);
-          L[j] = c;
-        }
+      for (int j = 0; j < m; ++j) {
+        const double sj = S[j];
+        if (__double_as_longlong(sj) != 0ll && c < sj) c = sj;
+        c = __dadd_rn(c, L[j]);
+        L[j] = c;
       }
     }
+    c = __shfl_sync(0xFFFFFFFFu, c, 0);
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
