@@ -1292,7 +1292,10 @@ __global__ void __launch_bounds__(FA_THREADS) fit_mape_attn_kernel(
 // the solve (every lane, the same arithmetic as fit_solve_attn_kernel) and
 // pass 2, whose re-read of the signature's points mostly hits L2 — 2 CTAs of 4
 // warps per SM keep (warps in flight x 20 B x points) within L2.
-__global__ void __launch_bounds__(FA_THREADS, 2) fit_fused_attn_kernel(
+#ifndef FA_FUSED_MINB
+#define FA_FUSED_MINB 2
+#endif
+__global__ void __launch_bounds__(FA_THREADS, FA_FUSED_MINB) fit_fused_attn_kernel(
     const uint32_t* __restrict__ x, int64_t n_pts, const double* __restrict__ y,
     const int64_t* __restrict__ off, int64_t n_sig, dooly_attn_row* __restrict__ table,
     double* __restrict__ fit_err, uint8_t* __restrict__ status, bool vec_ok, int grouped) {
@@ -1393,7 +1396,7 @@ cudaError_t launch_fit(int kind, const uint32_t* x, int64_t n_pts, const double*
     cudaError_t e = cudaFuncSetAttribute(fit_fused_attn_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FA_SMEM);
     if (e != cudaSuccess) return e;
-    int64_t blocks = (int64_t)n_sm * 2;
+    int64_t blocks = (int64_t)n_sm * FA_FUSED_MINB;
     const int64_t need = (n_sig + FA_THREADS / 32 - 1) / (FA_THREADS / 32);
     if (blocks > need) blocks = need;
     const char* grp = getenv("DOOLY_FIT_GROUPED");   // "0": per-point moments only
